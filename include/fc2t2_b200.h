@@ -1,0 +1,123 @@
+/*
+ * fc2t2_b200.h -- C ABI of the B200-native FC2T2 hot path.
+ *
+ * The reference (pkg/src/fc2t2, pure NumPy) has no native boundary; its hot
+ * path is the Python call surface of expansion.py / layers.py / ray.py.  This
+ * header is the drop-in replacement underneath that surface: every entry point
+ * below names the reference function it replaces (file:line, paths relative to
+ * pkg/src/fc2t2/).  The Python shim paper_2111_00110_b200 binds it with ctypes
+ * (INTEGRATION.md shows the same binding for the reference package).
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every pointer argument named d_* is
+ *     DEVICE memory owned by the caller (the library never allocates or frees
+ *     caller memory in a hot call; scratch comes from the caller's workspace,
+ *     sized by the matching *_workspace_size query);
+ *   - stream is a cudaStream_t passed as void*; all work is stream ordered,
+ *     no call synchronises except fc2t2_engine_upload;
+ *   - d_flag (int32, may be NULL) accumulates FLAG_* bits; the shim reads it
+ *     once per layer call and raises the reference exception;
+ *   - coefficient grids are (res, res, res, C, PP) float32, graded-lex order,
+ *     PP = index_count(rho) rounded up to a multiple of 4 (pad entries 0);
+ *     res = 2^(level+1).  Points are (n, 3) float32, weights (n, C) float32.
+ *   - return value: FC2T2_OK or an FC2T2_E* code; fc2t2_last_error() gives text.
+ */
+#ifndef FC2T2_B200_H
+#define FC2T2_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the shim maps them to the reference exception classes */
+#define FC2T2_OK 0
+#define FC2T2_EDOMAIN 1    /* expansion.py:23-24 DomainError           */
+#define FC2T2_ESTAGE 2     /* expansion.py:27-28 StageError            */
+#define FC2T2_EORDER 3     /* multiindex.py:20-21 OrderError           */
+#define FC2T2_ECUDA 4      /* CUDA runtime failure                     */
+#define FC2T2_EWORKSPACE 5 /* workspace too small                       */
+#define FC2T2_EVALUE 6     /* ValueError (bad shapes / arguments)      */
+
+#define FC2T2_FLAG_DOMAIN 1
+
+/* M2L table selector for fc2t2_m2l */
+#define FC2T2_TABLE_FAR 0      /* the level's far table (kernel.py:280-290)   */
+#define FC2T2_TABLE_NEAR 1     /* finest-level near table (kernel.py:295-299) */
+#define FC2T2_TABLE_FARNEAR 2  /* far + near merged (finest level only)       */
+
+/* L2P output selector bits for fc2t2_l2p */
+#define FC2T2_L2P_VALUE 1 /* Accessor.value    expansion.py:348-355 */
+#define FC2T2_L2P_GRAD 2  /* Accessor.partials expansion.py:367-369 */
+#define FC2T2_L2P_HESS 4  /* Accessor.partials2 expansion.py:371-373 */
+#define FC2T2_L2P_WGRAD 8 /* sum_c wts_c * grad f_c (layers.py:183, :186-187) */
+
+typedef struct fc2t2_engine fc2t2_engine;
+
+int fc2t2_version(void);
+const char* fc2t2_last_error(void);
+
+/* ---- instrumentation (no reference counterpart; used by bench.py) ----
+ * launch_count: kernels launched by this library since load.
+ * profile_enable(1): bracket every launch with CUDA events on its stream
+ * (clears previous records); profile_read syncs them and returns per-kernel
+ * totals: names (32 bytes each), ms, launch counts; returns #entries. */
+int64_t fc2t2_launch_count(void);
+int fc2t2_profile_enable(int on);
+int fc2t2_profile_read(int max_entries, char* names, double* ms, int64_t* counts);
+
+/* ---- engine: replaces Engine.__init__ table state (expansion.py:157-177) ---- */
+int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out);
+void fc2t2_engine_destroy(fc2t2_engine* e);
+/* Hand one fitted M2LTable to the engine (host arrays, kernel.py:124-141):
+ * offsets (K,3) int64, active (K,) uint8, coeffs (K,P,P) float64 [k][n]. */
+int fc2t2_engine_set_table(fc2t2_engine* e, int level, int nearfield, int64_t n_offsets,
+                           const int64_t* offsets, const uint8_t* active,
+                           const double* coeffs);
+/* Build the per-parity interaction lists and upload fp32 tables (once). */
+int fc2t2_engine_upload(fc2t2_engine* e, void* stream);
+/* number of (level, class) interaction-list entries, for diagnostics */
+int64_t fc2t2_engine_list_entries(const fc2t2_engine* e, int level, int table);
+/* copy a level's interaction list to host: (n, 4) int32 {dx,dy,dz,slot} and
+ * the class start offsets (ncls+1); returns ncls or -1 */
+int fc2t2_engine_get_list(const fc2t2_engine* e, int level, int table, int32_t* entries,
+                          int32_t* cls_start);
+
+/* ---- point -> cell: find_box (expansion.py:85-93) ---- */
+int fc2t2_find_box(int level, const float* d_pts, int64_t n, int32_t* d_box, int32_t* d_flag,
+                   void* stream);
+/* Stable sort of points by finest cell + per-cell ranges (the np.add.at key
+ * of expansion.py:195).  d_order (n) int32, d_cell_start (res^3 + 1) int32. */
+size_t fc2t2_cell_sort_workspace_size(int level, int64_t n);
+int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
+                    int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                    void* stream);
+
+/* ---- stages (expansion.py:186-264) ---- */
+int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
+              const int32_t* d_order, const int32_t* d_cell_start, float* d_m_finest,
+              void* stream);
+int fc2t2_m2m(const fc2t2_engine* e, int channels, int fine_level, const float* d_fine,
+              float* d_coarse, void* stream);
+int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float* d_coarse,
+              float* d_fine, int accumulate, void* stream);
+int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const float* d_m,
+              float* d_l, int accumulate, void* stream);
+
+/* ---- cascade: Engine.expand_from_moments (expansion.py:268-281) ---- */
+size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);
+int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                 float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- L2P: Accessor (expansion.py:335-373) ---- */
+int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d_q, int64_t n,
+              int mode, const float* d_wts, float* d_value, float* d_grad, float* d_hess,
+              float* d_wgrad, int32_t* d_flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FC2T2_B200_H */

@@ -1,0 +1,493 @@
+// extern "C" entry points (include/fc2t2_b200.h) and the engine handle.
+//
+// The engine owns the device copy of the M2L tables of one
+// Engine(kernel, levels) (reference expansion.py:157-177): fp32 PPxPP
+// matrices B[n][k] = A_o[k][n] for every *active* offset (the interaction
+// lists, kernel.py:275) and, per level, the list of (offset, slot) entries
+// grouped by target parity class.  For a parity stencil level
+// (reference expansion.py:236, :246-249) class (px, py, pz) sees -3 only on
+// odd axes and +3 only on even axes; the coarsest level and the near table
+// have one class.  At the finest level the near table is merged into every
+// class list so one M2L pass applies far + near.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/fc2t2_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return FC2T2_OK;
+  return fail(FC2T2_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+struct HostTable {
+  bool set = false;
+  std::vector<int64_t> offsets;  // K*3
+  std::vector<uint8_t> active;   // K
+  std::vector<double> coeffs;    // K*P*P
+};
+
+struct Plan {
+  int stride = 1, ncls = 1;
+  std::vector<int4> entries;
+  std::vector<int> cls_start;
+  int4* d_entries = nullptr;
+  int* d_cls_start = nullptr;
+  int max_list = 0;
+};
+
+}  // namespace
+
+// ------------------------------------------------------------ profiling ---
+namespace fc2t2 {
+namespace {
+std::atomic<long long> g_launches{0};
+bool g_prof = false;
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+size_t g_pool_used = 0;
+const char* g_pending = nullptr;
+cudaEvent_t g_pending_ev;
+
+cudaEvent_t next_event() {
+  if (g_pool_used == g_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_used++];
+}
+}  // namespace
+
+void prof_begin(const char* name, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof) return;
+  g_pending_ev = next_event();
+  cudaEventRecord(g_pending_ev, s);
+  g_pending = name;
+}
+
+void prof_end(cudaStream_t s) {
+  if (!g_prof || !g_pending) return;
+  cudaEvent_t b = next_event();
+  cudaEventRecord(b, s);
+  g_recs.push_back({g_pending, g_pending_ev, b});
+  g_pending = nullptr;
+}
+}  // namespace fc2t2
+
+struct fc2t2_engine {
+  int rho = 0, levels = 0, P = 0, PP = 0;
+  std::map<int, HostTable> far;
+  HostTable near;
+  bool uploaded = false;
+  float* d_coef = nullptr;
+  // plans[level][table]
+  std::map<int, std::map<int, Plan>> plans;
+};
+
+namespace {
+
+constexpr int kCoarsest = 2;
+
+// slot assignment and per-class entry lists for one table
+void append_table(const HostTable& t, int P, int PP, int parity, std::vector<float>& coef,
+                  std::vector<std::vector<int4>>& cls_lists) {
+  const int64_t K = (int64_t)t.active.size();
+  for (int64_t i = 0; i < K; ++i) {
+    if (!t.active[i]) continue;
+    const int dx = (int)t.offsets[3 * i], dy = (int)t.offsets[3 * i + 1],
+              dz = (int)t.offsets[3 * i + 2];
+    const int slot = (int)(coef.size() / ((size_t)PP * PP));
+    coef.resize(coef.size() + (size_t)PP * PP, 0.f);
+    float* B = coef.data() + (size_t)slot * PP * PP;
+    const double* A = t.coeffs.data() + (size_t)i * P * P;  // [k][n]
+    for (int k = 0; k < P; ++k)
+      for (int n = 0; n < P; ++n) B[(size_t)n * PP + k] = (float)A[(size_t)k * P + n];
+    const int ncls = (int)cls_lists.size();
+    for (int c = 0; c < ncls; ++c) {
+      if (parity) {
+        const int par[3] = {(c >> 2) & 1, (c >> 1) & 1, c & 1};
+        const int d[3] = {dx, dy, dz};
+        bool ok = true;
+        for (int a = 0; a < 3; ++a) {
+          if (d[a] == -3 && par[a] != 1) ok = false;
+          if (d[a] == 3 && par[a] != 0) ok = false;
+        }
+        if (!ok) continue;
+      }
+      cls_lists[c].push_back(make_int4(dx, dy, dz, slot));
+    }
+  }
+}
+
+void finish_plan(Plan& p, std::vector<std::vector<int4>>& lists) {
+  p.ncls = (int)lists.size();
+  p.cls_start.assign(1, 0);
+  p.entries.clear();
+  p.max_list = 0;
+  for (auto& l : lists) {
+    p.entries.insert(p.entries.end(), l.begin(), l.end());
+    p.cls_start.push_back((int)p.entries.size());
+    p.max_list = std::max(p.max_list, (int)l.size());
+  }
+}
+
+int plan_for(const fc2t2_engine* e, int level, int table, const Plan** out) {
+  if (!e || !e->uploaded) return fail(FC2T2_ESTAGE, "engine tables not uploaded");
+  auto it = e->plans.find(level);
+  if (it == e->plans.end()) return fail(FC2T2_ESTAGE, "no M2L table for this level");
+  auto jt = it->second.find(table);
+  if (jt == it->second.end()) return fail(FC2T2_ESTAGE, "table kind not available at this level");
+  *out = &jt->second;
+  return FC2T2_OK;
+}
+
+fc2t2::M2LLaunch launch_of(const Plan& p, int level) {
+  fc2t2::M2LLaunch l;
+  l.level = level;
+  l.stride = p.stride;
+  l.ncls = p.ncls;
+  l.entries = p.d_entries;
+  l.cls_start = p.d_cls_start;
+  l.max_list = p.max_list;
+  static const char* names[] = {"m2l_L0", "m2l_L1", "m2l_L2", "m2l_L3", "m2l_L4",
+                                "m2l_L5", "m2l_L6", "m2l_L7", "m2l_L8", "m2l_L9"};
+  l.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];
+  return l;
+}
+
+size_t grid_floats(int level, int C, int PP) {
+  const size_t res = (size_t)1 << (level + 1);
+  return res * res * res * (size_t)C * PP;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fc2t2_version(void) { return 1; }
+
+int64_t fc2t2_launch_count(void) { return fc2t2::g_launches.load(); }
+
+int fc2t2_profile_enable(int on) {
+  fc2t2::g_prof = on != 0;
+  fc2t2::g_recs.clear();
+  fc2t2::g_pool_used = 0;
+  fc2t2::g_pending = nullptr;
+  return FC2T2_OK;
+}
+
+int fc2t2_profile_read(int max_entries, char* names, double* ms, int64_t* counts) {
+  std::vector<std::string> keys;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto& r : fc2t2::g_recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return fail(FC2T2_ECUDA, "profile sync");
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    size_t k = 0;
+    while (k < keys.size() && keys[k] != r.name) ++k;
+    if (k == keys.size()) {
+      keys.push_back(r.name);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[k] += t;
+    cnt[k] += 1;
+  }
+  const int n = (int)std::min<size_t>(keys.size(), (size_t)max_entries);
+  for (int k = 0; k < n; ++k) {
+    std::snprintf(names + 32 * k, 32, "%s", keys[k].c_str());
+    ms[k] = tot[k];
+    counts[k] = cnt[k];
+  }
+  return n;
+}
+
+const char* fc2t2_last_error(void) { return g_last_error.c_str(); }
+
+int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out) {
+  if (!out) return fail(FC2T2_EVALUE, "null out pointer");
+  if (rho < 1 || rho > 6) return fail(FC2T2_EORDER, "expansion order must be in [1, 6]");
+  if (levels < kCoarsest || levels > 8) return fail(FC2T2_ESTAGE, "levels must be in [2, 8]");
+  auto* e = new fc2t2_engine();
+  e->rho = rho;
+  e->levels = levels;
+  e->P = fc2t2::index_count(rho);
+  e->PP = fc2t2::pad4(e->P);
+  *out = e;
+  return FC2T2_OK;
+}
+
+void fc2t2_engine_destroy(fc2t2_engine* e) {
+  if (!e) return;
+  cudaFree(e->d_coef);
+  for (auto& lv : e->plans)
+    for (auto& t : lv.second) {
+      cudaFree(t.second.d_entries);
+      cudaFree(t.second.d_cls_start);
+    }
+  delete e;
+}
+
+int fc2t2_engine_set_table(fc2t2_engine* e, int level, int nearfield, int64_t n_offsets,
+                           const int64_t* offsets, const uint8_t* active,
+                           const double* coeffs) {
+  if (!e) return fail(FC2T2_EVALUE, "null engine");
+  if (e->uploaded) return fail(FC2T2_ESTAGE, "engine already uploaded");
+  if (level < kCoarsest || level > e->levels) return fail(FC2T2_ESTAGE, "table level out of range");
+  if (nearfield && level != e->levels) return fail(FC2T2_ESTAGE, "near table must be finest level");
+  HostTable& t = nearfield ? e->near : e->far[level];
+  t.set = true;
+  t.offsets.assign(offsets, offsets + 3 * n_offsets);
+  t.active.assign(active, active + n_offsets);
+  t.coeffs.assign(coeffs, coeffs + (size_t)n_offsets * e->P * e->P);
+  return FC2T2_OK;
+}
+
+int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
+  if (!e) return fail(FC2T2_EVALUE, "null engine");
+  if (e->uploaded) return FC2T2_OK;
+  if (!e->near.set) return fail(FC2T2_ESTAGE, "near table missing");
+  for (int l = kCoarsest; l <= e->levels; ++l)
+    if (!e->far.count(l) || !e->far[l].set) return fail(FC2T2_ESTAGE, "far table missing");
+  std::vector<float> coef;
+  const int P = e->P, PP = e->PP;
+  for (int l = kCoarsest; l <= e->levels; ++l) {
+    const bool parity = l != kCoarsest;
+    {
+      std::vector<std::vector<int4>> lists(parity ? 8 : 1);
+      append_table(e->far[l], P, PP, parity, coef, lists);
+      Plan& p = e->plans[l][FC2T2_TABLE_FAR];
+      p.stride = parity ? 2 : 1;
+      finish_plan(p, lists);
+    }
+    if (l == e->levels) {
+      std::vector<std::vector<int4>> nl(1);
+      append_table(e->near, P, PP, 0, coef, nl);
+      Plan& pn = e->plans[l][FC2T2_TABLE_NEAR];
+      pn.stride = 1;
+      finish_plan(pn, nl);
+      // merged far + near: the near entries (same slots) appended to every class
+      const Plan& pf = e->plans[l][FC2T2_TABLE_FAR];
+      std::vector<std::vector<int4>> ml(pf.ncls);
+      for (int c = 0; c < pf.ncls; ++c) {
+        ml[c].assign(pf.entries.begin() + pf.cls_start[c], pf.entries.begin() + pf.cls_start[c + 1]);
+        ml[c].insert(ml[c].end(), pn.entries.begin(), pn.entries.end());
+      }
+      Plan& pm = e->plans[l][FC2T2_TABLE_FARNEAR];
+      pm.stride = pf.stride;
+      finish_plan(pm, ml);
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t err;
+  if (!coef.empty()) {
+    err = cudaMalloc(&e->d_coef, coef.size() * sizeof(float));
+    if (err != cudaSuccess) return cuda_status(err, "engine_upload malloc");
+    err = cudaMemcpyAsync(e->d_coef, coef.data(), coef.size() * sizeof(float),
+                          cudaMemcpyHostToDevice, s);
+    if (err != cudaSuccess) return cuda_status(err, "engine_upload copy");
+  }
+  for (auto& lv : e->plans)
+    for (auto& t : lv.second) {
+      Plan& p = t.second;
+      size_t ne = std::max<size_t>(p.entries.size(), 1);
+      err = cudaMalloc(&p.d_entries, ne * sizeof(int4));
+      if (err == cudaSuccess) err = cudaMalloc(&p.d_cls_start, p.cls_start.size() * sizeof(int));
+      if (err == cudaSuccess && !p.entries.empty())
+        err = cudaMemcpyAsync(p.d_entries, p.entries.data(), p.entries.size() * sizeof(int4),
+                              cudaMemcpyHostToDevice, s);
+      if (err == cudaSuccess)
+        err = cudaMemcpyAsync(p.d_cls_start, p.cls_start.data(), p.cls_start.size() * sizeof(int),
+                              cudaMemcpyHostToDevice, s);
+      if (err != cudaSuccess) return cuda_status(err, "engine_upload plans");
+    }
+  err = cudaStreamSynchronize(s);
+  if (err != cudaSuccess) return cuda_status(err, "engine_upload sync");
+  e->uploaded = true;
+  return FC2T2_OK;
+}
+
+int64_t fc2t2_engine_list_entries(const fc2t2_engine* e, int level, int table) {
+  const Plan* p;
+  if (plan_for(e, level, table, &p) != FC2T2_OK) return -1;
+  return (int64_t)p->entries.size();
+}
+
+int fc2t2_engine_get_list(const fc2t2_engine* e, int level, int table, int32_t* entries,
+                          int32_t* cls_start) {
+  const Plan* p;
+  if (plan_for(e, level, table, &p) != FC2T2_OK) return -1;
+  for (size_t i = 0; i < p->entries.size(); ++i) {
+    entries[4 * i] = p->entries[i].x;
+    entries[4 * i + 1] = p->entries[i].y;
+    entries[4 * i + 2] = p->entries[i].z;
+    entries[4 * i + 3] = p->entries[i].w;
+  }
+  for (size_t i = 0; i < p->cls_start.size(); ++i) cls_start[i] = p->cls_start[i];
+  return p->ncls;
+}
+
+int fc2t2_find_box(int level, const float* d_pts, int64_t n, int32_t* d_box, int32_t* d_flag,
+                   void* stream) {
+  if (level < 0 || level > 9 || n < 0) return fail(FC2T2_EVALUE, "bad find_box arguments");
+  return cuda_status(fc2t2::find_box(level, d_pts, n, d_box, d_flag, (cudaStream_t)stream),
+                     "find_box");
+}
+
+size_t fc2t2_cell_sort_workspace_size(int level, int64_t n) {
+  return fc2t2::cell_sort_workspace(level, n);
+}
+
+int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
+                    int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                    void* stream) {
+  if (level < 0 || level > 9 || n < 0 || n > INT32_MAX)
+    return fail(FC2T2_EVALUE, "bad cell_sort arguments");
+  if (ws_bytes < fc2t2::cell_sort_workspace(level, n))
+    return fail(FC2T2_EWORKSPACE, "cell_sort workspace too small");
+  return cuda_status(fc2t2::cell_sort(level, d_pts, n, d_order, d_cell_start, d_flag, d_ws,
+                                      ws_bytes, (cudaStream_t)stream),
+                     "cell_sort");
+}
+
+int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
+              const int32_t* d_order, const int32_t* d_cell_start, float* d_m_finest,
+              void* stream) {
+  if (!e || channels < 1) return fail(FC2T2_EVALUE, "bad p2m arguments");
+  return cuda_status(fc2t2::p2m_sorted(e->rho, e->levels, channels, d_pts, d_w, d_order,
+                                       d_cell_start, d_m_finest, (cudaStream_t)stream),
+                     "p2m");
+}
+
+int fc2t2_m2m(const fc2t2_engine* e, int channels, int fine_level, const float* d_fine,
+              float* d_coarse, void* stream) {
+  if (!e || channels < 1) return fail(FC2T2_EVALUE, "bad m2m arguments");
+  if (fine_level <= kCoarsest || fine_level > e->levels)
+    return fail(FC2T2_ESTAGE, "already at the coarsest level");
+  return cuda_status(
+      fc2t2::m2m(e->rho, fine_level, channels, d_fine, d_coarse, (cudaStream_t)stream), "m2m");
+}
+
+int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float* d_coarse,
+              float* d_fine, int accumulate, void* stream) {
+  if (!e || channels < 1) return fail(FC2T2_EVALUE, "bad l2l arguments");
+  if (coarse_level < kCoarsest - 1 || coarse_level >= 9)
+    return fail(FC2T2_ESTAGE, "bad l2l level");
+  return cuda_status(fc2t2::l2l(e->rho, coarse_level, channels, d_coarse, d_fine, accumulate,
+                                (cudaStream_t)stream),
+                     "l2l");
+}
+
+int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const float* d_m,
+              float* d_l, int accumulate, void* stream) {
+  const Plan* p;
+  int st = plan_for(e, level, table, &p);
+  if (st != FC2T2_OK) return st;
+  if (channels < 1) return fail(FC2T2_EVALUE, "channels must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->max_list == 0) {
+    if (accumulate) return FC2T2_OK;
+    return cuda_status(
+        cudaMemsetAsync(d_l, 0, grid_floats(level, channels, e->PP) * sizeof(float), s), "m2l");
+  }
+  return cuda_status(
+      fc2t2::m2l(e->rho, channels, launch_of(*p, level), e->d_coef, d_m, d_l, accumulate, s),
+      "m2l");
+}
+
+size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
+  if (!e) return 0;
+  size_t f = 0;
+  for (int l = kCoarsest; l < e->levels; ++l) f += 2 * grid_floats(l, channels, e->PP);
+  return f * sizeof(float) + 256;
+}
+
+int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                 float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!e || !e->uploaded) return fail(FC2T2_ESTAGE, "engine tables not uploaded");
+  if (channels < 1) return fail(FC2T2_EVALUE, "channels must be >= 1");
+  if (ws_bytes < fc2t2_expand_workspace_size(e, channels))
+    return fail(FC2T2_EWORKSPACE, "expand workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int L = e->levels;
+  std::vector<float*> Mg(L + 1, nullptr), Lg(L + 1, nullptr);
+  float* w = (float*)d_ws;
+  for (int l = kCoarsest; l < L; ++l) {
+    Mg[l] = w;
+    w += grid_floats(l, channels, e->PP);
+    Lg[l] = w;
+    w += grid_floats(l, channels, e->PP);
+  }
+  Mg[L] = const_cast<float*>(d_m_finest);
+  Lg[L] = d_l_finest;
+  // lowest level whose far table does any work (coarser M grids are unused)
+  int lowest = L;
+  for (int l = kCoarsest; l <= L; ++l) {
+    const int table = (l == L) ? FC2T2_TABLE_FARNEAR : FC2T2_TABLE_FAR;
+    if (e->plans.at(l).at(table).max_list > 0) {
+      lowest = l;
+      break;
+    }
+  }
+  int st;
+  for (int l = L; l > lowest; --l) {
+    st = cuda_status(fc2t2::m2m(e->rho, l, channels, Mg[l], Mg[l - 1], s), "expand m2m");
+    if (st != FC2T2_OK) return st;
+  }
+  bool have = false;
+  for (int l = lowest; l <= L; ++l) {
+    const int table = (l == L) ? FC2T2_TABLE_FARNEAR : FC2T2_TABLE_FAR;
+    const Plan& p = e->plans.at(l).at(table);
+    if (have) {
+      st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, Lg[l - 1], Lg[l], 0, s), "expand l2l");
+      if (st != FC2T2_OK) return st;
+    }
+    if (p.max_list > 0) {
+      st = cuda_status(fc2t2::m2l(e->rho, channels, launch_of(p, l), e->d_coef, Mg[l], Lg[l],
+                                  have ? 1 : 0, s),
+                       "expand m2l");
+      if (st != FC2T2_OK) return st;
+      have = true;
+    } else if (!have && l == L) {
+      st = cuda_status(
+          cudaMemsetAsync(Lg[L], 0, grid_floats(L, channels, e->PP) * sizeof(float), s),
+          "expand zero");
+      if (st != FC2T2_OK) return st;
+    }
+  }
+  return FC2T2_OK;
+}
+
+int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d_q, int64_t n,
+              int mode, const float* d_wts, float* d_value, float* d_grad, float* d_hess,
+              float* d_wgrad, int32_t* d_flag, void* stream) {
+  if (rho < 1 || rho > 6) return fail(FC2T2_EORDER, "expansion order must be in [1, 6]");
+  if (level < 0 || level > 9 || channels < 1 || n < 0) return fail(FC2T2_EVALUE, "bad l2p arguments");
+  if ((mode & FC2T2_L2P_WGRAD) && !d_wts) return fail(FC2T2_EVALUE, "WGRAD needs weights");
+  return cuda_status(fc2t2::l2p(rho, level, channels, d_l, d_q, n, mode, d_wts, d_value, d_grad,
+                                d_hess, d_wgrad, d_flag, (cudaStream_t)stream),
+                     "l2p");
+}
+
+}  // extern "C"

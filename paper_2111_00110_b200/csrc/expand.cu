@@ -1,0 +1,380 @@
+// The FC2T2 cascade on the device: P2M (sorted, segmented), M2M, M2L, L2L.
+//
+// Reference: pkg/src/fc2t2/expansion.py
+//   p2m   :186-198   M[cell, c, n] = sum_{i in cell} w_ic d_i^n / n!
+//   m2m   :200-213   coarse += sum_children fine[child] @ K_child^T, K lower-tri
+//   l2l   :215-225   fine[child] = coarse @ K_child^T, K upper-tri
+//   m2l   :227-264   L[t] += A_o M[t + o] over the level's active offsets,
+//                    parity restriction on +-3 offsets (:246-249)
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fc2t2 {
+
+namespace {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int PP>
+__device__ __forceinline__ void store_row(float* dst, const float (&v)[PP], bool accumulate) {
+#pragma unroll
+  for (int k = 0; k < PP; k += 4) {
+    float4 o = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+    if (accumulate) {
+      float4 a = *reinterpret_cast<const float4*>(dst + k);
+      o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+    }
+    *reinterpret_cast<float4*>(dst + k) = o;
+  }
+}
+
+template <int PP>
+__device__ __forceinline__ void load_row(const float* src, float (&v)[PP]) {
+#pragma unroll
+  for (int k = 0; k < PP; k += 4) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(src + k));
+    v[k] = a.x; v[k + 1] = a.y; v[k + 2] = a.z; v[k + 3] = a.w;
+  }
+}
+
+// ------------------------------------------------------------------ P2M ---
+// One thread per (cell, channel): walk the cell's points in ascending source
+// index (stable sort) and accumulate w * d^n/n! in registers -- the same
+// association order as np.add.at, no atomics.
+template <int RHO>
+__global__ void __launch_bounds__(128)
+p2m_sorted_kernel(const float* __restrict__ pts, const float* __restrict__ w, int C, int res,
+                  const int32_t* __restrict__ order, const int32_t* __restrict__ cell_start,
+                  float* __restrict__ M) {
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  const int64_t R = (int64_t)res * res * res;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R * C;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = g / C;
+    const int c = (int)(g - cell * C);
+    const int b2 = (int)(cell % res), b1 = (int)((cell / res) % res), b0 = (int)(cell / res / res);
+    float acc[PP];
+#pragma unroll
+    for (int j = 0; j < PP; ++j) acc[j] = 0.f;
+    const int beg = cell_start[cell], end = cell_start[cell + 1];
+    for (int k = beg; k < end; ++k) {
+      const int64_t i = order[k];
+      const float dx = box_offset(pts[3 * i], b0, res);
+      const float dy = box_offset(pts[3 * i + 1], b1, res);
+      const float dz = box_offset(pts[3 * i + 2], b2, res);
+      const float wv = w[i * C + c];
+      float mono[P];
+      monomials<RHO>(dx, dy, dz, mono);
+#pragma unroll
+      for (int j = 0; j < P; ++j) acc[j] = fmaf(wv, mono[j], acc[j]);
+    }
+    store_row<PP>(M + g * PP, acc, false);
+  }
+}
+
+// ------------------------------------------------------------- M2M/L2L ---
+// Child centre offset from the parent centre is d = (c - 1/2) * w_fine per
+// axis (reference expansion.py:170-175).  The binomial shift kernel
+// K[n, m] = d^(n-m) / (n-m)! (reference _shift_kernel, expansion.py:116-132)
+// factorises over the axes, so the 3D shift is three exact 1D shifts; every
+// intermediate index stays inside the total-degree table because a shift
+// only moves weight between indices of one axis.
+//
+//   UP   (M2M): out[n] = sum_{m <= n_a}  in[n - m e_a] t[m]
+//   DOWN (L2L): out[n] = sum_{m >= 0}    in[n + m e_a] t[m]   (|n + m e_a| <= rho)
+template <int RHO, int AXIS, bool UP>
+__device__ __forceinline__ void shift_axis(const float (&in)[MI<RHO>::P], float (&out)[MI<RHO>::P],
+                                           const float (&t)[RHO + 1]) {
+  constexpr MI<RHO> mi{};
+  constexpr int P = MI<RHO>::P;
+#pragma unroll
+  for (int n = 0; n < P; ++n) {
+    const int e0 = mi.e0[n], e1 = mi.e1[n], e2 = mi.e2[n];
+    float s = 0.f;
+#pragma unroll
+    for (int m = 0; m <= RHO; ++m) {
+      const int d0 = AXIS == 0 ? (UP ? -m : m) : 0;
+      const int d1 = AXIS == 1 ? (UP ? -m : m) : 0;
+      const int d2 = AXIS == 2 ? (UP ? -m : m) : 0;
+      const int j = MI<RHO>::index(e0 + d0, e1 + d1, e2 + d2);
+      if (j >= 0) s = fmaf(in[j], t[m], s);
+    }
+    out[n] = s;
+  }
+}
+
+template <int RHO, bool UP>
+__device__ __forceinline__ void shift3(float (&v)[MI<RHO>::P], float dx, float dy, float dz) {
+  constexpr int P = MI<RHO>::P;
+  float tx[RHO + 1], ty[RHO + 1], tz[RHO + 1];
+  tx[0] = ty[0] = tz[0] = 1.f;
+#pragma unroll
+  for (int m = 1; m <= RHO; ++m) {
+    tx[m] = tx[m - 1] * dx / (float)m;
+    ty[m] = ty[m - 1] * dy / (float)m;
+    tz[m] = tz[m - 1] * dz / (float)m;
+  }
+  float u[P];
+  shift_axis<RHO, 0, UP>(v, u, tx);
+  shift_axis<RHO, 1, UP>(u, v, ty);
+  shift_axis<RHO, 2, UP>(v, u, tz);
+#pragma unroll
+  for (int n = 0; n < P; ++n) v[n] = u[n];
+}
+
+template <int RHO>
+__global__ void __launch_bounds__(128)
+m2m_kernel(const float* __restrict__ fine, float* __restrict__ coarse, int C, int cres,
+           float half_fine) {
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  const int fres = 2 * cres;
+  const int64_t n = (int64_t)cres * cres * cres * C;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = g / C;
+    const int c = (int)(g - cell * C);
+    const int Z = (int)(cell % cres), Y = (int)((cell / cres) % cres), X = (int)(cell / cres / cres);
+    float acc[PP];
+#pragma unroll
+    for (int j = 0; j < PP; ++j) acc[j] = 0.f;
+#pragma unroll 1
+    for (int ch = 0; ch < 8; ++ch) {
+      const int cx = ch >> 2, cy = (ch >> 1) & 1, cz = ch & 1;
+      const int64_t fc = (((int64_t)(2 * X + cx) * fres + (2 * Y + cy)) * fres + (2 * Z + cz));
+      float f[PP];
+      load_row<PP>(fine + (fc * C + c) * PP, f);
+      float v[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) v[j] = f[j];
+      shift3<RHO, true>(v, cx ? half_fine : -half_fine, cy ? half_fine : -half_fine,
+                        cz ? half_fine : -half_fine);
+#pragma unroll
+      for (int j = 0; j < P; ++j) acc[j] += v[j];
+    }
+    store_row<PP>(coarse + g * PP, acc, false);
+  }
+}
+
+template <int RHO>
+__global__ void __launch_bounds__(128)
+l2l_kernel(const float* __restrict__ coarse, float* __restrict__ fine, int C, int cres,
+           float half_fine, int accumulate) {
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  const int fres = 2 * cres;
+  const int64_t n = (int64_t)fres * fres * fres * C;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = g / C;
+    const int c = (int)(g - cell * C);
+    const int z = (int)(cell % fres), y = (int)((cell / fres) % fres), x = (int)(cell / fres / fres);
+    const int64_t pc = ((int64_t)(x >> 1) * cres + (y >> 1)) * cres + (z >> 1);
+    float a[PP];
+    load_row<PP>(coarse + (pc * C + c) * PP, a);
+    float v[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = a[j];
+    shift3<RHO, false>(v, (x & 1) ? half_fine : -half_fine, (y & 1) ? half_fine : -half_fine,
+                       (z & 1) ? half_fine : -half_fine);
+    float out[PP];
+#pragma unroll
+    for (int j = 0; j < PP; ++j) out[j] = j < P ? v[j] : 0.f;
+    store_row<PP>(fine + g * PP, out, accumulate != 0);
+  }
+}
+
+// ------------------------------------------------------------------ M2L ---
+// Implicit GEMM on FP32 FFMA.  A CTA owns ROWS = 128*RPL (target, channel)
+// rows of one target parity class and walks that class's interaction list;
+// per entry it stages the gathered source rows M[t + o] (cp.async with
+// zero-fill for out-of-domain sources = the reference's slice clipping,
+// expansion.py:135-151) and the PPxPP table B[n][k] = A_o[k][n] in shared
+// memory (double buffered) and does a rank-PP update of its register tile.
+constexpr int M2L_THREADS = 128;
+
+template <int RHO, int RPL>
+__global__ void __launch_bounds__(M2L_THREADS, (RHO <= 4 ? 2 : 1))
+m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int res, int stride,
+                int nu, const int4* __restrict__ entries, const int* __restrict__ cls_start,
+                const float* __restrict__ coef, int accumulate) {
+  constexpr int PP = MI<RHO>::PP;
+  constexpr int NQ = PP / 4;
+  constexpr int ROWS = M2L_THREADS * RPL;
+  extern __shared__ __align__(16) float smem[];
+  float* As = smem;                                   // [2][ROWS][PP]
+  float* Bs = smem + 2 * ROWS * PP;                   // [2][PP][PP]
+  int4* rowinfo = reinterpret_cast<int4*>(Bs + 2 * PP * PP);  // [ROWS]
+
+  const int cls = blockIdx.y;
+  const int ox = stride == 2 ? (cls >> 2) & 1 : 0;
+  const int oy = stride == 2 ? (cls >> 1) & 1 : 0;
+  const int oz = stride == 2 ? cls & 1 : 0;
+  const int tpt = ROWS / C;
+  const int64_t ntgt = (int64_t)nu * nu * nu;
+  const int64_t t0 = (int64_t)blockIdx.x * tpt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (int r = tid; r < ROWS; r += M2L_THREADS) {
+    int4 info = make_int4(0, 0, 0, -1);
+    const int tl = r / C, c = r - tl * C;
+    const int64_t u = t0 + tl;
+    if (tl < tpt && u < ntgt) {
+      const int uz = (int)(u % nu), uy = (int)((u / nu) % nu), ux = (int)(u / nu / nu);
+      info = make_int4(ux * stride + ox, uy * stride + oy, uz * stride + oz, c);
+    }
+    rowinfo[r] = info;
+  }
+  __syncthreads();
+
+  const int lb = cls_start[cls], nl = cls_start[cls + 1] - lb;
+
+  auto stage = [&](int li, int buf) {
+    const int4 e = __ldg(entries + lb + li);
+    float* Ad = As + buf * ROWS * PP;
+    for (int q = tid; q < ROWS * NQ; q += M2L_THREADS) {
+      const int r = q / NQ, ch = q - r * NQ;
+      const int4 info = rowinfo[r];
+      const int sx = info.x + e.x, sy = info.y + e.y, sz = info.z + e.z;
+      const bool ok = info.w >= 0 && (unsigned)sx < (unsigned)res && (unsigned)sy < (unsigned)res &&
+                      (unsigned)sz < (unsigned)res;
+      const float* src =
+          ok ? M + ((((int64_t)sx * res + sy) * res + sz) * C + info.w) * PP + ch * 4 : M;
+      cp_async16(Ad + r * PP + ch * 4, src, ok ? 16 : 0);
+    }
+    const float* Bsrc = coef + (int64_t)e.w * PP * PP;
+    float* Bd = Bs + buf * PP * PP;
+    for (int q = tid; q < PP * NQ; q += M2L_THREADS) cp_async16(Bd + q * 4, Bsrc + q * 4, 16);
+    cp_async_commit();
+  };
+
+  float acc[RPL][PP];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i)
+#pragma unroll
+    for (int k = 0; k < PP; ++k) acc[i][k] = 0.f;
+
+  if (nl > 0) stage(0, 0);
+  for (int li = 0; li < nl; ++li) {
+    const int buf = li & 1;
+    if (li + 1 < nl) {
+      stage(li + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* Ab = As + buf * ROWS * PP + (warp * 32 * RPL + lane) * PP;
+    const float* Bb = Bs + buf * PP * PP;
+#pragma unroll 1
+    for (int n4 = 0; n4 < NQ; ++n4) {
+      float4 a[RPL];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        a[i] = *reinterpret_cast<const float4*>(Ab + i * 32 * PP + n4 * 4);
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        const float* brow = Bb + (n4 * 4 + nn) * PP;
+#pragma unroll
+        for (int k4 = 0; k4 < NQ; ++k4) {
+          const float4 b = *reinterpret_cast<const float4*>(brow + k4 * 4);
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const float av = nn == 0 ? a[i].x : nn == 1 ? a[i].y : nn == 2 ? a[i].z : a[i].w;
+            acc[i][4 * k4 + 0] = fmaf(av, b.x, acc[i][4 * k4 + 0]);
+            acc[i][4 * k4 + 1] = fmaf(av, b.y, acc[i][4 * k4 + 1]);
+            acc[i][4 * k4 + 2] = fmaf(av, b.z, acc[i][4 * k4 + 2]);
+            acc[i][4 * k4 + 3] = fmaf(av, b.w, acc[i][4 * k4 + 3]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = warp * 32 * RPL + i * 32 + lane;
+    const int4 info = rowinfo[r];
+    if (info.w < 0) continue;
+    const int64_t cell = ((int64_t)info.x * res + info.y) * res + info.z;
+    store_row<PP>(L + (cell * C + info.w) * PP, acc[i], accumulate != 0);
+  }
+}
+
+template <int RHO>
+constexpr int m2l_rpl() { return MI<RHO>::PP <= 36 ? 2 : 1; }
+
+template <int RHO>
+size_t m2l_smem() {
+  constexpr int PP = MI<RHO>::PP;
+  constexpr int ROWS = M2L_THREADS * m2l_rpl<RHO>();
+  return (size_t)(2 * ROWS * PP + 2 * PP * PP) * sizeof(float) + ROWS * sizeof(int4);
+}
+
+}  // namespace
+
+cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float* w,
+                       const int32_t* order, const int32_t* cell_start, float* M,
+                       cudaStream_t s) {
+  const int res = 1 << (level + 1);
+  const int64_t n = (int64_t)res * res * res * C;
+  FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("p2m", s,
+      p2m_sorted_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(
+          pts, w, C, res, order, cell_start, M)));
+  return cudaGetLastError();
+}
+
+cudaError_t m2m(int rho, int fine_level, int C, const float* fine, float* coarse,
+                cudaStream_t s) {
+  const int cres = 1 << fine_level;  // res of fine_level - 1
+  const int64_t n = (int64_t)cres * cres * cres * C;
+  const float half_fine = (float)(0.5 * 2.0 / (double)(2 * cres));
+  FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("m2m", s,
+      m2m_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(fine, coarse, C, cres,
+                                                                    half_fine)));
+  return cudaGetLastError();
+}
+
+cudaError_t l2l(int rho, int coarse_level, int C, const float* coarse, float* fine,
+                int accumulate, cudaStream_t s) {
+  const int cres = 1 << (coarse_level + 1);
+  const int64_t n = (int64_t)8 * cres * cres * cres * C;
+  const float half_fine = (float)(0.5 * 2.0 / (double)(2 * cres));
+  FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("l2l", s,
+      l2l_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(coarse, fine, C, cres,
+                                                                    half_fine, accumulate)));
+  return cudaGetLastError();
+}
+
+cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
+                float* L, int accumulate, cudaStream_t s) {
+  const int res = 1 << (plan.level + 1);
+  const int nu = res / plan.stride;
+  FC2T2_DISPATCH_RHO(rho, {
+    constexpr int RPL = m2l_rpl<RHO>();
+    constexpr int ROWS = M2L_THREADS * RPL;
+    if (C > ROWS) return cudaErrorNotSupported;
+    const int tpt = ROWS / C;
+    const int64_t ntgt = (int64_t)nu * nu * nu;
+    const size_t smem = m2l_smem<RHO>();
+    auto kern = m2l_ffma_kernel<RHO, RPL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((ntgt + tpt - 1) / tpt), (unsigned)plan.ncls);
+    FC2T2_LAUNCH(plan.level_name, s,
+                 kern<<<grid, M2L_THREADS, smem, s>>>(M, L, C, res, plan.stride, nu, plan.entries,
+                                                      plan.cls_start, coef, accumulate));
+  });
+  return cudaGetLastError();
+}
+
+}  // namespace fc2t2

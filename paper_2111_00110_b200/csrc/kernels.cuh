@@ -1,0 +1,53 @@
+// Internal launcher declarations (C++ side of the C ABI in abi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+namespace fc2t2 {
+
+// sort.cu ----------------------------------------------------------------
+size_t cell_sort_workspace(int level, int64_t n);
+cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order,
+                      int32_t* cell_start, int32_t* flag, void* ws, size_t ws_bytes,
+                      cudaStream_t s);
+cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,
+                     cudaStream_t s);
+size_t scan_ws_words(int64_t n);
+cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* ws,
+                           cudaStream_t s);
+
+// expand.cu --------------------------------------------------------------
+cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float* w,
+                       const int32_t* order, const int32_t* cell_start, float* M,
+                       cudaStream_t s);
+cudaError_t m2m(int rho, int fine_level, int C, const float* fine, float* coarse, cudaStream_t s);
+cudaError_t l2l(int rho, int coarse_level, int C, const float* coarse, float* fine,
+                int accumulate, cudaStream_t s);
+
+// One M2L launch: every target class (8 parity classes, or 1 for a
+// parity-free stencil) walks its own interaction list.
+struct M2LLaunch {
+  int level;
+  int stride;            // 2 with parity classes, 1 without
+  int ncls;              // 8 or 1
+  const int4* entries;   // device, {dx, dy, dz, slot}
+  const int* cls_start;  // device, ncls + 1
+  int max_list;          // host copy of the longest list (0 -> nothing to do)
+  const char* level_name;  // profiling label, e.g. "m2l_L5"
+};
+cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
+                float* L, int accumulate, cudaStream_t s);
+
+// l2p.cu -----------------------------------------------------------------
+enum L2PMode : int {
+  L2P_VALUE = 1,   // (n, C)
+  L2P_GRAD = 2,    // (n, C, 3)
+  L2P_HESS = 4,    // (n, C, 6)  xx yy zz xy xz yz
+  L2P_WGRAD = 8,   // (n, 3) = sum_c wts[n, c] * grad f_c
+};
+cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64_t n, int mode,
+                const float* wts, float* value, float* grad, float* hess, float* wgrad,
+                int32_t* flag, cudaStream_t s);
+
+}  // namespace fc2t2

@@ -1,0 +1,302 @@
+// Point -> cell keys and a stable counting/radix sort by cell.
+//
+// Replaces the reference's find_box + np.add.at key (reference
+// expansion.py:85-93, :195): P2M wants every cell's points contiguous and in
+// ascending source index so that the per-cell sum is accumulated in the same
+// order as np.add.at and is bit-reproducible run to run.  That is a *stable*
+// sort by cell id, done here as an LSD radix sort of (cell, index) pairs with
+// 6-8 bit digits (2-3 passes for 15-21 bit keys), plus a cell histogram whose
+// exclusive scan gives every cell's [start, end) range.  No float atomics
+// anywhere, so P2M is deterministic.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace fc2t2 {
+
+namespace {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096
+
+constexpr int RADIX_THREADS = 256;
+constexpr int RADIX_ROUNDS = 16;
+constexpr int RADIX_TILE = RADIX_THREADS * RADIX_ROUNDS;  // 4096 keys per block
+constexpr int RADIX_WARPS = RADIX_THREADS / 32;
+
+// ---------------------------------------------------------------- keys ---
+
+__global__ void cell_keys_kernel(const float* __restrict__ pts, int64_t n, int res,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                 uint32_t* __restrict__ counts, int32_t* __restrict__ flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+    bad |= outside_domain(x, y, z);
+    int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
+    uint32_t key = ((uint32_t)b0 * res + b1) * res + b2;
+    keys[i] = key;
+    vals[i] = (uint32_t)i;
+    atomicAdd(&counts[key], 1u);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
+}
+
+__global__ void find_box_kernel(const float* __restrict__ pts, int64_t n, int res,
+                                int32_t* __restrict__ box, int32_t* __restrict__ flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+    bad |= outside_domain(x, y, z);
+    box[3 * i] = box_axis(x, res);
+    box[3 * i + 1] = box_axis(y, res);
+    box[3 * i + 2] = box_axis(z, res);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- scan ---
+// Exclusive scan of uint32, three phases (tile scan, scan of tile sums,
+// add-back), recursion on the tile sums.
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot,
+                                                         uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  total = warp_tot[(blockDim.x >> 5) - 1];
+  uint32_t before = warp > 0 ? warp_tot[warp - 1] : 0u;
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void scan_tiles_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                  int64_t n, uint32_t* __restrict__ tile_sums) {
+  __shared__ uint32_t warp_tot[32];
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  uint32_t v[SCAN_ITEMS];
+  uint32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    int64_t i = base + k;
+    v[k] = i < n ? in[i] : 0u;
+    s += v[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive_scan(s, warp_tot, total);
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    int64_t i = base + k;
+    if (i < n) out[i] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void scan_add_kernel(uint32_t* __restrict__ out, int64_t n,
+                                const uint32_t* __restrict__ tile_offsets) {
+  const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  const uint32_t off = tile_offsets[blockIdx.x];
+  for (int k = threadIdx.x; k < SCAN_TILE; k += blockDim.x) {
+    int64_t i = base + k;
+    if (i < n) out[i] += off;
+  }
+}
+
+size_t scan_ws_words(int64_t n) {
+  size_t w = 0;
+  while (n > SCAN_TILE) {
+    n = (n + SCAN_TILE - 1) / SCAN_TILE;
+    w += (size_t)n;
+  }
+  return w;
+}
+
+cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* ws,
+                           cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+  uint32_t* sums = tiles > 1 ? ws : nullptr;
+  FC2T2_LAUNCH("scan", s, scan_tiles_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, sums));
+  if (tiles > 1) {
+    cudaError_t e = exclusive_scan(sums, sums, tiles, ws + tiles, s);
+    if (e != cudaSuccess) return e;
+    FC2T2_LAUNCH("scan", s, scan_add_kernel<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(out, n, sums));
+  }
+  return cudaGetLastError();
+}
+
+namespace {
+
+// --------------------------------------------------------------- radix ---
+
+__global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                  int bits, int nblocks, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[256];
+  const int nbins = 1 << bits;
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * RADIX_TILE;
+  const uint32_t mask = (uint32_t)nbins - 1;
+  for (int k = threadIdx.x; k < RADIX_TILE; k += blockDim.x) {
+    int64_t i = base + k;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    hist[(int64_t)b * nblocks + blockIdx.x] = h[b];
+}
+
+// Stable scatter: keys of one block are ranked in index order, round by
+// round (256 keys per round), with warp-level match for ties inside a warp
+// and a per-(warp, digit) prefix across the 8 warps of the round.
+__global__ void __launch_bounds__(RADIX_THREADS)
+radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                     int64_t n, int shift, int bits, int nblocks,
+                     const uint32_t* __restrict__ offsets) {
+  __shared__ uint32_t running[256];
+  __shared__ uint32_t wcount[RADIX_WARPS][256];
+  const int nbins = 1 << bits;
+  const uint32_t mask = (uint32_t)nbins - 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
+    running[b] = offsets[(int64_t)b * nblocks + blockIdx.x];
+  const int64_t base = (int64_t)blockIdx.x * RADIX_TILE;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  for (int r = 0; r < RADIX_ROUNDS; ++r) {
+    for (int b = threadIdx.x; b < RADIX_WARPS * 256; b += blockDim.x) (&wcount[0][0])[b] = 0;
+    __syncthreads();
+    const int64_t i = base + (int64_t)r * RADIX_THREADS + threadIdx.x;
+    const bool valid = i < n;
+    uint32_t key = 0, val = 0, digit = 0xffffffffu;
+    if (valid) {
+      key = keys_in[i];
+      val = vals_in[i];
+      digit = (key >> shift) & mask;
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, digit);
+    const uint32_t rank = __popc(peers & lt_mask);
+    if (valid && rank == 0) wcount[warp][digit] = __popc(peers);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+      uint32_t acc = running[b];
+#pragma unroll
+      for (int w = 0; w < RADIX_WARPS; ++w) {
+        uint32_t c = wcount[w][b];
+        wcount[w][b] = acc;
+        acc += c;
+      }
+      running[b] = acc;
+    }
+    __syncthreads();
+    if (valid) {
+      uint32_t pos = wcount[warp][digit] + rank;
+      keys_out[pos] = key;
+      vals_out[pos] = val;
+    }
+    __syncthreads();
+  }
+}
+
+struct SortWs {
+  uint32_t *keys, *keys2, *vals, *vals2, *hist, *scan, *counts;
+};
+
+size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+}  // namespace
+
+size_t cell_sort_workspace(int level, int64_t n) {
+  const int64_t R = (int64_t)1 << (3 * (level + 1));
+  const int64_t nblocks = (n + RADIX_TILE - 1) / RADIX_TILE;
+  const int64_t hist = 256 * (nblocks > 0 ? nblocks : 1);
+  size_t b = 0;
+  b += 4 * align256(4 * (size_t)n);  // keys, keys2, vals, vals2
+  b += align256(4 * (size_t)hist);
+  b += align256(4 * std::max(scan_ws_words(hist), scan_ws_words(R + 1)) + 4);
+  b += align256(4 * (size_t)(R + 1));  // counts
+  return b;
+}
+
+cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, int32_t* cell_start,
+                      int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int res = 1 << (level + 1);
+  const int64_t R = (int64_t)res * res * res;
+  if (ws_bytes < cell_sort_workspace(level, n)) return cudaErrorInvalidValue;
+  const int64_t nblocks = std::max<int64_t>(1, (n + RADIX_TILE - 1) / RADIX_TILE);
+  char* p = (char*)ws;
+  auto take = [&](size_t bytes) { char* q = p; p += align256(bytes); return (uint32_t*)q; };
+  SortWs w;
+  w.keys = take(4 * (size_t)n);
+  w.keys2 = take(4 * (size_t)n);
+  w.vals = take(4 * (size_t)n);
+  w.vals2 = take(4 * (size_t)n);
+  w.hist = take(4 * (size_t)(256 * nblocks));
+  w.scan = take(4 * std::max(scan_ws_words(256 * nblocks), scan_ws_words(R + 1)) + 4);
+  w.counts = take(4 * (size_t)(R + 1));
+
+  cudaError_t e = cudaMemsetAsync(w.counts, 0, 4 * (size_t)(R + 1), s);
+  if (e != cudaSuccess) return e;
+  if (n > 0)
+    FC2T2_LAUNCH("cell_keys", s,
+                 cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.vals,
+                                                                      w.counts, flag));
+  // cell ranges: exclusive scan of the per-cell counts (entry R = n)
+  e = exclusive_scan(w.counts, (uint32_t*)cell_start, R + 1, w.scan, s);
+  if (e != cudaSuccess || n == 0) return e != cudaSuccess ? e : cudaGetLastError();
+
+  const int key_bits = 3 * (level + 1);
+  const int passes = (key_bits + 7) / 8;
+  const int digit = (key_bits + passes - 1) / passes;
+  uint32_t *kin = w.keys, *vin = w.vals;
+  for (int ps = 0; ps < passes; ++ps) {
+    const int shift = ps * digit;
+    const int bits = std::min(digit, key_bits - shift);
+    const bool last = ps == passes - 1;
+    uint32_t* kout = (kin == w.keys) ? w.keys2 : w.keys;
+    uint32_t* vout = last ? (uint32_t*)order : ((vin == w.vals) ? w.vals2 : w.vals);
+    FC2T2_LAUNCH("radix_hist", s,
+                 radix_hist_kernel<<<(unsigned)nblocks, RADIX_THREADS, 0, s>>>(
+                     kin, n, shift, bits, (int)nblocks, w.hist));
+    e = exclusive_scan(w.hist, w.hist, (int64_t)(1 << bits) * nblocks, w.scan, s);
+    if (e != cudaSuccess) return e;
+    FC2T2_LAUNCH("radix_scatter", s,
+                 radix_scatter_kernel<<<(unsigned)nblocks, RADIX_THREADS, 0, s>>>(
+                     kin, vin, kout, vout, n, shift, bits, (int)nblocks, w.hist));
+    kin = kout;
+    vin = vout;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,
+                     cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  FC2T2_LAUNCH("find_box", s,
+               find_box_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, 1 << (level + 1), box,
+                                                                   flag));
+  return cudaGetLastError();
+}
+
+}  // namespace fc2t2

@@ -1,0 +1,530 @@
+"""Device-resident FC2T2 engine: the drop-in for ``fc2t2.expansion``.
+
+Same names, arguments, dataclass fields and exceptions as the reference
+(``pkg/src/fc2t2/expansion.py``); the arrays live in HBM as float32 torch
+tensors and every stage runs through the C ABI (``include/fc2t2_b200.h``):
+
+    SourceSet            reference :31-54   (p, w) on the device
+    ExpansionGrid        reference :57-76   ``storage`` is (res,res,res,C,PP);
+                                            ``data`` is the (res,res,res,C,P) view
+    find_box/box_centers reference :79-93   bit-exact cell indices (fp64 on device)
+    Engine.p2m           reference :186-198 stable sort by cell + segmented sum
+    Engine.m2m/l2l/m2l   reference :200-264
+    Engine.expand*       reference :268-285 one fused cascade call
+    Accessor             reference :296-398 L2P value / partials / partials2
+
+Inputs may be numpy arrays (converted to float32 and uploaded) or torch
+tensors; results come back in the caller's kind (numpy in -> numpy out,
+torch in -> torch CUDA out), so reference-style numpy user code keeps working.
+``Engine.flops`` and ``Engine.expansion_count`` follow the reference's
+counting rules exactly (they are host-side tallies, pinned by tests).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, flops
+from .kernel import (COARSEST_LEVEL, KernelModel, M2LTable, fit_m2l_tables,
+                     level_box_width, level_resolution)
+from .multiindex import MultiIndexTable
+
+
+class DomainError(ValueError):
+    """A location lies on or outside the boundary of (-1, 1)^3 (reference :23-24)."""
+
+
+class StageError(ValueError):
+    """A grid of the wrong kind/level was fed to a stage (reference :27-28)."""
+
+
+# ------------------------------------------------------------- plumbing ---
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the FC2T2 B200 engine needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream():
+    return ct_void(torch.cuda.current_stream().cuda_stream)
+
+
+def ct_void(v):
+    import ctypes
+    return ctypes.c_void_p(int(v))
+
+
+def _ptr(t: torch.Tensor | None):
+    import ctypes
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+_ONE_BELOW = np.float32(np.nextafter(np.float32(1.0), np.float32(0.0)))
+
+
+def to_device(x, cols: int | None = None, points: bool = False) -> torch.Tensor:
+    """float32 contiguous CUDA tensor from numpy / torch input.
+
+    ``points=True`` keeps coordinates strictly inside (-1, 1) after the
+    float32 rounding (a float64 value just below 1 can round to 1.0f); the
+    domain check itself happened on the float64 input.
+    """
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=_device(), dtype=torch.float32)
+    else:
+        a = np.asarray(x, dtype=np.float64)
+        a32 = a.astype(np.float32)
+        if points and a32.size:
+            a32 = np.clip(a32, -_ONE_BELOW, _ONE_BELOW)
+        t = torch.from_numpy(a32).to(_device())
+    if cols is not None:
+        if t.dim() == 1:
+            t = t.reshape(-1, cols) if cols == 3 else t.reshape(-1, 1)
+        t = t.reshape(t.shape[0], -1)
+    return t.contiguous()
+
+
+def like_input(t: torch.Tensor, ref):
+    """Return ``t`` in the caller's kind: CUDA tensor for CUDA input, a
+    (pinned) host tensor for host-tensor input, float64 numpy for numpy."""
+    if isinstance(ref, torch.Tensor):
+        if ref.is_cuda:
+            return t
+        out = t.to("cpu", non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _host_domain_check(a, what: str) -> None:
+    if isinstance(a, torch.Tensor):
+        return
+    a = np.asarray(a, dtype=np.float64)
+    if a.size and np.max(np.abs(a)) >= 1.0:
+        raise DomainError(f"{what} locations must lie strictly inside (-1, 1)^3")
+
+
+class DomainFlag:
+    """Device int32 accumulating FLAG_* bits; read once per public call."""
+
+    def __init__(self):
+        self.t = torch.zeros(1, dtype=torch.int32, device=_device())
+
+    def raise_if_set(self, what: str) -> None:
+        v = int(self.t.item())
+        if v & _lib.FLAG_DOMAIN:
+            self.t.zero_()
+            raise DomainError(f"{what} locations must lie strictly inside (-1, 1)^3")
+
+
+# ------------------------------------------------------------ datatypes ---
+
+@dataclass
+class SourceSet:
+    """Source locations and per-channel weights, device resident (reference :31-54)."""
+
+    p: object    # (N, 3)
+    w: object    # (N, C)
+
+    def __post_init__(self):
+        self._numpy_input = not isinstance(self.p, torch.Tensor)
+        p_np = None if isinstance(self.p, torch.Tensor) else np.atleast_2d(
+            np.asarray(self.p, dtype=np.float64))
+        w_in = self.w
+        if not isinstance(w_in, torch.Tensor):
+            w_in = np.asarray(w_in, dtype=np.float64)
+            if w_in.ndim == 1:
+                w_in = w_in[:, None]
+        elif w_in.dim() == 1:
+            w_in = w_in[:, None]
+        n_p = p_np.shape[0] if p_np is not None else self.p.reshape(-1, 3).shape[0]
+        if n_p != w_in.shape[0]:
+            raise ValueError("p and w disagree on the number of sources")
+        if p_np is not None:
+            _host_domain_check(p_np, "source")
+        self.p = to_device(p_np if p_np is not None else self.p, 3, points=True)
+        self.w = to_device(w_in).reshape(self.p.shape[0], -1)
+
+    @property
+    def n(self) -> int:
+        return int(self.p.shape[0])
+
+    @property
+    def channels(self) -> int:
+        return int(self.w.shape[1])
+
+
+@dataclass
+class ExpansionGrid:
+    """Per-level grid of coefficient rows (reference :57-76).
+
+    ``storage`` is the padded device tensor (res, res, res, C, PP); ``data``
+    is its (res, res, res, C, P) view in graded-lex order.
+    """
+
+    level: int
+    kind: str
+    storage: torch.Tensor
+    rho: int
+
+    @property
+    def data(self) -> torch.Tensor:
+        from .multiindex import index_count
+        return self.storage[..., :index_count(self.rho)]
+
+    @property
+    def res(self) -> int:
+        return int(self.storage.shape[0])
+
+    @property
+    def channels(self) -> int:
+        return int(self.storage.shape[3])
+
+    @property
+    def box_width(self) -> float:
+        return level_box_width(self.level)
+
+
+def box_centers(level: int, idx) -> np.ndarray:
+    """Centres of boxes with index triples ``idx`` (reference :79-82)."""
+    w = level_box_width(level)
+    return -1.0 + (np.asarray(idx, dtype=np.float64) + 0.5) * w
+
+
+def find_box(level: int, q):
+    """Box index triples, bit-exact with the reference (:85-93), computed by
+    the device kernel (float64 arithmetic on the float32 coordinates)."""
+    pts = to_device(q, 3)
+    out = torch.empty((pts.shape[0], 3), dtype=torch.int32, device=pts.device)
+    _lib.call("fc2t2_find_box", int(level), _ptr(pts), int(pts.shape[0]), _ptr(out),
+              _ptr(None), _stream())
+    if isinstance(q, torch.Tensor):
+        return out
+    return out.cpu().numpy().astype(np.int64).reshape(np.shape(q))
+
+
+def axis_points(n: int, a: float = -1.0, b: float = 1.0) -> np.ndarray:
+    """linspace with bare domain endpoints nudged inward (reference :288-293)."""
+    lo = np.nextafter(-1.0, 0.0) if a <= -1.0 else a
+    hi = np.nextafter(1.0, 0.0) if b >= 1.0 else b
+    return np.linspace(lo, hi, n)
+
+
+def _axis_target_count(res: int, delta: int, parity) -> int:
+    """Number of targets one stencil offset touches along an axis (the
+    slice bounds of reference _axis_slices, :135-151)."""
+    lo, hi = max(0, -delta), min(res - 1, res - 1 - delta)
+    if parity is not None:
+        if lo % 2 != parity:
+            lo += 1
+        if hi % 2 != parity:
+            hi -= 1
+        return 0 if lo > hi else (hi - lo) // 2 + 1
+    return max(0, hi - lo + 1)
+
+
+def m2l_pairs(table: M2LTable) -> int:
+    """(target, offset) pairs one M2L pass over ``table`` touches; times
+    C*P*P*2 this is the reference's FLOP count (expansion.py:262)."""
+    res = level_resolution(table.level)
+    parity_stencil = not table.nearfield and table.level != COARSEST_LEVEL
+    total = 0
+    for off, act in zip(table.offsets, table.active):
+        if not act:
+            continue
+        cnt = 1
+        for a in range(3):
+            d = int(off[a])
+            parity = (1 if d == -3 else 0) if (parity_stencil and abs(d) == 3) else None
+            cnt *= _axis_target_count(res, d, parity)
+        total += cnt
+    return total
+
+
+# --------------------------------------------------------------- engine ---
+
+class _Handle:
+    def __init__(self, rho: int, levels: int):
+        import ctypes
+        self.lib = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.fc2t2_engine_create(rho, levels, ctypes.byref(h)), "engine_create")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.fc2t2_engine_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Engine:
+    """A configured transform (reference expansion.py:154-285)."""
+
+    def __init__(self, kernel: KernelModel, levels: int, lsq: bool = True,
+                 nodes_per_axis: int = 6, admissibility_tol: float = 1e-3,
+                 check_admissibility: bool = True):
+        if levels < COARSEST_LEVEL:
+            raise StageError(f"levels must be >= {COARSEST_LEVEL}")
+        self.kernel = kernel
+        self.levels = levels
+        self.rho = kernel.rho
+        self.table: MultiIndexTable = kernel.table
+        self.lsq = lsq
+        self.m2l_tables = fit_m2l_tables(
+            kernel, levels, lsq=lsq, nodes_per_axis=nodes_per_axis,
+            admissibility_tol=admissibility_tol, check=check_admissibility)
+        self.flops = flops.FlopCounter()
+        self.expansion_count = 0
+        self.P = self.table.size
+        self.PP = self.table.padded_size
+        self._pairs = {("far", l): m2l_pairs(t) for l, t in self.m2l_tables["far"].items()}
+        self._pairs[("near", levels)] = m2l_pairs(self.m2l_tables["near"])
+        self._h = None
+        self.flag = None
+
+    # the device side is created lazily so the host tables can be built
+    # (and pinned by CPU tests) without a GPU
+    @property
+    def handle(self):
+        if self._h is None:
+            h = _Handle(self.rho, self.levels)
+            tabs = list(self.m2l_tables["far"].values()) + [self.m2l_tables["near"]]
+            for t in tabs:
+                off = np.ascontiguousarray(t.offsets, dtype=np.int64)
+                act = np.ascontiguousarray(t.active, dtype=np.uint8)
+                co = np.ascontiguousarray(t.coeffs, dtype=np.float64)
+                _lib.check(h.lib.fc2t2_engine_set_table(
+                    h.h, int(t.level), int(bool(t.nearfield)), int(off.shape[0]),
+                    off.ctypes.data, act.ctypes.data, co.ctypes.data), "engine_set_table")
+            _lib.check(h.lib.fc2t2_engine_upload(h.h, _stream()), "engine_upload")
+            self._h = h
+            self.flag = DomainFlag()
+        return self._h.h
+
+    def interaction_list(self, level: int, table: int = _lib.TABLE_FAR):
+        """Device interaction list of one level: (entries (n,4) {dx,dy,dz,slot},
+        class starts (ncls+1,)) -- exposed for the bit-exactness tests."""
+        n = _lib.lib().fc2t2_engine_list_entries(self.handle, level, table)
+        if n < 0:
+            _lib.check(_lib.ESTAGE, "engine_list_entries")
+        ent = np.zeros((max(n, 1), 4), dtype=np.int32)
+        starts = np.zeros(9, dtype=np.int32)
+        ncls = _lib.lib().fc2t2_engine_get_list(self.handle, level, table, ent.ctypes.data,
+                                                starts.ctypes.data)
+        return ent[:n], starts[:ncls + 1]
+
+    # -- grids --------------------------------------------------------------
+
+    def zero_grid(self, level: int, channels: int, kind: str) -> ExpansionGrid:
+        res = level_resolution(level)
+        st = torch.zeros((res, res, res, channels, self.PP), dtype=torch.float32,
+                         device=_device())
+        return ExpansionGrid(level=level, kind=kind, storage=st, rho=self.rho)
+
+    def _empty_grid(self, level: int, channels: int, kind: str) -> ExpansionGrid:
+        res = level_resolution(level)
+        st = torch.empty((res, res, res, channels, self.PP), dtype=torch.float32,
+                         device=_device())
+        return ExpansionGrid(level=level, kind=kind, storage=st, rho=self.rho)
+
+    # -- stages -------------------------------------------------------------
+
+    def sort_points(self, pts: torch.Tensor):
+        """Stable sort by finest cell: (order (n,), cell_start (res^3+1,))."""
+        n = int(pts.shape[0])
+        R = level_resolution(self.levels) ** 3
+        ws_bytes = _lib.lib().fc2t2_cell_sort_workspace_size(self.levels, n)
+        ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=pts.device)
+        order = torch.empty(max(n, 1), dtype=torch.int32, device=pts.device)
+        start = torch.empty(R + 1, dtype=torch.int32, device=pts.device)
+        _ = self.handle
+        _lib.call("fc2t2_cell_sort", self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
+                  _ptr(self.flag.t), _ptr(ws), int(ws_bytes), _stream())
+        return order, start
+
+    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor) -> ExpansionGrid:
+        grid = self._empty_grid(self.levels, int(w.shape[1]), "M")
+        order, start = self.sort_points(pts)
+        _lib.call("fc2t2_p2m", self.handle, int(w.shape[1]), _ptr(pts), _ptr(w), _ptr(order),
+                  _ptr(start), _ptr(grid.storage), _stream())
+        self.flops.add("p2m", flops.p2m_flops(int(pts.shape[0]), self.rho, self.P))
+        return grid
+
+    def p2m(self, sources: SourceSet) -> ExpansionGrid:
+        grid = self.p2m_device(sources.p, sources.w)
+        self.flag.raise_if_set("source")
+        return grid
+
+    def m2m(self, fine: ExpansionGrid) -> ExpansionGrid:
+        if fine.kind != "M":
+            raise StageError("m2m expects an M grid")
+        if fine.level <= COARSEST_LEVEL:
+            raise StageError("already at the coarsest level")
+        coarse = self._empty_grid(fine.level - 1, fine.channels, "M")
+        _lib.call("fc2t2_m2m", self.handle, fine.channels, fine.level,
+                  _ptr(fine.storage.contiguous()), _ptr(coarse.storage), _stream())
+        self.flops.add("m2m", flops.translate_flops(coarse.res, self.P))
+        return coarse
+
+    def l2l(self, coarse: ExpansionGrid) -> ExpansionGrid:
+        if coarse.kind != "L":
+            raise StageError("l2l expects an L grid")
+        fine = self._empty_grid(coarse.level + 1, coarse.channels, "L")
+        _lib.call("fc2t2_l2l", self.handle, coarse.channels, coarse.level,
+                  _ptr(coarse.storage.contiguous()), _ptr(fine.storage), 0, _stream())
+        self.flops.add("l2l", flops.translate_flops(coarse.res, self.P))
+        return fine
+
+    def m2l(self, m: ExpansionGrid, table: M2LTable) -> ExpansionGrid:
+        if m.kind != "M":
+            raise StageError("m2l expects an M grid")
+        if m.level != table.level:
+            raise StageError(f"grid level {m.level} != table level {table.level}")
+        kind = _lib.TABLE_NEAR if table.nearfield else _lib.TABLE_FAR
+        out = self._empty_grid(m.level, m.channels, "L")
+        _lib.call("fc2t2_m2l", self.handle, m.channels, m.level, kind,
+                  _ptr(m.storage.contiguous()), _ptr(out.storage), 0, _stream())
+        key = ("near" if table.nearfield else "far", table.level)
+        self.flops.add("m2l", self._pairs[key] * m.channels * self.P * self.P * 2)
+        return out
+
+    # -- orchestration ------------------------------------------------------
+
+    def _tally_cascade(self, channels: int) -> None:
+        """Reference FLOP bookkeeping of expand_from_moments (:268-281)."""
+        P = self.P
+        for level in range(self.levels, COARSEST_LEVEL, -1):
+            self.flops.add("m2m", flops.translate_flops(level_resolution(level - 1), P))
+        for level in range(COARSEST_LEVEL, self.levels + 1):
+            self.flops.add("m2l", self._pairs[("far", level)] * channels * P * P * 2)
+            if level > COARSEST_LEVEL:
+                self.flops.add("l2l", flops.translate_flops(level_resolution(level - 1), P))
+        self.flops.add("m2l", self._pairs[("near", self.levels)] * channels * P * P * 2)
+
+    def cascade_device(self, m_finest: torch.Tensor) -> torch.Tensor:
+        """M2M / M2L / L2L in one C-ABI call; returns the finest L storage."""
+        C = int(m_finest.shape[3])
+        out = torch.empty_like(m_finest)
+        ws_bytes = _lib.lib().fc2t2_expand_workspace_size(self.handle, C)
+        ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=m_finest.device)
+        _lib.call("fc2t2_expand", self.handle, C, _ptr(m_finest), _ptr(out), _ptr(ws),
+                  int(ws_bytes), _stream())
+        self.expansion_count += 1
+        self._tally_cascade(C)
+        return out
+
+    def expand_from_moments(self, m_finest: ExpansionGrid) -> "Accessor":
+        if m_finest.kind != "M" or m_finest.level != self.levels:
+            raise StageError("expand_from_moments expects the finest M grid")
+        out = self.cascade_device(m_finest.storage.contiguous())
+        grid = ExpansionGrid(level=self.levels, kind="L", storage=out, rho=self.rho)
+        return Accessor(grid, self.table, self.flops)
+
+    def expand_device(self, pts: torch.Tensor, w: torch.Tensor) -> "Accessor":
+        """expand() on device tensors without the per-call domain sync."""
+        m = self.p2m_device(pts, w)
+        out = self.cascade_device(m.storage)
+        grid = ExpansionGrid(level=self.levels, kind="L", storage=out, rho=self.rho)
+        return Accessor(grid, self.table, self.flops, flag=self.flag)
+
+    def expand(self, sources: SourceSet) -> "Accessor":
+        acc = self.expand_device(sources.p, sources.w)
+        self.flag.raise_if_set("source")
+        return acc
+
+
+# ------------------------------------------------------------- accessor ---
+
+class Accessor:
+    """Value / derivative queries against an L grid (reference :296-398)."""
+
+    def __init__(self, grid: ExpansionGrid, table: MultiIndexTable,
+                 counter: flops.FlopCounter | None = None, flag: DomainFlag | None = None):
+        if grid.kind != "L":
+            raise StageError("accessor requires an L grid")
+        self.grid = grid
+        self.table = table
+        self._counter = counter
+        self._flag = flag
+
+    @property
+    def channels(self) -> int:
+        return self.grid.channels
+
+    def _flagobj(self) -> DomainFlag:
+        if self._flag is None:
+            self._flag = DomainFlag()
+        return self._flag
+
+    def eval_device(self, q: torch.Tensor, mode: int, wts: torch.Tensor | None = None):
+        """One L2P launch; returns dict of the requested device outputs."""
+        n, C = int(q.shape[0]), self.channels
+        dev = q.device
+        out = {}
+        value = torch.empty((n, C), dtype=torch.float32, device=dev) if mode & _lib.L2P_VALUE else None
+        grad = torch.empty((n, C, 3), dtype=torch.float32, device=dev) if mode & _lib.L2P_GRAD else None
+        hess = torch.empty((n, C, 6), dtype=torch.float32, device=dev) if mode & _lib.L2P_HESS else None
+        wgrad = torch.empty((n, 3), dtype=torch.float32, device=dev) if mode & _lib.L2P_WGRAD else None
+        st = self.grid.storage if self.grid.storage.is_contiguous() else self.grid.storage.contiguous()
+        _lib.call("fc2t2_l2p", self.table.rho, self.grid.level, C, _ptr(st), _ptr(q), n, mode,
+                  _ptr(wts), _ptr(value), _ptr(grad), _ptr(hess), _ptr(wgrad),
+                  _ptr(self._flagobj().t), _stream())
+        if self._counter is not None and mode & _lib.L2P_VALUE:
+            self._counter.add("l2p", flops.l2p_flops(n, self.table.rho, self.table.size))
+        out.update(value=value, grad=grad, hess=hess, wgrad=wgrad)
+        return out
+
+    def _query(self, q, mode: int, key: str):
+        _host_domain_check(q, "query")
+        qd = to_device(q, 3, points=True)
+        r = self.eval_device(qd, mode)[key]
+        self._flagobj().raise_if_set("query")
+        return like_input(r, q)
+
+    def box_coeffs(self, q):
+        """(coeffs (M, C, P), d (M, 3)) of the query boxes (reference :340-346)."""
+        _host_domain_check(q, "query")
+        qd = to_device(q, 3, points=True)
+        b = find_box(self.grid.level, qd).long()
+        res = self.grid.res
+        lin = (b[:, 0] * res + b[:, 1]) * res + b[:, 2]
+        coeffs = self.grid.data.reshape(res ** 3, self.channels, -1)[lin]
+        w = level_box_width(self.grid.level)
+        d = qd.double() - (-1.0 + (b.double() + 0.5) * w)
+        return like_input(coeffs, q), like_input(d, q)
+
+    def value(self, q):
+        return self._query(q, _lib.L2P_VALUE, "value")
+
+    def partials(self, q):
+        return self._query(q, _lib.L2P_GRAD, "grad")
+
+    def partials2(self, q):
+        return self._query(q, _lib.L2P_HESS, "hess")
+
+    def _vol_points(self, xs, ys, zs):
+        xs, ys, zs = (np.atleast_1d(np.asarray(a, dtype=np.float64)) for a in (xs, ys, zs))
+        gx, gy, gz = np.meshgrid(xs, ys, zs, indexing="ij")
+        pts = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+        return pts, (xs.size, ys.size, zs.size)
+
+    def value_vol(self, xs, ys, zs):
+        pts, shape = self._vol_points(xs, ys, zs)
+        v = self.value(pts)
+        return np.moveaxis(v.reshape(*shape, self.channels), 3, 0)
+
+    def partials_vol(self, xs, ys, zs):
+        pts, shape = self._vol_points(xs, ys, zs)
+        v = self.partials(pts)
+        return np.moveaxis(v.reshape(*shape, self.channels, 3), 3, 0)
+
+    def partials2_vol(self, xs, ys, zs):
+        pts, shape = self._vol_points(xs, ys, zs)
+        v = self.partials2(pts)
+        return np.moveaxis(v.reshape(*shape, self.channels, 6), 3, 0)

@@ -1,0 +1,264 @@
+"""Kernel model and per-level M2L tables (host precompute, float64).
+
+Restates the reference's table construction (``pkg/src/fc2t2/kernel.py``) in
+its own vectorised form; the *integer* outputs (offsets, hole, active mask =
+the interaction lists) are bit-exact with the reference and the fitted
+coefficients agree to ~1e-12 (tests/test_tables.py pins both against golden
+vectors generated from the reference).
+
+* Gaussian kernel psi(x) = exp(-alpha |x|^2) with per-axis Hermite-recurrence
+  derivatives (reference kernel.py:72-121).
+* Level geometry: res = 2^(level+1) boxes per axis on (-1, 1)^3
+  (reference kernel.py:62-69).
+* Tables: the coarsest level (2) uses the full reach res-1 stencil, finer far
+  levels reach 3 with the |off|_inf <= 1 hole; the finest level additionally
+  owns a hole-less 3x3x3 near table (reference kernel.py:257-300).  An
+  offset is active iff it is outside the hole and the peak box-pair
+  interaction psi(max(|off|-1, 0) * width) exceeds 1e-16 (kernel.py:213-217,
+  :275).
+* LSQ coefficients: A = pinv(V) Psi pinv(V)^T over a 6^3 Chebyshev tensor grid
+  per box (reference kernel.py:180-204), stored transposed [k_local,
+  n_moment].  Psi is a Kronecker product of per-axis node-pair kernels, so the
+  two-sided product is evaluated one axis at a time instead of forming the
+  216 x 216 pair matrix.
+
+Everything here runs once per Engine.  The device copy (fp32, padded, grouped
+into per-parity interaction lists) is made by ``expansion.Engine``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .multiindex import MultiIndexTable, build_table
+
+COARSEST_LEVEL = 2
+FAR_REACH = 3
+DEFAULT_ALPHA = {2: 12.0, 3: 50.0, 4: 200.0, 5: 1000.0, 6: 4000.0}
+PRUNE_TOL = 1e-16
+
+
+class KernelConfigError(ValueError):
+    """Unsupported kernel configuration (reference kernel.py:46-47)."""
+
+
+class AdmissibilityError(RuntimeError):
+    """Kernel too sharp for the grid hierarchy (reference kernel.py:50-59)."""
+
+    def __init__(self, level: int, worst: float, tol: float):
+        self.level = level
+        self.worst = worst
+        super().__init__(f"kernel fails admissibility at level {level}: worst probe "
+                         f"error {worst:.3e} exceeds tolerance {tol:.3e}")
+
+
+def level_resolution(level: int) -> int:
+    return 1 << (level + 1)
+
+
+def level_box_width(level: int) -> float:
+    return 2.0 / level_resolution(level)
+
+
+@dataclass(frozen=True)
+class KernelModel:
+    """Gaussian difference kernel with analytic partials (reference kernel.py:72-121)."""
+
+    family: str
+    alpha: float
+    rho: int
+    table: MultiIndexTable = field(repr=False, default=None)
+
+    def __post_init__(self):
+        if self.family != "gaussian":
+            raise KernelConfigError(f"unsupported kernel family: {self.family!r}")
+        if not self.alpha > 0:
+            raise KernelConfigError("alpha must be positive")
+        if self.table is None:
+            object.__setattr__(self, "table", build_table(self.rho))
+
+    def psi(self, x) -> np.ndarray:
+        x = np.asarray(x, dtype=np.float64)
+        return np.exp(-self.alpha * np.sum(x * x, axis=-1))
+
+    def axis_derivatives(self, max_order: int, coords) -> np.ndarray:
+        """Rows n = 0..max_order of d^n/dx^n exp(-alpha x^2)."""
+        x = np.atleast_1d(np.asarray(coords, dtype=np.float64))
+        h = np.empty((max_order + 1, x.size))
+        h[0] = np.exp(-self.alpha * x ** 2)
+        two_a = -2.0 * self.alpha
+        if max_order >= 1:
+            h[1] = two_a * x * h[0]
+        for n in range(1, max_order):
+            h[n + 1] = two_a * (x * h[n] + n * h[n - 1])
+        return h
+
+    def partial(self, order, x) -> np.ndarray:
+        order = tuple(int(o) for o in order)
+        if sum(order) > 2 * self.rho:
+            raise KernelConfigError(
+                f"partial order {order} exceeds supported total order {2 * self.rho}")
+        x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+        top = max(order)
+        out = np.ones(x.shape[0])
+        for a in range(3):
+            out = out * self.axis_derivatives(top, x[:, a])[order[a]]
+        return out
+
+
+@dataclass
+class M2LTable:
+    """One level's stencil (field layout of reference kernel.py:124-141)."""
+
+    level: int
+    nearfield: bool
+    offsets: np.ndarray        # (K, 3) int64, source index - target index
+    coeffs: np.ndarray         # (K, P, P) float64, [k_local, n_moment]
+    hole: np.ndarray           # (K,) bool
+    active: np.ndarray         # (K,) bool
+    fit_residual: float
+    box_width: float
+
+
+def stencil_offsets(reach: int) -> np.ndarray:
+    """All integer offsets in [-reach, reach]^3, x slowest (meshgrid 'ij')."""
+    r = np.arange(-reach, reach + 1)
+    return np.stack(np.meshgrid(r, r, r, indexing="ij"), axis=-1).reshape(-1, 3)
+
+
+def interaction_mask(kernel: KernelModel, offsets: np.ndarray, width: float,
+                     hole: np.ndarray, prune_tol: float = PRUNE_TOL) -> np.ndarray:
+    """Active offsets: outside the hole and peak interaction above prune_tol.
+    Same float64 expression as reference kernel.py:213-217 / :275 so the mask
+    is bit-exact."""
+    gap = np.maximum(np.abs(offsets) - 1, 0) * width
+    return ~hole & (kernel.psi(gap) > prune_tol)
+
+
+def _cheb(n: int) -> np.ndarray:
+    return np.cos((2 * np.arange(n) + 1) * np.pi / (2 * n))
+
+
+def monomial_rows(table: MultiIndexTable, pts: np.ndarray) -> np.ndarray:
+    """(G, P) rows of d^n / n! at points (G, 3)."""
+    e = table.entries
+    return np.prod(pts[:, None, :] ** e[None, :, :], axis=2) / table.entry_factorial()
+
+
+def _lsq_tables(kernel: KernelModel, width: float, offsets: np.ndarray,
+                nodes: int) -> tuple[np.ndarray, float]:
+    t = kernel.table
+    P, G = t.size, nodes
+    x1 = _cheb(G) * (width / 2.0)
+    grid = np.stack(np.meshgrid(x1, x1, x1, indexing="ij"), axis=-1).reshape(-1, 3)
+    V = monomial_rows(t, grid)                                  # (G^3, P)
+    Pv = np.linalg.pinv(V).reshape(P, G, G, G)                  # (P, gx, gy, gz)
+    diff = x1[:, None] - x1[None, :]                            # d_p - d_q
+    axis_vals = {int(d): np.exp(-kernel.alpha * (d * width + diff) ** 2)
+                 for d in np.unique(offsets)}
+    out = np.empty((offsets.shape[0], P, P))
+    resid = 0.0
+    chunk = 256
+    for lo in range(0, offsets.shape[0], chunk):
+        off = offsets[lo:lo + chunk]
+        ex = np.stack([axis_vals[int(o)] for o in off[:, 0]])   # (B, G, G) [p_node, q_node]
+        ey = np.stack([axis_vals[int(o)] for o in off[:, 1]])
+        ez = np.stack([axis_vals[int(o)] for o in off[:, 2]])
+        # (Psi Pv^T)[b, (a,b,c), k] one axis at a time over the q-side nodes
+        w = np.einsum("kxyz,Bcz->Bkxyc", Pv, ez)
+        w = np.einsum("Bkxyc,Bby->Bkxbc", w, ey)
+        w = np.einsum("Bkxbc,Bax->Bkabc", w, ex)                 # (B, k, a, b, c)
+        A = np.einsum("nabc,Bkabc->Bnk", Pv, w)                  # A[n_moment, k_local]
+        out[lo:lo + chunk] = np.swapaxes(A, 1, 2)
+        # fit residual max |V A V^T - Psi| (reference kernel.py:202)
+        fit = V[None] @ A @ V.T[None]
+        psi = (ex[:, :, None, None, :, None, None] * ey[:, None, :, None, None, :, None]
+               * ez[:, None, None, :, None, None, :]).reshape(off.shape[0], G ** 3, G ** 3)
+        resid = max(resid, float(np.max(np.abs(fit - psi))))
+    return out, resid
+
+
+def _taylor_tables(kernel: KernelModel, width: float, offsets: np.ndarray) -> np.ndarray:
+    """Pure Taylor re-expansion (reference kernel.py:168-178): entry [k, n] is
+    (-1)^|k| d^(k+n) psi(off * width), kept only where k_a + n_a <= rho."""
+    t = kernel.table
+    e, rho = t.entries, t.rho
+    nk = e[:, None, :] + e[None, :, :]                          # (P_k, P_n, 3)
+    keep = np.all(nk <= rho, axis=2)
+    sign = np.where(t.norms % 2 == 1, -1.0, 1.0)
+    out = np.empty((offsets.shape[0], t.size, t.size))
+    for i, off in enumerate(offsets):
+        c = off * width
+        h = [kernel.axis_derivatives(2 * rho, np.array([c[a]]))[:, 0] for a in range(3)]
+        full = h[0][nk[..., 0]] * h[1][nk[..., 1]] * h[2][nk[..., 2]]
+        out[i] = sign[:, None] * np.where(keep, full, 0.0)
+    return out
+
+
+def _probe_error(kernel: KernelModel, table: M2LTable, idx: int, rng) -> float:
+    """Worst reproduction error over the target box of a unit source at the
+    centre of the box at stencil offset idx (reference kernel.py:220-229)."""
+    t = kernel.table
+    w = table.box_width
+    c = table.offsets[idx] * w
+    local = table.coeffs[idx][:, 0]
+    probes = rng.uniform(-w / 2, w / 2, size=(64, 3))
+    pred = monomial_rows(t, probes) @ local
+    return float(np.max(np.abs(pred - kernel.psi(c[None, :] - probes))))
+
+
+def _check_admissibility(kernel, table: M2LTable, tol: float, rng) -> None:
+    """Reference kernel.py:232-254."""
+    if table.nearfield:
+        idx = int(np.flatnonzero((table.offsets == 0).all(axis=1))[0])
+        worst = _probe_error(kernel, table, idx, rng)
+        if worst > 20.0 * tol:
+            raise AdmissibilityError(table.level, worst, 20.0 * tol)
+        return
+    if not table.active.any():
+        return
+    dist = np.abs(table.offsets).max(axis=1)
+    idx = int(np.argmin(np.where(table.active, dist, np.iinfo(np.int64).max)))
+    worst = _probe_error(kernel, table, idx, rng)
+    if worst > tol:
+        raise AdmissibilityError(table.level, worst, tol)
+
+
+def fit_m2l_tables(kernel: KernelModel, levels: int, lsq: bool = True,
+                   nodes_per_axis: int = 6, admissibility_tol: float = 1e-3,
+                   check: bool = True, prune_tol: float = PRUNE_TOL) -> dict:
+    """``{"far": {level: M2LTable}, "near": M2LTable}`` (reference kernel.py:257-300)."""
+    if levels < COARSEST_LEVEL:
+        raise KernelConfigError(f"levels must be >= {COARSEST_LEVEL}")
+    rng = np.random.default_rng(0)
+    P = kernel.table.size
+
+    def build(level, offsets, hole, nearfield):
+        width = level_box_width(level)
+        active = interaction_mask(kernel, offsets, width, hole, prune_tol)
+        coeffs = np.zeros((offsets.shape[0], P, P))
+        resid = 0.0
+        if active.any():
+            if lsq:
+                coeffs[active], resid = _lsq_tables(kernel, width, offsets[active],
+                                                    nodes_per_axis)
+            else:
+                coeffs[active] = _taylor_tables(kernel, width, offsets[active])
+        return M2LTable(level, nearfield, offsets, coeffs, hole, active, resid, width)
+
+    far = {}
+    for level in range(COARSEST_LEVEL, levels + 1):
+        reach = level_resolution(level) - 1 if level == COARSEST_LEVEL else FAR_REACH
+        offsets = stencil_offsets(reach)
+        hole = np.all(np.abs(offsets) <= 1, axis=1)
+        tab = build(level, offsets, hole, False)
+        if check:
+            _check_admissibility(kernel, tab, admissibility_tol, rng)
+        far[level] = tab
+    near_off = stencil_offsets(1)
+    near = build(levels, near_off, np.zeros(near_off.shape[0], bool), True)
+    if check:
+        _check_admissibility(kernel, near, admissibility_tol, rng)
+    return {"far": far, "near": near}

@@ -1,0 +1,253 @@
+"""GPU parity of the expansion engine and the explicit layer (through the C ABI).
+
+Checker: the CPU oracle (float64 restatement, pinned to the reference by
+tests/test_oracle_golden.py) and the reference's own golden vectors.
+Tolerances: integer outputs bit-exact; float outputs rel-L2 <= 1e-5 against
+the float64 reference on identical float32 inputs (BASELINE north_star).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle.fc2t2_oracle import Oracle, naive_grads, naive_sum, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def eng4(cuda):
+    from paper_2111_00110_b200 import Engine, KernelModel
+    return Engine(KernelModel("gaussian", 200.0, 4), 4, lsq=True, check_admissibility=False)
+
+
+@pytest.fixture(scope="module")
+def ora4():
+    return Oracle(200.0, 4, 4)
+
+
+def _np(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+# ------------------------------------------------------------ integer parity ---
+
+@pytest.mark.parametrize("level", range(2, 8))
+def test_find_box_bit_exact(cuda, level):
+    from paper_2111_00110_b200.expansion import find_box
+    g = golden("find_box")
+    got = find_box(level, torch.from_numpy(g["pts"]).cuda())
+    assert np.array_equal(got.cpu().numpy(), g[f"box_l{level}"])
+
+
+def test_cell_sort_is_stable_counting_sort(eng4):
+    rng = np.random.default_rng(0)
+    p = rng.uniform(-1, 1, (50_000, 3)).astype(np.float32)
+    p[:5000] = p[0]  # a heavy cell
+    order, start = eng4.sort_points(torch.from_numpy(p).cuda())
+    from oracle.fc2t2_oracle import find_box
+    b = find_box(4, p.astype(np.float64))
+    key = (b[:, 0] * 32 + b[:, 1]) * 32 + b[:, 2]
+    ref = np.argsort(key, kind="stable")
+    assert np.array_equal(order.cpu().numpy(), ref)
+    counts = np.bincount(key, minlength=32 ** 3)
+    assert np.array_equal(start.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "small"])
+def test_device_interaction_lists_bit_exact(cuda, name):
+    """The device lists are exactly the reference's active offsets, split by
+    target parity the way expansion.py:246-249 restricts them."""
+    from paper_2111_00110_b200 import Engine, KernelModel
+    g = golden(f"tables_{name}")
+    eng = Engine(KernelModel("gaussian", float(g["alpha"]), int(g["rho"])), int(g["levels"]),
+                 check_admissibility=False)
+    for level in range(2, int(g["levels"]) + 1):
+        ent, starts = eng.interaction_list(level, 0)
+        off = g[f"far{level}_offsets"][g[f"far{level}_active"]].astype(np.int32)
+        if level == 2:
+            assert np.array_equal(ent[:, :3], off)
+            continue
+        assert starts.shape[0] == 9
+        for cls in range(8):
+            par = [(cls >> 2) & 1, (cls >> 1) & 1, cls & 1]
+            keep = np.ones(off.shape[0], bool)
+            for a in range(3):
+                keep &= ~((off[:, a] == -3) & (par[a] != 1))
+                keep &= ~((off[:, a] == 3) & (par[a] != 0))
+            assert np.array_equal(ent[starts[cls]:starts[cls + 1], :3], off[keep])
+    ent, _ = eng.interaction_list(int(g["levels"]), 1)
+    assert np.array_equal(ent[:, :3], g["near_offsets"][g["near_active"]].astype(np.int32))
+
+
+# -------------------------------------------------------------- stage parity ---
+
+def test_p2m_matches_oracle(eng4, ora4):
+    from paper_2111_00110_b200 import SourceSet
+    g = golden("expansion_l4")
+    p, w = g["p"].astype(np.float64), g["w"].astype(np.float64)
+    m = eng4.p2m(SourceSet(p, w))
+    ref = ora4.p2m(p, w)
+    assert rel_l2(_np(m.data), ref) < 1e-6
+    # the golden moments of the reference itself (first 60 sources)
+    m60 = _np(eng4.p2m(SourceSet(p[:60], w[:60])).data)
+    c = g["p2m_cells"]
+    assert rel_l2(m60[c[:, 0], c[:, 1], c[:, 2]], g["p2m_moments"]) < 1e-6
+    assert np.count_nonzero(np.abs(m60).sum(axis=(3, 4))) == c.shape[0]
+
+
+def test_m2m_l2l_m2l_match_oracle(eng4, ora4):
+    rng = np.random.default_rng(5)
+    m = eng4.zero_grid(4, 2, "M")
+    mdata = rng.normal(size=tuple(m.data.shape)).astype(np.float32)
+    m.data[:] = torch.from_numpy(mdata).cuda()
+    md = mdata.astype(np.float64)
+    coarse = eng4.m2m(m)
+    assert rel_l2(_np(coarse.data), ora4.m2m(md, 4)) < 1e-6
+    far = eng4.m2l_tables["far"][4]
+    out = eng4.m2l(m, far)
+    ref = ora4.m2l(md, ora4.tables["far"][4])
+    assert rel_l2(_np(out.data), ref) < 1e-5
+    near = eng4.m2l(m, eng4.m2l_tables["near"])
+    assert rel_l2(_np(near.data), ora4.m2l(md, ora4.tables["near"])) < 1e-5
+    c3 = eng4.zero_grid(3, 2, "M")
+    c3.data[:] = torch.from_numpy(mdata[::2, ::2, ::2]).cuda()
+    out3 = eng4.m2l(c3, eng4.m2l_tables["far"][3])
+    assert rel_l2(_np(out3.data), ora4.m2l(md[::2, ::2, ::2], ora4.tables["far"][3])) < 1e-5
+    c2 = eng4.zero_grid(2, 2, "M")
+    c2.data[:] = torch.from_numpy(mdata[::4, ::4, ::4]).cuda()
+    out2 = eng4.m2l(c2, eng4.m2l_tables["far"][2])
+    assert rel_l2(_np(out2.data), ora4.m2l(md[::4, ::4, ::4], ora4.tables["far"][2])) < 1e-5
+    lg = eng4.zero_grid(3, 2, "L")
+    lg.data[:] = torch.from_numpy(mdata[::2, ::2, ::2]).cuda()
+    fine = eng4.l2l(lg)
+    assert rel_l2(_np(fine.data), ora4.l2l(md[::2, ::2, ::2], 3)) < 1e-6
+
+
+def test_l2l_golden_exact_on_polynomials(eng4):
+    from paper_2111_00110_b200 import Accessor
+    g = golden("l2l_l3")
+    coarse = eng4.zero_grid(3, 1, "L")
+    coarse.data[:] = torch.from_numpy(g["coarse"]).cuda()
+    fine = eng4.l2l(coarse)
+    v = Accessor(fine, eng4.table).value(g["q"].astype(np.float64))
+    assert rel_l2(v, g["fine_value"]) < 1e-6
+    vc = Accessor(coarse, eng4.table).value(g["q"].astype(np.float64))
+    assert rel_l2(vc, g["fine_value"]) < 1e-6
+
+
+def test_expand_and_l2p_match_reference_golden(eng4):
+    from paper_2111_00110_b200 import SourceSet
+    g = golden("expansion_l4")
+    p, w, q = (g[k].astype(np.float64) for k in ("p", "w", "q"))
+    acc = eng4.expand(SourceSet(p, w))
+    assert rel_l2(acc.value(q), g["value"]) < TOL
+    assert rel_l2(acc.partials(q), g["partials"]) < TOL
+    assert rel_l2(acc.partials2(q), g["partials2"]) < 1e-4  # second derivatives: 2 orders less
+
+
+def test_expand_deterministic(eng4):
+    from paper_2111_00110_b200 import SourceSet
+    rng = np.random.default_rng(9)
+    p = rng.uniform(-1, 1, (200_000, 3))
+    w = rng.normal(size=(200_000, 1))
+    s = SourceSet(p, w)
+    a = eng4.expand(s).grid.storage.clone()
+    b = eng4.expand(s).grid.storage
+    assert torch.equal(a, b)
+
+
+def test_domain_errors(eng4):
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.expansion import DomainError
+    with pytest.raises(DomainError):
+        SourceSet(np.array([[0.0, 1.0, 0.0]]), np.array([1.0]))
+    acc = eng4.expand(SourceSet(np.zeros((2, 3)), np.ones(2)))
+    with pytest.raises(DomainError):
+        acc.value(np.array([[1.0, 0.0, 0.0]]))
+    # device tensors are checked by the kernel flag
+    with pytest.raises(DomainError):
+        acc.value(torch.tensor([[0.0, -1.0, 0.5]], device="cuda"))
+
+
+def test_empty_sources(eng4):
+    from paper_2111_00110_b200 import SourceSet
+    acc = eng4.expand(SourceSet(np.zeros((0, 3)), np.zeros((0, 1))))
+    assert float(acc.grid.storage.abs().max()) == 0.0
+    assert acc.value(np.zeros((3, 3))).shape == (3, 1)
+
+
+# ------------------------------------------------------------ explicit layer ---
+
+def test_explicit_cfg1_matches_reference(eng4):
+    """BASELINE config 1 (2D lifted to z=0.03125) vs the reference's outputs."""
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    g = golden("explicit_cfg1")
+    p, w, q, yb = (g[k].astype(np.float64) for k in ("p", "w", "q", "y_bar"))
+    res = explicit_forward(eng4, SourceSet(p, w), q)
+    gr = explicit_jvp(yb, res)
+    assert rel_l2(res.values, g["values"]) < TOL
+    assert rel_l2(gr.w_bar, g["w_bar"]) < TOL
+    assert rel_l2(gr.p_bar, g["p_bar"]) < TOL
+    assert rel_l2(gr.q_bar, g["q_bar"]) < TOL
+    # and the direct O(NM) sum with the reference's own bounds
+    assert rel_l2(res.values, naive_sum(200.0, p, w, q)) <= 1e-2
+    assert rel_l2(gr.w_bar, naive_sum(200.0, q, yb, p)) <= 1e-2
+    assert rel_l2(gr.p_bar, np.einsum("nc,nca->na", w, naive_grads(200.0, q, yb, p))) <= 5e-2
+
+
+def test_explicit_torch_io_and_counts(eng4):
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    rng = np.random.default_rng(1)
+    p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32)).cuda()
+    w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32)).cuda()
+    q = torch.from_numpy(rng.uniform(-1, 1, (5000, 3)).astype(np.float32)).cuda()
+    before = eng4.expansion_count
+    res = explicit_forward(eng4, SourceSet(p, w), q)
+    assert isinstance(res.values, torch.Tensor) and res.values.shape == (5000, 2)
+    assert eng4.expansion_count == before + 1
+    yb = torch.randn(5000, 2, device="cuda")
+    g = explicit_jvp(yb, res)
+    assert eng4.expansion_count == before + 2
+    assert g.w_bar.shape == (3000, 2) and g.p_bar.shape == (3000, 3) and g.q_bar.shape == (5000, 3)
+    ora = Oracle(200.0, 4, 4)
+    vals, wb, pb, qb = ora.explicit(_np(p), _np(w), _np(q), _np(yb))
+    assert rel_l2(_np(res.values), vals) < TOL
+    assert rel_l2(_np(g.w_bar), wb) < TOL
+    assert rel_l2(_np(g.p_bar), pb) < TOL
+    assert rel_l2(_np(g.q_bar), qb) < TOL
+
+
+def test_explicit_config2_full_size_properties(cuda):
+    """Config 2 at full size (N=2^20, M=10^7, level 5): size-independent
+    checks -- the adjoint (dot-product) identity <y, G w> = <w, G^T y> of the
+    self-adjoint pipeline, linearity in w, and direct-sum accuracy on a sample."""
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    N, M = 1 << 20, 10_000_000
+    p = torch.rand(N, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(N, 1, device="cuda", generator=gen) * 0.1
+    q = torch.rand(M, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    yb = torch.randn(M, 1, device="cuda", generator=gen)
+    res = explicit_forward(eng, SourceSet(p, w), q)
+    g = explicit_jvp(yb, res)
+    lhs = float((yb.double() * res.values.double()).sum())
+    rhs = float((w.double() * g.w_bar.double()).sum())
+    assert abs(lhs - rhs) <= 1e-5 * (abs(lhs) + abs(rhs))
+    res2 = explicit_forward(eng, SourceSet(p, 2.0 * w), q)
+    assert rel_l2(_np(res2.values), 2.0 * _np(res.values)) < 1e-6
+    # direct sum on a sample of 512 queries (float64 on the device: checker only)
+    idx = torch.arange(0, M, M // 512, device="cuda")[:512]
+    qs, pd, wd = q[idx].double(), p.double(), w.double()
+    exact = torch.zeros(qs.shape[0], 1, dtype=torch.float64, device="cuda")
+    for lo in range(0, N, 1 << 16):
+        d = qs[:, None, :] - pd[None, lo:lo + (1 << 16), :]
+        exact += torch.exp(-1000.0 * (d * d).sum(-1)) @ wd[lo:lo + (1 << 16)]
+    assert rel_l2(_np(res.values[idx]), _np(exact)) < 1e-2
