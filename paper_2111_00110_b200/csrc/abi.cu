@@ -416,10 +416,25 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
       "m2l");
 }
 
+namespace {
+// split-K partial buffer (floats) the cascade needs for its small levels
+size_t split_floats(const fc2t2_engine* e, int channels) {
+  size_t best = 0;
+  for (auto& lv : e->plans)
+    for (auto& t : lv.second) {
+      if (t.second.max_list == 0) continue;
+      const int sp = fc2t2::m2l_splits(e->rho, channels, launch_of(t.second, lv.first));
+      if (sp > 1) best = std::max(best, (size_t)sp * grid_floats(lv.first, channels, e->PP));
+    }
+  return best;
+}
+}  // namespace
+
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
-  if (!e) return 0;
+  if (!e || !e->uploaded) return 0;
   size_t f = 0;
   for (int l = kCoarsest; l < e->levels; ++l) f += 2 * grid_floats(l, channels, e->PP);
+  f += split_floats(e, channels);
   return f * sizeof(float) + 256;
 }
 
@@ -441,6 +456,7 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
   }
   Mg[L] = const_cast<float*>(d_m_finest);
   Lg[L] = d_l_finest;
+  float* part = w;  // split-K partials (split_floats)
   // lowest level whose far table does any work (coarser M grids are unused)
   int lowest = L;
   for (int l = kCoarsest; l <= L; ++l) {
@@ -464,8 +480,9 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
       if (st != FC2T2_OK) return st;
     }
     if (p.max_list > 0) {
-      st = cuda_status(fc2t2::m2l(e->rho, channels, launch_of(p, l), e->d_coef, Mg[l], Lg[l],
-                                  have ? 1 : 0, s),
+      const fc2t2::M2LLaunch ml = launch_of(p, l);
+      st = cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, Mg[l], Lg[l], have ? 1 : 0, s,
+                                  part, fc2t2::m2l_splits(e->rho, channels, ml)),
                        "expand m2l");
       if (st != FC2T2_OK) return st;
       have = true;

@@ -204,7 +204,8 @@ template <int RHO, int RPL>
 __global__ void __launch_bounds__(M2L_THREADS, (RHO <= 4 ? 2 : 1))
 m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int res, int stride,
                 int nu, const int4* __restrict__ entries, const int* __restrict__ cls_start,
-                const float* __restrict__ coef, int accumulate) {
+                const float* __restrict__ coef, int accumulate, float* __restrict__ part,
+                int64_t part_stride) {
   constexpr int PP = MI<RHO>::PP;
   constexpr int NQ = PP / 4;
   constexpr int ROWS = M2L_THREADS * RPL;
@@ -234,7 +235,17 @@ m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int r
   }
   __syncthreads();
 
-  const int lb = cls_start[cls], nl = cls_start[cls + 1] - lb;
+  // split-K over the interaction list (blockIdx.z); each split writes its own
+  // partial grid, summed in split order by m2l_reduce_kernel (deterministic)
+  int lb = cls_start[cls], nl = cls_start[cls + 1] - lb;
+  if (gridDim.z > 1) {
+    const int chunk = (nl + gridDim.z - 1) / gridDim.z;
+    const int b = min(nl, (int)blockIdx.z * chunk);
+    nl = min(nl, b + chunk) - b;
+    lb += b;
+    L = part + blockIdx.z * part_stride;
+    accumulate = 0;
+  }
 
   auto stage = [&](int li, int buf) {
     const int4 e = __ldg(entries + lb + li);
@@ -309,6 +320,19 @@ m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int r
   }
 }
 
+__global__ void m2l_reduce_kernel(float4* __restrict__ L, const float4* __restrict__ part,
+                                  int64_t n4, int64_t stride4, int splits, int accumulate) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 s = accumulate ? L[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int z = 0; z < splits; ++z) {
+      const float4 v = part[z * stride4 + i];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    L[i] = s;
+  }
+}
+
 template <int RHO>
 constexpr int m2l_rpl() { return MI<RHO>::PP <= 36 ? 2 : 1; }
 
@@ -354,10 +378,22 @@ cudaError_t l2l(int rho, int coarse_level, int C, const float* coarse, float* fi
   return cudaGetLastError();
 }
 
-cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
-                float* L, int accumulate, cudaStream_t s) {
+int m2l_splits(int rho, int C, const M2LLaunch& plan) {
   const int res = 1 << (plan.level + 1);
   const int nu = res / plan.stride;
+  const int rows = 128 * (index_count(rho) <= 35 ? 2 : 1);
+  const int tpt = std::max(1, rows / C);
+  const int64_t ctas = ((int64_t)nu * nu * nu + tpt - 1) / tpt * plan.ncls;
+  const int64_t want = (2 * 148 + ctas - 1) / ctas;
+  return (int)std::max<int64_t>(1, std::min<int64_t>({want, 16, (int64_t)plan.max_list}));
+}
+
+cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
+                float* L, int accumulate, cudaStream_t s, float* part, int splits) {
+  const int res = 1 << (plan.level + 1);
+  const int nu = res / plan.stride;
+  if (!part) splits = 1;
+  const int64_t grid_f = (int64_t)res * res * res * C * pad4(index_count(rho));
   FC2T2_DISPATCH_RHO(rho, {
     constexpr int RPL = m2l_rpl<RHO>();
     constexpr int ROWS = M2L_THREADS * RPL;
@@ -369,11 +405,18 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((ntgt + tpt - 1) / tpt), (unsigned)plan.ncls);
+    dim3 grid((unsigned)((ntgt + tpt - 1) / tpt), (unsigned)plan.ncls, (unsigned)splits);
     FC2T2_LAUNCH(plan.level_name, s,
                  kern<<<grid, M2L_THREADS, smem, s>>>(M, L, C, res, plan.stride, nu, plan.entries,
-                                                      plan.cls_start, coef, accumulate));
+                                                      plan.cls_start, coef, accumulate, part,
+                                                      grid_f));
   });
+  if (splits > 1) {
+    const int64_t n4 = grid_f / 4;
+    FC2T2_LAUNCH("m2l_reduce", s,
+                 m2l_reduce_kernel<<<grid_blocks(n4, 256, 148 * 16), 256, 0, s>>>(
+                     (float4*)L, (const float4*)part, n4, grid_f / 4, splits, accumulate));
+  }
   return cudaGetLastError();
 }
 

@@ -36,8 +36,11 @@ struct M2LLaunch {
   int max_list;          // host copy of the longest list (0 -> nothing to do)
   const char* level_name;  // profiling label, e.g. "m2l_L5"
 };
+// splits > 1 (with a workspace ``part`` of splits * grid floats) splits each
+// class's interaction list across CTAs for small levels; m2l_splits picks it.
+int m2l_splits(int rho, int C, const M2LLaunch& plan);
 cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
-                float* L, int accumulate, cudaStream_t s);
+                float* L, int accumulate, cudaStream_t s, float* part = nullptr, int splits = 1);
 
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {

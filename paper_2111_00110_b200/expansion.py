@@ -82,9 +82,7 @@ def to_device(x, cols: int | None = None, points: bool = False) -> torch.Tensor:
             a32 = np.clip(a32, -_ONE_BELOW, _ONE_BELOW)
         t = torch.from_numpy(a32).to(_device())
     if cols is not None:
-        if t.dim() == 1:
-            t = t.reshape(-1, cols) if cols == 3 else t.reshape(-1, 1)
-        t = t.reshape(t.shape[0], -1)
+        t = t.reshape(-1, cols)
     return t.contiguous()
 
 
@@ -147,7 +145,7 @@ class SourceSet:
         if p_np is not None:
             _host_domain_check(p_np, "source")
         self.p = to_device(p_np if p_np is not None else self.p, 3, points=True)
-        self.w = to_device(w_in).reshape(self.p.shape[0], -1)
+        self.w = to_device(w_in).reshape(self.p.shape[0], int(w_in.shape[1]))
 
     @property
     def n(self) -> int:
