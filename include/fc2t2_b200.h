@@ -103,8 +103,11 @@ int fc2t2_m2m(const fc2t2_engine* e, int channels, int fine_level, const float* 
               float* d_coarse, void* stream);
 int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float* d_coarse,
               float* d_fine, int accumulate, void* stream);
+/* M2L of one table.  With a workspace of fc2t2_m2l_workspace_size bytes the
+ * parity levels run the tcgen05 3xTF32 kernel; without one, FP32 FFMA. */
+size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table);
 int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const float* d_m,
-              float* d_l, int accumulate, void* stream);
+              float* d_l, int accumulate, void* d_ws, size_t ws_bytes, void* stream);
 
 /* ---- cascade: Engine.expand_from_moments (expansion.py:268-281) ---- */
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);

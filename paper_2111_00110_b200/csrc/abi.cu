@@ -11,6 +11,7 @@
 // class list so one M2L pass applies far + near.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -48,6 +49,13 @@ struct Plan {
   int4* d_entries = nullptr;
   int* d_cls_start = nullptr;
   int max_list = 0;
+  // tcgen05 form (parity levels): {window start row, slot} grouped by
+  // (target class, source class), grp_start[8 * 8 + 1]
+  bool tc = false;
+  std::vector<int2> tc_entries;
+  std::vector<int> tc_grp;
+  int2* d_tc_entries = nullptr;
+  int* d_tc_grp = nullptr;
 };
 
 }  // namespace
@@ -100,6 +108,7 @@ struct fc2t2_engine {
   HostTable near;
   bool uploaded = false;
   float* d_coef = nullptr;
+  uint8_t* d_btab = nullptr;  // 3xTF32-split tables in the UMMA K-major layout
   // plans[level][table]
   std::map<int, std::map<int, Plan>> plans;
 };
@@ -108,9 +117,41 @@ namespace {
 
 constexpr int kCoarsest = 2;
 
+// host emulation of cvt.rna.tf32.f32 (round to nearest, ties away)
+float rn_tf32_host(double v) {
+  float f = (float)v;
+  uint32_t b;
+  std::memcpy(&b, &f, 4);
+  if ((b & 0x7f800000u) != 0x7f800000u) b = (b + 0x1000u) & 0xffffe000u;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+
+// One slot's table in the tcgen05 B layout: for every K step (8 inputs n),
+// [part hi/lo][kchunk 2][row k (NPAD)][4 floats], with A = hi + lo split in
+// float64 (hi = rn_tf32(A), lo = rn_tf32(A - hi)); zero padded.
+void append_btab(const double* A, int P, int rho, std::vector<float>& btab) {
+  const int KS = fc2t2::tc_kpad(rho) / 8, NPAD = fc2t2::tc_npad(rho);
+  const size_t stage = (size_t)fc2t2::tc_bstage(rho) / 4;
+  const size_t base = btab.size();
+  btab.resize(base + KS * stage, 0.f);
+  for (int ks = 0; ks < KS; ++ks)
+    for (int kc = 0; kc < 2; ++kc)
+      for (int k = 0; k < NPAD; ++k)
+        for (int f = 0; f < 4; ++f) {
+          const int n = 8 * ks + 4 * kc + f;
+          const double a = (k < P && n < P) ? A[(size_t)k * P + n] : 0.0;
+          const float hi = rn_tf32_host(a);
+          const float lo = rn_tf32_host(a - (double)hi);
+          float* st = btab.data() + base + ks * stage;
+          st[((0 * 2 + kc) * NPAD + k) * 4 + f] = hi;
+          st[((1 * 2 + kc) * NPAD + k) * 4 + f] = lo;
+        }
+}
+
 // slot assignment and per-class entry lists for one table
-void append_table(const HostTable& t, int P, int PP, int parity, std::vector<float>& coef,
-                  std::vector<std::vector<int4>>& cls_lists) {
+void append_table(const HostTable& t, int P, int PP, int rho, int parity, std::vector<float>& coef,
+                  std::vector<float>& btab, std::vector<std::vector<int4>>& cls_lists) {
   const int64_t K = (int64_t)t.active.size();
   for (int64_t i = 0; i < K; ++i) {
     if (!t.active[i]) continue;
@@ -122,6 +163,7 @@ void append_table(const HostTable& t, int P, int PP, int parity, std::vector<flo
     const double* A = t.coeffs.data() + (size_t)i * P * P;  // [k][n]
     for (int k = 0; k < P; ++k)
       for (int n = 0; n < P; ++n) B[(size_t)n * PP + k] = (float)A[(size_t)k * P + n];
+    append_btab(A, P, rho, btab);
     const int ncls = (int)cls_lists.size();
     for (int c = 0; c < ncls; ++c) {
       if (parity) {
@@ -149,6 +191,46 @@ void finish_plan(Plan& p, std::vector<std::vector<int4>>& lists) {
     p.cls_start.push_back((int)p.entries.size());
     p.max_list = std::max(p.max_list, (int)l.size());
   }
+  // tcgen05 regrouping by source parity class (parity stencils only): the
+  // entry order inside a (target, source) group keeps the reference order
+  p.tc = p.ncls == 8;
+  p.tc_entries.clear();
+  p.tc_grp.assign(1, 0);
+  if (!p.tc) return;
+  for (int c = 0; c < 8; ++c) {
+    const int pi[3] = {(c >> 2) & 1, (c >> 1) & 1, c & 1};
+    for (int sg = 0; sg < 8; ++sg) {
+      const int sig[3] = {(sg >> 2) & 1, (sg >> 1) & 1, sg & 1};
+      for (const int4& e : lists[c]) {
+        const int d[3] = {e.x, e.y, e.z};
+        int sh[3];
+        bool match = true;
+        for (int a = 0; a < 3; ++a) {
+          const int v = pi[a] + d[a];
+          if (((v % 2) + 2) % 2 != sig[a]) match = false;
+          sh[a] = (v - sig[a]) / 2;
+        }
+        if (!match) continue;
+        p.tc_entries.push_back(make_int2(fc2t2::tc_window_start(sh[0], sh[1], sh[2]), e.w));
+      }
+      p.tc_grp.push_back((int)p.tc_entries.size());
+    }
+  }
+}
+
+bool force_ffma() {
+  const char* v = std::getenv("FC2T2_M2L_FFMA");
+  return v && v[0] == '1';
+}
+
+// tensor-core M2L for a level: parity stencil and at least a 16^3 class lattice
+bool use_tc(const Plan& p, int level) {
+  return p.tc && p.max_list > 0 && (1 << (level + 1)) / 2 >= 16 && !force_ffma();
+}
+
+size_t tc_split_floats(int rho, int level, int C) {
+  const size_t res = (size_t)1 << (level + 1);
+  return 2 * res * res * res * (size_t)C * fc2t2::tc_kpad(rho);
 }
 
 int plan_for(const fc2t2_engine* e, int level, int table, const Plan** out) {
@@ -159,6 +241,18 @@ int plan_for(const fc2t2_engine* e, int level, int table, const Plan** out) {
   if (jt == it->second.end()) return fail(FC2T2_ESTAGE, "table kind not available at this level");
   *out = &jt->second;
   return FC2T2_OK;
+}
+
+fc2t2::TCPlan tc_of(const fc2t2_engine* e, const Plan& p, int level) {
+  fc2t2::TCPlan t;
+  t.level = level;
+  t.btab = e->d_btab;
+  t.entries = p.d_tc_entries;
+  t.grp_start = p.d_tc_grp;
+  static const char* names[] = {"m2l_tc_L0", "m2l_tc_L1", "m2l_tc_L2", "m2l_tc_L3", "m2l_tc_L4",
+                                "m2l_tc_L5", "m2l_tc_L6", "m2l_tc_L7", "m2l_tc_L8", "m2l_tc_L9"};
+  t.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];
+  return t;
 }
 
 fc2t2::M2LLaunch launch_of(const Plan& p, int level) {
@@ -241,10 +335,13 @@ int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out) {
 void fc2t2_engine_destroy(fc2t2_engine* e) {
   if (!e) return;
   cudaFree(e->d_coef);
+  cudaFree(e->d_btab);
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
       cudaFree(t.second.d_entries);
       cudaFree(t.second.d_cls_start);
+      cudaFree(t.second.d_tc_entries);
+      cudaFree(t.second.d_tc_grp);
     }
   delete e;
 }
@@ -270,20 +367,20 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
   if (!e->near.set) return fail(FC2T2_ESTAGE, "near table missing");
   for (int l = kCoarsest; l <= e->levels; ++l)
     if (!e->far.count(l) || !e->far[l].set) return fail(FC2T2_ESTAGE, "far table missing");
-  std::vector<float> coef;
+  std::vector<float> coef, btab;
   const int P = e->P, PP = e->PP;
   for (int l = kCoarsest; l <= e->levels; ++l) {
     const bool parity = l != kCoarsest;
     {
       std::vector<std::vector<int4>> lists(parity ? 8 : 1);
-      append_table(e->far[l], P, PP, parity, coef, lists);
+      append_table(e->far[l], P, PP, e->rho, parity, coef, btab, lists);
       Plan& p = e->plans[l][FC2T2_TABLE_FAR];
       p.stride = parity ? 2 : 1;
       finish_plan(p, lists);
     }
     if (l == e->levels) {
       std::vector<std::vector<int4>> nl(1);
-      append_table(e->near, P, PP, 0, coef, nl);
+      append_table(e->near, P, PP, e->rho, 0, coef, btab, nl);
       Plan& pn = e->plans[l][FC2T2_TABLE_NEAR];
       pn.stride = 1;
       finish_plan(pn, nl);
@@ -307,6 +404,11 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
     err = cudaMemcpyAsync(e->d_coef, coef.data(), coef.size() * sizeof(float),
                           cudaMemcpyHostToDevice, s);
     if (err != cudaSuccess) return cuda_status(err, "engine_upload copy");
+    err = cudaMalloc(&e->d_btab, btab.size() * sizeof(float));
+    if (err == cudaSuccess)
+      err = cudaMemcpyAsync(e->d_btab, btab.data(), btab.size() * sizeof(float),
+                            cudaMemcpyHostToDevice, s);
+    if (err != cudaSuccess) return cuda_status(err, "engine_upload btab");
   }
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
@@ -320,6 +422,16 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       if (err == cudaSuccess)
         err = cudaMemcpyAsync(p.d_cls_start, p.cls_start.data(), p.cls_start.size() * sizeof(int),
                               cudaMemcpyHostToDevice, s);
+      if (err == cudaSuccess && p.tc) {
+        err = cudaMalloc(&p.d_tc_entries, std::max<size_t>(p.tc_entries.size(), 1) * sizeof(int2));
+        if (err == cudaSuccess) err = cudaMalloc(&p.d_tc_grp, p.tc_grp.size() * sizeof(int));
+        if (err == cudaSuccess && !p.tc_entries.empty())
+          err = cudaMemcpyAsync(p.d_tc_entries, p.tc_entries.data(),
+                                p.tc_entries.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
+        if (err == cudaSuccess)
+          err = cudaMemcpyAsync(p.d_tc_grp, p.tc_grp.data(), p.tc_grp.size() * sizeof(int),
+                                cudaMemcpyHostToDevice, s);
+      }
       if (err != cudaSuccess) return cuda_status(err, "engine_upload plans");
     }
   err = cudaStreamSynchronize(s);
@@ -399,8 +511,14 @@ int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float
                      "l2l");
 }
 
+size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table) {
+  const Plan* p;
+  if (plan_for(e, level, table, &p) != FC2T2_OK) return 0;
+  return use_tc(*p, level) ? tc_split_floats(e->rho, level, channels) * sizeof(float) : 0;
+}
+
 int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const float* d_m,
-              float* d_l, int accumulate, void* stream) {
+              float* d_l, int accumulate, void* d_ws, size_t ws_bytes, void* stream) {
   const Plan* p;
   int st = plan_for(e, level, table, &p);
   if (st != FC2T2_OK) return st;
@@ -410,6 +528,15 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
     if (accumulate) return FC2T2_OK;
     return cuda_status(
         cudaMemsetAsync(d_l, 0, grid_floats(level, channels, e->PP) * sizeof(float), s), "m2l");
+  }
+  const size_t need = use_tc(*p, level) ? tc_split_floats(e->rho, level, channels) : 0;
+  if (need && d_ws && ws_bytes >= need * sizeof(float)) {
+    float* hi = (float*)d_ws;
+    float* lo = hi + need / 2;
+    st = cuda_status(fc2t2::split_tf32(e->rho, level, channels, d_m, hi, lo, s), "m2l split");
+    if (st != FC2T2_OK) return st;
+    return cuda_status(
+        fc2t2::m2l_tc(e->rho, channels, tc_of(e, *p, level), hi, lo, d_l, accumulate, s), "m2l_tc");
   }
   return cuda_status(
       fc2t2::m2l(e->rho, channels, launch_of(*p, level), e->d_coef, d_m, d_l, accumulate, s),
@@ -423,6 +550,10 @@ size_t split_floats(const fc2t2_engine* e, int channels) {
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
       if (t.second.max_list == 0) continue;
+      if (use_tc(t.second, lv.first)) {
+        best = std::max(best, tc_split_floats(e->rho, lv.first, channels));
+        continue;
+      }
       const int sp = fc2t2::m2l_splits(e->rho, channels, launch_of(t.second, lv.first));
       if (sp > 1) best = std::max(best, (size_t)sp * grid_floats(lv.first, channels, e->PP));
     }
@@ -479,7 +610,17 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
       st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, Lg[l - 1], Lg[l], 0, s), "expand l2l");
       if (st != FC2T2_OK) return st;
     }
-    if (p.max_list > 0) {
+    if (p.max_list > 0 && use_tc(p, l)) {
+      float* hi = part;
+      float* lo = part + tc_split_floats(e->rho, l, channels) / 2;
+      st = cuda_status(fc2t2::split_tf32(e->rho, l, channels, Mg[l], hi, lo, s), "expand split");
+      if (st != FC2T2_OK) return st;
+      st = cuda_status(
+          fc2t2::m2l_tc(e->rho, channels, tc_of(e, p, l), hi, lo, Lg[l], have ? 1 : 0, s),
+          "expand m2l_tc");
+      if (st != FC2T2_OK) return st;
+      have = true;
+    } else if (p.max_list > 0) {
       const fc2t2::M2LLaunch ml = launch_of(p, l);
       st = cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, Mg[l], Lg[l], have ? 1 : 0, s,
                                   part, fc2t2::m2l_splits(e->rho, channels, ml)),

@@ -42,6 +42,25 @@ int m2l_splits(int rho, int C, const M2LLaunch& plan);
 cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
                 float* L, int accumulate, cudaStream_t s, float* part = nullptr, int splits = 1);
 
+// m2l_tc.cu --------------------------------------------------------------
+// tcgen05 3xTF32 M2L for parity levels; entries are {window start row, slot}
+// grouped by (target class, source class): grp_start has 8*8+1 entries.
+struct TCPlan {
+  int level;
+  const uint8_t* btab;     // [slot][kstep][BSTAGE bytes] split tables
+  const int2* entries;
+  const int* grp_start;
+  const char* level_name;
+};
+int tc_kpad(int rho);
+int tc_npad(int rho);
+int tc_bstage(int rho);
+int tc_window_start(int sx, int sy, int sz);
+cudaError_t split_tf32(int rho, int level, int C, const float* M, float* hi, float* lo,
+                       cudaStream_t s);
+cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const float* Mlo,
+                   float* L, int accumulate, cudaStream_t s);
+
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {
   L2P_VALUE = 1,   // (n, C)

@@ -386,8 +386,11 @@ class Engine:
             raise StageError(f"grid level {m.level} != table level {table.level}")
         kind = _lib.TABLE_NEAR if table.nearfield else _lib.TABLE_FAR
         out = self._empty_grid(m.level, m.channels, "L")
+        ws_bytes = int(_lib.lib().fc2t2_m2l_workspace_size(self.handle, m.channels, m.level, kind))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=out.storage.device)
         _lib.call("fc2t2_m2l", self.handle, m.channels, m.level, kind,
-                  _ptr(m.storage.contiguous()), _ptr(out.storage), 0, _stream())
+                  _ptr(m.storage.contiguous()), _ptr(out.storage), 0, _ptr(ws), ws_bytes,
+                  _stream())
         key = ("near" if table.nearfield else "far", table.level)
         self.flops.add("m2l", self._pairs[key] * m.channels * self.P * self.P * 2)
         return out

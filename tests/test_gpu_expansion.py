@@ -251,3 +251,24 @@ def test_explicit_config2_full_size_properties(cuda):
         d = qs[:, None, :] - pd[None, lo:lo + (1 << 16), :]
         exact += torch.exp(-1000.0 * (d * d).sum(-1)) @ wd[lo:lo + (1 << 16)]
     assert rel_l2(_np(res.values[idx]), _np(exact)) < 1e-2
+
+
+def test_m2l_tensor_core_level5_matches_oracle(cuda):
+    """The finest level of configs 2-4 runs the tcgen05 3xTF32 M2L (far+near
+    merged); compare the full cascade against the float64 oracle."""
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    ora = Oracle(1000.0, 4, 5)
+    rng = np.random.default_rng(21)
+    p = rng.uniform(-1, 1, (20000, 3)).astype(np.float32).astype(np.float64)
+    w = rng.normal(size=(20000, 1)).astype(np.float32).astype(np.float64)
+    q = rng.uniform(-1, 1, (5000, 3)).astype(np.float32).astype(np.float64)
+    acc = eng.expand(SourceSet(p, w))
+    L = ora.expand(p, w)
+    assert rel_l2(_np(acc.grid.data), L) < TOL
+    assert rel_l2(acc.value(q), ora.evaluate(L, q)) < TOL
+    # per-table tensor-core path vs the FFMA path on the same moments
+    m = eng.p2m(SourceSet(p, w))
+    far = eng.m2l_tables["far"][5]
+    tc = _np(eng.m2l(m, far).data)
+    assert rel_l2(tc, ora.m2l(_np(m.data), ora.tables["far"][5])) < TOL
