@@ -16,12 +16,11 @@
 // lo = rn_tf32(x - hi); D += Ahi*Bhi + Ahi*Blo + Alo*Bhi accumulates in fp32 in
 // TMEM (3xTF32, rel-L2 ~1e-7; plain TF32 fails the 1e-5 gate).
 //
-// CTA: 4 warps, TILES target tiles (M = 128 rows each, one TMEM accumulator of
-// NPAD fp32 columns per tile).  warp 0 lane 0 issues the MMAs and streams the
-// per-offset B tables (cp.async.bulk into an NS-stage ring, mbarrier
-// complete_tx); warps 1-3 gather the window slices (cp.async, zero-fill for
-// out-of-domain sources); all four warps run the TMEM -> registers -> HBM
-// epilogue.  Loop order: source class sigma -> K step (8 tf32) -> offset, so
+// CTA: 8 warps, TILES target tiles (M = 128 rows each).  warp 0 lane 0 issues
+// the MMAs and streams the per-offset B tables (cp.async.bulk into an NS-stage
+// ring, mbarrier complete_tx); warps 1-3 gather the window slices (cp.async,
+// zero-fill for out-of-domain sources); warps 4-7 drain finished TMEM
+// accumulator sets into fp32 registers and write the L rows.  Loop order: source class sigma -> K step (8 tf32) -> offset, so
 // each B slice is loaded once per CTA and reused by TILES tiles.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -37,7 +36,8 @@ struct TCCfg {
   static constexpr int KPAD = (P + 7) / 8 * 8;      // K per offset (tf32 MMA K = 8)
   static constexpr int NPAD = (P + 15) / 16 * 16;   // MMA N (M = 128 needs N % 16 == 0)
   static constexpr int KSTEPS = KPAD / 8;
-  static constexpr int TILES = 2;
+  static constexpr int TILES = NPAD <= 64 ? 2 : 1;  // 8 accumulators must fit 512 TMEM cols
+  static constexpr int PLOAD = (P + 15) / 16 * 16;   // accumulator columns drained
   static constexpr int TY = 16, TZ = 8;             // tile = 1 x TY x TZ targets
   static constexpr int WX = 3, WY = TY + 2, WZ = TZ + 2;
   static constexpr int WROWS = WX * WY * WZ;        // 540
@@ -45,7 +45,7 @@ struct TCCfg {
   static constexpr int BSTAGE = 2 * 2 * NPAD * 16;            // [part][kc][row][16B]
   static constexpr int NS = 8;
   static constexpr int ACC = NPAD <= 64 ? 64 : 128;           // TMEM columns per tile
-  static constexpr int TMEM_COLS = TILES * ACC;               // 128 or 256
+  static constexpr int TMEM_COLS = 2 * TILES * 2 * ACC;       // sets x tiles x kinds
   static constexpr int GATHER_THREADS = 96;                   // warps 1..3
   static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 256;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
@@ -161,20 +161,27 @@ split_tf32_kernel(const float* __restrict__ M, float4* __restrict__ hi, float4* 
 }
 
 // ------------------------------------------------------------ M2L (tc) ---
+// Precision note: tensor-core accumulation into TMEM does not round to
+// nearest, so a single accumulator over all ~3000 MMAs of a tile drifts
+// (measured 2-4e-5 rel-L2).  Each source-class group therefore accumulates
+// into its own TMEM set (double buffered), with the hi*hi products and the two
+// small cross products in separate accumulators; drain warps fold every
+// finished set into float32 registers with round-to-nearest adds.
 template <int RHO>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(256, 1)
 m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, const int2* __restrict__ entries,
               const int* __restrict__ grp_start, float* __restrict__ L, int res, int nu, int C,
               int accumulate) {
   using Cfg = TCCfg<RHO>;
-  constexpr int WROWS = Cfg::WROWS, NS = Cfg::NS, KS = Cfg::KSTEPS;
+  constexpr int WROWS = Cfg::WROWS, NS = Cfg::NS, KS = Cfg::KSTEPS, TILES = Cfg::TILES;
+  constexpr int P = Cfg::P, PP = Cfg::PP, PL = Cfg::PLOAD;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* win = smem;                                   // [2][WSLICE]
   uint8_t* bring = smem + 2 * Cfg::WSLICE;               // [NS][BSTAGE]
   uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NS * Cfg::BSTAGE);
-  // bars: bfull[NS], bempty[NS], winready[2], winfree[2], done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 5);
+  // bars: bfull[NS], bempty[NS], winready[2], winfree[2], accfull[2], accfree[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cls = blockIdx.y;  // target class
@@ -182,25 +189,22 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   const int chan = blockIdx.z;
   const int nyb = (nu + Cfg::TY - 1) / Cfg::TY, nzb = (nu + Cfg::TZ - 1) / Cfg::TZ;
   const int ntiles = nu * nyb * nzb;
-  int tux[Cfg::TILES], tuy[Cfg::TILES], tuz[Cfg::TILES];
-  bool tvalid[Cfg::TILES];
-#pragma unroll
-  for (int t = 0; t < Cfg::TILES; ++t) {
-    const int id = blockIdx.x * Cfg::TILES + t;
-    tvalid[t] = id < ntiles;
-    const int idc = tvalid[t] ? id : 0;
-    tux[t] = idc / (nyb * nzb);
-    tuy[t] = ((idc / nzb) % nyb) * Cfg::TY;
-    tuz[t] = (idc % nzb) * Cfg::TZ;
-  }
+  const int tile0 = blockIdx.x * TILES;
+  auto tile_xyz = [&](int t, int& ux, int& uy, int& uz) {
+    const int id = min(tile0 + t, ntiles - 1);
+    ux = id / (nyb * nzb);
+    uy = ((id / nzb) % nyb) * Cfg::TY;
+    uz = (id % nzb) * Cfg::TZ;
+  };
   const uint32_t bar0 = smem_u32(bars);
   auto bfull = [&](int s) { return bar0 + 8u * s; };
   auto bempty = [&](int s) { return bar0 + 8u * (NS + s); };
   auto winready = [&](int b) { return bar0 + 8u * (2 * NS + b); };
   auto winfree = [&](int b) { return bar0 + 8u * (2 * NS + 2 + b); };
-  const uint32_t done = bar0 + 8u * (2 * NS + 4);
+  auto accfull = [&](int b) { return bar0 + 8u * (2 * NS + 4 + b); };
+  auto accfree = [&](int b) { return bar0 + 8u * (2 * NS + 6 + b); };
 
-  if (warp == 1) {
+  if (warp == 4) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(tmem_slot)),
                  "n"(Cfg::TMEM_COLS));
@@ -214,8 +218,9 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
     for (int b = 0; b < 2; ++b) {
       mbar_init(winready(b), Cfg::GATHER_THREADS);
       mbar_init(winfree(b), 1);
+      mbar_init(accfull(b), 1);
+      mbar_init(accfree(b), 128);
     }
-    mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tc_fence_before();
@@ -224,26 +229,24 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   const uint32_t tmem = *tmem_slot;
 
   const int gbase = cls * 8;
-  const int total_entries = grp_start[gbase + 8] - grp_start[gbase];
   const size_t cells = (size_t)res * res * res;
   const float* hi_c = Mhi + (size_t)chan * cells * Cfg::KPAD;
   const float* lo_c = Mlo + (size_t)chan * cells * Cfg::KPAD;
+  // accumulator column of (set, tile, kind): kind 0 = hi*hi, 1 = cross terms
+  auto acc_col = [](int set, int t, int kind) { return ((set * TILES + t) * 2 + kind) * Cfg::ACC; };
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- MMA issuer + B producer ----------------
-      // global B iteration i walks (sigma, ks, entry) in slice order
       int total = 0;
-      for (int sg = 0; sg < 8; ++sg) total += KS * (grp_start[gbase + sg + 1] - grp_start[gbase + sg]);
-      int p_sg = 0, p_ks = 0, p_j = 0;  // producer cursor
-      auto advance_to_valid = [&]() {
+      for (int sg = 0; sg < 8; ++sg)
+        total += KS * (grp_start[gbase + sg + 1] - grp_start[gbase + sg]);
+      int p_sg = 0, p_ks = 0, p_j = 0;  // producer cursor over (sigma, ks, entry)
+      auto issue_copy = [&](int n) {
         while (p_sg < 8 && p_j >= grp_start[gbase + p_sg + 1] - grp_start[gbase + p_sg]) {
           p_j = 0;
           if (++p_ks == KS) { p_ks = 0; ++p_sg; }
         }
-      };
-      auto issue_copy = [&](int n) {
-        advance_to_valid();
         const int s = n % NS;
         const int2 e = entries[grp_start[gbase + p_sg] + p_j];
         const uint8_t* src = Btab + ((size_t)e.y * KS + p_ks) * Cfg::BSTAGE;
@@ -252,11 +255,12 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
         ++p_j;
       };
       for (int n = 0; n < NS && n < total; ++n) issue_copy(n);
-      int i = 0, q = 0;
-      bool first = true;
+      int i = 0, q = 0, g = 0;
       for (int sg = 0; sg < 8; ++sg) {
         const int gb = grp_start[gbase + sg], ne = grp_start[gbase + sg + 1] - gb;
         if (ne == 0) continue;
+        const int set = g & 1;
+        if (g >= 2) mbar_wait(accfree(set), ((g - 2) >> 1) & 1);
         for (int ks = 0; ks < KS; ++ks, ++q) {
           const int buf = q & 1;
           mbar_wait(winready(buf), (q >> 1) & 1);
@@ -270,18 +274,17 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
             const uint32_t bb = smem_u32(bring + s * Cfg::BSTAGE);
             const uint64_t bh = sdesc(bb, Cfg::NPAD * 16, 128);
             const uint64_t bl = sdesc(bb + 2 * Cfg::NPAD * 16, Cfg::NPAD * 16, 128);
+            const uint32_t acc_in = (ks == 0 && j == 0) ? 0u : 1u;
 #pragma unroll
-            for (int t = 0; t < Cfg::TILES; ++t) {
+            for (int t = 0; t < TILES; ++t) {
               const uint32_t ah = wbase + (((t * 2 + 0) * 2) * WROWS + e.x) * 16;
               const uint32_t al = wbase + (((t * 2 + 1) * 2) * WROWS + e.x) * 16;
               const uint64_t dah = sdesc(ah, WROWS * 16, Cfg::WZ * 16);
               const uint64_t dal = sdesc(al, WROWS * 16, Cfg::WZ * 16);
-              const uint32_t d = tmem + t * Cfg::ACC;
-              umma_tf32(d, dah, bh, Cfg::IDESC, first ? 0u : 1u);
-              umma_tf32(d, dah, bl, Cfg::IDESC, 1u);
-              umma_tf32(d, dal, bh, Cfg::IDESC, 1u);
+              umma_tf32(tmem + acc_col(set, t, 0), dah, bh, Cfg::IDESC, acc_in);
+              umma_tf32(tmem + acc_col(set, t, 1), dah, bl, Cfg::IDESC, acc_in);
+              umma_tf32(tmem + acc_col(set, t, 1), dal, bh, Cfg::IDESC, 1u);
             }
-            first = false;
             umma_commit(bempty(s));
             if (i >= 1 && i - 1 + NS < total) {
               const int sp = (i - 1) % NS;
@@ -291,10 +294,11 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
           }
           umma_commit(winfree(buf));
         }
+        umma_commit(accfull(set));
+        ++g;
       }
-      umma_commit(done);
     }
-  } else {
+  } else if (warp < 4) {
     // ---------------- window gatherers (warps 1..3) ----------------
     const int gt = tid - 32;
     int q = 0;
@@ -306,14 +310,16 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
         const int buf = q & 1;
         if (q >= 2) mbar_wait(winfree(buf), ((q - 2) >> 1) & 1);
         uint8_t* wb = win + buf * Cfg::WSLICE;
-        for (int r = gt; r < Cfg::TILES * WROWS; r += Cfg::GATHER_THREADS) {
+        for (int r = gt; r < TILES * WROWS; r += Cfg::GATHER_THREADS) {
           const int t = r / WROWS, wr = r - t * WROWS;
+          int ux, uy, uz;
+          tile_xyz(t, ux, uy, uz);
           const int wx = wr / (Cfg::WY * Cfg::WZ), wy = (wr / Cfg::WZ) % Cfg::WY, wz = wr % Cfg::WZ;
-          const int cx = 2 * (tux[t] - 1 + wx) + sx;
-          const int cy = 2 * (tuy[t] - 1 + wy) + sy;
-          const int cz = 2 * (tuz[t] - 1 + wz) + sz;
-          const bool ok = tvalid[t] && (unsigned)cx < (unsigned)res && (unsigned)cy < (unsigned)res &&
-                          (unsigned)cz < (unsigned)res;
+          const int cx = 2 * (ux - 1 + wx) + sx;
+          const int cy = 2 * (uy - 1 + wy) + sy;
+          const int cz = 2 * (uz - 1 + wz) + sz;
+          const bool ok = tile0 + t < ntiles && (unsigned)cx < (unsigned)res &&
+                          (unsigned)cy < (unsigned)res && (unsigned)cz < (unsigned)res;
           const size_t off = ok ? (((size_t)cx * res + cy) * res + cz) * Cfg::KPAD + ks * 8 : 0;
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
@@ -331,45 +337,60 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
         mbar_arrive(winready(buf));
       }
     }
-  }
-
-  // ---------------- epilogue: TMEM -> registers -> L ----------------
-  mbar_wait(done, 0);
-  tc_fence_after();
-  constexpr int P = Cfg::P, PP = Cfg::PP;
-  const int row = warp * 32 + lane;
-#pragma unroll 1
-  for (int t = 0; t < Cfg::TILES; ++t) {
-    float acc[(PP + 15) / 16 * 16];
+  } else {
+    // ---------------- drain + epilogue (warps 4..7, TMEM quarters 0..3) ----------------
+    const int dq = warp - 4;
+    float accr[TILES][PL];
 #pragma unroll
-    for (int c0 = 0; c0 < PP; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + t * Cfg::ACC + c0, v);
+    for (int t = 0; t < TILES; ++t)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[c0 + j] = v[j];
-    }
-    if (total_entries == 0) {
+      for (int j = 0; j < PL; ++j) accr[t][j] = 0.f;
+    int g = 0;
+    for (int sg = 0; sg < 8; ++sg) {
+      if (grp_start[gbase + sg + 1] == grp_start[gbase + sg]) continue;
+      const int set = g & 1;
+      mbar_wait(accfull(set), (g >> 1) & 1);
+      tc_fence_after();
 #pragma unroll
-      for (int j = 0; j < (PP + 15) / 16 * 16; ++j) acc[j] = 0.f;
-    }
-    const int uy = tuy[t] + row / Cfg::TZ, uz = tuz[t] + row % Cfg::TZ;
-    if (!tvalid[t] || uy >= nu || uz >= nu) continue;
-    const int64_t cell = (((int64_t)(2 * tux[t] + px) * res + (2 * uy + py)) * res + (2 * uz + pz));
-    float* dst = L + (cell * C + chan) * PP;
+      for (int t = 0; t < TILES; ++t) {
 #pragma unroll
-    for (int k = 0; k < PP; k += 4) {
-      float4 o = make_float4(k + 0 < P ? acc[k] : 0.f, k + 1 < P ? acc[k + 1] : 0.f,
-                             k + 2 < P ? acc[k + 2] : 0.f, k + 3 < P ? acc[k + 3] : 0.f);
-      if (accumulate) {
-        const float4 a = *reinterpret_cast<const float4*>(dst + k);
-        o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+        for (int c0 = 0; c0 < PL; c0 += 16) {
+          float a[16], b[16];
+          const uint32_t lanes = (uint32_t)(dq * 32) << 16;
+          tmem_ld16(tmem + lanes + acc_col(set, t, 0) + c0, a);
+          tmem_ld16(tmem + lanes + acc_col(set, t, 1) + c0, b);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) accr[t][c0 + j] += a[j] + b[j];
+        }
       }
-      *reinterpret_cast<float4*>(dst + k) = o;
+      tc_fence_before();
+      mbar_arrive(accfree(set));
+      ++g;
+    }
+    const int row = dq * 32 + lane;
+#pragma unroll
+    for (int t = 0; t < TILES; ++t) {
+      int ux, uy0, uz0;
+      tile_xyz(t, ux, uy0, uz0);
+      const int uy = uy0 + row / Cfg::TZ, uz = uz0 + row % Cfg::TZ;
+      if (tile0 + t >= ntiles || uy >= nu || uz >= nu) continue;
+      const int64_t cell = (((int64_t)(2 * ux + px) * res + (2 * uy + py)) * res + (2 * uz + pz));
+      float* dst = L + (cell * C + chan) * PP;
+#pragma unroll
+      for (int k = 0; k < PP; k += 4) {
+        float4 o = make_float4(k + 0 < P ? accr[t][k] : 0.f, k + 1 < P ? accr[t][k + 1] : 0.f,
+                               k + 2 < P ? accr[t][k + 2] : 0.f, k + 3 < P ? accr[t][k + 3] : 0.f);
+        if (accumulate) {
+          const float4 a = *reinterpret_cast<const float4*>(dst + k);
+          o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+        }
+        *reinterpret_cast<float4*>(dst + k) = o;
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1)
+  if (warp == 4)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "n"(Cfg::TMEM_COLS));
 }
@@ -409,7 +430,7 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const f
     const int ntiles = nu * nyb * nzb;
     dim3 grid((unsigned)((ntiles + Cfg::TILES - 1) / Cfg::TILES), 8u, (unsigned)C);
     FC2T2_LAUNCH(plan.level_name, s,
-                 kern<<<grid, 128, Cfg::SMEM, s>>>(Mhi, Mlo, plan.btab, plan.entries,
+                 kern<<<grid, 256, Cfg::SMEM, s>>>(Mhi, Mlo, plan.btab, plan.entries,
                                                    plan.grp_start, L, res, nu, C, accumulate));
   });
   return cudaGetLastError();
