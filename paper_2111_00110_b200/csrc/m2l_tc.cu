@@ -46,8 +46,12 @@ struct TCCfg {
   static constexpr int NS = 8;
   static constexpr int ACC = NPAD <= 64 ? 64 : 128;           // TMEM columns per tile
   static constexpr int TMEM_COLS = 2 * TILES * 2 * ACC;       // sets x tiles x kinds
-  static constexpr int GATHER_THREADS = 96;                   // warps 1..3
-  static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 256;
+  static constexpr int THREADS = 384;                         // 12 warps
+  static constexpr int GATHER_WARP0 = 2, GATHER_WARPS = 6;    // warps 2..7
+  static constexpr int GATHER_THREADS = 32 * GATHER_WARPS;
+  static constexpr int DRAIN_WARP0 = 8;                       // warps 8..11 (TMEM quarters)
+  static constexpr int MAXE = 256;                            // entries of one target class
+  static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 256 + MAXE * 8 + 64;
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 };
@@ -167,8 +171,22 @@ split_tf32_kernel(const float* __restrict__ M, float4* __restrict__ hi, float4* 
 // into its own TMEM set (double buffered), with the hi*hi products and the two
 // small cross products in separate accumulators; drain warps fold every
 // finished set into float32 registers with round-to-nearest adds.
+//
+// Warp roles (12 warps): 0 MMA issuer (warp-uniform loop, elect-one issue),
+// 1 B-table producer (cp.async.bulk ring), 2-7 window gatherers, 8-11 TMEM
+// drain + epilogue (warp % 4 = TMEM lane quarter).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 template <int RHO>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, const int2* __restrict__ entries,
               const int* __restrict__ grp_start, float* __restrict__ L, int res, int nu, int C,
@@ -182,6 +200,8 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NS * Cfg::BSTAGE);
   // bars: bfull[NS], bempty[NS], winready[2], winfree[2], accfull[2], accfree[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 8);
+  int* sgrp = reinterpret_cast<int*>(tmem_slot + 4);     // [9] group starts (class-local)
+  int2* sent = reinterpret_cast<int2*>(sgrp + 12);       // [MAXE] class entries
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cls = blockIdx.y;  // target class
@@ -204,7 +224,13 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   auto accfull = [&](int b) { return bar0 + 8u * (2 * NS + 4 + b); };
   auto accfree = [&](int b) { return bar0 + 8u * (2 * NS + 6 + b); };
 
-  if (warp == 4) {
+  // stage this class's interaction list (class-local group starts) in smem
+  const int gb0 = grp_start[cls * 8];
+  const int nent = grp_start[cls * 8 + 8] - gb0;
+  if (tid < 9) sgrp[tid] = grp_start[cls * 8 + tid] - gb0;
+  for (int k = tid; k < nent && k < Cfg::MAXE; k += blockDim.x) sent[k] = entries[gb0 + k];
+
+  if (warp == Cfg::DRAIN_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_u32(tmem_slot)),
                  "n"(Cfg::TMEM_COLS));
@@ -228,7 +254,6 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int gbase = cls * 8;
   const size_t cells = (size_t)res * res * res;
   const float* hi_c = Mhi + (size_t)chan * cells * Cfg::KPAD;
   const float* lo_c = Mlo + (size_t)chan * cells * Cfg::KPAD;
@@ -236,42 +261,25 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   auto acc_col = [](int set, int t, int kind) { return ((set * TILES + t) * 2 + kind) * Cfg::ACC; };
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- MMA issuer + B producer ----------------
-      int total = 0;
-      for (int sg = 0; sg < 8; ++sg)
-        total += KS * (grp_start[gbase + sg + 1] - grp_start[gbase + sg]);
-      int p_sg = 0, p_ks = 0, p_j = 0;  // producer cursor over (sigma, ks, entry)
-      auto issue_copy = [&](int n) {
-        while (p_sg < 8 && p_j >= grp_start[gbase + p_sg + 1] - grp_start[gbase + p_sg]) {
-          p_j = 0;
-          if (++p_ks == KS) { p_ks = 0; ++p_sg; }
-        }
-        const int s = n % NS;
-        const int2 e = entries[grp_start[gbase + p_sg] + p_j];
-        const uint8_t* src = Btab + ((size_t)e.y * KS + p_ks) * Cfg::BSTAGE;
-        mbar_expect_tx(bfull(s), Cfg::BSTAGE);
-        bulk_g2s(smem_u32(bring + s * Cfg::BSTAGE), src, Cfg::BSTAGE, bfull(s));
-        ++p_j;
-      };
-      for (int n = 0; n < NS && n < total; ++n) issue_copy(n);
-      int i = 0, q = 0, g = 0;
-      for (int sg = 0; sg < 8; ++sg) {
-        const int gb = grp_start[gbase + sg], ne = grp_start[gbase + sg + 1] - gb;
-        if (ne == 0) continue;
-        const int set = g & 1;
-        if (g >= 2) mbar_wait(accfree(set), ((g - 2) >> 1) & 1);
-        for (int ks = 0; ks < KS; ++ks, ++q) {
-          const int buf = q & 1;
-          mbar_wait(winready(buf), (q >> 1) & 1);
+    // ---------------- MMA issuer (whole warp, uniform control flow) ----------------
+    int i = 0, q = 0, g = 0;
+    for (int sg = 0; sg < 8; ++sg) {
+      const int gb = sgrp[sg], ne = sgrp[sg + 1] - gb;
+      if (ne == 0) continue;
+      const int set = g & 1;
+      if (g >= 2) mbar_wait(accfree(set), ((g - 2) >> 1) & 1);
+      for (int ks = 0; ks < KS; ++ks, ++q) {
+        const int buf = q & 1;
+        mbar_wait(winready(buf), (q >> 1) & 1);
+        tc_fence_after();
+        const uint32_t wbase = smem_u32(win + buf * Cfg::WSLICE);
+        for (int j = 0; j < ne; ++j, ++i) {
+          const int s = i % NS;
+          mbar_wait(bfull(s), (i / NS) & 1);
           tc_fence_after();
-          const uint32_t wbase = smem_u32(win + buf * Cfg::WSLICE);
-          for (int j = 0; j < ne; ++j, ++i) {
-            const int s = i % NS;
-            mbar_wait(bfull(s), (i / NS) & 1);
-            tc_fence_after();
-            const int2 e = entries[gb + j];
-            const uint32_t bb = smem_u32(bring + s * Cfg::BSTAGE);
+          const int2 e = sent[gb + j];
+          const uint32_t bb = smem_u32(bring + s * Cfg::BSTAGE);
+          if (elect_one()) {
             const uint64_t bh = sdesc(bb, Cfg::NPAD * 16, 128);
             const uint64_t bl = sdesc(bb + 2 * Cfg::NPAD * 16, Cfg::NPAD * 16, 128);
             const uint32_t acc_in = (ks == 0 && j == 0) ? 0u : 1u;
@@ -286,24 +294,38 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
               umma_tf32(tmem + acc_col(set, t, 1), dal, bh, Cfg::IDESC, 1u);
             }
             umma_commit(bempty(s));
-            if (i >= 1 && i - 1 + NS < total) {
-              const int sp = (i - 1) % NS;
-              mbar_wait(bempty(sp), ((i - 1) / NS) & 1);
-              issue_copy(i - 1 + NS);
-            }
           }
-          umma_commit(winfree(buf));
+          __syncwarp();
         }
-        umma_commit(accfull(set));
-        ++g;
+        if (elect_one()) umma_commit(winfree(buf));
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(accfull(set));
+      __syncwarp();
+      ++g;
+    }
+  } else if (warp == 1) {
+    // ---------------- B-table producer ----------------
+    if (lane == 0) {
+      int n = 0;
+      for (int sg = 0; sg < 8; ++sg) {
+        const int gb = sgrp[sg], ne = sgrp[sg + 1] - gb;
+        for (int ks = 0; ks < KS; ++ks)
+          for (int j = 0; j < ne; ++j, ++n) {
+            const int s = n % NS;
+            if (n >= NS) mbar_wait(bempty(s), ((n / NS) - 1) & 1);
+            const uint8_t* src = Btab + ((size_t)sent[gb + j].y * KS + ks) * Cfg::BSTAGE;
+            mbar_expect_tx(bfull(s), Cfg::BSTAGE);
+            bulk_g2s(smem_u32(bring + s * Cfg::BSTAGE), src, Cfg::BSTAGE, bfull(s));
+          }
       }
     }
-  } else if (warp < 4) {
-    // ---------------- window gatherers (warps 1..3) ----------------
-    const int gt = tid - 32;
+  } else if (warp < Cfg::DRAIN_WARP0) {
+    // ---------------- window gatherers ----------------
+    const int gt = tid - 32 * Cfg::GATHER_WARP0;
     int q = 0;
     for (int sg = 0; sg < 8; ++sg) {
-      const int ne = grp_start[gbase + sg + 1] - grp_start[gbase + sg];
+      const int ne = sgrp[sg + 1] - sgrp[sg];
       if (ne == 0) continue;
       const int sx = (sg >> 2) & 1, sy = (sg >> 1) & 1, sz = sg & 1;
       for (int ks = 0; ks < KS; ++ks, ++q) {
@@ -338,8 +360,8 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
       }
     }
   } else {
-    // ---------------- drain + epilogue (warps 4..7, TMEM quarters 0..3) ----------------
-    const int dq = warp - 4;
+    // ---------------- drain + epilogue (TMEM quarters 0..3) ----------------
+    const int dq = warp & 3;
     float accr[TILES][PL];
 #pragma unroll
     for (int t = 0; t < TILES; ++t)
@@ -347,7 +369,7 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
       for (int j = 0; j < PL; ++j) accr[t][j] = 0.f;
     int g = 0;
     for (int sg = 0; sg < 8; ++sg) {
-      if (grp_start[gbase + sg + 1] == grp_start[gbase + sg]) continue;
+      if (sgrp[sg + 1] == sgrp[sg]) continue;
       const int set = g & 1;
       mbar_wait(accfull(set), (g >> 1) & 1);
       tc_fence_after();
@@ -390,7 +412,7 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4)
+  if (warp == Cfg::DRAIN_WARP0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "n"(Cfg::TMEM_COLS));
 }
@@ -430,7 +452,7 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const f
     const int ntiles = nu * nyb * nzb;
     dim3 grid((unsigned)((ntiles + Cfg::TILES - 1) / Cfg::TILES), 8u, (unsigned)C);
     FC2T2_LAUNCH(plan.level_name, s,
-                 kern<<<grid, 256, Cfg::SMEM, s>>>(Mhi, Mlo, plan.btab, plan.entries,
+                 kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(Mhi, Mlo, plan.btab, plan.entries,
                                                    plan.grp_start, L, res, nu, C, accumulate));
   });
   return cudaGetLastError();
