@@ -128,8 +128,9 @@ float rn_tf32_host(double v) {
 }
 
 // One slot's table in the tcgen05 B layout: for every K step (8 inputs n),
-// [part hi/lo][kchunk 2][row k (NPAD)][4 floats], with A = hi + lo split in
-// float64 (hi = rn_tf32(A), lo = rn_tf32(A - hi)); zero padded.
+// [kchunk 2][row: k (hi) for rows < NPAD, k (lo) for rows >= NPAD][4 floats],
+// with A = hi + lo split in float64 (hi = rn_tf32(A), lo = rn_tf32(A - hi));
+// zero padded.  Rows [0, 2 NPAD) form one N = 2 NPAD K-major operand.
 void append_btab(const double* A, int P, int rho, std::vector<float>& btab) {
   const int KS = fc2t2::tc_kpad(rho) / 8, NPAD = fc2t2::tc_npad(rho);
   const size_t stage = (size_t)fc2t2::tc_bstage(rho) / 4;
@@ -144,8 +145,8 @@ void append_btab(const double* A, int P, int rho, std::vector<float>& btab) {
           const float hi = rn_tf32_host(a);
           const float lo = rn_tf32_host(a - (double)hi);
           float* st = btab.data() + base + ks * stage;
-          st[((0 * 2 + kc) * NPAD + k) * 4 + f] = hi;
-          st[((1 * 2 + kc) * NPAD + k) * 4 + f] = lo;
+          st[(kc * 2 * NPAD + k) * 4 + f] = hi;
+          st[(kc * 2 * NPAD + NPAD + k) * 4 + f] = lo;
         }
 }
 

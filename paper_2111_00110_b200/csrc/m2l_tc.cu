@@ -42,18 +42,24 @@ struct TCCfg {
   static constexpr int WX = 3, WY = TY + 2, WZ = TZ + 2;
   static constexpr int WROWS = WX * WY * WZ;        // 540
   static constexpr int WSLICE = TILES * 2 * 2 * WROWS * 16;   // [tile][part][kc][row][16B]
-  static constexpr int BSTAGE = 2 * 2 * NPAD * 16;            // [part][kc][row][16B]
-  static constexpr int NS = 8;
-  static constexpr int ACC = NPAD <= 64 ? 64 : 128;           // TMEM columns per tile
-  static constexpr int TMEM_COLS = 2 * TILES * 2 * ACC;       // sets x tiles x kinds
+  static constexpr int BSTAGE = 2 * 2 * NPAD * 16;  // [kc][row: hi 0..NPAD-1, lo NPAD..][16B]
+  static constexpr int DPS = 9;                     // offsets per B stage
+  static constexpr int NS = RHO <= 4 ? 3 : 2;       // B stages (DPS tables each)
+  static constexpr int ACC = NPAD <= 64 ? 128 : 256;          // [hi*hi | cross] per tile
+  static constexpr int TMEM_COLS = 2 * TILES * ACC;           // sets x tiles
   static constexpr int THREADS = 384;                         // 12 warps
   static constexpr int GATHER_WARP0 = 2, GATHER_WARPS = 6;    // warps 2..7
   static constexpr int GATHER_THREADS = 32 * GATHER_WARPS;
   static constexpr int DRAIN_WARP0 = 8;                       // warps 8..11 (TMEM quarters)
   static constexpr int MAXE = 256;                            // entries of one target class
-  static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 256 + MAXE * 8 + 64;
-  static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
-                                    ((uint32_t)(NPAD >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  static constexpr size_t SMEM =
+      2 * (size_t)WSLICE + (size_t)NS * DPS * BSTAGE + 256 + MAXE * 8 + 64;
+  static constexpr uint32_t idesc(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(128 >> 4) << 24);
+  }
+  static constexpr uint32_t IDESC1 = idesc(NPAD);      // A x B_hi
+  static constexpr uint32_t IDESC2 = idesc(2 * NPAD);  // A_hi x [B_hi; B_lo]
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -196,8 +202,8 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   constexpr int P = Cfg::P, PP = Cfg::PP, PL = Cfg::PLOAD;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* win = smem;                                   // [2][WSLICE]
-  uint8_t* bring = smem + 2 * Cfg::WSLICE;               // [NS][BSTAGE]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NS * Cfg::BSTAGE);
+  uint8_t* bring = smem + 2 * Cfg::WSLICE;               // [NS][DPS][BSTAGE]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NS * Cfg::DPS * Cfg::BSTAGE);
   // bars: bfull[NS], bempty[NS], winready[2], winfree[2], accfull[2], accfree[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 8);
   int* sgrp = reinterpret_cast<int*>(tmem_slot + 4);     // [9] group starts (class-local)
@@ -257,12 +263,19 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   const size_t cells = (size_t)res * res * res;
   const float* hi_c = Mhi + (size_t)chan * cells * Cfg::KPAD;
   const float* lo_c = Mlo + (size_t)chan * cells * Cfg::KPAD;
-  // accumulator column of (set, tile, kind): kind 0 = hi*hi, 1 = cross terms
-  auto acc_col = [](int set, int t, int kind) { return ((set * TILES + t) * 2 + kind) * Cfg::ACC; };
+  // accumulator columns of (set, tile): [0, NPAD) hi*hi, [NPAD, 2 NPAD) cross terms
+  auto acc_col = [](int set, int t, int kind) {
+    return (set * TILES + t) * Cfg::ACC + kind * Cfg::NPAD;
+  };
 
   if (warp == 0) {
     // ---------------- MMA issuer (whole warp, uniform control flow) ----------------
-    int i = 0, q = 0, g = 0;
+    // B stages walk (sigma, ks, chunk of <= DPS offsets); one wait + one
+    // commit per stage.  Descriptors are built once and advanced by adding
+    // byte offsets / 16 to their start-address field.
+    const uint64_t bdesc0 = sdesc(smem_u32(bring), 2 * Cfg::NPAD * 16, 128);
+    const uint64_t wdesc0 = sdesc(smem_u32(win), WROWS * 16, Cfg::WZ * 16);
+    int n = 0, q = 0, g = 0;
     for (int sg = 0; sg < 8; ++sg) {
       const int gb = sgrp[sg], ne = sgrp[sg + 1] - gb;
       if (ne == 0) continue;
@@ -272,26 +285,24 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
         const int buf = q & 1;
         mbar_wait(winready(buf), (q >> 1) & 1);
         tc_fence_after();
-        const uint32_t wbase = smem_u32(win + buf * Cfg::WSLICE);
-        for (int j = 0; j < ne; ++j, ++i) {
-          const int s = i % NS;
-          mbar_wait(bfull(s), (i / NS) & 1);
+        const uint64_t wd = wdesc0 + (uint64_t)((buf * Cfg::WSLICE) >> 4);
+        for (int j0 = 0; j0 < ne; j0 += Cfg::DPS, ++n) {
+          const int s = n % NS, cnt = min(Cfg::DPS, ne - j0);
+          mbar_wait(bfull(s), (n / NS) & 1);
           tc_fence_after();
-          const int2 e = sent[gb + j];
-          const uint32_t bb = smem_u32(bring + s * Cfg::BSTAGE);
           if (elect_one()) {
-            const uint64_t bh = sdesc(bb, Cfg::NPAD * 16, 128);
-            const uint64_t bl = sdesc(bb + 2 * Cfg::NPAD * 16, Cfg::NPAD * 16, 128);
-            const uint32_t acc_in = (ks == 0 && j == 0) ? 0u : 1u;
+            for (int jj = 0; jj < cnt; ++jj) {
+              const int ex = sent[gb + j0 + jj].x;
+              const uint64_t bd = bdesc0 + (uint64_t)(((s * Cfg::DPS + jj) * Cfg::BSTAGE) >> 4);
+              const uint32_t acc_in = (ks == 0 && j0 + jj == 0) ? 0u : 1u;
 #pragma unroll
-            for (int t = 0; t < TILES; ++t) {
-              const uint32_t ah = wbase + (((t * 2 + 0) * 2) * WROWS + e.x) * 16;
-              const uint32_t al = wbase + (((t * 2 + 1) * 2) * WROWS + e.x) * 16;
-              const uint64_t dah = sdesc(ah, WROWS * 16, Cfg::WZ * 16);
-              const uint64_t dal = sdesc(al, WROWS * 16, Cfg::WZ * 16);
-              umma_tf32(tmem + acc_col(set, t, 0), dah, bh, Cfg::IDESC, acc_in);
-              umma_tf32(tmem + acc_col(set, t, 1), dah, bl, Cfg::IDESC, acc_in);
-              umma_tf32(tmem + acc_col(set, t, 1), dal, bh, Cfg::IDESC, 1u);
+              for (int t = 0; t < TILES; ++t) {
+                const uint64_t dah = wd + (uint64_t)(((t * 4 + 0) * WROWS + ex));
+                const uint64_t dal = wd + (uint64_t)(((t * 4 + 2) * WROWS + ex));
+                // D[:, 0:N) += Ahi Bhi and D[:, N:2N) += Ahi Blo in one N = 2 NPAD MMA
+                umma_tf32(tmem + acc_col(set, t, 0), dah, bd, Cfg::IDESC2, acc_in);
+                umma_tf32(tmem + acc_col(set, t, 1), dal, bd, Cfg::IDESC1, 1u);
+              }
             }
             umma_commit(bempty(s));
           }
@@ -311,12 +322,16 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
       for (int sg = 0; sg < 8; ++sg) {
         const int gb = sgrp[sg], ne = sgrp[sg + 1] - gb;
         for (int ks = 0; ks < KS; ++ks)
-          for (int j = 0; j < ne; ++j, ++n) {
-            const int s = n % NS;
+          for (int j0 = 0; j0 < ne; j0 += Cfg::DPS, ++n) {
+            const int s = n % NS, cnt = min(Cfg::DPS, ne - j0);
             if (n >= NS) mbar_wait(bempty(s), ((n / NS) - 1) & 1);
-            const uint8_t* src = Btab + ((size_t)sent[gb + j].y * KS + ks) * Cfg::BSTAGE;
-            mbar_expect_tx(bfull(s), Cfg::BSTAGE);
-            bulk_g2s(smem_u32(bring + s * Cfg::BSTAGE), src, Cfg::BSTAGE, bfull(s));
+            mbar_expect_tx(bfull(s), cnt * Cfg::BSTAGE);
+            for (int jj = 0; jj < cnt; ++jj) {
+              const uint8_t* src =
+                  Btab + ((size_t)sent[gb + j0 + jj].y * KS + ks) * Cfg::BSTAGE;
+              bulk_g2s(smem_u32(bring + (s * Cfg::DPS + jj) * Cfg::BSTAGE), src, Cfg::BSTAGE,
+                       bfull(s));
+            }
           }
       }
     }
