@@ -86,6 +86,57 @@ def to_device(x, cols: int | None = None, points: bool = False) -> torch.Tensor:
     return t.contiguous()
 
 
+class HostIO:
+    """Host <-> device staging for host-tensor callers: copies run on a
+    dedicated stream so they overlap the expansion work on the compute
+    stream; results land in pinned buffers (torch's caching host allocator)."""
+
+    _streams: dict = {}
+
+    @classmethod
+    def stream(cls) -> torch.cuda.Stream:
+        dev = torch.cuda.current_device()
+        if dev not in cls._streams:
+            cls._streams[dev] = torch.cuda.Stream(device=dev)
+        return cls._streams[dev]
+
+    @classmethod
+    def h2d(cls, x: torch.Tensor, cols: int | None = None):
+        """Async upload of a host tensor; returns (device tensor, ready event)."""
+        cs = torch.cuda.current_stream()
+        s = cls.stream()
+        src = x if x.is_pinned() else x.pin_memory()
+        with torch.cuda.stream(s):
+            t = torch.empty(tuple(src.shape), dtype=torch.float32, device=_device())
+            t.copy_(src, non_blocking=True)
+        ev = s.record_event()
+        t.record_stream(cs)
+        if cols is not None:
+            t = t.reshape(-1, cols)
+        return t, ev
+
+    @classmethod
+    def d2h(cls, t: torch.Tensor) -> torch.Tensor:
+        """Start an async download after the current stream's work; call
+        finish() before the host reads the result."""
+        cs = torch.cuda.current_stream()
+        s = cls.stream()
+        s.wait_stream(cs)
+        out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+        with torch.cuda.stream(s):
+            out.copy_(t, non_blocking=True)
+        t.record_stream(s)
+        return out
+
+    @classmethod
+    def finish(cls) -> None:
+        cls.stream().synchronize()
+
+
+def is_host_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor) and not x.is_cuda
+
+
 def like_input(t: torch.Tensor, ref):
     """Return ``t`` in the caller's kind: CUDA tensor for CUDA input, a
     (pinned) host tensor for host-tensor input, float64 numpy for numpy."""

@@ -21,8 +21,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .expansion import (Accessor, Engine, SourceSet, _host_domain_check,
-                        like_input, to_device)
+from .expansion import (Accessor, Engine, HostIO, SourceSet, _host_domain_check,
+                        is_host_tensor, like_input, to_device)
 
 
 @dataclass
@@ -49,6 +49,17 @@ class ExplicitResult:
 
 def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     _host_domain_check(q, "query")
+    if is_host_tensor(q):
+        # host tensors: the query upload overlaps the source expansion
+        qd, q_ready = HostIO.h2d(q, 3)
+        acc = engine.expand_device(sources.p, sources.w)
+        torch.cuda.current_stream().wait_event(q_ready)
+        vals = acc.eval_device(qd, _lib.L2P_VALUE)["value"]
+        out = HostIO.d2h(vals)
+        HostIO.finish()
+        engine.flag.raise_if_set("source/query")
+        return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine,
+                              q_dev=qd)
     qd = to_device(q, 3, points=True)
     acc = engine.expand_device(sources.p, sources.w)
     vals = acc.eval_device(qd, _lib.L2P_VALUE)["value"]
@@ -60,10 +71,23 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     eng = res.engine
     qd = res.q_dev
+    src = res.sources
+    if is_host_tensor(y_bar):
+        # host tensors: q_bar's download overlaps the backward expansion
+        yb, y_ready = HostIO.h2d(y_bar)
+        torch.cuda.current_stream().wait_event(y_ready)
+        yb = yb.reshape(qd.shape[0], -1)
+        q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb)["wgrad"]
+        q_bar_h = HostIO.d2h(q_bar)
+        back = eng.expand_device(qd, yb)
+        out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
+        w_bar_h, p_bar_h = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
+        HostIO.finish()
+        eng.flag.raise_if_set("source/query")
+        return LayerGradients(w_bar=w_bar_h, p_bar=p_bar_h, q_bar=q_bar_h)
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
     q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb)["wgrad"]
     back = eng.expand_device(qd, yb)
-    src = res.sources
     out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
     eng.flag.raise_if_set("source/query")
     ref = y_bar
