@@ -167,55 +167,107 @@ __global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, 
     hist[(int64_t)b * nblocks + blockIdx.x] = h[b];
 }
 
-// Stable scatter: keys of one block are ranked in index order, round by
-// round (256 keys per round), with warp-level match for ties inside a warp
-// and a per-(warp, digit) prefix across the 8 warps of the round.
+// Stable scatter.  Warp w of a block owns keys [w*512, (w+1)*512) of the
+// block's 4096-key tile and ranks them in index order with warp match_any
+// against its own digit histogram (no block barriers inside the loop); one
+// exclusive scan across the warps per digit then places every warp's run
+// after the earlier warps' runs, so the scatter is stable.
+constexpr int RADIX_ITEMS = RADIX_TILE / RADIX_THREADS;  // 16 keys per thread
+
 __global__ void __launch_bounds__(RADIX_THREADS)
 radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
                      uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                      int64_t n, int shift, int bits, int nblocks,
                      const uint32_t* __restrict__ offsets) {
-  __shared__ uint32_t running[256];
-  __shared__ uint32_t wcount[RADIX_WARPS][256];
+  __shared__ uint32_t whist[RADIX_WARPS][256];
   const int nbins = 1 << bits;
   const uint32_t mask = (uint32_t)nbins - 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
-    running[b] = offsets[(int64_t)b * nblocks + blockIdx.x];
-  const int64_t base = (int64_t)blockIdx.x * RADIX_TILE;
+  for (int b = threadIdx.x; b < RADIX_WARPS * 256; b += blockDim.x) (&whist[0][0])[b] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * RADIX_TILE + (int64_t)warp * (32 * RADIX_ITEMS);
   const uint32_t lt_mask = (1u << lane) - 1u;
-  for (int r = 0; r < RADIX_ROUNDS; ++r) {
-    for (int b = threadIdx.x; b < RADIX_WARPS * 256; b += blockDim.x) (&wcount[0][0])[b] = 0;
-    __syncthreads();
-    const int64_t i = base + (int64_t)r * RADIX_THREADS + threadIdx.x;
-    const bool valid = i < n;
-    uint32_t key = 0, val = 0, digit = 0xffffffffu;
-    if (valid) {
-      key = keys_in[i];
-      val = vals_in[i];
-      digit = (key >> shift) & mask;
-    }
-    const uint32_t peers = __match_any_sync(0xffffffffu, digit);
-    const uint32_t rank = __popc(peers & lt_mask);
-    if (valid && rank == 0) wcount[warp][digit] = __popc(peers);
-    __syncthreads();
-    for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-      uint32_t acc = running[b];
+  uint32_t key[RADIX_ITEMS], val[RADIX_ITEMS], pos[RADIX_ITEMS];
 #pragma unroll
-      for (int w = 0; w < RADIX_WARPS; ++w) {
-        uint32_t c = wcount[w][b];
-        wcount[w][b] = acc;
-        acc += c;
-      }
-      running[b] = acc;
+  for (int r = 0; r < RADIX_ITEMS; ++r) {
+    const int64_t i = base + r * 32 + lane;
+    const bool valid = i < n;
+    key[r] = valid ? keys_in[i] : 0xffffffffu;
+    val[r] = valid ? vals_in[i] : 0u;
+  }
+#pragma unroll
+  for (int r = 0; r < RADIX_ITEMS; ++r) {
+    const bool valid = key[r] != 0xffffffffu;
+    const uint32_t d = valid ? (key[r] >> shift) & mask : 0xffffffffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader && valid) {
+      old = whist[warp][d];
+      whist[warp][d] = old + __popc(peers);
     }
-    __syncthreads();
-    if (valid) {
-      uint32_t pos = wcount[warp][digit] + rank;
-      keys_out[pos] = key;
-      vals_out[pos] = val;
+    old = __shfl_sync(0xffffffffu, old, leader);
+    pos[r] = old + __popc(peers & lt_mask);
+    __syncwarp();
+  }
+  __syncthreads();
+  // block-local digit runs: per-warp prefix inside each digit, then an
+  // exclusive scan over the digits (warp 0, 8 bins per lane)
+  __shared__ uint32_t dstart[256], gstart[256];
+  for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int w = 0; w < RADIX_WARPS; ++w) {
+      const uint32_t c = whist[w][b];
+      whist[w][b] = acc;
+      acc += c;
     }
-    __syncthreads();
+    dstart[b] = acc;  // digit total for now
+    gstart[b] = offsets[(int64_t)b * nblocks + blockIdx.x];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int b = lane * 8 + k;
+      v[k] = b < nbins ? dstart[b] : 0u;
+      sum += v[k];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    uint32_t run = x - sum;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int b = lane * 8 + k;
+      if (b < nbins) dstart[b] = run;
+      run += v[k];
+    }
+  }
+  __syncthreads();
+  // stage the tile in digit order, then write every digit run contiguously
+  __shared__ uint32_t skey[RADIX_TILE], sval[RADIX_TILE];
+#pragma unroll
+  for (int r = 0; r < RADIX_ITEMS; ++r) {
+    if (key[r] == 0xffffffffu) continue;
+    const uint32_t d = (key[r] >> shift) & mask;
+    const uint32_t lp = dstart[d] + whist[warp][d] + pos[r];
+    skey[lp] = key[r];
+    sval[lp] = val[r];
+  }
+  __syncthreads();
+  const int64_t tbase = (int64_t)blockIdx.x * RADIX_TILE;
+  const int cnt = (int)min<int64_t>(RADIX_TILE, n - tbase);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint32_t k = skey[i];
+    const uint32_t d = (k >> shift) & mask;
+    const uint32_t gp = gstart[d] + (uint32_t)i - dstart[d];
+    keys_out[gp] = k;
+    vals_out[gp] = sval[i];
   }
 }
 
