@@ -119,6 +119,48 @@ int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d
               int mode, const float* d_wts, float* d_value, float* d_grad, float* d_hess,
               float* d_wgrad, int32_t* d_flag, void* stream);
 
+/* ---- rays: traversal (ray.py:101-157), layers (layers.py:193-402) ----
+ * Rays are (R, 3) float64 origins / directions on the device.  Traversal:
+ * count segments per ray, exclusive-scan the counts (fc2t2_scan_u32), fill
+ * ray_id (S) int32, t0/t1 (S) float64, box (S, 3) int32. */
+const char* fc2t2_ray_last_error(void);
+size_t fc2t2_scan_workspace_size(int64_t n);
+int fc2t2_scan_u32(const uint32_t* d_in, uint32_t* d_out, int64_t n, void* d_ws, size_t ws_bytes,
+                   void* stream);
+int fc2t2_traverse_count(int level, const double* d_org, const double* d_dir, int64_t R,
+                         uint32_t* d_counts, void* stream);
+int fc2t2_traverse_fill(int level, const double* d_org, const double* d_dir, int64_t R,
+                        const uint32_t* d_offsets, int32_t* d_ray_id, double* d_t0, double* d_t1,
+                        int32_t* d_box, void* stream);
+/* depth_forward + _first_root_per_ray (layers.py:208-272) fused with the
+ * gradient (and optional Hessian, xx yy zz xy xz yz) at the hit. */
+int fc2t2_depth_forward(int rho, int level, const float* d_l, const double* d_org,
+                        const double* d_dir, int64_t R, double bias, double* d_lengths,
+                        uint8_t* d_hit, double* d_points, float* d_grads, float* d_hess,
+                        float* d_denom, void* stream);
+/* depth_jvp / surface_gradient_jvp insertion payloads (layers.py:275-356);
+ * either tangent may be NULL; both given = one fused insertion. */
+int fc2t2_root_payload(int rho, int level, const double* d_dir, int64_t R, const uint8_t* d_hit,
+                       const double* d_points, const float* d_grads, const float* d_hess,
+                       const float* d_denom, const float* d_y_len, const float* d_y_grad,
+                       uint32_t* d_keys, float* d_payload, int32_t* d_n_clamped, void* stream);
+/* line_integral_forward (layers.py:371-386) and the jvp's segment payloads
+ * y_c * line2taylor (layers.py:389-402, ray.py:213-246). */
+int fc2t2_line_integral(int rho, int level, int channels, const float* d_l, const double* d_org,
+                        const double* d_dir, int64_t R, float* d_values, void* stream);
+int fc2t2_line_payload(int rho, int level, int channels, const double* d_org, const double* d_dir,
+                       int64_t R, const uint32_t* d_offsets, const float* d_y,
+                       const double* d_gl_x, const double* d_gl_w, int G, uint32_t* d_keys,
+                       float* d_payload, void* stream);
+/* generic insertion (_insert_moments, layers.py:144-153): stable sort of
+ * precomputed cell keys (key res^3 = no cell), then per-cell sums of the
+ * (n, C, PP) payload rows in sorted order into the finest M grid. */
+size_t fc2t2_key_sort_workspace_size(int level, int64_t n);
+int fc2t2_key_sort(int level, const uint32_t* d_keys, int64_t n, int32_t* d_order,
+                   int32_t* d_cell_start, void* d_ws, size_t ws_bytes, void* stream);
+int fc2t2_insert(int rho, int level, int channels, const float* d_payload, const int32_t* d_order,
+                 const int32_t* d_cell_start, float* d_m, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

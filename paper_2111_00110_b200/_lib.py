@@ -46,6 +46,21 @@ _SIGS = {
     "fc2t2_expand": (_i32, [_vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "fc2t2_l2p": (_i32, [_i32, _i32, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp]),
+    "fc2t2_ray_last_error": (ct.c_char_p, []),
+    "fc2t2_scan_workspace_size": (_sz, [_i64]),
+    "fc2t2_scan_u32": (_i32, [_vp, _vp, _i64, _vp, _sz, _vp]),
+    "fc2t2_traverse_count": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp]),
+    "fc2t2_traverse_fill": (_i32, [_i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fc2t2_depth_forward": (_i32, [_i32, _i32, _vp, _vp, _vp, _i64, ct.c_double, _vp, _vp, _vp,
+                                   _vp, _vp, _vp, _vp]),
+    "fc2t2_root_payload": (_i32, [_i32, _i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _vp]),
+    "fc2t2_line_integral": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "fc2t2_line_payload": (_i32, [_i32, _i32, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i32,
+                                  _vp, _vp, _vp]),
+    "fc2t2_key_sort_workspace_size": (_sz, [_i32, _i64]),
+    "fc2t2_key_sort": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "fc2t2_insert": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -86,6 +101,8 @@ def _exc_for(code: int):
 def check(code: int, what: str = "") -> None:
     if code != OK:
         msg = lib().fc2t2_last_error().decode(errors="replace")
+        rmsg = lib().fc2t2_ray_last_error().decode(errors="replace")
+        msg = rmsg if rmsg and not msg else (msg + ("; " + rmsg if rmsg else ""))
         raise _exc_for(code)(f"{what}: {msg}" if what else msg)
 
 

@@ -13,6 +13,10 @@ cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order,
                       cudaStream_t s);
 cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,
                      cudaStream_t s);
+// stable sort of precomputed cell keys (key >= res^3 = "no cell", sorted last)
+size_t key_sort_workspace(int level, int64_t n);
+cudaError_t key_sort(int level, const uint32_t* keys, int64_t n, int32_t* order,
+                     int32_t* cell_start, void* ws, size_t ws_bytes, cudaStream_t s);
 size_t scan_ws_words(int64_t n);
 cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* ws,
                            cudaStream_t s);
@@ -72,4 +76,28 @@ cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64
                 const float* wts, float* value, float* grad, float* hess, float* wgrad,
                 int32_t* flag, cudaStream_t s);
 
+}  // namespace fc2t2
+
+// rays.cu -----------------------------------------------------------------
+namespace fc2t2 {
+cudaError_t traverse_count(int level, const double* org, const double* dir, int64_t R,
+                           uint32_t* counts, cudaStream_t s);
+cudaError_t traverse_fill(int level, const double* org, const double* dir, int64_t R,
+                          const uint32_t* offsets, int32_t* ray_id, double* t0, double* t1,
+                          int32_t* box, cudaStream_t s);
+cudaError_t depth_walk(int rho, int level, const float* L, const double* org, const double* dir,
+                       int64_t R, double bias, double* lengths, uint8_t* hit, double* points,
+                       float* grads, float* hess, float* denom, cudaStream_t s);
+cudaError_t root_payload(int rho, int level, const double* dir, int64_t R, const uint8_t* hit,
+                         const double* points, const float* grads, const float* hess,
+                         const float* denom, const float* y_len, const float* y_grad,
+                         uint32_t* keys, float* payload, int32_t* n_clamped, cudaStream_t s);
+cudaError_t line_integral(int rho, int level, int C, const float* L, const double* org,
+                          const double* dir, int64_t R, float* values, cudaStream_t s);
+cudaError_t line_payload(int rho, int level, int C, const double* org, const double* dir,
+                         int64_t R, const uint32_t* offsets, const float* y, const double* gl_x,
+                         const double* gl_w, int G, uint32_t* keys, float* payload,
+                         cudaStream_t s);
+cudaError_t insert_sorted(int rho, int level, int C, const float* payload, const int32_t* order,
+                          const int32_t* cell_start, float* M, cudaStream_t s);
 }  // namespace fc2t2

@@ -261,7 +261,7 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
   }
   __syncthreads();
   const int64_t tbase = (int64_t)blockIdx.x * RADIX_TILE;
-  const int cnt = (int)min<int64_t>(RADIX_TILE, n - tbase);
+  const int cnt = (int)((n - tbase) < RADIX_TILE ? (n - tbase) : RADIX_TILE);
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
     const uint32_t k = skey[i];
     const uint32_t d = (k >> shift) & mask;
@@ -291,11 +291,21 @@ size_t cell_sort_workspace(int level, int64_t n) {
   return b;
 }
 
-cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, int32_t* cell_start,
-                      int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s) {
-  const int res = 1 << (level + 1);
-  const int64_t R = (int64_t)res * res * res;
-  if (ws_bytes < cell_sort_workspace(level, n)) return cudaErrorInvalidValue;
+namespace {
+
+__global__ void keys_prep_kernel(const uint32_t* __restrict__ keys_in, int64_t n, int64_t R,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                 uint32_t* __restrict__ counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys_in[i];
+    keys[i] = k;
+    vals[i] = (uint32_t)i;
+    if ((int64_t)k < R) atomicAdd(&counts[k], 1u);  // keys >= R sort last, belong to no cell
+  }
+}
+
+SortWs carve(void* ws, int64_t n, int64_t R) {
   const int64_t nblocks = std::max<int64_t>(1, (n + RADIX_TILE - 1) / RADIX_TILE);
   char* p = (char*)ws;
   auto take = [&](size_t bytes) { char* q = p; p += align256(bytes); return (uint32_t*)q; };
@@ -307,18 +317,15 @@ cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, in
   w.hist = take(4 * (size_t)(256 * nblocks));
   w.scan = take(4 * std::max(scan_ws_words(256 * nblocks), scan_ws_words(R + 1)) + 4);
   w.counts = take(4 * (size_t)(R + 1));
+  return w;
+}
 
-  cudaError_t e = cudaMemsetAsync(w.counts, 0, 4 * (size_t)(R + 1), s);
-  if (e != cudaSuccess) return e;
-  if (n > 0)
-    FC2T2_LAUNCH("cell_keys", s,
-                 cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.vals,
-                                                                      w.counts, flag));
-  // cell ranges: exclusive scan of the per-cell counts (entry R = n)
-  e = exclusive_scan(w.counts, (uint32_t*)cell_start, R + 1, w.scan, s);
+// keys/vals/counts already prepared in w: cell ranges + LSD radix passes
+cudaError_t sort_prepared(SortWs& w, int64_t n, int key_bits, int64_t R, int32_t* order,
+                          int32_t* cell_start, cudaStream_t s) {
+  const int64_t nblocks = std::max<int64_t>(1, (n + RADIX_TILE - 1) / RADIX_TILE);
+  cudaError_t e = exclusive_scan(w.counts, (uint32_t*)cell_start, R + 1, w.scan, s);
   if (e != cudaSuccess || n == 0) return e != cudaSuccess ? e : cudaGetLastError();
-
-  const int key_bits = 3 * (level + 1);
   const int passes = (key_bits + 7) / 8;
   const int digit = (key_bits + passes - 1) / passes;
   uint32_t *kin = w.keys, *vin = w.vals;
@@ -340,6 +347,41 @@ cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, in
     vin = vout;
   }
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, int32_t* cell_start,
+                      int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int res = 1 << (level + 1);
+  const int64_t R = (int64_t)res * res * res;
+  if (ws_bytes < cell_sort_workspace(level, n)) return cudaErrorInvalidValue;
+  SortWs w = carve(ws, n, R);
+  cudaError_t e = cudaMemsetAsync(w.counts, 0, 4 * (size_t)(R + 1), s);
+  if (e != cudaSuccess) return e;
+  if (n > 0)
+    FC2T2_LAUNCH("cell_keys", s,
+                 cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.vals,
+                                                                      w.counts, flag));
+  return sort_prepared(w, n, 3 * (level + 1), R, order, cell_start, s);
+}
+
+size_t key_sort_workspace(int level, int64_t n) { return cell_sort_workspace(level, n); }
+
+cudaError_t key_sort(int level, const uint32_t* keys, int64_t n, int32_t* order,
+                     int32_t* cell_start, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int res = 1 << (level + 1);
+  const int64_t R = (int64_t)res * res * res;
+  if (ws_bytes < key_sort_workspace(level, n)) return cudaErrorInvalidValue;
+  SortWs w = carve(ws, n, R);
+  cudaError_t e = cudaMemsetAsync(w.counts, 0, 4 * (size_t)(R + 1), s);
+  if (e != cudaSuccess) return e;
+  if (n > 0)
+    FC2T2_LAUNCH("keys_prep", s,
+                 keys_prep_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(keys, n, R, w.keys, w.vals,
+                                                                      w.counts));
+  // one extra key bit so the out-of-grid sentinel R sorts after every cell
+  return sort_prepared(w, n, 3 * (level + 1) + 1, R, order, cell_start, s);
 }
 
 cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,

@@ -21,8 +21,11 @@ import numpy as np
 import torch
 
 from . import _lib
-from .expansion import (Accessor, Engine, HostIO, SourceSet, _host_domain_check,
-                        is_host_tensor, like_input, to_device)
+from .expansion import (Accessor, Engine, ExpansionGrid, HostIO, SourceSet, _host_domain_check,
+                        _ptr, _stream, is_host_tensor, like_input, to_device)
+from .kernel import level_resolution
+from .multiindex import ROOT_MAX_ORDER, OrderError
+from .ray import RayBundle, segment_offsets
 
 
 @dataclass
@@ -93,3 +96,208 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),
                           q_bar=like_input(q_bar, ref))
+
+
+# ---------------------------------------------------------------- insertion ---
+
+def insert_and_expand(engine: Engine, keys: torch.Tensor, payload: torch.Tensor,
+                      channels: int) -> Accessor:
+    """_insert_moments (reference layers.py:144-153): stable sort of the item
+    cell keys, per-cell sums of the payload rows in sorted order (no atomics,
+    deterministic), then one cascade -- the one extra expansion of a JVP."""
+    n = int(keys.shape[0])
+    lv = engine.levels
+    R3 = level_resolution(lv) ** 3
+    dev = keys.device
+    ws_b = int(_lib.lib().fc2t2_key_sort_workspace_size(lv, n))
+    ws = torch.empty(max(ws_b, 4), dtype=torch.uint8, device=dev)
+    order = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    start = torch.empty(R3 + 1, dtype=torch.int32, device=dev)
+    _lib.call("fc2t2_key_sort", lv, _ptr(keys), n, _ptr(order), _ptr(start), _ptr(ws), ws_b,
+              _stream())
+    m = engine._empty_grid(lv, channels, "M")
+    _lib.call("fc2t2_insert", engine.rho, lv, channels, _ptr(payload), _ptr(order), _ptr(start),
+              _ptr(m.storage), _stream())
+    out = engine.cascade_device(m.storage)
+    grid = ExpansionGrid(level=lv, kind="L", storage=out, rho=engine.rho)
+    return Accessor(grid, engine.table, engine.flops, flag=engine.flag)
+
+
+def _source_adjoints(back: Accessor, sources: SourceSet):
+    """w_bar = B(p), p_bar = sum_c w_c grad B_c(p) (reference layers.py:8-12)."""
+    out = back.eval_device(sources.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=sources.w)
+    return out["value"], out["wgrad"]
+
+
+def _like(t: torch.Tensor, ref):
+    if isinstance(ref, torch.Tensor):
+        return t if ref.is_cuda else t.cpu()
+    a = t.detach().cpu().numpy()
+    return a.astype(np.float64) if a.dtype != np.bool_ else a
+
+
+def _tangent(y, n: int, cols: int) -> torch.Tensor:
+    t = to_device(y).reshape(n, cols) if cols > 1 else to_device(y).reshape(n)
+    return t.contiguous()
+
+
+# ------------------------------------------------------------ root layers ---
+
+@dataclass
+class RootResult:
+    """Reference layers.py:193-205; device tensors kept in ``dev`` for the JVPs."""
+
+    lengths: object
+    hit: object
+    points: object
+    grads: object
+    denom: object
+    accessor: Accessor
+    bundle: RayBundle
+    sources: SourceSet
+    engine: Engine
+    bias: float
+    diagnostics: dict
+    dev: dict = field(default_factory=dict, repr=False)
+
+
+def depth_forward(engine: Engine, sources: SourceSet, bundle: RayBundle, bias: float = 0.05,
+                  trav=None) -> RootResult:
+    """First root of f = sum w psi + bias along each ray (reference layers.py:244-272):
+    one expansion, then one fused walker per ray (traversal, line2poly, 5-sample
+    screen, closed-form roots, hit point, gradient and Hessian at the hit)."""
+    if sources.channels != 1:
+        raise ValueError("root layers expect a single-channel field")
+    if engine.rho > ROOT_MAX_ORDER:
+        raise OrderError(f"root layers need rho <= {ROOT_MAX_ORDER}")
+    acc = engine.expand_device(sources.p, sources.w)
+    org, dirs = bundle.dev()
+    R = bundle.count
+    dev = org.device
+    lengths = torch.empty(R, dtype=torch.float64, device=dev)
+    hit = torch.empty(R, dtype=torch.uint8, device=dev)
+    points = torch.empty((R, 3), dtype=torch.float64, device=dev)
+    grads = torch.empty((R, 3), dtype=torch.float32, device=dev)
+    hess = torch.empty((R, 6), dtype=torch.float32, device=dev)
+    denom = torch.empty(R, dtype=torch.float32, device=dev)
+    st = acc.grid.storage
+    _lib.call("fc2t2_depth_forward", engine.rho, engine.levels, _ptr(st), _ptr(org), _ptr(dirs), R,
+              float(bias), _ptr(lengths), _ptr(hit), _ptr(points), _ptr(grads), _ptr(hess),
+              _ptr(denom), _stream())
+    engine.flag.raise_if_set("source")
+    hitb = hit.bool()
+    ref = bundle.origins
+    diag = {"dead_pixels": int((~hitb).sum().item()), "ift_clamped": 0}
+    return RootResult(lengths=_like(lengths, ref), hit=_like(hitb, ref), points=_like(points, ref),
+                      grads=_like(grads, ref), denom=_like(denom, ref), accessor=acc,
+                      bundle=bundle, sources=sources, engine=engine, bias=bias,
+                      diagnostics=diag,
+                      dev={"hit": hit, "points": points, "grads": grads, "hess": hess,
+                           "denom": denom, "n_hit": R - diag["dead_pixels"]})
+
+
+def _root_jvp(res: RootResult, y_len, y_grad) -> LayerGradients:
+    eng, src, R = res.engine, res.sources, res.bundle.count
+    grads = LayerGradients(w_bar=None, p_bar=None, diagnostics=dict(res.diagnostics))
+    ref = y_len if y_len is not None else y_grad
+    if res.dev["n_hit"] == 0:
+        z = torch.zeros_like(src.w)
+        grads.w_bar, grads.p_bar = _like(z, ref), _like(torch.zeros_like(src.p), ref)
+        return grads
+    yl = _tangent(y_len, R, 1) if y_len is not None else None
+    yg = _tangent(y_grad, R, 3) if y_grad is not None else None
+    PP = eng.PP
+    keys = torch.empty(R, dtype=torch.int32, device=src.p.device)
+    payload = torch.empty((R, 1, PP), dtype=torch.float32, device=src.p.device)
+    nclamp = torch.zeros(1, dtype=torch.int32, device=src.p.device)
+    d = res.dev
+    _, dirs = res.bundle.dev()
+    _lib.call("fc2t2_root_payload", eng.rho, eng.levels, _ptr(dirs), R, _ptr(d["hit"]),
+              _ptr(d["points"]), _ptr(d["grads"]), _ptr(d["hess"]), _ptr(d["denom"]),
+              _ptr(yl), _ptr(yg), _ptr(keys), _ptr(payload), _ptr(nclamp), _stream())
+    back = insert_and_expand(eng, keys, payload, 1)
+    w_bar, p_bar = _source_adjoints(back, src)
+    eng.flag.raise_if_set("source")
+    grads.diagnostics["ift_clamped"] = int(nclamp.item())
+    grads.w_bar, grads.p_bar = _like(w_bar, ref), _like(p_bar, ref)
+    return grads
+
+
+def depth_jvp(y_bar, res: RootResult) -> LayerGradients:
+    """Ray-length adjoints via the IFT projection (reference layers.py:285-303)."""
+    return _root_jvp(res, y_bar, None)
+
+
+def surface_gradient_forward(engine: Engine, sources: SourceSet, bundle: RayBundle,
+                             bias: float = 0.05, trav=None) -> RootResult:
+    """Same roots; the output is grad f at the hit (reference layers.py:306-310)."""
+    return depth_forward(engine, sources, bundle, bias=bias, trav=trav)
+
+
+def surface_gradient_jvp(y_bar, res: RootResult) -> LayerGradients:
+    """Monopole mu = -sum y_i kappa_i plus dipoles y_a, one expansion
+    (reference layers.py:313-356)."""
+    return _root_jvp(res, None, y_bar)
+
+
+def depth_surface_jvp(y_len, y_grad, res: RootResult) -> LayerGradients:
+    """depth_jvp + surface_gradient_jvp in ONE insertion and one expansion
+    (the payloads add)."""
+    return _root_jvp(res, y_len, y_grad)
+
+
+# -------------------------------------------------------- integral layers ---
+
+@dataclass
+class IntegralResult:
+    """Reference layers.py:361-368."""
+
+    values: object
+    accessor: Accessor
+    trav: object
+    bundle: RayBundle
+    sources: SourceSet
+    engine: Engine
+
+
+def line_integral_forward(engine: Engine, sources: SourceSet, bundle: RayBundle,
+                          trav=None) -> IntegralResult:
+    """Exact integral of the field along every ray (reference layers.py:371-386)."""
+    acc = engine.expand_device(sources.p, sources.w)
+    org, dirs = bundle.dev()
+    R, C = bundle.count, sources.channels
+    vals = torch.empty((R, C), dtype=torch.float32, device=org.device)
+    _lib.call("fc2t2_line_integral", engine.rho, engine.levels, C, _ptr(acc.grid.storage),
+              _ptr(org), _ptr(dirs), R, _ptr(vals), _stream())
+    engine.flag.raise_if_set("source")
+    return IntegralResult(values=_like(vals, bundle.origins), accessor=acc, trav=trav,
+                          bundle=bundle, sources=sources, engine=engine)
+
+
+_GAUSS: dict = {}
+
+
+def _gauss_dev(G: int, dev):
+    if G not in _GAUSS:
+        x, w = np.polynomial.legendre.leggauss(G)
+        _GAUSS[G] = (torch.from_numpy(x).to(dev), torch.from_numpy(w).to(dev))
+    return _GAUSS[G]
+
+
+def line_integral_jvp(y_bar, res: IntegralResult) -> LayerGradients:
+    """Closed-form weighted-segment insertion, one expansion (reference layers.py:389-402)."""
+    eng, src, bundle = res.engine, res.sources, res.bundle
+    org, dirs = bundle.dev()
+    R, C = bundle.count, src.channels
+    yb = to_device(y_bar).reshape(R, C).contiguous()
+    offs, S = segment_offsets(bundle, eng.levels)
+    G = eng.rho // 2 + 1
+    gx, gw = _gauss_dev(G, org.device)
+    keys = torch.empty(max(S, 1), dtype=torch.int32, device=org.device)
+    payload = torch.empty((max(S, 1), C, eng.PP), dtype=torch.float32, device=org.device)
+    _lib.call("fc2t2_line_payload", eng.rho, eng.levels, C, _ptr(org), _ptr(dirs), R, _ptr(offs),
+              _ptr(yb), _ptr(gx), _ptr(gw), G, _ptr(keys), _ptr(payload), _stream())
+    back = insert_and_expand(eng, keys[:S], payload[:S], C)
+    w_bar, p_bar = _source_adjoints(back, src)
+    eng.flag.raise_if_set("source")
+    return LayerGradients(w_bar=_like(w_bar, y_bar), p_bar=_like(p_bar, y_bar))

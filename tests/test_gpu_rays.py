@@ -1,0 +1,145 @@
+"""GPU parity of traversal and the root-implicit / line-integral layers.
+
+Checkers: golden vectors from the reference (tests/golden/make_golden_rays.py)
+and the pinned CPU oracle (oracle/rays.py).  Box lists and hit masks are
+integer outputs (bit-exact / mismatch counts); floats rel-L2 against the
+float64 reference on identical float32 inputs.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle.fc2t2_oracle import Oracle, rel_l2
+from oracle.rays import camera_rays, traverse as ora_traverse
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def small():
+    return golden("rays_small")
+
+
+@pytest.fixture(scope="module")
+def eng3(cuda):
+    from paper_2111_00110_b200 import Engine, KernelModel
+    return Engine(KernelModel("gaussian", 50.0, 4), 3, check_admissibility=False)
+
+
+def _bundle(g):
+    from paper_2111_00110_b200.ray import RayBundle
+    return RayBundle(g["origins"], g["directions"])
+
+
+def test_traverse_bit_exact_vs_reference(small, cuda):
+    from paper_2111_00110_b200.ray import traverse
+    tr = traverse(_bundle(small), 3)
+    assert np.array_equal(tr.ray_id.cpu().numpy(), small["ray_id"])
+    assert np.array_equal(tr.box.cpu().numpy(), small["box"])
+    assert np.array_equal(tr.t0.cpu().numpy(), small["t0"])
+    assert np.array_equal(tr.t1.cpu().numpy(), small["t1"])
+    assert np.array_equal(tr.offsets.cpu().numpy(), small["offsets"])
+
+
+def test_traverse_bit_exact_config3_camera(cuda):
+    """Config-3 geometry at level 5 (radius 2, fov 60), 128x128 rays, vs the oracle."""
+    from paper_2111_00110_b200.ray import RayBundle, traverse
+    rng = np.random.default_rng(3)
+    u = rng.normal(size=3)
+    u /= np.linalg.norm(u)
+    o, d = camera_rays(2.0 * u, np.zeros(3), np.array([0.0, 1.0, 0.0]), 60.0, 128, 128)
+    # add axis-parallel and grazing rays
+    o = np.concatenate([o, [[-3.0, 0.001, 0.001], [0.3, -2.0, 0.5], [0.5, 0.5, -3.0]]])
+    d = np.concatenate([d, [[1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]]])
+    ref = ora_traverse(o, d, 5)
+    tr = traverse(RayBundle(o, d), 5)
+    for k in ("ray_id", "box", "t0", "t1", "offsets"):
+        assert np.array_equal(getattr(tr, k).cpu().numpy(), ref[k]), k
+
+
+def test_depth_forward_matches_reference(small, eng3):
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import depth_forward
+    res = depth_forward(eng3, SourceSet(small["p"], small["w"]), _bundle(small), bias=0.3)
+    assert np.array_equal(res.hit, small["hit"])
+    h = res.hit
+    assert rel_l2(res.lengths[h], small["lengths"][h]) < TOL
+    assert rel_l2(res.grads, small["grads"]) < TOL
+    assert rel_l2(res.denom, small["denom"]) < TOL
+    assert np.all(np.isnan(res.lengths[~h]))
+    assert res.diagnostics["dead_pixels"] == int((~h).sum())
+
+
+def test_root_jvps_match_reference(small, eng3):
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import (depth_forward, depth_jvp, depth_surface_jvp,
+                                              surface_gradient_jvp)
+    res = depth_forward(eng3, SourceSet(small["p"], small["w"]), _bundle(small), bias=0.3)
+    n0 = eng3.expansion_count
+    gd = depth_jvp(small["y_len"], res)
+    assert eng3.expansion_count == n0 + 1
+    assert rel_l2(gd.w_bar, small["depth_w_bar"]) < TOL
+    assert rel_l2(gd.p_bar, small["depth_p_bar"]) < TOL
+    gs = surface_gradient_jvp(small["y_grad"], res)
+    assert rel_l2(gs.w_bar, small["surf_w_bar"]) < TOL
+    assert rel_l2(gs.p_bar, small["surf_p_bar"]) < TOL
+    gf = depth_surface_jvp(small["y_len"], small["y_grad"], res)
+    assert rel_l2(gf.w_bar, small["depth_w_bar"] + small["surf_w_bar"]) < TOL
+    assert rel_l2(gf.p_bar, small["depth_p_bar"] + small["surf_p_bar"]) < TOL
+
+
+def test_depth_invariants(small, eng3):
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import depth_forward, depth_jvp
+    b = _bundle(small)
+    s = SourceSet(small["p"], small["w"])
+    dead = depth_forward(eng3, s, b, bias=-0.2)
+    assert not dead.hit.any() and dead.diagnostics["dead_pixels"] == b.count
+    a = depth_forward(eng3, s, b, bias=0.3)
+    c = depth_forward(eng3, SourceSet(small["p"], 3.0 * small["w"]), b, bias=0.9)
+    assert np.array_equal(a.hit, c.hit)
+    assert np.allclose(a.lengths[a.hit], c.lengths[c.hit], atol=1e-6)
+    z = depth_jvp(np.zeros(b.count), a)
+    assert not np.any(z.w_bar) and not np.any(z.p_bar)
+    # hit points re-evaluate to ~0 (acceptance criterion 3)
+    f = a.accessor.value(a.points[a.hit])[:, 0] + 0.3
+    assert np.max(np.abs(f)) < 1e-5
+
+
+def test_config3_small_matches_reference(cuda):
+    """Config-3 geometry at level 5 (reduced N and camera; golden from the reference)."""
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
+    from paper_2111_00110_b200.layers import depth_forward, depth_jvp, surface_gradient_jvp
+    g = golden("rays_cfg3")
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    res = depth_forward(eng, SourceSet(g["p"], g["w"]), _bundle(g), bias=float(g["bias"]))
+    mism = int((res.hit != g["hit"]).sum())
+    assert mism <= max(2, int(0.002 * g["hit"].size)), mism
+    both = res.hit & g["hit"]
+    assert rel_l2(res.lengths[both], g["lengths"][both]) < TOL
+    assert rel_l2(res.grads[both], g["grads"][both]) < TOL
+    if mism == 0:
+        gd = depth_jvp(g["y_len"], res)
+        assert rel_l2(gd.w_bar, g["depth_w_bar"]) < TOL
+        assert rel_l2(gd.p_bar, g["depth_p_bar"]) < TOL
+        gs = surface_gradient_jvp(g["y_grad"], res)
+        assert rel_l2(gs.w_bar, g["surf_w_bar"]) < TOL
+        assert rel_l2(gs.p_bar, g["surf_p_bar"]) < TOL
+
+
+def test_line_integral_matches_reference(small, eng3):
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import line_integral_forward, line_integral_jvp
+    res = line_integral_forward(eng3, SourceSet(small["p"], small["w"]), _bundle(small))
+    assert rel_l2(res.values, small["li_values"]) < TOL
+    n0 = eng3.expansion_count
+    g = line_integral_jvp(small["y_li"], res)
+    assert eng3.expansion_count == n0 + 1
+    assert rel_l2(g.w_bar, small["li_w_bar"]) < TOL
+    assert rel_l2(g.p_bar, small["li_p_bar"]) < TOL
+    res2 = line_integral_forward(eng3, SourceSet(small["p"], 2.5 * small["w"]), _bundle(small))
+    assert rel_l2(res2.values, 2.5 * res.values) < 1e-6
