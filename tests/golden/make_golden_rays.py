@@ -137,7 +137,21 @@ def part_cfg3_small():
     gd = depth_jvp(yl, res)
     gs = surface_gradient_jvp(yg, res)
     print(f"    cfg3 small: {time.time() - t0:.1f}s, hit fraction {res.hit.mean():.3f}")
+    # conditioning floor: the reference's own change under a 2^-24 relative
+    # perturbation of the weights (the IFT weights -y/<r, grad f> are large and
+    # of both signs, so w_bar = sum_r u_r psi(p - x_r) cancels)
+    pr = np.random.default_rng(0)
+    wp = w * (1 + pr.normal(size=w.shape) * 2.0 ** -24)
+    rp = depth_forward(eng, SourceSet(p, wp), b, bias=0.05)
+    dp, sp = depth_jvp(yl, rp), surface_gradient_jvp(yg, rp)
+
+    def rl(a, c):
+        return float(np.linalg.norm(a - c) / np.linalg.norm(c))
+    sens = np.array([rl(dp.w_bar, gd.w_bar), rl(dp.p_bar, gd.p_bar), rl(sp.w_bar, gs.w_bar),
+                     rl(sp.p_bar, gs.p_bar)])
+    print(f"    self-sensitivity (depth w,p / surface w,p): {sens}")
     save("rays_cfg3", p=p, w=w, origins=b.origins, directions=b.directions, bias=0.05,
+         sensitivity=sens,
          n_segments=res.hit.size, lengths=res.lengths, hit=res.hit, grads=res.grads,
          denom=res.denom, y_len=yl, y_grad=yg, depth_w_bar=gd.w_bar, depth_p_bar=gd.p_bar,
          surf_w_bar=gs.w_bar, surf_p_bar=gs.p_bar)

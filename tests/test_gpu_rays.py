@@ -123,12 +123,19 @@ def test_config3_small_matches_reference(cuda):
     assert rel_l2(res.lengths[both], g["lengths"][both]) < TOL
     assert rel_l2(res.grads[both], g["grads"][both]) < TOL
     if mism == 0:
+        # The root-layer adjoints are ill-conditioned: the IFT weights
+        # -y/<r, grad f> are large and of both signs and w_bar sums them with
+        # cancellation.  The reference itself moves by `sensitivity` (~2.3e-5)
+        # when the weights are perturbed by 2^-24 relative (stored in the
+        # golden file).  Tolerance: 25x that floor -- our float32 field carries
+        # ~1e-6 relative error, ~16x a 2^-24 perturbation.
+        sens = g["sensitivity"]
         gd = depth_jvp(g["y_len"], res)
-        assert rel_l2(gd.w_bar, g["depth_w_bar"]) < TOL
-        assert rel_l2(gd.p_bar, g["depth_p_bar"]) < TOL
+        assert rel_l2(gd.w_bar, g["depth_w_bar"]) < 25 * sens[0]
+        assert rel_l2(gd.p_bar, g["depth_p_bar"]) < 25 * sens[1]
         gs = surface_gradient_jvp(g["y_grad"], res)
-        assert rel_l2(gs.w_bar, g["surf_w_bar"]) < TOL
-        assert rel_l2(gs.p_bar, g["surf_p_bar"]) < TOL
+        assert rel_l2(gs.w_bar, g["surf_w_bar"]) < 25 * sens[2]
+        assert rel_l2(gs.p_bar, g["surf_p_bar"]) < 25 * sens[3]
 
 
 def test_line_integral_matches_reference(small, eng3):
