@@ -161,6 +161,27 @@ int fc2t2_key_sort(int level, const uint32_t* d_keys, int64_t n, int32_t* d_orde
 int fc2t2_insert(int rho, int level, int channels, const float* d_payload, const int32_t* d_order,
                  const int32_t* d_cell_start, float* d_m, void* stream);
 
+/* ---- integral-implicit radiance layer (layers.py:405-544), rho = 4 ----
+ * grid channels = 1 (density, relu'd weights) + colors; efit = the 5
+ * coefficients of the exp(-x) fit (poly1d.py:224-242), bg (colors,).
+ * forward: rgb (R, colors), depth_final (R) float64, optional per-segment
+ * alive flags (with traversal offsets).  backward: pass A (alive counts,
+ * totals (R, colors) float64, depth_final), exclusive scan of the counts,
+ * pass B (keys + (n_alive, 1+colors, PP) payload rows) -> fc2t2_insert. */
+int fc2t2_vol_gauss_nodes(int rho);
+int fc2t2_vol_forward(int rho, int level, int colors, const float* d_l, const double* d_org,
+                      const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
+                      float* d_rgb, double* d_depth_final, const uint32_t* d_seg_offsets,
+                      uint8_t* d_seg_alive, void* stream);
+int fc2t2_vol_totals(int rho, int level, int colors, const float* d_l, const double* d_org,
+                     const double* d_dir, int64_t R, const double* d_efit, uint32_t* d_n_alive,
+                     double* d_totals, double* d_depth_final, void* stream);
+int fc2t2_vol_payload(int rho, int level, int colors, const float* d_l, const double* d_org,
+                      const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
+                      const float* d_ybar, const uint32_t* d_alive_offsets,
+                      const double* d_totals, const double* d_depth_final, const double* d_gl_x,
+                      const double* d_gl_w, uint32_t* d_keys, float* d_payload, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,4 +113,41 @@ int fc2t2_insert(int rho, int level, int channels, const float* d_payload, const
                  "insert");
 }
 
+int fc2t2_vol_gauss_nodes(int rho) { return fc2t2::vol_gauss_nodes(rho); }
+
+int fc2t2_vol_forward(int rho, int level, int colors, const float* d_l, const double* d_org,
+                      const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
+                      float* d_rgb, double* d_depth_final, const uint32_t* d_seg_offsets,
+                      uint8_t* d_seg_alive, void* stream) {
+  if (rho != 4) return rfail(FC2T2_EORDER, "the radiance layer is built for rho = 4");
+  if (colors < 1 || colors > 4) return rfail(FC2T2_EVALUE, "1..4 colour channels supported");
+  return rstatus(fc2t2::vol_forward(rho, level, colors, d_l, d_org, d_dir, R, d_efit, d_bg, d_rgb,
+                                    d_depth_final, d_seg_offsets, d_seg_alive,
+                                    (cudaStream_t)stream),
+                 "vol_forward");
+}
+
+int fc2t2_vol_totals(int rho, int level, int colors, const float* d_l, const double* d_org,
+                     const double* d_dir, int64_t R, const double* d_efit, uint32_t* d_n_alive,
+                     double* d_totals, double* d_depth_final, void* stream) {
+  if (rho != 4) return rfail(FC2T2_EORDER, "the radiance layer is built for rho = 4");
+  if (colors < 1 || colors > 4) return rfail(FC2T2_EVALUE, "1..4 colour channels supported");
+  return rstatus(fc2t2::vol_totals(rho, level, colors, d_l, d_org, d_dir, R, d_efit, d_n_alive,
+                                   d_totals, d_depth_final, (cudaStream_t)stream),
+                 "vol_totals");
+}
+
+int fc2t2_vol_payload(int rho, int level, int colors, const float* d_l, const double* d_org,
+                      const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
+                      const float* d_ybar, const uint32_t* d_alive_offsets,
+                      const double* d_totals, const double* d_depth_final, const double* d_gl_x,
+                      const double* d_gl_w, uint32_t* d_keys, float* d_payload, void* stream) {
+  if (rho != 4) return rfail(FC2T2_EORDER, "the radiance layer is built for rho = 4");
+  if (colors < 1 || colors > 4) return rfail(FC2T2_EVALUE, "1..4 colour channels supported");
+  return rstatus(fc2t2::vol_payload(rho, level, colors, d_l, d_org, d_dir, R, d_efit, d_bg,
+                                    d_ybar, d_alive_offsets, d_totals, d_depth_final, d_gl_x,
+                                    d_gl_w, d_keys, d_payload, (cudaStream_t)stream),
+                 "vol_payload");
+}
+
 }  // extern "C"

@@ -101,3 +101,20 @@ cudaError_t line_payload(int rho, int level, int C, const double* org, const dou
 cudaError_t insert_sorted(int rho, int level, int C, const float* payload, const int32_t* order,
                           const int32_t* cell_start, float* M, cudaStream_t s);
 }  // namespace fc2t2
+
+// volume.cu ---------------------------------------------------------------
+namespace fc2t2 {
+int vol_gauss_nodes(int rho);
+cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double* org,
+                        const double* dir, int64_t R, const double* efit, const double* bg,
+                        float* rgb, double* depth_final, const uint32_t* seg_offsets,
+                        uint8_t* seg_alive, cudaStream_t s);
+cudaError_t vol_totals(int rho, int level, int CC, const float* L, const double* org,
+                       const double* dir, int64_t R, const double* efit, uint32_t* n_alive,
+                       double* totals, double* depth_final, cudaStream_t s);
+cudaError_t vol_payload(int rho, int level, int CC, const float* L, const double* org,
+                        const double* dir, int64_t R, const double* efit, const double* bg,
+                        const float* ybar, const uint32_t* alive_offsets, const double* totals,
+                        const double* depth_final, const double* gl_x, const double* gl_w,
+                        uint32_t* keys, float* payload, cudaStream_t s);
+}  // namespace fc2t2

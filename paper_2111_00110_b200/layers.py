@@ -301,3 +301,121 @@ def line_integral_jvp(y_bar, res: IntegralResult) -> LayerGradients:
     w_bar, p_bar = _source_adjoints(back, src)
     eng.flag.raise_if_set("source")
     return LayerGradients(w_bar=_like(w_bar, y_bar), p_bar=_like(p_bar, y_bar))
+
+
+# ------------------------------------------------------------ radiance layer ---
+
+EXP_CUTOFF = 4.5      # reference poly1d.py:22
+EXP_FIT_RANGE = 5.0   # reference poly1d.py:23
+
+
+def fit_exp_poly() -> np.ndarray:
+    """Degree-4 fit of exp(-x) over 64 Chebyshev nodes on [0, 5] with the value
+    1 at 0 (reference poly1d.py:224-242); host constant."""
+    k = np.arange(64)
+    x = 2.5 + 2.5 * np.cos((2 * k + 1) * np.pi / 128)
+    V = x[:, None] ** np.arange(1, 5)[None, :]
+    tail, *_ = np.linalg.lstsq(V, np.exp(-x) - 1.0, rcond=None)
+    return np.concatenate([[1.0], tail])
+
+
+@dataclass
+class RenderResult:
+    """Reference layers.py:405-424.  The per-segment caches of the reference
+    (sigma/colour/transmittance polynomials, depth0, anti) are recomputed by the
+    backward walker instead of stored; ``alive`` is materialised on access."""
+
+    rgb: object
+    accessor: Accessor
+    trav: object
+    bundle: RayBundle
+    p: object
+    w_sigma: object
+    w_color: object
+    background: object
+    engine: Engine
+    depth_final: object = None
+    dev: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def alive(self):
+        """Per-segment alive flags in traversal order (depth0 <= 4.5, layers.py:453)."""
+        if "alive" not in self.dev:
+            eng, b = self.engine, self.bundle
+            org, dirs = b.dev()
+            offs, S = segment_offsets(b, eng.levels)
+            flags = torch.empty(max(S, 1), dtype=torch.uint8, device=org.device)
+            rgb = torch.empty((b.count, self.dev["colors"]), dtype=torch.float32, device=org.device)
+            dfin = torch.empty(b.count, dtype=torch.float64, device=org.device)
+            _lib.call("fc2t2_vol_forward", eng.rho, eng.levels, self.dev["colors"],
+                      _ptr(self.accessor.grid.storage), _ptr(org), _ptr(dirs), b.count,
+                      _ptr(self.dev["efit"]), _ptr(self.dev["bg"]), _ptr(rgb), _ptr(dfin),
+                      _ptr(offs), _ptr(flags), _stream())
+            self.dev["alive"] = flags[:S].bool()
+        return _like(self.dev["alive"], self.bundle.origins)
+
+
+def volumetric_forward(engine: Engine, p, w_sigma, w_color, bundle: RayBundle, background,
+                       trav=None) -> RenderResult:
+    """Emission/absorption rendering with closed-form per-segment algebra
+    (reference layers.py:427-480): relu'd density weights, one 1+C channel
+    expansion, then one walker thread per ray."""
+    ws = to_device(w_sigma).reshape(-1, 1)
+    wc = to_device(w_color)
+    wc = wc.reshape(ws.shape[0], -1)
+    C = int(wc.shape[1])
+    src = SourceSet(p, torch.cat([ws.clamp(min=0.0), wc], dim=1))
+    acc = engine.expand_device(src.p, src.w)
+    org, dirs = bundle.dev()
+    R = bundle.count
+    efit = torch.from_numpy(fit_exp_poly()).to(org.device)
+    bg = torch.as_tensor(np.asarray(background, dtype=np.float64) if not isinstance(
+        background, torch.Tensor) else background, dtype=torch.float64).to(org.device).reshape(-1)
+    rgb = torch.empty((R, C), dtype=torch.float32, device=org.device)
+    dfin = torch.empty(R, dtype=torch.float64, device=org.device)
+    _lib.call("fc2t2_vol_forward", engine.rho, engine.levels, C, _ptr(acc.grid.storage),
+              _ptr(org), _ptr(dirs), R, _ptr(efit), _ptr(bg), _ptr(rgb), _ptr(dfin), _ptr(None),
+              _ptr(None), _stream())
+    engine.flag.raise_if_set("source")
+    ref = bundle.origins
+    return RenderResult(rgb=_like(rgb, ref), accessor=acc, trav=trav, bundle=bundle, p=p,
+                        w_sigma=w_sigma, w_color=w_color, background=background, engine=engine,
+                        depth_final=_like(dfin, ref),
+                        dev={"src": src, "ws": ws, "colors": C, "efit": efit, "bg": bg})
+
+
+def volumetric_jvp(y_bar, res: RenderResult) -> LayerGradients:
+    """Adjoint rendering via weighted-segment insertion, one expansion
+    (reference layers.py:483-544).  Uses E' of the fitted quartic, so the JVP
+    is exact for the implemented forward."""
+    eng, b = res.engine, res.bundle
+    org, dirs = b.dev()
+    R, C = b.count, res.dev["colors"]
+    dev = org.device
+    yb = to_device(y_bar).reshape(R, C).contiguous()
+    st = res.accessor.grid.storage
+    n_alive = torch.zeros(R + 1, dtype=torch.int32, device=dev)
+    totals = torch.empty((R, C), dtype=torch.float64, device=dev)
+    dfin = torch.empty(R, dtype=torch.float64, device=dev)
+    efit, bg = res.dev["efit"], res.dev["bg"]
+    _lib.call("fc2t2_vol_totals", eng.rho, eng.levels, C, _ptr(st), _ptr(org), _ptr(dirs), R,
+              _ptr(efit), _ptr(n_alive), _ptr(totals), _ptr(dfin), _stream())
+    offs = torch.empty_like(n_alive)
+    ws_b = int(_lib.lib().fc2t2_scan_workspace_size(R + 1))
+    wsp = torch.empty(max(ws_b, 4), dtype=torch.uint8, device=dev)
+    _lib.call("fc2t2_scan_u32", _ptr(n_alive), _ptr(offs), R + 1, _ptr(wsp), ws_b, _stream())
+    A = int(offs[R].item())
+    G = int(_lib.lib().fc2t2_vol_gauss_nodes(eng.rho))
+    gx, gw = _gauss_dev(G, dev)
+    keys = torch.empty(max(A, 1), dtype=torch.int32, device=dev)
+    payload = torch.empty((max(A, 1), 1 + C, eng.PP), dtype=torch.float32, device=dev)
+    _lib.call("fc2t2_vol_payload", eng.rho, eng.levels, C, _ptr(st), _ptr(org), _ptr(dirs), R,
+              _ptr(efit), _ptr(bg), _ptr(yb), _ptr(offs), _ptr(totals), _ptr(dfin), _ptr(gx),
+              _ptr(gw), _ptr(keys), _ptr(payload), _stream())
+    back = insert_and_expand(eng, keys[:A], payload[:A], 1 + C)
+    src = res.dev["src"]
+    val, p_bar = _source_adjoints(back, src)
+    w_bar = val.clone()
+    w_bar[:, 0] = torch.where(res.dev["ws"][:, 0] > 0.0, val[:, 0], torch.zeros_like(val[:, 0]))
+    eng.flag.raise_if_set("source")
+    return LayerGradients(w_bar=_like(w_bar, y_bar), p_bar=_like(p_bar, y_bar))

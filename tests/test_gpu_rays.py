@@ -150,3 +150,39 @@ def test_line_integral_matches_reference(small, eng3):
     assert rel_l2(g.p_bar, small["li_p_bar"]) < TOL
     res2 = line_integral_forward(eng3, SourceSet(small["p"], 2.5 * small["w"]), _bundle(small))
     assert rel_l2(res2.values, 2.5 * res.values) < 1e-6
+
+
+def test_volumetric_matches_reference(small, eng3):
+    from paper_2111_00110_b200.layers import volumetric_forward, volumetric_jvp
+    res = volumetric_forward(eng3, small["p"], small["w_sigma"], small["w_color"], _bundle(small),
+                             small["bg"])
+    assert rel_l2(res.rgb, small["rgb"]) < TOL
+    assert np.array_equal(res.alive, small["alive"])
+    n0 = eng3.expansion_count
+    g = volumetric_jvp(small["y_vol"], res)
+    assert eng3.expansion_count == n0 + 1
+    assert rel_l2(g.w_bar, small["vol_w_bar"]) < TOL
+    assert rel_l2(g.p_bar, small["vol_p_bar"]) < TOL
+    # relu mask: clipped density weights get no density gradient (test_layers.py:266-272)
+    neg = small["w_sigma"][:, 0] <= 0
+    assert not np.any(g.w_bar[neg, 0])
+
+
+def test_volumetric_zero_density_is_background(small, eng3):
+    from paper_2111_00110_b200.layers import volumetric_forward
+    res = volumetric_forward(eng3, small["p"], np.zeros_like(small["w_sigma"]), small["w_color"],
+                             _bundle(small), small["bg"])
+    assert np.allclose(res.rgb, np.broadcast_to(small["bg"], res.rgb.shape), atol=1e-7)
+
+
+def test_volumetric_config4_small_matches_reference(cuda):
+    """Config-4 geometry (level 5, 3 colours, radius 2.5, fov 50), reduced N and rays."""
+    from paper_2111_00110_b200 import Engine, KernelModel
+    from paper_2111_00110_b200.layers import volumetric_forward, volumetric_jvp
+    g = golden("rays_cfg4")
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    res = volumetric_forward(eng, g["p"], g["w_sigma"], g["w_color"], _bundle(g), g["bg"])
+    assert rel_l2(res.rgb, g["rgb"]) < TOL
+    gr = volumetric_jvp(g["y"], res)
+    assert rel_l2(gr.w_bar, g["w_bar"]) < TOL
+    assert rel_l2(gr.p_bar, g["p_bar"]) < TOL
