@@ -18,9 +18,14 @@ Gaussian alpha = 1000 (reference default kernel, DEFAULT_ALPHA[5]).
   cpu_baseline / --impl reference  the oracle port (float64 NumPy restatement
          of the reference, all host threads for BLAS) on a bounded sample.
 
-Multi-GPU (torchrun): every rank runs its own copy of the per-GPU workload
-(weak scaling, replicas -- see DESIGN.md section 6); timing is the max over
-ranks of the device time.
+Multi-GPU (torchrun): weak scaling -- every rank owns a per-GPU shard of
+config-2 size of one global problem; the finest moment grids are summed with
+one NCCL all-reduce per expansion (paper_2111_00110_b200/parallel.py); timing
+is the max over ranks of the device time.
+
+Secondary lines (rank 0, single GPU): configs 1, 3 and 4 (explicit 2D-lifted,
+root-implicit depth+normal, radiance) are measured in the same run and
+reported under "secondary" with their own metrics (points/s, rays/s).
 """
 
 from __future__ import annotations
@@ -49,11 +54,12 @@ WORKLOAD = ("cfg2 explicit layer fwd+bwd (w, p, q adjoints): N=2^20 sources, M=1
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--small", action="store_true", help="reduced sizes for a quick check")
+    ap.add_argument("--no-secondary", action="store_true", help="skip configs 1, 3, 4")
     return ap.parse_args()
 
 
@@ -87,7 +93,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -189,6 +195,113 @@ def run_reference(args, rank: int) -> None:
 
 # ------------------------------------------------------------- GPU arm ---
 
+def seeded_direction(rng):
+    """Unit vector, rejecting near-vertical ones (SURVEY 8(d) camera rule)."""
+    while True:
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        if abs(u[1]) <= 0.99:
+            return u
+
+
+def timed_steps(fn, steps: int, warmup: int, flush, stream):
+    """(total device ms over `steps`, last result): per-step CUDA events on the
+    launching stream, L2 flush between steps outside the events."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    out = None
+    for i in range(steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        out = fn()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return float(sum(a.elapsed_time(b) for a, b in ev)), out
+
+
+def secondary(dev, flush, stream, steps: int) -> dict:
+    """Configs 1, 3, 4 on one GPU (their own metrics, secondary to the headline)."""
+    import torch
+
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
+    from paper_2111_00110_b200.layers import (depth_forward, depth_surface_jvp,
+                                              explicit_forward, explicit_jvp,
+                                              volumetric_forward, volumetric_jvp)
+    from paper_2111_00110_b200.ray import Camera, RayBundle, generate_rays
+    out = {}
+    # config 1: 2D explicit layer lifted to z = 0.03125, level 4
+    rng = np.random.default_rng(11)
+    n = 4096
+    lo = np.nextafter(-1.0, 0.0)
+    p = np.concatenate([rng.uniform(lo, 1, (n, 2)), np.full((n, 1), 0.03125)], 1).astype(np.float32)
+    q = np.concatenate([rng.uniform(lo, 1, (n, 2)), np.full((n, 1), 0.03125)], 1).astype(np.float32)
+    w = rng.standard_normal((n, 1)).astype(np.float32)
+    yb = rng.standard_normal((n, 1)).astype(np.float32)
+    P, Q, W, YB = (torch.from_numpy(a).to(dev) for a in (p, q, w, yb))
+    e1 = Engine(KernelModel("gaussian", 200.0, 4), 4, check_admissibility=False)
+    ms, _ = timed_steps(lambda: explicit_jvp(YB, explicit_forward(e1, SourceSet(P, W), Q)),
+                        steps, 3, flush, stream)
+    out["cfg1_explicit_2d"] = {"metric": "points/s (N+M)", "value": 2 * n / (ms / steps / 1e3),
+                               "ms_per_step": ms / steps,
+                               "workload": "N=M=4096, 2D lifted to z=0.03125, level 4, alpha 200"}
+    # config 3: root-implicit depth + normal, 512x512 rays, level 5, bias +0.05
+    rng = np.random.default_rng(33)
+    N3 = 1 << 18
+    p = rng.uniform(lo, 1, (N3, 3)).astype(np.float32)
+    w = rng.normal(0.0, 0.1, (N3, 1)).astype(np.float32)
+    cam = Camera(2.0 * seeded_direction(rng), np.zeros(3), np.array([0.0, 1.0, 0.0]), 60.0,
+                 512, 512)
+    b3 = generate_rays(cam)
+    R3 = b3.count
+    yl = torch.from_numpy(rng.standard_normal(R3).astype(np.float32)).to(dev)
+    yg = torch.from_numpy(rng.standard_normal((R3, 3)).astype(np.float32)).to(dev)
+    b3 = RayBundle(torch.from_numpy(b3.origins).to(dev), torch.from_numpy(b3.directions).to(dev))
+    e5 = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    src3 = SourceSet(torch.from_numpy(p).to(dev), torch.from_numpy(w).to(dev))
+
+    def step3():
+        res = depth_forward(e5, src3, b3, bias=0.05)
+        return depth_surface_jvp(yl, yg, res), res
+    ms, (g3, r3) = timed_steps(step3, steps, 2, flush, stream)
+    out["cfg3_root_depth_normal"] = {
+        "metric": "rays/s", "value": R3 / (ms / steps / 1e3), "ms_per_step": ms / steps,
+        "hit_fraction": float(r3.hit.float().mean().item()),
+        "workload": "N=2^18, 512x512 rays, radius 2, fov 60, level 5, bias +0.05, depth+normal "
+                    "adjoints in one fused insertion"}
+    # config 4: radiance, 8 poses of 400x400 rays, N = 2^20, 3 colours
+    rng = np.random.default_rng(44)
+    N4 = 1 << 20
+    p = torch.from_numpy(rng.uniform(lo, 1, (N4, 3)).astype(np.float32)).to(dev)
+    ws = torch.from_numpy(np.abs(rng.standard_normal((N4, 1))).astype(np.float32)).to(dev)
+    wc = torch.from_numpy(rng.uniform(0, 1, (N4, 3)).astype(np.float32)).to(dev)
+    org, dirs = [], []
+    for _ in range(8):
+        bb = generate_rays(Camera(2.5 * seeded_direction(rng), np.zeros(3),
+                                  np.array([0.0, 1.0, 0.0]), 50.0, 400, 400))
+        org.append(bb.origins)
+        dirs.append(bb.directions)
+    b4 = RayBundle(torch.from_numpy(np.concatenate(org)).to(dev),
+                   torch.from_numpy(np.concatenate(dirs)).to(dev))
+    R4 = b4.count
+    target = torch.from_numpy(rng.uniform(0, 1, (R4, 3)).astype(np.float32)).to(dev)
+    bg = np.ones(3)
+
+    def step4():
+        res = volumetric_forward(e5, p, ws, wc, b4, bg)
+        ybar = 2.0 * (res.rgb - target) / float(res.rgb.numel())   # MSE tangent (trainer.py:96-97)
+        return volumetric_jvp(ybar, res)
+    ms, _ = timed_steps(step4, max(2, steps // 4), 1, flush, stream)
+    k = max(2, steps // 4)
+    out["cfg4_radiance"] = {"metric": "rays/s", "value": R4 / (ms / k / 1e3), "ms_per_step": ms / k,
+                            "workload": "N=2^20 (|N(0,1)| density, U(0,1) RGB), 8 poses x 400x400, "
+                                        "radius 2.5, fov 50, level 5, MSE vs U(0,1) target"}
+    return out
+
+
 def run_ours(args, rank: int, world: int) -> None:
     import torch
     import torch.distributed as dist
@@ -196,6 +309,8 @@ def run_ours(args, rank: int, world: int) -> None:
     from paper_2111_00110_b200 import Engine, KernelModel, SourceSet, _lib
     from paper_2111_00110_b200.expansion import m2l_pairs
     from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    from paper_2111_00110_b200.parallel import (DeviceBackend, explicit_forward_sharded,
+                                                explicit_jvp_sharded)
 
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -208,6 +323,7 @@ def run_ours(args, rank: int, world: int) -> None:
     _ = eng.handle
     t_tables = time.perf_counter() - t0
 
+    # this rank's shard of the global problem (weak scaling: shard = config-2 size)
     p, w, q, yb = inputs(CFG["seed"] + 1000 * rank, N, M)
     P = torch.from_numpy(p).to(dev)
     W = torch.from_numpy(w).to(dev)
@@ -215,11 +331,14 @@ def run_ours(args, rank: int, world: int) -> None:
     YB = torch.from_numpy(yb).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    backend = DeviceBackend(eng)
 
     def step_dev():
+        if world > 1:
+            res = explicit_forward_sharded(backend, P, W, Q)
+            return explicit_jvp_sharded(backend, YB, res)
         res = explicit_forward(eng, SourceSet(P, W), Q)
-        g = explicit_jvp(YB, res)
-        return res, g
+        return explicit_jvp(YB, res)
 
     def barrier():
         if world > 1:
@@ -259,6 +378,14 @@ def run_ours(args, rank: int, world: int) -> None:
     h2d = sum(a.numel() * 4 for a in (hp, hw, hq, hy))
 
     def step_host():
+        if world > 1:
+            res = explicit_forward_sharded(backend, hp.to(dev, non_blocking=True),
+                                           hw.to(dev, non_blocking=True),
+                                           hq.to(dev, non_blocking=True))
+            wb, pb, qb = explicit_jvp_sharded(backend, hy.to(dev, non_blocking=True), res)
+            outs = [t.to("cpu", non_blocking=True) for t in (res.values, wb, pb, qb)]
+            torch.cuda.synchronize()
+            return outs
         res = explicit_forward(eng, SourceSet(hp, hw), hq)
         g = explicit_jvp(hy, res)
         return res.values, g.w_bar, g.p_bar, g.q_bar
@@ -285,7 +412,8 @@ def run_ours(args, rank: int, world: int) -> None:
         return
 
     # ---- roofline of the dominant kernel (finest-level M2L: far + near)
-    key = f"m2l_L{CFG['levels']}"
+    key = next((k for k in (f"m2l_tc_L{CFG['levels']}", f"m2l_L{CFG['levels']}") if k in prof),
+               None)
     k_ms, k_n = prof.get(key, (float("nan"), 1))
     pairs = m2l_pairs(eng.m2l_tables["far"][CFG["levels"]]) + m2l_pairs(eng.m2l_tables["near"])
     flops_launch = pairs * 1 * eng.P * eng.P * 2
@@ -306,7 +434,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "config": {"workload": WORKLOAD, "N": N, "M": M, "levels": CFG["levels"],
                    "rho": CFG["rho"], "alpha": CFG["alpha"],
                    "l2": "inputs 176 MB > 126 MB L2, and a 256 MB L2 flush between steps",
-                   "parallelism": f"dp{world} (replicas)"},
+                   "parallelism": f"dp{world}" + (" (grid all-reduce, NCCL)" if world > 1 else "")},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
@@ -314,13 +442,16 @@ def run_ours(args, rank: int, world: int) -> None:
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
                      "flops_per_launch": flops_launch, "launch_ms": k_ms / k_n,
+                     "precision": "3xTF32 (tcgen05 kind::tf32), fp32 accumulate",
                      "fp32_ffma_nominal_tflops": 74.4,
                      "frac_of_fp32_ffma_nominal": achieved / 74.4},
         "stages_ms_per_step": stages,
         "table_fit_s": t_tables,
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline and not args.small:
+    if world == 1 and not args.no_secondary and not args.small:
+        line["secondary"] = secondary(dev, flush, stream, args.steps)
+    if not args.no_cpu_baseline and not args.small and world == 1:
         cb = cpu_sample(1, 0, N, M, CFG["seed"])
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     print(json.dumps(line), flush=True)
