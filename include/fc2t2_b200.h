@@ -114,10 +114,12 @@ size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream);
 
-/* ---- L2P: Accessor (expansion.py:335-373) ---- */
+/* ---- L2P: Accessor (expansion.py:335-373) ----
+ * d_order (optional, n int32): evaluate the points in this (cell-sorted) order;
+ * outputs are still indexed by point. */
 int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d_q, int64_t n,
-              int mode, const float* d_wts, float* d_value, float* d_grad, float* d_hess,
-              float* d_wgrad, int32_t* d_flag, void* stream);
+              int mode, const int32_t* d_order, const float* d_wts, float* d_value,
+              float* d_grad, float* d_hess, float* d_wgrad, int32_t* d_flag, void* stream);
 
 /* ---- rays: traversal (ray.py:101-157), layers (layers.py:193-402) ----
  * Rays are (R, 3) float64 origins / directions on the device.  Traversal:

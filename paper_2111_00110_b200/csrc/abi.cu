@@ -639,13 +639,13 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
 }
 
 int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d_q, int64_t n,
-              int mode, const float* d_wts, float* d_value, float* d_grad, float* d_hess,
-              float* d_wgrad, int32_t* d_flag, void* stream) {
+              int mode, const int32_t* d_order, const float* d_wts, float* d_value,
+              float* d_grad, float* d_hess, float* d_wgrad, int32_t* d_flag, void* stream) {
   if (rho < 1 || rho > 6) return fail(FC2T2_EORDER, "expansion order must be in [1, 6]");
   if (level < 0 || level > 9 || channels < 1 || n < 0) return fail(FC2T2_EVALUE, "bad l2p arguments");
   if ((mode & FC2T2_L2P_WGRAD) && !d_wts) return fail(FC2T2_EVALUE, "WGRAD needs weights");
-  return cuda_status(fc2t2::l2p(rho, level, channels, d_l, d_q, n, mode, d_wts, d_value, d_grad,
-                                d_hess, d_wgrad, d_flag, (cudaStream_t)stream),
+  return cuda_status(fc2t2::l2p(rho, level, channels, d_l, d_q, n, mode, d_order, d_wts, d_value,
+                                d_grad, d_hess, d_wgrad, d_flag, (cudaStream_t)stream),
                      "l2p");
 }
 

@@ -73,8 +73,8 @@ enum L2PMode : int {
   L2P_WGRAD = 8,   // (n, 3) = sum_c wts[n, c] * grad f_c
 };
 cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64_t n, int mode,
-                const float* wts, float* value, float* grad, float* hess, float* wgrad,
-                int32_t* flag, cudaStream_t s);
+                const int32_t* order, const float* wts, float* value, float* grad, float* hess,
+                float* wgrad, int32_t* flag, cudaStream_t s);
 
 }  // namespace fc2t2
 

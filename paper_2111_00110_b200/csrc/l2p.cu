@@ -7,6 +7,10 @@
 // reference _shift_indices :309-329) and the Hessian (xx yy zz xy xz yz).
 // L2P_WGRAD fuses the adjoint contraction sum_c wts_c grad f_c used by the
 // explicit layer's q_bar and p_bar (reference layers.py:183, :186-187).
+//
+// With a cell-sorted `order` (the stable sort P2M needs anyway), thread i
+// evaluates point order[i]: neighbouring threads share cell rows, which then
+// come from L1 instead of one 144-byte L2 gather per point.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -17,13 +21,15 @@ namespace {
 template <int RHO, int MODE>
 __global__ void __launch_bounds__(256)
 l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, int C, int res,
-           const float* __restrict__ wts, float* __restrict__ value, float* __restrict__ grad,
-           float* __restrict__ hess, float* __restrict__ wgrad, int32_t* __restrict__ flag) {
+           const int32_t* __restrict__ order, const float* __restrict__ wts,
+           float* __restrict__ value, float* __restrict__ grad, float* __restrict__ hess,
+           float* __restrict__ wgrad, int32_t* __restrict__ flag) {
   constexpr MI<RHO> mi{};
   constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
   int bad = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = order ? (int64_t)order[t] : t;
     const float x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
     bad |= outside_domain(x, y, z);
     const int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
@@ -88,14 +94,14 @@ l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, 
 
 template <int RHO>
 cudaError_t l2p_rho(int level, int C, const float* L, const float* q, int64_t n, int mode,
-                    const float* wts, float* value, float* grad, float* hess, float* wgrad,
-                    int32_t* flag, cudaStream_t s) {
+                    const int32_t* order, const float* wts, float* value, float* grad,
+                    float* hess, float* wgrad, int32_t* flag, cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int blocks = grid_blocks(n, 256, 148 * 16);
 #define FC2T2_L2P_CASE(M)                                                               \
   case M:                                                                               \
     FC2T2_LAUNCH("l2p", s, l2p_kernel<RHO, M><<<blocks, 256, 0, s>>>(                   \
-        L, q, n, C, res, wts, value, grad, hess, wgrad, flag));                         \
+        L, q, n, C, res, order, wts, value, grad, hess, wgrad, flag));                  \
     break;
   switch (mode) {
     FC2T2_L2P_CASE(1)
@@ -116,11 +122,11 @@ cudaError_t l2p_rho(int level, int C, const float* L, const float* q, int64_t n,
 }  // namespace
 
 cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64_t n, int mode,
-                const float* wts, float* value, float* grad, float* hess, float* wgrad,
-                int32_t* flag, cudaStream_t s) {
+                const int32_t* order, const float* wts, float* value, float* grad, float* hess,
+                float* wgrad, int32_t* flag, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  FC2T2_DISPATCH_RHO(rho, return l2p_rho<RHO>(level, C, L, q, n, mode, wts, value, grad, hess,
-                                              wgrad, flag, s));
+  FC2T2_DISPATCH_RHO(rho, return l2p_rho<RHO>(level, C, L, q, n, mode, order, wts, value, grad,
+                                              hess, wgrad, flag, s));
   return cudaSuccess;
 }
 

@@ -23,6 +23,8 @@ constexpr int RADIX_THREADS = 256;
 constexpr int RADIX_ROUNDS = 16;
 constexpr int RADIX_TILE = RADIX_THREADS * RADIX_ROUNDS;  // 4096 keys per block
 constexpr int RADIX_WARPS = RADIX_THREADS / 32;
+constexpr int RADIX_MAX_BITS = 9;  // 512 bins: 18-bit cell keys sort in 2 passes
+constexpr int RADIX_MAX_BINS = 1 << RADIX_MAX_BITS;
 
 // ---------------------------------------------------------------- keys ---
 
@@ -152,7 +154,7 @@ namespace {
 
 __global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                   int bits, int nblocks, uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[256];
+  __shared__ uint32_t h[RADIX_MAX_BINS];
   const int nbins = 1 << bits;
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
   __syncthreads();
@@ -179,11 +181,17 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
                      uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                      int64_t n, int shift, int bits, int nblocks,
                      const uint32_t* __restrict__ offsets) {
-  __shared__ uint32_t whist[RADIX_WARPS][256];
+  extern __shared__ uint32_t rsm[];
   const int nbins = 1 << bits;
+  uint32_t* whist_base = rsm;                          // [RADIX_WARPS][nbins]
+  uint32_t* dstart = rsm + RADIX_WARPS * nbins;        // [nbins]
+  uint32_t* gstart = dstart + nbins;                   // [nbins]
+  uint32_t* skey = gstart + nbins;                     // [RADIX_TILE]
+  uint32_t* sval = skey + RADIX_TILE;                  // [RADIX_TILE]
+  auto whist = [&](int w, uint32_t b) -> uint32_t& { return whist_base[w * nbins + b]; };
   const uint32_t mask = (uint32_t)nbins - 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b = threadIdx.x; b < RADIX_WARPS * 256; b += blockDim.x) (&whist[0][0])[b] = 0;
+  for (int b = threadIdx.x; b < RADIX_WARPS * nbins; b += blockDim.x) whist_base[b] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * RADIX_TILE + (int64_t)warp * (32 * RADIX_ITEMS);
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -203,8 +211,8 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
     const int leader = __ffs(peers) - 1;
     uint32_t old = 0;
     if (lane == leader && valid) {
-      old = whist[warp][d];
-      whist[warp][d] = old + __popc(peers);
+      old = whist(warp, d);
+      whist(warp, d) = old + __popc(peers);
     }
     old = __shfl_sync(0xffffffffu, old, leader);
     pos[r] = old + __popc(peers & lt_mask);
@@ -213,13 +221,12 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
   __syncthreads();
   // block-local digit runs: per-warp prefix inside each digit, then an
   // exclusive scan over the digits (warp 0, 8 bins per lane)
-  __shared__ uint32_t dstart[256], gstart[256];
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
     uint32_t acc = 0;
 #pragma unroll
     for (int w = 0; w < RADIX_WARPS; ++w) {
-      const uint32_t c = whist[w][b];
-      whist[w][b] = acc;
+      const uint32_t c = whist(w, b);
+      whist(w, b) = acc;
       acc += c;
     }
     dstart[b] = acc;  // digit total for now
@@ -227,10 +234,11 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
   }
   __syncthreads();
   if (warp == 0) {
-    uint32_t v[8], sum = 0;
+    constexpr int PER = RADIX_MAX_BINS / 32;
+    uint32_t v[PER], sum = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int b = lane * 8 + k;
+    for (int k = 0; k < PER; ++k) {
+      const int b = lane * PER + k;
       v[k] = b < nbins ? dstart[b] : 0u;
       sum += v[k];
     }
@@ -242,20 +250,19 @@ radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __res
     }
     uint32_t run = x - sum;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int b = lane * 8 + k;
+    for (int k = 0; k < PER; ++k) {
+      const int b = lane * PER + k;
       if (b < nbins) dstart[b] = run;
       run += v[k];
     }
   }
   __syncthreads();
   // stage the tile in digit order, then write every digit run contiguously
-  __shared__ uint32_t skey[RADIX_TILE], sval[RADIX_TILE];
 #pragma unroll
   for (int r = 0; r < RADIX_ITEMS; ++r) {
     if (key[r] == 0xffffffffu) continue;
     const uint32_t d = (key[r] >> shift) & mask;
-    const uint32_t lp = dstart[d] + whist[warp][d] + pos[r];
+    const uint32_t lp = dstart[d] + whist(warp, d) + pos[r];
     skey[lp] = key[r];
     sval[lp] = val[r];
   }
@@ -282,7 +289,7 @@ size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 size_t cell_sort_workspace(int level, int64_t n) {
   const int64_t R = (int64_t)1 << (3 * (level + 1));
   const int64_t nblocks = (n + RADIX_TILE - 1) / RADIX_TILE;
-  const int64_t hist = 256 * (nblocks > 0 ? nblocks : 1);
+  const int64_t hist = RADIX_MAX_BINS * (nblocks > 0 ? nblocks : 1);
   size_t b = 0;
   b += 4 * align256(4 * (size_t)n);  // keys, keys2, vals, vals2
   b += align256(4 * (size_t)hist);
@@ -314,8 +321,8 @@ SortWs carve(void* ws, int64_t n, int64_t R) {
   w.keys2 = take(4 * (size_t)n);
   w.vals = take(4 * (size_t)n);
   w.vals2 = take(4 * (size_t)n);
-  w.hist = take(4 * (size_t)(256 * nblocks));
-  w.scan = take(4 * std::max(scan_ws_words(256 * nblocks), scan_ws_words(R + 1)) + 4);
+  w.hist = take(4 * (size_t)(RADIX_MAX_BINS * nblocks));
+  w.scan = take(4 * std::max(scan_ws_words(RADIX_MAX_BINS * nblocks), scan_ws_words(R + 1)) + 4);
   w.counts = take(4 * (size_t)(R + 1));
   return w;
 }
@@ -326,7 +333,7 @@ cudaError_t sort_prepared(SortWs& w, int64_t n, int key_bits, int64_t R, int32_t
   const int64_t nblocks = std::max<int64_t>(1, (n + RADIX_TILE - 1) / RADIX_TILE);
   cudaError_t e = exclusive_scan(w.counts, (uint32_t*)cell_start, R + 1, w.scan, s);
   if (e != cudaSuccess || n == 0) return e != cudaSuccess ? e : cudaGetLastError();
-  const int passes = (key_bits + 7) / 8;
+  const int passes = (key_bits + RADIX_MAX_BITS - 1) / RADIX_MAX_BITS;
   const int digit = (key_bits + passes - 1) / passes;
   uint32_t *kin = w.keys, *vin = w.vals;
   for (int ps = 0; ps < passes; ++ps) {
@@ -340,8 +347,14 @@ cudaError_t sort_prepared(SortWs& w, int64_t n, int key_bits, int64_t R, int32_t
                      kin, n, shift, bits, (int)nblocks, w.hist));
     e = exclusive_scan(w.hist, w.hist, (int64_t)(1 << bits) * nblocks, w.scan, s);
     if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)(RADIX_WARPS * (1 << bits) + 2 * (1 << bits) + 2 * RADIX_TILE) * 4;
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+      if (e != cudaSuccess) return e;
+    }
     FC2T2_LAUNCH("radix_scatter", s,
-                 radix_scatter_kernel<<<(unsigned)nblocks, RADIX_THREADS, 0, s>>>(
+                 radix_scatter_kernel<<<(unsigned)nblocks, RADIX_THREADS, smem, s>>>(
                      kin, vin, kout, vout, n, shift, bits, (int)nblocks, w.hist));
     kin = kout;
     vin = vout;

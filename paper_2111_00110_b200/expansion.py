@@ -397,9 +397,10 @@ class Engine:
                   _ptr(self.flag.t), _ptr(ws), int(ws_bytes), _stream())
         return order, start
 
-    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor) -> ExpansionGrid:
+    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor, sort=None) -> ExpansionGrid:
+        """P2M; ``sort`` = (order, cell_start) of ``pts`` if already computed."""
         grid = self._empty_grid(self.levels, int(w.shape[1]), "M")
-        order, start = self.sort_points(pts)
+        order, start = sort if sort is not None else self.sort_points(pts)
         _lib.call("fc2t2_p2m", self.handle, int(w.shape[1]), _ptr(pts), _ptr(w), _ptr(order),
                   _ptr(start), _ptr(grid.storage), _stream())
         self.flops.add("p2m", flops.p2m_flops(int(pts.shape[0]), self.rho, self.P))
@@ -478,9 +479,9 @@ class Engine:
         grid = ExpansionGrid(level=self.levels, kind="L", storage=out, rho=self.rho)
         return Accessor(grid, self.table, self.flops)
 
-    def expand_device(self, pts: torch.Tensor, w: torch.Tensor) -> "Accessor":
+    def expand_device(self, pts: torch.Tensor, w: torch.Tensor, sort=None) -> "Accessor":
         """expand() on device tensors without the per-call domain sync."""
-        m = self.p2m_device(pts, w)
+        m = self.p2m_device(pts, w, sort)
         out = self.cascade_device(m.storage)
         grid = ExpansionGrid(level=self.levels, kind="L", storage=out, rho=self.rho)
         return Accessor(grid, self.table, self.flops, flag=self.flag)
@@ -514,8 +515,11 @@ class Accessor:
             self._flag = DomainFlag()
         return self._flag
 
-    def eval_device(self, q: torch.Tensor, mode: int, wts: torch.Tensor | None = None):
-        """One L2P launch; returns dict of the requested device outputs."""
+    def eval_device(self, q: torch.Tensor, mode: int, wts: torch.Tensor | None = None,
+                    order: torch.Tensor | None = None):
+        """One L2P launch; returns dict of the requested device outputs.  With a
+        cell-sorted ``order`` the points are evaluated in that order (L1 reuse
+        of the cell rows); outputs stay indexed by point."""
         n, C = int(q.shape[0]), self.channels
         dev = q.device
         out = {}
@@ -525,7 +529,7 @@ class Accessor:
         wgrad = torch.empty((n, 3), dtype=torch.float32, device=dev) if mode & _lib.L2P_WGRAD else None
         st = self.grid.storage if self.grid.storage.is_contiguous() else self.grid.storage.contiguous()
         _lib.call("fc2t2_l2p", self.table.rho, self.grid.level, C, _ptr(st), _ptr(q), n, mode,
-                  _ptr(wts), _ptr(value), _ptr(grad), _ptr(hess), _ptr(wgrad),
+                  _ptr(order), _ptr(wts), _ptr(value), _ptr(grad), _ptr(hess), _ptr(wgrad),
                   _ptr(self._flagobj().t), _stream())
         if self._counter is not None and mode & _lib.L2P_VALUE:
             self._counter.add("l2p", flops.l2p_flops(n, self.table.rho, self.table.size))

@@ -48,50 +48,60 @@ class ExplicitResult:
     sources: SourceSet
     engine: Engine
     q_dev: torch.Tensor = None
+    sorts: tuple = None      # ((p order, p cell_start), (q order, q cell_start))
 
 
 def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     _host_domain_check(q, "query")
+    # The cell sorts of the sources and queries are computed once and reused:
+    # p's by P2M now and by the source-side L2P of the backward, q's by the
+    # query L2Ps (cell-coherent order) and by the backward P2M of q.
     if is_host_tensor(q):
         # host tensors: the query upload overlaps the source expansion
         qd, q_ready = HostIO.h2d(q, 3)
-        acc = engine.expand_device(sources.p, sources.w)
+        p_sort = engine.sort_points(sources.p)
+        acc = engine.expand_device(sources.p, sources.w, p_sort)
         torch.cuda.current_stream().wait_event(q_ready)
-        vals = acc.eval_device(qd, _lib.L2P_VALUE)["value"]
+        q_sort = engine.sort_points(qd)
+        vals = acc.eval_device(qd, _lib.L2P_VALUE, order=q_sort[0])["value"]
         out = HostIO.d2h(vals)
         HostIO.finish()
         engine.flag.raise_if_set("source/query")
         return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine,
-                              q_dev=qd)
+                              q_dev=qd, sorts=(p_sort, q_sort))
     qd = to_device(q, 3, points=True)
-    acc = engine.expand_device(sources.p, sources.w)
-    vals = acc.eval_device(qd, _lib.L2P_VALUE)["value"]
+    p_sort = engine.sort_points(sources.p)
+    acc = engine.expand_device(sources.p, sources.w, p_sort)
+    q_sort = engine.sort_points(qd)
+    vals = acc.eval_device(qd, _lib.L2P_VALUE, order=q_sort[0])["value"]
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=like_input(vals, q), accessor=acc, q=q, sources=sources,
-                          engine=engine, q_dev=qd)
+                          engine=engine, q_dev=qd, sorts=(p_sort, q_sort))
 
 
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     eng = res.engine
     qd = res.q_dev
     src = res.sources
+    p_sort, q_sort = res.sorts
     if is_host_tensor(y_bar):
         # host tensors: q_bar's download overlaps the backward expansion
         yb, y_ready = HostIO.h2d(y_bar)
         torch.cuda.current_stream().wait_event(y_ready)
         yb = yb.reshape(qd.shape[0], -1)
-        q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb)["wgrad"]
+        q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb, order=q_sort[0])["wgrad"]
         q_bar_h = HostIO.d2h(q_bar)
-        back = eng.expand_device(qd, yb)
-        out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
+        back = eng.expand_device(qd, yb, q_sort)
+        out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
+                               order=p_sort[0])
         w_bar_h, p_bar_h = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
         HostIO.finish()
         eng.flag.raise_if_set("source/query")
         return LayerGradients(w_bar=w_bar_h, p_bar=p_bar_h, q_bar=q_bar_h)
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb)["wgrad"]
-    back = eng.expand_device(qd, yb)
-    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
+    q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb, order=q_sort[0])["wgrad"]
+    back = eng.expand_device(qd, yb, q_sort)
+    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w, order=p_sort[0])
     eng.flag.raise_if_set("source/query")
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),
