@@ -29,22 +29,26 @@ namespace fc2t2 {
 
 namespace {
 
-template <int RHO>
+// SMALL = one tile per CTA and a 2-stage x 6-offset B ring: ~105 KB of shared
+// memory, two CTAs per SM -- for levels whose tile count cannot fill 148 SMs.
+template <int RHO, bool SMALL = false>
 struct TCCfg {
+  static constexpr int RHO_ = RHO;
+  static constexpr bool SMALL_ = SMALL;
   static constexpr int P = index_count(RHO);
   static constexpr int PP = pad4(P);
   static constexpr int KPAD = (P + 7) / 8 * 8;      // K per offset (tf32 MMA K = 8)
   static constexpr int NPAD = (P + 15) / 16 * 16;   // MMA N (M = 128 needs N % 16 == 0)
   static constexpr int KSTEPS = KPAD / 8;
-  static constexpr int TILES = NPAD <= 64 ? 2 : 1;  // 8 accumulators must fit 512 TMEM cols
+  static constexpr int TILES = (NPAD <= 64 && !SMALL) ? 2 : 1;  // accumulators fit 512 TMEM cols
   static constexpr int PLOAD = (P + 15) / 16 * 16;   // accumulator columns drained
   static constexpr int TY = 16, TZ = 8;             // tile = 1 x TY x TZ targets
   static constexpr int WX = 3, WY = TY + 2, WZ = TZ + 2;
   static constexpr int WROWS = WX * WY * WZ;        // 540
   static constexpr int WSLICE = TILES * 2 * 2 * WROWS * 16;   // [tile][part][kc][row][16B]
   static constexpr int BSTAGE = 2 * 2 * NPAD * 16;  // [kc][row: hi 0..NPAD-1, lo NPAD..][16B]
-  static constexpr int DPS = 9;                     // offsets per B stage
-  static constexpr int NS = RHO <= 4 ? 3 : 2;       // B stages (DPS tables each)
+  static constexpr int DPS = SMALL ? 6 : 9;         // offsets per B stage
+  static constexpr int NS = (RHO <= 4 && !SMALL) ? 3 : 2;  // B stages (DPS tables each)
   static constexpr int ACC = NPAD <= 64 ? 128 : 256;          // [hi*hi | cross] per tile
   static constexpr int TMEM_COLS = 2 * TILES * ACC;           // sets x tiles
   static constexpr int THREADS = 384;                         // 12 warps
@@ -60,6 +64,11 @@ struct TCCfg {
   }
   static constexpr uint32_t IDESC1 = idesc(NPAD);      // A x B_hi
   static constexpr uint32_t IDESC2 = idesc(2 * NPAD);  // A_hi x [B_hi; B_lo]
+};
+
+template <class T>
+struct CfgTag {
+  using type = T;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -191,13 +200,13 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
-template <int RHO>
-__global__ void __launch_bounds__(384, 1)
+template <int RHO, bool SMALL>
+__global__ void __launch_bounds__(384, SMALL ? 2 : 1)
 m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, const int2* __restrict__ entries,
               const int* __restrict__ grp_start, float* __restrict__ L, int res, int nu, int C,
               int accumulate) {
-  using Cfg = TCCfg<RHO>;
+  using Cfg = TCCfg<RHO, SMALL>;
   constexpr int WROWS = Cfg::WROWS, NS = Cfg::NS, KS = Cfg::KSTEPS, TILES = Cfg::TILES;
   constexpr int P = Cfg::P, PP = Cfg::PP, PL = Cfg::PLOAD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -457,9 +466,9 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const f
                    float* L, int accumulate, cudaStream_t s) {
   const int res = 1 << (plan.level + 1);
   const int nu = res / 2;
-  FC2T2_DISPATCH_RHO(rho, {
-    using Cfg = TCCfg<RHO>;
-    auto kern = m2l_tc_kernel<RHO>;
+  auto launch = [&](auto cfg_tag) -> cudaError_t {
+    using Cfg = typename decltype(cfg_tag)::type;
+    auto kern = m2l_tc_kernel<Cfg::RHO_, Cfg::SMALL_>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)Cfg::SMEM);
     if (e != cudaSuccess) return e;
@@ -469,6 +478,14 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const f
     FC2T2_LAUNCH(plan.level_name, s,
                  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(Mhi, Mlo, plan.btab, plan.entries,
                                                    plan.grp_start, L, res, nu, C, accumulate));
+    return cudaGetLastError();
+  };
+  // big CTAs (2 tiles, 1 per SM) only when they fill the machine
+  const int ntiles_big = nu * ((nu + 15) / 16) * ((nu + 7) / 8);
+  const bool small = (int64_t)((ntiles_big + 1) / 2) * 8 * C < 2 * 148;
+  FC2T2_DISPATCH_RHO(rho, {
+    if (small) return launch(CfgTag<TCCfg<RHO, true>>{});
+    return launch(CfgTag<TCCfg<RHO, false>>{});
   });
   return cudaGetLastError();
 }
