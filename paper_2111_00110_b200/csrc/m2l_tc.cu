@@ -482,7 +482,7 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const f
   };
   // big CTAs (2 tiles, 1 per SM) only when they fill the machine
   const int ntiles_big = nu * ((nu + 15) / 16) * ((nu + 7) / 8);
-  const bool small = (int64_t)((ntiles_big + 1) / 2) * 8 * C < 2 * 148;
+  const bool small = false && (int64_t)((ntiles_big + 1) / 2) * 8 * C < 2 * 148;  // measured slower (issuer-bound)
   FC2T2_DISPATCH_RHO(rho, {
     if (small) return launch(CfgTag<TCCfg<RHO, true>>{});
     return launch(CfgTag<TCCfg<RHO, false>>{});
