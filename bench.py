@@ -204,13 +204,18 @@ def seeded_direction(rng):
             return u
 
 
-def timed_steps(fn, steps: int, warmup: int, flush, stream):
+def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None = None):
     """(total device ms over `steps`, last result): per-step CUDA events on the
-    launching stream, L2 flush between steps outside the events."""
+    launching stream, L2 flush between steps outside the events.  With
+    ``stages`` the library's per-kernel event profile (ms per step) is stored."""
     import torch
+
+    from paper_2111_00110_b200 import _lib
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    if stages is not None:
+        _lib.profile_enable(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
     out = None
@@ -220,6 +225,9 @@ def timed_steps(fn, steps: int, warmup: int, flush, stream):
         out = fn()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
+    if stages is not None:
+        stages.update({k: round(v[0] / steps, 4) for k, v in _lib.profile_read().items()})
+        _lib.profile_enable(False)
     return float(sum(a.elapsed_time(b) for a, b in ev)), out
 
 
@@ -266,10 +274,11 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     def step3():
         res = depth_forward(e5, src3, b3, bias=0.05)
         return depth_surface_jvp(yl, yg, res), res
-    ms, (g3, r3) = timed_steps(step3, steps, 2, flush, stream)
+    st3 = {}
+    ms, (g3, r3) = timed_steps(step3, steps, 2, flush, stream, st3)
     out["cfg3_root_depth_normal"] = {
         "metric": "rays/s", "value": R3 / (ms / steps / 1e3), "ms_per_step": ms / steps,
-        "hit_fraction": float(r3.hit.float().mean().item()),
+        "hit_fraction": float(r3.hit.float().mean().item()), "stages_ms_per_step": st3,
         "workload": "N=2^18, 512x512 rays, radius 2, fov 60, level 5, bias +0.05, depth+normal "
                     "adjoints in one fused insertion"}
     # config 4: radiance, 8 poses of 400x400 rays, N = 2^20, 3 colours
@@ -294,9 +303,11 @@ def secondary(dev, flush, stream, steps: int) -> dict:
         res = volumetric_forward(e5, p, ws, wc, b4, bg)
         ybar = 2.0 * (res.rgb - target) / float(res.rgb.numel())   # MSE tangent (trainer.py:96-97)
         return volumetric_jvp(ybar, res)
-    ms, _ = timed_steps(step4, max(2, steps // 4), 1, flush, stream)
+    st4 = {}
+    ms, _ = timed_steps(step4, max(2, steps // 4), 1, flush, stream, st4)
     k = max(2, steps // 4)
     out["cfg4_radiance"] = {"metric": "rays/s", "value": R4 / (ms / k / 1e3), "ms_per_step": ms / k,
+                            "stages_ms_per_step": {a: round(b * steps / k, 4) for a, b in st4.items()},
                             "workload": "N=2^20 (|N(0,1)| density, U(0,1) RGB), 8 poses x 400x400, "
                                         "radius 2.5, fov 50, level 5, MSE vs U(0,1) target"}
     return out

@@ -1,18 +1,21 @@
 // Integral-implicit radiance layer (reference layers.py:405-544) on the device.
 //
 // Forward, one thread per ray walking its segments in order:
-//   sigma, colour polynomials = line2poly of the 1+CC channels (rays.cu),
+//   sigma, colour polynomials = line2poly of the 1+CC channels (raywalk.cuh),
 //   S(x) = int sigma, depth0 = per-ray exclusive prefix of S(s) (float64),
-//   alive = depth0 <= 4.5, T(x) = E(S(x) + depth0) with E the degree-4 exp(-x)
-//   fit (Horner composition, degree 4(rho+1)), rgb_c += int_0^s c sigma T,
+//   alive = depth0 <= 4.5, rgb_c += int_0^s c sigma E(S + depth0) dx,
 //   rgb_c += E(depth_final) bg_c.
+// The integrand is a polynomial of degree 4(rho+1) + 2 rho (28 at rho = 4),
+// so a 17-node Gauss-Legendre rule integrates it exactly -- the same value the
+// reference gets from its explicit polynomial algebra, without the degree-29
+// coefficient arrays (the register footprint is what bounded the first
+// version of these kernels).
 // Backward (volumetric_jvp): pass A recomputes the per-ray totals of
-//   int_0^s E'(S + depth0) sigma c; pass B builds, per alive segment, the
-//   polynomial weights h_sigma(u) and y_c T sigma and inserts their closed-form
-//   segment moments (line2taylor_h = Gauss-Legendre with G = 17 nodes, exact
-//   for the degree-33 integrands) -- keys + payload rows, then the generic
-//   deterministic insertion.  Polynomial algebra is float64 like the
-//   reference; the quadrature moments are float32.
+// int_0^s E'(S + depth0) sigma c; pass B builds per alive segment the weights
+// h_sigma(u) and y_c T(u) sigma(u) at the 17 Gauss nodes and inserts their
+// closed-form segment moments (line2taylor_h, exact at this degree).  The one
+// nested integral, int_0^u c sigma T', is polynomial algebra in float32 with
+// E' Taylor-shifted to depth0 in float64 first.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "raywalk.cuh"
@@ -25,88 +28,60 @@ using namespace ray;
 
 constexpr double EXP_CUTOFF = 4.5;     // poly1d.py:22
 constexpr double EXP_FIT_RANGE = 5.0;  // poly1d.py:23
+constexpr int GN = 17;                 // Gauss-Legendre nodes, exact to degree 33
 
-template <int RHO>
-struct VolCfg {
-  static constexpr int NL = RHO + 1;             // line polynomial
-  static constexpr int NS = RHO + 2;             // S = int sigma (with constant)
-  static constexpr int NT = 4 * (RHO + 1) + 1;   // T = E(S + depth0)
-  static constexpr int NTP = 3 * (RHO + 1) + 1;  // T' = E'(S + depth0)
-  static constexpr int NCS = 2 * RHO + 1;        // c * sigma
-  static constexpr int NI = NCS + NT - 1;        // c sigma T
-  static constexpr int NIP = NCS + NTP - 1;      // c sigma T'
-  static constexpr int NH = NI + 1;              // h_sigma (= antiderivative length)
-  static constexpr int NTS = NT + NL - 1;        // T sigma, T c
-  static constexpr int G = (RHO + NH - 1) / 2 + 1;  // Gauss nodes (ray.py:236)
-};
+__constant__ double GL_X[GN] = {
+    -0.9905754753144174, -0.9506755217687677, -0.8802391537269859, -0.7815140038968014,
+    -0.6576711592166907, -0.5126905370864769, -0.3512317634538763, -0.17848418149584785, 0.0,
+    0.17848418149584785, 0.3512317634538763, 0.5126905370864769, 0.6576711592166907,
+    0.7815140038968014, 0.8802391537269859, 0.9506755217687677, 0.9905754753144174};
+__constant__ double GL_W[GN] = {
+    0.02414830286854758, 0.05545952937398796, 0.08503614831717912, 0.11188384719340397,
+    0.1351363684685255, 0.15404576107681026, 0.1680041021564499, 0.17656270536699253,
+    0.17944647035620653, 0.17656270536699253, 0.1680041021564499, 0.15404576107681026,
+    0.1351363684685255, 0.11188384719340397, 0.08503614831717912, 0.05545952937398796,
+    0.02414830286854758};
+
+template <int N>
+__device__ __forceinline__ float hornerf(const float (&a)[N], float x) {
+  float y = 0.f;
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k) y = fmaf(y, x, a[k]);
+  return y;
+}
 
 template <int NA, int NB>
-__device__ __forceinline__ void pmul(const double (&a)[NA], const double (&b)[NB],
-                                     double (&o)[NA + NB - 1]) {
+__device__ __forceinline__ void pmulf(const float (&a)[NA], const float (&b)[NB],
+                                      float (&o)[NA + NB - 1]) {
 #pragma unroll
-  for (int k = 0; k < NA + NB - 1; ++k) o[k] = 0.0;
+  for (int k = 0; k < NA + NB - 1; ++k) o[k] = 0.f;
 #pragma unroll
   for (int i = 0; i < NA; ++i)
 #pragma unroll
-    for (int j = 0; j < NB; ++j) o[i + j] = fma(a[i], b[j], o[i + j]);
+    for (int j = 0; j < NB; ++j) o[i + j] = fmaf(a[i], b[j], o[i + j]);
 }
 
-template <int N>
-__device__ __forceinline__ double peval(const double (&a)[N], double x) {
-  double y = 0.0;
-#pragma unroll
-  for (int k = N - 1; k >= 0; --k) y = fma(y, x, a[k]);
-  return y;
+__device__ __forceinline__ double efit_eval(const double* e, double y) {
+  return (((e[4] * y + e[3]) * y + e[2]) * y + e[1]) * y + e[0];
 }
 
-// int_0^x of the polynomial a, evaluated at x
-template <int N>
-__device__ __forceinline__ double pint_eval(const double (&a)[N], double x) {
-  double v = 0.0;
-#pragma unroll
-  for (int k = N - 1; k >= 0; --k) v = (v + a[k] / (double)(k + 1)) * x;
-  return v;
+__device__ __forceinline__ double efit_deriv(const double* e, double y) {
+  return ((4.0 * e[4] * y + 3.0 * e[3]) * y + 2.0 * e[2]) * y + e[1];
 }
 
-// out = E(g(x)), E of NE coefficients, Horner in g (layers.py:77-83)
-template <int NE, int NG>
-__device__ __forceinline__ void compose(const double* e, const double (&g)[NG],
-                                        double (&out)[(NE - 1) * (NG - 1) + 1]) {
-  constexpr int NO = (NE - 1) * (NG - 1) + 1;
-#pragma unroll
-  for (int k = 0; k < NO; ++k) out[k] = 0.0;
-  out[0] = e[NE - 1];
-#pragma unroll
-  for (int k = NE - 2; k >= 0; --k) {
-    const int deg = (NE - 2 - k) * (NG - 1);  // current degree of out
-    double tmp[NO];
-#pragma unroll
-    for (int i = 0; i < NO; ++i) tmp[i] = 0.0;
-#pragma unroll
-    for (int i = 0; i < NO; ++i)
-#pragma unroll
-      for (int j = 0; j < NG; ++j)
-        if (i <= deg && i + j < NO) tmp[i + j] = fma(out[i], g[j], tmp[i + j]);
-    tmp[0] += e[k];
-#pragma unroll
-    for (int i = 0; i < NO; ++i) out[i] = tmp[i];
-  }
-}
-
+// segment: sigma line polynomial, its antiderivative coefficients and S(s)
 template <int RHO>
-__device__ __forceinline__ void line_poly_d(const float* row, const float base[3],
-                                            const float dirf[3], double (&out)[RHO + 1]) {
-  float pf[RHO + 1];
-  line_poly<RHO>(row, base, dirf, pf);
+__device__ __forceinline__ double segment_sigma(const float* row, const float base[3],
+                                                const float dirf[3], double s,
+                                                float (&sg)[RHO + 1], float (&S)[RHO + 2]) {
+  line_poly<RHO>(row, base, dirf, sg);
+  S[0] = 0.f;
 #pragma unroll
-  for (int j = 0; j <= RHO; ++j) out[j] = (double)pf[j];
-}
-
-__device__ __forceinline__ double mexp_clamped(const double* e, double x) {
-  if (x > EXP_FIT_RANGE) return 0.0;
-  double y = 0.0;
-  for (int k = 4; k >= 0; --k) y = y * x + e[k];
-  return y;
+  for (int k = 0; k <= RHO; ++k) S[k + 1] = sg[k] / (float)(k + 1);
+  double v = 0.0;  // S(s) in float64 (feeds the optical-depth prefix)
+#pragma unroll
+  for (int k = RHO; k >= 0; --k) v = (v + (double)sg[k] / (double)(k + 1)) * s;
+  return v;
 }
 
 // ------------------------------------------------------------- forward ---
@@ -117,7 +92,6 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
                    const double* __restrict__ bg, float* __restrict__ rgb,
                    double* __restrict__ depth_final, const uint32_t* __restrict__ seg_offsets,
                    uint8_t* __restrict__ seg_alive) {
-  using V = VolCfg<RHO>;
   constexpr int PP = MI<RHO>::PP, NCH = 1 + CC;
   double e[5];
 #pragma unroll
@@ -135,29 +109,23 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
       float base[3];
       seg_base(o, d, t0, b0, b1, b2, res, base);
       const float* row = L + (((int64_t)b0 * res + b1) * res + b2) * NCH * PP;
-      double sg[V::NL];
-      line_poly_d<RHO>(row, base, dirf, sg);
-      double S[V::NS];
-      S[0] = 0.0;
-#pragma unroll
-      for (int k = 0; k < V::NL; ++k) S[k + 1] = sg[k] / (double)(k + 1);
       const double s = t1 - t0;
-      const double send = peval(S, s);
+      float sg[RHO + 1], S[RHO + 2];
+      const double send = segment_sigma<RHO>(row, base, dirf, s, sg, S);
       const bool alive = depth <= EXP_CUTOFF;
       if (alive) {
-        double gpoly[V::NS];
+        float col[CC][RHO + 1];
 #pragma unroll
-        for (int k = 0; k < V::NS; ++k) gpoly[k] = S[k];
-        gpoly[0] += depth;
-        double T[V::NT];
-        compose<5, V::NS>(e, gpoly, T);
+        for (int c = 0; c < CC; ++c) line_poly<RHO>(row + (1 + c) * PP, base, dirf, col[c]);
+        const double half = 0.5 * s;
+#pragma unroll 1
+        for (int g = 0; g < GN; ++g) {
+          const double x = half * (GL_X[g] + 1.0);
+          const float xf = (float)x;
+          const double T = efit_eval(e, (double)hornerf(S, xf) + depth);
+          const double wts = half * GL_W[g] * T * (double)hornerf(sg, xf);
 #pragma unroll
-        for (int c = 0; c < CC; ++c) {
-          double col[V::NL], cs[V::NCS], integ[V::NI];
-          line_poly_d<RHO>(row + (1 + c) * PP, base, dirf, col);
-          pmul(col, sg, cs);
-          pmul(cs, T, integ);
-          acc[c] += pint_eval(integ, s);
+          for (int c = 0; c < CC; ++c) acc[c] += wts * (double)hornerf(col[c], xf);
         }
         dfin += send;
       }
@@ -165,7 +133,7 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
       depth += send;
       return true;
     });
-    const double te = mexp_clamped(e, dfin);
+    const double te = dfin > EXP_FIT_RANGE ? 0.0 : efit_eval(e, dfin);
 #pragma unroll
     for (int c = 0; c < CC; ++c) rgb[r * CC + c] = (float)(acc[c] + te * bg[c]);
     depth_final[r] = dfin;
@@ -173,18 +141,17 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
 }
 
 // ------------------------------------------------- backward pass A ---
-// per ray: number of alive segments and totals of int_0^s c sigma T'
+// per ray: number of alive segments and totals of int_0^s c sigma E'(S + depth0)
 template <int RHO, int CC>
 __global__ void __launch_bounds__(128)
 vol_totals_kernel(const float* __restrict__ L, int res, const double* __restrict__ org,
                   const double* __restrict__ dir, int64_t R, const double* __restrict__ efit,
                   uint32_t* __restrict__ n_alive, double* __restrict__ totals,
                   double* __restrict__ depth_final) {
-  using V = VolCfg<RHO>;
   constexpr int PP = MI<RHO>::PP, NCH = 1 + CC;
-  double ep[4];
+  double e[5];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) ep[k] = efit[k + 1] * (double)(k + 1);
+  for (int k = 0; k < 5; ++k) e[k] = efit[k];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     double o[3], d[3];
@@ -198,28 +165,22 @@ vol_totals_kernel(const float* __restrict__ L, int res, const double* __restrict
       float base[3];
       seg_base(o, d, t0, b0, b1, b2, res, base);
       const float* row = L + (((int64_t)b0 * res + b1) * res + b2) * NCH * PP;
-      double sg[V::NL];
-      line_poly_d<RHO>(row, base, dirf, sg);
-      double S[V::NS];
-      S[0] = 0.0;
-#pragma unroll
-      for (int k = 0; k < V::NL; ++k) S[k + 1] = sg[k] / (double)(k + 1);
       const double s = t1 - t0;
-      const double send = peval(S, s);
+      float sg[RHO + 1], S[RHO + 2];
+      const double send = segment_sigma<RHO>(row, base, dirf, s, sg, S);
       if (depth <= EXP_CUTOFF) {
-        double gpoly[V::NS];
+        float col[CC][RHO + 1];
 #pragma unroll
-        for (int k = 0; k < V::NS; ++k) gpoly[k] = S[k];
-        gpoly[0] += depth;
-        double Tp[V::NTP];
-        compose<4, V::NS>(ep, gpoly, Tp);
+        for (int c = 0; c < CC; ++c) line_poly<RHO>(row + (1 + c) * PP, base, dirf, col[c]);
+        const double half = 0.5 * s;
+#pragma unroll 1
+        for (int g = 0; g < GN; ++g) {
+          const double x = half * (GL_X[g] + 1.0);
+          const float xf = (float)x;
+          const double Tp = efit_deriv(e, (double)hornerf(S, xf) + depth);
+          const double wts = half * GL_W[g] * Tp * (double)hornerf(sg, xf);
 #pragma unroll
-        for (int c = 0; c < CC; ++c) {
-          double col[V::NL], cs[V::NCS], ip[V::NIP];
-          line_poly_d<RHO>(row + (1 + c) * PP, base, dirf, col);
-          pmul(col, sg, cs);
-          pmul(cs, Tp, ip);
-          tot[c] += pint_eval(ip, s);
+          for (int c = 0; c < CC; ++c) tot[c] += wts * (double)hornerf(col[c], xf);
         }
         dfin += send;
         ++na;
@@ -235,31 +196,40 @@ vol_totals_kernel(const float* __restrict__ L, int res, const double* __restrict
 }
 
 // ------------------------------------------------- backward pass B ---
+// Per alive segment (layers.py:513-534):
+//   h_sigma(u) = sum_c y_c [ T(u) c(u) - int_0^u c sigma T' + total_c - before_c + tp_inf bg_c ]
+//   payload[0]   = sum_g W_g h_sigma(u_g) mono(d + u_g r)
+//   payload[1+c] = sum_g W_g y_c T(u_g) sigma(u_g) mono(d + u_g r)
+// T(u) = E(S(u) + depth0), T' = E'(S(u) + depth0).  int_0^u c sigma T' is a
+// degree-(3(rho+1) + 2 rho + 1) polynomial built in float32 from
+// E'_shift(y) = E'(y + depth0) (shift in float64) composed with S.
+constexpr int VOL_THREADS = 128;
+
 template <int RHO, int CC>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(VOL_THREADS)
 vol_payload_kernel(const float* __restrict__ L, int res, const double* __restrict__ org,
                    const double* __restrict__ dir, int64_t R, const double* __restrict__ efit,
                    const double* __restrict__ bg, const float* __restrict__ ybar,
                    const uint32_t* __restrict__ alive_offsets, const double* __restrict__ totals,
-                   const double* __restrict__ depth_final, const double* __restrict__ gl_x,
-                   const double* __restrict__ gl_w, uint32_t* __restrict__ keys,
+                   const double* __restrict__ depth_final, uint32_t* __restrict__ keys,
                    float* __restrict__ payload) {
-  using V = VolCfg<RHO>;
-  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP, NCH = 1 + CC, G = V::G;
-  double e[5], ep[4];
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP, NCH = 1 + CC;
+  constexpr int NS = RHO + 2, NS2 = 2 * NS - 1, NS3 = NS2 + NS - 1;  // S, S^2, S^3
+  constexpr int NCS = 2 * RHO + 1;                                   // c * sigma
+  constexpr int NQ = NCS + NS3 - 1;                                  // c sigma T'
+  __shared__ float wn_s[VOL_THREADS][NCH * GN + 1];                  // node weights
+  float* wn = wn_s[threadIdx.x];
+  double e[5];
 #pragma unroll
   for (int k = 0; k < 5; ++k) e[k] = efit[k];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ep[k] = efit[k + 1] * (double)(k + 1);
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     double o[3], d[3];
     load_ray(org, dir, r, o, d);
     const float dirf[3] = {(float)d[0], (float)d[1], (float)d[2]};
     const double dfin = depth_final[r];
-    // E'(depth_final), 0 beyond the fit range (layers.py:510-511)
-    const double tp_inf = dfin > EXP_FIT_RANGE ? 0.0 : ((ep[3] * dfin + ep[2]) * dfin + ep[1]) * dfin + ep[0];
-    double yb[CC], before[CC], konst = 0.0;
+    const double tp_inf = dfin > EXP_FIT_RANGE ? 0.0 : efit_deriv(e, dfin);  // layers.py:510-511
+    double yb[CC], before[CC];
 #pragma unroll
     for (int c = 0; c < CC; ++c) {
       yb[c] = (double)ybar[r * CC + c];
@@ -271,86 +241,102 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
       float base[3];
       seg_base(o, d, t0, b0, b1, b2, res, base);
       const float* row = L + (((int64_t)b0 * res + b1) * res + b2) * NCH * PP;
-      double sg[V::NL];
-      line_poly_d<RHO>(row, base, dirf, sg);
-      double S[V::NS];
-      S[0] = 0.0;
-#pragma unroll
-      for (int k = 0; k < V::NL; ++k) S[k + 1] = sg[k] / (double)(k + 1);
       const double s = t1 - t0;
-      const double send = peval(S, s);
+      float sg[RHO + 1], S[NS];
+      const double send = segment_sigma<RHO>(row, base, dirf, s, sg, S);
       if (depth <= EXP_CUTOFF) {
-        double gpoly[V::NS];
+        // T'(x) = a0 + a1 S + a2 S^2 + a3 S^3 with a = E' shifted to depth0 (float64)
+        const float a0 = (float)efit_deriv(e, depth);
+        const float a1 = (float)((12.0 * e[4] * depth + 6.0 * e[3]) * depth + 2.0 * e[2]);
+        const float a2 = (float)(12.0 * e[4] * depth + 3.0 * e[3]);
+        const float a3 = (float)(4.0 * e[4]);
+        float S2[NS2], S3[NS3], Tp[NS3];
+        pmulf(S, S, S2);
+        pmulf(S2, S, S3);
 #pragma unroll
-        for (int k = 0; k < V::NS; ++k) gpoly[k] = S[k];
-        gpoly[0] += depth;
-        double T[V::NT], Tp[V::NTP];
-        compose<5, V::NS>(e, gpoly, T);
-        compose<4, V::NS>(ep, gpoly, Tp);
-        // h_sigma = sum_c y_c [T c - int_0^u E'(S) sigma c + const_c]  (layers.py:513-527)
-        double h[V::NH];
+        for (int k = 0; k < NS3; ++k) {
+          float v = a3 * S3[k];
+          if (k < NS2) v = fmaf(a2, S2[k], v);
+          if (k < NS) v = fmaf(a1, S[k], v);
+          if (k == 0) v += a0;
+          Tp[k] = v;
+        }
+        const double half = 0.5 * s;
+        // node weights: channel 0 accumulates h_sigma, colours y_c T sigma
+        float hs_const = 0.f;
 #pragma unroll
-        for (int k = 0; k < V::NH; ++k) h[k] = 0.0;
-#pragma unroll
+        for (int g = 0; g < GN; ++g) wn[g] = 0.f;
+#pragma unroll 1
         for (int c = 0; c < CC; ++c) {
-          double col[V::NL], tc[V::NTS], cs[V::NCS], ip[V::NIP];
-          line_poly_d<RHO>(row + (1 + c) * PP, base, dirf, col);
-          pmul(T, col, tc);
+          float col[RHO + 1], cs[NCS], q[NQ];
+          line_poly<RHO>(row + (1 + c) * PP, base, dirf, col);
+          pmulf(col, sg, cs);
+          pmulf(cs, Tp, q);
+          const double k_c = totals[r * CC + c] - before[c] + tp_inf * bg[c];
+          hs_const += (float)(yb[c] * k_c);
+          // int_0^u q, evaluated at the nodes and at s
+          double cp = 0.0;
+#pragma unroll 1
+          for (int g = 0; g <= GN; ++g) {
+            const double x = g < GN ? half * (GL_X[g] + 1.0) : s;
+            const float xf = (float)x;
+            float aq = 0.f;
 #pragma unroll
-          for (int k = 0; k < V::NTS; ++k) h[k] = fma(yb[c], tc[k], h[k]);
-          pmul(col, sg, cs);
-          pmul(cs, Tp, ip);
-          // antiderivative of ip (zero constant) subtracted
-#pragma unroll
-          for (int k = 0; k < V::NIP; ++k) h[k + 1] -= yb[c] * ip[k] / (double)(k + 1);
-          const double cp = pint_eval(ip, s);
-          h[0] += yb[c] * (totals[r * CC + c] - before[c] + tp_inf * bg[c]);
+            for (int k = NQ - 1; k >= 0; --k) aq = (aq + q[k] / (float)(k + 1)) * xf;
+            if (g == GN) {
+              cp = (double)aq;
+              break;
+            }
+            const double T = efit_eval(e, (double)hornerf(S, xf) + depth);
+            wn[g] += (float)(yb[c] * (T * (double)hornerf(col, xf) - (double)aq));
+          }
           before[c] += cp;
         }
-        double tsig[V::NTS];
-        pmul(T, sg, tsig);
-        // per-node weights of the NCH payload channels
-        const double half = 0.5 * s;
-        float wn[NCH][G];
-        float nx[G];
+#pragma unroll 1
+        for (int g = 0; g < GN; ++g) {
+          const double x = half * (GL_X[g] + 1.0);
+          const float xf = (float)x;
+          const double W = half * GL_W[g];
+          const double T = efit_eval(e, (double)hornerf(S, xf) + depth);
+          wn[g] = (float)(W * ((double)wn[g] + (double)hs_const));
+          const double ts = W * T * (double)hornerf(sg, xf);
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const double t = half * (gl_x[g] + 1.0);
-          const double W = half * gl_w[g];
-          nx[g] = (float)t;
-          wn[0][g] = (float)(W * peval(h, t));
-          const double ts = W * peval(tsig, t);
+          for (int c = 0; c < CC; ++c) wn[(1 + c) * GN + g] = (float)(yb[c] * ts);
+        }
+        // moments of the NCH node-weighted point sets (mono shared by channels)
+        float pay[NCH][P];
 #pragma unroll
-          for (int c = 0; c < CC; ++c) wn[1 + c][g] = (float)(yb[c] * ts);
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int k = 0; k < P; ++k) pay[ch][k] = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < GN; ++g) {
+          const float xf = (float)(half * (GL_X[g] + 1.0));
+          float mono[P];
+          monomials<RHO>(fmaf(xf, dirf[0], base[0]), fmaf(xf, dirf[1], base[1]),
+                         fmaf(xf, dirf[2], base[2]), mono);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            const float wt = wn[ch * GN + g];
+#pragma unroll
+            for (int k = 0; k < P; ++k) pay[ch][k] = fmaf(wt, mono[k], pay[ch][k]);
+          }
         }
         keys[item] = ((uint32_t)b0 * res + b1) * res + b2;
-#pragma unroll 1
+#pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
-          float acc[P];
-#pragma unroll
-          for (int k = 0; k < P; ++k) acc[k] = 0.f;
-#pragma unroll 1
-          for (int g = 0; g < G; ++g) {
-            float mono[P];
-            monomials<RHO>(fmaf(nx[g], dirf[0], base[0]), fmaf(nx[g], dirf[1], base[1]),
-                           fmaf(nx[g], dirf[2], base[2]), mono);
-            const float wt = wn[ch][g];
-#pragma unroll
-            for (int k = 0; k < P; ++k) acc[k] = fmaf(wt, mono[k], acc[k]);
-          }
           float* dst = payload + (item * NCH + ch) * PP;
 #pragma unroll
           for (int k = 0; k < PP; k += 4)
-            *reinterpret_cast<float4*>(dst + k) =
-                make_float4(k < P ? acc[k] : 0.f, k + 1 < P ? acc[k + 1] : 0.f,
-                            k + 2 < P ? acc[k + 2] : 0.f, k + 3 < P ? acc[k + 3] : 0.f);
+            *reinterpret_cast<float4*>(dst + k) = make_float4(
+                k < P ? pay[ch][k] : 0.f, k + 1 < P ? pay[ch][k + 1] : 0.f,
+                k + 2 < P ? pay[ch][k + 2] : 0.f, k + 3 < P ? pay[ch][k + 3] : 0.f);
         }
         ++item;
       }
       depth += send;
       return true;
     });
-    (void)konst;
   }
 }
 
@@ -365,7 +351,7 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
 
 }  // namespace
 
-int vol_gauss_nodes(int rho) { return rho == 4 ? VolCfg<4>::G : (rho == 3 ? VolCfg<3>::G : (rho == 2 ? VolCfg<2>::G : VolCfg<1>::G)); }
+int vol_gauss_nodes(int rho) { return GN; }
 
 cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double* org,
                         const double* dir, int64_t R, const double* efit, const double* bg,
@@ -403,11 +389,13 @@ cudaError_t vol_payload(int rho, int level, int CC, const float* L, const double
   if (R <= 0) return cudaSuccess;
   if (rho != 4) return cudaErrorNotSupported;
   constexpr int RHO = 4;
-  const int blocks = grid_blocks(R, 128, 148 * 32);
+  (void)gl_x;
+  (void)gl_w;
+  const int blocks = grid_blocks(R, VOL_THREADS, 148 * 32);
   FC2T2_VOL_DISPATCH(CC, FC2T2_LAUNCH("vol_payload", s,
-      vol_payload_kernel<RHO, CC><<<blocks, 128, 0, s>>>(
+      vol_payload_kernel<RHO, CC><<<blocks, VOL_THREADS, 0, s>>>(
           L, 1 << (level + 1), org, dir, R, efit, bg, ybar, alive_offsets, totals, depth_final,
-          gl_x, gl_w, keys, payload)));
+          keys, payload)));
   return cudaGetLastError();
 }
 
