@@ -307,9 +307,29 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     ms, _ = timed_steps(step4, max(2, steps // 4), 1, flush, stream, st4)
     k = max(2, steps // 4)
     out["cfg4_radiance"] = {"metric": "rays/s", "value": R4 / (ms / k / 1e3), "ms_per_step": ms / k,
-                            "stages_ms_per_step": {a: round(b * steps / k, 4) for a, b in st4.items()},
+                            "stages_ms_per_step": st4,
                             "workload": "N=2^20 (|N(0,1)| density, U(0,1) RGB), 8 poses x 400x400, "
                                         "radius 2.5, fov 50, level 5, MSE vs U(0,1) target"}
+    # config 5 on one GPU: rho = 6 (P = 84), level 6 (128^3), N = 2^24, M = 2^27
+    del P, Q, W, YB, p, ws, wc, b4, target, src3, b3
+    torch.cuda.empty_cache()
+    e6 = Engine(KernelModel("gaussian", 4000.0, 6), 6, check_admissibility=False)
+    _ = e6.handle
+    gen = torch.Generator(device=dev).manual_seed(55)
+    N5, M5 = 1 << 24, 1 << 27
+    lo32 = -0.99999994
+    p5 = torch.rand(N5, 3, device=dev, generator=gen) * (2 * 0.99999994) + lo32
+    w5 = torch.randn(N5, 1, device=dev, generator=gen) * 0.1
+    q5 = torch.rand(M5, 3, device=dev, generator=gen) * (2 * 0.99999994) + lo32
+    y5 = torch.randn(M5, 1, device=dev, generator=gen)
+    st5 = {}
+    ms, _ = timed_steps(lambda: explicit_jvp(y5, explicit_forward(e6, SourceSet(p5, w5), q5)),
+                        2, 1, flush, stream, st5)
+    out["cfg5_explicit_rho6_1gpu"] = {
+        "metric": "points/s (N+M)", "value": (N5 + M5) / (ms / 2 / 1e3), "ms_per_step": ms / 2,
+        "stages_ms_per_step": st5,
+        "workload": "N=2^24, M=2^27, level 6 (128^3), rho 6 (P=84), alpha 4000, one GPU "
+                    "(the multi-GPU runs shard this with the grid all-reduce)"}
     return out
 
 

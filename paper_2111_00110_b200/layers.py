@@ -51,6 +51,17 @@ class ExplicitResult:
     sorts: tuple = None      # ((p order, p cell_start), (q order, q cell_start))
 
 
+# Grids larger than this are not L2 resident (126 MB L2): evaluate points in
+# cell-sorted order so consecutive threads share cell rows (measured: at a
+# 37.7 MB grid the scattered point gathers cost more than they save).
+COHERENT_L2P_BYTES = 64 << 20
+
+
+def _coherent(acc: Accessor, sort):
+    st = acc.grid.storage
+    return sort[0] if st.numel() * st.element_size() > COHERENT_L2P_BYTES else None
+
+
 def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     _host_domain_check(q, "query")
     # The cell sorts of the sources and queries are computed once and reused:
@@ -63,7 +74,7 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
         acc = engine.expand_device(sources.p, sources.w, p_sort)
         torch.cuda.current_stream().wait_event(q_ready)
         q_sort = engine.sort_points(qd)
-        vals = acc.eval_device(qd, _lib.L2P_VALUE)["value"]
+        vals = acc.eval_device(qd, _lib.L2P_VALUE, order=_coherent(acc, q_sort))["value"]
         out = HostIO.d2h(vals)
         HostIO.finish()
         engine.flag.raise_if_set("source/query")
@@ -73,7 +84,7 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     p_sort = engine.sort_points(sources.p)
     acc = engine.expand_device(sources.p, sources.w, p_sort)
     q_sort = engine.sort_points(qd)
-    vals = acc.eval_device(qd, _lib.L2P_VALUE)["value"]
+    vals = acc.eval_device(qd, _lib.L2P_VALUE, order=_coherent(acc, q_sort))["value"]
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=like_input(vals, q), accessor=acc, q=q, sources=sources,
                           engine=engine, q_dev=qd, sorts=(p_sort, q_sort))
@@ -89,19 +100,23 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
         yb, y_ready = HostIO.h2d(y_bar)
         torch.cuda.current_stream().wait_event(y_ready)
         yb = yb.reshape(qd.shape[0], -1)
-        q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb)["wgrad"]
+        q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb,
+                                         order=_coherent(res.accessor, q_sort))["wgrad"]
         q_bar_h = HostIO.d2h(q_bar)
         back = eng.expand_device(qd, yb, q_sort)
         out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
+                               order=_coherent(back, p_sort),
                                )
         w_bar_h, p_bar_h = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
         HostIO.finish()
         eng.flag.raise_if_set("source/query")
         return LayerGradients(w_bar=w_bar_h, p_bar=p_bar_h, q_bar=q_bar_h)
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb)["wgrad"]
+    q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb,
+                                     order=_coherent(res.accessor, q_sort))["wgrad"]
     back = eng.expand_device(qd, yb, q_sort)
-    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
+    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
+                           order=_coherent(back, p_sort))
     eng.flag.raise_if_set("source/query")
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),
