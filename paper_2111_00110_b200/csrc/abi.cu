@@ -49,13 +49,10 @@ struct Plan {
   int4* d_entries = nullptr;
   int* d_cls_start = nullptr;
   int max_list = 0;
-  // tcgen05 form (parity levels): {window start row, slot} grouped by
-  // (target class, source class), grp_start[8 * 8 + 1]
+  // tcgen05 form (parity levels): dense split tables, see build_tc_table
   bool tc = false;
-  std::vector<int2> tc_entries;
-  std::vector<int> tc_grp;
-  int2* d_tc_entries = nullptr;
-  int* d_tc_grp = nullptr;
+  std::vector<float> tcb;
+  uint8_t* d_tcb = nullptr;
 };
 
 }  // namespace
@@ -108,7 +105,6 @@ struct fc2t2_engine {
   HostTable near;
   bool uploaded = false;
   float* d_coef = nullptr;
-  uint8_t* d_btab = nullptr;  // 3xTF32-split tables in the UMMA K-major layout
   // plans[level][table]
   std::map<int, std::map<int, Plan>> plans;
 };
@@ -127,32 +123,66 @@ float rn_tf32_host(double v) {
   return f;
 }
 
-// One slot's table in the tcgen05 B layout: for every K step (8 inputs n),
-// [kchunk 2][row: k (hi) for rows < NPAD, k (lo) for rows >= NPAD][4 floats],
-// with A = hi + lo split in float64 (hi = rn_tf32(A), lo = rn_tf32(A - hi));
-// zero padded.  Rows [0, 2 NPAD) form one N = 2 NPAD K-major operand.
-void append_btab(const double* A, int P, int rho, std::vector<float>& btab) {
-  const int KS = fc2t2::tc_kpad(rho) / 8, NPAD = fc2t2::tc_npad(rho);
-  const size_t stage = (size_t)fc2t2::tc_bstage(rho) / 4;
-  const size_t base = btab.size();
-  btab.resize(base + KS * stage, 0.f);
-  for (int ks = 0; ks < KS; ++ks)
-    for (int kc = 0; kc < 2; ++kc)
-      for (int k = 0; k < NPAD; ++k)
-        for (int f = 0; f < 4; ++f) {
-          const int n = 8 * ks + 4 * kc + f;
-          const double a = (k < P && n < P) ? A[(size_t)k * P + n] : 0.0;
-          const float hi = rn_tf32_host(a);
-          const float lo = rn_tf32_host(a - (double)hi);
-          float* st = btab.data() + base + ks * stage;
-          st[(kc * 2 * NPAD + k) * 4 + f] = hi;
-          st[(kc * 2 * NPAD + NPAD + k) * 4 + f] = lo;
+// Dense tcgen05 tables of one parity plan (m2l_tc.cu): for class group cg
+// (target classes cg*CLS + ci), source class sigma, shift slot
+// s = (slot/9 - 1, slot/3%3 - 1, slot%3 - 1) and K step, the B operand rows
+// are the CLS tables A_delta, delta = 2 s + sigma - pi (the sum of the plan's
+// entries with that offset for class pi; zero if none), each split in float64
+// into hi = rn_tf32(A) and lo = rn_tf32(A - hi).  Row order: even sigma
+// [lo(class 0..) | hi(class 0..)], odd sigma [hi | lo]; K-major no-swizzle
+// [kchunk][row][4 floats].
+void build_tc_table(const std::vector<std::vector<int4>>& lists,
+                    const std::vector<const double*>& slot_src, int P, int rho,
+                    std::vector<float>& out) {
+  int CLS, NC, KS, BSLOT;
+  if (fc2t2::tc_geometry(rho, &CLS, &NC, &KS, &BSLOT) != 0) return;
+  const int W = CLS * NC, R = 2 * W, NCG = 8 / CLS;
+  const size_t slot_f = (size_t)BSLOT / 4;
+  out.assign((size_t)NCG * 8 * KS * 27 * slot_f, 0.f);
+  std::vector<double> A((size_t)P * P);
+  for (int cg = 0; cg < NCG; ++cg)
+    for (int sg = 0; sg < 8; ++sg) {
+      const int sig[3] = {(sg >> 2) & 1, (sg >> 1) & 1, sg & 1};
+      for (int slot = 0; slot < 27; ++slot) {
+        const int sh[3] = {slot / 9 - 1, (slot / 3) % 3 - 1, slot % 3 - 1};
+        for (int ci = 0; ci < CLS; ++ci) {
+          const int c = cg * CLS + ci;
+          const int pi[3] = {(c >> 2) & 1, (c >> 1) & 1, c & 1};
+          int dl[3];
+          for (int a = 0; a < 3; ++a) dl[a] = 2 * sh[a] + sig[a] - pi[a];
+          std::fill(A.begin(), A.end(), 0.0);
+          bool any = false;
+          for (const int4& e : lists[c])
+            if (e.x == dl[0] && e.y == dl[1] && e.z == dl[2]) {
+              const double* src = slot_src[e.w];
+              for (size_t i = 0; i < A.size(); ++i) A[i] += src[i];
+              any = true;
+            }
+          if (!any) continue;
+          const int hi_row = (sg & 1) ? ci * NC : W + ci * NC;
+          const int lo_row = (sg & 1) ? W + ci * NC : ci * NC;
+          for (int ks = 0; ks < KS; ++ks) {
+            float* st = out.data() + ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * slot_f;
+            for (int kc = 0; kc < 2; ++kc)
+              for (int k = 0; k < P; ++k)
+                for (int f = 0; f < 4; ++f) {
+                  const int n = 8 * ks + 4 * kc + f;
+                  if (n >= P) continue;
+                  const double a = A[(size_t)k * P + n];
+                  const float hi = rn_tf32_host(a);
+                  const float lo = rn_tf32_host(a - (double)hi);
+                  st[((size_t)kc * R + hi_row + k) * 4 + f] = hi;
+                  st[((size_t)kc * R + lo_row + k) * 4 + f] = lo;
+                }
+          }
         }
+      }
+    }
 }
 
 // slot assignment and per-class entry lists for one table
-void append_table(const HostTable& t, int P, int PP, int rho, int parity, std::vector<float>& coef,
-                  std::vector<float>& btab, std::vector<std::vector<int4>>& cls_lists) {
+void append_table(const HostTable& t, int P, int PP, int parity, std::vector<float>& coef,
+                  std::vector<const double*>& slot_src, std::vector<std::vector<int4>>& cls_lists) {
   const int64_t K = (int64_t)t.active.size();
   for (int64_t i = 0; i < K; ++i) {
     if (!t.active[i]) continue;
@@ -164,7 +194,7 @@ void append_table(const HostTable& t, int P, int PP, int rho, int parity, std::v
     const double* A = t.coeffs.data() + (size_t)i * P * P;  // [k][n]
     for (int k = 0; k < P; ++k)
       for (int n = 0; n < P; ++n) B[(size_t)n * PP + k] = (float)A[(size_t)k * P + n];
-    append_btab(A, P, rho, btab);
+    slot_src.push_back(A);
     const int ncls = (int)cls_lists.size();
     for (int c = 0; c < ncls; ++c) {
       if (parity) {
@@ -192,31 +222,7 @@ void finish_plan(Plan& p, std::vector<std::vector<int4>>& lists) {
     p.cls_start.push_back((int)p.entries.size());
     p.max_list = std::max(p.max_list, (int)l.size());
   }
-  // tcgen05 regrouping by source parity class (parity stencils only): the
-  // entry order inside a (target, source) group keeps the reference order
   p.tc = p.ncls == 8;
-  p.tc_entries.clear();
-  p.tc_grp.assign(1, 0);
-  if (!p.tc) return;
-  for (int c = 0; c < 8; ++c) {
-    const int pi[3] = {(c >> 2) & 1, (c >> 1) & 1, c & 1};
-    for (int sg = 0; sg < 8; ++sg) {
-      const int sig[3] = {(sg >> 2) & 1, (sg >> 1) & 1, sg & 1};
-      for (const int4& e : lists[c]) {
-        const int d[3] = {e.x, e.y, e.z};
-        int sh[3];
-        bool match = true;
-        for (int a = 0; a < 3; ++a) {
-          const int v = pi[a] + d[a];
-          if (((v % 2) + 2) % 2 != sig[a]) match = false;
-          sh[a] = (v - sig[a]) / 2;
-        }
-        if (!match) continue;
-        p.tc_entries.push_back(make_int2(fc2t2::tc_window_start(sh[0], sh[1], sh[2]), e.w));
-      }
-      p.tc_grp.push_back((int)p.tc_entries.size());
-    }
-  }
 }
 
 bool force_ffma() {
@@ -226,7 +232,7 @@ bool force_ffma() {
 
 // tensor-core M2L for a level: parity stencil and at least a 16^3 class lattice
 bool use_tc(const Plan& p, int level) {
-  return p.tc && p.max_list > 0 && (1 << (level + 1)) / 2 >= 16 && !force_ffma();
+  return p.tc && p.d_tcb && p.max_list > 0 && (1 << (level + 1)) / 2 >= 16 && !force_ffma();
 }
 
 size_t tc_split_floats(int rho, int level, int C) {
@@ -247,9 +253,7 @@ int plan_for(const fc2t2_engine* e, int level, int table, const Plan** out) {
 fc2t2::TCPlan tc_of(const fc2t2_engine* e, const Plan& p, int level) {
   fc2t2::TCPlan t;
   t.level = level;
-  t.btab = e->d_btab;
-  t.entries = p.d_tc_entries;
-  t.grp_start = p.d_tc_grp;
+  t.btab = p.d_tcb;
   static const char* names[] = {"m2l_tc_L0", "m2l_tc_L1", "m2l_tc_L2", "m2l_tc_L3", "m2l_tc_L4",
                                 "m2l_tc_L5", "m2l_tc_L6", "m2l_tc_L7", "m2l_tc_L8", "m2l_tc_L9"};
   t.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];
@@ -336,13 +340,11 @@ int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out) {
 void fc2t2_engine_destroy(fc2t2_engine* e) {
   if (!e) return;
   cudaFree(e->d_coef);
-  cudaFree(e->d_btab);
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
       cudaFree(t.second.d_entries);
       cudaFree(t.second.d_cls_start);
-      cudaFree(t.second.d_tc_entries);
-      cudaFree(t.second.d_tc_grp);
+      cudaFree(t.second.d_tcb);
     }
   delete e;
 }
@@ -368,20 +370,24 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
   if (!e->near.set) return fail(FC2T2_ESTAGE, "near table missing");
   for (int l = kCoarsest; l <= e->levels; ++l)
     if (!e->far.count(l) || !e->far[l].set) return fail(FC2T2_ESTAGE, "far table missing");
-  std::vector<float> coef, btab;
+  std::vector<float> coef;
+  std::vector<const double*> slot_src;
   const int P = e->P, PP = e->PP;
+  // dense tensor-core tables only where use_tc can pick the plan (class lattice >= 16^3)
+  auto tc_level = [](int l) { return (1 << (l + 1)) / 2 >= 16; };
   for (int l = kCoarsest; l <= e->levels; ++l) {
     const bool parity = l != kCoarsest;
     {
       std::vector<std::vector<int4>> lists(parity ? 8 : 1);
-      append_table(e->far[l], P, PP, e->rho, parity, coef, btab, lists);
+      append_table(e->far[l], P, PP, parity, coef, slot_src, lists);
       Plan& p = e->plans[l][FC2T2_TABLE_FAR];
       p.stride = parity ? 2 : 1;
       finish_plan(p, lists);
+      if (p.tc && tc_level(l)) build_tc_table(lists, slot_src, P, e->rho, p.tcb);
     }
     if (l == e->levels) {
       std::vector<std::vector<int4>> nl(1);
-      append_table(e->near, P, PP, e->rho, 0, coef, btab, nl);
+      append_table(e->near, P, PP, 0, coef, slot_src, nl);
       Plan& pn = e->plans[l][FC2T2_TABLE_NEAR];
       pn.stride = 1;
       finish_plan(pn, nl);
@@ -395,6 +401,7 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       Plan& pm = e->plans[l][FC2T2_TABLE_FARNEAR];
       pm.stride = pf.stride;
       finish_plan(pm, ml);
+      if (pm.tc && tc_level(l)) build_tc_table(ml, slot_src, P, e->rho, pm.tcb);
     }
   }
   cudaStream_t s = (cudaStream_t)stream;
@@ -405,11 +412,6 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
     err = cudaMemcpyAsync(e->d_coef, coef.data(), coef.size() * sizeof(float),
                           cudaMemcpyHostToDevice, s);
     if (err != cudaSuccess) return cuda_status(err, "engine_upload copy");
-    err = cudaMalloc(&e->d_btab, btab.size() * sizeof(float));
-    if (err == cudaSuccess)
-      err = cudaMemcpyAsync(e->d_btab, btab.data(), btab.size() * sizeof(float),
-                            cudaMemcpyHostToDevice, s);
-    if (err != cudaSuccess) return cuda_status(err, "engine_upload btab");
   }
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
@@ -423,20 +425,18 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       if (err == cudaSuccess)
         err = cudaMemcpyAsync(p.d_cls_start, p.cls_start.data(), p.cls_start.size() * sizeof(int),
                               cudaMemcpyHostToDevice, s);
-      if (err == cudaSuccess && p.tc) {
-        err = cudaMalloc(&p.d_tc_entries, std::max<size_t>(p.tc_entries.size(), 1) * sizeof(int2));
-        if (err == cudaSuccess) err = cudaMalloc(&p.d_tc_grp, p.tc_grp.size() * sizeof(int));
-        if (err == cudaSuccess && !p.tc_entries.empty())
-          err = cudaMemcpyAsync(p.d_tc_entries, p.tc_entries.data(),
-                                p.tc_entries.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
+      if (err == cudaSuccess && !p.tcb.empty()) {
+        err = cudaMalloc(&p.d_tcb, p.tcb.size() * sizeof(float));
         if (err == cudaSuccess)
-          err = cudaMemcpyAsync(p.d_tc_grp, p.tc_grp.data(), p.tc_grp.size() * sizeof(int),
+          err = cudaMemcpyAsync(p.d_tcb, p.tcb.data(), p.tcb.size() * sizeof(float),
                                 cudaMemcpyHostToDevice, s);
       }
       if (err != cudaSuccess) return cuda_status(err, "engine_upload plans");
     }
   err = cudaStreamSynchronize(s);
   if (err != cudaSuccess) return cuda_status(err, "engine_upload sync");
+  for (auto& lv : e->plans)
+    for (auto& t : lv.second) std::vector<float>().swap(t.second.tcb);
   e->uploaded = true;
   return FC2T2_OK;
 }

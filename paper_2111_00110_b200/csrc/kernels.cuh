@@ -47,19 +47,17 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
                 float* L, int accumulate, cudaStream_t s, float* part = nullptr, int splits = 1);
 
 // m2l_tc.cu --------------------------------------------------------------
-// tcgen05 3xTF32 M2L for parity levels; entries are {window start row, slot}
-// grouped by (target class, source class): grp_start has 8*8+1 entries.
+// tcgen05 3xTF32 M2L for parity levels.  btab is the plan's dense table:
+// [class group][source class 8][K step][slot 27][kchunk 2][row 2W][4 floats]
+// (see tc_geometry and abi.cu build_tc_table).
 struct TCPlan {
   int level;
-  const uint8_t* btab;     // [slot][kstep][BSTAGE bytes] split tables
-  const int2* entries;
-  const int* grp_start;
+  const uint8_t* btab;
   const char* level_name;
 };
 int tc_kpad(int rho);
-int tc_npad(int rho);
-int tc_bstage(int rho);
-int tc_window_start(int sx, int sy, int sz);
+// classes per CTA, N per class, K steps, bytes per slot table; 0 on success
+int tc_geometry(int rho, int* cls, int* nc, int* ks, int* bslot);
 cudaError_t split_tf32(int rho, int level, int C, const float* M, float* hi, float* lo,
                        cudaStream_t s);
 cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const float* Mlo,
