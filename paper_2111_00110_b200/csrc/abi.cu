@@ -107,6 +107,10 @@ struct fc2t2_engine {
   float* d_coef = nullptr;
   // plans[level][table]
   std::map<int, std::map<int, Plan>> plans;
+  // fork/join for fc2t2_expand: the finest-level M2L runs on `side` while the
+  // M2M chain and the coarse levels run on the caller's stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
@@ -340,6 +344,9 @@ int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out) {
 void fc2t2_engine_destroy(fc2t2_engine* e) {
   if (!e) return;
   cudaFree(e->d_coef);
+  if (e->side) cudaStreamDestroy(e->side);
+  if (e->fork) cudaEventDestroy(e->fork);
+  if (e->join) cudaEventDestroy(e->join);
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
       cudaFree(t.second.d_entries);
@@ -437,6 +444,10 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
   if (err != cudaSuccess) return cuda_status(err, "engine_upload sync");
   for (auto& lv : e->plans)
     for (auto& t : lv.second) std::vector<float>().swap(t.second.tcb);
+  err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking);
+  if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming);
+  if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming);
+  if (err != cudaSuccess) return cuda_status(err, "engine_upload streams");
   e->uploaded = true;
   return FC2T2_OK;
 }
@@ -545,31 +556,62 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
 }
 
 namespace {
-// split-K partial buffer (floats) the cascade needs for its small levels
-size_t split_floats(const fc2t2_engine* e, int channels) {
-  size_t best = 0;
-  for (auto& lv : e->plans)
-    for (auto& t : lv.second) {
-      if (t.second.max_list == 0) continue;
-      if (use_tc(t.second, lv.first)) {
-        best = std::max(best, tc_split_floats(e->rho, lv.first, channels));
-        continue;
-      }
-      const int sp = fc2t2::m2l_splits(e->rho, channels, launch_of(t.second, lv.first));
-      if (sp > 1) best = std::max(best, (size_t)sp * grid_floats(lv.first, channels, e->PP));
-    }
-  return best;
+// scratch (floats) one M2L launch of plan p needs: tcgen05 hi/lo planes or
+// split-K partial grids
+size_t part_floats(const fc2t2_engine* e, const Plan& p, int level, int channels) {
+  if (p.max_list == 0) return 0;
+  if (use_tc(p, level)) return tc_split_floats(e->rho, level, channels);
+  const int sp = fc2t2::m2l_splits(e->rho, channels, launch_of(p, level));
+  return sp > 1 ? (size_t)sp * grid_floats(level, channels, e->PP) : 0;
+}
+
+struct ExpandLayout {
+  size_t coarse_grids = 0, fine_part = 0, coarse_part = 0;
+  size_t total() const { return coarse_grids + fine_part + coarse_part; }
+};
+
+ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
+  ExpandLayout w;
+  const int L = e->levels;
+  for (int l = kCoarsest; l < L; ++l) {
+    w.coarse_grids += 2 * grid_floats(l, channels, e->PP);
+    w.coarse_part =
+        std::max(w.coarse_part, part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels));
+  }
+  w.fine_part = part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
+  return w;
+}
+
+// one level's M2L (tcgen05 or FFMA split-K) into Lg, using scratch `part`
+int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const float* M, float* Lg,
+              int accumulate, float* part, cudaStream_t s) {
+  int st;
+  if (use_tc(p, l)) {
+    float* hi = part;
+    float* lo = part + tc_split_floats(e->rho, l, channels) / 2;
+    st = cuda_status(fc2t2::split_tf32(e->rho, l, channels, M, hi, lo, s), "expand split");
+    if (st != FC2T2_OK) return st;
+    return cuda_status(fc2t2::m2l_tc(e->rho, channels, tc_of(e, p, l), hi, lo, Lg, accumulate, s),
+                       "expand m2l_tc");
+  }
+  const fc2t2::M2LLaunch ml = launch_of(p, l);
+  return cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, M, Lg, accumulate, s, part,
+                                fc2t2::m2l_splits(e->rho, channels, ml)),
+                     "expand m2l");
 }
 }  // namespace
 
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
-  if (!e || !e->uploaded) return 0;
-  size_t f = 0;
-  for (int l = kCoarsest; l < e->levels; ++l) f += 2 * grid_floats(l, channels, e->PP);
-  f += split_floats(e, channels);
-  return f * sizeof(float) + 256;
+  if (!e || !e->uploaded || channels < 1) return 0;
+  return expand_layout(e, channels).total() * sizeof(float) + 256;
 }
 
+// L_finest = M2L_finest(M_finest) + L2L(L_{finest-1}); the coarse chain
+// (M2M down, then per level L2L + M2L) and the finest M2L are independent, so
+// the finest M2L runs on the engine's side stream (fork/join by events) and
+// the coarse kernels fill the SMs its last wave leaves idle.  The summation
+// order is fixed (M2L written first, L2L accumulated after the join), so
+// results do not depend on the overlap.
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream) {
   if (!e || !e->uploaded) return fail(FC2T2_ESTAGE, "engine tables not uploaded");
@@ -578,6 +620,7 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
     return fail(FC2T2_EWORKSPACE, "expand workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
   const int L = e->levels;
+  const ExpandLayout lay = expand_layout(e, channels);
   std::vector<float*> Mg(L + 1, nullptr), Lg(L + 1, nullptr);
   float* w = (float*)d_ws;
   for (int l = kCoarsest; l < L; ++l) {
@@ -588,7 +631,8 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
   }
   Mg[L] = const_cast<float*>(d_m_finest);
   Lg[L] = d_l_finest;
-  float* part = w;  // split-K partials (split_floats)
+  float* fine_part = w;
+  float* coarse_part = w + lay.fine_part;
   // lowest level whose far table does any work (coarser M grids are unused)
   int lowest = L;
   for (int l = kCoarsest; l <= L; ++l) {
@@ -598,42 +642,60 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
       break;
     }
   }
+  const Plan& pL = e->plans.at(L).at(FC2T2_TABLE_FARNEAR);
+  const bool fine = pL.max_list > 0, coarse = lowest < L;
+  const bool overlap = fine && coarse && e->side;
   int st;
-  for (int l = L; l > lowest; --l) {
-    st = cuda_status(fc2t2::m2m(e->rho, l, channels, Mg[l], Mg[l - 1], s), "expand m2m");
+  if (overlap) {
+    st = cuda_status(cudaEventRecord(e->fork, s), "expand fork");
+    if (st == FC2T2_OK) st = cuda_status(cudaStreamWaitEvent(e->side, e->fork, 0), "expand fork");
     if (st != FC2T2_OK) return st;
   }
-  bool have = false;
-  for (int l = lowest; l <= L; ++l) {
-    const int table = (l == L) ? FC2T2_TABLE_FARNEAR : FC2T2_TABLE_FAR;
-    const Plan& p = e->plans.at(l).at(table);
-    if (have) {
-      st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, Lg[l - 1], Lg[l], 0, s), "expand l2l");
+  if (fine) {
+    st = level_m2l(e, channels, L, pL, Mg[L], Lg[L], 0, fine_part, overlap ? e->side : s);
+    if (st != FC2T2_OK) return st;
+    if (overlap) {
+      st = cuda_status(cudaEventRecord(e->join, e->side), "expand join");
       if (st != FC2T2_OK) return st;
     }
-    if (p.max_list > 0 && use_tc(p, l)) {
-      float* hi = part;
-      float* lo = part + tc_split_floats(e->rho, l, channels) / 2;
-      st = cuda_status(fc2t2::split_tf32(e->rho, l, channels, Mg[l], hi, lo, s), "expand split");
-      if (st != FC2T2_OK) return st;
-      st = cuda_status(
-          fc2t2::m2l_tc(e->rho, channels, tc_of(e, p, l), hi, lo, Lg[l], have ? 1 : 0, s),
-          "expand m2l_tc");
-      if (st != FC2T2_OK) return st;
-      have = true;
-    } else if (p.max_list > 0) {
-      const fc2t2::M2LLaunch ml = launch_of(p, l);
-      st = cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, Mg[l], Lg[l], have ? 1 : 0, s,
-                                  part, fc2t2::m2l_splits(e->rho, channels, ml)),
-                       "expand m2l");
-      if (st != FC2T2_OK) return st;
-      have = true;
-    } else if (!have && l == L) {
-      st = cuda_status(
-          cudaMemsetAsync(Lg[L], 0, grid_floats(L, channels, e->PP) * sizeof(float), s),
-          "expand zero");
+  }
+  if (coarse) {
+    for (int l = L; l > lowest; --l) {
+      st = cuda_status(fc2t2::m2m(e->rho, l, channels, Mg[l], Mg[l - 1], s), "expand m2m");
       if (st != FC2T2_OK) return st;
     }
+    bool have = false;
+    for (int l = lowest; l < L; ++l) {
+      const Plan& p = e->plans.at(l).at(FC2T2_TABLE_FAR);
+      if (have) {
+        st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, Lg[l - 1], Lg[l], 0, s), "expand l2l");
+        if (st != FC2T2_OK) return st;
+      }
+      if (p.max_list > 0) {
+        st = level_m2l(e, channels, l, p, Mg[l], Lg[l], have ? 1 : 0, coarse_part, s);
+        if (st != FC2T2_OK) return st;
+        have = true;
+      } else if (have == false) {
+        // nothing at this level yet: the next L2L needs a zero grid
+        st = cuda_status(
+            cudaMemsetAsync(Lg[l], 0, grid_floats(l, channels, e->PP) * sizeof(float), s),
+            "expand zero");
+        if (st != FC2T2_OK) return st;
+        have = true;
+      }
+    }
+    if (overlap) {
+      st = cuda_status(cudaStreamWaitEvent(s, e->join, 0), "expand join");
+      if (st != FC2T2_OK) return st;
+    }
+    st = cuda_status(fc2t2::l2l(e->rho, L - 1, channels, Lg[L - 1], Lg[L], fine ? 1 : 0, s),
+                     "expand l2l");
+    if (st != FC2T2_OK) return st;
+  } else if (!fine) {
+    st = cuda_status(
+        cudaMemsetAsync(Lg[L], 0, grid_floats(L, channels, e->PP) * sizeof(float), s),
+        "expand zero");
+    if (st != FC2T2_OK) return st;
   }
   return FC2T2_OK;
 }
