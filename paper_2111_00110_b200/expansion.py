@@ -87,50 +87,75 @@ def to_device(x, cols: int | None = None, points: bool = False) -> torch.Tensor:
 
 
 class HostIO:
-    """Host <-> device staging for host-tensor callers: copies run on a
-    dedicated stream so they overlap the expansion work on the compute
-    stream; results land in pinned buffers (torch's caching host allocator)."""
+    """Host <-> device staging for host-tensor callers.  Uploads run on an
+    "up" stream and downloads on a "down" stream, so the two PCIe directions
+    overlap each other and the compute stream; results land in pinned buffers
+    (torch's caching host allocator).  ``h2d(..., chunks=k)`` splits an upload
+    by rows with one ready event per chunk, letting per-chunk consumers start
+    while the rest is in flight."""
 
     _streams: dict = {}
+    _aux: dict = {}
 
     @classmethod
-    def stream(cls) -> torch.cuda.Stream:
+    def aux(cls) -> torch.cuda.Stream:
+        """A second compute stream for work that overlaps the main one."""
+        dev = torch.cuda.current_device()
+        if dev not in cls._aux:
+            cls._aux[dev] = torch.cuda.Stream(device=dev)
+        return cls._aux[dev]
+
+    @classmethod
+    def _pair(cls):
         dev = torch.cuda.current_device()
         if dev not in cls._streams:
-            cls._streams[dev] = torch.cuda.Stream(device=dev)
+            cls._streams[dev] = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
         return cls._streams[dev]
 
     @classmethod
-    def h2d(cls, x: torch.Tensor, cols: int | None = None):
-        """Async upload of a host tensor; returns (device tensor, ready event)."""
+    def h2d(cls, x: torch.Tensor, cols: int | None = None, chunks: int = 1):
+        """Async upload of a host tensor.  Returns (device tensor, ready event)
+        for chunks == 1, else (device tensor, [(row0, row1, event), ...])."""
         cs = torch.cuda.current_stream()
-        s = cls.stream()
+        up, _ = cls._pair()
         src = x if x.is_pinned() else x.pin_memory()
-        with torch.cuda.stream(s):
-            t = torch.empty(tuple(src.shape), dtype=torch.float32, device=_device())
-            t.copy_(src, non_blocking=True)
-        ev = s.record_event()
-        t.record_stream(cs)
         if cols is not None:
-            t = t.reshape(-1, cols)
-        return t, ev
+            src = src.reshape(-1, cols)
+        n = int(src.shape[0]) if src.dim() else 1
+        k = max(1, min(int(chunks), n)) if n else 1
+        bounds = [(n * i) // k for i in range(k + 1)]
+        with torch.cuda.stream(up):
+            t = torch.empty(tuple(src.shape), dtype=torch.float32, device=_device())
+            evs = []
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                if b > a:
+                    t[a:b].copy_(src[a:b], non_blocking=True)
+                evs.append((a, b, up.record_event()))
+        t.record_stream(cs)
+        if chunks == 1:
+            return t, evs[-1][2]
+        return t, evs
 
     @classmethod
-    def d2h(cls, t: torch.Tensor) -> torch.Tensor:
-        """Start an async download after the current stream's work; call
-        finish() before the host reads the result."""
+    def d2h(cls, t: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Start an async download of ``t`` after the current stream's work
+        (into ``out`` if given, else a new pinned tensor); call finish()
+        before the host reads the result."""
         cs = torch.cuda.current_stream()
-        s = cls.stream()
-        s.wait_stream(cs)
-        out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
-        with torch.cuda.stream(s):
+        _, down = cls._pair()
+        down.wait_stream(cs)
+        if out is None:
+            out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+        with torch.cuda.stream(down):
             out.copy_(t, non_blocking=True)
-        t.record_stream(s)
+        t.record_stream(down)
         return out
 
     @classmethod
     def finish(cls) -> None:
-        cls.stream().synchronize()
+        up, down = cls._pair()
+        down.synchronize()
+        up.synchronize()
 
 
 def is_host_tensor(x) -> bool:

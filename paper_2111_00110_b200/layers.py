@@ -57,9 +57,87 @@ class ExplicitResult:
 COHERENT_L2P_BYTES = 64 << 20
 
 
+def _sorts(res: "ExplicitResult"):
+    """(p sort, q sort) of an explicit result; the query sort is computed on
+    first use (the forward skips it unless its L2P needs the coherent order)."""
+    p_sort, q_sort = res.sorts
+    if q_sort is None:
+        q_sort = res.engine.sort_points(res.q_dev)
+        res.sorts = (p_sort, q_sort)
+    return p_sort, q_sort
+
+
 def _coherent(acc: Accessor, sort):
     st = acc.grid.storage
     return sort[0] if st.numel() * st.element_size() > COHERENT_L2P_BYTES else None
+
+
+# Host-tensor callers: the per-point streams (q, y_bar up; values, q_bar down)
+# move in HOST_CHUNKS row chunks so PCIe uploads, downloads (separate streams,
+# both directions at once) and the L2P of finished chunks overlap each other
+# and the expansions.  Cell-coherent L2P (grids beyond L2) needs the whole
+# point set, so it runs unchunked.
+HOST_CHUNKS = 8
+
+
+def _explicit_forward_host(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
+    qd, chunks = HostIO.h2d(q, 3, chunks=HOST_CHUNKS)
+    p_sort = engine.sort_points(sources.p)
+    acc = engine.expand_device(sources.p, sources.w, p_sort)
+    cs = torch.cuda.current_stream()
+    coherent = acc.grid.storage.numel() * 4 > COHERENT_L2P_BYTES
+    out = torch.empty((qd.shape[0], acc.channels), dtype=torch.float32, pin_memory=True)
+    if not coherent:
+        for a, b, ev in chunks:
+            cs.wait_event(ev)
+            if b > a:
+                HostIO.d2h(acc.eval_device(qd[a:b], _lib.L2P_VALUE)["value"], out[a:b])
+        q_sort = None      # sorted lazily by the backward (hidden under the y_bar upload)
+    else:
+        cs.wait_event(chunks[-1][2])
+        q_sort = engine.sort_points(qd)
+        HostIO.d2h(acc.eval_device(qd, _lib.L2P_VALUE, order=q_sort[0])["value"], out)
+    HostIO.finish()
+    engine.flag.raise_if_set("source/query")
+    return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine, q_dev=qd,
+                          sorts=(p_sort, q_sort))
+
+
+def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
+    eng, qd, src, acc = res.engine, res.q_dev, res.sources, res.accessor
+    yb, chunks = HostIO.h2d(y_bar, acc.channels, chunks=HOST_CHUNKS)
+    cs = torch.cuda.current_stream()
+    p_sort, q_sort = res.sorts
+    aux = None
+    if q_sort is None:
+        # the query sort runs beside the per-chunk q_bar L2Ps, under the y_bar upload
+        aux = HostIO.aux()
+        aux.wait_stream(cs)
+        with torch.cuda.stream(aux):
+            q_sort = eng.sort_points(qd)
+        for t in q_sort:
+            t.record_stream(cs)
+        res.sorts = (p_sort, q_sort)
+    q_bar = torch.empty((qd.shape[0], 3), dtype=torch.float32, pin_memory=True)
+    order = _coherent(acc, q_sort)
+    if order is None:
+        for a, b, ev in chunks:
+            cs.wait_event(ev)
+            if b > a:
+                HostIO.d2h(acc.eval_device(qd[a:b], _lib.L2P_WGRAD, wts=yb[a:b])["wgrad"],
+                           q_bar[a:b])
+    else:
+        cs.wait_event(chunks[-1][2])
+        HostIO.d2h(acc.eval_device(qd, _lib.L2P_WGRAD, wts=yb, order=order)["wgrad"], q_bar)
+    if aux is not None:
+        cs.wait_stream(aux)
+    back = eng.expand_device(qd, yb, q_sort)
+    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
+                           order=_coherent(back, p_sort))
+    w_bar, p_bar = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
+    HostIO.finish()
+    eng.flag.raise_if_set("source/query")
+    return LayerGradients(w_bar=w_bar, p_bar=p_bar, q_bar=q_bar)
 
 
 def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
@@ -68,49 +146,25 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     # p's by P2M now and by the source-side L2P of the backward, q's by the
     # query L2Ps (cell-coherent order) and by the backward P2M of q.
     if is_host_tensor(q):
-        # host tensors: the query upload overlaps the source expansion
-        qd, q_ready = HostIO.h2d(q, 3)
-        p_sort = engine.sort_points(sources.p)
-        acc = engine.expand_device(sources.p, sources.w, p_sort)
-        torch.cuda.current_stream().wait_event(q_ready)
-        q_sort = engine.sort_points(qd)
-        vals = acc.eval_device(qd, _lib.L2P_VALUE, order=_coherent(acc, q_sort))["value"]
-        out = HostIO.d2h(vals)
-        HostIO.finish()
-        engine.flag.raise_if_set("source/query")
-        return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine,
-                              q_dev=qd, sorts=(p_sort, q_sort))
+        return _explicit_forward_host(engine, sources, q)
     qd = to_device(q, 3, points=True)
     p_sort = engine.sort_points(sources.p)
     acc = engine.expand_device(sources.p, sources.w, p_sort)
-    q_sort = engine.sort_points(qd)
-    vals = acc.eval_device(qd, _lib.L2P_VALUE, order=_coherent(acc, q_sort))["value"]
+    coherent = acc.grid.storage.numel() * 4 > COHERENT_L2P_BYTES
+    q_sort = engine.sort_points(qd) if coherent else None   # else sorted by the backward
+    vals = acc.eval_device(qd, _lib.L2P_VALUE, order=q_sort[0] if coherent else None)["value"]
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=like_input(vals, q), accessor=acc, q=q, sources=sources,
                           engine=engine, q_dev=qd, sorts=(p_sort, q_sort))
 
 
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
+    if is_host_tensor(y_bar):
+        return _explicit_jvp_host(y_bar, res)
     eng = res.engine
     qd = res.q_dev
     src = res.sources
-    p_sort, q_sort = res.sorts
-    if is_host_tensor(y_bar):
-        # host tensors: q_bar's download overlaps the backward expansion
-        yb, y_ready = HostIO.h2d(y_bar)
-        torch.cuda.current_stream().wait_event(y_ready)
-        yb = yb.reshape(qd.shape[0], -1)
-        q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb,
-                                         order=_coherent(res.accessor, q_sort))["wgrad"]
-        q_bar_h = HostIO.d2h(q_bar)
-        back = eng.expand_device(qd, yb, q_sort)
-        out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
-                               order=_coherent(back, p_sort),
-                               )
-        w_bar_h, p_bar_h = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
-        HostIO.finish()
-        eng.flag.raise_if_set("source/query")
-        return LayerGradients(w_bar=w_bar_h, p_bar=p_bar_h, q_bar=q_bar_h)
+    p_sort, q_sort = _sorts(res)
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
     q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb,
                                      order=_coherent(res.accessor, q_sort))["wgrad"]

@@ -223,6 +223,32 @@ def test_explicit_torch_io_and_counts(eng4):
     assert rel_l2(_np(g.q_bar), qb) < TOL
 
 
+@pytest.mark.parametrize("coherent", [False, True])
+@pytest.mark.parametrize("m", [5001, 5])
+def test_explicit_host_tensors_match_device(eng4, monkeypatch, coherent, m):
+    """Host (pinned / pageable) torch inputs take the chunked duplex-copy path
+    (layers._explicit_*_host); every output must equal the device path bit for
+    bit, for ragged chunk sizes and for the unchunked cell-coherent branch."""
+    import paper_2111_00110_b200.layers as layers
+    from paper_2111_00110_b200 import SourceSet
+    if coherent:
+        monkeypatch.setattr(layers, "COHERENT_L2P_BYTES", 0)
+    rng = np.random.default_rng(7)
+    p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32))
+    w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32))
+    q = torch.from_numpy(rng.uniform(-1, 1, (m, 3)).astype(np.float32))
+    yb = torch.from_numpy(rng.normal(size=(m, 2)).astype(np.float32))
+    rd = layers.explicit_forward(eng4, SourceSet(p.cuda(), w.cuda()), q.cuda())
+    gd = layers.explicit_jvp(yb.cuda(), rd)
+    rh = layers.explicit_forward(eng4, SourceSet(p, w), q.pin_memory())
+    gh = layers.explicit_jvp(yb, rh)          # pageable: staged through a pinned copy
+    assert not rh.values.is_cuda and not gh.q_bar.is_cuda
+    assert torch.equal(rh.values, rd.values.cpu())
+    assert torch.equal(gh.q_bar, gd.q_bar.cpu())
+    assert torch.equal(gh.w_bar, gd.w_bar.cpu())
+    assert torch.equal(gh.p_bar, gd.p_bar.cpu())
+
+
 def test_explicit_config2_full_size_properties(cuda):
     """Config 2 at full size (N=2^20, M=10^7, level 5): size-independent
     checks -- the adjoint (dot-product) identity <y, G w> = <w, G^T y> of the
