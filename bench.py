@@ -219,16 +219,24 @@ def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
     out = None
+    host = 0.0
     for i in range(steps):
         flush.fill_(i & 0xFF)
         ev[i][0].record(stream)
+        h0 = time.perf_counter()
         out = fn()
+        host += time.perf_counter() - h0
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     if stages is not None:
         stages.update({k: round(v[0] / steps, 4) for k, v in _lib.profile_read().items()})
+        stages["_host_call_ms"] = round(1e3 * host / steps, 4)
         _lib.profile_enable(False)
-    return float(sum(a.elapsed_time(b) for a, b in ev)), out
+    per = sorted(a.elapsed_time(b) for a, b in ev)
+    if stages is not None:
+        stages["_step_ms_median"] = round(per[len(per) // 2], 4)
+        stages["_step_ms_max"] = round(per[-1], 4)
+    return float(sum(per)), out
 
 
 def secondary(dev, flush, stream, steps: int) -> dict:

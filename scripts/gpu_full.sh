@@ -1,6 +1,5 @@
-set -x
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -4
-timeout 120 python __graft_entry__.py smoke 2>&1 | tail -2
-timeout 600 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench rc=$?; tail -3 gpurun_out/bench_full.err
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?; tail -3 gpurun_out/bench_ref.err
-nproc; lscpu | grep "Model name"
+# full round check: GPU tests, smoke, default bench, reference arm
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -4
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo bench rc=$?; tail -2 gpurun_out/bench_full.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?; tail -2 gpurun_out/bench_ref.err
