@@ -113,6 +113,13 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream);
+/* Same cascade, but only finest-level cells with x in [x_begin, x_end) are
+ * produced (multiples of 4; x_end < 0 = res): the x-slab of one rank in the
+ * multi-GPU cascade; the caller all-gathers the slabs.  Other
+ * finest cells of d_l_finest are left unspecified.  Same workspace. */
+int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                      float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
+                      void* stream);
 
 /* ---- L2P: Accessor (expansion.py:335-373) ----
  * d_order (optional, n int32): evaluate the points in this (cell-sorted) order;

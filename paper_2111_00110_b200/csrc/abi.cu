@@ -583,15 +583,18 @@ ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
 }
 
 // one level's M2L (tcgen05 or FFMA split-K) into Lg, using scratch `part`
+// x_begin/x_end restrict the tcgen05 path's targets to an x-slab of cells
+// (fc2t2_expand_slab); the FFMA path always covers the whole grid.
 int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const float* M, float* Lg,
-              int accumulate, float* part, cudaStream_t s) {
+              int accumulate, float* part, cudaStream_t s, int x_begin = 0, int x_end = -1) {
   int st;
   if (use_tc(p, l)) {
     float* hi = part;
     float* lo = part + tc_split_floats(e->rho, l, channels) / 2;
     st = cuda_status(fc2t2::split_tf32(e->rho, l, channels, M, hi, lo, s), "expand split");
     if (st != FC2T2_OK) return st;
-    return cuda_status(fc2t2::m2l_tc(e->rho, channels, tc_of(e, p, l), hi, lo, Lg, accumulate, s),
+    return cuda_status(fc2t2::m2l_tc(e->rho, channels, tc_of(e, p, l), hi, lo, Lg, accumulate, s,
+                                     x_begin, x_end),
                        "expand m2l_tc");
   }
   const fc2t2::M2LLaunch ml = launch_of(p, l);
@@ -614,8 +617,21 @@ size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
 // results do not depend on the overlap.
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream) {
+  return fc2t2_expand_slab(e, channels, d_m_finest, d_l_finest, 0, -1, d_ws, ws_bytes, stream);
+}
+
+// Only the finest-level cells with x in [x_begin, x_end) are guaranteed (the
+// rest of d_l_finest is unspecified): the multi-GPU cascade gives each rank an
+// x-slab of the dominant finest-level M2L and all-gathers the slabs.
+int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                      float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
+                      void* stream) {
   if (!e || !e->uploaded) return fail(FC2T2_ESTAGE, "engine tables not uploaded");
   if (channels < 1) return fail(FC2T2_EVALUE, "channels must be >= 1");
+  const int res_f = 1 << (e->levels + 1);
+  if (x_end < 0) x_end = res_f;
+  if (x_begin < 0 || x_end > res_f || x_begin > x_end || x_begin % 4 || x_end % 4)
+    return fail(FC2T2_EVALUE, "slab bounds must be multiples of 4 inside [0, res]");
   if (ws_bytes < fc2t2_expand_workspace_size(e, channels))
     return fail(FC2T2_EWORKSPACE, "expand workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
@@ -652,7 +668,8 @@ int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
     if (st != FC2T2_OK) return st;
   }
   if (fine) {
-    st = level_m2l(e, channels, L, pL, Mg[L], Lg[L], 0, fine_part, overlap ? e->side : s);
+    st = level_m2l(e, channels, L, pL, Mg[L], Lg[L], 0, fine_part, overlap ? e->side : s,
+                   x_begin, x_end);
     if (st != FC2T2_OK) return st;
     if (overlap) {
       st = cuda_status(cudaEventRecord(e->join, e->side), "expand join");

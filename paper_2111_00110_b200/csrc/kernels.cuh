@@ -60,8 +60,9 @@ int tc_kpad(int rho);
 int tc_geometry(int rho, int* cls, int* nc, int* ks, int* bslot);
 cudaError_t split_tf32(int rho, int level, int C, const float* M, float* hi, float* lo,
                        cudaStream_t s);
+// targets restricted to cells with x in [x_begin, x_end) (multiples of 4; x_end < 0 = res)
 cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const float* Mlo,
-                   float* L, int accumulate, cudaStream_t s);
+                   float* L, int accumulate, cudaStream_t s, int x_begin = 0, int x_end = -1);
 
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {

@@ -216,7 +216,7 @@ template <int RHO>
 __global__ void __launch_bounds__(512, 1)
 m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, float* __restrict__ L, int res, int nu, int C,
-              int accumulate) {
+              int accumulate, int ux_begin) {
   using T = TC<RHO>;
   constexpr int W = T::W, NS = T::NS, KS = T::KS, TILES = T::TILES, CW = T::CW;
   constexpr int WROWS = T::WROWS, WY = T::WY, WZ = T::WZ;
@@ -232,7 +232,7 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
   const int chan = blockIdx.z;
   const int nyb = nu / T::TY, nzb = nu / T::TZ;
   const int bid = blockIdx.x;
-  const int ux0 = (bid / (nyb * nzb)) * TILES;
+  const int ux0 = ux_begin + (bid / (nyb * nzb)) * TILES;
   const int uy0 = ((bid / nzb) % nyb) * T::TY;
   const int uz0 = (bid % nzb) * T::TZ;
 
@@ -457,21 +457,26 @@ cudaError_t split_tf32(int rho, int level, int C, const float* M, float* hi, flo
 }
 
 cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const float* Mlo,
-                   float* L, int accumulate, cudaStream_t s) {
+                   float* L, int accumulate, cudaStream_t s, int x_begin, int x_end) {
   const int res = 1 << (plan.level + 1);
   const int nu = res / 2;
-  if (nu % 16 != 0) return cudaErrorInvalidValue;
+  if (x_end < 0) x_end = res;
+  // target cells with x in [x_begin, x_end): class-lattice planes [x_begin/2, x_end/2)
+  if (nu % 16 != 0 || x_begin < 0 || x_end > res || x_begin % 4 || x_end % 4)
+    return cudaErrorInvalidValue;
+  if (x_end <= x_begin) return cudaSuccess;
+  const int ux_begin = x_begin / 2, ux_count = (x_end - x_begin) / 2;
   FC2T2_DISPATCH_RHO(rho, {
     using T = TC<RHO>;
     auto kern = m2l_tc_kernel<RHO>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)T::SMEM);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((nu / T::TILES) * (nu / T::TY) * (nu / T::TZ)), (unsigned)(8 / T::CLS),
-              (unsigned)C);
+    dim3 grid((unsigned)((ux_count / T::TILES) * (nu / T::TY) * (nu / T::TZ)),
+              (unsigned)(8 / T::CLS), (unsigned)C);
     FC2T2_LAUNCH(plan.level_name, s,
                  kern<<<grid, T::THREADS, T::SMEM, s>>>(Mhi, Mlo, plan.btab, L, res, nu, C,
-                                                        accumulate));
+                                                        accumulate, ux_begin));
   });
   return cudaGetLastError();
 }

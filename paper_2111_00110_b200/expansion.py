@@ -485,14 +485,18 @@ class Engine:
                 self.flops.add("l2l", flops.translate_flops(level_resolution(level - 1), P))
         self.flops.add("m2l", self._pairs[("near", self.levels)] * channels * P * P * 2)
 
-    def cascade_device(self, m_finest: torch.Tensor) -> torch.Tensor:
-        """M2M / M2L / L2L in one C-ABI call; returns the finest L storage."""
+    def cascade_device(self, m_finest: torch.Tensor, x_range: tuple | None = None) -> torch.Tensor:
+        """M2M / M2L / L2L in one C-ABI call; returns the finest L storage.
+        ``x_range=(x0, x1)`` (multiples of 4) computes only the finest cells
+        with x in [x0, x1) -- one rank's slab of the sharded cascade; the rest
+        of the returned grid is unspecified."""
         C = int(m_finest.shape[3])
         out = torch.empty_like(m_finest)
         ws_bytes = _lib.lib().fc2t2_expand_workspace_size(self.handle, C)
         ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=m_finest.device)
-        _lib.call("fc2t2_expand", self.handle, C, _ptr(m_finest), _ptr(out), _ptr(ws),
-                  int(ws_bytes), _stream())
+        x0, x1 = (0, -1) if x_range is None else (int(x_range[0]), int(x_range[1]))
+        _lib.call("fc2t2_expand_slab", self.handle, C, _ptr(m_finest), _ptr(out), x0, x1,
+                  _ptr(ws), int(ws_bytes), _stream())
         self.expansion_count += 1
         self._tally_cascade(C)
         return out

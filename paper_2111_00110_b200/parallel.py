@@ -1,21 +1,25 @@
 """Data-parallel sharding of the explicit layer across GPUs.
 
 Sources and queries are independent units: each rank owns a shard of the
-sources (p, w) and of the queries (q, y_bar).  The only exchange step is the
-finest moment grid -- each rank's P2M of its shard is summed with one
-all-reduce (NCCL over NVLink on B200s; gloo in the CPU tests) -- after which
-every rank holds the global field and evaluates its own queries / sources with
-no further communication:
+sources (p, w) and of the queries (q, y_bar).  Per expansion there are two
+exchange steps on the finest grids (NCCL over NVLink on B200s; gloo in the CPU
+tests):
 
-    forward   M_r = P2M(p_r, w_r);  M = allreduce(M_r);  L = cascade(M);  f(q_r)
-    backward  B_r = P2M(q_r, y_r);  B = allreduce(B_r);  G = cascade(B);
-              w_bar_r = G(p_r),  p_bar_r = w_r grad G(p_r),  q_bar_r = y_r grad f(q_r)
+    M   = allreduce_r P2M(p_r, w_r)             full finest moments on every rank
+    L_r = cascade(M) on the x-slab r             coarse levels replicated (cheap),
+                                                 finest M2L only for x in slab r
+    L   = allgather_r L_r                        slabs are contiguous (x is the
+                                                 slowest grid axis)
+    f(q_r), and in the backward the same with (q_r, y_r), then G(p_r), grad G(p_r)
 
-The cascade is replicated (per-GPU work constant under weak scaling; the
-all-reduce of 37.7 MB at config 2 costs ~0.1 ms over NVLink).  The compute
-backend is any object with ``p2m_grid``, ``cascade_grid``, ``evaluate`` (the
-device Engine adapter below; tests/test_parallel_gloo.py plugs the CPU oracle
-in to check the sharding logic on CPU with world size 2).
+The dominant finest-level M2L (about 80% of a cascade) is thus divided among
+the ranks instead of replicated; the all-reduce provides every rank with the
+halo planes its slab's M2L reads.  Slabs are multiples of 4 cells (two class
+lattice planes, the tensor-core kernel's tile pair); when the grid does not
+split evenly the cascade falls back to replication.  The compute backend is
+any object with ``p2m_grid``, ``cascade_grid(m, x_range=None)``, ``evaluate``
+(the device Engine adapter below; tests/test_parallel_gloo.py plugs the CPU
+oracle in to check the sharding logic on CPU with world size 2).
 """
 
 from __future__ import annotations
@@ -44,8 +48,8 @@ class DeviceBackend:
     def p2m_grid(self, p: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
         return self.engine.p2m_device(p, w).storage
 
-    def cascade_grid(self, m: torch.Tensor) -> torch.Tensor:
-        return self.engine.cascade_device(m)
+    def cascade_grid(self, m: torch.Tensor, x_range: tuple | None = None) -> torch.Tensor:
+        return self.engine.cascade_device(m, x_range)
 
     def evaluate(self, L: torch.Tensor, pts: torch.Tensor, wts: torch.Tensor | None, value: bool):
         from .expansion import Accessor, ExpansionGrid
@@ -72,10 +76,35 @@ def _allreduce(t: torch.Tensor, group) -> torch.Tensor:
     return t
 
 
+def slab_range(res: int, rank: int, world: int) -> tuple[int, int] | None:
+    """This rank's x-slab [x0, x1) of the finest grid, or None when res does
+    not split into equal multiples of 4 cells."""
+    if res % 4 or (res // 4) % world:
+        return None
+    width = res // world
+    return rank * width, (rank + 1) * width
+
+
+def _cascade(backend, m: torch.Tensor, group) -> torch.Tensor:
+    """Finest L on every rank: each rank computes its x-slab, one all-gather."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return backend.cascade_grid(m)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    sl = slab_range(int(m.shape[0]), rank, world)
+    if sl is None:
+        return backend.cascade_grid(m)
+    L = backend.cascade_grid(m, sl)
+    mine = L[sl[0]:sl[1]]
+    if dist.get_backend(group) != "nccl":
+        mine = mine.clone()     # NCCL gathers in place; gloo wants a separate input
+    dist.all_gather_into_tensor(L, mine, group=group)
+    return L
+
+
 def explicit_forward_sharded(backend, p, w, q, group=None) -> ShardedExplicitResult:
     """Forward of the explicit layer on this rank's shards (see module doc)."""
     m = _allreduce(backend.p2m_grid(p, w), group)
-    L = backend.cascade_grid(m)
+    L = _cascade(backend, m, group)
     values, _ = backend.evaluate(L, q, None, True)
     return ShardedExplicitResult(values=values, L=L, q=q, p=p, w=w)
 
@@ -84,6 +113,6 @@ def explicit_jvp_sharded(backend, y_bar, res: ShardedExplicitResult, group=None)
     """(w_bar_r, p_bar_r, q_bar_r) for this rank's shards."""
     _, q_bar = backend.evaluate(res.L, res.q, y_bar, False)
     b = _allreduce(backend.p2m_grid(res.q, y_bar), group)
-    G = backend.cascade_grid(b)
+    G = _cascade(backend, b, group)
     w_bar, p_bar = backend.evaluate(G, res.p, res.w, True)
     return w_bar, p_bar, q_bar

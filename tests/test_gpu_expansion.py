@@ -298,3 +298,25 @@ def test_m2l_tensor_core_level5_matches_oracle(cuda):
     far = eng.m2l_tables["far"][5]
     tc = _np(eng.m2l(m, far).data)
     assert rel_l2(tc, ora.m2l(_np(m.data), ora.tables["far"][5])) < TOL
+
+
+def test_expand_slabs_assemble_full_cascade(cuda):
+    """fc2t2_expand_slab (one rank's x-slab of the sharded cascade, SURVEY
+    8(e)): the finest cells of every slab equal the full cascade bit for bit
+    (level 5, tcgen05 finest level), so the multi-GPU all-gather reproduces
+    the single-GPU grid exactly."""
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    p = torch.rand(200_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(200_000, 1, device="cuda", generator=gen)
+    m = eng.p2m_device(p, w).storage
+    full = eng.cascade_device(m)
+    res = full.shape[0]
+    for world in (2, 8):
+        width = res // world
+        parts = [eng.cascade_device(m, (r * width, (r + 1) * width))[r * width:(r + 1) * width]
+                 for r in range(world)]
+        assert torch.equal(torch.cat(parts), full)
+    with pytest.raises(Exception):
+        eng.cascade_device(m, (2, 16))        # not a multiple of 4

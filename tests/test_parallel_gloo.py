@@ -16,18 +16,26 @@ import torch.multiprocessing as mp
 
 from oracle.fc2t2_oracle import Oracle
 from paper_2111_00110_b200.parallel import (explicit_forward_sharded, explicit_jvp_sharded,
-                                            shard_range)
+                                            shard_range, slab_range)
 
 
 class OracleBackend:
     def __init__(self, ora):
         self.o = ora
+        self.slabs = []
 
     def p2m_grid(self, p, w):
         return torch.from_numpy(self.o.p2m(p.numpy(), w.numpy()))
 
-    def cascade_grid(self, m):
-        return torch.from_numpy(self.o.cascade(m.numpy()))
+    def cascade_grid(self, m, x_range=None):
+        L = torch.from_numpy(self.o.cascade(m.numpy()))
+        if x_range is not None:
+            # outside this rank's slab the grid is unspecified: poison it so
+            # the test proves the all-gather assembles only owned slabs
+            L[:x_range[0]] = float("nan")
+            L[x_range[1]:] = float("nan")
+            self.slabs.append(tuple(x_range))
+        return L
 
     def evaluate(self, L, pts, wts, value):
         Ln, x = L.numpy(), pts.numpy()
@@ -61,7 +69,8 @@ def _worker(rank, world, port, out):
         res = explicit_forward_sharded(be, t(p[a:b]), t(w[a:b]), t(q[c:d]))
         wb, pb, qb = explicit_jvp_sharded(be, t(yb[c:d]), res)
         np.savez(os.path.join(out, f"rank{rank}.npz"), values=res.values.numpy(),
-                 w_bar=wb.numpy(), p_bar=pb.numpy(), q_bar=qb.numpy())
+                 w_bar=wb.numpy(), p_bar=pb.numpy(), q_bar=qb.numpy(),
+                 slabs=np.array(be.slabs))
     finally:
         dist.destroy_process_group()
 
@@ -90,3 +99,12 @@ def test_two_rank_explicit_layer_matches_single_process(tmp_path):
     for got, ref in ((cat("values"), values), (cat("w_bar"), w_bar), (cat("p_bar"), p_bar),
                      (cat("q_bar"), q_bar)):
         assert np.allclose(got, ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
+    # each rank computed only its own x-slab of the level-3 (16^3) grid, twice
+    assert [tuple(map(tuple, x["slabs"])) for x in r] == [((0, 8), (0, 8)), ((8, 16), (8, 16))]
+
+
+def test_slab_range():
+    assert [slab_range(128, r, 8) for r in range(8)] == [(16 * r, 16 * r + 16) for r in range(8)]
+    assert slab_range(64, 1, 2) == (32, 64)
+    assert slab_range(16, 0, 3) is None      # 4 units do not split over 3 ranks
+    assert slab_range(16, 3, 4) == (12, 16)
