@@ -484,7 +484,8 @@ def run_ours(args, rank: int, world: int) -> None:
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
                      "flops_per_launch": flops_launch, "launch_ms": k_ms / k_n,
-                     "precision": "3xTF32 (tcgen05 kind::tf32), fp32 accumulate",
+                     "precision": "two-term fp16 split with power-of-two operand scaling "
+                                  "(tcgen05 kind::f16, 3 products, ~22-bit), fp32 accumulate",
                      "fp32_ffma_nominal_tflops": 74.4,
                      "frac_of_fp32_ffma_nominal": achieved / 74.4},
         "stages_ms_per_step": stages,

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <string>
@@ -51,8 +52,12 @@ struct Plan {
   int max_list = 0;
   // tcgen05 form (parity levels): dense split tables, see build_tc_table
   bool tc = false;
-  std::vector<float> tcb;
+  bool f16 = true;
+  std::vector<uint8_t> tcb;
+  std::vector<float> rk, s_inv;
   uint8_t* d_tcb = nullptr;
+  float* d_rk = nullptr;
+  float* d_sinv = nullptr;
 };
 
 }  // namespace
@@ -127,22 +132,80 @@ float rn_tf32_host(double v) {
   return f;
 }
 
+// host round-to-nearest-even to fp16; returns the bits and the exact value
+uint16_t half_rn(double v, double* val) {
+  const uint16_t sign = v < 0 ? 0x8000 : 0;
+  const double a = std::fabs(v);
+  uint16_t bits = 0;
+  double r = 0.0;
+  if (a > 0.0) {
+    int ex;
+    std::frexp(a, &ex);
+    int E = ex - 1;  // a in [2^E, 2^(E+1))
+    if (E < -14) {
+      const double q = std::nearbyint(std::ldexp(a, 24));
+      bits = (uint16_t)q;
+      r = std::ldexp(q, -24);
+    } else {
+      double q = std::nearbyint(std::ldexp(a, 10 - E));
+      if (q >= 2048.0) {
+        q = 1024.0;
+        ++E;
+      }
+      if (E > 15) {  // clamp (the scaling keeps |x| <= 2^13)
+        E = 15;
+        q = 2047.0;
+      }
+      bits = (uint16_t)(((E + 15) << 10) | ((int)q - 1024));
+      r = std::ldexp(q, E - 10);
+    }
+  }
+  *val = sign ? -r : r;
+  return (uint16_t)(sign | bits);
+}
+
 // Dense tcgen05 tables of one parity plan (m2l_tc.cu): for class group cg
 // (target classes cg*CLS + ci), source class sigma, shift slot
 // s = (slot/9 - 1, slot/3%3 - 1, slot%3 - 1) and K step, the B operand rows
 // are the CLS tables A_delta, delta = 2 s + sigma - pi (the sum of the plan's
-// entries with that offset for class pi; zero if none), each split in float64
-// into hi = rn_tf32(A) and lo = rn_tf32(A - hi).  Row order: even sigma
-// [lo(class 0..) | hi(class 0..)], odd sigma [hi | lo]; K-major no-swizzle
-// [kchunk][row][4 floats].
+// entries with that offset for class pi; zero if none), split in float64 into
+// hi and lo parts.  Row order: even sigma [lo(class 0..) | hi(class 0..)], odd
+// sigma [hi | lo]; K-major no-swizzle [kchunk][row][16 B].
+//   tf32: hi = rn_tf32(A), lo = rn_tf32(A - hi).
+//   f16:  B' = A s_n / r_k, hi = rn_f16(B'), lo = rn_f16((B' - hi) 2^11), with
+//         s_n = (h/2)^|n|/n! at the plan's level and r_k a power of two with
+//         max_{slot,n} |B'| <= 2^13 (returned in rk, NC entries; s_inv = 1/s_n).
 void build_tc_table(const std::vector<std::vector<int4>>& lists,
-                    const std::vector<const double*>& slot_src, int P, int rho,
-                    std::vector<float>& out) {
+                    const std::vector<const double*>& slot_src, int P, int PP, int rho, int level,
+                    bool f16, Plan& plan) {
   int CLS, NC, KS, BSLOT;
-  if (fc2t2::tc_geometry(rho, &CLS, &NC, &KS, &BSLOT) != 0) return;
+  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, &CLS, &NC, &KS, &BSLOT) != 0) return;
   const int W = CLS * NC, R = 2 * W, NCG = 8 / CLS;
-  const size_t slot_f = (size_t)BSLOT / 4;
-  out.assign((size_t)NCG * 8 * KS * 27 * slot_f, 0.f);
+  const int KI = f16 ? 16 : 8, ESZ = f16 ? 2 : 4;
+  std::vector<double> sn(P, 1.0);
+  if (f16) fc2t2::tc_moment_scales(rho, level, sn.data());
+  plan.s_inv.assign(PP, 0.f);
+  for (int n = 0; n < P; ++n) plan.s_inv[n] = (float)(1.0 / sn[n]);
+  // per output column k: power of two r_k with max |A[k][n] s_n| / r_k <= 2^13
+  std::vector<double> rk(NC, 1.0);
+  if (f16) {
+    std::vector<double> mx(P, 0.0);
+    for (const auto& l : lists)
+      for (const int4& e : l) {
+        const double* A = slot_src[e.w];
+        for (int k = 0; k < P; ++k)
+          for (int n = 0; n < P; ++n) mx[k] = std::max(mx[k], std::fabs(A[(size_t)k * P + n] * sn[n]));
+      }
+    for (int k = 0; k < P; ++k)
+      if (mx[k] > 0.0) {
+        int ex;
+        std::frexp(mx[k], &ex);            // mx < 2^ex
+        rk[k] = std::ldexp(1.0, ex - 13);
+      }
+  }
+  plan.rk.assign(NC, 1.f);
+  for (int k = 0; k < NC; ++k) plan.rk[k] = (float)rk[k];
+  plan.tcb.assign((size_t)NCG * 8 * KS * 27 * BSLOT, 0);
   std::vector<double> A((size_t)P * P);
   for (int cg = 0; cg < NCG; ++cg)
     for (int sg = 0; sg < 8; ++sg) {
@@ -166,17 +229,28 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
           const int hi_row = (sg & 1) ? ci * NC : W + ci * NC;
           const int lo_row = (sg & 1) ? W + ci * NC : ci * NC;
           for (int ks = 0; ks < KS; ++ks) {
-            float* st = out.data() + ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * slot_f;
+            uint8_t* st = plan.tcb.data() + ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * BSLOT;
             for (int kc = 0; kc < 2; ++kc)
               for (int k = 0; k < P; ++k)
-                for (int f = 0; f < 4; ++f) {
-                  const int n = 8 * ks + 4 * kc + f;
+                for (int f = 0; f < KI / 2; ++f) {
+                  const int n = KI * ks + (KI / 2) * kc + f;
                   if (n >= P) continue;
                   const double a = A[(size_t)k * P + n];
-                  const float hi = rn_tf32_host(a);
-                  const float lo = rn_tf32_host(a - (double)hi);
-                  st[((size_t)kc * R + hi_row + k) * 4 + f] = hi;
-                  st[((size_t)kc * R + lo_row + k) * 4 + f] = lo;
+                  uint8_t* ph = st + ((size_t)kc * R + hi_row + k) * 16 + f * ESZ;
+                  uint8_t* pl = st + ((size_t)kc * R + lo_row + k) * 16 + f * ESZ;
+                  if (f16) {
+                    const double b = a * sn[n] / rk[k];
+                    double hv, lv;
+                    const uint16_t hb = half_rn(b, &hv);
+                    const uint16_t lb = half_rn((b - hv) * 2048.0, &lv);
+                    std::memcpy(ph, &hb, 2);
+                    std::memcpy(pl, &lb, 2);
+                  } else {
+                    const float hi = rn_tf32_host(a);
+                    const float lo = rn_tf32_host(a - (double)hi);
+                    std::memcpy(ph, &hi, 4);
+                    std::memcpy(pl, &lo, 4);
+                  }
                 }
           }
         }
@@ -229,6 +303,11 @@ void finish_plan(Plan& p, std::vector<std::vector<int4>>& lists) {
   p.tc = p.ncls == 8;
 }
 
+bool tf32_mode() {
+  const char* v = std::getenv("FC2T2_M2L_TF32");
+  return v && v[0] == '1';
+}
+
 bool force_ffma() {
   const char* v = std::getenv("FC2T2_M2L_FFMA");
   return v && v[0] == '1';
@@ -239,9 +318,8 @@ bool use_tc(const Plan& p, int level) {
   return p.tc && p.d_tcb && p.max_list > 0 && (1 << (level + 1)) / 2 >= 16 && !force_ffma();
 }
 
-size_t tc_split_floats(int rho, int level, int C) {
-  const size_t res = (size_t)1 << (level + 1);
-  return 2 * res * res * res * (size_t)C * fc2t2::tc_kpad(rho);
+size_t tc_ws_bytes(const Plan& p, int rho, int level, int C) {
+  return fc2t2::tc_workspace_bytes(rho, level, C, p.f16 ? 1 : 0);
 }
 
 int plan_for(const fc2t2_engine* e, int level, int table, const Plan** out) {
@@ -258,6 +336,9 @@ fc2t2::TCPlan tc_of(const fc2t2_engine* e, const Plan& p, int level) {
   fc2t2::TCPlan t;
   t.level = level;
   t.btab = p.d_tcb;
+  t.f16 = p.f16;
+  t.rk = p.d_rk;
+  t.s_inv = p.d_sinv;
   static const char* names[] = {"m2l_tc_L0", "m2l_tc_L1", "m2l_tc_L2", "m2l_tc_L3", "m2l_tc_L4",
                                 "m2l_tc_L5", "m2l_tc_L6", "m2l_tc_L7", "m2l_tc_L8", "m2l_tc_L9"};
   t.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];
@@ -352,6 +433,8 @@ void fc2t2_engine_destroy(fc2t2_engine* e) {
       cudaFree(t.second.d_entries);
       cudaFree(t.second.d_cls_start);
       cudaFree(t.second.d_tcb);
+      cudaFree(t.second.d_rk);
+      cudaFree(t.second.d_sinv);
     }
   delete e;
 }
@@ -390,7 +473,10 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       Plan& p = e->plans[l][FC2T2_TABLE_FAR];
       p.stride = parity ? 2 : 1;
       finish_plan(p, lists);
-      if (p.tc && tc_level(l)) build_tc_table(lists, slot_src, P, e->rho, p.tcb);
+      if (p.tc && tc_level(l)) {
+        p.f16 = !tf32_mode();
+        build_tc_table(lists, slot_src, P, PP, e->rho, l, p.f16, p);
+      }
     }
     if (l == e->levels) {
       std::vector<std::vector<int4>> nl(1);
@@ -408,7 +494,10 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       Plan& pm = e->plans[l][FC2T2_TABLE_FARNEAR];
       pm.stride = pf.stride;
       finish_plan(pm, ml);
-      if (pm.tc && tc_level(l)) build_tc_table(ml, slot_src, P, e->rho, pm.tcb);
+      if (pm.tc && tc_level(l)) {
+        pm.f16 = !tf32_mode();
+        build_tc_table(ml, slot_src, P, PP, e->rho, l, pm.f16, pm);
+      }
     }
   }
   cudaStream_t s = (cudaStream_t)stream;
@@ -433,9 +522,16 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
         err = cudaMemcpyAsync(p.d_cls_start, p.cls_start.data(), p.cls_start.size() * sizeof(int),
                               cudaMemcpyHostToDevice, s);
       if (err == cudaSuccess && !p.tcb.empty()) {
-        err = cudaMalloc(&p.d_tcb, p.tcb.size() * sizeof(float));
+        err = cudaMalloc(&p.d_tcb, p.tcb.size());
         if (err == cudaSuccess)
-          err = cudaMemcpyAsync(p.d_tcb, p.tcb.data(), p.tcb.size() * sizeof(float),
+          err = cudaMemcpyAsync(p.d_tcb, p.tcb.data(), p.tcb.size(), cudaMemcpyHostToDevice, s);
+        if (err == cudaSuccess) err = cudaMalloc(&p.d_rk, p.rk.size() * sizeof(float));
+        if (err == cudaSuccess)
+          err = cudaMemcpyAsync(p.d_rk, p.rk.data(), p.rk.size() * sizeof(float),
+                                cudaMemcpyHostToDevice, s);
+        if (err == cudaSuccess) err = cudaMalloc(&p.d_sinv, p.s_inv.size() * sizeof(float));
+        if (err == cudaSuccess)
+          err = cudaMemcpyAsync(p.d_sinv, p.s_inv.data(), p.s_inv.size() * sizeof(float),
                                 cudaMemcpyHostToDevice, s);
       }
       if (err != cudaSuccess) return cuda_status(err, "engine_upload plans");
@@ -443,7 +539,7 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
   err = cudaStreamSynchronize(s);
   if (err != cudaSuccess) return cuda_status(err, "engine_upload sync");
   for (auto& lv : e->plans)
-    for (auto& t : lv.second) std::vector<float>().swap(t.second.tcb);
+    for (auto& t : lv.second) std::vector<uint8_t>().swap(t.second.tcb);
   err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking);
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming);
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming);
@@ -526,7 +622,7 @@ int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float
 size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table) {
   const Plan* p;
   if (plan_for(e, level, table, &p) != FC2T2_OK) return 0;
-  return use_tc(*p, level) ? tc_split_floats(e->rho, level, channels) * sizeof(float) : 0;
+  return use_tc(*p, level) ? tc_ws_bytes(*p, e->rho, level, channels) : 0;
 }
 
 int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const float* d_m,
@@ -541,14 +637,12 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
     return cuda_status(
         cudaMemsetAsync(d_l, 0, grid_floats(level, channels, e->PP) * sizeof(float), s), "m2l");
   }
-  const size_t need = use_tc(*p, level) ? tc_split_floats(e->rho, level, channels) : 0;
-  if (need && d_ws && ws_bytes >= need * sizeof(float)) {
-    float* hi = (float*)d_ws;
-    float* lo = hi + need / 2;
-    st = cuda_status(fc2t2::split_tf32(e->rho, level, channels, d_m, hi, lo, s), "m2l split");
+  const size_t need = use_tc(*p, level) ? tc_ws_bytes(*p, e->rho, level, channels) : 0;
+  if (need && d_ws && ws_bytes >= need) {
+    const fc2t2::TCPlan tp = tc_of(e, *p, level);
+    st = cuda_status(fc2t2::tc_prepare(e->rho, channels, tp, d_m, d_ws, s), "m2l split");
     if (st != FC2T2_OK) return st;
-    return cuda_status(
-        fc2t2::m2l_tc(e->rho, channels, tc_of(e, *p, level), hi, lo, d_l, accumulate, s), "m2l_tc");
+    return cuda_status(fc2t2::m2l_tc(e->rho, channels, tp, d_ws, d_l, accumulate, s), "m2l_tc");
   }
   return cuda_status(
       fc2t2::m2l(e->rho, channels, launch_of(*p, level), e->d_coef, d_m, d_l, accumulate, s),
@@ -560,7 +654,7 @@ namespace {
 // split-K partial grids
 size_t part_floats(const fc2t2_engine* e, const Plan& p, int level, int channels) {
   if (p.max_list == 0) return 0;
-  if (use_tc(p, level)) return tc_split_floats(e->rho, level, channels);
+  if (use_tc(p, level)) return (tc_ws_bytes(p, e->rho, level, channels) + 3) / 4;
   const int sp = fc2t2::m2l_splits(e->rho, channels, launch_of(p, level));
   return sp > 1 ? (size_t)sp * grid_floats(level, channels, e->PP) : 0;
 }
@@ -589,13 +683,12 @@ int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const f
               int accumulate, float* part, cudaStream_t s, int x_begin = 0, int x_end = -1) {
   int st;
   if (use_tc(p, l)) {
-    float* hi = part;
-    float* lo = part + tc_split_floats(e->rho, l, channels) / 2;
-    st = cuda_status(fc2t2::split_tf32(e->rho, l, channels, M, hi, lo, s), "expand split");
+    const fc2t2::TCPlan tp = tc_of(e, p, l);
+    st = cuda_status(fc2t2::tc_prepare(e->rho, channels, tp, M, part, s), "expand split");
     if (st != FC2T2_OK) return st;
-    return cuda_status(fc2t2::m2l_tc(e->rho, channels, tc_of(e, p, l), hi, lo, Lg, accumulate, s,
-                                     x_begin, x_end),
-                       "expand m2l_tc");
+    return cuda_status(
+        fc2t2::m2l_tc(e->rho, channels, tp, part, Lg, accumulate, s, x_begin, x_end),
+        "expand m2l_tc");
   }
   const fc2t2::M2LLaunch ml = launch_of(p, l);
   return cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, M, Lg, accumulate, s, part,
@@ -660,7 +753,13 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
   }
   const Plan& pL = e->plans.at(L).at(FC2T2_TABLE_FARNEAR);
   const bool fine = pL.max_list > 0, coarse = lowest < L;
-  const bool overlap = fine && coarse && e->side;
+  // FC2T2_SERIAL_CASCADE=1 keeps everything on the caller's stream (clean
+  // per-kernel event timings for profiling)
+  static const bool serial = [] {
+    const char* v = std::getenv("FC2T2_SERIAL_CASCADE");
+    return v && v[0] == '1';
+  }();
+  const bool overlap = fine && coarse && e->side && !serial;
   int st;
   if (overlap) {
     st = cuda_status(cudaEventRecord(e->fork, s), "expand fork");

@@ -47,22 +47,30 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
                 float* L, int accumulate, cudaStream_t s, float* part = nullptr, int splits = 1);
 
 // m2l_tc.cu --------------------------------------------------------------
-// tcgen05 3xTF32 M2L for parity levels.  btab is the plan's dense table:
-// [class group][source class 8][K step][slot 27][kchunk 2][row 2W][4 floats]
-// (see tc_geometry and abi.cu build_tc_table).
+// tcgen05 M2L for parity levels.  btab is the plan's dense table:
+// [class group][source class 8][K step][slot 27][kchunk 2][row 2W][16 B]
+// (see tc_geometry and abi.cu build_tc_table).  f16 plans use the scaled
+// two-term fp16 split (rk: per-output-column scales, s_inv: 1/s_n per
+// coefficient); otherwise 3xTF32.
 struct TCPlan {
   int level;
   const uint8_t* btab;
   const char* level_name;
+  bool f16 = true;
+  const float* rk = nullptr;
+  const float* s_inv = nullptr;
 };
-int tc_kpad(int rho);
 // classes per CTA, N per class, K steps, bytes per slot table; 0 on success
-int tc_geometry(int rho, int* cls, int* nc, int* ks, int* bslot);
-cudaError_t split_tf32(int rho, int level, int C, const float* M, float* hi, float* lo,
+int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot);
+// s_n = (h/2)^|n| / n! at a level, graded-lex order (P doubles)
+int tc_moment_scales(int rho, int level, double* s);
+// scratch of one M2L launch: per-channel scale bits + hi/lo operand planes
+size_t tc_workspace_bytes(int rho, int level, int C, int f16);
+cudaError_t tc_prepare(int rho, int C, const TCPlan& plan, const float* M, void* ws,
                        cudaStream_t s);
 // targets restricted to cells with x in [x_begin, x_end) (multiples of 4; x_end < 0 = res)
-cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const float* Mlo,
-                   float* L, int accumulate, cudaStream_t s, int x_begin = 0, int x_end = -1);
+cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L, int accumulate,
+                   cudaStream_t s, int x_begin = 0, int x_end = -1);
 
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {

@@ -18,15 +18,27 @@
 // MMA is operand-bandwidth bound; pairing classes lifts rho = 4 from N = 96/48
 // (one class) to N = 160/80.
 //
-// Precision (3xTF32): x = hi + lo, hi = rn_tf32(x), lo = rn_tf32(x - hi);
-// D += Ahi Bhi + Ahi Blo + Alo Bhi.  Tensor-core accumulation into TMEM
-// truncates, so the large hi*hi products of each source class sigma go to
-// their own TMEM set (double buffered, drained into fp32 registers with RN
-// adds and re-zeroed), while the small terms (2^-11 smaller) accumulate in
-// one persistent set.  TMEM per tile: [hh1 | s | hh0], W = CLS*NC columns
-// each.  Even sigma: B rows [lo | hi] and the main MMA A_hi*B writes [s | hh0];
-// odd sigma: B rows [hi | lo], main writes [hh1 | s]; the cross MMA A_lo*B_hi
-// always writes s.  All MMAs accumulate (TMEM is zeroed by the drain warps).
+// Precision: both operands are split x = hi + lo so that D = Ahi Bhi +
+// (Ahi Blo + Alo Bhi) carries ~22 significant bits (3 products; Alo Blo is
+// below fp32 resolution).  Two element formats:
+//  * kind::f16 (default): fp16 hi = rn(x'), lo = rn((x' - hi) * 2^11) on
+//    power-of-two scaled operands -- moments A' = M / (g_c s_n) with static
+//    per-coefficient scales s_n = (h/2)^|n| / n! (|M_n| <= sum|w| s_n), a
+//    per-call per-channel power of two g_c (device abs-max, max|A'| <= 2^13),
+//    tables B' = B s_n / r_k with static per-output-column r_k.  The cross
+//    products are 2^11 too large and the output is L = g_c r_k (D_hh +
+//    2^-11 D_s).  An instruction takes K = 16 (tf32: 8) at the same cycle
+//    cost, so a K step covers twice the coefficients.
+//  * kind::tf32 (FC2T2_M2L_TF32=1): hi = rna_tf32(x), lo = rna_tf32(x - hi),
+//    unscaled (3xTF32).
+// Tensor-core accumulation into TMEM truncates, so the large hi*hi products
+// of each source class sigma go to their own TMEM set (double buffered,
+// drained into fp32 registers with RN adds and re-zeroed), while the small
+// terms (2^-11 smaller) accumulate in one persistent set.  TMEM per tile:
+// [hh1 | s | hh0], W = CLS*NC columns each.  Even sigma: B rows [lo | hi] and
+// the main MMA A_hi*B writes [s | hh0]; odd sigma: B rows [hi | lo], main
+// writes [hh1 | s]; the cross MMA A_lo*B_hi always writes s.  All MMAs
+// accumulate (TMEM is zeroed by the drain warps).
 //
 // CTA (16 warps): 0 MMA issuer (warp-uniform loop, elect-one per MMA),
 // 1 B producer (one cp.async.bulk per 9-slot stage), 2-7 window gatherers
@@ -34,6 +46,7 @@
 // 8-15 TMEM drain (warp % 4 = TMEM lane quarter, two column halves).
 // TILES 1 x 16 x 8 target tiles stacked along x share one
 // (TILES + 2) x 18 x 10 window.
+#include <cuda_fp16.h>
 #include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
@@ -48,12 +61,20 @@ constexpr int pow2_at_least(int v) {
   return p;
 }
 
-template <int RHO>
+template <class T>
+struct Tag {
+  using type = T;
+};
+
+template <int RHO, bool H>
 struct TC {
+  static constexpr int RHO_ = RHO;
   static constexpr int P = index_count(RHO);
   static constexpr int PP = pad4(P);
-  static constexpr int KPAD = (P + 7) / 8 * 8;         // K per offset (tf32 MMA K = 8)
-  static constexpr int KS = KPAD / 8;
+  static constexpr int KI = H ? 16 : 8;                 // K per MMA instruction (32 B rows)
+  static constexpr int KPAD = (P + KI - 1) / KI * KI;   // K per offset
+  static constexpr int KS = KPAD / KI;
+  static constexpr int ESZ = H ? 2 : 4;                 // bytes per operand element
   static constexpr int CLS = 4 * ((P + 7) / 8 * 8) <= 256 ? 2 : 1;   // target classes per CTA
   static constexpr int NC = CLS == 2 ? (P + 7) / 8 * 8 : (P + 15) / 16 * 16;  // N per class
   static constexpr int W = CLS * NC;                   // one TMEM set; cross MMA N
@@ -74,15 +95,19 @@ struct TC {
   static constexpr int DRAIN_THREADS = 32 * 4 * DW;
   static constexpr int CW = TILES * W / DW;           // accumulator columns per drain thread
   static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 256;
+  // instruction descriptor: D f32; A/B tf32 (2) or f16 (0); K-major; N >> 3; M >> 4
   static constexpr uint32_t idesc(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
-           ((uint32_t)(128 >> 4) << 24);
+    return (1u << 4) | ((H ? 0u : 2u) << 7) | ((H ? 0u : 2u) << 10) |
+           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   }
   static constexpr uint32_t IDESC_MAIN = idesc(2 * W);
   static constexpr uint32_t IDESC_CROSS = idesc(W);
   static_assert(2 * W <= 256 && W % 16 == 0, "MMA N out of range");
   static_assert(CW % 8 == 0 && (TILES == 1 || CW == W), "drain split");
 };
+
+constexpr float kLoScale = 2048.f;   // fp16 lo parts carry the residual * 2^11
+constexpr int kGExp = 13;            // max |A'| <= 2^13
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -124,13 +149,14 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
 
-__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                          uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+template <bool H>
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+  if constexpr (H)
+    asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem),
+                 "l"(a), "l"(b), "r"(idesc));
+  else
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem),
+                 "l"(a), "l"(b), "r"(idesc));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile(
@@ -151,13 +177,13 @@ __device__ __forceinline__ float rn_tf32(float x) {
 }
 
 // ------------------------------------------------------------ pre-split ---
-// (res^3, C, PP) fp32 grid -> per-channel hi / lo grids (C, res^3, KPAD),
+// (res^3, C, PP) fp32 grid -> per-channel hi / lo planes (C, res^3, KPAD),
 // zero-padded from P to KPAD.
 template <int RHO>
 __global__ void __launch_bounds__(256)
 split_tf32_kernel(const float* __restrict__ M, float4* __restrict__ hi, float4* __restrict__ lo,
                   int64_t cells, int C) {
-  using Cfg = TC<RHO>;
+  using Cfg = TC<RHO, false>;
   constexpr int Q = Cfg::KPAD / 4;
   const int64_t n = cells * C * Q;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
@@ -175,6 +201,79 @@ split_tf32_kernel(const float* __restrict__ M, float4* __restrict__ hi, float4* 
     h.w = rn_tf32(v.w); l.w = rn_tf32(v.w - h.w);
     hi[g] = h;
     lo[g] = l;
+  }
+}
+
+// per-channel max over cells and n of |M[cell, c, n]| / s_n, as float bits
+// (non-negative floats order like their bit patterns: atomicMax is exact and
+// order independent).  grid.y = channel; one atomic per block.
+template <int RHO>
+__global__ void __launch_bounds__(256)
+absmax_kernel(const float* __restrict__ M, const float* __restrict__ s_inv, int64_t cells, int C,
+              uint32_t* __restrict__ gbits) {
+  constexpr int PP = pad4(index_count(RHO)), Q = PP / 4;
+  const int c = blockIdx.y;
+  const int64_t n = cells * Q;
+  float m = 0.f;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = g / Q;
+    const int q = (int)(g - cell * Q);
+    const float4 v = *reinterpret_cast<const float4*>(M + (cell * C + c) * PP + 4 * q);
+    const float* si = s_inv + 4 * q;
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x) * si[0], fabsf(v.y) * si[1]),
+                       fmaxf(fabsf(v.z) * si[2], fabsf(v.w) * si[3])));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = wm[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) b = fmaxf(b, wm[i]);
+    atomicMax(gbits + c, __float_as_uint(b));
+  }
+}
+
+// exponent e with max |M/s| <= 2^e (0 for an all-zero channel)
+__device__ __forceinline__ int gexp_of(uint32_t bits) {
+  return bits == 0u ? 0 : (int)((bits >> 23) & 0xFF) - 127 + 1;
+}
+
+// fp16 two-term split of A' = M / (g_c s_n): (C, res^3, KPAD) halves
+template <int RHO>
+__global__ void __launch_bounds__(256)
+split_f16_kernel(const float* __restrict__ M, const float* __restrict__ s_inv,
+                 const uint32_t* __restrict__ gbits, uint2* __restrict__ hi,
+                 uint2* __restrict__ lo, int64_t cells, int C) {
+  using Cfg = TC<RHO, true>;
+  constexpr int Q = Cfg::KPAD / 4;
+  const int64_t n = cells * C * Q;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(g % Q);
+    const int64_t cc = g / Q;  // (channel, cell) in output order
+    const int c = (int)(cc / cells);
+    const int64_t cell = cc - (int64_t)c * cells;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (4 * q < Cfg::PP) {
+      const float4 m4 = *reinterpret_cast<const float4*>(M + (cell * C + c) * Cfg::PP + 4 * q);
+      const float sc = ldexpf(1.f, kGExp - gexp_of(gbits[c]));
+      v[0] = m4.x * s_inv[4 * q] * sc;
+      v[1] = m4.y * s_inv[4 * q + 1] * sc;
+      v[2] = m4.z * s_inv[4 * q + 2] * sc;
+      v[3] = m4.w * s_inv[4 * q + 3] * sc;
+    }
+    uint16_t h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __half hh = __float2half_rn(v[i]);
+      h[i] = __half_as_ushort(hh);
+      l[i] = __half_as_ushort(__float2half_rn((v[i] - __half2float(hh)) * kLoScale));
+    }
+    hi[g] = make_uint2((uint32_t)h[0] | ((uint32_t)h[1] << 16), (uint32_t)h[2] | ((uint32_t)h[3] << 16));
+    lo[g] = make_uint2((uint32_t)l[0] | ((uint32_t)l[1] << 16), (uint32_t)l[2] | ((uint32_t)l[3] << 16));
   }
 }
 
@@ -212,12 +311,13 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ------------------------------------------------------------ M2L (tc) ---
-template <int RHO>
+template <int RHO, bool H>
 __global__ void __launch_bounds__(512, 1)
-m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
-              const uint8_t* __restrict__ Btab, float* __restrict__ L, int res, int nu, int C,
+m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
+              const uint8_t* __restrict__ Btab, const float* __restrict__ rk,
+              const uint32_t* __restrict__ gbits, float* __restrict__ L, int res, int nu, int C,
               int accumulate, int ux_begin) {
-  using T = TC<RHO>;
+  using T = TC<RHO, H>;
   constexpr int W = T::W, NS = T::NS, KS = T::KS, TILES = T::TILES, CW = T::CW;
   constexpr int WROWS = T::WROWS, WY = T::WY, WZ = T::WZ;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -299,8 +399,8 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
             for (int t = 0; t < TILES; ++t) {
               const uint64_t arow = ex + (uint64_t)(t * WY * WZ);
               const uint32_t dt = tmem + (uint32_t)(t * 3 * W);
-              if (elect_one()) umma_tf32(dt + mcol, ahi + arow, bd, T::IDESC_MAIN, 1u);
-              if (elect_one()) umma_tf32(dt + W, alo + arow, bd + xoff, T::IDESC_CROSS, 1u);
+              if (elect_one()) umma<H>(dt + mcol, ahi + arow, bd, T::IDESC_MAIN);
+              if (elect_one()) umma<H>(dt + W, alo + arow, bd + xoff, T::IDESC_CROSS);
             }
           }
           if (elect_one()) umma_commit(bempty(s));
@@ -332,8 +432,8 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
     // ---------------- window gatherers ----------------
     const int gt = tid - 32 * T::GATHER_WARP0;
     const size_t cells = (size_t)res * res * res;
-    const float* hi_c = Mhi + (size_t)chan * cells * T::KPAD;
-    const float* lo_c = Mlo + (size_t)chan * cells * T::KPAD;
+    const uint8_t* hi_c = Mhi + (size_t)chan * cells * T::KPAD * T::ESZ;
+    const uint8_t* lo_c = Mlo + (size_t)chan * cells * T::KPAD * T::ESZ;
     int q = 0;
     for (int sg = 0; sg < 8; ++sg) {
       const int sx = (sg >> 2) & 1, sy = (sg >> 1) & 1, sz = sg & 1;
@@ -348,13 +448,14 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
           const int cz = 2 * (uz0 - 1 + wz) + sz;
           const bool ok = (unsigned)cx < (unsigned)res && (unsigned)cy < (unsigned)res &&
                           (unsigned)cz < (unsigned)res;
-          const size_t off = ok ? (((size_t)cx * res + cy) * res + cz) * T::KPAD + ks * 8 : 0;
+          const size_t off =
+              ok ? ((((size_t)cx * res + cy) * res + cz) * T::KPAD + ks * T::KI) * T::ESZ : 0;
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
-            const float* src = (part ? lo_c : hi_c) + off;
+            const uint8_t* src = (part ? lo_c : hi_c) + off;
 #pragma unroll
             for (int kc = 0; kc < 2; ++kc)
-              cp_async16_zfill(smem_u32(wb + ((part * 2 + kc) * WROWS + r) * 16), src + kc * 4,
+              cp_async16_zfill(smem_u32(wb + ((part * 2 + kc) * WROWS + r) * 16), src + kc * 16,
                                ok ? 16 : 0);
           }
         }
@@ -397,12 +498,19 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
       mbar_arrive(accfree(set));
     }
     // the small-term set is complete once the last group's commit has fired
+    const float sfac = H ? 1.f / kLoScale : 1.f;
 #pragma unroll
     for (int c = 0; c < CW; c += 8) {
       float v[8];
       tmem_ld8(tb + W + c, v);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[c + i] += v[i];
+      for (int i = 0; i < 8; ++i) acc[c + i] += v[i] * sfac;
+    }
+    if constexpr (H) {
+      // undo the operand scaling: L = g_c r_k (D_hh + 2^-11 D_s)
+      const float g = ldexpf(1.f, gexp_of(gbits[chan]) - kGExp);
+#pragma unroll
+      for (int c = 0; c < CW; ++c) acc[c] *= g * rk[(c0 + c) % T::NC];
     }
     const int row = dq * 32 + lane;
     const int ux = ux0 + t, uy = uy0 + row / T::TZ, uz = uz0 + row % T::TZ;
@@ -432,32 +540,89 @@ m2l_tc_kernel(const float* __restrict__ Mhi, const float* __restrict__ Mlo,
 
 }  // namespace
 
-int tc_kpad(int rho) { return (index_count(rho) + 7) / 8 * 8; }
-
-int tc_geometry(int rho, int* cls, int* nc, int* ks, int* bslot) {
+int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot) {
   FC2T2_DISPATCH_RHO(rho, {
-    *cls = TC<RHO>::CLS;
-    *nc = TC<RHO>::NC;
-    *ks = TC<RHO>::KS;
-    *bslot = TC<RHO>::BSLOT;
+    auto fill = [&](auto tag) {
+      using T = typename decltype(tag)::type;
+      *cls = T::CLS;
+      *nc = T::NC;
+      *ks = T::KS;
+      *bslot = T::BSLOT;
+    };
+    if (f16) fill(Tag<TC<RHO, true>>{});
+    else fill(Tag<TC<RHO, false>>{});
     return 0;
   });
   return -1;
 }
 
-cudaError_t split_tf32(int rho, int level, int C, const float* M, float* hi, float* lo,
+int tc_moment_scales(int rho, int level, double* s) {
+  const double half = 1.0 / (double)(1 << (level + 1));   // half the cell width 2/res
+  FC2T2_DISPATCH_RHO(rho, {
+    constexpr MI<RHO> mi{};
+    for (int j = 0; j < MI<RHO>::P; ++j) {
+      const int e[3] = {mi.e0[j], mi.e1[j], mi.e2[j]};
+      double v = 1.0;
+      for (int a = 0; a < 3; ++a)
+        for (int t = 1; t <= e[a]; ++t) v *= half / t;
+      s[j] = v;
+    }
+    return 0;
+  });
+  return -1;
+}
+
+namespace {
+template <int RHO, bool H>
+size_t plane_bytes(int level, int C) {
+  const size_t res = (size_t)1 << (level + 1);
+  return res * res * res * (size_t)C * TC<RHO, H>::KPAD * TC<RHO, H>::ESZ;
+}
+size_t gbits_bytes(int C) { return ((size_t)C * 4 + 255) / 256 * 256; }
+}  // namespace
+
+size_t tc_workspace_bytes(int rho, int level, int C, int f16) {
+  FC2T2_DISPATCH_RHO(rho, {
+    const size_t pb = f16 ? plane_bytes<RHO, true>(level, C) : plane_bytes<RHO, false>(level, C);
+    return gbits_bytes(C) + 2 * pb;
+  });
+  return 0;
+}
+
+cudaError_t tc_prepare(int rho, int C, const TCPlan& plan, const float* M, void* ws,
                        cudaStream_t s) {
-  const int64_t res = (int64_t)1 << (level + 1);
+  const int64_t res = (int64_t)1 << (plan.level + 1);
   const int64_t cells = res * res * res;
-  const int64_t n = cells * C * (tc_kpad(rho) / 4);
-  FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("m2l_split", s,
-      split_tf32_kernel<RHO><<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(
-          M, (float4*)hi, (float4*)lo, cells, C)));
+  uint8_t* w = (uint8_t*)ws;
+  uint32_t* gbits = (uint32_t*)w;
+  FC2T2_DISPATCH_RHO(rho, {
+    if (plan.f16) {
+      using T = TC<RHO, true>;
+      uint8_t* hi = w + gbits_bytes(C);
+      uint8_t* lo = hi + plane_bytes<RHO, true>(plan.level, C);
+      cudaError_t e = cudaMemsetAsync(gbits, 0, (size_t)C * 4, s);
+      if (e != cudaSuccess) return e;
+      const int64_t n4 = cells * (T::PP / 4);
+      dim3 ag((unsigned)grid_blocks(n4, 256, 148 * 4), (unsigned)C);
+      FC2T2_LAUNCH("m2l_absmax", s, absmax_kernel<RHO><<<ag, 256, 0, s>>>(M, plan.s_inv, cells, C,
+                                                                            gbits));
+      const int64_t n = cells * C * (T::KPAD / 4);
+      FC2T2_LAUNCH("m2l_split", s, split_f16_kernel<RHO><<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(
+                                       M, plan.s_inv, gbits, (uint2*)hi, (uint2*)lo, cells, C));
+    } else {
+      using T = TC<RHO, false>;
+      uint8_t* hi = w + gbits_bytes(C);
+      uint8_t* lo = hi + plane_bytes<RHO, false>(plan.level, C);
+      const int64_t n = cells * C * (T::KPAD / 4);
+      FC2T2_LAUNCH("m2l_split", s, split_tf32_kernel<RHO><<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(
+                                       M, (float4*)hi, (float4*)lo, cells, C));
+    }
+  });
   return cudaGetLastError();
 }
 
-cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const float* Mlo,
-                   float* L, int accumulate, cudaStream_t s, int x_begin, int x_end) {
+cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L, int accumulate,
+                   cudaStream_t s, int x_begin, int x_end) {
   const int res = 1 << (plan.level + 1);
   const int nu = res / 2;
   if (x_end < 0) x_end = res;
@@ -466,17 +631,27 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const float* Mhi, const f
     return cudaErrorInvalidValue;
   if (x_end <= x_begin) return cudaSuccess;
   const int ux_begin = x_begin / 2, ux_count = (x_end - x_begin) / 2;
-  FC2T2_DISPATCH_RHO(rho, {
-    using T = TC<RHO>;
-    auto kern = m2l_tc_kernel<RHO>;
+  const uint8_t* w = (const uint8_t*)ws;
+  const uint32_t* gbits = (const uint32_t*)w;
+  auto launch = [&](auto tag) -> cudaError_t {
+    using T = typename decltype(tag)::type;
+    constexpr bool H = T::ESZ == 2;
+    auto kern = m2l_tc_kernel<T::RHO_, H>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)T::SMEM);
     if (e != cudaSuccess) return e;
+    const uint8_t* hi = w + gbits_bytes(C);
+    const uint8_t* lo = hi + plane_bytes<T::RHO_, H>(plan.level, C);
     dim3 grid((unsigned)((ux_count / T::TILES) * (nu / T::TY) * (nu / T::TZ)),
               (unsigned)(8 / T::CLS), (unsigned)C);
     FC2T2_LAUNCH(plan.level_name, s,
-                 kern<<<grid, T::THREADS, T::SMEM, s>>>(Mhi, Mlo, plan.btab, L, res, nu, C,
-                                                        accumulate, ux_begin));
+                 kern<<<grid, T::THREADS, T::SMEM, s>>>(hi, lo, plan.btab, plan.rk, gbits, L, res,
+                                                        nu, C, accumulate, ux_begin));
+    return cudaGetLastError();
+  };
+  FC2T2_DISPATCH_RHO(rho, {
+    if (plan.f16) return launch(Tag<TC<RHO, true>>{});
+    return launch(Tag<TC<RHO, false>>{});
   });
   return cudaGetLastError();
 }

@@ -18,8 +18,12 @@ for _ in range(3):
     explicit_forward(eng, SourceSet(p, w), q)
 torch.cuda.synchronize()
 _lib.profile_enable(True)
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+e0.record()
 for _ in range(10):
     explicit_forward(eng, SourceSet(p, w), q)
+e1.record()
 torch.cuda.synchronize()
+print("FWD_MS", round(e0.elapsed_time(e1) / 10, 4))
 prof = _lib.profile_read(); _lib.profile_enable(False)
 print("DIAG", os.environ.get("FC2T2_TC_DIAG", "0"), {k: round(v[0] / v[1], 4) for k, v in prof.items() if "m2l" in k})
