@@ -1,13 +1,18 @@
-// Point -> cell keys and a stable counting/radix sort by cell.
+// Point -> cell keys and a stable sort by cell.
 //
 // Replaces the reference's find_box + np.add.at key (reference
 // expansion.py:85-93, :195): P2M wants every cell's points contiguous and in
 // ascending source index so that the per-cell sum is accumulated in the same
-// order as np.add.at and is bit-reproducible run to run.  That is a *stable*
-// sort by cell id, done here as an LSD radix sort of (cell, index) pairs with
-// 6-8 bit digits (2-3 passes for 15-21 bit keys), plus a cell histogram whose
-// exclusive scan gives every cell's [start, end) range.  No float atomics
-// anywhere, so P2M is deterministic.
+// order as np.add.at and is bit-reproducible run to run.  The output is the
+// stable sort by cell id -- order = points sorted by (cell, index) -- plus
+// every cell's [start, end) range, computed as a counting sort:
+//   1. keys + arrival ranks: rank = atomicAdd(&count[cell], 1) (an arbitrary
+//      order inside a cell), 2. exclusive scan of the counts = cell_start,
+//   3. order[cell_start[cell] + rank] = i, 4. every cell's segment sorted by
+//      index (cells hold tens of points: a warp bitonic network up to 1024,
+//      a shared-memory block sort up to 8192, a block merge sort beyond).
+// Step 4 makes the result independent of the atomics' interleaving, i.e.
+// identical to a stable sort.  No float atomics anywhere: P2M is deterministic.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -19,17 +24,14 @@ constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;  // 4096
 
-constexpr int RADIX_THREADS = 256;
-constexpr int RADIX_ROUNDS = 16;
-constexpr int RADIX_TILE = RADIX_THREADS * RADIX_ROUNDS;  // 4096 keys per block
-constexpr int RADIX_WARPS = RADIX_THREADS / 32;
-constexpr int RADIX_MAX_BITS = 9;  // 512 bins: 18-bit cell keys sort in 2 passes
-constexpr int RADIX_MAX_BINS = 1 << RADIX_MAX_BITS;
+constexpr int WARP_SEG_MAX = 1024;    // warp bitonic network (up to 32 per lane)
+constexpr int BLOCK_SEG_MAX = 8192;   // shared-memory bitonic sort
+constexpr int SEG_BLOCK = 1024;
 
 // ---------------------------------------------------------------- keys ---
 
 __global__ void cell_keys_kernel(const float* __restrict__ pts, int64_t n, int res,
-                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks,
                                  uint32_t* __restrict__ counts, int32_t* __restrict__ flag) {
   int bad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -39,8 +41,7 @@ __global__ void cell_keys_kernel(const float* __restrict__ pts, int64_t n, int r
     int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
     uint32_t key = ((uint32_t)b0 * res + b1) * res + b2;
     keys[i] = key;
-    vals[i] = (uint32_t)i;
-    atomicAdd(&counts[key], 1u);
+    ranks[i] = atomicAdd(&counts[key], 1u);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
 }
@@ -150,251 +151,292 @@ cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_
 
 namespace {
 
-// --------------------------------------------------------------- radix ---
+// ------------------------------------------------------- counting sort ---
 
-__global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
-                                  int bits, int nblocks, uint32_t* __restrict__ hist) {
-  __shared__ uint32_t h[RADIX_MAX_BINS];
-  const int nbins = 1 << bits;
-  for (int b = threadIdx.x; b < nbins; b += blockDim.x) h[b] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * RADIX_TILE;
-  const uint32_t mask = (uint32_t)nbins - 1;
-  for (int k = threadIdx.x; k < RADIX_TILE; k += blockDim.x) {
-    int64_t i = base + k;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & mask], 1u);
+// nocell_rank (key sorts only): stable ranks of the key-R items, an exclusive
+// scan of their flags, so the no-cell bucket needs no segment sort
+__global__ void place_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
+                             int64_t n, int64_t R, const uint32_t* __restrict__ start,
+                             const uint32_t* __restrict__ nocell_rank,
+                             uint32_t* __restrict__ order) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[i];
+    const uint32_t r = (nocell_rank && (int64_t)k == R) ? nocell_rank[i] : ranks[i];
+    order[start[k] + r] = (uint32_t)i;
   }
-  __syncthreads();
-  for (int b = threadIdx.x; b < nbins; b += blockDim.x)
-    hist[(int64_t)b * nblocks + blockIdx.x] = h[b];
 }
 
-// Stable scatter.  Warp w of a block owns keys [w*512, (w+1)*512) of the
-// block's 4096-key tile and ranks them in index order with warp match_any
-// against its own digit histogram (no block barriers inside the loop); one
-// exclusive scan across the warps per digit then places every warp's run
-// after the earlier warps' runs, so the scatter is stable.
-constexpr int RADIX_ITEMS = RADIX_TILE / RADIX_THREADS;  // 16 keys per thread
+// keys >= R (no cell) go to bucket R, after every cell; flags[i] = 1 for them
+__global__ void key_rank_kernel(const uint32_t* __restrict__ keys_in, int64_t n, int64_t R,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ ranks,
+                                uint32_t* __restrict__ counts, uint32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys_in[i];
+    const bool cell = (int64_t)k < R;
+    keys[i] = cell ? k : (uint32_t)R;
+    ranks[i] = cell ? atomicAdd(&counts[k], 1u) : 0u;
+    flags[i] = cell ? 0u : 1u;
+  }
+}
 
-__global__ void __launch_bounds__(RADIX_THREADS)
-radix_scatter_kernel(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                     int64_t n, int shift, int bits, int nblocks,
-                     const uint32_t* __restrict__ offsets) {
-  extern __shared__ uint32_t rsm[];
-  const int nbins = 1 << bits;
-  uint32_t* whist_base = rsm;                          // [RADIX_WARPS][nbins]
-  uint32_t* dstart = rsm + RADIX_WARPS * nbins;        // [nbins]
-  uint32_t* gstart = dstart + nbins;                   // [nbins]
-  uint32_t* skey = gstart + nbins;                     // [RADIX_TILE]
-  uint32_t* sval = skey + RADIX_TILE;                  // [RADIX_TILE]
-  auto whist = [&](int w, uint32_t b) -> uint32_t& { return whist_base[w * nbins + b]; };
-  const uint32_t mask = (uint32_t)nbins - 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int b = threadIdx.x; b < RADIX_WARPS * nbins; b += blockDim.x) whist_base[b] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * RADIX_TILE + (int64_t)warp * (32 * RADIX_ITEMS);
-  const uint32_t lt_mask = (1u << lane) - 1u;
-  uint32_t key[RADIX_ITEMS], val[RADIX_ITEMS], pos[RADIX_ITEMS];
+// Bitonic sort of 32*K values held as v[j] = element j*32 + lane.
+template <int K>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&v)[K], int lane) {
+  constexpr int N = 32 * K;
 #pragma unroll
-  for (int r = 0; r < RADIX_ITEMS; ++r) {
-    const int64_t i = base + r * 32 + lane;
-    const bool valid = i < n;
-    key[r] = valid ? keys_in[i] : 0xffffffffu;
-    val[r] = valid ? vals_in[i] : 0u;
-  }
+  for (int k = 2; k <= N; k <<= 1) {
 #pragma unroll
-  for (int r = 0; r < RADIX_ITEMS; ++r) {
-    const bool valid = key[r] != 0xffffffffu;
-    const uint32_t d = valid ? (key[r] >> shift) & mask : 0xffffffffu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (lane == leader && valid) {
-      old = whist(warp, d);
-      whist(warp, d) = old + __popc(peers);
-    }
-    old = __shfl_sync(0xffffffffu, old, leader);
-    pos[r] = old + __popc(peers & lt_mask);
-    __syncwarp();
-  }
-  __syncthreads();
-  // block-local digit runs: per-warp prefix inside each digit, then an
-  // exclusive scan over the digits (warp 0, 8 bins per lane)
-  for (int b = threadIdx.x; b < nbins; b += blockDim.x) {
-    uint32_t acc = 0;
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= 32) {
+        const int js = jj >> 5;
 #pragma unroll
-    for (int w = 0; w < RADIX_WARPS; ++w) {
-      const uint32_t c = whist(w, b);
-      whist(w, b) = acc;
-      acc += c;
-    }
-    dstart[b] = acc;  // digit total for now
-    gstart[b] = offsets[(int64_t)b * nblocks + blockIdx.x];
-  }
-  __syncthreads();
-  if (warp == 0) {
-    constexpr int PER = RADIX_MAX_BINS / 32;
-    uint32_t v[PER], sum = 0;
+        for (int j = 0; j < K; ++j) {
+          const int q = j ^ js;
+          if (q > j) {
+            const bool up = (((j << 5) | lane) & k) == 0;
+            const uint32_t a = v[j], b = v[q];
+            if ((a > b) == up) {
+              v[j] = b;
+              v[q] = a;
+            }
+          }
+        }
+      } else {
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int b = lane * PER + k;
-      v[k] = b < nbins ? dstart[b] : 0u;
-      sum += v[k];
-    }
-    uint32_t x = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    uint32_t run = x - sum;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int b = lane * PER + k;
-      if (b < nbins) dstart[b] = run;
-      run += v[k];
+        for (int j = 0; j < K; ++j) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, v[j], jj);
+          const bool up = (((j << 5) | lane) & k) == 0;
+          const bool lower = (lane & jj) == 0;
+          v[j] = (lower == up) ? min(v[j], o) : max(v[j], o);
+        }
+      }
     }
   }
-  __syncthreads();
-  // stage the tile in digit order, then write every digit run contiguously
+}
+
+template <int K>
+__device__ __forceinline__ void warp_sort_segment(uint32_t* seg, int size, int lane) {
+  uint32_t v[K];
 #pragma unroll
-  for (int r = 0; r < RADIX_ITEMS; ++r) {
-    if (key[r] == 0xffffffffu) continue;
-    const uint32_t d = (key[r] >> shift) & mask;
-    const uint32_t lp = dstart[d] + whist(warp, d) + pos[r];
-    skey[lp] = key[r];
-    sval[lp] = val[r];
+  for (int j = 0; j < K; ++j) {
+    const int e = j * 32 + lane;
+    v[j] = e < size ? seg[e] : 0xffffffffu;
   }
+  warp_bitonic<K>(v, lane);
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int e = j * 32 + lane;
+    if (e < size) seg[e] = v[j];
+  }
+}
+
+// segment c = [start[c], c < R ? start[c+1] : n); one warp per segment,
+// segments above WARP_SEG_MAX go to the block worklist
+__global__ void __launch_bounds__(256)
+segment_sort_warp_kernel(uint32_t* __restrict__ order, const uint32_t* __restrict__ start,
+                         int64_t nseg, int64_t R, int64_t n, uint32_t* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < nseg;
+       c += warps) {
+    const int64_t b = start[c];
+    const int64_t e = c < R ? (int64_t)start[c + 1] : n;
+    const int64_t size = e - b;
+    if (size <= 1) continue;
+    if (size > WARP_SEG_MAX) {
+      if (lane == 0) work[1 + atomicAdd(work, 1u)] = (uint32_t)c;
+      continue;
+    }
+    uint32_t* seg = order + b;
+    if (size <= 32) warp_sort_segment<1>(seg, (int)size, lane);
+    else if (size <= 64) warp_sort_segment<2>(seg, (int)size, lane);
+    else if (size <= 128) warp_sort_segment<4>(seg, (int)size, lane);
+    else if (size <= 256) warp_sort_segment<8>(seg, (int)size, lane);
+    else if (size <= 512) warp_sort_segment<16>(seg, (int)size, lane);
+    else warp_sort_segment<32>(seg, (int)size, lane);
+  }
+}
+
+// shared-memory bitonic sort of one run (len <= BLOCK_SEG_MAX), in place
+__device__ void block_sort_run(uint32_t* run, int len, uint32_t* sm) {
+  int N = 1;
+  while (N < len) N <<= 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) sm[i] = i < len ? run[i] : 0xffffffffu;
   __syncthreads();
-  const int64_t tbase = (int64_t)blockIdx.x * RADIX_TILE;
-  const int cnt = (int)((n - tbase) < RADIX_TILE ? (n - tbase) : RADIX_TILE);
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const uint32_t k = skey[i];
-    const uint32_t d = (k >> shift) & mask;
-    const uint32_t gp = gstart[d] + (uint32_t)i - dstart[d];
-    keys_out[gp] = k;
-    vals_out[gp] = sval[i];
+  for (int k = 2; k <= N; k <<= 1)
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int p = i ^ jj;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const uint32_t a = sm[i], b = sm[p];
+          if ((a > b) == up) {
+            sm[i] = b;
+            sm[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < len; i += blockDim.x) run[i] = sm[i];
+  __syncthreads();
+}
+
+__device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// first index of the merge of sorted a[0,na) and b[0,nb) at diagonal d
+__device__ __forceinline__ int64_t merge_path(const uint32_t* a, int64_t na, const uint32_t* b,
+                                              int64_t nb, int64_t d) {
+  int64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (a[m] < b[d - 1 - m]) lo = m + 1;
+    else hi = m;
+  }
+  return lo;  // elements taken from a
+}
+
+// segments from the worklist: one block each; runs of BLOCK_SEG_MAX sorted in
+// shared memory, then merged pairwise through `tmp` (merge path per thread)
+__global__ void __launch_bounds__(SEG_BLOCK)
+segment_sort_block_kernel(uint32_t* __restrict__ order, uint32_t* __restrict__ tmp,
+                          const uint32_t* __restrict__ start, int64_t R, int64_t n,
+                          const uint32_t* __restrict__ work) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t count = work[0];
+  for (uint32_t w = blockIdx.x; w < count; w += gridDim.x) {
+    const int64_t c = work[1 + w];
+    const int64_t b = start[c];
+    const int64_t e = c < R ? (int64_t)start[c + 1] : n;
+    const int64_t size = e - b;
+    for (int64_t r = 0; r < size; r += BLOCK_SEG_MAX)
+      block_sort_run(order + b + r, (int)lmin(BLOCK_SEG_MAX, size - r), sm);
+    uint32_t* src = order + b;
+    uint32_t* dst = tmp + b;
+    for (int64_t width = BLOCK_SEG_MAX; width < size; width <<= 1) {
+      for (int64_t r0 = 0; r0 < size; r0 += 2 * width) {
+        const int64_t na = lmin(width, size - r0);
+        const int64_t nb = lmin(width, size - r0 - na);
+        const uint32_t* A = src + r0;
+        const uint32_t* B = A + na;
+        const int64_t tot = na + nb;
+        const int64_t per = (tot + blockDim.x - 1) / blockDim.x;
+        const int64_t d0 = lmin(tot, per * threadIdx.x), d1 = lmin(tot, d0 + per);
+        int64_t ia = merge_path(A, na, B, nb, d0), ib = d0 - ia;
+        for (int64_t d = d0; d < d1; ++d) {
+          const bool takeA = ib >= nb || (ia < na && A[ia] <= B[ib]);
+          dst[r0 + d] = takeA ? A[ia++] : B[ib++];
+        }
+      }
+      __syncthreads();
+      uint32_t* t = src;
+      src = dst;
+      dst = t;
+    }
+    if (src != order + b)
+      for (int64_t i = threadIdx.x; i < size; i += blockDim.x) order[b + i] = src[i];
+    __syncthreads();
   }
 }
 
 struct SortWs {
-  uint32_t *keys, *keys2, *vals, *vals2, *hist, *scan, *counts;
+  uint32_t *keys, *ranks, *tmp, *counts, *scan, *work;
 };
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-}  // namespace
-
-size_t cell_sort_workspace(int level, int64_t n) {
-  const int64_t R = (int64_t)1 << (3 * (level + 1));
-  const int64_t nblocks = (n + RADIX_TILE - 1) / RADIX_TILE;
-  const int64_t hist = RADIX_MAX_BINS * (nblocks > 0 ? nblocks : 1);
-  size_t b = 0;
-  b += 4 * align256(4 * (size_t)n);  // keys, keys2, vals, vals2
-  b += align256(4 * (size_t)hist);
-  b += align256(4 * std::max(scan_ws_words(hist), scan_ws_words(R + 1)) + 4);
-  b += align256(4 * (size_t)(R + 1));  // counts
-  return b;
-}
-
-namespace {
-
-__global__ void keys_prep_kernel(const uint32_t* __restrict__ keys_in, int64_t n, int64_t R,
-                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                 uint32_t* __restrict__ counts) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys_in[i];
-    keys[i] = k;
-    vals[i] = (uint32_t)i;
-    if ((int64_t)k < R) atomicAdd(&counts[k], 1u);  // keys >= R sort last, belong to no cell
-  }
-}
-
 SortWs carve(void* ws, int64_t n, int64_t R) {
-  const int64_t nblocks = std::max<int64_t>(1, (n + RADIX_TILE - 1) / RADIX_TILE);
   char* p = (char*)ws;
   auto take = [&](size_t bytes) { char* q = p; p += align256(bytes); return (uint32_t*)q; };
   SortWs w;
   w.keys = take(4 * (size_t)n);
-  w.keys2 = take(4 * (size_t)n);
-  w.vals = take(4 * (size_t)n);
-  w.vals2 = take(4 * (size_t)n);
-  w.hist = take(4 * (size_t)(RADIX_MAX_BINS * nblocks));
-  w.scan = take(4 * std::max(scan_ws_words(RADIX_MAX_BINS * nblocks), scan_ws_words(R + 1)) + 4);
+  w.ranks = take(4 * (size_t)n);
+  w.tmp = take(4 * (size_t)n);
   w.counts = take(4 * (size_t)(R + 1));
+  w.scan = take(4 * std::max(scan_ws_words(R + 1), scan_ws_words(n)) + 4);
+  w.work = take(4 * (size_t)(R + 2));
   return w;
 }
 
-// keys/vals/counts already prepared in w: cell ranges + LSD radix passes
-cudaError_t sort_prepared(SortWs& w, int64_t n, int key_bits, int64_t R, int32_t* order,
-                          int32_t* cell_start, cudaStream_t s) {
-  const int64_t nblocks = std::max<int64_t>(1, (n + RADIX_TILE - 1) / RADIX_TILE);
+size_t ws_bytes(int64_t n, int64_t R) {
+  return 3 * align256(4 * (size_t)n) + align256(4 * (size_t)(R + 1)) +
+         align256(4 * std::max(scan_ws_words(R + 1), scan_ws_words(n)) + 4) +
+         align256(4 * (size_t)(R + 2));
+}
+
+// keys/ranks/counts prepared: cell ranges, placement, per-cell index sort.
+// nocell: key sorts, whose bucket R is ranked stably by a scan of w.tmp flags.
+cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t* cell_start,
+                        bool nocell, cudaStream_t s) {
   cudaError_t e = exclusive_scan(w.counts, (uint32_t*)cell_start, R + 1, w.scan, s);
   if (e != cudaSuccess || n == 0) return e != cudaSuccess ? e : cudaGetLastError();
-  const int passes = (key_bits + RADIX_MAX_BITS - 1) / RADIX_MAX_BITS;
-  const int digit = (key_bits + passes - 1) / passes;
-  uint32_t *kin = w.keys, *vin = w.vals;
-  for (int ps = 0; ps < passes; ++ps) {
-    const int shift = ps * digit;
-    const int bits = std::min(digit, key_bits - shift);
-    const bool last = ps == passes - 1;
-    uint32_t* kout = (kin == w.keys) ? w.keys2 : w.keys;
-    uint32_t* vout = last ? (uint32_t*)order : ((vin == w.vals) ? w.vals2 : w.vals);
-    FC2T2_LAUNCH("radix_hist", s,
-                 radix_hist_kernel<<<(unsigned)nblocks, RADIX_THREADS, 0, s>>>(
-                     kin, n, shift, bits, (int)nblocks, w.hist));
-    e = exclusive_scan(w.hist, w.hist, (int64_t)(1 << bits) * nblocks, w.scan, s);
+  if (nocell) {
+    e = exclusive_scan(w.tmp, w.tmp, n, w.scan, s);
     if (e != cudaSuccess) return e;
-    const size_t smem = (size_t)(RADIX_WARPS * (1 << bits) + 2 * (1 << bits) + 2 * RADIX_TILE) * 4;
-    if (smem > 48 * 1024) {
-      e = cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    FC2T2_LAUNCH("radix_scatter", s,
-                 radix_scatter_kernel<<<(unsigned)nblocks, RADIX_THREADS, smem, s>>>(
-                     kin, vin, kout, vout, n, shift, bits, (int)nblocks, w.hist));
-    kin = kout;
-    vin = vout;
   }
+  uint32_t* ord = (uint32_t*)order;
+  FC2T2_LAUNCH("sort_place", s,
+               place_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(
+                   w.keys, w.ranks, n, R, (const uint32_t*)cell_start, nocell ? w.tmp : nullptr,
+                   ord));
+  e = cudaMemsetAsync(w.work, 0, 4, s);
+  if (e != cudaSuccess) return e;
+  const int64_t nseg = nocell ? R : R + 1;
+  FC2T2_LAUNCH("sort_segments", s,
+               segment_sort_warp_kernel<<<grid_blocks(nseg * 32, 256), 256, 0, s>>>(
+                   ord, (const uint32_t*)cell_start, nseg, R, n, w.work));
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(segment_sort_block_kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, BLOCK_SEG_MAX * 4);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  FC2T2_LAUNCH("sort_segments", s,
+               segment_sort_block_kernel<<<148, SEG_BLOCK, BLOCK_SEG_MAX * 4, s>>>(
+                   ord, w.tmp, (const uint32_t*)cell_start, R, n, w.work));
   return cudaGetLastError();
 }
 
 }  // namespace
 
+size_t cell_sort_workspace(int level, int64_t n) {
+  const int64_t R = (int64_t)1 << (3 * (level + 1));
+  return ws_bytes(n, R);
+}
+
 cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, int32_t* cell_start,
-                      int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s) {
+                      int32_t* flag, void* ws, size_t ws_bytes_, cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int64_t R = (int64_t)res * res * res;
-  if (ws_bytes < cell_sort_workspace(level, n)) return cudaErrorInvalidValue;
+  if (ws_bytes_ < cell_sort_workspace(level, n)) return cudaErrorInvalidValue;
   SortWs w = carve(ws, n, R);
   cudaError_t e = cudaMemsetAsync(w.counts, 0, 4 * (size_t)(R + 1), s);
   if (e != cudaSuccess) return e;
   if (n > 0)
     FC2T2_LAUNCH("cell_keys", s,
-                 cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.vals,
+                 cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.ranks,
                                                                       w.counts, flag));
-  return sort_prepared(w, n, 3 * (level + 1), R, order, cell_start, s);
+  return sort_ranked(w, n, R, order, cell_start, false, s);
 }
 
 size_t key_sort_workspace(int level, int64_t n) { return cell_sort_workspace(level, n); }
 
 cudaError_t key_sort(int level, const uint32_t* keys, int64_t n, int32_t* order,
-                     int32_t* cell_start, void* ws, size_t ws_bytes, cudaStream_t s) {
+                     int32_t* cell_start, void* ws, size_t ws_bytes_, cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int64_t R = (int64_t)res * res * res;
-  if (ws_bytes < key_sort_workspace(level, n)) return cudaErrorInvalidValue;
+  if (ws_bytes_ < key_sort_workspace(level, n)) return cudaErrorInvalidValue;
   SortWs w = carve(ws, n, R);
   cudaError_t e = cudaMemsetAsync(w.counts, 0, 4 * (size_t)(R + 1), s);
   if (e != cudaSuccess) return e;
   if (n > 0)
     FC2T2_LAUNCH("keys_prep", s,
-                 keys_prep_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(keys, n, R, w.keys, w.vals,
-                                                                      w.counts));
-  // one extra key bit so the out-of-grid sentinel R sorts after every cell
-  return sort_prepared(w, n, 3 * (level + 1) + 1, R, order, cell_start, s);
+                 key_rank_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(keys, n, R, w.keys, w.ranks,
+                                                                     w.counts, w.tmp));
+  return sort_ranked(w, n, R, order, cell_start, true, s);
 }
 
 cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,

@@ -43,10 +43,17 @@ def test_find_box_bit_exact(cuda, level):
     assert np.array_equal(got.cpu().numpy(), g[f"box_l{level}"])
 
 
-def test_cell_sort_is_stable_counting_sort(eng4):
+@pytest.mark.parametrize("heavy", [0, 5000, 20_000])
+def test_cell_sort_is_stable_counting_sort(eng4, heavy):
+    """order == stable argsort by cell for every segment path of the sort:
+    uniform cells (warp networks), a 5000-point cell (shared-memory block
+    sort), a 20000-point cell (block runs + merge path) and a 300-point one."""
     rng = np.random.default_rng(0)
     p = rng.uniform(-1, 1, (50_000, 3)).astype(np.float32)
-    p[:5000] = p[0]  # a heavy cell
+    if heavy:
+        idx = rng.permutation(50_000)
+        p[idx[:heavy]] = p[idx[0]]            # a heavy cell, scattered indices
+        p[idx[heavy:heavy + 300]] = p[idx[heavy]]
     order, start = eng4.sort_points(torch.from_numpy(p).cuda())
     from oracle.fc2t2_oracle import find_box
     b = find_box(4, p.astype(np.float64))
@@ -54,6 +61,31 @@ def test_cell_sort_is_stable_counting_sort(eng4):
     ref = np.argsort(key, kind="stable")
     assert np.array_equal(order.cpu().numpy(), ref)
     counts = np.bincount(key, minlength=32 ** 3)
+    assert np.array_equal(start.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
+
+
+def test_key_sort_stable_with_no_cell_bucket(cuda):
+    """fc2t2_key_sort (insertions): keys >= R (no cell) sort after every cell,
+    everything stable; heavy keys exercise the block sort and merge paths."""
+    from paper_2111_00110_b200 import _lib
+    from paper_2111_00110_b200.expansion import _ptr, _stream
+    lv = 3
+    R = (1 << (lv + 1)) ** 3
+    rng = np.random.default_rng(4)
+    keys = rng.integers(0, R + 40, 60_000).astype(np.uint32)   # ~1 % no-cell
+    keys[rng.permutation(60_000)[:9000]] = 17                  # > 8192 in one cell
+    keys[keys >= R] = R + 7
+    kd = torch.from_numpy(keys.astype(np.int64)).to(torch.int32).cuda()
+    n = keys.size
+    ws_b = int(_lib.lib().fc2t2_key_sort_workspace_size(lv, n))
+    ws = torch.empty(ws_b, dtype=torch.uint8, device="cuda")
+    order = torch.empty(n, dtype=torch.int32, device="cuda")
+    start = torch.empty(R + 1, dtype=torch.int32, device="cuda")
+    _lib.call("fc2t2_key_sort", lv, _ptr(kd), n, _ptr(order), _ptr(start), _ptr(ws), ws_b,
+              _stream())
+    ref = np.argsort(np.minimum(keys, R), kind="stable")
+    assert np.array_equal(order.cpu().numpy(), ref)
+    counts = np.bincount(keys[keys < R], minlength=R)
     assert np.array_equal(start.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
 
 
