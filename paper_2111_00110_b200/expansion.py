@@ -220,6 +220,19 @@ class SourceSet:
             raise ValueError("p and w disagree on the number of sources")
         if p_np is not None:
             _host_domain_check(p_np, "source")
+        if (isinstance(self.p, torch.Tensor) and isinstance(w_in, torch.Tensor)
+                and not self.p.is_cuda and not w_in.is_cuda and self.p.is_pinned()
+                and w_in.is_pinned() and self.p.dtype == torch.float32
+                and w_in.dtype == torch.float32):
+            # pinned host tensors: asynchronous upload on the copy stream (the
+            # compute stream waits on it), torch's non_blocking convention --
+            # every layer call returns only after its results are downloaded,
+            # so the copies have completed by the time the caller regains
+            # control from one
+            self.p, _ = HostIO.h2d(self.p, 3)
+            self.w, ev = HostIO.h2d(w_in.reshape(self.p.shape[0], -1))
+            torch.cuda.current_stream().wait_event(ev)
+            return
         self.p = to_device(p_np if p_np is not None else self.p, 3, points=True)
         self.w = to_device(w_in).reshape(self.p.shape[0], int(w_in.shape[1]))
 

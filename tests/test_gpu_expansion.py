@@ -272,7 +272,8 @@ def test_explicit_host_tensors_match_device(eng4, monkeypatch, coherent, m):
     yb = torch.from_numpy(rng.normal(size=(m, 2)).astype(np.float32))
     rd = layers.explicit_forward(eng4, SourceSet(p.cuda(), w.cuda()), q.cuda())
     gd = layers.explicit_jvp(yb.cuda(), rd)
-    rh = layers.explicit_forward(eng4, SourceSet(p, w), q.pin_memory())
+    src = SourceSet(p.pin_memory(), w.pin_memory()) if m > 100 else SourceSet(p, w)  # async / sync upload
+    rh = layers.explicit_forward(eng4, src, q.pin_memory())
     gh = layers.explicit_jvp(yb, rh)          # pageable: staged through a pinned copy
     assert not rh.values.is_cuda and not gh.q_bar.is_cuda
     assert torch.equal(rh.values, rd.values.cpu())
