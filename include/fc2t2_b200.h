@@ -53,6 +53,9 @@ extern "C" {
 #define FC2T2_L2P_GRAD 2  /* Accessor.partials expansion.py:367-369 */
 #define FC2T2_L2P_HESS 4  /* Accessor.partials2 expansion.py:371-373 */
 #define FC2T2_L2P_WGRAD 8 /* sum_c wts_c * grad f_c (layers.py:183, :186-187) */
+/* d_q / d_wts are already permuted into d_order's sequence (row t = point
+ * d_order[t], see fc2t2_cell_sort_ex); outputs stay indexed by point */
+#define FC2T2_L2P_PRESORTED 16
 
 typedef struct fc2t2_engine fc2t2_engine;
 
@@ -94,8 +97,20 @@ size_t fc2t2_cell_sort_workspace_size(int level, int64_t n);
 int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
                     int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
                     void* stream);
+/* The same sort, also returning d_inv (n) int32 = sorted position of every
+ * point and d_pts_sorted (n, 3) = the points in sorted order, both written
+ * without random reads of d_pts (give both or neither).  With them, P2M takes
+ * d_pts_sorted and weights permuted by fc2t2_permute_rows with d_order = NULL,
+ * and L2P reads its inputs coalesced (FC2T2_L2P_PRESORTED). */
+int fc2t2_cell_sort_ex(int level, const float* d_pts, int64_t n, int32_t* d_order,
+                       int32_t* d_cell_start, int32_t* d_inv, float* d_pts_sorted,
+                       int32_t* d_flag, void* d_ws, size_t ws_bytes, void* stream);
+/* d_dst[d_inv[i], :] = d_src[i, :] for n rows of `cols` floats */
+int fc2t2_permute_rows(const float* d_src, int64_t n, int cols, const int32_t* d_inv,
+                       float* d_dst, void* stream);
 
 /* ---- stages (expansion.py:186-264) ---- */
+/* d_order NULL: d_pts / d_w are already in cell-sorted order */
 int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
               const int32_t* d_order, const int32_t* d_cell_start, float* d_m_finest,
               void* stream);

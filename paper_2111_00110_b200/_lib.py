@@ -16,7 +16,7 @@ LIB_PATH = HERE / "libfc2t2_b200.so"
 OK, EDOMAIN, ESTAGE, EORDER, ECUDA, EWORKSPACE, EVALUE = range(7)
 FLAG_DOMAIN = 1
 TABLE_FAR, TABLE_NEAR, TABLE_FARNEAR = 0, 1, 2
-L2P_VALUE, L2P_GRAD, L2P_HESS, L2P_WGRAD = 1, 2, 4, 8
+L2P_VALUE, L2P_GRAD, L2P_HESS, L2P_WGRAD, L2P_PRESORTED = 1, 2, 4, 8, 16
 
 _vp = ct.c_void_p
 _i32, _i64, _sz = ct.c_int, ct.c_int64, ct.c_size_t
@@ -37,6 +37,8 @@ _SIGS = {
     "fc2t2_find_box": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp]),
     "fc2t2_cell_sort_workspace_size": (_sz, [_i32, _i64]),
     "fc2t2_cell_sort": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fc2t2_cell_sort_ex": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fc2t2_permute_rows": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "fc2t2_p2m": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fc2t2_m2m": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "fc2t2_l2l": (_i32, [_vp, _i32, _i32, _vp, _vp, _i32, _vp]),

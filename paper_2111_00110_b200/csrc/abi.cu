@@ -591,6 +591,28 @@ int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
                      "cell_sort");
 }
 
+int fc2t2_cell_sort_ex(int level, const float* d_pts, int64_t n, int32_t* d_order,
+                       int32_t* d_cell_start, int32_t* d_inv, float* d_pts_sorted,
+                       int32_t* d_flag, void* d_ws, size_t ws_bytes, void* stream) {
+  if (level < 0 || level > 9 || n < 0 || n > INT32_MAX)
+    return fail(FC2T2_EVALUE, "bad cell_sort arguments");
+  if ((d_inv == nullptr) != (d_pts_sorted == nullptr))
+    return fail(FC2T2_EVALUE, "cell_sort_ex: give both d_inv and d_pts_sorted or neither");
+  if (ws_bytes < fc2t2::cell_sort_workspace(level, n))
+    return fail(FC2T2_EWORKSPACE, "cell_sort workspace too small");
+  return cuda_status(fc2t2::cell_sort(level, d_pts, n, d_order, d_cell_start, d_flag, d_ws,
+                                      ws_bytes, (cudaStream_t)stream, d_inv, d_pts_sorted),
+                     "cell_sort_ex");
+}
+
+int fc2t2_permute_rows(const float* d_src, int64_t n, int cols, const int32_t* d_inv,
+                       float* d_dst, void* stream) {
+  if (n < 0 || cols < 1 || (n > 0 && (!d_src || !d_inv || !d_dst)))
+    return fail(FC2T2_EVALUE, "bad permute_rows arguments");
+  return cuda_status(fc2t2::permute_rows(d_src, n, cols, d_inv, d_dst, (cudaStream_t)stream),
+                     "permute_rows");
+}
+
 int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
               const int32_t* d_order, const int32_t* d_cell_start, float* d_m_finest,
               void* stream) {
@@ -822,6 +844,8 @@ int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d
   if (rho < 1 || rho > 6) return fail(FC2T2_EORDER, "expansion order must be in [1, 6]");
   if (level < 0 || level > 9 || channels < 1 || n < 0) return fail(FC2T2_EVALUE, "bad l2p arguments");
   if ((mode & FC2T2_L2P_WGRAD) && !d_wts) return fail(FC2T2_EVALUE, "WGRAD needs weights");
+  if ((mode & FC2T2_L2P_PRESORTED) && !d_order)
+    return fail(FC2T2_EVALUE, "PRESORTED needs the order that maps rows to points");
   return cuda_status(fc2t2::l2p(rho, level, channels, d_l, d_q, n, mode, d_order, d_wts, d_value,
                                 d_grad, d_hess, d_wgrad, d_flag, (cudaStream_t)stream),
                      "l2p");

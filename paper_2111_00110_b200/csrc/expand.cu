@@ -67,7 +67,7 @@ p2m_sorted_kernel(const float* __restrict__ pts, const float* __restrict__ w, in
     for (int j = 0; j < PP; ++j) acc[j] = 0.f;
     const int beg = cell_start[cell], end = cell_start[cell + 1];
     for (int k = beg; k < end; ++k) {
-      const int64_t i = order[k];
+      const int64_t i = order ? (int64_t)order[k] : (int64_t)k;  // no order: pre-sorted inputs
       const float dx = box_offset(pts[3 * i], b0, res);
       const float dy = box_offset(pts[3 * i + 1], b1, res);
       const float dz = box_offset(pts[3 * i + 2], b2, res);

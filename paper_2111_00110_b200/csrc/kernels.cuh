@@ -10,7 +10,10 @@ namespace fc2t2 {
 size_t cell_sort_workspace(int level, int64_t n);
 cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order,
                       int32_t* cell_start, int32_t* flag, void* ws, size_t ws_bytes,
-                      cudaStream_t s);
+                      cudaStream_t s, int32_t* inv = nullptr, float* pts_sorted = nullptr);
+// dst[inv[i], :] = src[i, :]
+cudaError_t permute_rows(const float* src, int64_t n, int cols, const int32_t* inv, float* dst,
+                         cudaStream_t s);
 cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,
                      cudaStream_t s);
 // stable sort of precomputed cell keys (key >= res^3 = "no cell", sorted last)
@@ -78,6 +81,7 @@ enum L2PMode : int {
   L2P_GRAD = 2,    // (n, C, 3)
   L2P_HESS = 4,    // (n, C, 6)  xx yy zz xy xz yz
   L2P_WGRAD = 8,   // (n, 3) = sum_c wts[n, c] * grad f_c
+  L2P_PRESORTED = 16,  // q / wts given in `order` sequence; outputs by point
 };
 cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64_t n, int mode,
                 const int32_t* order, const float* wts, float* value, float* grad, float* hess,

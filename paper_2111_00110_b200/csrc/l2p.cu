@@ -8,9 +8,12 @@
 // L2P_WGRAD fuses the adjoint contraction sum_c wts_c grad f_c used by the
 // explicit layer's q_bar and p_bar (reference layers.py:183, :186-187).
 //
-// With a cell-sorted `order` (the stable sort P2M needs anyway), thread i
-// evaluates point order[i]: neighbouring threads share cell rows, which then
-// come from L1 instead of one 144-byte L2 gather per point.
+// With a cell-sorted `order` (the stable sort P2M needs anyway), thread t
+// evaluates point order[t]: neighbouring threads share cell rows, which then
+// come from L1 instead of one 144-byte L2 gather per point.  With
+// L2P_PRESORTED the inputs (q, wts) are already permuted into that order
+// (fc2t2_cell_sort_ex / fc2t2_permute_rows), so they are read coalesced and
+// only the outputs are scattered to order[t].
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -21,7 +24,7 @@ namespace {
 template <int RHO, int MODE>
 __global__ void __launch_bounds__(256)
 l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, int C, int res,
-           const int32_t* __restrict__ order, const float* __restrict__ wts,
+           const int32_t* __restrict__ order, bool presorted, const float* __restrict__ wts,
            float* __restrict__ value, float* __restrict__ grad, float* __restrict__ hess,
            float* __restrict__ wgrad, int32_t* __restrict__ flag) {
   constexpr MI<RHO> mi{};
@@ -29,8 +32,10 @@ l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, 
   int bad = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
+    // outputs at point i; inputs at i, or at t when they are pre-permuted
     const int64_t i = order ? (int64_t)order[t] : t;
-    const float x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
+    const int64_t in = presorted ? t : i;
+    const float x = q[3 * in], y = q[3 * in + 1], z = q[3 * in + 2];
     bad |= outside_domain(x, y, z);
     const int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
     float mono[P];
@@ -66,7 +71,7 @@ l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, 
           grad[(i * C + c) * 3 + 2] = g[2];
         }
         if constexpr (MODE & L2P_WGRAD) {
-          const float wv = wts[i * C + c];
+          const float wv = wts[in * C + c];
           wg0 = fmaf(wv, g[0], wg0);
           wg1 = fmaf(wv, g[1], wg1);
           wg2 = fmaf(wv, g[2], wg2);
@@ -98,10 +103,12 @@ cudaError_t l2p_rho(int level, int C, const float* L, const float* q, int64_t n,
                     float* hess, float* wgrad, int32_t* flag, cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int blocks = grid_blocks(n, 256, 148 * 16);
+  const bool presorted = (mode & L2P_PRESORTED) != 0;
+  mode &= ~L2P_PRESORTED;
 #define FC2T2_L2P_CASE(M)                                                               \
   case M:                                                                               \
     FC2T2_LAUNCH("l2p", s, l2p_kernel<RHO, M><<<blocks, 256, 0, s>>>(                   \
-        L, q, n, C, res, order, wts, value, grad, hess, wgrad, flag));                  \
+        L, q, n, C, res, order, presorted, wts, value, grad, hess, wgrad, flag));                  \
     break;
   switch (mode) {
     FC2T2_L2P_CASE(1)

@@ -72,6 +72,20 @@ def _coherent(acc: Accessor, sort):
     return sort[0] if st.numel() * st.element_size() > COHERENT_L2P_BYTES else None
 
 
+def _l2p(acc: Accessor, pts, mode: int, sort=None, wts=None):
+    """L2P at pts.  For grids beyond L2 the points are evaluated in cell order
+    so neighbouring threads share cell rows; with the sort's sorted points the
+    inputs (and weights, permuted once) are read coalesced and only outputs
+    are scattered (FC2T2_L2P_PRESORTED).  Otherwise natural order."""
+    order = _coherent(acc, sort) if sort is not None else None
+    if order is None:
+        return acc.eval_device(pts, mode, wts=wts)
+    if getattr(sort, "pts_sorted", None) is not None:
+        w_s = None if wts is None else sort.permuted(wts)
+        return acc.eval_device(sort.pts_sorted, mode | _lib.L2P_PRESORTED, wts=w_s, order=order)
+    return acc.eval_device(pts, mode, wts=wts, order=order)
+
+
 # Host-tensor callers: the per-point streams (q, y_bar up; values, q_bar down)
 # move in HOST_CHUNKS row chunks so PCIe uploads, downloads (separate streams,
 # both directions at once) and the L2P of finished chunks overlap each other
@@ -96,7 +110,7 @@ def _explicit_forward_host(engine: Engine, sources: SourceSet, q) -> ExplicitRes
     else:
         cs.wait_event(chunks[-1][2])
         q_sort = engine.sort_points(qd)
-        HostIO.d2h(acc.eval_device(qd, _lib.L2P_VALUE, order=q_sort[0])["value"], out)
+        HostIO.d2h(_l2p(acc, qd, _lib.L2P_VALUE, q_sort)["value"], out)
     HostIO.finish()
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine, q_dev=qd,
@@ -115,8 +129,9 @@ def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
         aux.wait_stream(cs)
         with torch.cuda.stream(aux):
             q_sort = eng.sort_points(qd)
-        for t in q_sort:
-            t.record_stream(cs)
+        for t in (*q_sort, q_sort.inv, q_sort.pts_sorted):
+            if t is not None:
+                t.record_stream(cs)
         res.sorts = (p_sort, q_sort)
     q_bar = torch.empty((qd.shape[0], 3), dtype=torch.float32, pin_memory=True)
     order = _coherent(acc, q_sort)
@@ -128,12 +143,13 @@ def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
                            q_bar[a:b])
     else:
         cs.wait_event(chunks[-1][2])
-        HostIO.d2h(acc.eval_device(qd, _lib.L2P_WGRAD, wts=yb, order=order)["wgrad"], q_bar)
+        if aux is not None:
+            cs.wait_stream(aux)
+        HostIO.d2h(_l2p(acc, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"], q_bar)
     if aux is not None:
         cs.wait_stream(aux)
     back = eng.expand_device(qd, yb, q_sort)
-    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
-                           order=_coherent(back, p_sort))
+    out = _l2p(back, src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, p_sort, wts=src.w)
     w_bar, p_bar = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
     HostIO.finish()
     eng.flag.raise_if_set("source/query")
@@ -152,7 +168,7 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     acc = engine.expand_device(sources.p, sources.w, p_sort)
     coherent = acc.grid.storage.numel() * 4 > COHERENT_L2P_BYTES
     q_sort = engine.sort_points(qd) if coherent else None   # else sorted by the backward
-    vals = acc.eval_device(qd, _lib.L2P_VALUE, order=q_sort[0] if coherent else None)["value"]
+    vals = _l2p(acc, qd, _lib.L2P_VALUE, q_sort)["value"]
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=like_input(vals, q), accessor=acc, q=q, sources=sources,
                           engine=engine, q_dev=qd, sorts=(p_sort, q_sort))
@@ -166,11 +182,9 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     src = res.sources
     p_sort, q_sort = _sorts(res)
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    q_bar = res.accessor.eval_device(qd, _lib.L2P_WGRAD, wts=yb,
-                                     order=_coherent(res.accessor, q_sort))["wgrad"]
+    q_bar = _l2p(res.accessor, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"]
     back = eng.expand_device(qd, yb, q_sort)
-    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w,
-                           order=_coherent(back, p_sort))
+    out = _l2p(back, src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, p_sort, wts=src.w)
     eng.flag.raise_if_set("source/query")
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),

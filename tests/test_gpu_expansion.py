@@ -54,7 +54,12 @@ def test_cell_sort_is_stable_counting_sort(eng4, heavy):
         idx = rng.permutation(50_000)
         p[idx[:heavy]] = p[idx[0]]            # a heavy cell, scattered indices
         p[idx[heavy:heavy + 300]] = p[idx[heavy]]
-    order, start = eng4.sort_points(torch.from_numpy(p).cuda())
+    srt = eng4.sort_points(torch.from_numpy(p).cuda(), with_points=True)
+    order, start = srt
+    o = order.cpu().numpy()
+    # by-products: inverse permutation and the points in sorted order
+    assert np.array_equal(srt.inv.cpu().numpy()[o], np.arange(o.size))
+    assert np.array_equal(srt.pts_sorted.cpu().numpy(), p[o])
     from oracle.fc2t2_oracle import find_box
     b = find_box(4, p.astype(np.float64))
     key = (b[:, 0] * 32 + b[:, 1]) * 32 + b[:, 2]
@@ -353,3 +358,28 @@ def test_expand_slabs_assemble_full_cascade(cuda):
         assert torch.equal(torch.cat(parts), full)
     with pytest.raises(Exception):
         eng.cascade_device(m, (2, 16))        # not a multiple of 4
+
+
+def test_presorted_l2p_and_p2m_match_natural_order(eng4):
+    """FC2T2_L2P_PRESORTED (inputs permuted into cell order, outputs scattered
+    by order) and P2M on pre-sorted points give bit-identical results to the
+    natural-order paths."""
+    from paper_2111_00110_b200 import _lib
+    from paper_2111_00110_b200.expansion import Accessor
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    p = torch.rand(20_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(20_000, 2, device="cuda", generator=gen)
+    plain = eng4.p2m_device(p, w, eng4.sort_points(p))
+    srt = eng4.sort_points(p, with_points=True)
+    pre = eng4.p2m_device(p, w, srt)
+    assert torch.equal(plain.storage, pre.storage)
+    from paper_2111_00110_b200.expansion import ExpansionGrid
+    L = ExpansionGrid(plain.level, "L", plain.storage, plain.rho)
+    acc = Accessor(L, eng4.table, eng4.flops, flag=eng4.flag)
+    for mode, keys in ((_lib.L2P_VALUE | _lib.L2P_WGRAD, ("value", "wgrad")),
+                       (_lib.L2P_GRAD, ("grad",))):
+        nat = acc.eval_device(p, mode, wts=w)
+        got = acc.eval_device(srt.pts_sorted, mode | _lib.L2P_PRESORTED, wts=srt.permuted(w),
+                              order=srt[0])
+        for k in keys:
+            assert torch.equal(nat[k], got[k])
