@@ -31,6 +31,7 @@ reported under "secondary" with their own metrics (points/s, rays/s).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -214,6 +215,8 @@ def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None 
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    gc.collect()
+    gc.disable()   # like timeit: no interpreter GC pause inside a timed step
     if stages is not None:
         _lib.profile_enable(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -228,6 +231,7 @@ def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None 
         host += time.perf_counter() - h0
         ev[i][1].record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     if stages is not None:
         stages.update({k: round(v[0] / steps, 4) for k, v in _lib.profile_read().items()})
         stages["_host_call_ms"] = round(1e3 * host / steps, 4)
@@ -393,6 +397,8 @@ def run_ours(args, rank: int, world: int) -> None:
           for _ in range(args.steps)]
     launches0 = _lib.launch_count()
     _lib.profile_enable(True)
+    gc.collect()
+    gc.disable()   # like timeit: no interpreter GC pause inside the timed region
     with Clocks(local) as clk:
         barrier()
         for i in range(args.steps):
@@ -401,6 +407,7 @@ def run_ours(args, rank: int, world: int) -> None:
             step_dev()
             ev[i][1].record(stream)
         barrier()
+    gc.enable()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
     launches = (_lib.launch_count() - launches0) // args.steps
@@ -435,6 +442,8 @@ def run_ours(args, rank: int, world: int) -> None:
     for _ in range(max(0, args.warmup - 1)):
         step_host()
     barrier()
+    gc.collect()
+    gc.disable()
     te0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -444,6 +453,7 @@ def run_ours(args, rank: int, world: int) -> None:
     e1.record(stream)
     barrier()
     e2e_ms = max(e0.elapsed_time(e1), 1000.0 * (time.perf_counter() - te0)) / args.steps
+    gc.enable()
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
