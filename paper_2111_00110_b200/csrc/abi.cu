@@ -178,8 +178,8 @@ uint16_t half_rn(double v, double* val) {
 void build_tc_table(const std::vector<std::vector<int4>>& lists,
                     const std::vector<const double*>& slot_src, int P, int PP, int rho, int level,
                     bool f16, Plan& plan) {
-  int CLS, NC, KS, BSLOT;
-  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, &CLS, &NC, &KS, &BSLOT) != 0) return;
+  int CLS, NC, KS, BSLOT, SB;
+  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, &CLS, &NC, &KS, &BSLOT, &SB) != 0) return;
   const int W = CLS * NC, R = 2 * W, NCG = 8 / CLS;
   const int KI = f16 ? 16 : 8, ESZ = f16 ? 2 : 4;
   std::vector<double> sn(P, 1.0);
@@ -226,8 +226,9 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
               any = true;
             }
           if (!any) continue;
-          const int hi_row = (sg & 1) ? ci * NC : W + ci * NC;
-          const int lo_row = (sg & 1) ? W + ci * NC : ci * NC;
+          const bool odd = (sg & 1) && !SB;   // single-buffered kernels keep [lo | hi]
+          const int hi_row = odd ? ci * NC : W + ci * NC;
+          const int lo_row = odd ? W + ci * NC : ci * NC;
           for (int ks = 0; ks < KS; ++ks) {
             uint8_t* st = plan.tcb.data() + ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * BSLOT;
             for (int kc = 0; kc < 2; ++kc)

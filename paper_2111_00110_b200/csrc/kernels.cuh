@@ -63,8 +63,9 @@ struct TCPlan {
   const float* rk = nullptr;
   const float* s_inv = nullptr;
 };
-// classes per CTA, N per class, K steps, bytes per slot table; 0 on success
-int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot);
+// classes per CTA, N per class, K steps, bytes per slot table, single-buffered
+// layout (B rows always [lo | hi]); 0 on success
+int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* sb);
 // s_n = (h/2)^|n| / n! at a level, graded-lex order (P doubles)
 int tc_moment_scales(int rho, int level, double* s);
 // scratch of one M2L launch: per-channel scale bits + hi/lo operand planes

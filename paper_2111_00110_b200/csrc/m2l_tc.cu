@@ -78,8 +78,16 @@ struct TC {
   static constexpr int CLS = 4 * ((P + 7) / 8 * 8) <= 256 ? 2 : 1;   // target classes per CTA
   static constexpr int NC = CLS == 2 ? (P + 7) / 8 * 8 : (P + 15) / 16 * 16;  // N per class
   static constexpr int W = CLS * NC;                   // one TMEM set; cross MMA N
-  static constexpr int TILES = 6 * W <= 512 ? 2 : 1;
-  static constexpr int TMEM_COLS = pow2_at_least(TILES * 3 * W);
+  // Two target tiles per CTA halve the table traffic.  With the hi*hi set
+  // double buffered a tile needs 3W columns ([hh1 | s | hh0]); when two such
+  // tiles do not fit in 512 columns (rho >= 5) the set is single buffered,
+  // [s | hh] per tile, and the MMA waits for each source-class drain (~3 % of
+  // a group's MMA time).
+  static constexpr bool SB = 6 * W > 512 && 4 * W <= 512;
+  static constexpr int NSETS = SB ? 1 : 2;
+  static constexpr int TW = (SB ? 2 : 3) * W;          // TMEM columns per tile
+  static constexpr int TILES = (6 * W <= 512 || SB) ? 2 : 1;
+  static constexpr int TMEM_COLS = pow2_at_least(TILES * TW);
   static constexpr int TY = 16, TZ = 8;
   static constexpr int WX = TILES + 2, WY = TY + 2, WZ = TZ + 2;
   static constexpr int WROWS = WX * WY * WZ;
@@ -104,6 +112,7 @@ struct TC {
   static constexpr uint32_t IDESC_CROSS = idesc(W);
   static_assert(2 * W <= 256 && W % 16 == 0, "MMA N out of range");
   static_assert(CW % 8 == 0 && (TILES == 1 || CW == W), "drain split");
+  static_assert(TILES * TW <= 512, "TMEM");
 };
 
 constexpr float kLoScale = 2048.f;   // fp16 lo parts carry the residual * 2^11
@@ -373,11 +382,14 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
     const uint32_t wb0 = smem_u32(win), bb0 = smem_u32(bring);
     int n = 0, q = 0;
     for (int sg = 0; sg < 8; ++sg) {
-      const int set = sg & 1;
-      mbar_wait(accfree(set), (sg >> 1) & 1);
+      const int set = T::SB ? 0 : (sg & 1);
+      mbar_wait(accfree(set), (sg / T::NSETS) & 1);
       tc_fence_after();
-      const uint32_t mcol = set ? 0u : (uint32_t)W;     // main D: [hh1 | s] or [s | hh0]
-      const uint64_t xoff = set ? 0u : (uint64_t)W;     // B_hi rows: second half when even
+      // main D: [hh1 | s] (odd) or [s | hh0] (even); single buffered: [s | hh]
+      const uint32_t mcol = (T::SB || set) ? 0u : (uint32_t)W;
+      // B_hi rows: second half for even sigma and always when single buffered
+      const uint64_t xoff = (T::SB || !set) ? (uint64_t)W : 0u;
+      const uint32_t scol = T::SB ? 0u : (uint32_t)W;   // small-term set
       for (int ks = 0; ks < KS; ++ks, ++q) {
         const int buf = q & 1;
         mbar_wait(winready(buf), (q >> 1) & 1);
@@ -398,9 +410,9 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
 #pragma unroll
             for (int t = 0; t < TILES; ++t) {
               const uint64_t arow = ex + (uint64_t)(t * WY * WZ);
-              const uint32_t dt = tmem + (uint32_t)(t * 3 * W);
+              const uint32_t dt = tmem + (uint32_t)(t * T::TW);
               if (elect_one()) umma<H>(dt + mcol, ahi + arow, bd, T::IDESC_MAIN);
-              if (elect_one()) umma<H>(dt + W, alo + arow, bd + xoff, T::IDESC_CROSS);
+              if (elect_one()) umma<H>(dt + scol, alo + arow, bd + xoff, T::IDESC_CROSS);
             }
           }
           if (elect_one()) umma_commit(bempty(s));
@@ -468,9 +480,9 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
     // ---------------- TMEM drain + epilogue ----------------
     const int dq = warp & 3, d = (warp - T::DRAIN_WARP0) >> 2;
     const int t = (d * CW) / W, c0 = (d * CW) % W;
-    const uint32_t tb = tmem + ((uint32_t)(dq * 32) << 16) + (uint32_t)(t * 3 * W + c0);
+    const uint32_t tb = tmem + ((uint32_t)(dq * 32) << 16) + (uint32_t)(t * T::TW + c0);
 #pragma unroll
-    for (int o = 0; o < 3; ++o)
+    for (int o = 0; o < T::TW / W; ++o)
 #pragma unroll
       for (int c = 0; c < CW; c += 8) tmem_zero8(tb + o * W + c);
     tmem_wait_st();
@@ -481,10 +493,10 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
 #pragma unroll
     for (int c = 0; c < CW; ++c) acc[c] = 0.f;
     for (int sg = 0; sg < 8; ++sg) {
-      const int set = sg & 1;
-      mbar_wait(accfull(set), (sg >> 1) & 1);
+      const int set = T::SB ? 0 : (sg & 1);
+      mbar_wait(accfull(set), (sg / T::NSETS) & 1);
       tc_fence_after();
-      const uint32_t hb = tb + (set ? 0u : (uint32_t)(2 * W));
+      const uint32_t hb = tb + (T::SB ? (uint32_t)W : (set ? 0u : (uint32_t)(2 * W)));
 #pragma unroll
       for (int c = 0; c < CW; c += 8) {
         float v[8];
@@ -502,7 +514,7 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
 #pragma unroll
     for (int c = 0; c < CW; c += 8) {
       float v[8];
-      tmem_ld8(tb + W + c, v);
+      tmem_ld8(tb + (T::SB ? 0u : (uint32_t)W) + c, v);
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[c + i] += v[i] * sfac;
     }
@@ -540,7 +552,7 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
 
 }  // namespace
 
-int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot) {
+int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* sb) {
   FC2T2_DISPATCH_RHO(rho, {
     auto fill = [&](auto tag) {
       using T = typename decltype(tag)::type;
@@ -548,6 +560,7 @@ int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot) {
       *nc = T::NC;
       *ks = T::KS;
       *bslot = T::BSLOT;
+      *sb = T::SB ? 1 : 0;
     };
     if (f16) fill(Tag<TC<RHO, true>>{});
     else fill(Tag<TC<RHO, false>>{});
