@@ -204,9 +204,10 @@ vol_totals_kernel(const float* __restrict__ L, int res, const double* __restrict
 // degree-(3(rho+1) + 2 rho + 1) polynomial built in float32 from
 // E'_shift(y) = E'(y + depth0) (shift in float64) composed with S.
 constexpr int VOL_THREADS = 128;
+constexpr int VOL_CH = 2;   // payload channels accumulated per pass over the nodes
 
 template <int RHO, int CC>
-__global__ void __launch_bounds__(VOL_THREADS)
+__global__ void __launch_bounds__(VOL_THREADS, 3)
 vol_payload_kernel(const float* __restrict__ L, int res, const double* __restrict__ org,
                    const double* __restrict__ dir, int64_t R, const double* __restrict__ efit,
                    const double* __restrict__ bg, const float* __restrict__ ybar,
@@ -303,34 +304,40 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
 #pragma unroll
           for (int c = 0; c < CC; ++c) wn[(1 + c) * GN + g] = (float)(yb[c] * ts);
         }
-        // moments of the NCH node-weighted point sets (mono shared by channels)
-        float pay[NCH][P];
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-          for (int k = 0; k < P; ++k) pay[ch][k] = 0.f;
-#pragma unroll 1
-        for (int g = 0; g < GN; ++g) {
-          const float xf = (float)(half * (GL_X[g] + 1.0));
-          float mono[P];
-          monomials<RHO>(fmaf(xf, dirf[0], base[0]), fmaf(xf, dirf[1], base[1]),
-                         fmaf(xf, dirf[2], base[2]), mono);
-#pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
-            const float wt = wn[ch * GN + g];
-#pragma unroll
-            for (int k = 0; k < P; ++k) pay[ch][k] = fmaf(wt, mono[k], pay[ch][k]);
-          }
-        }
+        // moments of the NCH node-weighted point sets, VOL_CH channels per
+        // pass over the nodes (monomials recomputed per pass: bounds the
+        // live accumulators to VOL_CH * P registers)
         keys[item] = ((uint32_t)b0 * res + b1) * res + b2;
+#pragma unroll 1
+        for (int ch0 = 0; ch0 < NCH; ch0 += VOL_CH) {
+          float pay[VOL_CH][P];
 #pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-          float* dst = payload + (item * NCH + ch) * PP;
+          for (int ch = 0; ch < VOL_CH; ++ch)
 #pragma unroll
-          for (int k = 0; k < PP; k += 4)
-            *reinterpret_cast<float4*>(dst + k) = make_float4(
-                k < P ? pay[ch][k] : 0.f, k + 1 < P ? pay[ch][k + 1] : 0.f,
-                k + 2 < P ? pay[ch][k + 2] : 0.f, k + 3 < P ? pay[ch][k + 3] : 0.f);
+            for (int k = 0; k < P; ++k) pay[ch][k] = 0.f;
+#pragma unroll 1
+          for (int g = 0; g < GN; ++g) {
+            const float xf = (float)(half * (GL_X[g] + 1.0));
+            float mono[P];
+            monomials<RHO>(fmaf(xf, dirf[0], base[0]), fmaf(xf, dirf[1], base[1]),
+                           fmaf(xf, dirf[2], base[2]), mono);
+#pragma unroll
+            for (int ch = 0; ch < VOL_CH; ++ch) {
+              const float wt = ch0 + ch < NCH ? wn[(ch0 + ch) * GN + g] : 0.f;
+#pragma unroll
+              for (int k = 0; k < P; ++k) pay[ch][k] = fmaf(wt, mono[k], pay[ch][k]);
+            }
+          }
+#pragma unroll
+          for (int ch = 0; ch < VOL_CH; ++ch) {
+            if (ch0 + ch >= NCH) break;
+            float* dst = payload + (item * NCH + ch0 + ch) * PP;
+#pragma unroll
+            for (int k = 0; k < PP; k += 4)
+              *reinterpret_cast<float4*>(dst + k) = make_float4(
+                  k < P ? pay[ch][k] : 0.f, k + 1 < P ? pay[ch][k + 1] : 0.f,
+                  k + 2 < P ? pay[ch][k + 2] : 0.f, k + 3 < P ? pay[ch][k + 3] : 0.f);
+          }
         }
         ++item;
       }
