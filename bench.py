@@ -268,6 +268,15 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     out["cfg1_explicit_2d"] = {"metric": "points/s (N+M)", "value": 2 * n / (ms / steps / 1e3),
                                "ms_per_step": ms / steps,
                                "workload": "N=M=4096, 2D lifted to z=0.03125, level 4, alpha 200"}
+    # the same step replayed as one CUDA graph (graphs.GraphedExplicit): the
+    # config is launch-bound, ~45 kernels for 8192 points
+    from paper_2111_00110_b200.graphs import GraphedExplicit
+    g1 = GraphedExplicit(e1, P, W, Q, YB)
+    ms, _ = timed_steps(lambda: g1(P, W, Q, YB), steps, 3, flush, stream)
+    out["cfg1_explicit_2d_graphed"] = {
+        "metric": "points/s (N+M)", "value": 2 * n / (ms / steps / 1e3), "ms_per_step": ms / steps,
+        "workload": "config 1 as a CUDA-graph replay (inputs copied in, domain flag read per step)"}
+    del g1
     # config 3: root-implicit depth + normal, 512x512 rays, level 5, bias +0.05
     rng = np.random.default_rng(33)
     N3 = 1 << 18

@@ -66,9 +66,10 @@ struct Tag {
   using type = T;
 };
 
-template <int RHO, bool H>
+template <int RHO, bool H, int TL = 0>   // TL > 0 overrides the tiles per CTA
 struct TC {
   static constexpr int RHO_ = RHO;
+  static constexpr int TL_ = TL;
   static constexpr int P = index_count(RHO);
   static constexpr int PP = pad4(P);
   static constexpr int KI = H ? 16 : 8;                 // K per MMA instruction (32 B rows)
@@ -86,7 +87,7 @@ struct TC {
   static constexpr bool SB = 6 * W > 512 && 4 * W <= 512;
   static constexpr int NSETS = SB ? 1 : 2;
   static constexpr int TW = (SB ? 2 : 3) * W;          // TMEM columns per tile
-  static constexpr int TILES = (6 * W <= 512 || SB) ? 2 : 1;
+  static constexpr int TILES = TL > 0 ? TL : ((6 * W <= 512 || SB) ? 2 : 1);
   static constexpr int TMEM_COLS = pow2_at_least(TILES * TW);
   static constexpr int TY = 16, TZ = 8;
   static constexpr int WX = TILES + 2, WY = TY + 2, WZ = TZ + 2;
@@ -320,13 +321,13 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ------------------------------------------------------------ M2L (tc) ---
-template <int RHO, bool H>
+template <int RHO, bool H, int TL>
 __global__ void __launch_bounds__(512, 1)
 m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, const float* __restrict__ rk,
               const uint32_t* __restrict__ gbits, float* __restrict__ L, int res, int nu, int C,
               int accumulate, int ux_begin) {
-  using T = TC<RHO, H>;
+  using T = TC<RHO, H, TL>;
   constexpr int W = T::W, NS = T::NS, KS = T::KS, TILES = T::TILES, CW = T::CW;
   constexpr int WROWS = T::WROWS, WY = T::WY, WZ = T::WZ;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -649,10 +650,14 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
   auto launch = [&](auto tag) -> cudaError_t {
     using T = typename decltype(tag)::type;
     constexpr bool H = T::ESZ == 2;
-    auto kern = m2l_tc_kernel<T::RHO_, H>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)T::SMEM);
-    if (e != cudaSuccess) return e;
+    auto kern = m2l_tc_kernel<T::RHO_, H, T::TL_>;
+    static bool attr = false;   // once per instantiation (nothing but launches in graph capture)
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)T::SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
     const uint8_t* hi = w + gbits_bytes(C);
     const uint8_t* lo = hi + plane_bytes<T::RHO_, H>(plan.level, C);
     dim3 grid((unsigned)((ux_count / T::TILES) * (nu / T::TY) * (nu / T::TZ)),
@@ -662,8 +667,20 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
                                                         nu, C, accumulate, ux_begin));
     return cudaGetLastError();
   };
+  // grids that cannot fill the machine with two-tile CTAs (small levels, thin
+  // slabs) use one tile per CTA: twice the CTAs, same tables
+  auto ctas = [&](auto tag) -> int64_t {
+    using T = typename decltype(tag)::type;
+    return (int64_t)(ux_count / T::TILES) * (nu / T::TY) * (nu / T::TZ) * (8 / T::CLS) * C;
+  };
   FC2T2_DISPATCH_RHO(rho, {
-    if (plan.f16) return launch(Tag<TC<RHO, true>>{});
+    if (plan.f16) {
+      if (TC<RHO, true>::TILES == 2 && ctas(Tag<TC<RHO, true>>{}) < 148)
+        return launch(Tag<TC<RHO, true, 1>>{});
+      return launch(Tag<TC<RHO, true>>{});
+    }
+    if (TC<RHO, false>::TILES == 2 && ctas(Tag<TC<RHO, false>>{}) < 148)
+      return launch(Tag<TC<RHO, false, 1>>{});
     return launch(Tag<TC<RHO, false>>{});
   });
   return cudaGetLastError();

@@ -183,12 +183,30 @@ def _host_domain_check(a, what: str) -> None:
 
 
 class DomainFlag:
-    """Device int32 accumulating FLAG_* bits; read once per public call."""
+    """Device int32 accumulating FLAG_* bits; read once per public call.
+    ``deferred()`` suspends the read (CUDA-graph capture: a host sync cannot
+    be captured; graphs.py checks the flag once after each replay)."""
 
     def __init__(self):
         self.t = torch.zeros(1, dtype=torch.int32, device=_device())
+        self._defer = 0
+
+    class _Deferred:
+        def __init__(self, flag):
+            self.flag = flag
+
+        def __enter__(self):
+            self.flag._defer += 1
+
+        def __exit__(self, *a):
+            self.flag._defer -= 1
+
+    def deferred(self):
+        return DomainFlag._Deferred(self)
 
     def raise_if_set(self, what: str) -> None:
+        if self._defer:
+            return
         v = int(self.t.item())
         if v & _lib.FLAG_DOMAIN:
             self.t.zero_()

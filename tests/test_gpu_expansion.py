@@ -383,3 +383,31 @@ def test_presorted_l2p_and_p2m_match_natural_order(eng4):
                               order=srt[0])
         for k in keys:
             assert torch.equal(nat[k], got[k])
+
+
+def test_graphed_explicit_replays_bit_identical(eng4):
+    """CUDA-graph replay of the explicit layer step (graphs.GraphedExplicit):
+    outputs equal the eager layer bit for bit, new inputs are picked up on
+    replay, and an out-of-domain input raises DomainError after the replay."""
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.expansion import DomainError
+    from paper_2111_00110_b200.graphs import GraphedExplicit
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    mk = lambda *s: torch.rand(*s, device="cuda", generator=gen) * 1.999998 - 0.999999  # noqa: E731
+    p, q = mk(4096, 3), mk(4096, 3)
+    w, yb = torch.randn(4096, 1, device="cuda", generator=gen), torch.randn(4096, 1, device="cuda", generator=gen)
+    step = GraphedExplicit(eng4, p, w, q, yb)
+    for it in range(2):
+        if it:
+            p, q = mk(4096, 3), mk(4096, 3)
+        got = [t.clone() for t in step(p, w, q, yb)]
+        r = explicit_forward(eng4, SourceSet(p, w), q)
+        g = explicit_jvp(yb, r)
+        for a, b in zip(got, (r.values, g.w_bar, g.p_bar, g.q_bar)):
+            assert torch.equal(a, b)
+    bad = q.clone()
+    bad[7, 0] = 1.5
+    with pytest.raises(DomainError):
+        step(q=bad)
+    step(q=q)   # the flag is re-zeroed inside the graph
