@@ -53,6 +53,7 @@ struct Plan {
   // tcgen05 form (parity levels): dense split tables, see build_tc_table
   bool tc = false;
   bool f16 = true;
+  bool merge_last = false;
   std::vector<uint8_t> tcb;
   std::vector<float> rk, s_inv;
   uint8_t* d_tcb = nullptr;
@@ -132,6 +133,11 @@ float rn_tf32_host(double v) {
   return f;
 }
 
+bool nomerge_mode() {
+  const char* v = std::getenv("FC2T2_TC_NOMERGE");
+  return v && v[0] == '1';
+}
+
 // host round-to-nearest-even to fp16; returns the bits and the exact value
 uint16_t half_rn(double v, double* val) {
   const uint16_t sign = v < 0 ? 0x8000 : 0;
@@ -178,8 +184,10 @@ uint16_t half_rn(double v, double* val) {
 void build_tc_table(const std::vector<std::vector<int4>>& lists,
                     const std::vector<const double*>& slot_src, int P, int PP, int rho, int level,
                     bool f16, Plan& plan) {
-  int CLS, NC, KS, BSLOT, SB;
-  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, &CLS, &NC, &KS, &BSLOT, &SB) != 0) return;
+  int CLS, NC, KS, BSLOT, FL;
+  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, &CLS, &NC, &KS, &BSLOT, &FL) != 0) return;
+  const bool SB = FL & 1, MERGE = (FL & 2) && !nomerge_mode();
+  plan.merge_last = MERGE;
   const int W = CLS * NC, R = 2 * W, NCG = 8 / CLS;
   const int KI = f16 ? 16 : 8, ESZ = f16 ? 2 : 4;
   std::vector<double> sn(P, 1.0);
@@ -231,14 +239,28 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
           const int lo_row = odd ? W + ci * NC : ci * NC;
           for (int ks = 0; ks < KS; ++ks) {
             uint8_t* st = plan.tcb.data() + ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * BSLOT;
+            // merged last step (TC::MERGE_LAST): chunk 1 multiplies the A_lo
+            // chunk of the same inputs -> rows [hi: 0 | lo: B_hi]
+            const bool merged = MERGE && ks == KS - 1;
             for (int kc = 0; kc < 2; ++kc)
               for (int k = 0; k < P; ++k)
                 for (int f = 0; f < KI / 2; ++f) {
-                  const int n = KI * ks + (KI / 2) * kc + f;
+                  const int n = KI * ks + (merged ? 0 : (KI / 2) * kc) + f;
                   if (n >= P) continue;
                   const double a = A[(size_t)k * P + n];
                   uint8_t* ph = st + ((size_t)kc * R + hi_row + k) * 16 + f * ESZ;
                   uint8_t* pl = st + ((size_t)kc * R + lo_row + k) * 16 + f * ESZ;
+                  if (merged && kc == 1) {
+                    if (f16) {
+                      double hv;
+                      const uint16_t hb = half_rn(a * sn[n] / rk[k], &hv);
+                      std::memcpy(pl, &hb, 2);
+                    } else {
+                      const float hi = rn_tf32_host(a);
+                      std::memcpy(pl, &hi, 4);
+                    }
+                    continue;   // hi rows stay zero
+                  }
                   if (f16) {
                     const double b = a * sn[n] / rk[k];
                     double hv, lv;
@@ -340,6 +362,7 @@ fc2t2::TCPlan tc_of(const fc2t2_engine* e, const Plan& p, int level) {
   t.f16 = p.f16;
   t.rk = p.d_rk;
   t.s_inv = p.d_sinv;
+  t.merge_last = p.merge_last;
   static const char* names[] = {"m2l_tc_L0", "m2l_tc_L1", "m2l_tc_L2", "m2l_tc_L3", "m2l_tc_L4",
                                 "m2l_tc_L5", "m2l_tc_L6", "m2l_tc_L7", "m2l_tc_L8", "m2l_tc_L9"};
   t.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];

@@ -62,9 +62,11 @@ struct TCPlan {
   bool f16 = true;
   const float* rk = nullptr;
   const float* s_inv = nullptr;
+  bool merge_last = true;   // tables built with the merged last K step
 };
-// classes per CTA, N per class, K steps, bytes per slot table, single-buffered
-// layout (B rows always [lo | hi]); 0 on success
+// classes per CTA, N per class, K steps, bytes per slot table, flags (bit 0:
+// single-buffered layout, B rows always [lo | hi]; bit 1: merged last K step,
+// see TC::MERGE_LAST); 0 on success
 int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* sb);
 // s_n = (h/2)^|n| / n! at a level, graded-lex order (P doubles)
 int tc_moment_scales(int rho, int level, double* s);

@@ -103,6 +103,11 @@ struct TC {
   static constexpr int DRAIN_WARP0 = 8, DW = 2;
   static constexpr int DRAIN_THREADS = 32 * 4 * DW;
   static constexpr int CW = TILES * W / DW;           // accumulator columns per drain thread
+  // The last K step holds P - (KS-1)*KI real inputs; when they fit in one
+  // chunk (KI/2), its A operand is [A_hi chunk | A_lo chunk] (descriptor LBO
+  // spanning the two window parts) against table rows [B_hi | B_lo] and
+  // [0 | B_hi]: one main MMA yields all three products, no cross MMA.
+  static constexpr bool MERGE_LAST = P - (KS - 1) * KI <= KI / 2;
   static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 256;
   // instruction descriptor: D f32; A/B tf32 (2) or f16 (0); K-major; N >> 3; M >> 4
   static constexpr uint32_t idesc(int n) {
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(512, 1)
 m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, const float* __restrict__ rk,
               const uint32_t* __restrict__ gbits, float* __restrict__ L, int res, int nu, int C,
-              int accumulate, int ux_begin) {
+              int accumulate, int ux_begin, int merge_last) {
   using T = TC<RHO, H, TL>;
   constexpr int W = T::W, NS = T::NS, KS = T::KS, TILES = T::TILES, CW = T::CW;
   constexpr int WROWS = T::WROWS, WY = T::WY, WZ = T::WZ;
@@ -397,6 +402,9 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
         tc_fence_after();
         const uint64_t ahi = sdesc(wb0 + buf * T::WSLICE, WROWS * 16, WZ * 16);
         const uint64_t alo = ahi + (uint64_t)(2 * WROWS);
+        const bool merged = T::MERGE_LAST && merge_last && ks == KS - 1;
+        // merged last step: K chunk 1 = the lo part's chunk 0, 2 WROWS rows on
+        const uint64_t amain = merged ? sdesc(wb0 + buf * T::WSLICE, 2 * WROWS * 16, WZ * 16) : ahi;
 #pragma unroll
         for (int ch = 0; ch < T::CHUNKS; ++ch, ++n) {
           const int s = n % NS;
@@ -412,8 +420,9 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
             for (int t = 0; t < TILES; ++t) {
               const uint64_t arow = ex + (uint64_t)(t * WY * WZ);
               const uint32_t dt = tmem + (uint32_t)(t * T::TW);
-              if (elect_one()) umma<H>(dt + mcol, ahi + arow, bd, T::IDESC_MAIN);
-              if (elect_one()) umma<H>(dt + scol, alo + arow, bd + xoff, T::IDESC_CROSS);
+              if (elect_one()) umma<H>(dt + mcol, amain + arow, bd, T::IDESC_MAIN);
+              if (!merged && elect_one())
+                umma<H>(dt + scol, alo + arow, bd + xoff, T::IDESC_CROSS);
             }
           }
           if (elect_one()) umma_commit(bempty(s));
@@ -561,7 +570,7 @@ int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* s
       *nc = T::NC;
       *ks = T::KS;
       *bslot = T::BSLOT;
-      *sb = T::SB ? 1 : 0;
+      *sb = (T::SB ? 1 : 0) | (T::MERGE_LAST ? 2 : 0);
     };
     if (f16) fill(Tag<TC<RHO, true>>{});
     else fill(Tag<TC<RHO, false>>{});
@@ -664,7 +673,8 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
               (unsigned)(8 / T::CLS), (unsigned)C);
     FC2T2_LAUNCH(plan.level_name, s,
                  kern<<<grid, T::THREADS, T::SMEM, s>>>(hi, lo, plan.btab, plan.rk, gbits, L, res,
-                                                        nu, C, accumulate, ux_begin));
+                                                        nu, C, accumulate, ux_begin,
+                                                        plan.merge_last ? 1 : 0));
     return cudaGetLastError();
   };
   // grids that cannot fill the machine with two-tile CTAs (small levels, thin
