@@ -277,6 +277,32 @@ def secondary(dev, flush, stream, steps: int) -> dict:
         "metric": "points/s (N+M)", "value": 2 * n / (ms / steps / 1e3), "ms_per_step": ms / steps,
         "workload": "config 1 as a CUDA-graph replay (inputs copied in, domain flag read per step)"}
     del g1
+    # one fit-sdf training epoch (cli.py:129-145) at config-2
+    # size on the device: explicit layer fwd, MAE loss + tangent, JVP, Adam step
+    from paper_2111_00110_b200.trainer import Optimizer, TrainConfig, fit_sdf_epoch
+    rng_f = np.random.default_rng(22)
+    e5f = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    Nf, Mf = 1 << 20, 10_000_000
+    pf = torch.from_numpy(rng_f.uniform(-1 + 1e-6, 1 - 1e-6, (Nf, 3)).astype(np.float32)).to(dev)
+    wf = torch.from_numpy(rng_f.uniform(-1e-2, 1e-2, (Nf, 1)).astype(np.float32)).to(dev)
+    qf = torch.from_numpy(rng_f.uniform(lo, 1, (Mf, 3)).astype(np.float32)).to(dev)
+    tf = torch.from_numpy(rng_f.normal(0, 0.1, (Mf, 1)).astype(np.float32)).to(dev)
+    optf = Optimizer(TrainConfig(optimizer="adam", learning_rate=1e-3, l1_weight=1e-6))
+    state = {"src": SourceSet(pf, wf), "bias": 0.0, "epoch": 0}
+
+    def epoch_f():
+        st = state
+        st["src"], st["bias"], loss, _ = fit_sdf_epoch(e5f, st["src"], st["bias"], qf, tf, optf,
+                                                       st["epoch"])
+        st["epoch"] += 1
+        return loss
+    ms, _ = timed_steps(epoch_f, steps, 3, flush, stream)
+    out["fit_sdf_epoch"] = {
+        "metric": "epochs/s", "value": 1e3 / (ms / steps), "ms_per_step": ms / steps,
+        "points_per_s": (Nf + Mf) / (ms / steps / 1e3),
+        "workload": "fit-sdf epoch (cli.py:129-145): N=2^20 sources, batch M=10^7 samples, "
+                    "level 5, Adam lr 1e-3, MAE, L1 1e-6; loss read back every epoch"}
+    del pf, wf, qf, tf, state, optf, e5f
     # config 3: root-implicit depth + normal, 512x512 rays, level 5, bias +0.05
     rng = np.random.default_rng(33)
     N3 = 1 << 18

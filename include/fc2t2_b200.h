@@ -206,6 +206,30 @@ int fc2t2_vol_payload(int rho, int level, int colors, const float* d_l, const do
                       const double* d_totals, const double* d_depth_final, const double* d_gl_x,
                       const double* d_gl_w, uint32_t* d_keys, float* d_payload, void* stream);
 
+/* ---- training glue: trainer.py (reference trainer.py:70-152) ----
+ * Losses (loss_and_tangent, trainer.py:70-105): diff = pred + bias - target
+ * over valid entries (d_mask (n) uint8, optional, broadcast over the `cols`
+ * columns); d_tangent (n, cols) = d loss / d pred; d_stats (3 doubles) =
+ * count, loss, sum(tangent) (the bias tangent of cli.py fit loops).
+ * Deterministic float64 reductions. */
+#define FC2T2_LOSS_MAE 0
+#define FC2T2_LOSS_MSE 1
+size_t fc2t2_loss_workspace_size(int64_t n, int cols);
+int fc2t2_loss(const float* d_pred, const float* d_target, const uint8_t* d_mask, int64_t n,
+               int cols, float bias, int kind, float* d_tangent, double* d_stats, void* d_ws,
+               size_t ws_bytes, void* stream);
+/* sets *d_flag |= 1 when d_x holds a NaN or Inf (Optimizer.step's check) */
+int fc2t2_nonfinite(const float* d_x, int64_t n, int32_t* d_flag, void* stream);
+/* Optimizer.step for one tensor (trainer.py:122-152): grad + l1 sign(x)
+ * (l1_term, trainer.py:108-112); Adam (t = step count, bias-corrected, betas
+ * 0.9/0.999, eps 1e-8; d_m/d_v state) or SGD; x -= lr d; clip (positions) to
+ * [-1 + 1e-6, 1 - 1e-6].  No-op while *d_flag != 0 (non-finite gradient). */
+#define FC2T2_OPT_SGD 0
+#define FC2T2_OPT_ADAM 1
+int fc2t2_opt_step(float* d_x, const float* d_grad, float* d_m, float* d_v, int64_t n,
+                   int optimizer, float lr, int64_t t, float l1, int clip, const int32_t* d_flag,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -131,4 +131,14 @@ cudaError_t vol_payload(int rho, int level, int CC, const float* L, const double
                         const float* ybar, const uint32_t* alive_offsets, const double* totals,
                         const double* depth_final, const double* gl_x, const double* gl_w,
                         uint32_t* keys, float* payload, cudaStream_t s);
+// train.cu ----------------------------------------------------------------
+size_t loss_workspace_bytes(int64_t n, int cols);
+// stats (3 doubles): count, loss, sum(tangent)
+cudaError_t loss_tangent(const float* pred, const float* target, const uint8_t* mask, int64_t n,
+                         int cols, float bias, int mse, float* tangent, double* stats, void* ws,
+                         cudaStream_t s);
+cudaError_t nonfinite(const float* x, int64_t n, int32_t* flag, cudaStream_t s);
+cudaError_t opt_step(float* x, const float* g, float* m, float* v, int64_t n, int adam, float lr,
+                     float c1, float c2, float l1, int clip, const int32_t* flag, cudaStream_t s);
+
 }  // namespace fc2t2
