@@ -457,6 +457,16 @@ line_payload_kernel(int res, int C, const double* __restrict__ org,
 // ----------------------------------------------------------- insertion ---
 // Sum per-item payload rows into their cells in sorted (deterministic) order
 // (reference _insert_moments, layers.py:144-153).
+// Light cells (<= INS_LIGHT items): one thread per (cell, channel) sums the
+// rows in sorted order.  Heavier cells (surface cells collecting hundreds of
+// root payloads, or the segment moments of the radiance backward) are summed
+// by one warp each in a second kernel (a warp per (cell, channel), light ones
+// skipped): PP/4 lanes read one row (coalesced), WR = 32 /
+// (PP/4) rows in flight; lane (r, q) accumulates float4 q of rows r, r+WR, ...
+// and the WR partial sums are added in fixed order.  The summation order
+// depends only on the cell's item count -> deterministic.
+constexpr int INS_LIGHT = 8;
+
 template <int PP>
 __global__ void __launch_bounds__(128)
 insert_sorted_kernel(const float* __restrict__ payload, int C, int64_t R,
@@ -466,10 +476,11 @@ insert_sorted_kernel(const float* __restrict__ payload, int C, int64_t R,
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cell = g / C;
     const int c = (int)(g - cell * C);
+    const int beg = cell_start[cell], end = cell_start[cell + 1];
+    if (end - beg > INS_LIGHT) continue;   // insert_heavy_kernel
     float acc[PP];
 #pragma unroll
     for (int j = 0; j < PP; ++j) acc[j] = 0.f;
-    const int beg = cell_start[cell], end = cell_start[cell + 1];
     for (int k = beg; k < end; ++k) {
       const float* src = payload + ((int64_t)order[k] * C + c) * PP;
 #pragma unroll
@@ -482,6 +493,42 @@ insert_sorted_kernel(const float* __restrict__ payload, int C, int64_t R,
     for (int j = 0; j < PP; j += 4)
       *reinterpret_cast<float4*>(M + g * PP + j) =
           make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+  }
+}
+
+template <int PP>
+__global__ void __launch_bounds__(256)
+insert_heavy_kernel(const float* __restrict__ payload, int C, int64_t R,
+                    const int32_t* __restrict__ order, const int32_t* __restrict__ cell_start,
+                    float* __restrict__ M) {
+  constexpr int Q = PP / 4;                  // float4 per row
+  constexpr int WR = 32 / Q > 0 ? 32 / Q : 1;  // rows in flight per warp
+  const int lane = threadIdx.x & 31;
+  const int r = lane / Q, q = lane - r * Q;
+  const bool active = r < WR && q < Q;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < R * C;
+       g += warps) {
+    const int64_t cell = g / C;
+    const int c = (int)(g - cell * C);
+    const int beg = cell_start[cell], end = cell_start[cell + 1];
+    if (end - beg <= INS_LIGHT) continue;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (active)
+      for (int k = beg + r; k < end; k += WR) {
+        const float4 v =
+            __ldg(reinterpret_cast<const float4*>(payload + ((int64_t)order[k] * C + c) * PP) + q);
+        a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+      }
+    // fixed-order sum of the WR row partials into lanes 0..Q-1
+    for (int rr = 1; rr < WR; ++rr) {
+      const float bx = __shfl_sync(0xffffffffu, a.x, rr * Q + q);
+      const float by = __shfl_sync(0xffffffffu, a.y, rr * Q + q);
+      const float bz = __shfl_sync(0xffffffffu, a.z, rr * Q + q);
+      const float bw = __shfl_sync(0xffffffffu, a.w, rr * Q + q);
+      if (r == 0) { a.x += bx; a.y += by; a.z += bz; a.w += bw; }
+    }
+    if (r == 0 && q < Q) reinterpret_cast<float4*>(M + g * PP)[q] = a;
   }
 }
 
@@ -562,6 +609,8 @@ cudaError_t insert_sorted(int rho, int level, int C, const float* payload, const
     FC2T2_LAUNCH("insert", s, insert_sorted_kernel<V><<<grid_blocks(R * C, 128, 148 * 64),  \
                                                         128, 0, s>>>(payload, C, R, order,   \
                                                                      cell_start, M));        \
+    FC2T2_LAUNCH("insert", s, insert_heavy_kernel<V><<<grid_blocks(R * C * 32, 256, 148 * 32), \
+                                  256, 0, s>>>(payload, C, R, order, cell_start, M));        \
     break;
     FC2T2_INS(4)
     FC2T2_INS(12)

@@ -31,6 +31,13 @@ for i in range(30):
     torch.cuda.synchronize(); t0 = time.perf_counter(); step3(); torch.cuda.synchronize()
     ts.append(1e3 * (time.perf_counter() - t0))
 print("STEP ms", [round(t, 2) for t in ts])
+from paper_2111_00110_b200 import _lib
+_lib.profile_enable(True)
+for _ in range(10):
+    step3()
+torch.cuda.synchronize()
+prof = _lib.profile_read(); _lib.profile_enable(False)
+print("CFG3", {k: (round(v[0] / 10, 4), v[1] // 10) for k, v in sorted(prof.items(), key=lambda x: -x[1][0])})
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     for _ in range(3):
         step3()
