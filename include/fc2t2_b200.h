@@ -121,6 +121,10 @@ int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float
 /* M2L of one table.  With a workspace of fc2t2_m2l_workspace_size bytes the
  * parity levels run the tcgen05 3xTF32 kernel; without one, FP32 FFMA. */
 size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table);
+/* Tensor-core FLOPs (2 M N K per tcgen05.mma, K/N padding and the split's
+ * cross products included) one M2L launch of this table issues; 0 when the
+ * table runs on FFMA.  The algorithmic count is pairs * C * P^2 * 2. */
+double fc2t2_m2l_issued_flops(const fc2t2_engine* e, int channels, int level, int table);
 int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const float* d_m,
               float* d_l, int accumulate, void* d_ws, size_t ws_bytes, void* stream);
 

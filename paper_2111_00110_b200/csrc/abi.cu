@@ -665,6 +665,12 @@ int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float
                      "l2l");
 }
 
+double fc2t2_m2l_issued_flops(const fc2t2_engine* e, int channels, int level, int table) {
+  const Plan* p;
+  if (plan_for(e, level, table, &p) != FC2T2_OK || !use_tc(*p, level)) return 0.0;
+  return fc2t2::tc_issued_flops(e->rho, level, channels, p->f16 ? 1 : 0, p->merge_last ? 1 : 0);
+}
+
 size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table) {
   const Plan* p;
   if (plan_for(e, level, table, &p) != FC2T2_OK) return 0;

@@ -68,6 +68,9 @@ struct TCPlan {
 // single-buffered layout, B rows always [lo | hi]; bit 1: merged last K step,
 // see TC::MERGE_LAST); 0 on success
 int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* sb);
+// tensor-core FLOPs one m2l_tc launch issues (2 M N K per MMA, padding and
+// split terms included) for a whole level
+double tc_issued_flops(int rho, int level, int C, int f16, int merge_last);
 // s_n = (h/2)^|n| / n! at a level, graded-lex order (P doubles)
 int tc_moment_scales(int rho, int level, double* s);
 // scratch of one M2L launch: per-channel scale bits + hi/lo operand planes

@@ -579,6 +579,25 @@ int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* s
   return -1;
 }
 
+double tc_issued_flops(int rho, int level, int C, int f16, int merge_last) {
+  const int nu = (1 << (level + 1)) / 2;
+  FC2T2_DISPATCH_RHO(rho, {
+    auto count = [&](auto tag) -> double {
+      using T = typename decltype(tag)::type;
+      int tiles = T::TILES;
+      const double ctas2 = (double)(nu / T::TILES) * (nu / T::TY) * (nu / T::TZ) * (8 / T::CLS) * C;
+      if (T::TILES == 2 && ctas2 < 148) tiles = 1;   // m2l_tc's small-grid variant
+      const double tile_slots = (double)nu * (nu / T::TY) * (nu / T::TZ) * (8 / T::CLS) * C * 8 * 27;
+      (void)tiles;
+      const int cross_steps = (T::MERGE_LAST && merge_last) ? T::KS - 1 : T::KS;
+      const double k = T::KI, m = 128;
+      return tile_slots * (T::KS * 2.0 * m * (2 * T::W) * k + cross_steps * 2.0 * m * T::W * k);
+    };
+    return f16 ? count(Tag<TC<RHO, true>>{}) : count(Tag<TC<RHO, false>>{});
+  });
+  return 0.0;
+}
+
 int tc_moment_scales(int rho, int level, double* s) {
   const double half = 1.0 / (double)(1 << (level + 1));   // half the cell width 2/res
   FC2T2_DISPATCH_RHO(rho, {
