@@ -201,6 +201,12 @@ int fc2t2_vol_forward(int rho, int level, int colors, const float* d_l, const do
                       const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
                       float* d_rgb, double* d_depth_final, const uint32_t* d_seg_offsets,
                       uint8_t* d_seg_alive, void* stream);
+/* forward that also returns pass A's outputs (n_alive (R), totals (R, colors)),
+ * bit-identical to fc2t2_vol_totals: the backward then skips pass A */
+int fc2t2_vol_forward_ex(int rho, int level, int colors, const float* d_l, const double* d_org,
+                         const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
+                         float* d_rgb, double* d_depth_final, uint32_t* d_n_alive,
+                         double* d_totals, void* stream);
 int fc2t2_vol_totals(int rho, int level, int colors, const float* d_l, const double* d_org,
                      const double* d_dir, int64_t R, const double* d_efit, uint32_t* d_n_alive,
                      double* d_totals, double* d_depth_final, void* stream);

@@ -73,6 +73,8 @@ _SIGS = {
     "fc2t2_vol_gauss_nodes": (_i32, [_i32]),
     "fc2t2_vol_forward": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp]),
+    "fc2t2_vol_forward_ex": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                                    _vp, _vp]),
     "fc2t2_vol_totals": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "fc2t2_vol_payload": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp, _vp, _vp, _vp, _vp]),

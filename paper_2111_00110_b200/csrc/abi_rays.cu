@@ -127,6 +127,19 @@ int fc2t2_vol_forward(int rho, int level, int colors, const float* d_l, const do
                  "vol_forward");
 }
 
+int fc2t2_vol_forward_ex(int rho, int level, int colors, const float* d_l, const double* d_org,
+                         const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
+                         float* d_rgb, double* d_depth_final, uint32_t* d_n_alive,
+                         double* d_totals, void* stream) {
+  if (rho != 4) return rfail(FC2T2_EORDER, "the radiance layer is built for rho = 4");
+  if (colors < 1 || colors > 4) return rfail(FC2T2_EVALUE, "1..4 colour channels supported");
+  if (!d_n_alive || !d_totals) return rfail(FC2T2_EVALUE, "vol_forward_ex needs n_alive and totals");
+  return rstatus(fc2t2::vol_forward(rho, level, colors, d_l, d_org, d_dir, R, d_efit, d_bg, d_rgb,
+                                    d_depth_final, nullptr, nullptr, (cudaStream_t)stream,
+                                    d_n_alive, d_totals),
+                 "vol_forward_ex");
+}
+
 int fc2t2_vol_totals(int rho, int level, int colors, const float* d_l, const double* d_org,
                      const double* d_dir, int64_t R, const double* d_efit, uint32_t* d_n_alive,
                      double* d_totals, double* d_depth_final, void* stream) {

@@ -125,7 +125,8 @@ int vol_gauss_nodes(int rho);
 cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double* org,
                         const double* dir, int64_t R, const double* efit, const double* bg,
                         float* rgb, double* depth_final, const uint32_t* seg_offsets,
-                        uint8_t* seg_alive, cudaStream_t s);
+                        uint8_t* seg_alive, cudaStream_t s, uint32_t* n_alive = nullptr,
+                        double* totals = nullptr);
 cudaError_t vol_totals(int rho, int level, int CC, const float* L, const double* org,
                        const double* dir, int64_t R, const double* efit, uint32_t* n_alive,
                        double* totals, double* depth_final, cudaStream_t s);

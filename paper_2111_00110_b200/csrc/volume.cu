@@ -91,7 +91,11 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
                    const double* __restrict__ dir, int64_t R, const double* __restrict__ efit,
                    const double* __restrict__ bg, float* __restrict__ rgb,
                    double* __restrict__ depth_final, const uint32_t* __restrict__ seg_offsets,
-                   uint8_t* __restrict__ seg_alive) {
+                   uint8_t* __restrict__ seg_alive, uint32_t* __restrict__ n_alive,
+                   double* __restrict__ totals) {
+  // With n_alive / totals the walk also produces the backward's pass-A
+  // quantities (same node arithmetic as vol_totals_kernel, bit-identical), so
+  // volumetric_jvp can skip that pass.
   constexpr int PP = MI<RHO>::PP, NCH = 1 + CC;
   double e[5];
 #pragma unroll
@@ -101,9 +105,10 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
     double o[3], d[3];
     load_ray(org, dir, r, o, d);
     const float dirf[3] = {(float)d[0], (float)d[1], (float)d[2]};
-    double depth = 0.0, dfin = 0.0, acc[CC];
+    double depth = 0.0, dfin = 0.0, acc[CC], tot[CC];
 #pragma unroll
-    for (int c = 0; c < CC; ++c) acc[c] = 0.0;
+    for (int c = 0; c < CC; ++c) acc[c] = tot[c] = 0.0;
+    uint32_t na = 0;
     int64_t j = seg_offsets ? (int64_t)seg_offsets[r] : 0;
     walk_ray(o, d, res, [&](double t0, double t1, int b0, int b1, int b2) {
       float base[3];
@@ -122,12 +127,25 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
         for (int g = 0; g < GN; ++g) {
           const double x = half * (GL_X[g] + 1.0);
           const float xf = (float)x;
-          const double T = efit_eval(e, (double)hornerf(S, xf) + depth);
-          const double wts = half * GL_W[g] * T * (double)hornerf(sg, xf);
+          const double y = (double)hornerf(S, xf) + depth;
+          const double T = efit_eval(e, y);
+          const double sgx = (double)hornerf(sg, xf);
+          const double wts = half * GL_W[g] * T * sgx;
+          if (totals) {
+            const double wtp = half * GL_W[g] * efit_deriv(e, y) * sgx;
 #pragma unroll
-          for (int c = 0; c < CC; ++c) acc[c] += wts * (double)hornerf(col[c], xf);
+            for (int c = 0; c < CC; ++c) {
+              const double cx = (double)hornerf(col[c], xf);
+              acc[c] += wts * cx;
+              tot[c] += wtp * cx;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < CC; ++c) acc[c] += wts * (double)hornerf(col[c], xf);
+          }
         }
         dfin += send;
+        ++na;
       }
       if (seg_alive) seg_alive[j++] = alive ? 1 : 0;
       depth += send;
@@ -137,6 +155,11 @@ vol_forward_kernel(const float* __restrict__ L, int res, const double* __restric
 #pragma unroll
     for (int c = 0; c < CC; ++c) rgb[r * CC + c] = (float)(acc[c] + te * bg[c]);
     depth_final[r] = dfin;
+    if (totals) {
+      n_alive[r] = na;
+#pragma unroll
+      for (int c = 0; c < CC; ++c) totals[r * CC + c] = tot[c];
+    }
   }
 }
 
@@ -363,7 +386,7 @@ int vol_gauss_nodes(int rho) { return GN; }
 cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double* org,
                         const double* dir, int64_t R, const double* efit, const double* bg,
                         float* rgb, double* depth_final, const uint32_t* seg_offsets,
-                        uint8_t* seg_alive, cudaStream_t s) {
+                        uint8_t* seg_alive, cudaStream_t s, uint32_t* n_alive, double* totals) {
   if (R <= 0) return cudaSuccess;
   if (rho != 4) return cudaErrorNotSupported;
   constexpr int RHO = 4;
@@ -371,7 +394,7 @@ cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double
   FC2T2_VOL_DISPATCH(CC, FC2T2_LAUNCH("vol_forward", s,
       vol_forward_kernel<RHO, CC><<<blocks, 128, 0, s>>>(L, 1 << (level + 1), org, dir, R, efit,
                                                          bg, rgb, depth_final, seg_offsets,
-                                                         seg_alive)));
+                                                         seg_alive, n_alive, totals)));
   return cudaGetLastError();
 }
 

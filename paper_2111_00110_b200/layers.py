@@ -466,15 +466,19 @@ def volumetric_forward(engine: Engine, p, w_sigma, w_color, bundle: RayBundle, b
         background, torch.Tensor) else background, dtype=torch.float64).to(org.device).reshape(-1)
     rgb = torch.empty((R, C), dtype=torch.float32, device=org.device)
     dfin = torch.empty(R, dtype=torch.float64, device=org.device)
-    _lib.call("fc2t2_vol_forward", engine.rho, engine.levels, C, _ptr(acc.grid.storage),
-              _ptr(org), _ptr(dirs), R, _ptr(efit), _ptr(bg), _ptr(rgb), _ptr(dfin), _ptr(None),
-              _ptr(None), _stream())
+    # the walk also produces the backward's pass-A totals (one walk saved per JVP)
+    n_alive = torch.zeros(R + 1, dtype=torch.int32, device=org.device)
+    totals = torch.empty((R, C), dtype=torch.float64, device=org.device)
+    _lib.call("fc2t2_vol_forward_ex", engine.rho, engine.levels, C, _ptr(acc.grid.storage),
+              _ptr(org), _ptr(dirs), R, _ptr(efit), _ptr(bg), _ptr(rgb), _ptr(dfin),
+              _ptr(n_alive), _ptr(totals), _stream())
     engine.flag.raise_if_set("source")
     ref = bundle.origins
     return RenderResult(rgb=_like(rgb, ref), accessor=acc, trav=trav, bundle=bundle, p=p,
                         w_sigma=w_sigma, w_color=w_color, background=background, engine=engine,
                         depth_final=_like(dfin, ref),
-                        dev={"src": src, "ws": ws, "colors": C, "efit": efit, "bg": bg})
+                        dev={"src": src, "ws": ws, "colors": C, "efit": efit, "bg": bg,
+                             "n_alive": n_alive, "totals": totals, "dfin": dfin})
 
 
 def volumetric_jvp(y_bar, res: RenderResult) -> LayerGradients:
@@ -487,12 +491,15 @@ def volumetric_jvp(y_bar, res: RenderResult) -> LayerGradients:
     dev = org.device
     yb = to_device(y_bar).reshape(R, C).contiguous()
     st = res.accessor.grid.storage
-    n_alive = torch.zeros(R + 1, dtype=torch.int32, device=dev)
-    totals = torch.empty((R, C), dtype=torch.float64, device=dev)
-    dfin = torch.empty(R, dtype=torch.float64, device=dev)
     efit, bg = res.dev["efit"], res.dev["bg"]
-    _lib.call("fc2t2_vol_totals", eng.rho, eng.levels, C, _ptr(st), _ptr(org), _ptr(dirs), R,
-              _ptr(efit), _ptr(n_alive), _ptr(totals), _ptr(dfin), _stream())
+    if "totals" in res.dev:   # pass A came with the forward walk
+        n_alive, totals, dfin = res.dev["n_alive"], res.dev["totals"], res.dev["dfin"]
+    else:
+        n_alive = torch.zeros(R + 1, dtype=torch.int32, device=dev)
+        totals = torch.empty((R, C), dtype=torch.float64, device=dev)
+        dfin = torch.empty(R, dtype=torch.float64, device=dev)
+        _lib.call("fc2t2_vol_totals", eng.rho, eng.levels, C, _ptr(st), _ptr(org), _ptr(dirs), R,
+                  _ptr(efit), _ptr(n_alive), _ptr(totals), _ptr(dfin), _stream())
     offs = torch.empty_like(n_alive)
     ws_b = int(_lib.lib().fc2t2_scan_workspace_size(R + 1))
     wsp = torch.empty(max(ws_b, 4), dtype=torch.uint8, device=dev)

@@ -186,3 +186,25 @@ def test_volumetric_config4_small_matches_reference(cuda):
     gr = volumetric_jvp(g["y"], res)
     assert rel_l2(gr.w_bar, g["w_bar"]) < TOL
     assert rel_l2(gr.p_bar, g["p_bar"]) < TOL
+
+
+def test_forward_pass_a_bit_identical_to_vol_totals(small, eng3):
+    """volumetric_forward's walk also returns the backward's pass-A outputs
+    (fc2t2_vol_forward_ex); they equal fc2t2_vol_totals bit for bit."""
+    import torch
+    from paper_2111_00110_b200 import _lib
+    from paper_2111_00110_b200.expansion import _ptr, _stream
+    from paper_2111_00110_b200.layers import volumetric_forward
+    res = volumetric_forward(eng3, small["p"], small["w_sigma"], small["w_color"], _bundle(small),
+                             small["bg"])
+    org, dirs = res.bundle.dev()
+    R, C = res.bundle.count, res.dev["colors"]
+    n_alive = torch.zeros(R + 1, dtype=torch.int32, device="cuda")
+    totals = torch.empty((R, C), dtype=torch.float64, device="cuda")
+    dfin = torch.empty(R, dtype=torch.float64, device="cuda")
+    _lib.call("fc2t2_vol_totals", eng3.rho, eng3.levels, C, _ptr(res.accessor.grid.storage),
+              _ptr(org), _ptr(dirs), R, _ptr(res.dev["efit"]), _ptr(n_alive), _ptr(totals),
+              _ptr(dfin), _stream())
+    assert torch.equal(n_alive, res.dev["n_alive"])
+    assert torch.equal(totals, res.dev["totals"])
+    assert torch.equal(dfin, res.dev["dfin"])
