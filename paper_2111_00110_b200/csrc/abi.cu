@@ -54,6 +54,7 @@ struct Plan {
   bool tc = false;
   bool f16 = true;
   bool merge_last = false;
+  int cg = 1;
   std::vector<uint8_t> tcb;
   std::vector<float> rk, s_inv;
   uint8_t* d_tcb = nullptr;
@@ -133,6 +134,14 @@ float rn_tf32_host(double v) {
   return f;
 }
 
+// CTA pairs (cta_group::2) are built and parity-tested but opt-in: measured
+// on one box, level 5 0.500 vs 0.484 ms and rho 6 1.94 vs 1.84 ms single-CTA --
+// the kernel is bound by its MMA stream, not by the table traffic pairs halve.
+bool cg2_mode() {
+  const char* v = std::getenv("FC2T2_TC_CG2");
+  return v && v[0] == '1';
+}
+
 bool nomerge_mode() {
   const char* v = std::getenv("FC2T2_TC_NOMERGE");
   return v && v[0] == '1';
@@ -184,11 +193,17 @@ uint16_t half_rn(double v, double* val) {
 void build_tc_table(const std::vector<std::vector<int4>>& lists,
                     const std::vector<const double*>& slot_src, int P, int PP, int rho, int level,
                     bool f16, Plan& plan) {
-  int CLS, NC, KS, BSLOT, FL;
-  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, &CLS, &NC, &KS, &BSLOT, &FL) != 0) return;
+  int CLS, NC, KS, BSLOT, FL, TILES;
+  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, 1, &CLS, &NC, &KS, &BSLOT, &FL, &TILES) != 0) return;
+  // CTA pairs (cta_group::2) when the level fills at least two waves of CTAs
+  const int nu = (1 << (level + 1)) / 2;
+  const long ctas = (long)(nu / TILES) * (nu / 16) * (nu / 8) * (8 / CLS);
+  const int CG = (ctas >= 2 * 148 && cg2_mode() && (CLS * NC / 2) % 8 == 0) ? 2 : 1;
+  if (CG == 2) fc2t2::tc_geometry(rho, f16 ? 1 : 0, 2, &CLS, &NC, &KS, &BSLOT, &FL, &TILES);
+  plan.cg = CG;
   const bool SB = FL & 1, MERGE = (FL & 2) && !nomerge_mode();
   plan.merge_last = MERGE;
-  const int W = CLS * NC, R = 2 * W, NCG = 8 / CLS;
+  const int W = CLS * NC, R = CG == 2 ? 3 * W / 2 : 2 * W, NCG = 8 / CLS;
   const int KI = f16 ? 16 : 8, ESZ = f16 ? 2 : 4;
   std::vector<double> sn(P, 1.0);
   if (f16) fc2t2::tc_moment_scales(rho, level, sn.data());
@@ -213,7 +228,7 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
   }
   plan.rk.assign(NC, 1.f);
   for (int k = 0; k < NC; ++k) plan.rk[k] = (float)rk[k];
-  plan.tcb.assign((size_t)NCG * 8 * KS * 27 * BSLOT, 0);
+  plan.tcb.assign((size_t)NCG * 8 * KS * CG * 27 * BSLOT, 0);
   std::vector<double> A((size_t)P * P);
   for (int cg = 0; cg < NCG; ++cg)
     for (int sg = 0; sg < 8; ++sg) {
@@ -235,47 +250,67 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
             }
           if (!any) continue;
           const bool odd = (sg & 1) && !SB;   // single-buffered kernels keep [lo | hi]
-          const int hi_row = odd ? ci * NC : W + ci * NC;
-          const int lo_row = odd ? W + ci * NC : ci * NC;
-          for (int ks = 0; ks < KS; ++ks) {
-            uint8_t* st = plan.tcb.data() + ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * BSLOT;
-            // merged last step (TC::MERGE_LAST): chunk 1 multiplies the A_lo
-            // chunk of the same inputs -> rows [hi: 0 | lo: B_hi]
-            const bool merged = MERGE && ks == KS - 1;
-            for (int kc = 0; kc < 2; ++kc)
-              for (int k = 0; k < P; ++k)
-                for (int f = 0; f < KI / 2; ++f) {
-                  const int n = KI * ks + (merged ? 0 : (KI / 2) * kc) + f;
-                  if (n >= P) continue;
-                  const double a = A[(size_t)k * P + n];
-                  uint8_t* ph = st + ((size_t)kc * R + hi_row + k) * 16 + f * ESZ;
-                  uint8_t* pl = st + ((size_t)kc * R + lo_row + k) * 16 + f * ESZ;
-                  if (merged && kc == 1) {
+          // one CTA: rows [lo | hi] (even) or [hi | lo] (odd), 2W per slot.
+          // CTA pairs: rank 0 holds the first main half, rank 1 the second
+          // (W rows each), then each holds its half of the cross operand B_hi
+          // (W/2 rows); rows of another rank are skipped (-1).
+          const int f = ci * NC;                     // flattened (class, k) base
+          for (int ks = 0; ks < KS; ++ks)
+            for (int rk_ = 0; rk_ < CG; ++rk_) {
+              int hi_row, lo_row, x_lo = -1;         // x_lo: cross rows [x_lo, x_lo + W/2)
+              if (CG == 1) {
+                hi_row = odd ? f : W + f;
+                lo_row = odd ? W + f : f;
+              } else {
+                // main half: rank 0 = D cols [mcol, mcol + W) = lo (even) / hi (odd)
+                const bool lo_first = !odd;
+                hi_row = (lo_first ? (rk_ == 1) : (rk_ == 0)) ? f : -1;
+                lo_row = (lo_first ? (rk_ == 0) : (rk_ == 1)) ? f : -1;
+                x_lo = rk_ * (W / 2);
+              }
+              uint8_t* st = plan.tcb.data() +
+                            (((((size_t)cg * 8 + sg) * KS + ks) * CG + rk_) * 27 + slot) * BSLOT;
+              const bool merged = MERGE && ks == KS - 1;
+              for (int kc = 0; kc < 2; ++kc)
+                for (int k = 0; k < P; ++k)
+                  for (int fi = 0; fi < KI / 2; ++fi) {
+                    const int n = KI * ks + (merged ? 0 : (KI / 2) * kc) + fi;
+                    if (n >= P) continue;
+                    const double a = A[(size_t)k * P + n];
+                    double bh, bl, bhl;   // tf32: raw parts; f16: scaled parts
+                    uint8_t hb[4], lb[4], hb1[4];
                     if (f16) {
-                      double hv;
-                      const uint16_t hb = half_rn(a * sn[n] / rk[k], &hv);
-                      std::memcpy(pl, &hb, 2);
+                      const double b = a * sn[n] / rk[k];
+                      double hv, lv;
+                      const uint16_t h16 = half_rn(b, &hv);
+                      const uint16_t l16 = half_rn((b - hv) * 2048.0, &lv);
+                      std::memcpy(hb, &h16, 2);
+                      std::memcpy(lb, &l16, 2);
+                      std::memcpy(hb1, &h16, 2);
+                      (void)bh; (void)bl; (void)bhl;
                     } else {
                       const float hi = rn_tf32_host(a);
-                      std::memcpy(pl, &hi, 4);
+                      const float lo = rn_tf32_host(a - (double)hi);
+                      std::memcpy(hb, &hi, 4);
+                      std::memcpy(lb, &lo, 4);
+                      std::memcpy(hb1, &hi, 4);
                     }
-                    continue;   // hi rows stay zero
+                    auto put = [&](int row, const uint8_t* v) {
+                      std::memcpy(st + ((size_t)kc * R + row) * 16 + fi * ESZ, v, ESZ);
+                    };
+                    if (merged && kc == 1) {
+                      // chunk 1 multiplies the A_lo chunk: lo rows get B_hi, hi rows 0
+                      if (lo_row >= 0) put(lo_row + k, hb1);
+                      continue;
+                    }
+                    if (hi_row >= 0) put(hi_row + k, hb);
+                    if (lo_row >= 0) put(lo_row + k, lb);
+                    if (CG == 2 && !merged) {
+                      const int fk = f + k;           // flattened column of B_hi
+                      if (fk >= x_lo && fk < x_lo + W / 2) put(W + (fk - x_lo), hb);
+                    }
                   }
-                  if (f16) {
-                    const double b = a * sn[n] / rk[k];
-                    double hv, lv;
-                    const uint16_t hb = half_rn(b, &hv);
-                    const uint16_t lb = half_rn((b - hv) * 2048.0, &lv);
-                    std::memcpy(ph, &hb, 2);
-                    std::memcpy(pl, &lb, 2);
-                  } else {
-                    const float hi = rn_tf32_host(a);
-                    const float lo = rn_tf32_host(a - (double)hi);
-                    std::memcpy(ph, &hi, 4);
-                    std::memcpy(pl, &lo, 4);
-                  }
-                }
-          }
+            }
         }
       }
     }
@@ -363,6 +398,7 @@ fc2t2::TCPlan tc_of(const fc2t2_engine* e, const Plan& p, int level) {
   t.rk = p.d_rk;
   t.s_inv = p.d_sinv;
   t.merge_last = p.merge_last;
+  t.cg = p.cg;
   static const char* names[] = {"m2l_tc_L0", "m2l_tc_L1", "m2l_tc_L2", "m2l_tc_L3", "m2l_tc_L4",
                                 "m2l_tc_L5", "m2l_tc_L6", "m2l_tc_L7", "m2l_tc_L8", "m2l_tc_L9"};
   t.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];

@@ -63,11 +63,13 @@ struct TCPlan {
   const float* rk = nullptr;
   const float* s_inv = nullptr;
   bool merge_last = true;   // tables built with the merged last K step
+  int cg = 1;               // 2: CTA-pair tables and kernel (cta_group::2)
 };
 // classes per CTA, N per class, K steps, bytes per slot table, flags (bit 0:
 // single-buffered layout, B rows always [lo | hi]; bit 1: merged last K step,
 // see TC::MERGE_LAST); 0 on success
-int tc_geometry(int rho, int f16, int* cls, int* nc, int* ks, int* bslot, int* sb);
+int tc_geometry(int rho, int f16, int cg, int* cls, int* nc, int* ks, int* bslot, int* sb,
+                int* tiles);
 // tensor-core FLOPs one m2l_tc launch issues (2 M N K per MMA, padding and
 // split terms included) for a whole level
 double tc_issued_flops(int rho, int level, int C, int f16, int merge_last);

@@ -27,7 +27,8 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
 }
 
 template <int MODE, int W = 1>
-__global__ void __launch_bounds__(128, 1) mma_rate(int n, int iters, long long* out) {
+__global__ void __launch_bounds__(128, 1) mma_rate(int n, int iters, long long* out,
+                                                   int a_off = 0, int a_sbo = 128) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t bar;
@@ -47,8 +48,8 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int n, int iters, long long* 
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tslot;
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const uint64_t ad = sdesc(smem_u32(smem), 128 * 16, 128);
-  const uint64_t bd = sdesc(smem_u32(smem + 32768), 256 * 16, 128);
+  const uint64_t ad = sdesc(smem_u32(smem) + a_off, 128 * 16 * 2, a_sbo);
+  const uint64_t bd = sdesc(smem_u32(smem + 40000), 256 * 16, 128);
   const uint32_t stride = (uint32_t)((512 / 4) & ~7);
   if (MODE == 0 ? threadIdx.x == 0 : warp < W) {
     const uint32_t tm = tmem + (uint32_t)(warp * (512 / W));
@@ -169,21 +170,28 @@ void runp(long long* d) {
 }
 
 template <int MODE, int W = 1>
-void run(int n, long long* d) {
+void run(int n, long long* d, int a_off = 0, int a_sbo = 128) {
   long long h[148];
   const int iters = 4096;
-  cudaFuncSetAttribute(mma_rate<MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  for (int rep = 0; rep < 2; ++rep) mma_rate<MODE, W><<<148, 128, 64 * 1024>>>(n, iters, d);
+  cudaFuncSetAttribute(mma_rate<MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int rep = 0; rep < 2; ++rep) mma_rate<MODE, W><<<148, 128, 100 * 1024>>>(n, iters, d, a_off, a_sbo);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); fflush(stdout); return; }
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   double s = 0; for (int i = 0; i < 148; ++i) s += h[i];
-  printf("MMA mode=%d warps=%d N=%3d : %.1f cyc/mma total (floor %d)\n", MODE, W, n, s / 148 / iters / W, 128 * n / 256);
+  printf("MMA mode=%d warps=%d N=%3d a_off=%d a_sbo=%d : %.1f cyc/mma total (floor %d)\n", MODE, W, n, a_off, a_sbo, s / 148 / iters / W, 128 * n / 256);
   fflush(stdout);
 }
 
 int main() {
   long long* d; cudaMalloc(&d, 148 * sizeof(long long));
-  for (int n : {16, 48, 96}) { run<1, 1>(n, d); run<1, 2>(n, d); run<1, 4>(n, d); }
+  for (int n : {80, 160}) {
+    run<1, 1>(n, d, 0, 128);     // aligned, contiguous groups
+    run<1, 1>(n, d, 0, 256);     // aligned groups, 256 B stride
+    run<1, 1>(n, d, 0, 160);     // the window's 160 B group stride
+    run<1, 1>(n, d, 16, 160);    // + 16 B shift
+    run<1, 1>(n, d, 32, 160);
+    run<1, 1>(n, d, 16, 128);    // misaligned by 16 B, contiguous
+  }
   return 0;
 }
