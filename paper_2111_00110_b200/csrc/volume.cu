@@ -242,6 +242,9 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
   constexpr int NCS = 2 * RHO + 1;                                   // c * sigma
   constexpr int NQ = NCS + NS3 - 1;                                  // c sigma T'
   __shared__ float wn_s[VOL_THREADS][NCH * GN + 1];                  // node weights
+  // T at the nodes, once per segment, when it fits the 48 KB static limit
+  constexpr bool TN = (NCH * GN + 1 + GN) * 4 * VOL_THREADS <= 48 * 1024;
+  __shared__ float tn_s[TN ? GN : 1][VOL_THREADS];
   float* wn = wn_s[threadIdx.x];
   double e[5];
 #pragma unroll
@@ -286,6 +289,18 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
           Tp[k] = v;
         }
         const double half = 0.5 * s;
+        // T(x_g) = E(S(x_g) + depth0) once per node (shared by every channel
+        // and by the weight loop below)
+        if constexpr (TN) {
+#pragma unroll 1
+          for (int g = 0; g < GN; ++g)
+            tn_s[g][threadIdx.x] =
+                (float)efit_eval(e, (double)hornerf(S, (float)(half * (GL_X[g] + 1.0))) + depth);
+        }
+        auto t_at = [&](int g, float xf) -> double {
+          if constexpr (TN) return (double)tn_s[g][threadIdx.x];
+          else return efit_eval(e, (double)hornerf(S, xf) + depth);
+        };
         // node weights: channel 0 accumulates h_sigma, colours y_c T sigma
         float hs_const = 0.f;
 #pragma unroll
@@ -311,7 +326,7 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
               cp = (double)aq;
               break;
             }
-            const double T = efit_eval(e, (double)hornerf(S, xf) + depth);
+            const double T = t_at(g, xf);
             wn[g] += (float)(yb[c] * (T * (double)hornerf(col, xf) - (double)aq));
           }
           before[c] += cp;
@@ -321,7 +336,7 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
           const double x = half * (GL_X[g] + 1.0);
           const float xf = (float)x;
           const double W = half * GL_W[g];
-          const double T = efit_eval(e, (double)hornerf(S, xf) + depth);
+          const double T = t_at(g, xf);
           wn[g] = (float)(W * ((double)wn[g] + (double)hs_const));
           const double ts = W * T * (double)hornerf(sg, xf);
 #pragma unroll
