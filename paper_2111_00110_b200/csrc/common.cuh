@@ -109,6 +109,18 @@ __device__ __forceinline__ bool outside_domain(float x, float y, float z) {
   return !(fabsf(x) < 1.0f && fabsf(y) < 1.0f && fabsf(z) < 1.0f);
 }
 
+// Function attributes are per device: `mask` (one per kernel instantiation)
+// records the devices already configured, so a launch path sets them once per
+// device and issues nothing but launches afterwards (CUDA-graph capture).
+inline bool attr_needed(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 inline int grid_blocks(int64_t n, int threads, int cap = 148 * 32) {
   int64_t b = (n + threads - 1) / threads;
   if (b < 1) b = 1;

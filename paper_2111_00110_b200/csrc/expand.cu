@@ -402,12 +402,11 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
     const int64_t ntgt = (int64_t)nu * nu * nu;
     const size_t smem = m2l_smem<RHO>();
     auto kern = m2l_ffma_kernel<RHO, RPL>;
-    static bool attr = false;   // once per instantiation (nothing but launches in graph capture)
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices configured (per instantiation)
+    if (attr_needed(attr)) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
       if (e != cudaSuccess) return e;
-      attr = true;
     }
     dim3 grid((unsigned)((ntgt + tpt - 1) / tpt), (unsigned)plan.ncls, (unsigned)splits);
     FC2T2_LAUNCH(plan.level_name, s,

@@ -805,8 +805,8 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
     using T = typename decltype(tag)::type;
     constexpr bool H = T::ESZ == 2;
     auto kern = m2l_tc_kernel<T::RHO_, H, T::TL_, T::CG_>;
-    static bool attr = false;   // once per instantiation (nothing but launches in graph capture)
-    if (!attr) {
+    static unsigned long long attr = 0;   // devices configured (per instantiation)
+    if (attr_needed(attr)) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)T::SMEM);
       if (e != cudaSuccess) return e;
@@ -814,7 +814,6 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         if (e != cudaSuccess) return e;
       }
-      attr = true;
     }
     const uint8_t* hi = w + gbits_bytes(C);
     const uint8_t* lo = hi + plane_bytes<T::RHO_, H>(plan.level, C);

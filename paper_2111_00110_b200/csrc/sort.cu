@@ -461,12 +461,11 @@ cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t
                  segment_sort_warp_kernel<false><<<grid_blocks(nseg * 32, 256), 256, 0, s>>>(
                      ord, (const uint32_t*)cell_start, nseg, R, n, w.work, nullptr, nullptr,
                      nullptr));
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;   // devices configured
+  if (attr_needed(attr)) {
     e = cudaFuncSetAttribute(segment_sort_block_kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, BLOCK_SEG_MAX * 4);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   FC2T2_LAUNCH("sort_segments", s,
                segment_sort_block_kernel<<<148, SEG_BLOCK, BLOCK_SEG_MAX * 4, s>>>(

@@ -226,8 +226,90 @@ vol_totals_kernel(const float* __restrict__ L, int res, const double* __restrict
 // T(u) = E(S(u) + depth0), T' = E'(S(u) + depth0).  int_0^u c sigma T' is a
 // degree-(3(rho+1) + 2 rho + 1) polynomial built in float32 from
 // E'_shift(y) = E'(y + depth0) (shift in float64) composed with S.
+// Moments of NCH node-weighted point sets on one segment line p(x) = base +
+// x dir: pay[ch][n] = sum_g wn[ch][g] mono_n(p(x_g)).  Each monomial is a
+// polynomial in x, mono_n(p(x)) = inv_fact[n] prod_a (base_a + x dir_a)^{n_a}
+// = sum_i c_{n,i} x^i (|n| <= RHO), so pay[ch][n] = sum_i c_{n,i} mu[ch][i] with
+// the power moments mu[ch][i] = sum_g wn[ch][g] x_g^i: ~1.5k instead of ~3.6k
+// FMAs per segment at rho 4 (same absolute rounding scale).  Rows go to
+// dst[ch * PP .. ] as float4.
+template <int RHO, int NCH, int GNODES>
+__device__ __forceinline__ void segment_moments(const float base[3], const float dirf[3],
+                                                const float (&xs)[GNODES], const float* wn,
+                                                float* __restrict__ dst) {
+  constexpr MI<RHO> mi{};
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  float mu[NCH][RHO + 1];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+    for (int i = 0; i <= RHO; ++i) mu[ch][i] = 0.f;
+#pragma unroll 1
+  for (int g = 0; g < GNODES; ++g) {
+    const float x = xs[g];
+    float w[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) w[ch] = wn[ch * GNODES + g];
+#pragma unroll
+    for (int i = 0; i <= RHO; ++i) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) mu[ch][i] += w[ch];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) w[ch] *= x;
+    }
+  }
+  // per-axis binomial polynomials Q[a][k][i] = coefficient of x^i in (b + x d)^k
+  float Q[3][RHO + 1][RHO + 1];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    Q[a][0][0] = 1.f;
+#pragma unroll
+    for (int k = 1; k <= RHO; ++k)
+#pragma unroll
+      for (int i = 0; i <= k; ++i)
+        Q[a][k][i] = (i < k ? Q[a][k - 1][i] * base[a] : 0.f) +
+                     (i > 0 ? Q[a][k - 1][i - 1] * dirf[a] : 0.f);
+  }
+  float out[NCH][4];
+#pragma unroll
+  for (int n = 0; n < PP; ++n) {
+    if (n < P) {
+      const int n0 = mi.e0[n], n1 = mi.e1[n], n2 = mi.e2[n];
+      float c01[RHO + 1], c[RHO + 1];
+#pragma unroll
+      for (int i = 0; i <= RHO; ++i) c01[i] = c[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i <= RHO; ++i)
+#pragma unroll
+        for (int j = 0; j <= RHO; ++j)
+          if (i <= n0 && j <= n1) c01[i + j] = fmaf(Q[0][n0][i], Q[1][n1][j], c01[i + j]);
+#pragma unroll
+      for (int i = 0; i <= RHO; ++i)
+#pragma unroll
+        for (int j = 0; j <= RHO; ++j)
+          if (i <= n0 + n1 && j <= n2 && i + j <= RHO) c[i + j] = fmaf(c01[i], Q[2][n2][j], c[i + j]);
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        float v = 0.f;
+#pragma unroll
+        for (int i = 0; i <= RHO; ++i)
+          if (i <= n0 + n1 + n2) v = fmaf(c[i], mu[ch][i], v);
+        out[ch][n & 3] = v * mi.inv_fact[n];
+      }
+    } else {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) out[ch][n & 3] = 0.f;
+    }
+    if ((n & 3) == 3) {
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch)
+        *reinterpret_cast<float4*>(dst + ch * PP + (n - 3)) =
+            make_float4(out[ch][0], out[ch][1], out[ch][2], out[ch][3]);
+    }
+  }
+}
+
 constexpr int VOL_THREADS = 128;
-constexpr int VOL_CH = 2;   // payload channels accumulated per pass over the nodes
 
 template <int RHO, int CC>
 __global__ void __launch_bounds__(VOL_THREADS, 3)
@@ -342,41 +424,11 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
 #pragma unroll
           for (int c = 0; c < CC; ++c) wn[(1 + c) * GN + g] = (float)(yb[c] * ts);
         }
-        // moments of the NCH node-weighted point sets, VOL_CH channels per
-        // pass over the nodes (monomials recomputed per pass: bounds the
-        // live accumulators to VOL_CH * P registers)
         keys[item] = ((uint32_t)b0 * res + b1) * res + b2;
-#pragma unroll 1
-        for (int ch0 = 0; ch0 < NCH; ch0 += VOL_CH) {
-          float pay[VOL_CH][P];
+        float xs[GN];
 #pragma unroll
-          for (int ch = 0; ch < VOL_CH; ++ch)
-#pragma unroll
-            for (int k = 0; k < P; ++k) pay[ch][k] = 0.f;
-#pragma unroll 1
-          for (int g = 0; g < GN; ++g) {
-            const float xf = (float)(half * (GL_X[g] + 1.0));
-            float mono[P];
-            monomials<RHO>(fmaf(xf, dirf[0], base[0]), fmaf(xf, dirf[1], base[1]),
-                           fmaf(xf, dirf[2], base[2]), mono);
-#pragma unroll
-            for (int ch = 0; ch < VOL_CH; ++ch) {
-              const float wt = ch0 + ch < NCH ? wn[(ch0 + ch) * GN + g] : 0.f;
-#pragma unroll
-              for (int k = 0; k < P; ++k) pay[ch][k] = fmaf(wt, mono[k], pay[ch][k]);
-            }
-          }
-#pragma unroll
-          for (int ch = 0; ch < VOL_CH; ++ch) {
-            if (ch0 + ch >= NCH) break;
-            float* dst = payload + (item * NCH + ch0 + ch) * PP;
-#pragma unroll
-            for (int k = 0; k < PP; k += 4)
-              *reinterpret_cast<float4*>(dst + k) = make_float4(
-                  k < P ? pay[ch][k] : 0.f, k + 1 < P ? pay[ch][k + 1] : 0.f,
-                  k + 2 < P ? pay[ch][k + 2] : 0.f, k + 3 < P ? pay[ch][k + 3] : 0.f);
-          }
-        }
+        for (int g = 0; g < GN; ++g) xs[g] = (float)(half * (GL_X[g] + 1.0));
+        segment_moments<RHO, NCH, GN>(base, dirf, xs, wn, payload + item * NCH * PP);
         ++item;
       }
       depth += send;
