@@ -26,6 +26,3 @@ def t(fn, n=3):
 for name, od in (("natural", None), ("sorted", order)):
     print("L2P", lvl, rho, M, name, "value", t(lambda: acc.eval_device(q, _lib.L2P_VALUE, order=od)),
           "wgrad", t(lambda: acc.eval_device(q, _lib.L2P_WGRAD, wts=y, order=od)), flush=True)
-for mb in (32, 64, 96):
-    print("L2P", lvl, rho, M, f"slabs{mb}MB", "value", t(lambda: acc.eval_slabs(q, _lib.L2P_VALUE, slab_bytes=mb << 20)),
-          "wgrad", t(lambda: acc.eval_slabs(q, _lib.L2P_WGRAD, wts=y, slab_bytes=mb << 20)), flush=True)
