@@ -1,6 +1,7 @@
 """torch.autograd wrappers of the layers (optional
 ``torch.autograd.Function`` entry points for explicit(q, p, w),
-depth + normal(p, w, bias, rays) and radiance(p, w_sigma, w_colour, rays, bg)).
+depth + normal(p, w, bias, rays) and radiance(p, w_sigma, w_colour, rays, bg);
+plus the line integral).
 
 Each backward is the layer's own JVP -- one insertion and one expansion, the
 self-adjoint pipeline of the reference (layers.py:1-22) -- so gradients equal
@@ -14,7 +15,7 @@ import torch
 
 from .expansion import Engine, SourceSet
 from .layers import (depth_forward, depth_surface_jvp, explicit_forward, explicit_jvp,
-                     volumetric_forward, volumetric_jvp)
+                     line_integral_forward, line_integral_jvp, volumetric_forward, volumetric_jvp)
 from .ray import RayBundle
 
 
@@ -84,3 +85,24 @@ def radiance(engine: Engine, p: torch.Tensor, w_sigma: torch.Tensor, w_color: to
     with gradients to p, the density and the colour weights (volumetric_jvp,
     layers.py:483-544)."""
     return _Radiance.apply(engine, p, w_sigma, w_color, origins, directions, background)
+
+
+class _LineIntegral(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, engine: Engine, p, w, origins, directions):
+        res = line_integral_forward(engine, SourceSet(p.detach(), w.detach()),
+                                    RayBundle(origins.detach(), directions.detach()))
+        ctx.res, ctx.w_shape = res, w.shape
+        return res.values
+
+    @staticmethod
+    def backward(ctx, y_bar):
+        g = line_integral_jvp(y_bar.contiguous(), ctx.res)
+        return None, g.p_bar, g.w_bar.reshape(ctx.w_shape), None, None
+
+
+def line_integral(engine: Engine, p: torch.Tensor, w: torch.Tensor, origins: torch.Tensor,
+                  directions: torch.Tensor) -> torch.Tensor:
+    """Integral of the field along each ray through the domain (reference
+    line_integral_forward / _jvp, layers.py:371-402) with gradients to p, w."""
+    return _LineIntegral.apply(engine, p, w, origins, directions)

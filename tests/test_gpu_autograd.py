@@ -98,3 +98,18 @@ def test_radiance_autograd_equals_jvp_and_reference():
     assert torch.equal(ws.grad, jv.w_bar[:, :1]) and torch.equal(wc.grad, jv.w_bar[:, 1:])
     assert rel_l2(torch.cat([ws.grad, wc.grad], 1).cpu().numpy(), g["vol_w_bar"]) < 1e-5
     assert rel_l2(p.grad.cpu().numpy(), g["vol_p_bar"]) < 1e-5
+
+
+def test_line_integral_autograd_matches_reference():
+    from paper_2111_00110_b200 import Engine, KernelModel
+    from paper_2111_00110_b200.autograd import line_integral
+    g = golden("rays_small")
+    eng = Engine(KernelModel("gaussian", 50.0, 4), 3, check_admissibility=False)
+    p, w = _t(g["p"], True), _t(g["w"], True)
+    org = torch.tensor(g["origins"], dtype=torch.float64, device="cuda")
+    dirs = torch.tensor(g["directions"], dtype=torch.float64, device="cuda")
+    v = line_integral(eng, p, w, org, dirs)
+    assert rel_l2(v.detach().cpu().numpy(), g["li_values"]) < 1e-5
+    (v * _t(g["y_li"])).sum().backward()
+    assert rel_l2(w.grad.cpu().numpy(), g["li_w_bar"]) < 1e-5
+    assert rel_l2(p.grad.cpu().numpy(), g["li_p_bar"]) < 1e-5
