@@ -2,8 +2,10 @@
 
 Same names and semantics as the reference (trainer.py:1-152): TrainConfig,
 init_params, loss_and_tangent, l1_term and Optimizer (SGD / Adam over
-(w, p, bias) with domain clipping of p), plus ``fit_sdf_epoch`` = one epoch of
-the reference's fit-sdf loop (cli.py:129-145).  Tensors stay on the GPU: the
+(w, p, bias) with domain clipping of p), plus the loop bodies of the
+reference CLI's fitting commands: ``fit_sdf_epoch`` (cli.py:129-145),
+``cgls_sdf`` (the CGLS solver, cli.py:173-224), ``fit_depth_epoch``
+(cli.py:288-306) and ``fit_radiance_epoch`` (cli.py:363-382).  Tensors stay on the GPU: the
 loss and its tangent come from one fused CUDA pass (train.cu, deterministic
 float64 reductions), each parameter step is one fused kernel (gradient + L1
 subgradient, Adam moments, clipping), and the non-finite check is a device
@@ -23,7 +25,8 @@ import torch
 
 from . import _lib
 from .expansion import Engine, SourceSet, _device, _ptr, _stream, to_device
-from .layers import explicit_forward, explicit_jvp
+from .layers import (_l2p, depth_forward, depth_jvp, explicit_forward, explicit_jvp,
+                     volumetric_forward, volumetric_jvp)
 
 DOMAIN_MARGIN = 1e-6  # sources are clipped back to (-1+eps, 1-eps)
 
@@ -204,3 +207,100 @@ def fit_sdf_epoch(engine: Engine, sources: SourceSet, bias: float, q, target,
     sources, bias = opt.step(sources, g.w_bar, g.p_bar, epoch, bias=bias,
                              bias_bar=float(st[2]), l1_weight=tc.l1_weight)
     return sources, bias, float(st[1]) + reg, float(st[1])
+
+
+def cgls_sdf(engine: Engine, p, q, target, iterations: int) -> dict:
+    """Conjugate-gradient least squares on the (w, bias) sub-problem of fit-sdf
+    (reference cli.py:173-224): positions stay fixed, each iteration is one
+    forward product (expand the sources, evaluate at the samples) and one
+    adjoint product (expand the residual at the samples, evaluate at the
+    sources).  The CG vectors and scalars are float64 device tensors; the
+    products run through the fp32 engine.  The cell sorts of p and q are made
+    once and reused by every product; nothing is read back until the end.
+
+    Returns {"w": (N, 1), "bias": float, "mae": [per iteration], "final_mae"}.
+    """
+    pd = to_device(p, 3, points=True)
+    qd = to_device(q, 3, points=True)
+    d = to_device(target).reshape(-1).double()
+    p_sort, q_sort = engine.sort_points(pd), engine.sort_points(qd)
+    value = _lib.L2P_VALUE
+
+    def a_fwd(w, b):
+        acc = engine.expand_device(pd, w.float().reshape(-1, 1).contiguous(), p_sort)
+        return _l2p(acc, qd, value, q_sort)["value"].reshape(-1).double() + b
+
+    def a_adj(r):
+        acc = engine.expand_device(qd, r.float().reshape(-1, 1).contiguous(), q_sort)
+        return _l2p(acc, pd, value, p_sort)["value"].reshape(-1).double(), r.sum()
+
+    with engine.flag.deferred():
+        w = torch.zeros(pd.shape[0], dtype=torch.float64, device=pd.device)
+        bias = torch.zeros((), dtype=torch.float64, device=pd.device)
+        r = d - a_fwd(w, bias)
+        s_w, s_b = a_adj(r)
+        pk_w, pk_b = s_w.clone(), s_b.clone()
+        gamma = s_w @ s_w + s_b * s_b
+        maes = []
+        for _ in range(iterations):
+            qk = a_fwd(pk_w, pk_b)
+            alpha = gamma / (qk @ qk)
+            w += alpha * pk_w
+            bias += alpha * pk_b
+            r -= alpha * qk
+            s_w, s_b = a_adj(r)
+            gamma_new = s_w @ s_w + s_b * s_b
+            beta = gamma_new / gamma
+            pk_w = s_w + beta * pk_w
+            pk_b = s_b + beta * pk_b
+            gamma = gamma_new
+            maes.append(r.abs().mean())
+        final = (a_fwd(w, bias) - d).abs().mean()
+    engine.flag.raise_if_set("source/query")
+    host = torch.stack(maes + [final, bias]).cpu().numpy() if maes else \
+        torch.stack([final, bias]).cpu().numpy()
+    return {"w": w.float().reshape(-1, 1), "bias": float(host[-1]),
+            "mae": [float(v) for v in host[:-2]], "final_mae": float(host[-2])}
+
+
+def fit_depth_epoch(engine: Engine, sources: SourceSet, bias: float, bundle, target,
+                    opt: Optimizer, epoch: int, miss_penalty: float = 0.1):
+    """One epoch of the reference fit-depth loop (cli.py:288-306): depth layer,
+    masked loss over rays that hit and have a finite target, JVP, L1, step;
+    the bias is pushed by miss_penalty * miss fraction.  ``target`` holds NaN
+    where there is no valid depth.  Returns (sources, bias, loss, miss_fraction)."""
+    tc = opt.config
+    res = depth_forward(engine, sources, bundle, bias=bias)
+    tgt = to_device(target).reshape(-1)
+    valid = torch.isfinite(tgt)
+    mask = res.dev["hit"].bool() & valid
+    lengths = res.lengths if isinstance(res.lengths, torch.Tensor) else to_device(res.lengths)
+    pred = torch.where(mask, lengths.to(torch.float32), 0.0)
+    tg = torch.where(mask, tgt.to(torch.float32), 0.0)
+    stats, tangent = _loss_device(pred, tg, tc.loss, mask=mask)
+    g = depth_jvp(tangent.reshape(-1), res)
+    miss = (~mask).sum()
+    host = torch.cat([stats, miss.double().reshape(1)]).cpu().numpy()
+    miss_frac = float(host[3]) / mask.numel()
+    sources, bias = opt.step(sources, g.w_bar, g.p_bar, epoch, bias=bias,
+                             bias_bar=miss_penalty * miss_frac, l1_weight=tc.l1_weight)
+    return sources, bias, float(host[1]), miss_frac
+
+
+def fit_radiance_epoch(engine: Engine, p, w_sigma, w_color, bundle, target, background,
+                       opt: Optimizer, epoch: int):
+    """One epoch of the reference fit-radiance loop (cli.py:363-382) on one
+    minibatch of rays: volumetric forward, loss + tangent of rgb (fused),
+    volumetric JVP, L1 on the packed weights, one step over (p, [w_sigma |
+    w_color]).  The minibatch draw stays the caller's (the reference draws it
+    on the host).  Returns (p, w_sigma, w_color, loss)."""
+    tc = opt.config
+    res = volumetric_forward(engine, p, w_sigma, w_color, bundle, background)
+    rgb = res.rgb if isinstance(res.rgb, torch.Tensor) else to_device(res.rgb)
+    stats, tangent = _loss_device(rgb, target, tc.loss)
+    g = volumetric_jvp(tangent.reshape(rgb.shape), res)
+    ws, wc = to_device(w_sigma), to_device(w_color)
+    packed = SourceSet(to_device(p, 3, points=True),
+                       torch.cat([ws.reshape(ws.shape[0], -1), wc.reshape(wc.shape[0], -1)], 1))
+    packed, _ = opt.step(packed, g.w_bar, g.p_bar, epoch, l1_weight=tc.l1_weight)
+    return packed.p, packed.w[:, :1], packed.w[:, 1:], float(stats[1].item())
