@@ -79,6 +79,20 @@ void fc2t2_engine_destroy(fc2t2_engine* e);
 int fc2t2_engine_set_table(fc2t2_engine* e, int level, int nearfield, int64_t n_offsets,
                            const int64_t* offsets, const uint8_t* active,
                            const double* coeffs);
+/* On-device table fitting (replaces _build_offset_matrices / the LSQ fit of
+ * kernel.py:180-204).  For `count` offsets (d_offsets (count,3)
+ * int32, source - target) at one level: coeffs[o] = (pinv(V) Psi(o)
+ * pinv(V)^T)^T as (count, P, P) float64 [k_local][n_moment], and d_resid[o] =
+ * max |V A V^T - Psi(o)| (kernel.py:202).  d_pinv (P, nodes^3) and d_v
+ * (nodes^3, P) float64 are pinv(V) and V over the nodes^3 Chebyshev grid with
+ * per-axis coordinates d_nodes (nodes,) (already scaled by width/2); only
+ * nodes == 6 (the reference default) is supported.  All pointers are device
+ * memory; stream-ordered, no host sync.  EVALUE for bad sizes. */
+int fc2t2_fit_tables(int rho, int nodes, const double* d_pinv, const double* d_v,
+                     const double* d_nodes, double alpha, double width, const int32_t* d_offsets,
+                     int64_t count, double* d_coeffs, double* d_resid, void* stream);
+/* dynamic shared memory one fit CTA uses (bytes) */
+size_t fc2t2_fit_tables_smem(int rho);
 /* Build the per-parity interaction lists and upload fp32 tables (once). */
 int fc2t2_engine_upload(fc2t2_engine* e, void* stream);
 /* number of (level, class) interaction-list entries, for diagnostics */

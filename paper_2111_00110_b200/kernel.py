@@ -22,6 +22,12 @@ vectors generated from the reference).
   two-sided product is evaluated one axis at a time instead of forming the
   216 x 216 pair matrix.
 
+On a GPU the LSQ fit itself runs on the device (``_lsq_tables_device`` ->
+``fc2t2_fit_tables``, csrc/tables.cu: one CTA per offset, float64, SURVEY
+8(f)3); only pinv(V) -- one small SVD per level -- stays on the host.
+``FC2T2_HOST_TABLES=1`` (or a machine without CUDA) selects the numpy fit
+above, which the same golden tests pin.
+
 Everything here runs once per Engine.  The device copy (fp32, padded, grouped
 into per-parity interaction lists) is made by ``expansion.Engine``.
 """
@@ -180,6 +186,45 @@ def _lsq_tables(kernel: KernelModel, width: float, offsets: np.ndarray,
     return out, resid
 
 
+def _lsq_tables_device(kernel: KernelModel, width: float, offsets: np.ndarray,
+                       nodes: int) -> tuple[np.ndarray, float]:
+    """_lsq_tables on the device (csrc/tables.cu): same float64 arithmetic per
+    offset, summed in a different order (agrees to ~1e-13 relative)."""
+    import torch
+
+    from . import _lib
+    t = kernel.table
+    P, G = t.size, nodes
+    x1 = _cheb(G) * (width / 2.0)
+    grid = np.stack(np.meshgrid(x1, x1, x1, indexing="ij"), axis=-1).reshape(-1, 3)
+    V = monomial_rows(t, grid)                                  # (G^3, P)
+    Pv = np.linalg.pinv(V)                                      # (P, G^3)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_pv = torch.from_numpy(np.ascontiguousarray(Pv)).to(dev)
+    d_v = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
+    d_x = torch.from_numpy(x1).to(dev)
+    d_off = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int32)).to(dev)
+    K = int(offsets.shape[0])
+    d_c = torch.empty((K, P, P), dtype=torch.float64, device=dev)
+    d_r = torch.empty(max(K, 1), dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    _lib.call("fc2t2_fit_tables", t.rho, G, d_pv.data_ptr(), d_v.data_ptr(), d_x.data_ptr(),
+              float(kernel.alpha), float(width), d_off.data_ptr(), K, d_c.data_ptr(),
+              d_r.data_ptr(), s)
+    return d_c.cpu().numpy(), float(d_r[:K].max().item()) if K else 0.0
+
+
+def _device_fit_available(nodes: int) -> bool:
+    import os
+    if os.environ.get("FC2T2_HOST_TABLES", "0") == "1" or nodes != 6:
+        return False
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except ImportError:
+        return False
+
+
 def _taylor_tables(kernel: KernelModel, width: float, offsets: np.ndarray) -> np.ndarray:
     """Pure Taylor re-expansion (reference kernel.py:168-178): entry [k, n] is
     (-1)^|k| d^(k+n) psi(off * width), kept only where k_a + n_a <= rho."""
@@ -228,8 +273,13 @@ def _check_admissibility(kernel, table: M2LTable, tol: float, rng) -> None:
 
 def fit_m2l_tables(kernel: KernelModel, levels: int, lsq: bool = True,
                    nodes_per_axis: int = 6, admissibility_tol: float = 1e-3,
-                   check: bool = True, prune_tol: float = PRUNE_TOL) -> dict:
-    """``{"far": {level: M2LTable}, "near": M2LTable}`` (reference kernel.py:257-300)."""
+                   check: bool = True, prune_tol: float = PRUNE_TOL,
+                   device: bool | None = None) -> dict:
+    """``{"far": {level: M2LTable}, "near": M2LTable}`` (reference kernel.py:257-300).
+    ``device`` (default: when a GPU is present) fits the LSQ tables on it."""
+    if device is None:
+        device = lsq and _device_fit_available(nodes_per_axis)
+    lsq_fit = _lsq_tables_device if device else _lsq_tables
     if levels < COARSEST_LEVEL:
         raise KernelConfigError(f"levels must be >= {COARSEST_LEVEL}")
     rng = np.random.default_rng(0)
@@ -242,8 +292,8 @@ def fit_m2l_tables(kernel: KernelModel, levels: int, lsq: bool = True,
         resid = 0.0
         if active.any():
             if lsq:
-                coeffs[active], resid = _lsq_tables(kernel, width, offsets[active],
-                                                    nodes_per_axis)
+                coeffs[active], resid = lsq_fit(kernel, width, offsets[active],
+                                                nodes_per_axis)
             else:
                 coeffs[active] = _taylor_tables(kernel, width, offsets[active])
         return M2LTable(level, nearfield, offsets, coeffs, hole, active, resid, width)
