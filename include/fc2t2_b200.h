@@ -93,6 +93,16 @@ int fc2t2_fit_tables(int rho, int nodes, const double* d_pinv, const double* d_v
                      int64_t count, double* d_coeffs, double* d_resid, void* stream);
 /* dynamic shared memory one fit CTA uses (bytes) */
 size_t fc2t2_fit_tables_smem(int rho);
+/* ---- data formats: dataio.py ----
+ * Interleaved float64 rows (x, y, z, v1..vC) of an FCPT payload
+ * (dataio.py:99-104) or a checkpoint's p block (C = 0) -> float32 columns
+ * d_p (m, 3) and d_v (m, C), one coalesced pass.  With d_first_bad (one
+ * uint64, caller-initialised to UINT64_MAX) the smallest row index with a
+ * coordinate outside (-1, 1) (or NaN) is recorded: the point PointSampleSet
+ * rejects (dataio.py:49-51). */
+int fc2t2_unpack_rows(const double* d_rows, int64_t m, int c, float* d_p, float* d_v,
+                      uint64_t* d_first_bad, void* stream);
+
 /* Build the per-parity interaction lists and upload fp32 tables (once). */
 int fc2t2_engine_upload(fc2t2_engine* e, void* stream);
 /* number of (level, class) interaction-list entries, for diagnostics */

@@ -35,6 +35,7 @@ _SIGS = {
     "fc2t2_fit_tables": (_i32, [_i32, _i32, _vp, _vp, _vp, ct.c_double, ct.c_double, _vp, _i64,
                                 _vp, _vp, _vp]),
     "fc2t2_fit_tables_smem": (_sz, [_i32]),
+    "fc2t2_unpack_rows": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "fc2t2_engine_list_entries": (_i64, [_vp, _i32, _i32]),
     "fc2t2_engine_get_list": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "fc2t2_find_box": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp]),

@@ -339,6 +339,58 @@ def depth_surface_jvp(y_len, y_grad, res: RootResult) -> LayerGradients:
     return _root_jvp(res, y_len, y_grad)
 
 
+@dataclass
+class RGBDResult:
+    """RGBD composition: depth = first root of the SDF field,
+    rgb = colour field at the hit point (0 where the ray misses)."""
+
+    depth: object
+    hit: object
+    rgb: object
+    root: RootResult
+    color: ExplicitResult
+
+
+def rgbd_forward(engine: Engine, sdf: SourceSet, color: SourceSet, bundle: RayBundle,
+                 bias: float = 0.05) -> RGBDResult:
+    """Composed, not bespoke: depth_forward supplies the roots and
+    explicit_forward evaluates the colour channels at the hit points.  Missed
+    rays query the domain centre and are masked, so no compaction (and no
+    extra host sync) is needed."""
+    root = depth_forward(engine, sdf, bundle, bias=bias)
+    hit = root.dev["hit"].bool()
+    q = torch.where(hit[:, None], root.dev["points"], 0.0).to(torch.float32).contiguous()
+    col = explicit_forward(engine, color, q)
+    rgb = torch.where(hit[:, None], col.values, 0.0)
+    lengths = root.lengths if isinstance(root.lengths, torch.Tensor) else to_device(root.lengths)
+    depth = torch.where(hit, lengths.to(torch.float64), 0.0)
+    ref = bundle.origins
+    return RGBDResult(depth=_like(depth, ref), hit=_like(hit, ref), rgb=_like(rgb, ref), root=root,
+                      color=col)
+
+
+def rgbd_jvp(y_depth, y_rgb, res: RGBDResult) -> tuple[LayerGradients, LayerGradients]:
+    """(SDF-source gradients, colour-source gradients).  The colour layer's
+    JVP also yields q_bar at the hit point x = o + t r, which moves the root:
+    dL/dt += q_bar . r, so the depth tangent handed to depth_jvp is
+    y_depth + q_bar . r on hit rays -- two insertions, two expansions."""
+    hit = res.root.dev["hit"].bool()
+    R = hit.shape[0]
+    C = int(res.color.values.shape[1])
+    yr = torch.where(hit[:, None], to_device(y_rgb).reshape(R, C), 0.0)
+    gc = explicit_jvp(yr.contiguous(), res.color)
+    q_bar = gc.q_bar if isinstance(gc.q_bar, torch.Tensor) else to_device(gc.q_bar)
+    _, dirs = res.root.bundle.dev()
+    dt = (q_bar.to(torch.float64) * dirs).sum(1)
+    yd = _tangent(y_depth, R, 1).reshape(R).to(torch.float64) if y_depth is not None else 0.0
+    tangent = torch.where(hit, yd + dt, 0.0).to(torch.float32).contiguous()
+    gd = _root_jvp(res.root, tangent, None)
+    ref = y_rgb
+    for g in (gc, gd):
+        g.w_bar, g.p_bar = _like(to_device(g.w_bar), ref), _like(to_device(g.p_bar), ref)
+    return gd, gc
+
+
 # -------------------------------------------------------- integral layers ---
 
 @dataclass
