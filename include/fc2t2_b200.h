@@ -103,6 +103,12 @@ size_t fc2t2_fit_tables_smem(int rho);
 int fc2t2_unpack_rows(const double* d_rows, int64_t m, int c, float* d_p, float* d_v,
                       uint64_t* d_first_bad, void* stream);
 
+/* Sets FLAG_DOMAIN in *d_flag if any coordinate of d_pts (n, 3) float32
+ * (16-byte aligned) is not strictly inside (-1, 1) -- the check of
+ * Accessor._local / SourceSet (expansion.py:45-46, :337-338) as a
+ * stand-alone read, so a layer can test its inputs early. */
+int fc2t2_domain_check(const float* d_pts, int64_t n, int32_t* d_flag, void* stream);
+
 /* Build the per-parity interaction lists and upload fp32 tables (once). */
 int fc2t2_engine_upload(fc2t2_engine* e, void* stream);
 /* number of (level, class) interaction-list entries, for diagnostics */

@@ -36,6 +36,7 @@ _SIGS = {
                                 _vp, _vp, _vp]),
     "fc2t2_fit_tables_smem": (_sz, [_i32]),
     "fc2t2_unpack_rows": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "fc2t2_domain_check": (_i32, [_vp, _i64, _vp, _vp]),
     "fc2t2_engine_list_entries": (_i64, [_vp, _i32, _i32]),
     "fc2t2_engine_get_list": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "fc2t2_find_box": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp]),

@@ -184,12 +184,22 @@ def _host_domain_check(a, what: str) -> None:
 
 class DomainFlag:
     """Device int32 accumulating FLAG_* bits; read once per public call.
-    ``deferred()`` suspends the read (CUDA-graph capture: a host sync cannot
-    be captured; graphs.py checks the flag once after each replay)."""
+
+    A layer whose inputs are checked by early kernels calls ``mark()`` right
+    after them; ``raise_if_set`` then copies the flag on a side stream that
+    waits only for that point, so the main stream is not drained (its later
+    kernels keep running while the host decides).  Without a mark the read is
+    stream-ordered after everything enqueued.  ``deferred()`` suspends the
+    read (CUDA-graph capture: a host sync cannot be captured; graphs.py checks
+    the flag once after each replay)."""
 
     def __init__(self):
         self.t = torch.zeros(1, dtype=torch.int32, device=_device())
         self._defer = 0
+        self._host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._side = None
+        self._mark = None
+        self._done = None
 
     class _Deferred:
         def __init__(self, flag):
@@ -204,13 +214,39 @@ class DomainFlag:
     def deferred(self):
         return DomainFlag._Deferred(self)
 
-    def raise_if_set(self, what: str) -> None:
+    def mark(self):
+        """Every kernel that checks this call's inputs has been enqueued;
+        returns the token the same call passes to ``raise_if_set``."""
+        if self._defer:
+            return None
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.t.device)
+            self._mark = torch.cuda.Event()
+            self._done = torch.cuda.Event()
+        self._mark.record(torch.cuda.current_stream(self.t.device))
+        return self._mark
+
+    def raise_if_set(self, what: str, mark=None) -> None:
         if self._defer:
             return
-        v = int(self.t.item())
+        if mark is not None:
+            with torch.cuda.stream(self._side):
+                self._side.wait_event(self._mark)
+                self._host.copy_(self.t, non_blocking=True)
+                self._done.record(self._side)
+            self._done.synchronize()
+            v = int(self._host[0])
+        else:
+            v = int(self.t.item())
         if v & _lib.FLAG_DOMAIN:
-            self.t.zero_()
+            self.t.zero_()      # stream-ordered: after the call's trailing kernels too
             raise DomainError(f"{what} locations must lie strictly inside (-1, 1)^3")
+
+    def check_points(self, pts: torch.Tensor) -> None:
+        """Enqueue a stand-alone domain check of pts (n, 3) float32."""
+        n = int(pts.shape[0])
+        if n:
+            _lib.call("fc2t2_domain_check", _ptr(pts), n, _ptr(self.t), _stream())
 
 
 # ------------------------------------------------------------ datatypes ---
@@ -454,6 +490,9 @@ class Engine:
         st = torch.zeros((res, res, res, channels, self.PP), dtype=torch.float32,
                          device=_device())
         return ExpansionGrid(level=level, kind=kind, storage=st, rho=self.rho)
+
+    def finest_grid_bytes(self, channels: int) -> int:
+        return level_resolution(self.levels) ** 3 * channels * self.PP * 4
 
     def _empty_grid(self, level: int, channels: int, kind: str) -> ExpansionGrid:
         res = level_resolution(level)

@@ -165,11 +165,14 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
         return _explicit_forward_host(engine, sources, q)
     qd = to_device(q, 3, points=True)
     p_sort = engine.sort_points(sources.p)
-    acc = engine.expand_device(sources.p, sources.w, p_sort)
-    coherent = acc.grid.storage.numel() * 4 > COHERENT_L2P_BYTES
+    coherent = engine.finest_grid_bytes(sources.channels) > COHERENT_L2P_BYTES
     q_sort = engine.sort_points(qd) if coherent else None   # else sorted by the backward
+    if q_sort is None:
+        engine.flag.check_points(qd)    # the L2P at q would only see q at the very end
+    checked = engine.flag.mark()
+    acc = engine.expand_device(sources.p, sources.w, p_sort)
     vals = _l2p(acc, qd, _lib.L2P_VALUE, q_sort)["value"]
-    engine.flag.raise_if_set("source/query")
+    engine.flag.raise_if_set("source/query", checked)
     return ExplicitResult(values=like_input(vals, q), accessor=acc, q=q, sources=sources,
                           engine=engine, q_dev=qd, sorts=(p_sort, q_sort))
 
@@ -181,11 +184,12 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     qd = res.q_dev
     src = res.sources
     p_sort, q_sort = _sorts(res)
+    checked = eng.flag.mark()           # the sorts re-checked p and q
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
     q_bar = _l2p(res.accessor, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"]
     back = eng.expand_device(qd, yb, q_sort)
     out = _l2p(back, src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, p_sort, wts=src.w)
-    eng.flag.raise_if_set("source/query")
+    eng.flag.raise_if_set("source/query", checked)
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),
                           q_bar=like_input(q_bar, ref))
@@ -263,7 +267,9 @@ def depth_forward(engine: Engine, sources: SourceSet, bundle: RayBundle, bias: f
         raise ValueError("root layers expect a single-channel field")
     if engine.rho > ROOT_MAX_ORDER:
         raise OrderError(f"root layers need rho <= {ROOT_MAX_ORDER}")
-    acc = engine.expand_device(sources.p, sources.w)
+    p_sort = engine.sort_points(sources.p)
+    checked = engine.flag.mark()
+    acc = engine.expand_device(sources.p, sources.w, p_sort)
     org, dirs = bundle.dev()
     R = bundle.count
     dev = org.device
@@ -277,26 +283,59 @@ def depth_forward(engine: Engine, sources: SourceSet, bundle: RayBundle, bias: f
     _lib.call("fc2t2_depth_forward", engine.rho, engine.levels, _ptr(st), _ptr(org), _ptr(dirs), R,
               float(bias), _ptr(lengths), _ptr(hit), _ptr(points), _ptr(grads), _ptr(hess),
               _ptr(denom), _stream())
-    engine.flag.raise_if_set("source")
+    engine.flag.raise_if_set("source", checked)
     hitb = hit.bool()
     ref = bundle.origins
-    diag = {"dead_pixels": int((~hitb).sum().item()), "ift_clamped": 0}
+    diag = Diagnostics(dead_pixels=R - hit.sum(dtype=torch.int64), ift_clamped=0)
     return RootResult(lengths=_like(lengths, ref), hit=_like(hitb, ref), points=_like(points, ref),
                       grads=_like(grads, ref), denom=_like(denom, ref), accessor=acc,
                       bundle=bundle, sources=sources, engine=engine, bias=bias,
                       diagnostics=diag,
                       dev={"hit": hit, "points": points, "grads": grads, "hess": hess,
-                           "denom": denom, "n_hit": R - diag["dead_pixels"]})
+                           "denom": denom})
+
+
+class Diagnostics(dict):
+    """The reference's diagnostics dict ({"dead_pixels": int, "ift_clamped":
+    int}); counts produced on the device stay device scalars until a value is
+    first read, so a layer call does not stall the stream for them."""
+
+    def _get(self, k):
+        v = dict.__getitem__(self, k)
+        if isinstance(v, torch.Tensor):
+            v = int(v.item())
+            dict.__setitem__(self, k, v)
+        return v
+
+    def __getitem__(self, k):
+        return self._get(k)
+
+    def get(self, k, default=None):
+        return self._get(k) if k in self else default
+
+    def items(self):
+        return [(k, self._get(k)) for k in list(self.keys())]
+
+    def values(self):
+        return [self._get(k) for k in list(self.keys())]
+
+    def resolved(self) -> dict:
+        return dict(self.items())
+
+    def __eq__(self, other):
+        return self.resolved() == (other.resolved() if isinstance(other, Diagnostics) else other)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return repr(self.resolved())
 
 
 def _root_jvp(res: RootResult, y_len, y_grad) -> LayerGradients:
     eng, src, R = res.engine, res.sources, res.bundle.count
-    grads = LayerGradients(w_bar=None, p_bar=None, diagnostics=dict(res.diagnostics))
+    grads = LayerGradients(w_bar=None, p_bar=None, diagnostics=Diagnostics(res.diagnostics))
     ref = y_len if y_len is not None else y_grad
-    if res.dev["n_hit"] == 0:
-        z = torch.zeros_like(src.w)
-        grads.w_bar, grads.p_bar = _like(z, ref), _like(torch.zeros_like(src.p), ref)
-        return grads
+    checked = eng.flag.mark()           # p and the rays were checked by the forward
     yl = _tangent(y_len, R, 1) if y_len is not None else None
     yg = _tangent(y_grad, R, 3) if y_grad is not None else None
     PP = eng.PP
@@ -310,8 +349,8 @@ def _root_jvp(res: RootResult, y_len, y_grad) -> LayerGradients:
               _ptr(yl), _ptr(yg), _ptr(keys), _ptr(payload), _ptr(nclamp), _stream())
     back = insert_and_expand(eng, keys, payload, 1)
     w_bar, p_bar = _source_adjoints(back, src)
-    eng.flag.raise_if_set("source")
-    grads.diagnostics["ift_clamped"] = int(nclamp.item())
+    eng.flag.raise_if_set("source", checked)
+    grads.diagnostics["ift_clamped"] = nclamp[0]
     grads.w_bar, grads.p_bar = _like(w_bar, ref), _like(p_bar, ref)
     return grads
 

@@ -210,6 +210,34 @@ def test_domain_errors(eng4):
         acc.value(torch.tensor([[0.0, -1.0, 0.5]], device="cuda"))
 
 
+def test_explicit_layer_domain_errors_and_recovery(eng4):
+    """The explicit layer raises DomainError at return for device inputs
+    (checked by early kernels, read without draining the stream); a valid
+    call right after is unaffected (the trailing kernels' flag writes are
+    cleared in stream order)."""
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.expansion import DomainError
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    rng = np.random.default_rng(4)
+    p = torch.from_numpy(rng.uniform(-0.9, 0.9, (500, 3)).astype(np.float32)).cuda()
+    w = torch.from_numpy(rng.normal(0, 1, (500, 1)).astype(np.float32)).cuda()
+    q = torch.from_numpy(rng.uniform(-0.9, 0.9, (777, 3)).astype(np.float32)).cuda()
+    ok = explicit_forward(eng4, SourceSet(p, w), q).values.clone()
+    for bad_q in (1.0, float("nan"), -1.5):
+        qb = q.clone()
+        qb[700, 1] = bad_q
+        with pytest.raises(DomainError):
+            explicit_forward(eng4, SourceSet(p, w), qb)
+        res = explicit_forward(eng4, SourceSet(p, w), q)
+        assert torch.equal(res.values, ok)
+        explicit_jvp(torch.ones(777, 1, device="cuda"), res)
+    pb = p.clone()
+    pb[3, 0] = -1.0
+    with pytest.raises(DomainError):
+        explicit_forward(eng4, SourceSet(pb, w), q)
+    assert torch.equal(explicit_forward(eng4, SourceSet(p, w), q).values, ok)
+
+
 def test_empty_sources(eng4):
     from paper_2111_00110_b200 import SourceSet
     acc = eng4.expand(SourceSet(np.zeros((0, 3)), np.zeros((0, 1))))

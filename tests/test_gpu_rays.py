@@ -99,6 +99,9 @@ def test_depth_invariants(small, eng3):
     s = SourceSet(small["p"], small["w"])
     dead = depth_forward(eng3, s, b, bias=-0.2)
     assert not dead.hit.any() and dead.diagnostics["dead_pixels"] == b.count
+    zd = depth_jvp(np.ones(b.count), dead)          # no hits: exact zeros, no shortcut
+    assert not np.any(zd.w_bar) and not np.any(zd.p_bar)
+    assert zd.diagnostics == {"dead_pixels": b.count, "ift_clamped": 0}
     a = depth_forward(eng3, s, b, bias=0.3)
     c = depth_forward(eng3, SourceSet(small["p"], 3.0 * small["w"]), b, bias=0.9)
     assert np.array_equal(a.hit, c.hit)
