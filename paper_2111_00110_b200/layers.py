@@ -17,6 +17,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 
@@ -51,10 +53,17 @@ class ExplicitResult:
     sorts: tuple = None      # ((p order, p cell_start), (q order, q cell_start))
 
 
-# Grids larger than this are not L2 resident (126 MB L2): evaluate points in
-# cell-sorted order so consecutive threads share cell rows (measured: at a
-# 37.7 MB grid the scattered point gathers cost more than they save).
-COHERENT_L2P_BYTES = 64 << 20
+# Cell-coherent L2P (points evaluated in cell-sorted order so neighbouring
+# threads share rows) for grids larger than this many bytes; 0 = never.  Off
+# by default: with the warp-cooperative row fetch (l2p.cu) natural order is as
+# fast for values and faster for gradients even at config 5's 704 MB grid
+# (B200, 2^27 points: 9.3 / 10.2 ms natural vs 9.0 / 14.3 ms sorted), and it
+# needs no query sort before the forward.  FC2T2_COHERENT_L2P_MB re-enables it.
+COHERENT_L2P_BYTES = int(os.environ.get("FC2T2_COHERENT_L2P_MB", "0")) << 20
+
+
+def _beyond_coherent(nbytes: int) -> bool:
+    return COHERENT_L2P_BYTES > 0 and nbytes > COHERENT_L2P_BYTES
 
 
 def _sorts(res: "ExplicitResult"):
@@ -69,7 +78,7 @@ def _sorts(res: "ExplicitResult"):
 
 def _coherent(acc: Accessor, sort):
     st = acc.grid.storage
-    return sort[0] if st.numel() * st.element_size() > COHERENT_L2P_BYTES else None
+    return sort[0] if _beyond_coherent(st.numel() * st.element_size()) else None
 
 
 def _l2p(acc: Accessor, pts, mode: int, sort=None, wts=None):
@@ -99,7 +108,7 @@ def _explicit_forward_host(engine: Engine, sources: SourceSet, q) -> ExplicitRes
     p_sort = engine.sort_points(sources.p)
     acc = engine.expand_device(sources.p, sources.w, p_sort)
     cs = torch.cuda.current_stream()
-    coherent = acc.grid.storage.numel() * 4 > COHERENT_L2P_BYTES
+    coherent = _beyond_coherent(acc.grid.storage.numel() * 4)
     out = torch.empty((qd.shape[0], acc.channels), dtype=torch.float32, pin_memory=True)
     if not coherent:
         for a, b, ev in chunks:
@@ -165,7 +174,7 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
         return _explicit_forward_host(engine, sources, q)
     qd = to_device(q, 3, points=True)
     p_sort = engine.sort_points(sources.p)
-    coherent = engine.finest_grid_bytes(sources.channels) > COHERENT_L2P_BYTES
+    coherent = _beyond_coherent(engine.finest_grid_bytes(sources.channels))
     q_sort = engine.sort_points(qd) if coherent else None   # else sorted by the backward
     if q_sort is None:
         engine.flag.check_points(qd)    # the L2P at q would only see q at the very end

@@ -297,7 +297,7 @@ def test_explicit_host_tensors_match_device(eng4, monkeypatch, coherent, m):
     import paper_2111_00110_b200.layers as layers
     from paper_2111_00110_b200 import SourceSet
     if coherent:
-        monkeypatch.setattr(layers, "COHERENT_L2P_BYTES", 0)
+        monkeypatch.setattr(layers, "COHERENT_L2P_BYTES", 1)
     rng = np.random.default_rng(7)
     p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32))
     w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32))
@@ -411,6 +411,34 @@ def test_presorted_l2p_and_p2m_match_natural_order(eng4):
                               order=srt[0])
         for k in keys:
             assert torch.equal(nat[k], got[k])
+
+
+@pytest.mark.parametrize("rho,level,C,n", [(4, 4, 1, 4133), (4, 3, 3, 70), (6, 5, 1, 3001),
+                                           (2, 3, 2, 33), (6, 3, 2, 1)])
+def test_warp_cooperative_l2p_matches_per_thread_gather(cuda, rho, level, C, n):
+    """Natural-order L2P uses the warp-cooperative row fetch (rows staged in
+    shared memory by cp.async); an explicit order selects the per-thread
+    gather.  With the identity order both evaluate the same arithmetic, so
+    every mode (value, grad, Hessian, weighted grad), ragged tails and C > 1
+    must agree bit for bit."""
+    from paper_2111_00110_b200 import Engine, KernelModel, _lib
+    from paper_2111_00110_b200.expansion import Accessor
+    eng = Engine(KernelModel("gaussian", 300.0, rho), level, check_admissibility=False)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    L = eng._empty_grid(level, C, "L")
+    L.storage.normal_(generator=gen)       # pad entries are never read by the contractions
+    acc = Accessor(L, eng.table, eng.flops, flag=eng.flag)
+    q = torch.rand(n, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(n, C, device="cuda", generator=gen)
+    ident = torch.arange(n, dtype=torch.int32, device="cuda")
+    for mode, keys in ((_lib.L2P_VALUE | _lib.L2P_WGRAD, ("value", "wgrad")),
+                       (_lib.L2P_GRAD | _lib.L2P_HESS, ("grad", "hess")),
+                       (_lib.L2P_VALUE | _lib.L2P_GRAD | _lib.L2P_HESS, ("value", "grad", "hess"))):
+        nat = acc.eval_device(q, mode, wts=w)
+        thr = acc.eval_device(q, mode, wts=w, order=ident)
+        for k in keys:
+            assert torch.isfinite(nat[k]).all()
+            assert torch.equal(nat[k], thr[k]), (mode, k)
 
 
 def test_graphed_explicit_replays_bit_identical(eng4):
