@@ -159,6 +159,19 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
               float* d_l, int accumulate, void* d_ws, size_t ws_bytes, void* stream);
 
 /* ---- cascade: Engine.expand_from_moments (expansion.py:268-281) ---- */
+/* Separable finest-level M2L.  The finest far (parity stencil) + near tables
+ * of a Gaussian engine factor per axis (kernel.py separable_factors; the LSQ
+ * fit of ref kernel.py:180-204 and the Taylor tables of :169-177):
+ * coeffs(o) = post_S (K(o_x) (x) K(o_y) (x) K(o_z))_S pre_S.  With the
+ * factors set, fc2t2_expand runs the finest far + near M2L
+ * (ref expansion.py:276-279) as three 1-D convolutions (m2l_sep.cu) instead
+ * of the dense tables; valid only when every stencil offset of that level is
+ * active (the caller checks: kernel.py separable_eligible).  pre, post
+ * (rho+1)^2 and conv 7 (rho+1)^2 float64, [out][in], d = -3..3; NULL
+ * pointers switch back to the dense path.  rho <= 5, finest res >= 32. */
+int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
+                               const double* conv);
+int fc2t2_engine_separable(const fc2t2_engine* e);
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream);

@@ -118,6 +118,9 @@ struct fc2t2_engine {
   // M2M chain and the coarse levels run on the caller's stream
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // separable finest M2L (m2l_sep.cu): per-axis factors, [out][in] float64
+  bool sep = false;
+  std::vector<double> sep_pre, sep_post, sep_conv;
 };
 
 namespace {
@@ -760,7 +763,8 @@ ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
     w.coarse_part =
         std::max(w.coarse_part, part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels));
   }
-  w.fine_part = part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
+  w.fine_part = e->sep ? fc2t2::m2l_sep_workspace_floats(e->rho, L, channels)
+                       : part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
   return w;
 }
 
@@ -784,6 +788,26 @@ int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const f
                      "expand m2l");
 }
 }  // namespace
+
+int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
+                               const double* conv) {
+  if (!e) return fail(FC2T2_EVALUE, "null engine");
+  if (!pre || !post || !conv) {
+    e->sep = false;
+    return FC2T2_OK;
+  }
+  const int res = 1 << (e->levels + 1);
+  if (e->rho > 5 || e->levels <= kCoarsest || res % 32)
+    return fail(FC2T2_EVALUE, "separable M2L needs rho <= 5 and a finest grid of >= 32 cells");
+  const int R1 = e->rho + 1;
+  e->sep_pre.assign(pre, pre + R1 * R1);
+  e->sep_post.assign(post, post + R1 * R1);
+  e->sep_conv.assign(conv, conv + 7 * R1 * R1);
+  e->sep = true;
+  return FC2T2_OK;
+}
+
+int fc2t2_engine_separable(const fc2t2_engine* e) { return e && e->sep ? 1 : 0; }
 
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
   if (!e || !e->uploaded || channels < 1) return 0;
@@ -854,7 +878,17 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
     if (st == FC2T2_OK) st = cuda_status(cudaStreamWaitEvent(e->side, e->fork, 0), "expand fork");
     if (st != FC2T2_OK) return st;
   }
-  if (fine) {
+  if (fine && e->sep) {
+    st = cuda_status(fc2t2::m2l_sep(e->rho, L, channels, e->sep_pre.data(), e->sep_post.data(),
+                                    e->sep_conv.data(), Mg[L], Lg[L], fine_part, x_begin, x_end,
+                                    overlap ? e->side : s),
+                     "expand m2l_sep");
+    if (st != FC2T2_OK) return st;
+    if (overlap) {
+      st = cuda_status(cudaEventRecord(e->join, e->side), "expand join");
+      if (st != FC2T2_OK) return st;
+    }
+  } else if (fine) {
     st = level_m2l(e, channels, L, pL, Mg[L], Lg[L], 0, fine_part, overlap ? e->side : s,
                    x_begin, x_end);
     if (st != FC2T2_OK) return st;

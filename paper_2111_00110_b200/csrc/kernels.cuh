@@ -83,6 +83,16 @@ cudaError_t tc_prepare(int rho, int C, const TCPlan& plan, const float* M, void*
 cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L, int accumulate,
                    cudaStream_t s, int x_begin = 0, int x_end = -1);
 
+// m2l_sep.cu -------------------------------------------------------------
+// Finest-level far + near M2L through the per-axis factors of the tables
+// (kernel.py separable_factors): pre/post (R1 x R1) and conv (7 x R1 x R1),
+// [out][in] float64 row-major, R1 = rho + 1 <= 6.  Writes L (no accumulate)
+// for cells with x in [x_begin, x_end); ws = m2l_sep_workspace_floats.
+size_t m2l_sep_workspace_floats(int rho, int level, int C);
+cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
+                    const double* conv, const float* M, float* L, float* ws, int x_begin,
+                    int x_end, cudaStream_t s);
+
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {
   L2P_VALUE = 1,   // (n, C)

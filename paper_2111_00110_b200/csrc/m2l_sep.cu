@@ -1,0 +1,580 @@
+// Finest-level M2L (far + near) as three 1-D convolutions between two
+// per-axis triangular transforms.
+//
+// Reference: Engine.m2l (expansion.py:227-264) over the finest far table
+// (parity stencil, :246-249) plus the near table, with the tables of
+// kernel.py:180-204 (LSQ) or :169-177 (Taylor).  The Gaussian factors per
+// axis, so every finest table does too (paper_2111_00110_b200/kernel.py,
+// separable_factors): coeffs(o) = post_S . (K(o_x) (x) K(o_y) (x) K(o_z))_S .
+// pre_S, and far + near give every target the full 6 x 6 x 6 box of source
+// offsets ({-2..3} per axis for an even target index, {-3..2} for an odd
+// one).  So, per channel:
+//
+//   pre    M'(a,b,c)  = sum pre[a'][a] pre[b'][b] pre[c'][c] M      (lower tri)
+//   z pass Z(a,b,c')  = sum_{dz, c} K(dz)[c'][c]  M'(a,b,c)(z+dz)
+//   y pass Y(a,b',c') = sum_{dy, b} K(dy)[b'][b]  Z(a,b,c')(y+dy)
+//   x pass X(a',b',c')= sum_{dx, a} K(dx)[a'][a]  Y(a,b',c')(x+dx)
+//   post   L          = post (x) post (x) post  X                  (upper tri)
+//
+// with every index set truncated to what the next step can use (total degree
+// <= rho at the end; the triangular transforms never need more).  At rho = 4
+// that is ~4e3 multiply-adds per cell instead of the dense 216 x 35 x 35.
+// Sources outside the grid contribute nothing (the reference's clipped
+// slices).  The factor matrices are kernel parameters (__grid_constant__),
+// and every loop over them unrolls, so each FFMA reads its coefficient from
+// the constant bank.
+//
+// Layouts (one channel block after another; x fastest unless noted):
+//   M' : [e in AB order][y][z][x]       AB(a,b,c) = ab(a,b) + c
+//   Z  : [e = pair(a,b)*R1 + c'][y][z][x]
+//   Y  : [e = a*NAB + pair(b',c')][y][z][x]
+//   X  : [e = graded-lex (a',b',c')][x][y][z]   (z fastest)
+// Each pass CTA stages a 14/16-deep window (8 outputs + the 3/3 halo) of 32
+// lines of the entries one partition needs (lanes along the contiguous
+// axis); warp g computes one output group for all 8 positions of its lane's
+// line with the accumulators in registers (see "passes" below).
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <cstdlib>
+
+namespace fc2t2 {
+
+namespace {
+
+template <int RHO>
+struct SepIdx {
+  static constexpr int R1 = RHO + 1;
+  static constexpr int NAB = R1 * (R1 + 1) / 2;  // pairs (a, b) with a + b <= RHO
+  static constexpr int T = NAB * R1;             // entries of Z and Y
+  static constexpr int P = MI<RHO>::P;
+  static constexpr int pair(int a, int b) { return a * R1 - a * (a - 1) / 2 + b; }
+  static constexpr int ab(int a, int b) {
+    int o = 0;
+    for (int i = 0; i < a; ++i) o += (R1 - i) * (R1 - i + 1) / 2;
+    for (int j = 0; j < b; ++j) o += R1 - a - j;
+    return o;
+  }
+  static constexpr int zoff(int a, int b, int c) { return pair(a, b) * R1 + c; }
+  static constexpr int yoff(int a, int b, int c) { return a * NAB + pair(b, c); }
+};
+
+constexpr int kLines = 32;
+// POS output positions per tile (8 or 16, FC2T2_SEP_POS); the z/y window holds
+// POS + 6 positions, the x window POS + 8 (16-byte aligned runs) in an odd
+// number of 16-byte chunks per lane (conflict-free 128-bit reads)
+constexpr int win_of(int POS) { return POS + 6; }
+constexpr int xs_of(int POS) { return 4 * (((POS + 8) / 4) | 1); }
+
+
+// ------------------------------------------------------------ pre / post ---
+
+// in place: v(a',..) = sum_{a <= a'} m[a'][a] v(a,..) along `axis`, on S
+template <int RHO, int AXIS>
+__device__ __forceinline__ void lower_axis(float (&v)[MI<RHO>::P], const float (&m)[RHO + 1][RHO + 1]) {
+  constexpr MI<RHO> mi{};
+#pragma unroll
+  for (int j = MI<RHO>::P - 1; j >= 0; --j) {
+    const int e[3] = {mi.e0[j], mi.e1[j], mi.e2[j]};
+    float s = 0.f;
+#pragma unroll
+    for (int a = 0; a <= e[AXIS]; ++a) {
+      const int i = MI<RHO>::index(AXIS == 0 ? a : e[0], AXIS == 1 ? a : e[1], AXIS == 2 ? a : e[2]);
+      s = fmaf(m[e[AXIS]][a], v[i], s);
+    }
+    v[j] = s;  // entries with a larger AXIS degree were already rewritten
+  }
+}
+
+// in place: v(a',..) = sum_{a >= a'} m[a'][a] v(a,..) along `axis`, on S
+template <int RHO, int AXIS>
+__device__ __forceinline__ void upper_axis(float (&v)[MI<RHO>::P], const float (&m)[RHO + 1][RHO + 1]) {
+  constexpr MI<RHO> mi{};
+#pragma unroll
+  for (int j = 0; j < MI<RHO>::P; ++j) {
+    const int e[3] = {mi.e0[j], mi.e1[j], mi.e2[j]};
+    const int top = RHO - (e[0] + e[1] + e[2] - e[AXIS]);
+    float s = 0.f;
+#pragma unroll
+    for (int a = e[AXIS]; a <= top; ++a) {
+      const int i = MI<RHO>::index(AXIS == 0 ? a : e[0], AXIS == 1 ? a : e[1], AXIS == 2 ? a : e[2]);
+      s = fmaf(m[e[AXIS]][a], v[i], s);
+    }
+    v[j] = s;  // reads only entries of equal or higher AXIS degree: not yet rewritten
+  }
+}
+
+}  // namespace
+
+template <int RHO>
+struct SepParams {
+  float pre[RHO + 1][RHO + 1];
+  float post[RHO + 1][RHO + 1];
+  float conv[7][RHO + 1][RHO + 1];  // K(d) for d = -3..3, [out][in]
+};
+
+namespace {
+
+// M (res^3, C, PP) rows -> M' (AB order, x fastest).  Thread per cell,
+// lanes along x.
+template <int RHO>
+__global__ void __launch_bounds__(256)
+sep_pre_kernel(const float* __restrict__ M, float* __restrict__ Mp, int res, int C, int x_lo,
+               int nx, const __grid_constant__ SepParams<RHO> prm) {
+  using I = SepIdx<RHO>;
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  constexpr MI<RHO> mi{};
+  const int64_t cells = (int64_t)nx * res * res;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= cells * C) return;
+  const int ch = (int)(t / cells);
+  const int64_t r = t - (int64_t)ch * cells;
+  const int x = x_lo + (int)(r % nx);
+  const int64_t yz = r / nx;
+  const int z = (int)(yz % res), y = (int)(yz / res);
+  const float* row = M + ((((int64_t)x * res + y) * res + z) * C + ch) * PP;
+  float v[P];
+#pragma unroll
+  for (int k = 0; k < PP; k += 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(row + k));
+    if (k < P) v[k] = q.x;
+    if (k + 1 < P) v[k + 1] = q.y;
+    if (k + 2 < P) v[k + 2] = q.z;
+    if (k + 3 < P) v[k + 3] = q.w;
+  }
+  lower_axis<RHO, 0>(v, prm.pre);
+  lower_axis<RHO, 1>(v, prm.pre);
+  lower_axis<RHO, 2>(v, prm.pre);
+  const int64_t plane = (int64_t)res * res * res;
+  float* out = Mp + (int64_t)ch * P * plane + ((int64_t)y * res + z) * res + x;
+#pragma unroll
+  for (int j = 0; j < P; ++j) out[(int64_t)I::ab(mi.e0[j], mi.e1[j]) * plane + mi.e2[j] * plane] = v[j];
+}
+
+// X (graded-lex, z fastest) -> L rows.  Thread per cell, lanes along z.
+template <int RHO>
+__global__ void __launch_bounds__(256)
+sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int C, int x_lo,
+                int nx, const __grid_constant__ SepParams<RHO> prm) {
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  const int64_t cells = (int64_t)nx * res * res;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= cells * C) return;
+  const int ch = (int)(t / cells);
+  const int64_t r = t - (int64_t)ch * cells;
+  const int z = (int)(r % res);
+  const int64_t xy = r / res;
+  const int y = (int)(xy % res), x = x_lo + (int)(xy / res);
+  const int64_t plane = (int64_t)res * res * res;
+  const float* in = X + (int64_t)ch * P * plane + ((int64_t)x * res + y) * res + z;
+  float v[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] = in[(int64_t)j * plane];
+  upper_axis<RHO, 0>(v, prm.post);
+  upper_axis<RHO, 1>(v, prm.post);
+  upper_axis<RHO, 2>(v, prm.post);
+  float* row = L + ((((int64_t)x * res + y) * res + z) * C + ch) * PP;
+#pragma unroll
+  for (int k = 0; k < PP; k += 4) {
+    float4 q;
+    q.x = k < P ? v[k] : 0.f;
+    q.y = k + 1 < P ? v[k + 1] : 0.f;
+    q.z = k + 2 < P ? v[k + 2] : 0.f;
+    q.w = k + 3 < P ? v[k + 3] : 0.f;
+    *reinterpret_cast<float4*>(row + k) = q;
+  }
+}
+
+// ------------------------------------------------------------------ passes ---
+//
+// A pass CTA owns 32 lines x 8 consecutive output positions (even first
+// position, so output w has parity w & 1) of one partition of the entries;
+// warp g computes group g of that partition for all 8 positions of its
+// lane's line, holding the 8 x n_out accumulators in registers and reading
+// each staged input once (a 14/16-deep window: 8 outputs + the 3/3 halo).
+//   z pass, partition a = A, group b:  in  M'(A,b,c)  c <= RHO-A-b
+//                                      out Z(A,b,c')  c' <= RHO
+//   y pass, partition a = A, group c': in  Z(A,b,c')  b <= RHO-A
+//                                      out Y(A,b',c') b' <= RHO-c'
+//   x pass, partition b' = B, group c': in Y(a,B,c')  a <= RHO
+//                                      out X(a',B,c') a' <= RHO-B-c'
+// Every contraction is sum_{d, i} K(d)[j][i] in_i(pos + d).
+
+enum { PASS_Z = 0, PASS_Y = 1, PASS_X = 2 };
+
+template <int RHO, int PASS, int PART>
+struct Part {
+  using I = SepIdx<RHO>;
+  static constexpr int R1 = RHO + 1;
+  static constexpr int NE = PASS == PASS_Z ? (R1 - PART) * (R1 - PART + 1) / 2
+                                           : (PASS == PASS_Y ? (R1 - PART) * R1 : R1 * (R1 - PART));
+  static constexpr int EBASE = PASS == PASS_Z ? I::ab(PART, 0)
+                                              : (PASS == PASS_Y ? I::pair(PART, 0) * R1 : 0);
+  // global entry of local window entry le (x pass: le = a * (R1 - B) + c')
+  static constexpr int entry(int le) {
+    return PASS == PASS_X ? (le / (R1 - PART)) * I::NAB + I::pair(PART, le % (R1 - PART))
+                          : EBASE + le;
+  }
+};
+
+// z/y window: [q][le NE][lane 32] (q = position - pos0 + 3), filled by
+// 16-byte copies of the 32-float x-runs.  x window: [le][lane][xs] (q =
+// position - pos0 + 4), filled by 16-byte copies of x-runs and read back with
+// 128-bit loads; an odd number of 16-byte chunks per lane row puts the 8 lanes
+// of a quarter-warp on distinct bank quads.
+
+// One output group for 8 positions of this lane's line: NOUT outputs,
+// `nin` inputs at window entries in_base + i * in_stride.  Only NOUT (and the
+// pass's window layout) is compile-time, so the whole pass is a handful of
+// small code paths (instruction-cache resident); the K(d)[.][i] column of an
+// input comes from shared memory (Kt[i][d][j], warp-uniform broadcast).
+template <int RHO, int PASS, int POS, int NOUT>
+__device__ __forceinline__ void group_body(const float* sm, const float* Kt, int ne, int lane,
+                                           int nin, int in_base, int in_stride,
+                                           const int (&oe)[RHO + 1], float* out,
+                                           int64_t pos_stride, int64_t plane, int nvalid) {
+  constexpr int OFF = PASS == PASS_X ? 4 : 3;
+  constexpr int NQ = PASS == PASS_X ? POS + 8 : win_of(POS);
+  float acc[POS][NOUT];
+#pragma unroll
+  for (int w = 0; w < POS; ++w)
+#pragma unroll
+    for (int j = 0; j < NOUT; ++j) acc[w][j] = 0.f;
+#pragma unroll 1
+  for (int i = 0; i < nin; ++i) {
+    const int le = in_base + i * in_stride;
+    float v[NQ];
+    if constexpr (PASS == PASS_X) {
+      const float4* r4 = reinterpret_cast<const float4*>(sm + (le * kLines + lane) * xs_of(POS));
+#pragma unroll
+      for (int q = 0; q < NQ / 4; ++q) {
+        const float4 t = r4[q];
+        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) v[q] = sm[(q * ne + le) * kLines + lane];
+    }
+    float k[7][NOUT];
+    const float4* kc = reinterpret_cast<const float4*>(Kt + i * 56);
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+      const float4 lo = kc[2 * d];
+      const float lo_[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+      for (int j = 0; j < NOUT && j < 4; ++j) k[d][j] = lo_[j];
+      if constexpr (NOUT > 4) {
+        const float4 hi = kc[2 * d + 1];
+        const float hi_[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+        for (int j = 4; j < NOUT; ++j) k[d][j] = hi_[j - 4];
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < POS; ++w) {
+#pragma unroll
+      for (int kk = 0; kk < 6; ++kk) {
+        const int d = kk - 2 - (w & 1);
+        const float x = v[w + OFF + d];
+#pragma unroll
+        for (int j = 0; j < NOUT; ++j) acc[w][j] = fmaf(k[d + 3][j], x, acc[w][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < POS; ++w) {
+    if (w < nvalid) {
+#pragma unroll
+      for (int j = 0; j < NOUT; ++j) out[(int64_t)oe[j] * plane + w * pos_stride] = acc[w][j];
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// tile geometry decoded from a linear tile index
+struct Tile {
+  int ch, part, fixed, line0, pos0;
+};
+__device__ __forceinline__ Tile decode_tile(int64_t t, int R1, int res, int line_lo, int nlt,
+                                            int pos_lo, int npt, int POS) {
+  Tile r;
+  r.line0 = line_lo + (int)(t % nlt) * kLines; t /= nlt;
+  r.pos0 = pos_lo + (int)(t % npt) * POS; t /= npt;
+  r.fixed = (int)(t % res); t /= res;
+  r.part = (int)(t % R1);
+  r.ch = (int)(t / R1);
+  return r;
+}
+
+template <int RHO, int PASS, int POS, int PART>
+__device__ __forceinline__ void load_part(float* sm, const float* src, int res, const Tile& T) {
+  using PT = Part<RHO, PASS, PART>;
+  if constexpr (PASS != PASS_X) {
+    constexpr int total = win_of(POS) * PT::NE * (kLines / 4);
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int c4 = i & 7;
+      const int r = i >> 3;
+      const int le = r % PT::NE, q = r / PT::NE;
+      const int pos = T.pos0 - 3 + q;
+      const bool ok = pos >= 0 && pos < res;
+      const int64_t e = PT::entry(le);
+      // z pass: [e][y=fixed][z=pos][x]; y pass: [e][y=pos][z=fixed][x]
+      const int64_t g = PASS == PASS_Z ? ((e * res + T.fixed) * res + (ok ? pos : 0)) * res
+                                       : ((e * res + (ok ? pos : 0)) * res + T.fixed) * res;
+      cp_async16(sm + (q * PT::NE + le) * kLines + 4 * c4, src + g + T.line0 + 4 * c4, ok);
+    }
+  } else {
+    constexpr int NC = (POS + 8) / 4;
+    constexpr int total = PT::NE * kLines * NC;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int c4 = i % NC;
+      const int r = i / NC;
+      const int lane = r & (kLines - 1), le = r >> 5;
+      const int x = T.pos0 - 4 + 4 * c4;
+      const bool ok = x >= 0 && x < res;
+      // [e][y=fixed][z=line][x]
+      const int64_t g =
+          (((int64_t)PT::entry(le) * res + T.fixed) * res + T.line0 + lane) * res + (ok ? x : 0);
+      cp_async16(sm + (le * kLines + lane) * xs_of(POS) + 4 * c4, src + g, ok);
+    }
+  }
+}
+
+template <int RHO, int PASS, int POS>
+__device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, float* dst, int res,
+                                             int pos_end, const Tile& T) {
+  using I = SepIdx<RHO>;
+  constexpr int R1 = RHO + 1;
+  const int64_t plane = (int64_t)res * res * res;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P_ = T.part;
+  int ng, ne, nin, in_base, in_stride, nout;
+  int oe[R1];
+  if (PASS == PASS_Z) {            // partition a = P_, group b = g
+    ng = R1 - P_;
+    ne = (R1 - P_) * (R1 - P_ + 1) / 2;
+    nin = R1 - P_ - g;
+    in_base = I::ab(P_, g) - I::ab(P_, 0);
+    in_stride = 1;
+    nout = R1;
+#pragma unroll
+    for (int j = 0; j < R1; ++j) oe[j] = I::zoff(P_, g, j);
+  } else if (PASS == PASS_Y) {     // partition a = P_, group c' = g
+    ng = R1;
+    ne = (R1 - P_) * R1;
+    nin = R1 - P_;
+    in_base = g;
+    in_stride = R1;
+    nout = R1 - g;
+#pragma unroll
+    for (int j = 0; j < R1; ++j) oe[j] = I::yoff(P_, j, g);
+  } else {                         // partition b' = P_, group c' = g
+    ng = R1 - P_;
+    ne = R1 * (R1 - P_);
+    nin = R1;
+    in_base = g;
+    in_stride = R1 - P_;
+    nout = R1 - P_ - g;
+#pragma unroll
+    for (int j = 0; j < R1; ++j) oe[j] = MI<RHO>::index(j, P_, g) < 0 ? 0 : MI<RHO>::index(j, P_, g);
+  }
+  if (g >= ng) return;
+  float* o;
+  int64_t pos_stride;
+  if (PASS == PASS_Z) {
+    o = dst + ((int64_t)T.fixed * res + T.pos0) * res + T.line0 + lane;
+    pos_stride = res;
+  } else {
+    o = dst + ((int64_t)T.pos0 * res + T.fixed) * res + T.line0 + lane;
+    pos_stride = (int64_t)res * res;
+  }
+  const int nvalid = min(POS, pos_end - T.pos0);
+#define FC2T2_SEP_N(Q)                                                                     \
+  case Q:                                                                                  \
+    if constexpr (Q <= R1)                                                                 \
+      group_body<RHO, PASS, POS, Q>(sm, Kt, ne, lane, nin, in_base, in_stride, oe, o,           \
+                               pos_stride, plane, nvalid);                                 \
+    break;
+  switch (nout) {
+    FC2T2_SEP_N(1)
+    FC2T2_SEP_N(2)
+    FC2T2_SEP_N(3)
+    FC2T2_SEP_N(4)
+    FC2T2_SEP_N(5)
+    FC2T2_SEP_N(6)
+    default:
+      break;
+  }
+#undef FC2T2_SEP_N
+}
+
+template <int RHO, int PASS, int POS>
+constexpr int pass_win_floats() {
+  constexpr int R1 = RHO + 1;
+  return PASS == PASS_X ? R1 * R1 * kLines * xs_of(POS)
+                        : win_of(POS) * (PASS == PASS_Z ? R1 * (R1 + 1) / 2 : R1 * R1) * kLines;
+}
+template <int RHO, int PASS, int POS>
+constexpr int pass_smem_floats() {  // window + Kt[i][d][8]
+  return pass_win_floats<RHO, PASS, POS>() + 7 * 8 * (RHO + 1);
+}
+
+// One pass.  Tile = 32 lines x 8 output positions of one partition/channel:
+//   z pass: lines x, positions z, fixed y      (in M', out Z)
+//   y pass: lines x, positions y, fixed z      (in Z,  out Y)
+//   x pass: lines z, positions x, fixed y      (in Y,  out X)
+template <int RHO, int PASS, int POS>
+__global__ void __launch_bounds__(32 * (RHO + 1))
+sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, int C,
+                int line_lo, int nlt, int pos_lo, int npt, int pos_end,
+                const __grid_constant__ SepParams<RHO> prm) {
+  using I = SepIdx<RHO>;
+  extern __shared__ __align__(16) float sm[];
+  constexpr int R1 = RHO + 1;
+  float* Kt = sm + pass_win_floats<RHO, PASS, POS>();
+  const int64_t plane = (int64_t)res * res * res;
+  const int in_entries = PASS == PASS_Z ? I::P : I::T;
+  const int out_entries = PASS == PASS_X ? I::P : I::T;
+  const Tile T = decode_tile(blockIdx.x, R1, res, line_lo, nlt, pos_lo, npt, POS);
+  const float* src = in + (int64_t)T.ch * in_entries * plane;
+#define FC2T2_LOAD(Q) \
+  if constexpr (Q <= RHO) load_part<RHO, PASS, POS, Q>(sm, src, res, T)
+  switch (T.part) {
+    case 0: FC2T2_LOAD(0); break;
+    case 1: FC2T2_LOAD(1); break;
+    case 2: FC2T2_LOAD(2); break;
+    case 3: FC2T2_LOAD(3); break;
+    case 4: FC2T2_LOAD(4); break;
+    case 5: FC2T2_LOAD(5); break;
+    default: break;
+  }
+#undef FC2T2_LOAD
+  // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads)
+  for (int t = threadIdx.x; t < 7 * 8 * R1; t += blockDim.x) {
+    const int j = t & 7, d = (t >> 3) % 7, i = t / 56;
+    Kt[t] = j < R1 ? prm.conv[d][j][i] : 0.f;
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T);
+}
+
+template <int RHO>
+SepParams<RHO> to_params(const double* pre, const double* post, const double* conv) {
+  SepParams<RHO> p;
+  constexpr int R1 = RHO + 1;
+  for (int i = 0; i < R1; ++i)
+    for (int j = 0; j < R1; ++j) {
+      p.pre[i][j] = (float)pre[i * R1 + j];
+      p.post[i][j] = (float)post[i * R1 + j];
+      for (int d = 0; d < 7; ++d) p.conv[d][i][j] = (float)conv[(d * R1 + i) * R1 + j];
+    }
+  return p;
+}
+
+int sep_pos() {
+  static const int v = [] {
+    const char* e = std::getenv("FC2T2_SEP_POS");
+    return e && e[0] == '1' && e[1] == '6' ? 16 : 8;
+  }();
+  return v;
+}
+
+template <int RHO, int PASS, int POS>
+cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int line_lo, int line_hi,
+                            int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
+                            cudaStream_t s) {
+  const int nlt = (line_hi - line_lo + kLines - 1) / kLines;
+  const int npt = (pos_hi - pos_lo + POS - 1) / POS;
+  const int64_t blocks = (int64_t)nlt * npt * res * (RHO + 1) * C;
+  if (blocks <= 0) return cudaSuccess;
+  constexpr int smem = pass_smem_floats<RHO, PASS, POS>() * (int)sizeof(float);
+  static unsigned long long configured = 0;
+  if (smem > 48 * 1024 && attr_needed(configured))
+    cudaFuncSetAttribute(sep_pass_kernel<RHO, PASS, POS>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  FC2T2_LAUNCH(name, s,
+               sep_pass_kernel<RHO, PASS, POS><<<(unsigned)blocks, 32 * (RHO + 1), smem, s>>>(
+                   in, out, res, C, line_lo, nlt, pos_lo, npt, pos_hi, prm));
+  return cudaGetLastError();
+}
+
+template <int RHO, int PASS>
+cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo, int line_hi,
+                        int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
+                        cudaStream_t s) {
+  if (sep_pos() == 8)
+    return launch_pass_pos<RHO, PASS, 8>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
+                                         name, s);
+  return launch_pass_pos<RHO, PASS, 16>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
+                                        name, s);
+}
+
+template <int RHO>
+cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
+                        const double* conv, const float* M, float* L, float* wa, float* wb,
+                        int x_begin, int x_end, cudaStream_t s) {
+  const int res = 1 << (level + 1);
+  if (res % kLines) return cudaErrorInvalidValue;
+  const SepParams<RHO> prm = to_params<RHO>(pre, post, conv);
+  // x range the z/y passes must cover: the slab plus the x pass's halo,
+  // widened to whole 32-line tiles
+  const int xl = std::max(0, x_begin - 3) / kLines * kLines;
+  const int xh = std::min(res, (x_end + 3 + kLines - 1) / kLines * kLines);
+  cudaError_t err;
+  {
+    const int64_t n = (int64_t)(xh - xl) * res * res * C;
+    FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+                                       M, wa, res, C, xl, xh - xl, prm));
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  if ((err = launch_pass<RHO, PASS_Z>(wa, wb, res, C, xl, xh, 0, res, prm, "m2l_sep_z", s)))
+    return err;
+  if ((err = launch_pass<RHO, PASS_Y>(wb, wa, res, C, xl, xh, 0, res, prm, "m2l_sep_y", s)))
+    return err;
+  if ((err = launch_pass<RHO, PASS_X>(wa, wb, res, C, 0, res, x_begin, x_end, prm, "m2l_sep_x", s)))
+    return err;
+  {
+    const int64_t n = (int64_t)(x_end - x_begin) * res * res * C;
+    if (n > 0) {
+      FC2T2_LAUNCH("m2l_sep_post", s,
+                   sep_post_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+                       wb, L, res, C, x_begin, x_end - x_begin, prm));
+      if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    }
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+size_t m2l_sep_workspace_floats(int rho, int level, int C) {
+  const int64_t res = 1 << (level + 1);
+  const int64_t R1 = rho + 1, T = R1 * (R1 + 1) / 2 * R1;
+  return (size_t)(2 * T * res * res * res * C);
+}
+
+cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
+                    const double* conv, const float* M, float* L, float* ws, int x_begin,
+                    int x_end, cudaStream_t s) {
+  const int64_t res = 1 << (level + 1);
+  if (x_end < 0) x_end = (int)res;
+  float* wa = ws;
+  float* wb = ws + m2l_sep_workspace_floats(rho, level, C) / 2;
+  switch (rho) {
+    case 1: return m2l_sep_rho<1>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
+    case 2: return m2l_sep_rho<2>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
+    case 3: return m2l_sep_rho<3>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
+    case 4: return m2l_sep_rho<4>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
+    case 5: return m2l_sep_rho<5>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace fc2t2

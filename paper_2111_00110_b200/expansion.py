@@ -23,12 +23,14 @@ counting rules exactly (they are host-side tallies, pinned by tests).
 from __future__ import annotations
 
 from dataclasses import dataclass
+import os
 
 import numpy as np
 import torch
 
 from . import _lib, flops
 from .kernel import (COARSEST_LEVEL, KernelModel, M2LTable, fit_m2l_tables,
+                     separable_eligible, separable_factors,
                      level_box_width, level_resolution)
 from .multiindex import MultiIndexTable
 
@@ -432,7 +434,7 @@ class Engine:
 
     def __init__(self, kernel: KernelModel, levels: int, lsq: bool = True,
                  nodes_per_axis: int = 6, admissibility_tol: float = 1e-3,
-                 check_admissibility: bool = True):
+                 check_admissibility: bool = True, *, separable: bool | None = None):
         if levels < COARSEST_LEVEL:
             raise StageError(f"levels must be >= {COARSEST_LEVEL}")
         self.kernel = kernel
@@ -451,6 +453,15 @@ class Engine:
         self._pairs[("near", levels)] = m2l_pairs(self.m2l_tables["near"])
         self._h = None
         self.flag = None
+        # finest far + near M2L through the per-axis factors of its tables
+        # (kernel.separable_factors, csrc/m2l_sep.cu) when they factor;
+        # separable=False or FC2T2_M2L_DENSE=1 keeps the dense tcgen05 path
+        if separable is None:
+            separable = os.environ.get("FC2T2_M2L_DENSE", "0") != "1"
+        self.separable = bool(separable) and separable_eligible(
+            self.m2l_tables, levels, self.rho, lsq, nodes_per_axis)
+        self._sep = (separable_factors(kernel, levels, lsq, nodes_per_axis)
+                     if self.separable else None)
 
     # the device side is created lazily so the host tables can be built
     # (and pinned by CPU tests) without a GPU
@@ -467,6 +478,11 @@ class Engine:
                     h.h, int(t.level), int(bool(t.nearfield)), int(off.shape[0]),
                     off.ctypes.data, act.ctypes.data, co.ctypes.data), "engine_set_table")
             _lib.check(h.lib.fc2t2_engine_upload(h.h, _stream()), "engine_upload")
+            if self._sep is not None:
+                f = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in self._sep.items()}
+                _lib.check(h.lib.fc2t2_engine_set_separable(
+                    h.h, f["pre"].ctypes.data, f["post"].ctypes.data, f["conv"].ctypes.data),
+                    "engine_set_separable")
             self._h = h
             self.flag = DomainFlag()
         return self._h.h

@@ -366,13 +366,16 @@ def test_m2l_tensor_core_level5_matches_oracle(cuda):
     assert rel_l2(tc, ora.m2l(_np(m.data), ora.tables["far"][5])) < TOL
 
 
-def test_expand_slabs_assemble_full_cascade(cuda):
+@pytest.mark.parametrize("separable", [True, False])
+def test_expand_slabs_assemble_full_cascade(cuda, separable):
     """fc2t2_expand_slab (one rank's x-slab of the sharded cascade, SURVEY
     8(e)): the finest cells of every slab equal the full cascade bit for bit
-    (level 5, tcgen05 finest level), so the multi-GPU all-gather reproduces
-    the single-GPU grid exactly."""
+    (level 5, separable or dense tcgen05 finest level), so the multi-GPU
+    all-gather reproduces the single-GPU grid exactly."""
     from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
-    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False,
+                 separable=separable)
+    assert eng.separable == separable
     gen = torch.Generator(device="cuda").manual_seed(3)
     p = torch.rand(200_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
     w = torch.randn(200_000, 1, device="cuda", generator=gen)
@@ -495,3 +498,37 @@ def test_m2l_cta_pair_kernel_matches_single_cta():
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         outs.append(torch.load(path))
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("alpha,rho,level,C,lsq", [(1000.0, 4, 5, 1, True), (200.0, 4, 4, 2, True),
+                                                   (200.0, 3, 4, 1, True), (1000.0, 4, 5, 1, False),
+                                                   (1000.0, 5, 5, 1, True), (50.0, 2, 4, 3, True)])
+def test_separable_finest_m2l_matches_dense_and_oracle(cuda, alpha, rho, level, C, lsq):
+    """The separable finest far + near M2L (csrc/m2l_sep.cu: per-axis
+    triangular transforms around three 1-D convolutions) against the dense
+    per-offset tables (tcgen05 path of the same engine configuration) and the
+    float64 oracle cascade.  The orthonormal per-axis factors keep float32
+    rounding at input level: rel-L2 of the finest L grid < 2e-6."""
+    from paper_2111_00110_b200 import Engine, KernelModel
+    from oracle.fc2t2_oracle import Oracle
+    k = KernelModel("gaussian", alpha, rho)
+    sep = Engine(k, level, lsq=lsq, check_admissibility=False, separable=True)
+    dense = Engine(k, level, lsq=lsq, check_admissibility=False, separable=False)
+    assert sep.separable and not dense.separable
+    gen = torch.Generator(device="cuda").manual_seed(rho * 10 + level)
+    n = 60_000
+    p = torch.rand(n, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(n, C, device="cuda", generator=gen)
+    m = sep.p2m_device(p, w).storage
+    Ls = sep.cascade_device(m)
+    Ld = dense.cascade_device(m)
+    P = sep.P
+    a, b = _np(Ls)[..., :P], _np(Ld)[..., :P]
+    assert np.all(_np(Ls)[..., P:] == 0)
+    assert rel_l2(a, b) < 2e-6
+    ora = Oracle(alpha, rho, level, lsq=lsq)
+    ref = ora.cascade(_np(m)[..., :P].astype(np.float64))
+    assert rel_l2(a, ref) < 2e-6
+    # per channel too (channels are independent convolutions)
+    for c in range(C):
+        assert rel_l2(a[..., c, :], ref[..., c, :]) < 2e-6

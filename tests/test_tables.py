@@ -132,3 +132,38 @@ def test_taylor_tables_zeroth_column():
 def test_polynomial_kernel_fit_exact():
     tabs = fit_m2l_tables(KernelModel("gaussian", 1e-4, 4), 4, lsq=True, check=False)
     assert tabs["near"].fit_residual < 1e-12
+
+
+@pytest.mark.parametrize("alpha,rho,level,lsq", [(200.0, 4, 4, True), (1000.0, 4, 5, True),
+                                                 (1000.0, 4, 5, False), (200.0, 3, 4, True),
+                                                 (50.0, 2, 3, True), (4000.0, 6, 6, False),
+                                                 (300.0, 1, 4, True)])
+def test_separable_factors_reproduce_finest_tables(alpha, rho, level, lsq):
+    """kernel.separable_factors: post_S (K(o_x) (x) K(o_y) (x) K(o_z))_S pre_S
+    equals every active finest far and near table (float64).  The LSQ
+    residual (~5e-8) is the reference pinv's own conditioning (cond V up to
+    4.6e9 at level 5); Taylor tables factor exactly."""
+    from paper_2111_00110_b200.kernel import separable_dense, separable_factors
+    k = KernelModel("gaussian", alpha, rho)
+    tabs = fit_m2l_tables(k, level, lsq=lsq, check=False, device=False)
+    f = separable_factors(k, level, lsq)
+    tol = 2e-7 if lsq else 1e-14
+    for t in (tabs["far"][level], tabs["near"]):
+        for i in np.flatnonzero(t.active):
+            d = separable_dense(f, k.table, t.offsets[i])
+            assert np.abs(d - t.coeffs[i]).max() <= tol * np.abs(t.coeffs[i]).max()
+
+
+def test_separable_eligibility():
+    """The separable path needs the full 6^3 finest box (every stencil offset
+    active), a >= 32-cell grid and a full-rank per-axis LSQ fit."""
+    from paper_2111_00110_b200.kernel import separable_eligible
+    t = fit_m2l_tables(KernelModel("gaussian", 1000.0, 4), 5, check=False, device=False)
+    assert separable_eligible(t, 5, 4)
+    assert not separable_eligible(t, 5, 6)                     # rank-deficient LSQ at 6 nodes
+    assert separable_eligible(t, 5, 6, lsq=False)
+    t3 = fit_m2l_tables(KernelModel("gaussian", 50.0, 2), 3, check=False, device=False)
+    assert not separable_eligible(t3, 3, 2)                    # 16-cell grid
+    pruned = fit_m2l_tables(KernelModel("gaussian", 12000.0, 2), 4, check=False, device=False)
+    assert not pruned["far"][4].active[~pruned["far"][4].hole].all()
+    assert not separable_eligible(pruned, 4, 2)
