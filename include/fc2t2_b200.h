@@ -189,6 +189,11 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
 int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d_q, int64_t n,
               int mode, const int32_t* d_order, const float* d_wts, float* d_value,
               float* d_grad, float* d_hess, float* d_wgrad, int32_t* d_flag, void* stream);
+/* q_bar recycling (explicit_jvp, ref layers.py:183): d_out (n, 3) =
+ * sum_c d_w[n, c] * d_grad[n, c, :] from the gradient a VALUE | GRAD L2P
+ * stored in the forward -- bit-identical to an FC2T2_L2P_WGRAD launch. */
+int fc2t2_weighted_grad(const float* d_grad, const float* d_w, int64_t n, int channels,
+                        float* d_out, void* stream);
 
 /* ---- rays: traversal (ray.py:101-157), layers (layers.py:193-402) ----
  * Rays are (R, 3) float64 origins / directions on the device.  Traversal:

@@ -938,6 +938,13 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
   return FC2T2_OK;
 }
 
+int fc2t2_weighted_grad(const float* d_grad, const float* d_w, int64_t n, int channels,
+                        float* d_out, void* stream) {
+  if (n < 0 || channels < 1) return fail(FC2T2_EVALUE, "bad weighted_grad arguments");
+  return cuda_status(fc2t2::weighted_grad(d_grad, d_w, n, channels, d_out, (cudaStream_t)stream),
+                     "weighted_grad");
+}
+
 int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d_q, int64_t n,
               int mode, const int32_t* d_order, const float* d_wts, float* d_value,
               float* d_grad, float* d_hess, float* d_wgrad, int32_t* d_flag, void* stream) {

@@ -101,6 +101,9 @@ enum L2PMode : int {
   L2P_WGRAD = 8,   // (n, 3) = sum_c wts[n, c] * grad f_c
   L2P_PRESORTED = 16,  // q / wts given in `order` sequence; outputs by point
 };
+// out (n, 3) = sum_c w (n, C) * grad (n, C, 3): L2P_WGRAD from stored gradients
+cudaError_t weighted_grad(const float* grad, const float* w, int64_t n, int C, float* out,
+                          cudaStream_t s);
 cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64_t n, int mode,
                 const int32_t* order, const float* wts, float* value, float* grad, float* hess,
                 float* wgrad, int32_t* flag, cudaStream_t s);

@@ -239,7 +239,35 @@ cudaError_t l2p_rho(int level, int C, const float* L, const float* q, int64_t n,
 #undef FC2T2_L2P_CASE
 }
 
+// out[i] = sum_c w[i, c] grad[i, c, :], the same fmaf sequence as L2P_WGRAD
+__global__ void __launch_bounds__(256)
+weighted_grad_kernel(const float* __restrict__ grad, const float* __restrict__ w, int64_t n,
+                     int C, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float wg0 = 0.f, wg1 = 0.f, wg2 = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float wv = w[i * C + c];
+      const float* g = grad + (i * C + c) * 3;
+      wg0 = fmaf(wv, g[0], wg0);
+      wg1 = fmaf(wv, g[1], wg1);
+      wg2 = fmaf(wv, g[2], wg2);
+    }
+    out[3 * i + 0] = wg0;
+    out[3 * i + 1] = wg1;
+    out[3 * i + 2] = wg2;
+  }
+}
+
 }  // namespace
+
+cudaError_t weighted_grad(const float* grad, const float* w, int64_t n, int C, float* out,
+                          cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  FC2T2_LAUNCH("wgrad_recycle", s,
+               weighted_grad_kernel<<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(grad, w, n, C, out));
+  return cudaGetLastError();
+}
 
 cudaError_t l2p(int rho, int level, int C, const float* L, const float* q, int64_t n, int mode,
                 const int32_t* order, const float* wts, float* value, float* grad, float* hess,

@@ -686,15 +686,18 @@ class Accessor:
         return self._flag
 
     def eval_device(self, q: torch.Tensor, mode: int, wts: torch.Tensor | None = None,
-                    order: torch.Tensor | None = None):
+                    order: torch.Tensor | None = None, outs: dict | None = None):
         """One L2P launch; returns dict of the requested device outputs.  With a
         cell-sorted ``order`` the points are evaluated in that order (L1 reuse
-        of the cell rows); outputs stay indexed by point."""
+        of the cell rows); outputs stay indexed by point.  ``outs`` may supply
+        contiguous output tensors (e.g. row slices of a larger buffer)."""
         n, C = int(q.shape[0]), self.channels
         dev = q.device
         out = {}
+        outs = outs or {}
         value = torch.empty((n, C), dtype=torch.float32, device=dev) if mode & _lib.L2P_VALUE else None
-        grad = torch.empty((n, C, 3), dtype=torch.float32, device=dev) if mode & _lib.L2P_GRAD else None
+        grad = (outs.get("grad") if "grad" in outs else
+                torch.empty((n, C, 3), dtype=torch.float32, device=dev)) if mode & _lib.L2P_GRAD else None
         hess = torch.empty((n, C, 6), dtype=torch.float32, device=dev) if mode & _lib.L2P_HESS else None
         wgrad = torch.empty((n, 3), dtype=torch.float32, device=dev) if mode & _lib.L2P_WGRAD else None
         st = self.grid.storage if self.grid.storage.is_contiguous() else self.grid.storage.contiguous()

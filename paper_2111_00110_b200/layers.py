@@ -51,6 +51,23 @@ class ExplicitResult:
     engine: Engine
     q_dev: torch.Tensor = None
     sorts: tuple = None      # ((p order, p cell_start), (q order, q cell_start))
+    q_grad: torch.Tensor = None   # (M, C, 3) grad f at q, stored for the backward
+
+
+# q_bar recycling ("expansion recycling"): the forward L2P at q
+# also returns grad f(q) -- the same cell-row gather, 12 B more per point and
+# channel written -- so explicit_jvp forms q_bar = sum_c y_bar_c grad f_c
+# (fc2t2_weighted_grad, bit-identical to the L2P_WGRAD pass it replaces)
+# instead of gathering every query's cell row a second time.
+# FC2T2_NO_RECYCLE=1 restores the second L2P pass.
+RECYCLE_QUERY_GRAD = os.environ.get("FC2T2_NO_RECYCLE", "0") != "1"
+
+
+def _weighted_grad(grad: torch.Tensor, wts: torch.Tensor) -> torch.Tensor:
+    n, C = int(grad.shape[0]), int(grad.shape[1])
+    out = torch.empty((n, 3), dtype=torch.float32, device=grad.device)
+    _lib.call("fc2t2_weighted_grad", _ptr(grad), _ptr(wts.contiguous()), n, C, _ptr(out), _stream())
+    return out
 
 
 # Cell-coherent L2P (points evaluated in cell-sorted order so neighbouring
@@ -110,11 +127,18 @@ def _explicit_forward_host(engine: Engine, sources: SourceSet, q) -> ExplicitRes
     cs = torch.cuda.current_stream()
     coherent = _beyond_coherent(acc.grid.storage.numel() * 4)
     out = torch.empty((qd.shape[0], acc.channels), dtype=torch.float32, pin_memory=True)
+    q_grad = None
     if not coherent:
+        mode = _lib.L2P_VALUE
+        if RECYCLE_QUERY_GRAD:
+            q_grad = torch.empty((qd.shape[0], acc.channels, 3), dtype=torch.float32,
+                                 device=qd.device)
+            mode |= _lib.L2P_GRAD
         for a, b, ev in chunks:
             cs.wait_event(ev)
             if b > a:
-                HostIO.d2h(acc.eval_device(qd[a:b], _lib.L2P_VALUE)["value"], out[a:b])
+                o = {"grad": q_grad[a:b]} if q_grad is not None else None
+                HostIO.d2h(acc.eval_device(qd[a:b], mode, outs=o)["value"], out[a:b])
         q_sort = None      # sorted lazily by the backward (hidden under the y_bar upload)
     else:
         cs.wait_event(chunks[-1][2])
@@ -123,7 +147,7 @@ def _explicit_forward_host(engine: Engine, sources: SourceSet, q) -> ExplicitRes
     HostIO.finish()
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine, q_dev=qd,
-                          sorts=(p_sort, q_sort))
+                          sorts=(p_sort, q_sort), q_grad=q_grad)
 
 
 def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
@@ -148,8 +172,11 @@ def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
         for a, b, ev in chunks:
             cs.wait_event(ev)
             if b > a:
-                HostIO.d2h(acc.eval_device(qd[a:b], _lib.L2P_WGRAD, wts=yb[a:b])["wgrad"],
-                           q_bar[a:b])
+                if res.q_grad is not None:
+                    qb = _weighted_grad(res.q_grad[a:b], yb[a:b])
+                else:
+                    qb = acc.eval_device(qd[a:b], _lib.L2P_WGRAD, wts=yb[a:b])["wgrad"]
+                HostIO.d2h(qb, q_bar[a:b])
     else:
         cs.wait_event(chunks[-1][2])
         if aux is not None:
@@ -180,10 +207,12 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
         engine.flag.check_points(qd)    # the L2P at q would only see q at the very end
     checked = engine.flag.mark()
     acc = engine.expand_device(sources.p, sources.w, p_sort)
-    vals = _l2p(acc, qd, _lib.L2P_VALUE, q_sort)["value"]
+    recycle = RECYCLE_QUERY_GRAD and q_sort is None
+    r = _l2p(acc, qd, _lib.L2P_VALUE | (_lib.L2P_GRAD if recycle else 0), q_sort)
     engine.flag.raise_if_set("source/query", checked)
-    return ExplicitResult(values=like_input(vals, q), accessor=acc, q=q, sources=sources,
-                          engine=engine, q_dev=qd, sorts=(p_sort, q_sort))
+    return ExplicitResult(values=like_input(r["value"], q), accessor=acc, q=q, sources=sources,
+                          engine=engine, q_dev=qd, sorts=(p_sort, q_sort),
+                          q_grad=r["grad"] if recycle else None)
 
 
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
@@ -195,7 +224,10 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     p_sort, q_sort = _sorts(res)
     checked = eng.flag.mark()           # the sorts re-checked p and q
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    q_bar = _l2p(res.accessor, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"]
+    if res.q_grad is not None:
+        q_bar = _weighted_grad(res.q_grad, yb)
+    else:
+        q_bar = _l2p(res.accessor, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"]
     back = eng.expand_device(qd, yb, q_sort)
     out = _l2p(back, src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, p_sort, wts=src.w)
     eng.flag.raise_if_set("source/query", checked)

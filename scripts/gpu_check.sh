@@ -1,7 +1,5 @@
 # GPU tests + L2P diag + full bench (no CPU baseline)
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-LEVEL=5 RHO=4 M=10000000 timeout 300 python scripts/diag_l2p.py 2>&1 | tail -2
-LEVEL=6 RHO=6 timeout 300 python scripts/diag_l2p.py 2>&1 | tail -2
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/check.json 2>gpurun_out/check.err; echo bench rc=$?
 python - <<'PY'
 import json;d=json.load(open('gpurun_out/check.json'))

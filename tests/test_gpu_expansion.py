@@ -532,3 +532,30 @@ def test_separable_finest_m2l_matches_dense_and_oracle(cuda, alpha, rho, level, 
     # per channel too (channels are independent convolutions)
     for c in range(C):
         assert rel_l2(a[..., c, :], ref[..., c, :]) < 2e-6
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_query_gradient_recycling_is_bit_identical(eng4, monkeypatch, host):
+    """explicit_forward stores grad f(q) from its VALUE | GRAD L2P and
+    explicit_jvp forms q_bar with fc2t2_weighted_grad: every output equals the
+    second-L2P_WGRAD-pass path bit for bit (device and chunked host paths)."""
+    import paper_2111_00110_b200.layers as layers
+    from paper_2111_00110_b200 import SourceSet
+    rng = np.random.default_rng(12)
+    p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32))
+    w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32))
+    q = torch.from_numpy(rng.uniform(-1, 1, (7001, 3)).astype(np.float32))
+    yb = torch.from_numpy(rng.normal(size=(7001, 2)).astype(np.float32))
+    outs = []
+    for recycle in (True, False):
+        monkeypatch.setattr(layers, "RECYCLE_QUERY_GRAD", recycle)
+        if host:
+            r = layers.explicit_forward(eng4, SourceSet(p.pin_memory(), w.pin_memory()), q.pin_memory())
+            g = layers.explicit_jvp(yb.pin_memory(), r)
+        else:
+            r = layers.explicit_forward(eng4, SourceSet(p.cuda(), w.cuda()), q.cuda())
+            g = layers.explicit_jvp(yb.cuda(), r)
+        assert (r.q_grad is not None) == recycle
+        outs.append((r.values, g.w_bar, g.p_bar, g.q_bar))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
