@@ -205,6 +205,86 @@ def seeded_direction(rng):
             return u
 
 
+# Algorithmic bytes per config-2 step, per stage; C = 1.
+# Two expansions per step: the forward of (p, w) and the backward of (q, y_bar).
+STAGE_GROUPS = {
+    "l2p": ["l2p"],
+    "p2m": ["p2m"],
+    "cell_sort": ["cell_keys", "scan", "sort_place", "sort_segments"],
+    "m2l_finest": ["m2l_sep_pre", "m2l_sep_z", "m2l_sep_y", "m2l_sep_x", "m2l_sep_post"],
+    "m2l_finest_dense": ["m2l_absmax", "m2l_split", "m2l_tc_L5"],
+    "l2l": ["l2l"],
+    "m2m": ["m2m"],
+    "wgrad_recycle": ["wgrad_recycle"],
+}
+
+
+def stage_rooflines(eng, prof, steps, N, M, hbm_peak):
+    """{stage: bytes per step (the 8(d) model), ms per step, achieved GB/s,
+    fraction of the HBM peak}.  Times are the library's per-launch CUDA events
+    on each launch's stream (the finest M2L overlaps the coarse levels, so
+    coarse-stage times include SM sharing)."""
+    P, PP, L = eng.P, eng.PP, eng.levels
+    R = (2 ** (L + 1)) ** 3
+    R1 = eng.rho + 1
+    T = R1 * (R1 + 1) // 2 * R1
+    grid = 4 * PP * R
+    model = {
+        "l2p": (M * (12 + 4 + 12) + grid + N * (12 + 4 + 4 + 12) + grid,
+                "q: 12 B in + 4 B value + 12 B grad; p: 12 B + 4 B w + 4 B w_bar + 12 B p_bar; "
+                "+ one finest L grid read per launch"),
+        "p2m": ((N + M) * (12 + 4) + 2 * grid, "12 B point + 4 B weight per point + grid write"),
+        "cell_sort": ((N + M) * (12 + 4) + 2 * 4 * (R + 1),
+                      "12 B point in + 4 B order out per point + cell starts"),
+        "m2l_finest": (2 * 4 * R * (2 * PP + 4 * P + 4 * T),
+                       "per expansion each intermediate read + written once: M rows -> M' -> Z "
+                       "-> Y -> X -> L rows, 4 R (2 PP + 4 P + 4 T) B"),
+        "m2l_finest_dense": (2 * 2 * grid, "per expansion M read + L write"),
+        "l2l": (2 * sum(4 * PP * ((2 ** (l + 1)) ** 3 * 2 + (2 ** l) ** 3)
+                        for l in range(3, L)), "fine read+write + coarse read per level"),
+        "m2m": (2 * sum(4 * PP * ((2 ** (l + 1)) ** 3 + (2 ** l) ** 3) for l in range(3, L + 1)),
+                "fine read + coarse write per level"),
+        "wgrad_recycle": (M * (12 + 4 + 12), "12 B grad + 4 B y_bar in, 12 B q_bar out"),
+    }
+    out = {}
+    for st, names in STAGE_GROUPS.items():
+        hit = [n for n in names if n in prof]
+        if not hit:
+            continue
+        ms = sum(prof[n][0] for n in hit) / steps
+        launches = sum(prof[n][1] for n in hit) / steps
+        b, how = model[st]
+        gbps = b / (ms / 1000.0) / 1e9
+        out[st] = {"kernels": hit, "ms_per_step": round(ms, 4), "launches_per_step": launches,
+                   "bytes_per_step": b, "achieved_gbps": round(gbps, 1),
+                   "frac": round(gbps / hbm_peak, 4), "model": how}
+    if "l2p" in out:
+        # the cell-row gathers are L2 traffic: 5 sectors (160 B) per point and channel
+        sect = (M + N) * 160
+        o = out["l2p"]
+        o["l2_sector_bytes_per_step"] = sect
+        o["l2_tbps"] = round(sect / (o["ms_per_step"] / 1000.0) / 1e12, 2)
+        o["l2_note"] = ("each point gathers its 144-byte cell row = 5 L2 sectors; the 37.7 MB "
+                        "level-5 grid is L2 resident, so the binding resource is the L2 slice "
+                        "throughput (~6300 B/clk chip-wide, B300_MICROARCH.md)")
+    return out
+
+
+def measured_traffic(kernels):
+    """DRAM bytes per step of these kernels from the committed ncu --set full
+    capture (profiles/traffic.json, written by scripts/ncu_traffic.py), or None."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+    except Exception:
+        return None
+    tot, hit = 0.0, False
+    for k in kernels:
+        if k in t.get("bytes_per_step", {}):
+            tot += t["bytes_per_step"][k]
+            hit = True
+    return {"bytes_per_step": tot, "source": t.get("source")} if hit else None
+
+
 def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None = None):
     """(total device ms over `steps`, last result): per-step CUDA events on the
     launching stream, L2 flush between steps outside the events.  With
@@ -649,24 +729,47 @@ def run_ours(args, rank: int, world: int) -> None:
     if rank != 0:
         return
 
-    # ---- roofline of the dominant kernel (finest-level M2L: far + near)
-    key = next((k for k in (f"m2l_tc_L{CFG['levels']}", f"m2l_L{CFG['levels']}") if k in prof),
-               None)
-    k_ms, k_n = prof.get(key, (float("nan"), 1))
-    pairs = m2l_pairs(eng.m2l_tables["far"][CFG["levels"]]) + m2l_pairs(eng.m2l_tables["near"])
-    flops_launch = pairs * 1 * eng.P * eng.P * 2
-    achieved = flops_launch / (k_ms / k_n / 1000.0) / 1e12
-    issued = float(_lib.lib().fc2t2_m2l_issued_flops(eng.handle, 1, CFG["levels"],
-                                                     _lib.TABLE_FARNEAR))
-    issued_tf = issued / (k_ms / k_n / 1000.0) / 1e12
+    # ---- rooflines: every stage against the bound SURVEY 8(d) gives it
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
     except Exception:
         pass
+    hbm_peak = float(peaks.get("hbm_gbs", 7672.0))
+    hbm_src = ("measured HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks
+               else "fallback (B200_PROFILING.md)")
     peak = float(peaks.get("bf16_tflops", 1590.0))
     peak_src = "measured bf16 dense (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks else \
         "fallback 1.59 PF (B200_PROFILING.md)"
+    rl_stages = stage_rooflines(eng, prof, args.steps, N, M, hbm_peak)
+    dom = max(rl_stages, key=lambda k: rl_stages[k]["ms_per_step"])
+    d = rl_stages[dom]
+    traffic = measured_traffic(d["kernels"])
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbps"], "peak": hbm_peak,
+                "unit": "GB/s", "frac": d["frac"],
+                "traffic": (traffic["bytes_per_step"] if traffic else None),
+                "traffic_source": (traffic["source"] if traffic else None),
+                "peak_source": hbm_src, "bytes_per_step": d["bytes_per_step"],
+                "launch_ms": d["ms_per_step"] / max(d["launches_per_step"], 1),
+                "launches_per_step": d["launches_per_step"], "bytes_model": d["model"]}
+    if "l2_sector_bytes_per_step" in d:
+        roofline["l2_sector_bytes_per_step"] = d["l2_sector_bytes_per_step"]
+        roofline["l2_tbps"] = d["l2_tbps"]
+        roofline["l2_note"] = d["l2_note"]
+    # the finest-level M2L against the reference's own FLOP count (8(a) a8)
+    m2l_keys = [k for k in prof if k.startswith("m2l_sep_") or k == f"m2l_tc_L{CFG['levels']}"]
+    m2l_ms = sum(prof[k][0] for k in m2l_keys) / args.steps
+    pairs = m2l_pairs(eng.m2l_tables["far"][CFG["levels"]]) + m2l_pairs(eng.m2l_tables["near"])
+    flops_exp = pairs * 1 * eng.P * eng.P * 2
+    m2l_line = {"kernels": sorted(m2l_keys), "ms_per_step": m2l_ms,
+                "reference_flops_per_expansion": flops_exp,
+                "reference_flop_rate_tflops": 2 * flops_exp / (m2l_ms / 1000.0) / 1e12,
+                "vs_bf16_peak": 2 * flops_exp / (m2l_ms / 1000.0) / 1e12 / peak,
+                "peak_source": peak_src,
+                "algorithm": ("separable: per-axis transforms + three 1-D convolutions "
+                              "(FFMA, memory bound -- see roofline_stages.m2l_finest)"
+                              if eng.separable else
+                              "dense tcgen05 kind::f16 two-term split")}
     stages = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items())}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -679,20 +782,9 @@ def run_ours(args, rank: int, world: int) -> None:
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
-        "roofline": {"kernel": key, "bound": "tensor", "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src,
-                     "flops_per_launch": flops_launch, "launch_ms": k_ms / k_n,
-                     "precision": "two-term fp16 split with power-of-two operand scaling "
-                                  "(tcgen05 kind::f16, 3 products, ~22-bit), fp32 accumulate",
-                     "issued_flops_per_launch": issued,
-                     "issued_tflops": issued_tf,
-                     "frac_issued": issued_tf / peak,
-                     "issued_note": "tensor FLOPs the kernel issues (split cross products and "
-                                    "K/N padding included) vs the same peak: pipe utilisation; "
-                                    "achieved/frac count only the reference's algorithmic FLOPs",
-                     "fp32_ffma_nominal_tflops": 74.4,
-                     "frac_of_fp32_ffma_nominal": achieved / 74.4},
+        "roofline": roofline,
+        "roofline_stages": rl_stages,
+        "m2l_finest_vs_reference_flops": m2l_line,
         "stages_ms_per_step": stages,
         "graphed": graphed,
         "table_fit_s": t_tables,

@@ -487,6 +487,13 @@ class Engine:
             self.flag = DomainFlag()
         return self._h.h
 
+    def aux_stream(self) -> torch.cuda.Stream:
+        """A second stream for work that only depends on a layer's inputs
+        (the query sort the backward needs, started by the forward)."""
+        if getattr(self, "_aux", None) is None:
+            self._aux = torch.cuda.Stream(device=_device())
+        return self._aux
+
     def interaction_list(self, level: int, table: int = _lib.TABLE_FAR):
         """Device interaction list of one level: (entries (n,4) {dx,dy,dz,slot},
         class starts (ncls+1,)) -- exposed for the bit-exactness tests."""

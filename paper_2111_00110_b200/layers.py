@@ -52,6 +52,7 @@ class ExplicitResult:
     q_dev: torch.Tensor = None
     sorts: tuple = None      # ((p order, p cell_start), (q order, q cell_start))
     q_grad: torch.Tensor = None   # (M, C, 3) grad f at q, stored for the backward
+    q_sort_ready: object = None   # event after the aux-stream query sort
 
 
 # q_bar recycling ("expansion recycling"): the forward L2P at q
@@ -85,12 +86,38 @@ def _beyond_coherent(nbytes: int) -> bool:
 
 def _sorts(res: "ExplicitResult"):
     """(p sort, q sort) of an explicit result; the query sort is computed on
-    first use (the forward skips it unless its L2P needs the coherent order)."""
+    first use unless the forward started it on the engine's aux stream, in
+    which case the current stream joins it here."""
     p_sort, q_sort = res.sorts
     if q_sort is None:
         q_sort = res.engine.sort_points(res.q_dev)
         res.sorts = (p_sort, q_sort)
+    elif res.q_sort_ready is not None:
+        torch.cuda.current_stream().wait_event(res.q_sort_ready)
+        res.q_sort_ready = None
     return p_sort, q_sort
+
+
+# The backward's P2M of (q, y_bar) needs the cell sort of q, which depends on
+# q alone: the device forward starts it on the engine's aux stream, where it
+# overlaps the forward cascade and L2P (atomic/scatter-bound sort kernels
+# beside bandwidth/latency-bound cascade kernels), and explicit_jvp joins it.
+# FC2T2_NO_EARLY_QSORT=1 sorts in the backward instead.
+EARLY_QUERY_SORT = os.environ.get("FC2T2_NO_EARLY_QSORT", "0") != "1"
+
+
+def _early_sort(engine: Engine, qd: torch.Tensor):
+    """(CellSort, ready event) of qd sorted on the engine's aux stream."""
+    cs = torch.cuda.current_stream()
+    aux = engine.aux_stream()
+    aux.wait_stream(cs)
+    with torch.cuda.stream(aux):
+        srt = engine.sort_points(qd)
+        ready = torch.cuda.Event()
+        ready.record(aux)
+    for t in srt:
+        t.record_stream(cs)
+    return srt, ready
 
 
 def _coherent(acc: Accessor, sort):
@@ -202,17 +229,20 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     qd = to_device(q, 3, points=True)
     p_sort = engine.sort_points(sources.p)
     coherent = _beyond_coherent(engine.finest_grid_bytes(sources.channels))
-    q_sort = engine.sort_points(qd) if coherent else None   # else sorted by the backward
+    q_sort = engine.sort_points(qd) if coherent else None   # else sorted for the backward
+    ready = None
     if q_sort is None:
         engine.flag.check_points(qd)    # the L2P at q would only see q at the very end
     checked = engine.flag.mark()
+    if q_sort is None and EARLY_QUERY_SORT:
+        q_sort, ready = _early_sort(engine, qd)
     acc = engine.expand_device(sources.p, sources.w, p_sort)
-    recycle = RECYCLE_QUERY_GRAD and q_sort is None
+    recycle = RECYCLE_QUERY_GRAD and not coherent
     r = _l2p(acc, qd, _lib.L2P_VALUE | (_lib.L2P_GRAD if recycle else 0), q_sort)
     engine.flag.raise_if_set("source/query", checked)
     return ExplicitResult(values=like_input(r["value"], q), accessor=acc, q=q, sources=sources,
                           engine=engine, q_dev=qd, sorts=(p_sort, q_sort),
-                          q_grad=r["grad"] if recycle else None)
+                          q_grad=r["grad"] if recycle else None, q_sort_ready=ready)
 
 
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
