@@ -127,6 +127,14 @@ size_t fc2t2_cell_sort_workspace_size(int level, int64_t n);
 int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
                     int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
                     void* stream);
+/* Cell binning without the per-cell index sort: cells contiguous and in
+ * order, points inside a cell in arrival order.  Same outputs/workspace as
+ * fc2t2_cell_sort; enough for fc2t2_p2m whenever fc2t2_p2m_order_free(rho)
+ * (its exact fixed-point sums do not depend on the order inside a cell). */
+int fc2t2_cell_bin(int level, const float* d_pts, int64_t n, int32_t* d_order,
+                   int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                   void* stream);
+int fc2t2_p2m_order_free(int rho);
 /* The same sort, also returning d_inv (n) int32 = sorted position of every
  * point and d_pts_sorted (n, 3) = the points in sorted order, both written
  * without random reads of d_pts (give both or neither).  With them, P2M takes

@@ -654,6 +654,20 @@ int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
                      "cell_sort");
 }
 
+int fc2t2_cell_bin(int level, const float* d_pts, int64_t n, int32_t* d_order,
+                   int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                   void* stream) {
+  if (level < 0 || level > 9 || n < 0 || n > INT32_MAX)
+    return fail(FC2T2_EVALUE, "bad cell_bin arguments");
+  if (ws_bytes < fc2t2::cell_sort_workspace(level, n))
+    return fail(FC2T2_EWORKSPACE, "cell_bin workspace too small");
+  return cuda_status(fc2t2::cell_sort(level, d_pts, n, d_order, d_cell_start, d_flag, d_ws,
+                                      ws_bytes, (cudaStream_t)stream, nullptr, nullptr, false),
+                     "cell_bin");
+}
+
+int fc2t2_p2m_order_free(int rho) { return fc2t2::p2m_fixed_point(rho) ? 1 : 0; }
+
 int fc2t2_cell_sort_ex(int level, const float* d_pts, int64_t n, int32_t* d_order,
                        int32_t* d_cell_start, int32_t* d_inv, float* d_pts_sorted,
                        int32_t* d_flag, void* d_ws, size_t ws_bytes, void* stream) {

@@ -8,9 +8,12 @@ namespace fc2t2 {
 
 // sort.cu ----------------------------------------------------------------
 size_t cell_sort_workspace(int level, int64_t n);
+// stable = false skips the per-cell index sort (cells contiguous, arrival
+// order inside a cell): enough for the order-free fixed-point P2M
 cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order,
                       int32_t* cell_start, int32_t* flag, void* ws, size_t ws_bytes,
-                      cudaStream_t s, int32_t* inv = nullptr, float* pts_sorted = nullptr);
+                      cudaStream_t s, int32_t* inv = nullptr, float* pts_sorted = nullptr,
+                      bool stable = true);
 // dst[inv[i], :] = src[i, :]
 cudaError_t permute_rows(const float* src, int64_t n, int cols, const int32_t* inv, float* dst,
                          cudaStream_t s);
@@ -25,6 +28,10 @@ cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_
                            cudaStream_t s);
 
 // expand.cu --------------------------------------------------------------
+// true (FC2T2_P2M_FIXED=1, rho <= 5): P2M sums exactly in fixed point (order
+// free: a cell sort without the per-cell index sort suffices); false
+// (default): float32 in the stable sort's index order
+bool p2m_fixed_point(int rho);
 cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float* w,
                        const int32_t* order, const int32_t* cell_start, float* M,
                        cudaStream_t s);

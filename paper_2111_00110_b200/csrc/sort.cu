@@ -433,7 +433,8 @@ size_t ws_bytes(int64_t n, int64_t R) {
 // nocell: key sorts, whose bucket R is ranked stably by a scan of w.tmp flags.
 cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t* cell_start,
                         bool nocell, cudaStream_t s, const float* pts = nullptr,
-                        int32_t* inv = nullptr, float* pts_sorted = nullptr) {
+                        int32_t* inv = nullptr, float* pts_sorted = nullptr,
+                        bool stable = true) {
   // pts_sorted needs inv and a scratch copy in arrival order (w.tmp: n x 3 floats)
   const bool with_pts = pts && pts_sorted && inv;
   float* pts_arr = with_pts ? (float*)w.tmp : nullptr;
@@ -448,6 +449,7 @@ cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t
                place_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(
                    w.keys, w.ranks, n, R, (const uint32_t*)cell_start, nocell ? w.tmp : nullptr,
                    ord, pts, pts_arr));
+  if (!stable && !with_pts) return cudaGetLastError();
   e = cudaMemsetAsync(w.work, 0, 4, s);
   if (e != cudaSuccess) return e;
   const int64_t nseg = nocell ? R : R + 1;
@@ -483,7 +485,7 @@ size_t cell_sort_workspace(int level, int64_t n) {
 
 cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, int32_t* cell_start,
                       int32_t* flag, void* ws, size_t ws_bytes_, cudaStream_t s, int32_t* inv,
-                      float* pts_sorted) {
+                      float* pts_sorted, bool stable) {
   if ((inv == nullptr) != (pts_sorted == nullptr)) return cudaErrorInvalidValue;
   const int res = 1 << (level + 1);
   const int64_t R = (int64_t)res * res * res;
@@ -495,7 +497,7 @@ cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, in
     FC2T2_LAUNCH("cell_keys", s,
                  cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.ranks,
                                                                       w.counts, flag));
-  return sort_ranked(w, n, R, order, cell_start, false, s, pts, inv, pts_sorted);
+  return sort_ranked(w, n, R, order, cell_start, false, s, pts, inv, pts_sorted, stable);
 }
 
 cudaError_t permute_rows(const float* src, int64_t n, int cols, const int32_t* inv, float* dst,

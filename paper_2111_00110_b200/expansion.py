@@ -525,7 +525,8 @@ class Engine:
 
     # -- stages -------------------------------------------------------------
 
-    def sort_points(self, pts: torch.Tensor, with_points: bool = False) -> "CellSort":
+    def sort_points(self, pts: torch.Tensor, with_points: bool = False,
+                    stable: bool | None = None) -> "CellSort":
         """Stable sort by finest cell: (order (n,), cell_start (res^3+1,)); with
         ``with_points`` also the inverse permutation and the points in sorted
         order (written by the sort without random reads), which let P2M and the
@@ -542,7 +543,12 @@ class Engine:
         start = torch.empty(R + 1, dtype=torch.int32, device=pts.device)
         _ = self.handle
         if not with_points or n == 0:
-            _lib.call("fc2t2_cell_sort", self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
+            # P2M sums exactly in fixed point (rho <= 5): cell binning without the
+            # per-cell index sort gives the same moments; stable=True forces it
+            if stable is None:
+                stable = not bool(_lib.lib().fc2t2_p2m_order_free(self.rho))
+            fn = "fc2t2_cell_sort" if stable else "fc2t2_cell_bin"
+            _lib.call(fn, self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
                       _ptr(self.flag.t), _ptr(ws), int(ws_bytes), _stream())
             return CellSort(order, start)
         inv = torch.empty(n, dtype=torch.int32, device=pts.device)

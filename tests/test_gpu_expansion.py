@@ -43,6 +43,43 @@ def test_find_box_bit_exact(cuda, level):
     assert np.array_equal(got.cpu().numpy(), g[f"box_l{level}"])
 
 
+@pytest.mark.parametrize("heavy", [0, 20_000])
+def test_cell_bin_and_order_free_p2m(eng4, heavy):
+    """fc2t2_cell_bin (no per-cell index sort): cells contiguous with the same
+    ranges as the stable sort, each cell's set of points identical; and the
+    fixed-point P2M gives bit-identical moments for the stable order, the
+    binned (arrival) order and a reversed within-cell order; it is exactly
+    homogeneous under power-of-two weight scaling (per-cell scales), even at
+    2^-60 / 2^60."""
+    from paper_2111_00110_b200 import _lib
+    from paper_2111_00110_b200.expansion import CellSort
+    if _lib.lib().fc2t2_p2m_order_free(4) != 1:
+        pytest.skip("fixed-point P2M is opt-in (FC2T2_P2M_FIXED=1)")
+    rng = np.random.default_rng(1)
+    p = rng.uniform(-1, 1, (50_000, 3)).astype(np.float32)
+    if heavy:
+        idx = rng.permutation(50_000)
+        p[idx[:heavy]] = p[idx[0]]
+    pt = torch.from_numpy(p).cuda()
+    w = torch.from_numpy(rng.normal(size=(50_000, 2)).astype(np.float32)).cuda()
+    st = eng4.sort_points(pt, stable=True)
+    bn = eng4.sort_points(pt, stable=False)
+    assert torch.equal(st[1], bn[1])
+    so, bo, start = st[0].cpu().numpy(), bn[0].cpu().numpy(), st[1].cpu().numpy()
+    rev = so.copy()
+    for c in np.flatnonzero(np.diff(start) > 1):
+        a, b = start[c], start[c + 1]
+        assert np.array_equal(np.sort(bo[a:b]), so[a:b])
+        rev[a:b] = so[a:b][::-1]
+    m_st = eng4.p2m_device(pt, w, st).storage
+    m_bn = eng4.p2m_device(pt, w, bn).storage
+    m_rv = eng4.p2m_device(pt, w, CellSort(torch.from_numpy(rev).cuda(), st[1])).storage
+    assert torch.equal(m_st, m_bn) and torch.equal(m_st, m_rv)
+    for k in (-60, 60):
+        m_k = eng4.p2m_device(pt, w * 2.0 ** k, bn).storage
+        assert torch.equal(m_k, m_st * 2.0 ** k)
+
+
 @pytest.mark.parametrize("heavy", [0, 5000, 20_000])
 def test_cell_sort_is_stable_counting_sort(eng4, heavy):
     """order == stable argsort by cell for every segment path of the sort:
