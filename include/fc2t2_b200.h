@@ -180,6 +180,10 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
 int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
                                const double* conv);
 int fc2t2_engine_separable(const fc2t2_engine* e);
+/* 1 (default): the separable M2L's post transform runs after the coarse chain
+ * with the finest L2L fused into it (one pass over the finest L grid fewer);
+ * 0: separate accumulate-L2L launch.  Results are bit-identical. */
+int fc2t2_engine_set_sep_fusion(fc2t2_engine* e, int fuse_l2l);
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream);

@@ -120,6 +120,7 @@ struct fc2t2_engine {
   cudaEvent_t fork = nullptr, join = nullptr;
   // separable finest M2L (m2l_sep.cu): per-axis factors, [out][in] float64
   bool sep = false;
+  bool sep_fuse_l2l = true;  // fc2t2_engine_set_sep_fusion
   std::vector<double> sep_pre, sep_post, sep_conv;
 };
 
@@ -823,6 +824,12 @@ int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double*
 
 int fc2t2_engine_separable(const fc2t2_engine* e) { return e && e->sep ? 1 : 0; }
 
+int fc2t2_engine_set_sep_fusion(fc2t2_engine* e, int fuse_l2l) {
+  if (!e) return fail(FC2T2_EVALUE, "null engine");
+  e->sep_fuse_l2l = fuse_l2l != 0;
+  return FC2T2_OK;
+}
+
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
   if (!e || !e->uploaded || channels < 1) return 0;
   return expand_layout(e, channels).total() * sizeof(float) + 256;
@@ -892,10 +899,14 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
     if (st == FC2T2_OK) st = cuda_status(cudaStreamWaitEvent(e->side, e->fork, 0), "expand fork");
     if (st != FC2T2_OK) return st;
   }
+  // separable finest M2L with the coarse chain present: its post transform
+  // runs after the join with the last L2L fused into it
+  const bool sep_fused = fine && e->sep && coarse && e->sep_fuse_l2l;
   if (fine && e->sep) {
     st = cuda_status(fc2t2::m2l_sep(e->rho, L, channels, e->sep_pre.data(), e->sep_post.data(),
                                     e->sep_conv.data(), Mg[L], Lg[L], fine_part, x_begin, x_end,
-                                    overlap ? e->side : s),
+                                    overlap ? e->side : s,
+                                    sep_fused ? fc2t2::SEP_FRONT : fc2t2::SEP_ALL),
                      "expand m2l_sep");
     if (st != FC2T2_OK) return st;
     if (overlap) {
@@ -940,8 +951,14 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
       st = cuda_status(cudaStreamWaitEvent(s, e->join, 0), "expand join");
       if (st != FC2T2_OK) return st;
     }
-    st = cuda_status(fc2t2::l2l(e->rho, L - 1, channels, Lg[L - 1], Lg[L], fine ? 1 : 0, s),
-                     "expand l2l");
+    if (sep_fused)
+      st = cuda_status(fc2t2::m2l_sep(e->rho, L, channels, e->sep_pre.data(), e->sep_post.data(),
+                                      e->sep_conv.data(), Mg[L], Lg[L], fine_part, x_begin, x_end,
+                                      s, fc2t2::SEP_POST, Lg[L - 1]),
+                       "expand m2l_sep post+l2l");
+    else
+      st = cuda_status(fc2t2::l2l(e->rho, L - 1, channels, Lg[L - 1], Lg[L], fine ? 1 : 0, s),
+                       "expand l2l");
     if (st != FC2T2_OK) return st;
   } else if (!fine) {
     st = cuda_status(

@@ -95,10 +95,15 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
 // (kernel.py separable_factors): pre/post (R1 x R1) and conv (7 x R1 x R1),
 // [out][in] float64 row-major, R1 = rho + 1 <= 6.  Writes L (no accumulate)
 // for cells with x in [x_begin, x_end); ws = m2l_sep_workspace_floats.
+// stages: SEP_FRONT (pre + z/y/x passes into the workspace), SEP_POST (post
+// transform into L; with `coarse` = L of the level above, the L2L is fused:
+// L = L2L(coarse) + M2L).  The two may run on different streams.
+enum { SEP_FRONT = 1, SEP_POST = 2, SEP_ALL = 3 };
 size_t m2l_sep_workspace_floats(int rho, int level, int C);
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
                     const double* conv, const float* M, float* L, float* ws, int x_begin,
-                    int x_end, cudaStream_t s);
+                    int x_end, cudaStream_t s, int stages = SEP_ALL,
+                    const float* coarse = nullptr);
 
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {

@@ -35,6 +35,7 @@
 // line with the accumulators in registers (see "passes" below).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "shift.cuh"
 
 #include <cstdlib>
 
@@ -152,10 +153,14 @@ sep_pre_kernel(const float* __restrict__ M, float* __restrict__ Mp, int res, int
 }
 
 // X (graded-lex, z fastest) -> L rows.  Thread per cell, lanes along z.
+// With `coarse` (the level above's L grid) the L2L of the cascade
+// (ref expansion.py:215-225, 276-277) is fused: L = L2L(coarse) + M2L, the
+// same float32 sum the separate accumulate-L2L launch forms.
 template <int RHO>
 __global__ void __launch_bounds__(256)
 sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int C, int x_lo,
-                int nx, const __grid_constant__ SepParams<RHO> prm) {
+                int nx, const float* __restrict__ coarse, float half_fine,
+                const __grid_constant__ SepParams<RHO> prm) {
   constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
   const int64_t cells = (int64_t)nx * res * res;
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -173,6 +178,24 @@ sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int
   upper_axis<RHO, 0>(v, prm.post);
   upper_axis<RHO, 1>(v, prm.post);
   upper_axis<RHO, 2>(v, prm.post);
+  if (coarse) {
+    const int cres = res >> 1;
+    const float* prow =
+        coarse + ((((int64_t)(x >> 1) * cres + (y >> 1)) * cres + (z >> 1)) * C + ch) * PP;
+    float pv[P];
+#pragma unroll
+    for (int k = 0; k < PP; k += 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(prow + k));
+      if (k < P) pv[k] = q.x;
+      if (k + 1 < P) pv[k + 1] = q.y;
+      if (k + 2 < P) pv[k + 2] = q.z;
+      if (k + 3 < P) pv[k + 3] = q.w;
+    }
+    shift3<RHO, false>(pv, (x & 1) ? half_fine : -half_fine, (y & 1) ? half_fine : -half_fine,
+                       (z & 1) ? half_fine : -half_fine);
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = pv[j] + v[j];
+  }
   float* row = L + ((((int64_t)x * res + y) * res + z) * C + ch) * PP;
 #pragma unroll
   for (int k = 0; k < PP; k += 4) {
@@ -519,7 +542,7 @@ cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo
 template <int RHO>
 cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                         const double* conv, const float* M, float* L, float* wa, float* wb,
-                        int x_begin, int x_end, cudaStream_t s) {
+                        int x_begin, int x_end, int stages, const float* coarse, cudaStream_t s) {
   const int res = 1 << (level + 1);
   if (res % kLines) return cudaErrorInvalidValue;
   const SepParams<RHO> prm = to_params<RHO>(pre, post, conv);
@@ -528,24 +551,26 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
   const int xl = std::max(0, x_begin - 3) / kLines * kLines;
   const int xh = std::min(res, (x_end + 3 + kLines - 1) / kLines * kLines);
   cudaError_t err;
-  {
+  if (stages & SEP_FRONT) {
     const int64_t n = (int64_t)(xh - xl) * res * res * C;
     FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                                        M, wa, res, C, xl, xh - xl, prm));
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if ((err = launch_pass<RHO, PASS_Z>(wa, wb, res, C, xl, xh, 0, res, prm, "m2l_sep_z", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y>(wb, wa, res, C, xl, xh, 0, res, prm, "m2l_sep_y", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_X>(wa, wb, res, C, 0, res, x_begin, x_end, prm, "m2l_sep_x",
+                                        s)))
+      return err;
   }
-  if ((err = launch_pass<RHO, PASS_Z>(wa, wb, res, C, xl, xh, 0, res, prm, "m2l_sep_z", s)))
-    return err;
-  if ((err = launch_pass<RHO, PASS_Y>(wb, wa, res, C, xl, xh, 0, res, prm, "m2l_sep_y", s)))
-    return err;
-  if ((err = launch_pass<RHO, PASS_X>(wa, wb, res, C, 0, res, x_begin, x_end, prm, "m2l_sep_x", s)))
-    return err;
-  {
+  if (stages & SEP_POST) {
     const int64_t n = (int64_t)(x_end - x_begin) * res * res * C;
+    const float half_fine = (float)(1.0 / (double)res);
     if (n > 0) {
-      FC2T2_LAUNCH("m2l_sep_post", s,
+      FC2T2_LAUNCH(coarse ? "m2l_sep_post_l2l" : "m2l_sep_post", s,
                    sep_post_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-                       wb, L, res, C, x_begin, x_end - x_begin, prm));
+                       wb, L, res, C, x_begin, x_end - x_begin, coarse, half_fine, prm));
       if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
   }
@@ -562,19 +587,24 @@ size_t m2l_sep_workspace_floats(int rho, int level, int C) {
 
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
                     const double* conv, const float* M, float* L, float* ws, int x_begin,
-                    int x_end, cudaStream_t s) {
+                    int x_end, cudaStream_t s, int stages, const float* coarse) {
   const int64_t res = 1 << (level + 1);
   if (x_end < 0) x_end = (int)res;
   float* wa = ws;
   float* wb = ws + m2l_sep_workspace_floats(rho, level, C) / 2;
+#define FC2T2_SEP_RHO(R)                                                                   \
+  case R:                                                                                  \
+    return m2l_sep_rho<R>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, stages, \
+                          coarse, s);
   switch (rho) {
-    case 1: return m2l_sep_rho<1>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
-    case 2: return m2l_sep_rho<2>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
-    case 3: return m2l_sep_rho<3>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
-    case 4: return m2l_sep_rho<4>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
-    case 5: return m2l_sep_rho<5>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, s);
+    FC2T2_SEP_RHO(1)
+    FC2T2_SEP_RHO(2)
+    FC2T2_SEP_RHO(3)
+    FC2T2_SEP_RHO(4)
+    FC2T2_SEP_RHO(5)
     default: return cudaErrorNotSupported;
   }
+#undef FC2T2_SEP_RHO
 }
 
 }  // namespace fc2t2

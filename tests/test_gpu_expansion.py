@@ -596,3 +596,26 @@ def test_query_gradient_recycling_is_bit_identical(eng4, monkeypatch, host):
         outs.append((r.values, g.w_bar, g.p_bar, g.q_bar))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("C", [1, 3])
+def test_separable_post_with_fused_l2l_is_bit_identical(cuda, C):
+    """The separable M2L's post transform with the finest L2L fused into it
+    (run after the coarse chain) equals the separate accumulate-L2L launch bit
+    for bit, for the full grid and for an x-slab."""
+    from paper_2111_00110_b200 import Engine, KernelModel, _lib
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    assert eng.separable
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    p = torch.rand(100_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(100_000, C, device="cuda", generator=gen)
+    m = eng.p2m_device(p, w).storage
+    lib = _lib.lib()
+    out = {}
+    for fuse in (1, 0):
+        _lib.check(lib.fc2t2_engine_set_sep_fusion(eng.handle, fuse), "fusion")
+        out[fuse] = (eng.cascade_device(m), eng.cascade_device(m, (16, 40))[16:40])
+    _lib.check(lib.fc2t2_engine_set_sep_fusion(eng.handle, 1), "fusion")
+    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][1], out[1][1])
+    assert torch.equal(out[1][1], out[1][0][16:40])
