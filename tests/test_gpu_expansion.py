@@ -102,6 +102,12 @@ def test_cell_sort_is_stable_counting_sort(eng4, heavy):
     key = (b[:, 0] * 32 + b[:, 1]) * 32 + b[:, 2]
     ref = np.argsort(key, kind="stable")
     assert np.array_equal(order.cpu().numpy(), ref)
+    # the plain sort (no points): segments already in index order skip the network
+    plain, _ = eng4.sort_points(torch.from_numpy(p).cuda(), stable=True)
+    assert np.array_equal(plain.cpu().numpy(), ref)
+    pr = p[::-1].copy()        # reversed input: arrival order is mostly descending
+    plain_r, _ = eng4.sort_points(torch.from_numpy(pr).cuda(), stable=True)
+    assert np.array_equal(plain_r.cpu().numpy(), np.argsort(key[::-1], kind="stable"))
     counts = np.bincount(key, minlength=32 ** 3)
     assert np.array_equal(start.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
 
