@@ -211,7 +211,8 @@ STAGE_GROUPS = {
     "l2p": ["l2p"],
     "p2m": ["p2m"],
     "cell_sort": ["cell_keys", "scan", "sort_place", "sort_segments"],
-    "m2l_finest": ["m2l_sep_pre", "m2l_sep_z", "m2l_sep_y", "m2l_sep_x", "m2l_sep_post"],
+    "m2l_finest": ["m2l_sep_pre", "m2l_sep_z", "m2l_sep_y", "m2l_sep_x", "m2l_sep_post",
+                   "m2l_sep_post_l2l"],
     "m2l_finest_dense": ["m2l_absmax", "m2l_split", "m2l_tc_L5"],
     "l2l": ["l2l"],
     "m2m": ["m2m"],
@@ -277,12 +278,14 @@ def measured_traffic(kernels):
         t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
     except Exception:
         return None
-    tot, hit = 0.0, False
+    tot, ms, hit = 0.0, 0.0, False
     for k in kernels:
         if k in t.get("bytes_per_step", {}):
             tot += t["bytes_per_step"][k]
+            ms += t.get("serial_ms_per_step", {}).get(k, 0.0)
             hit = True
-    return {"bytes_per_step": tot, "source": t.get("source")} if hit else None
+    return {"bytes_per_step": tot, "serial_ms_per_step": ms or None,
+            "source": t.get("source")} if hit else None
 
 
 def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None = None):
@@ -749,6 +752,7 @@ def run_ours(args, rank: int, world: int) -> None:
                 "unit": "GB/s", "frac": d["frac"],
                 "traffic": (traffic["bytes_per_step"] if traffic else None),
                 "traffic_source": (traffic["source"] if traffic else None),
+                "ncu_serial_ms_per_step": (traffic["serial_ms_per_step"] if traffic else None),
                 "peak_source": hbm_src, "bytes_per_step": d["bytes_per_step"],
                 "launch_ms": d["ms_per_step"] / max(d["launches_per_step"], 1),
                 "launches_per_step": d["launches_per_step"], "bytes_model": d["model"]}

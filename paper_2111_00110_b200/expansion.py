@@ -216,16 +216,17 @@ class DomainFlag:
     def deferred(self):
         return DomainFlag._Deferred(self)
 
-    def mark(self):
-        """Every kernel that checks this call's inputs has been enqueued;
-        returns the token the same call passes to ``raise_if_set``."""
+    def mark(self, stream=None):
+        """Every kernel that checks this call's inputs has been enqueued (on
+        ``stream``, default the current one); returns the token the same call
+        passes to ``raise_if_set``."""
         if self._defer:
             return None
         if self._side is None:
             self._side = torch.cuda.Stream(device=self.t.device)
             self._mark = torch.cuda.Event()
             self._done = torch.cuda.Event()
-        self._mark.record(torch.cuda.current_stream(self.t.device))
+        self._mark.record(stream if stream is not None else torch.cuda.current_stream(self.t.device))
         return self._mark
 
     def raise_if_set(self, what: str, mark=None) -> None:

@@ -13,7 +13,7 @@ MAP = [  # (regex on the ncu kernel name, library profile label)
     (r"l2p_(warp_)?kernel", "l2p"), (r"p2m_sorted_kernel", "p2m"),
     (r"cell_keys_kernel", "cell_keys"), (r"place_kernel", "sort_place"),
     (r"segment_sort_\w+_kernel", "sort_segments"), (r"scan_\w+_kernel", "scan"),
-    (r"sep_pre_kernel", "m2l_sep_pre"), (r"sep_post_kernel", "m2l_sep_post"),
+    (r"sep_pre_kernel", "m2l_sep_pre"), (r"sep_post_kernel", "m2l_sep_post_l2l"),
     (r"sep_pass_kernel<\d+, 0", "m2l_sep_z"), (r"sep_pass_kernel<\d+, 1", "m2l_sep_y"),
     (r"sep_pass_kernel<\d+, 2", "m2l_sep_x"), (r"m2l_tc_kernel", "m2l_tc"),
     (r"m2l_ffma_kernel", "m2l_ffma"), (r"m2l_reduce_kernel", "m2l_reduce"),
@@ -32,7 +32,7 @@ def main():
     h = rows[0]
     units = dict(zip(h, rows[1]))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tot, launches = {}, {}
+    tot, launches, dur = {}, {}, {}
     for r in rows[2:]:
         d = dict(zip(h, r))
         name = d["Kernel Name"]
@@ -43,10 +43,14 @@ def main():
                 for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         tot[lab] = tot.get(lab, 0.0) + b
         launches[lab] = launches.get(lab, 0) + 1
+        t = float(d["gpu__time_duration.sum"].replace(",", ""))
+        t *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(units["gpu__time_duration.sum"], 1e-3)
+        dur[lab] = dur.get(lab, 0.0) + t
     res = {"source": f"ncu --set full --clock-control none, {rep.split('/')[-1]}, "
                      f"{steps:g} steps captured (cold-cache replays)",
            "bytes_per_step": {k: v / steps for k, v in tot.items()},
-           "launches_per_step": {k: v / steps for k, v in launches.items()}}
+           "launches_per_step": {k: v / steps for k, v in launches.items()},
+           "serial_ms_per_step": {k: v / steps for k, v in dur.items()}}
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
