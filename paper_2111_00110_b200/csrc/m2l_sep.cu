@@ -33,11 +33,15 @@
 // lines of the entries one partition needs (lanes along the contiguous
 // axis); warp g computes one output group for all 8 positions of its lane's
 // line with the accumulators in registers (see "passes" below).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "shift.cuh"
 
 #include <cstdlib>
+#include <cstring>
 
 namespace fc2t2 {
 
@@ -61,11 +65,9 @@ struct SepIdx {
 };
 
 constexpr int kLines = 32;
-// POS output positions per tile (8 or 16, FC2T2_SEP_POS); the z/y window holds
-// POS + 6 positions, the x window POS + 8 (16-byte aligned runs) in an odd
-// number of 16-byte chunks per lane (conflict-free 128-bit reads)
+// POS = 8 output positions per tile; the z/y window holds POS + 6 positions,
+// the x window POS + 8 (16-byte aligned runs)
 constexpr int win_of(int POS) { return POS + 6; }
-constexpr int xs_of(int POS) { return 4 * (((POS + 8) / 4) | 1); }
 
 
 // ------------------------------------------------------------ pre / post ---
@@ -268,15 +270,19 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
     const int le = in_base + i * in_stride;
     float v[NQ];
     if constexpr (PASS == PASS_X) {
-      const float4* r4 = reinterpret_cast<const float4*>(sm + (le * kLines + lane) * xs_of(POS));
+      // [le][lane][16], 16-byte chunk c of lane l in slot c ^ ((l >> 1) & 3)
+      // (the TMA 64-byte swizzle): conflict-free 128-bit reads
+      const float4* r4 = reinterpret_cast<const float4*>(sm + (le * kLines + lane) * 16);
+      const int sw = (lane >> 1) & 3;
 #pragma unroll
       for (int q = 0; q < NQ / 4; ++q) {
-        const float4 t = r4[q];
+        const float4 t = r4[q ^ sw];
         v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
       }
     } else {
+      // [le][q][lane]
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) v[q] = sm[(q * ne + le) * kLines + lane];
+      for (int q = 0; q < NQ; ++q) v[q] = sm[(le * NQ + q) * kLines + lane];
     }
     float k[7][NOUT];
     const float4* kc = reinterpret_cast<const float4*>(Kt + i * 56);
@@ -350,7 +356,7 @@ __device__ __forceinline__ void load_part(float* sm, const float* src, int res, 
       // z pass: [e][y=fixed][z=pos][x]; y pass: [e][y=pos][z=fixed][x]
       const int64_t g = PASS == PASS_Z ? ((e * res + T.fixed) * res + (ok ? pos : 0)) * res
                                        : ((e * res + (ok ? pos : 0)) * res + T.fixed) * res;
-      cp_async16(sm + (q * PT::NE + le) * kLines + 4 * c4, src + g + T.line0 + 4 * c4, ok);
+      cp_async16(sm + (le * win_of(POS) + q) * kLines + 4 * c4, src + g + T.line0 + 4 * c4, ok);
     }
   } else {
     constexpr int NC = (POS + 8) / 4;
@@ -364,7 +370,7 @@ __device__ __forceinline__ void load_part(float* sm, const float* src, int res, 
       // [e][y=fixed][z=line][x]
       const int64_t g =
           (((int64_t)PT::entry(le) * res + T.fixed) * res + T.line0 + lane) * res + (ok ? x : 0);
-      cp_async16(sm + (le * kLines + lane) * xs_of(POS) + 4 * c4, src + g, ok);
+      cp_async16(sm + (le * kLines + lane) * 16 + 4 * (c4 ^ ((lane >> 1) & 3)), src + g, ok);
     }
   }
 }
@@ -440,50 +446,112 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
 template <int RHO, int PASS, int POS>
 constexpr int pass_win_floats() {
   constexpr int R1 = RHO + 1;
-  return PASS == PASS_X ? R1 * R1 * kLines * xs_of(POS)
+  return PASS == PASS_X ? R1 * R1 * kLines * 16
                         : win_of(POS) * (PASS == PASS_Z ? R1 * (R1 + 1) / 2 : R1 * R1) * kLines;
 }
 template <int RHO, int PASS, int POS>
-constexpr int pass_smem_floats() {  // window + Kt[i][d][8]
-  return pass_win_floats<RHO, PASS, POS>() + 7 * 8 * (RHO + 1);
+constexpr int pass_smem_floats() {  // window + Kt[i][d][8] + mbarrier + 1 KB alignment slack
+  return pass_win_floats<RHO, PASS, POS>() + 7 * 8 * (RHO + 1) + 2 + 256;
+}
+
+// TMA: one tensor map per partition (box = the partition's window); the
+// out-of-range halo positions come back zero-filled (the reference's clipped
+// source slices).  Dims, x fastest: z/y passes (x, z, y, channel * entries,
+// 1); x pass (x, z, y, pair(b', c'), channel * (rho + 1) + a) with the
+// 64-byte swizzle.
+struct SepMaps {
+  CUtensorMap m[6];
+};
+
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, int c4, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+
+template <int RHO, int PASS, int POS>
+__device__ __forceinline__ uint32_t window_bytes(int part) {
+  constexpr int R1 = RHO + 1;
+  const int ne = PASS == PASS_Z ? (R1 - part) * (R1 - part + 1) / 2
+                                : (PASS == PASS_Y ? (R1 - part) * R1 : R1 * (R1 - part));
+  return (uint32_t)(PASS == PASS_X ? 16 * kLines * ne * 4 : win_of(POS) * kLines * ne * 4);
 }
 
 // One pass.  Tile = 32 lines x 8 output positions of one partition/channel:
 //   z pass: lines x, positions z, fixed y      (in M', out Z)
 //   y pass: lines x, positions y, fixed z      (in Z,  out Y)
 //   x pass: lines z, positions x, fixed y      (in Y,  out X)
+// The window comes from one TMA tensor copy issued by thread 0 (use_tma), or
+// from 16-byte cp.async copies by every thread.
 template <int RHO, int PASS, int POS>
 __global__ void __launch_bounds__(32 * (RHO + 1))
 sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, int C,
                 int line_lo, int nlt, int pos_lo, int npt, int pos_end,
-                const __grid_constant__ SepParams<RHO> prm) {
+                const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps,
+                int use_tma) {
   using I = SepIdx<RHO>;
-  extern __shared__ __align__(16) float sm[];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  float* sm = reinterpret_cast<float*>(
+      smraw + ((1024 - ((unsigned)__cvta_generic_to_shared(smraw) & 1023)) & 1023));
   constexpr int R1 = RHO + 1;
   float* Kt = sm + pass_win_floats<RHO, PASS, POS>();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Kt + 7 * 8 * R1);
   const int64_t plane = (int64_t)res * res * res;
   const int in_entries = PASS == PASS_Z ? I::P : I::T;
   const int out_entries = PASS == PASS_X ? I::P : I::T;
   const Tile T = decode_tile(blockIdx.x, R1, res, line_lo, nlt, pos_lo, npt, POS);
-  const float* src = in + (int64_t)T.ch * in_entries * plane;
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
+  if (use_tma) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
+                   "r"(window_bytes<RHO, PASS, POS>(T.part)));
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm);
+      const CUtensorMap* mp = &maps.m[T.part];
+      if (PASS == PASS_Z)
+        tma_load_5d(dst, mp, T.line0, T.pos0 - 3, T.fixed, T.ch * I::P + I::ab(T.part, 0), 0,
+                    bar_s);
+      else if (PASS == PASS_Y)
+        tma_load_5d(dst, mp, T.line0, T.fixed, T.pos0 - 3, T.ch * I::T + I::pair(T.part, 0) * R1,
+                    0, bar_s);
+      else
+        tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(T.part, 0), T.ch * R1, bar_s);
+    }
+  } else {
+    const float* src = in + (int64_t)T.ch * in_entries * plane;
 #define FC2T2_LOAD(Q) \
   if constexpr (Q <= RHO) load_part<RHO, PASS, POS, Q>(sm, src, res, T)
-  switch (T.part) {
-    case 0: FC2T2_LOAD(0); break;
-    case 1: FC2T2_LOAD(1); break;
-    case 2: FC2T2_LOAD(2); break;
-    case 3: FC2T2_LOAD(3); break;
-    case 4: FC2T2_LOAD(4); break;
-    case 5: FC2T2_LOAD(5); break;
-    default: break;
-  }
+    switch (T.part) {
+      case 0: FC2T2_LOAD(0); break;
+      case 1: FC2T2_LOAD(1); break;
+      case 2: FC2T2_LOAD(2); break;
+      case 3: FC2T2_LOAD(3); break;
+      case 4: FC2T2_LOAD(4); break;
+      case 5: FC2T2_LOAD(5); break;
+      default: break;
+    }
 #undef FC2T2_LOAD
+  }
   // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads)
   for (int t = threadIdx.x; t < 7 * 8 * R1; t += blockDim.x) {
     const int j = t & 7, d = (t >> 3) % 7, i = t / 56;
     Kt[t] = j < R1 ? prm.conv[d][j][i] : 0.f;
   }
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (use_tma) {
+    __syncthreads();   // the barrier init is visible before anyone waits on it
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(bar_s)
+        : "memory");
+  } else {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
   __syncthreads();
   compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T);
 }
@@ -501,12 +569,67 @@ SepParams<RHO> to_params(const double* pre, const double* post, const double* co
   return p;
 }
 
-int sep_pos() {
-  static const int v = [] {
-    const char* e = std::getenv("FC2T2_SEP_POS");
-    return e && e[0] == '1' && e[1] == '6' ? 16 : 8;
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
   }();
-  return v;
+  return fn;
+}
+
+bool sep_use_tma() {
+  static const bool v = [] {
+    const char* e = std::getenv("FC2T2_SEP_NOTMA");
+    return !(e && e[0] == '1');
+  }();
+  return v && tmap_encoder() != nullptr;
+}
+
+// tensor maps of one pass over `base` (one per partition); false on failure
+template <int RHO, int PASS, int POS>
+bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
+  using I = SepIdx<RHO>;
+  constexpr int R1 = RHO + 1;
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t r = (cuuint64_t)res, f = sizeof(float);
+  for (int part = 0; part < R1; ++part) {
+    cuuint64_t dims[5], strides[4];
+    cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+    CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+    dims[0] = dims[1] = dims[2] = r;
+    strides[0] = r * f;
+    strides[1] = r * r * f;
+    strides[2] = r * r * r * f;
+    if (PASS == PASS_X) {
+      dims[3] = I::NAB;
+      dims[4] = (cuuint64_t)C * R1;
+      strides[3] = (cuuint64_t)I::NAB * r * r * r * f;
+      box[0] = 16; box[1] = kLines; box[2] = 1; box[3] = R1 - part; box[4] = R1;
+      sw = CU_TENSOR_MAP_SWIZZLE_64B;
+    } else {
+      const int ent = PASS == PASS_Z ? I::P : I::T;
+      const int ne = PASS == PASS_Z ? (R1 - part) * (R1 - part + 1) / 2 : (R1 - part) * R1;
+      dims[3] = (cuuint64_t)C * ent;
+      dims[4] = 1;
+      strides[3] = dims[3] * r * r * r * f;
+      box[0] = kLines;
+      box[1] = PASS == PASS_Z ? win_of(POS) : 1;
+      box[2] = PASS == PASS_Z ? 1 : win_of(POS);
+      box[3] = ne;
+      box[4] = 1;
+    }
+    if (enc(&maps.m[part], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims,
+            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
 }
 
 template <int RHO, int PASS, int POS>
@@ -522,9 +645,12 @@ cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int lin
   if (smem > 48 * 1024 && attr_needed(configured))
     cudaFuncSetAttribute(sep_pass_kernel<RHO, PASS, POS>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  SepMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  const int tma = sep_use_tma() && encode_maps<RHO, PASS, POS>(maps, in, res, C) ? 1 : 0;
   FC2T2_LAUNCH(name, s,
                sep_pass_kernel<RHO, PASS, POS><<<(unsigned)blocks, 32 * (RHO + 1), smem, s>>>(
-                   in, out, res, C, line_lo, nlt, pos_lo, npt, pos_hi, prm));
+                   in, out, res, C, line_lo, nlt, pos_lo, npt, pos_hi, prm, maps, tma));
   return cudaGetLastError();
 }
 
@@ -532,11 +658,8 @@ template <int RHO, int PASS>
 cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                         int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
                         cudaStream_t s) {
-  if (sep_pos() == 8)
-    return launch_pass_pos<RHO, PASS, 8>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
-                                         name, s);
-  return launch_pass_pos<RHO, PASS, 16>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
-                                        name, s);
+  return launch_pass_pos<RHO, PASS, 8>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
+                                       name, s);
 }
 
 template <int RHO>
