@@ -69,7 +69,32 @@ p2m_sorted_kernel(const float* __restrict__ pts, const float* __restrict__ w, in
 #pragma unroll
     for (int j = 0; j < PP; ++j) acc[j] = 0.f;
     const int beg = cell_start[cell], end = cell_start[cell + 1];
-    for (int k = beg; k < end; ++k) {
+    int k = beg;
+    // batches of 4 points: the 4 index loads, then the 4 coordinate/weight
+    // gathers are all in flight before the first contraction (the sum order
+    // is unchanged: points still accumulate one by one in index order)
+    for (; k + 4 <= end; k += 4) {
+      int64_t ii[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ii[u] = order ? (int64_t)order[k + u] : (int64_t)(k + u);
+      float px[4], py[4], pz[4], pw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        px[u] = pts[3 * ii[u]];
+        py[u] = pts[3 * ii[u] + 1];
+        pz[u] = pts[3 * ii[u] + 2];
+        pw[u] = w[ii[u] * C + c];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float mono[P];
+        monomials<RHO>(box_offset(px[u], b0, res), box_offset(py[u], b1, res),
+                       box_offset(pz[u], b2, res), mono);
+#pragma unroll
+        for (int j = 0; j < P; ++j) acc[j] = fmaf(pw[u], mono[j], acc[j]);
+      }
+    }
+    for (; k < end; ++k) {
       const int64_t i = order ? (int64_t)order[k] : (int64_t)k;  // no order: pre-sorted inputs
       const float dx = box_offset(pts[3 * i], b0, res);
       const float dy = box_offset(pts[3 * i + 1], b1, res);
