@@ -180,6 +180,14 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
 int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
                                const double* conv);
 int fc2t2_engine_separable(const fc2t2_engine* e);
+/* Separable far table of a coarse level (3 <= level < levels, res >= 32):
+ * the parity stencil minus the hole as three disjoint per-axis pieces (no
+ * cancellation against the hole terms).  Includes the offsets the reference
+ * prunes (peak interaction < 1e-16, ref kernel.py:275), i.e. differs from the
+ * pruned sum by less than 1e-16 of the kernel peak per unit weight.  Same
+ * factor layout as fc2t2_engine_set_separable; NULL pointers remove it. */
+int fc2t2_engine_set_separable_far(fc2t2_engine* e, int level, const double* pre,
+                                   const double* post, const double* conv);
 /* 1 (default): the separable M2L's post transform runs after the coarse chain
  * with the finest L2L fused into it (one pass over the finest L grid fewer);
  * 0: separate accumulate-L2L launch.  Results are bit-identical. */

@@ -122,6 +122,8 @@ struct fc2t2_engine {
   bool sep = false;
   bool sep_fuse_l2l = true;  // fc2t2_engine_set_sep_fusion
   std::vector<double> sep_pre, sep_post, sep_conv;
+  // separable far tables of coarse levels: level -> {pre, post, conv}
+  std::map<int, std::vector<double>> sep_far;
 };
 
 namespace {
@@ -775,8 +777,10 @@ ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
   const int L = e->levels;
   for (int l = kCoarsest; l < L; ++l) {
     w.coarse_grids += 2 * grid_floats(l, channels, e->PP);
-    w.coarse_part =
-        std::max(w.coarse_part, part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels));
+    const size_t need = e->sep_far.count(l)
+                            ? fc2t2::m2l_sep_workspace_floats(e->rho, l, channels, true)
+                            : part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels);
+    w.coarse_part = std::max(w.coarse_part, need);
   }
   w.fine_part = e->sep ? fc2t2::m2l_sep_workspace_floats(e->rho, L, channels)
                        : part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
@@ -823,6 +827,25 @@ int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double*
 }
 
 int fc2t2_engine_separable(const fc2t2_engine* e) { return e && e->sep ? 1 : 0; }
+
+int fc2t2_engine_set_separable_far(fc2t2_engine* e, int level, const double* pre,
+                                   const double* post, const double* conv) {
+  if (!e) return fail(FC2T2_EVALUE, "null engine");
+  if (!pre || !post || !conv) {
+    e->sep_far.erase(level);
+    return FC2T2_OK;
+  }
+  const int res = 1 << (level + 1);
+  if (e->rho > 5 || level <= kCoarsest || level >= e->levels || res % 32)
+    return fail(FC2T2_EVALUE, "separable far M2L needs rho <= 5 and a coarse level of >= 32 cells");
+  const int R1 = e->rho + 1;
+  std::vector<double> f(9 * R1 * R1);
+  std::copy(pre, pre + R1 * R1, f.begin());
+  std::copy(post, post + R1 * R1, f.begin() + R1 * R1);
+  std::copy(conv, conv + 7 * R1 * R1, f.begin() + 2 * R1 * R1);
+  e->sep_far[level] = std::move(f);
+  return FC2T2_OK;
+}
 
 int fc2t2_engine_set_sep_fusion(fc2t2_engine* e, int fuse_l2l) {
   if (!e) return fail(FC2T2_EVALUE, "null engine");
@@ -930,6 +953,19 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
     bool have = false;
     for (int l = lowest; l < L; ++l) {
       const Plan& p = e->plans.at(l).at(FC2T2_TABLE_FAR);
+      auto sf = e->sep_far.find(l);
+      if (p.max_list > 0 && sf != e->sep_far.end()) {
+        // separable far table, its post transform with this level's L2L fused
+        const int R1 = e->rho + 1;
+        const double* f = sf->second.data();
+        st = cuda_status(fc2t2::m2l_sep(e->rho, l, channels, f, f + R1 * R1, f + 2 * R1 * R1,
+                                        Mg[l], Lg[l], coarse_part, 0, -1, s, fc2t2::SEP_ALL,
+                                        have ? Lg[l - 1] : nullptr, true),
+                         "expand m2l_sep far");
+        if (st != FC2T2_OK) return st;
+        have = true;
+        continue;
+      }
       if (have) {
         st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, Lg[l - 1], Lg[l], 0, s), "expand l2l");
         if (st != FC2T2_OK) return st;

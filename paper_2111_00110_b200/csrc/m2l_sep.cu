@@ -257,7 +257,8 @@ template <int RHO, int PASS, int POS, int NOUT>
 __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int ne, int lane,
                                            int nin, int in_base, int in_stride,
                                            const int (&oe)[RHO + 1], float* out,
-                                           int64_t pos_stride, int64_t plane, int nvalid) {
+                                           int64_t pos_stride, int64_t plane, int nvalid,
+                                           bool accumulate) {
   constexpr int OFF = PASS == PASS_X ? 4 : 3;
   constexpr int NQ = PASS == PASS_X ? POS + 8 : win_of(POS);
   float acc[POS][NOUT];
@@ -314,7 +315,10 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
   for (int w = 0; w < POS; ++w) {
     if (w < nvalid) {
 #pragma unroll
-      for (int j = 0; j < NOUT; ++j) out[(int64_t)oe[j] * plane + w * pos_stride] = acc[w][j];
+      for (int j = 0; j < NOUT; ++j) {
+        float* o = out + (int64_t)oe[j] * plane + w * pos_stride;
+        *o = accumulate ? *o + acc[w][j] : acc[w][j];
+      }
     }
   }
 }
@@ -377,7 +381,7 @@ __device__ __forceinline__ void load_part(float* sm, const float* src, int res, 
 
 template <int RHO, int PASS, int POS>
 __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, float* dst, int res,
-                                             int pos_end, const Tile& T) {
+                                             int pos_end, const Tile& T, bool accumulate) {
   using I = SepIdx<RHO>;
   constexpr int R1 = RHO + 1;
   const int64_t plane = (int64_t)res * res * res;
@@ -428,7 +432,7 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
   case Q:                                                                                  \
     if constexpr (Q <= R1)                                                                 \
       group_body<RHO, PASS, POS, Q>(sm, Kt, ne, lane, nin, in_base, in_stride, oe, o,           \
-                               pos_stride, plane, nvalid);                                 \
+                               pos_stride, plane, nvalid, accumulate);                     \
     break;
   switch (nout) {
     FC2T2_SEP_N(1)
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(32 * (RHO + 1))
 sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, int C,
                 int line_lo, int nlt, int pos_lo, int npt, int pos_end,
                 const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps,
-                int use_tma) {
+                int use_tma, int accumulate) {
   using I = SepIdx<RHO>;
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(
@@ -553,7 +557,8 @@ sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, 
     asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
   __syncthreads();
-  compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T);
+  compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T,
+                               accumulate != 0);
 }
 
 template <int RHO>
@@ -635,7 +640,7 @@ bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
 template <int RHO, int PASS, int POS>
 cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                             int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                            cudaStream_t s) {
+                            cudaStream_t s, int accumulate) {
   const int nlt = (line_hi - line_lo + kLines - 1) / kLines;
   const int npt = (pos_hi - pos_lo + POS - 1) / POS;
   const int64_t blocks = (int64_t)nlt * npt * res * (RHO + 1) * C;
@@ -650,22 +655,36 @@ cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int lin
   const int tma = sep_use_tma() && encode_maps<RHO, PASS, POS>(maps, in, res, C) ? 1 : 0;
   FC2T2_LAUNCH(name, s,
                sep_pass_kernel<RHO, PASS, POS><<<(unsigned)blocks, 32 * (RHO + 1), smem, s>>>(
-                   in, out, res, C, line_lo, nlt, pos_lo, npt, pos_hi, prm, maps, tma));
+                   in, out, res, C, line_lo, nlt, pos_lo, npt, pos_hi, prm, maps, tma, accumulate));
   return cudaGetLastError();
 }
 
 template <int RHO, int PASS>
 cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                         int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                        cudaStream_t s) {
+                        cudaStream_t s, int accumulate = 0) {
   return launch_pass_pos<RHO, PASS, 8>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
-                                       name, s);
+                                       name, s, accumulate);
+}
+
+// the K(d) of an offset subset: F = {|d| >= 2}, N = {|d| <= 1}
+template <int RHO>
+SepParams<RHO> masked(const SepParams<RHO>& p, bool keep_far) {
+  SepParams<RHO> q = p;
+  for (int d = 0; d < 7; ++d) {
+    const bool far = d - 3 <= -2 || d - 3 >= 2;
+    if (far != keep_far)
+      for (int i = 0; i <= RHO; ++i)
+        for (int j = 0; j <= RHO; ++j) q.conv[d][i][j] = 0.f;
+  }
+  return q;
 }
 
 template <int RHO>
 cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                         const double* conv, const float* M, float* L, float* wa, float* wb,
-                        int x_begin, int x_end, int stages, const float* coarse, cudaStream_t s) {
+                        int x_begin, int x_end, int stages, const float* coarse, bool far_only,
+                        cudaStream_t s) {
   const int res = 1 << (level + 1);
   if (res % kLines) return cudaErrorInvalidValue;
   const SepParams<RHO> prm = to_params<RHO>(pre, post, conv);
@@ -674,7 +693,35 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
   const int xl = std::max(0, x_begin - 3) / kLines * kLines;
   const int xh = std::min(res, (x_end + 3 + kLines - 1) / kLines * kLines);
   cudaError_t err;
-  if (stages & SEP_FRONT) {
+  if ((stages & SEP_FRONT) && far_only) {
+    // far table of a coarse level: the parity box minus the hole {-1,0,1}^3
+    // as three disjoint separable pieces (no cancellation against the large
+    // hole terms): F x A x A + N x F x A + N x N x F over (x, y, z), F = far
+    // and N = near axis offsets, A = both -- z passes A and F, y passes
+    // A(Z_A), F(Z_A) + N(Z_F), x passes F(Y1) + N(Y23).  Full grid only.
+    const size_t tb = SepIdx<RHO>::T * (size_t)res * res * res * C;
+    float *b0 = wa, *b1 = wb, *b2 = wb + tb, *b3 = wb + 2 * tb;
+    const SepParams<RHO> pF = masked(prm, true), pN = masked(prm, false);
+    const int64_t n = (int64_t)res * res * res * C;
+    FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+                                       M, b0, res, C, 0, res, prm));
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if ((err = launch_pass<RHO, PASS_Z>(b0, b1, res, C, 0, res, 0, res, prm, "m2l_sep_z", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Z>(b0, b2, res, C, 0, res, 0, res, pF, "m2l_sep_z", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y>(b1, b0, res, C, 0, res, 0, res, prm, "m2l_sep_y", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y>(b1, b3, res, C, 0, res, 0, res, pF, "m2l_sep_y", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y>(b2, b3, res, C, 0, res, 0, res, pN, "m2l_sep_y", s, 1)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_X>(b0, b1, res, C, 0, res, 0, res, pF, "m2l_sep_x", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_X>(b3, b1, res, C, 0, res, 0, res, pN, "m2l_sep_x", s, 1)))
+      return err;
+    wb = b1;   // the post stage reads X from here
+  } else if (stages & SEP_FRONT) {
     const int64_t n = (int64_t)(xh - xl) * res * res * C;
     FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                                        M, wa, res, C, xl, xh - xl, prm));
@@ -702,23 +749,24 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
 
 }  // namespace
 
-size_t m2l_sep_workspace_floats(int rho, int level, int C) {
+size_t m2l_sep_workspace_floats(int rho, int level, int C, bool far_only) {
   const int64_t res = 1 << (level + 1);
   const int64_t R1 = rho + 1, T = R1 * (R1 + 1) / 2 * R1;
-  return (size_t)(2 * T * res * res * res * C);
+  return (size_t)((far_only ? 4 : 2) * T * res * res * res * C);
 }
 
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
                     const double* conv, const float* M, float* L, float* ws, int x_begin,
-                    int x_end, cudaStream_t s, int stages, const float* coarse) {
+                    int x_end, cudaStream_t s, int stages, const float* coarse, bool far_only) {
   const int64_t res = 1 << (level + 1);
   if (x_end < 0) x_end = (int)res;
+  if (far_only && (x_begin != 0 || x_end != res)) return cudaErrorInvalidValue;
   float* wa = ws;
-  float* wb = ws + m2l_sep_workspace_floats(rho, level, C) / 2;
+  float* wb = ws + m2l_sep_workspace_floats(rho, level, C, false) / 2;
 #define FC2T2_SEP_RHO(R)                                                                   \
   case R:                                                                                  \
     return m2l_sep_rho<R>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, stages, \
-                          coarse, s);
+                          coarse, far_only, s);
   switch (rho) {
     FC2T2_SEP_RHO(1)
     FC2T2_SEP_RHO(2)

@@ -545,7 +545,8 @@ def test_m2l_cta_pair_kernel_matches_single_cta():
 
 @pytest.mark.parametrize("alpha,rho,level,C,lsq", [(1000.0, 4, 5, 1, True), (200.0, 4, 4, 2, True),
                                                    (200.0, 3, 4, 1, True), (1000.0, 4, 5, 1, False),
-                                                   (1000.0, 5, 5, 1, True), (50.0, 2, 4, 3, True)])
+                                                   (1000.0, 5, 5, 1, True), (50.0, 2, 4, 3, True),
+                                                   (200.0, 4, 5, 2, True)])
 def test_separable_finest_m2l_matches_dense_and_oracle(cuda, alpha, rho, level, C, lsq):
     """The separable finest far + near M2L (csrc/m2l_sep.cu: per-axis
     triangular transforms around three 1-D convolutions) against the dense
@@ -625,3 +626,25 @@ def test_separable_post_with_fused_l2l_is_bit_identical(cuda, C):
     assert torch.equal(out[0][0], out[1][0])
     assert torch.equal(out[0][1], out[1][1])
     assert torch.equal(out[1][1], out[1][0][16:40])
+
+
+def test_separable_far_levels_match_dense(cuda, monkeypatch):
+    """Coarse-level far tables run separably (opt-in FC2T2_SEP_FAR=1; parity
+    box minus the hole as three disjoint per-axis pieces,
+    fc2t2_engine_set_separable_far): the
+    cascade with them equals the one with dense coarse levels to < 1e-6
+    (both with the separable finest level), at levels 5 and 6."""
+    from paper_2111_00110_b200 import Engine, KernelModel
+    for alpha, L in ((1000.0, 5), (1000.0, 6)):
+        k = KernelModel("gaussian", alpha, 4)
+        monkeypatch.setenv("FC2T2_SEP_FAR", "1")
+        far = Engine(k, L, check_admissibility=False)
+        monkeypatch.delenv("FC2T2_SEP_FAR")
+        nofar = Engine(k, L, check_admissibility=False)
+        assert far._sep_far and not nofar._sep_far
+        gen = torch.Generator(device="cuda").manual_seed(L)
+        p = torch.rand(200_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+        w = torch.randn(200_000, 1, device="cuda", generator=gen)
+        m = far.p2m_device(p, w).storage
+        a, b = _np(far.cascade_device(m)), _np(nofar.cascade_device(m))
+        assert rel_l2(a, b) < 1e-6
