@@ -278,15 +278,14 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     coherent = _beyond_coherent(engine.finest_grid_bytes(sources.channels))
     q_sort = engine.sort_points(qd) if coherent else None   # else sorted for the backward
     ready = None
+    if q_sort is None:
+        # a stand-alone check: the aux-stream query sort also checks q, but
+        # waiting for its end would stall the host for the whole sort when it
+        # outlasts the forward (config 5: +40 ms per step, measured)
+        engine.flag.check_points(qd)
+    checked = engine.flag.mark()
     if q_sort is None and EARLY_QUERY_SORT:
-        # the aux-stream query sort checks q's domain (after the p sort, which
-        # the aux stream waits for): the flag read waits for its end only
         q_sort, ready = _early_sort(engine, qd)
-        checked = engine.flag.mark(engine.aux_stream())
-    else:
-        if q_sort is None:
-            engine.flag.check_points(qd)    # the L2P at q would only see q at the very end
-        checked = engine.flag.mark()
     acc = engine.expand_device(sources.p, sources.w, p_sort)
     recycle = RECYCLE_QUERY_GRAD and not coherent
     r = _l2p(acc, qd, _lib.L2P_VALUE | (_lib.L2P_GRAD if recycle else 0), q_sort)
