@@ -648,3 +648,40 @@ def test_separable_far_levels_match_dense(cuda, monkeypatch):
         m = far.p2m_device(p, w).storage
         a, b = _np(far.cascade_device(m)), _np(nofar.cascade_device(m))
         assert rel_l2(a, b) < 1e-6
+
+
+def _run_subprocess(env_extra: dict, code: str) -> str:
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, **env_extra)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return r.stdout
+
+
+def test_opt_in_paths_in_subprocesses(cuda):
+    """The process-wide switches (read once by the library): the order-free
+    fixed-point P2M (FC2T2_P2M_FIXED=1, its own test run with it on) and the
+    cp.async window loader of the separable M2L (FC2T2_SEP_NOTMA=1), whose
+    cascade must equal the TMA loader's bit for bit."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = _run_subprocess({"FC2T2_P2M_FIXED": "1"},
+                          "import sys, pytest; sys.exit(pytest.main(['-q', '-x', '-p', "
+                          "'no:cacheprovider', '-k', 'cell_bin_and_order_free', "
+                          f"'{root}/tests/test_gpu_expansion.py']))")
+    assert "passed" in out and "skipped" not in out
+    code = ("import torch, hashlib\n"
+            "from paper_2111_00110_b200 import Engine, KernelModel\n"
+            "e = Engine(KernelModel('gaussian', 1000.0, 4), 5, check_admissibility=False)\n"
+            "g = torch.Generator(device='cuda').manual_seed(4)\n"
+            "p = torch.rand(100000, 3, device='cuda', generator=g) * 1.999998 - 0.999999\n"
+            "w = torch.randn(100000, 1, device='cuda', generator=g)\n"
+            "L = e.cascade_device(e.p2m_device(p, w).storage)\n"
+            "print(hashlib.sha1(L.cpu().numpy().tobytes()).hexdigest())\n")
+    a = _run_subprocess({}, code).strip().splitlines()[-1]
+    b = _run_subprocess({"FC2T2_SEP_NOTMA": "1"}, code).strip().splitlines()[-1]
+    assert a == b
