@@ -454,8 +454,20 @@ int m2l_splits(int rho, int C, const M2LLaunch& plan) {
   const int rows = 128 * (index_count(rho) <= 35 ? 2 : 1);
   const int tpt = std::max(1, rows / C);
   const int64_t ctas = ((int64_t)nu * nu * nu + tpt - 1) / tpt * plan.ncls;
-  const int64_t want = (2 * 148 + ctas - 1) / ctas;
-  return (int)std::max<int64_t>(1, std::min<int64_t>({want, 16, (int64_t)plan.max_list}));
+  static const int waves = [] {
+    const char* e = std::getenv("FC2T2_M2L_SPLIT_WAVES");
+    const int v = e ? std::atoi(e) : 2;
+    return v > 0 ? v : 2;
+  }();
+  static const int cap = [] {
+    // measured at config 2 level 3 (16 CTAs per split): 19 splits 45 us,
+    // 16 splits 54 us, 32 splits 56 us per launch
+    const char* e = std::getenv("FC2T2_M2L_SPLIT_CAP");
+    const int v = e ? std::atoi(e) : 32;
+    return v > 0 ? v : 32;
+  }();
+  const int64_t want = (waves * 148 + ctas - 1) / ctas;
+  return (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)cap, (int64_t)plan.max_list}));
 }
 
 cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
