@@ -8,10 +8,15 @@ class it stands for (DomainError, StageError, OrderError, ...).
 from __future__ import annotations
 
 import ctypes as ct
+import os
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "libfc2t2_b200.so"
+# A/B experiments may point at an alternative build of the same library
+# (e.g. scripts building with different -D flags); the product uses LIB_PATH.
+if os.environ.get("FC2T2_LIB_OVERRIDE"):
+    LIB_PATH = Path(os.environ["FC2T2_LIB_OVERRIDE"])
 
 OK, EDOMAIN, ESTAGE, EORDER, ECUDA, EWORKSPACE, EVALUE = range(7)
 FLAG_DOMAIN = 1
