@@ -12,11 +12,12 @@ tests):
                                                  slowest grid axis)
     f(q_r), and in the backward the same with (q_r, y_r), then G(p_r), grad G(p_r)
 
-The dominant finest-level M2L (about 80% of a cascade) is thus divided among
-the ranks instead of replicated; the all-reduce provides every rank with the
-halo planes its slab's M2L reads.  Slabs are multiples of 4 cells (two class
-lattice planes, the tensor-core kernel's tile pair); when the grid does not
-split evenly the cascade falls back to replication.  The compute backend is
+The finest-level M2L is thus divided among the ranks instead of replicated;
+the all-reduce provides every rank with the halo planes its slab's M2L reads.
+Slabs are multiples of 4 cells (for the dense tensor-core kernel, two class
+lattice planes; the separable form restricts its passes to the slab plus the
+3-cell halo); when the grid does not split evenly the cascade falls back to
+replication.  The compute backend is
 any object with ``p2m_grid``, ``cascade_grid(m, x_range=None)``, ``evaluate``
 (the device Engine adapter below; tests/test_parallel_gloo.py plugs the CPU
 oracle in to check the sharding logic on CPU with world size 2).
@@ -40,13 +41,32 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
 
 
 class DeviceBackend:
-    """The B200 engine as a sharding backend (grids are device tensors)."""
+    """The B200 engine as a sharding backend (grids are device tensors).  Beyond
+    the three methods every backend has, it offers the single-GPU layer's
+    shortcuts (layers.py): the query cell sort started on the engine's aux
+    stream in the forward, and q_bar recycled from the forward's grad f(q)."""
 
     def __init__(self, engine):
         self.engine = engine
 
-    def p2m_grid(self, p: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
-        return self.engine.p2m_device(p, w).storage
+    def p2m_grid(self, p: torch.Tensor, w: torch.Tensor, sort=None) -> torch.Tensor:
+        return self.engine.p2m_device(p, w, sort).storage
+
+    def early_sort(self, q: torch.Tensor):
+        from .layers import EARLY_QUERY_SORT, _early_sort
+        return _early_sort(self.engine, q) if EARLY_QUERY_SORT else (None, None)
+
+    def evaluate_value_grad(self, L: torch.Tensor, pts: torch.Tensor):
+        from .expansion import Accessor, ExpansionGrid
+        eng = self.engine
+        acc = Accessor(ExpansionGrid(eng.levels, "L", L, eng.rho), eng.table, eng.flops,
+                       flag=eng.flag)
+        out = acc.eval_device(pts, _lib.L2P_VALUE | _lib.L2P_GRAD)
+        return out["value"], out["grad"]
+
+    def weighted_grad(self, grad: torch.Tensor, wts: torch.Tensor) -> torch.Tensor:
+        from .layers import _weighted_grad
+        return _weighted_grad(grad, wts.reshape(grad.shape[0], -1))
 
     def cascade_grid(self, m: torch.Tensor, x_range: tuple | None = None) -> torch.Tensor:
         return self.engine.cascade_device(m, x_range)
@@ -68,6 +88,8 @@ class ShardedExplicitResult:
     q: torch.Tensor
     p: torch.Tensor
     w: torch.Tensor
+    q_grad: torch.Tensor = None     # grad f(q_r), when the backend recycles it
+    q_sort: object = None           # (CellSort, ready event) of q_r from the aux stream
 
 
 def _allreduce(t: torch.Tensor, group) -> torch.Tensor:
@@ -103,16 +125,29 @@ def _cascade(backend, m: torch.Tensor, group) -> torch.Tensor:
 
 def explicit_forward_sharded(backend, p, w, q, group=None) -> ShardedExplicitResult:
     """Forward of the explicit layer on this rank's shards (see module doc)."""
+    q_sort = backend.early_sort(q) if hasattr(backend, "early_sort") else None
     m = _allreduce(backend.p2m_grid(p, w), group)
     L = _cascade(backend, m, group)
-    values, _ = backend.evaluate(L, q, None, True)
-    return ShardedExplicitResult(values=values, L=L, q=q, p=p, w=w)
+    q_grad = None
+    if hasattr(backend, "evaluate_value_grad"):
+        values, q_grad = backend.evaluate_value_grad(L, q)
+    else:
+        values, _ = backend.evaluate(L, q, None, True)
+    return ShardedExplicitResult(values=values, L=L, q=q, p=p, w=w, q_grad=q_grad, q_sort=q_sort)
 
 
 def explicit_jvp_sharded(backend, y_bar, res: ShardedExplicitResult, group=None):
     """(w_bar_r, p_bar_r, q_bar_r) for this rank's shards."""
-    _, q_bar = backend.evaluate(res.L, res.q, y_bar, False)
-    b = _allreduce(backend.p2m_grid(res.q, y_bar), group)
+    if res.q_grad is not None:
+        q_bar = backend.weighted_grad(res.q_grad, y_bar)
+    else:
+        _, q_bar = backend.evaluate(res.L, res.q, y_bar, False)
+    srt = None
+    if res.q_sort is not None and res.q_sort[0] is not None:
+        srt, ready = res.q_sort
+        torch.cuda.current_stream().wait_event(ready)
+    b = _allreduce(backend.p2m_grid(res.q, y_bar, srt) if srt is not None
+                   else backend.p2m_grid(res.q, y_bar), group)
     G = _cascade(backend, b, group)
     w_bar, p_bar = backend.evaluate(G, res.p, res.w, True)
     return w_bar, p_bar, q_bar

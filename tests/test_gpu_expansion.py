@@ -685,3 +685,26 @@ def test_opt_in_paths_in_subprocesses(cuda):
     a = _run_subprocess({}, code).strip().splitlines()[-1]
     b = _run_subprocess({"FC2T2_SEP_NOTMA": "1"}, code).strip().splitlines()[-1]
     assert a == b
+
+
+def test_sharded_layer_single_rank_matches_layers(eng4):
+    """The sharded explicit layer (parallel.py) with the device backend on one
+    rank (no process group) equals layers.explicit_forward / explicit_jvp bit
+    for bit: same early query sort, recycled q_bar and cascade."""
+    from paper_2111_00110_b200 import SourceSet
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    from paper_2111_00110_b200.parallel import (DeviceBackend, explicit_forward_sharded,
+                                                explicit_jvp_sharded)
+    gen = torch.Generator(device="cuda").manual_seed(31)
+    p = torch.rand(20_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    w = torch.randn(20_000, 1, device="cuda", generator=gen)
+    q = torch.rand(50_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
+    yb = torch.randn(50_000, 1, device="cuda", generator=gen)
+    be = DeviceBackend(eng4)
+    rs = explicit_forward_sharded(be, p, w, q)
+    wb, pb, qb = explicit_jvp_sharded(be, yb, rs)
+    rl = explicit_forward(eng4, SourceSet(p, w), q)
+    g = explicit_jvp(yb, rl)
+    assert rs.q_grad is not None
+    assert torch.equal(rs.values, rl.values)
+    assert torch.equal(qb, g.q_bar) and torch.equal(wb, g.w_bar) and torch.equal(pb, g.p_bar)
