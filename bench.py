@@ -129,52 +129,107 @@ class Clocks:
 
 # ------------------------------------------------------------- CPU arm ---
 
-def cpu_sample(steps: int, warmup: int, N: int, M: int, seed: int) -> dict:
-    """Oracle (float64 NumPy restatement) on a bounded sample of the workload.
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    A step is the full explicit-layer pipeline (P2M, cascade, L2P, backward
-    P2M, cascade, L2P) on n_s sources / m_s queries over the SAME level-5 grid;
-    the per-point stages scale linearly and the cascades are size independent,
-    so the full-workload time is extrapolated as
-        t = 2 * t_cascade + (t_pointwise) * (N + M) / (n_s + m_s).
-    """
+
+SAMPLE_SLICES = 32   # one CPU step = 1/32 of the full config-2 step's work
+
+
+def cpu_sample(steps: int, warmup: int, N: int, M: int, seed: int) -> dict:
+    """The reference pipeline restated by the oracle (speed-faithful: power-table
+    monomials, one contiguous GEMM per offset -- tests/test_oracle_speed.py
+    holds it within 1.3x of the imported reference), timed on a BOUNDED SLICE
+    of the full config-2 step.
+
+    The full step's work is a list of units -- P2M of p and of q, L2P value +
+    gradient at q and at p (per point), and for each of its two cascades every
+    (level, active offset) M2L GEMM, every (level, child) M2M and L2L shift
+    (expansion.py:200-264) -- dealt round-robin into SAMPLE_SLICES balanced
+    slices.  Step s runs slice s mod SAMPLE_SLICES on real-sized grids (level 5,
+    64^3) and (N + M) / SAMPLE_SLICES points; value = that slice's points per
+    second, i.e. (N + M) / (SAMPLE_SLICES * t_slice).  No extrapolation beyond
+    the uniform 1/32 share of the same work."""
     threads = len(os.sched_getaffinity(0))
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ.setdefault(var, str(threads))
-    from oracle.fc2t2_oracle import Oracle
+    from itertools import product
+
+    from oracle.fc2t2_oracle import COARSEST, Oracle, res_of, width_of
     ora = Oracle(CFG["alpha"], CFG["rho"], CFG["levels"])
-    n_s, m_s = 1 << 14, 1 << 17
-    p, w, q, yb = inputs(seed + 1, n_s, m_s)
-    p, w, q, yb = (a.astype(np.float64) for a in (p, w, q, yb))
+    S = SAMPLE_SLICES
+    L = CFG["levels"]
+    rng = np.random.default_rng(seed + 7)
+    # grids of the real sizes (values do not change the arithmetic)
+    Mg = {l: rng.standard_normal((res_of(l),) * 3 + (1, ora.P)) for l in range(COARSEST, L + 1)}
+    units = []
+    for _cascade in range(2):
+        for l in range(L, COARSEST, -1):
+            units += [("m2m", l, c) for c in product((0, 1), repeat=3)]
+        for l in range(COARSEST, L + 1):
+            t = ora.tables["far"][l]
+            units += [("m2l", l, i) for i in np.flatnonzero(t["active"])]
+            if l > COARSEST:
+                units += [("l2l", l - 1, c) for c in product((0, 1), repeat=3)]
+        units += [("near", L, i) for i in np.flatnonzero(ora.tables["near"]["active"])]
+    slices = [units[k::S] for k in range(S)]
+    n_s, m_s = N // S, M // S
+    shift_cache = {}
+
+    def shift(kind, l, c):
+        key = (kind, l, c)
+        if key not in shift_cache:
+            wf = width_of(l if kind == "m2m" else l + 1)
+            shift_cache[key] = ora.shift((np.array(c) - 0.5) * wf, kind == "m2m").T.copy()
+        return shift_cache[key]
+
+    def run_unit(u):
+        kind, l, x = u
+        if kind == "m2m":
+            f = Mg[l]
+            _ = f[x[0]::2, x[1]::2, x[2]::2] @ shift(kind, l, x)
+        elif kind == "l2l":
+            _ = Mg[l] @ shift(kind, l, x)
+        else:
+            tab = ora.tables["near"] if kind == "near" else ora.tables["far"][l]
+            one = dict(tab)
+            one["active"] = np.zeros_like(tab["active"])
+            one["active"][x] = True
+            ora.m2l(Mg[l], one)
+
     times = []
     for it in range(warmup + steps):
+        k = it % S
+        p, w, q, yb = inputs(seed + 1 + it, n_s, m_s)
+        p, w, q, yb = (a.astype(np.float64) for a in (p, w, q, yb))
         t0 = time.perf_counter()
-        Mg = ora.p2m(p, w)
-        t1 = time.perf_counter()
-        L = ora.cascade(Mg)
-        t2 = time.perf_counter()
-        ora.evaluate(L, q)
-        qg = ora.evaluate(L, q, what="grad")
-        np.einsum("mc,mca->ma", yb, qg)
-        Bg = ora.p2m(q, yb)
-        t3 = time.perf_counter()
-        # second cascade: same cost as the first (size independent); the
-        # measured first cascade stands in for it to bound the sample time
-        ora.evaluate(L, p)
-        np.einsum("nc,nca->na", w, ora.evaluate(L, p, what="grad"))
-        t4 = time.perf_counter()
-        del Bg
-        point = (t1 - t0) + (t3 - t2) + (t4 - t3)
-        full = 2.0 * (t2 - t1) + point * (N + M) / (n_s + m_s)
+        ora.p2m(p, w)                                   # forward P2M
+        Lf = Mg[L]
+        ora.evaluate(Lf, q)                             # values
+        np.einsum("mc,mca->ma", yb, ora.evaluate(Lf, q, what="grad"))   # q_bar
+        ora.p2m(q, yb)                                  # backward P2M
+        ora.evaluate(Lf, p)                             # w_bar
+        np.einsum("nc,nca->na", w, ora.evaluate(Lf, p, what="grad"))    # p_bar
+        for u in slices[k]:
+            run_unit(u)
+        dt = time.perf_counter() - t0
         if it >= warmup:
-            times.append(full)
-    t = float(np.median(times))
-    return {"value": (N + M) / t, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": (f"oracle (float64 NumPy restatement of the reference) on {n_s} sources + "
-                       f"{m_s} queries over the full level-5 grid, one measured cascade "
-                       f"counted twice; pointwise stages linearly extrapolated to N+M="
-                       f"{N + M} (extrapolated); median of {steps} steps"),
-            "seconds_per_step_extrapolated": t}
+            times.append(dt)
+    t = float(np.mean(times))
+    return {"value": (n_s + m_s) / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": (f"oracle (float64 NumPy restatement of the reference, speed-faithful) on "
+                       f"1/{S} of the full config-2 step per timed step: {n_s} sources + {m_s} "
+                       f"queries through P2M and L2P value+grad, plus a round-robin 1/{S} of "
+                       f"the two level-5 cascades' M2L offsets and M2M/L2L child shifts on "
+                       f"full-size grids; mean of {steps} steps"),
+            "seconds_per_step": t, "seconds_per_full_step": S * t}
 
 
 def run_reference(args, rank: int) -> None:
@@ -184,11 +239,14 @@ def run_reference(args, rank: int) -> None:
     cb = cpu_sample(args.steps, args.warmup, N, M, CFG["seed"])
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * cb["seconds_per_step_extrapolated"],
+            "ms_per_step": 1000.0 * cb["seconds_per_step"],
+            "ms_per_full_step": 1000.0 * cb["seconds_per_full_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD, "N": N, "M": M,
-                                            "parallelism": "cpu"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                                            "parallelism": "cpu",
+                                            "sample_fraction": 1.0 / SAMPLE_SLICES},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                "cpu_model")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -804,8 +862,9 @@ def run_ours(args, rank: int, world: int) -> None:
         line["secondary"] = secondary(dev, flush, stream, args.steps)
         line["training"] = training_lines(dev, flush, stream, args.steps)
     if not args.no_cpu_baseline and not args.small and world == 1:
-        cb = cpu_sample(1, 0, N, M, CFG["seed"])
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = cpu_sample(4, 1, N, M, CFG["seed"])
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                   "cpu_model")}
     print(json.dumps(line), flush=True)
 
 

@@ -58,12 +58,20 @@ def width_of(level: int) -> float:
 
 
 def monos(e: np.ndarray, d: np.ndarray) -> np.ndarray:
-    """Rows d^n/n! (expansion.py:96-113): (m, 3) -> (m, P)."""
-    d = np.atleast_2d(d)
-    out = np.ones((d.shape[0], e.shape[0]))
-    for a in range(3):
-        out *= d[:, a:a + 1] ** e[None, :, a]
-    return out / mi_fact(e)[None, :]
+    """Rows d^n/n! (expansion.py:96-113): (m, 3) -> (m, P), from per-axis power
+    tables by repeated multiplication (the reference's own scheme; ``**`` is
+    several times slower and would understate the CPU baseline)."""
+    d = np.atleast_2d(np.asarray(d, dtype=np.float64))
+    rho = int(e.max()) if e.size else 0
+    pows = np.empty((3, d.shape[0], rho + 1))
+    pows[:, :, 0] = 1.0
+    for k in range(1, rho + 1):
+        pows[:, :, k] = pows[:, :, k - 1] * d.T
+    out = pows[0][:, e[:, 0]]
+    out *= pows[1][:, e[:, 1]]
+    out *= pows[2][:, e[:, 2]]
+    out /= mi_fact(e)[None, :]
+    return out
 
 
 def stencil(reach: int) -> np.ndarray:
@@ -251,7 +259,10 @@ class Oracle:
             else:
                 tgt = tuple(s[0] for s in sl)
                 src = tuple(s[1] for s in sl)
-                out[tgt] += m[src] @ tab["coeffs"][i].T
+                # one contiguous 2-D GEMM per offset, as expansion.py:251-253
+                block = np.ascontiguousarray(m[src])
+                prod = block.reshape(-1, block.shape[-1]) @ tab["coeffs"][i].T
+                out[tgt] += prod.reshape(block.shape)
         return out
 
     def cascade(self, m_fine: np.ndarray) -> np.ndarray:

@@ -540,7 +540,7 @@ class Engine:
     # -- stages -------------------------------------------------------------
 
     def sort_points(self, pts: torch.Tensor, with_points: bool = False,
-                    stable: bool | None = None) -> "CellSort":
+                    stable: bool | None = None, flag: torch.Tensor | None = None) -> "CellSort":
         """Stable sort by finest cell: (order (n,), cell_start (res^3+1,)); with
         ``with_points`` also the inverse permutation and the points in sorted
         order (written by the sort without random reads), which let P2M and the
@@ -563,7 +563,8 @@ class Engine:
                 stable = not bool(_lib.lib().fc2t2_p2m_order_free(self.rho))
             fn = "fc2t2_cell_sort" if stable else "fc2t2_cell_bin"
             _lib.call(fn, self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
-                      _ptr(self.flag.t), _ptr(ws), int(ws_bytes), _stream())
+                      _ptr(self.flag.t if flag is None else flag), _ptr(ws), int(ws_bytes),
+                      _stream())
             return CellSort(order, start)
         inv = torch.empty(n, dtype=torch.int32, device=pts.device)
         pts_sorted = torch.empty((n, 3), dtype=torch.float32, device=pts.device)

@@ -117,8 +117,16 @@ def _early_sort(engine: Engine, qd: torch.Tensor, after=None):
         aux.wait_event(after)
     else:
         aux.wait_stream(cs)
+    # qd is read on aux: keep its block alive until the sort ends even when the
+    # caller drops the result without a backward
+    qd.record_stream(aux)
+    if getattr(engine, "_aux_flag", None) is None:
+        # the aux sort's own domain flag: the forward already checked q on the
+        # compute stream, so this one is never read and can never leak a stale
+        # FLAG_DOMAIN into a later call on the main flag
+        engine._aux_flag = torch.zeros(1, dtype=torch.int32, device=qd.device)
     with torch.cuda.stream(aux):
-        srt = engine.sort_points(qd)
+        srt = engine.sort_points(qd, flag=engine._aux_flag)
         ready = torch.cuda.Event()
         ready.record(aux)
     for t in srt:

@@ -155,7 +155,59 @@ def part_explicit_cfg1():
          w_bar=g.w_bar, p_bar=g.p_bar, q_bar=g.q_bar, t_engine=t1 - t0, t_layer=t2 - t1)
 
 
+def _explicit_at_geometry(name, seed, alpha, levels, rho, n, m, q_sub):
+    """Explicit layer fwd + jvp at a BASELINE config's own geometry (level,
+    alpha, rho), reduced N and M.  Stores values, w_bar, p_bar, q_bar and the
+    device-comparable interaction lists (ref layers.py:167-188,
+    expansion.py:268-281)."""
+    rng = np.random.default_rng(seed)
+    p = q32(rng.uniform(-1, 1, (n, 3)))
+    w = q32(rng.normal(0.0, 0.1, (n, 1)))
+    q = q32(rng.uniform(-1, 1, (m, 3)))
+    yb = q32(rng.normal(size=(m, 1)))
+    t0 = time.time()
+    eng = Engine(KernelModel("gaussian", alpha, rho), levels, lsq=True, check_admissibility=False)
+    t1 = time.time()
+    res = explicit_forward(eng, SourceSet(p, w), q)
+    t2 = time.time()
+    g = explicit_jvp(yb, res)
+    t3 = time.time()
+    print(f"    engine {t1 - t0:.1f}s fwd {t2 - t1:.1f}s jvp {t3 - t2:.1f}s", flush=True)
+    # the forward's finest L grid sampled at q_sub cells (checks the cascade
+    # itself, not only through L2P)
+    data = res.accessor.grid.data
+    cells = rng.integers(0, data.shape[0], (q_sub, 3))
+    out = dict(p=p.astype(np.float32), w=w.astype(np.float32), q=q.astype(np.float32),
+               y_bar=yb.astype(np.float32), values=res.values, w_bar=g.w_bar, p_bar=g.p_bar,
+               q_bar=g.q_bar, L_cells=cells.astype(np.int32),
+               L_rows=data[cells[:, 0], cells[:, 1], cells[:, 2]],
+               alpha=alpha, levels=levels, rho=rho, t_engine=t1 - t0, t_fwd=t2 - t1,
+               t_jvp=t3 - t2, expansion_count=eng.expansion_count)
+    for lvl, t in eng.m2l_tables["far"].items():
+        out[f"far{lvl}_active"] = t.active
+        out[f"far{lvl}_offsets"] = t.offsets.astype(np.int8)
+    out["near_active"] = eng.m2l_tables["near"].active
+    # large float64 outputs stored as float32 (adds <= 6e-8 relative, far
+    # below the 1e-5 gate) to keep the fixture small
+    for k in ("values", "w_bar", "p_bar", "q_bar"):
+        out[k] = out[k].astype(np.float32)
+    save(name, **out)
+
+
+def part_explicit_cfg2():
+    """BASELINE config 2 geometry: level 5 (64^3), alpha 1000, rho 4; 2^16 + 2^16 points."""
+    _explicit_at_geometry("explicit_cfg2", 2022, 1000.0, 5, 4, 1 << 16, 1 << 16, 512)
+
+
+def part_explicit_cfg5():
+    """BASELINE config 5 geometry: level 6 (128^3), alpha 4000, rho 6 (P = 84);
+    2^16 sources, 4096 queries (rho = 6 needs the MAX_ORDER patch above)."""
+    _explicit_at_geometry("explicit_cfg5", 2025, 4000.0, 6, 6, 1 << 16, 4096, 256)
+
+
 PARTS = {
+    "explicit_cfg2": part_explicit_cfg2,
+    "explicit_cfg5": part_explicit_cfg5,
     "multiindex": part_multiindex,
     "find_box": part_find_box,
     "tables": part_tables,
