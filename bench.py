@@ -51,6 +51,11 @@ WORKLOAD = ("cfg2 explicit layer fwd+bwd (w, p, q adjoints): N=2^20 sources, M=1
             "uniform in [-1,1]^3, w~N(0,0.1^2), y_bar~N(0,1), level 5 (64^3), rho=4 (P=35), "
             "gaussian alpha=1000")
 
+CFG5 = dict(N=1 << 24, M=1 << 27, levels=6, rho=6, alpha=4000.0, seed=5)
+WORKLOAD5 = ("cfg5 explicit layer fwd+bwd (w, p, q adjoints), strong scaling: N=2^24 sources, "
+             "M=2^27 queries uniform in [-1,1]^3 split evenly over the ranks, w~N(0,0.1^2), "
+             "y_bar~N(0,1), level 6 (128^3), rho=6 (P=84), gaussian alpha=4000")
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -61,6 +66,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--small", action="store_true", help="reduced sizes for a quick check")
     ap.add_argument("--no-secondary", action="store_true", help="skip configs 1, 3, 4")
+    ap.add_argument("--config", type=int, choices=[2, 5], default=None,
+                    help="2: the headline (default at one GPU); 5: the multi-GPU scaling "
+                         "config (default under torchrun), strong scaling over the ranks")
     return ap.parse_args()
 
 
@@ -142,7 +150,8 @@ def cpu_model() -> str:
 SAMPLE_SLICES = 32   # one CPU step = 1/32 of the full config-2 step's work
 
 
-def cpu_sample(steps: int, warmup: int, N: int, M: int, seed: int) -> dict:
+def cpu_sample(steps: int, warmup: int, N: int, M: int, seed: int, cfg: dict | None = None,
+               slices: int | None = None) -> dict:
     """The reference pipeline restated by the oracle (speed-faithful: power-table
     monomials, one contiguous GEMM per offset -- tests/test_oracle_speed.py
     holds it within 1.3x of the imported reference), timed on a BOUNDED SLICE
@@ -162,9 +171,10 @@ def cpu_sample(steps: int, warmup: int, N: int, M: int, seed: int) -> dict:
     from itertools import product
 
     from oracle.fc2t2_oracle import COARSEST, Oracle, res_of, width_of
-    ora = Oracle(CFG["alpha"], CFG["rho"], CFG["levels"])
-    S = SAMPLE_SLICES
-    L = CFG["levels"]
+    cfg = cfg or CFG
+    ora = Oracle(cfg["alpha"], cfg["rho"], cfg["levels"])
+    S = slices or SAMPLE_SLICES
+    L = cfg["levels"]
     rng = np.random.default_rng(seed + 7)
     # grids of the real sizes (values do not change the arithmetic)
     Mg = {l: rng.standard_normal((res_of(l),) * 3 + (1, ora.P)) for l in range(COARSEST, L + 1)}
@@ -225,26 +235,31 @@ def cpu_sample(steps: int, warmup: int, N: int, M: int, seed: int) -> dict:
     return {"value": (n_s + m_s) / t, "unit": UNIT, "cores": threads, "kind": "port",
             "cpu_model": cpu_model(),
             "sample": (f"oracle (float64 NumPy restatement of the reference, speed-faithful) on "
-                       f"1/{S} of the full config-2 step per timed step: {n_s} sources + {m_s} "
+                       f"1/{S} of the full step per timed step: {n_s} sources + {m_s} "
                        f"queries through P2M and L2P value+grad, plus a round-robin 1/{S} of "
-                       f"the two level-5 cascades' M2L offsets and M2M/L2L child shifts on "
+                       f"the two level-{L} cascades' M2L offsets and M2M/L2L child shifts on "
                        f"full-size grids; mean of {steps} steps"),
+            "slices": S,
             "seconds_per_step": t, "seconds_per_full_step": S * t}
 
 
 def run_reference(args, rank: int) -> None:
     if rank != 0:
         return
-    N, M = CFG["N"], CFG["M"]
-    cb = cpu_sample(args.steps, args.warmup, N, M, CFG["seed"])
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    five = world > 1 or args.config == 5
+    cfg, wl = (CFG5, WORKLOAD5) if five else (CFG, WORKLOAD)
+    N, M = cfg["N"], cfg["M"]
+    cb = cpu_sample(args.steps, args.warmup, N, M, cfg["seed"], cfg, 256 if five else None)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * cb["seconds_per_step"],
             "ms_per_full_step": 1000.0 * cb["seconds_per_full_step"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "N": N, "M": M,
+            "higher_is_better": True, "scaling": "strong" if five else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": wl, "N": N, "M": M,
                                             "parallelism": "cpu",
-                                            "sample_fraction": 1.0 / SAMPLE_SLICES},
+                                            "sample_fraction": 1.0 / cb["slices"]},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
                                                 "cpu_model")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -868,6 +883,132 @@ def run_ours(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_scaling(args, rank: int, world: int) -> None:
+    """BASELINE config 5 as strong scaling: the global problem (N = 2^24
+    sources, M = 2^27 queries) is split over the ranks; every expansion runs
+    the sharded cascade (parallel.py: reduce-scatter into x-slabs, 3-plane
+    halos, slab M2M / M2L / L2L at every level, all-gathers).  value =
+    (N + M) / max over ranks of the device time per step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet, _lib
+    from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
+    from paper_2111_00110_b200.parallel import DeviceBackend, shard_range, sharded, slab_range
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    C5 = dict(CFG5)
+    if args.small:
+        C5.update(N=1 << 18, M=1 << 21)
+    N, M = C5["N"], C5["M"]
+    eng = Engine(KernelModel("gaussian", C5["alpha"], C5["rho"]), C5["levels"],
+                 check_admissibility=False)
+    _ = eng.handle
+    a, b = shard_range(N, rank, world)
+    c, d = shard_range(M, rank, world)
+    gen = torch.Generator(device=dev).manual_seed(C5["seed"] * 1000 + rank)
+    one = 0.99999994
+    P = torch.rand(b - a, 3, device=dev, generator=gen) * (2 * one) - one
+    W = torch.randn(b - a, 1, device=dev, generator=gen) * 0.1
+    Q = torch.rand(d - c, 3, device=dev, generator=gen) * (2 * one) - one
+    YB = torch.randn(d - c, 1, device=dev, generator=gen)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    res = 2 ** (C5["levels"] + 1)
+    sl = slab_range(res, rank, world)
+    split = world == 1 or (sl is not None and DeviceBackend(eng).slab_split_ok(*sl))
+
+    def step(p, w, q, yb):
+        with sharded(eng):
+            r = explicit_forward(eng, SourceSet(p, w), q)
+            return explicit_jvp(yb, r), r
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(P, W, Q, YB)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    gc.collect()
+    gc.disable()
+    with Clocks(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            step(P, W, Q, YB)
+            ev[i][1].record(stream)
+        barrier()
+    gc.enable()
+    launches = (_lib.launch_count() - launches0) // args.steps
+    per = [a_.elapsed_time(b_) for a_, b_ in ev]
+    ms = float(sum(per))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    # e2e: this rank's shard in pinned host memory through the public API
+    hp, hw, hq, hy = (t.cpu().pin_memory() for t in (P, W, Q, YB))
+    del P, W, Q, YB
+    torch.cuda.empty_cache()
+
+    def step_host():
+        g, r = step(hp.to(dev, non_blocking=True), hw.to(dev, non_blocking=True),
+                    hq.to(dev, non_blocking=True), hy.to(dev, non_blocking=True))
+        outs = [x.to("cpu", non_blocking=True) for x in (r.values, g.w_bar, g.p_bar, g.q_bar)]
+        torch.cuda.synchronize()
+        return outs
+    outs = step_host()
+    h2d = sum(x.numel() * 4 for x in (hp, hw, hq, hy))
+    d2h = sum(o.numel() * 4 for o in outs)
+    del outs
+    barrier()
+    k = max(2, args.steps // 4)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    te0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(k):
+        step_host()
+    e1.record(stream)
+    barrier()
+    e2e_ms = max(e0.elapsed_time(e1), 1000.0 * (time.perf_counter() - te0)) / k
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": (N + M) / (ms_step / 1000.0), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "ms_per_step_median_rank0": float(np.median(per)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD5, "N": N, "M": M, "levels": C5["levels"],
+                   "rho": C5["rho"], "alpha": C5["alpha"],
+                   "l2": "inputs 2.4 GB > 126 MB L2, and a 256 MB L2 flush between steps",
+                   "parallelism": (f"dp{world}: reduce-scatter + 3-plane halo + slab cascade "
+                                   f"at every level + all-gathers "
+                                   f"({'NCCL' if world > 1 else 'single GPU'})"),
+                   "slab_cascade_no_replication": bool(split)},
+        "e2e": {"value": (N + M) / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "note": "rank 0's shard bytes; every rank moves its own shard"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -883,6 +1024,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, rank)
+        elif world > 1 or args.config == 5:
+            run_scaling(args, rank, world)
         else:
             run_ours(args, rank, world)
     finally:

@@ -147,6 +147,18 @@ int fc2t2_cell_sort_ex(int level, const float* d_pts, int64_t n, int32_t* d_orde
 int fc2t2_permute_rows(const float* d_src, int64_t n, int cols, const int32_t* d_inv,
                        float* d_dst, void* stream);
 
+/* ---- P2M from unsorted points (Engine.p2m, expansion.py:186-198) ----
+ * d_pts (n, 3), d_w (n, C) in the caller's order; no sort object.  A
+ * deterministic stable partition of the points into bricks of 8 x 8 x 4
+ * cells (8 x 8 x 8 at level 6), then one CTA per brick sums every cell's
+ * points in index order (the np.add.at order) -- no atomics, bit-reproducible.
+ * Sets FLAG_DOMAIN for points outside (-1, 1)^3.  Levels >= 7 fall back to
+ * the stable cell sort + gather P2M below (same results). */
+size_t fc2t2_p2m_points_workspace_size(const fc2t2_engine* e, int channels, int64_t n);
+int fc2t2_p2m_points(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
+                     int64_t n, float* d_m_finest, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                     void* stream);
+
 /* ---- stages (expansion.py:186-264) ---- */
 /* d_order NULL: d_pts / d_w are already in cell-sorted order */
 int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
@@ -180,14 +192,6 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
 int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
                                const double* conv);
 int fc2t2_engine_separable(const fc2t2_engine* e);
-/* Separable far table of a coarse level (3 <= level < levels, res >= 32):
- * the parity stencil minus the hole as three disjoint per-axis pieces (no
- * cancellation against the hole terms).  Includes the offsets the reference
- * prunes (peak interaction < 1e-16, ref kernel.py:275), i.e. differs from the
- * pruned sum by less than 1e-16 of the kernel peak per unit weight.  Same
- * factor layout as fc2t2_engine_set_separable; NULL pointers remove it. */
-int fc2t2_engine_set_separable_far(fc2t2_engine* e, int level, const double* pre,
-                                   const double* post, const double* conv);
 /* 1 (default): the separable M2L's post transform runs after the coarse chain
  * with the finest L2L fused into it (one pass over the finest L grid fewer);
  * 0: separate accumulate-L2L launch.  Results are bit-identical. */
@@ -196,12 +200,34 @@ size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels);
 int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
                  float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream);
 /* Same cascade, but only finest-level cells with x in [x_begin, x_end) are
- * produced (multiples of 4; x_end < 0 = res): the x-slab of one rank in the
- * multi-GPU cascade; the caller all-gathers the slabs.  Other
- * finest cells of d_l_finest are left unspecified.  Same workspace. */
+ * produced (multiples of 4; x_end < 0 = res): one rank's x-slab (SURVEY
+ * 8(e)).  The coarse M2L and L2L run only on the slab's cells at every level
+ * where the slab maps to whole cells (else on the whole level); the M2M chain
+ * runs on the whole grid (d_m_finest must be complete).  Other finest cells
+ * of d_l_finest are left unspecified.  Same workspace. */
 int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_finest,
                       float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
                       void* stream);
+/* The slab cascade in two phases for a reduce-scattered finest M (the
+ * multi-GPU cascade: no level is replicated).
+ *   expand_up:   M2M chain on the slab only (d_m_finest valid on the slab),
+ *                coarse M grids written into the workspace at
+ *                fc2t2_expand_grid_offset(level) (x-slowest, so the slab's
+ *                cells are contiguous); the caller all-gathers every coarse
+ *                level in [fc2t2_expand_lowest, levels) in place;
+ *   expand_down: coarse M2L + L2L on the slab at every level, the finest M2L
+ *                on the slab (d_m_finest valid on [x_begin - 3, x_end + 3):
+ *                the M2L reach, ref kernel.py:39) and the last L2L.
+ * fc2t2_expand_slab_split(x_begin, x_end) = 1 when every coarse level maps
+ * the slab to whole cells (else use fc2t2_expand_slab on a complete M). */
+int fc2t2_expand_up(const fc2t2_engine* e, int channels, const float* d_m_finest, int x_begin,
+                    int x_end, void* d_ws, size_t ws_bytes, void* stream);
+int fc2t2_expand_down(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                      float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
+                      void* stream);
+int fc2t2_expand_lowest(const fc2t2_engine* e);
+int64_t fc2t2_expand_grid_offset(const fc2t2_engine* e, int channels, int level);
+int fc2t2_expand_slab_split(const fc2t2_engine* e, int x_begin, int x_end);
 
 /* ---- L2P: Accessor (expansion.py:335-373) ----
  * d_order (optional, n int32): evaluate the points in this (cell-sorted) order;

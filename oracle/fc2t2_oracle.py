@@ -74,6 +74,13 @@ def monos(e: np.ndarray, d: np.ndarray) -> np.ndarray:
     return out
 
 
+def monos_pow(e: np.ndarray, d: np.ndarray) -> np.ndarray:
+    """The LSQ basis rows d^n/n! exactly as kernel.py:147-153 builds them
+    (generic ``**``; the table fit's pinv amplifies rounding differences)."""
+    d = np.atleast_2d(d)
+    return (d[:, None, :] ** e[None, :, :]).prod(axis=2) / mi_fact(e)[None, :]
+
+
 def stencil(reach: int) -> np.ndarray:
     """meshgrid-'ij' offsets (kernel.py:207-210)."""
     r = np.arange(-reach, reach + 1)
@@ -99,7 +106,7 @@ def lsq_matrix(alpha: float, e: np.ndarray, width: float, off, nodes: int = 6) -
         k = np.arange(nodes)
         x1 = np.cos((2 * k + 1) * np.pi / (2 * nodes)) * (width / 2.0)
         g = np.stack(np.meshgrid(x1, x1, x1, indexing="ij"), axis=-1).reshape(-1, 3)
-        _LSQ_CACHE[key] = (g, np.linalg.pinv(monos(e, g)))
+        _LSQ_CACHE[key] = (g, np.linalg.pinv(monos_pow(e, g)))
     g, Pi = _LSQ_CACHE[key]
     c = np.asarray(off, dtype=np.float64) * width
     diff = c[None, None, :] + g[:, None, :] - g[None, :, :]        # p-node, q-node
@@ -179,8 +186,9 @@ class Oracle:
 
     # P2M (expansion.py:186-198)
     def p2m(self, p: np.ndarray, w: np.ndarray) -> np.ndarray:
-        p = np.atleast_2d(np.asarray(p, dtype=np.float64))
-        w = np.asarray(w, dtype=np.float64).reshape(p.shape[0], -1)
+        p = np.asarray(p, dtype=np.float64).reshape(-1, 3)
+        w = np.asarray(w, dtype=np.float64)
+        w = w.reshape(p.shape[0], w.shape[-1] if w.ndim > 1 else 1)
         res = res_of(self.levels)
         grid = np.zeros((res ** 3, w.shape[1], self.P))
         if p.shape[0]:

@@ -57,6 +57,8 @@ _SIGS = {
     "fc2t2_opt_step": (_i32, [_vp, _vp, _vp, _vp, _i64, _i32, ct.c_float, _i64, ct.c_float,
                               _i32, _vp, _vp]),
     "fc2t2_p2m": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fc2t2_p2m_points_workspace_size": (_sz, [_vp, _i32, _i64]),
+    "fc2t2_p2m_points": (_i32, [_vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "fc2t2_m2m": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "fc2t2_l2l": (_i32, [_vp, _i32, _i32, _vp, _vp, _i32, _vp]),
     "fc2t2_m2l_issued_flops": (ct.c_double, [_vp, _i32, _i32, _i32]),
@@ -64,12 +66,16 @@ _SIGS = {
     "fc2t2_m2l": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _sz, _vp]),
     "fc2t2_engine_set_separable": (_i32, [_vp, _vp, _vp, _vp]),
     "fc2t2_engine_separable": (_i32, [_vp]),
-    "fc2t2_engine_set_separable_far": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "fc2t2_engine_set_sep_fusion": (_i32, [_vp, _i32]),
     "fc2t2_expand_workspace_size": (_sz, [_vp, _i32]),
     "fc2t2_weighted_grad": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "fc2t2_expand": (_i32, [_vp, _i32, _vp, _vp, _vp, _sz, _vp]),
     "fc2t2_expand_slab": (_i32, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _sz, _vp]),
+    "fc2t2_expand_up": (_i32, [_vp, _i32, _vp, _i32, _i32, _vp, _sz, _vp]),
+    "fc2t2_expand_down": (_i32, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _sz, _vp]),
+    "fc2t2_expand_lowest": (_i32, [_vp]),
+    "fc2t2_expand_grid_offset": (_i64, [_vp, _i32, _i32]),
+    "fc2t2_expand_slab_split": (_i32, [_vp, _i32, _i32]),
     "fc2t2_l2p": (_i32, [_i32, _i32, _i32, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
                          _vp, _vp]),
     "fc2t2_ray_last_error": (ct.c_char_p, []),

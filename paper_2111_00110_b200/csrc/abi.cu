@@ -122,8 +122,6 @@ struct fc2t2_engine {
   bool sep = false;
   bool sep_fuse_l2l = true;  // fc2t2_engine_set_sep_fusion
   std::vector<double> sep_pre, sep_post, sep_conv;
-  // separable far tables of coarse levels: level -> {pre, post, conv}
-  std::map<int, std::vector<double>> sep_far;
 };
 
 namespace {
@@ -702,6 +700,40 @@ int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const flo
                      "p2m");
 }
 
+size_t fc2t2_p2m_points_workspace_size(const fc2t2_engine* e, int channels, int64_t n) {
+  if (!e || channels < 1 || n < 0) return 0;
+  if (fc2t2::p2m_brick_supported(e->levels, channels))
+    return fc2t2::p2m_brick_workspace(e->levels, n, channels);
+  // level >= 7: stable cell sort + gather P2M; order and cell starts live in
+  // the workspace after the sort's own scratch
+  const int64_t R = (int64_t)1 << (3 * (e->levels + 1));
+  return fc2t2::cell_sort_workspace(e->levels, n) + 256 + 4 * (size_t)std::max<int64_t>(n, 1) +
+         256 + 4 * (size_t)(R + 1) + 256;
+}
+
+int fc2t2_p2m_points(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
+                     int64_t n, float* d_m_finest, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                     void* stream) {
+  if (!e || channels < 1 || n < 0 || n > INT32_MAX) return fail(FC2T2_EVALUE, "bad p2m arguments");
+  if (ws_bytes < fc2t2_p2m_points_workspace_size(e, channels, n))
+    return fail(FC2T2_EWORKSPACE, "p2m workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (fc2t2::p2m_brick_supported(e->levels, channels))
+    return cuda_status(fc2t2::p2m_brick(e->rho, e->levels, channels, d_pts, d_w, n, d_m_finest,
+                                        d_flag, d_ws, ws_bytes, s),
+                       "p2m_points");
+  const size_t sw = fc2t2::cell_sort_workspace(e->levels, n);
+  char* p = (char*)d_ws + ((sw + 255) & ~(size_t)255);
+  int32_t* order = (int32_t*)p;
+  int32_t* start = (int32_t*)(p + ((4 * (size_t)std::max<int64_t>(n, 1) + 255) & ~(size_t)255));
+  int st = cuda_status(fc2t2::cell_sort(e->levels, d_pts, n, order, start, d_flag, d_ws, sw, s),
+                       "p2m_points sort");
+  if (st != FC2T2_OK) return st;
+  return cuda_status(fc2t2::p2m_sorted(e->rho, e->levels, channels, d_pts, d_w, order, start,
+                                       d_m_finest, s),
+                     "p2m_points");
+}
+
 int fc2t2_m2m(const fc2t2_engine* e, int channels, int fine_level, const float* d_fine,
               float* d_coarse, void* stream) {
   if (!e || channels < 1) return fail(FC2T2_EVALUE, "bad m2m arguments");
@@ -767,45 +799,6 @@ size_t part_floats(const fc2t2_engine* e, const Plan& p, int level, int channels
   return sp > 1 ? (size_t)sp * grid_floats(level, channels, e->PP) : 0;
 }
 
-struct ExpandLayout {
-  size_t coarse_grids = 0, fine_part = 0, coarse_part = 0;
-  size_t total() const { return coarse_grids + fine_part + coarse_part; }
-};
-
-ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
-  ExpandLayout w;
-  const int L = e->levels;
-  for (int l = kCoarsest; l < L; ++l) {
-    w.coarse_grids += 2 * grid_floats(l, channels, e->PP);
-    const size_t need = e->sep_far.count(l)
-                            ? fc2t2::m2l_sep_workspace_floats(e->rho, l, channels, true)
-                            : part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels);
-    w.coarse_part = std::max(w.coarse_part, need);
-  }
-  w.fine_part = e->sep ? fc2t2::m2l_sep_workspace_floats(e->rho, L, channels)
-                       : part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
-  return w;
-}
-
-// one level's M2L (tcgen05 or FFMA split-K) into Lg, using scratch `part`
-// x_begin/x_end restrict the tcgen05 path's targets to an x-slab of cells
-// (fc2t2_expand_slab); the FFMA path always covers the whole grid.
-int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const float* M, float* Lg,
-              int accumulate, float* part, cudaStream_t s, int x_begin = 0, int x_end = -1) {
-  int st;
-  if (use_tc(p, l)) {
-    const fc2t2::TCPlan tp = tc_of(e, p, l);
-    st = cuda_status(fc2t2::tc_prepare(e->rho, channels, tp, M, part, s), "expand split");
-    if (st != FC2T2_OK) return st;
-    return cuda_status(
-        fc2t2::m2l_tc(e->rho, channels, tp, part, Lg, accumulate, s, x_begin, x_end),
-        "expand m2l_tc");
-  }
-  const fc2t2::M2LLaunch ml = launch_of(p, l);
-  return cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, M, Lg, accumulate, s, part,
-                                fc2t2::m2l_splits(e->rho, channels, ml)),
-                     "expand m2l");
-}
 }  // namespace
 
 int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
@@ -828,87 +821,153 @@ int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double*
 
 int fc2t2_engine_separable(const fc2t2_engine* e) { return e && e->sep ? 1 : 0; }
 
-int fc2t2_engine_set_separable_far(fc2t2_engine* e, int level, const double* pre,
-                                   const double* post, const double* conv) {
-  if (!e) return fail(FC2T2_EVALUE, "null engine");
-  if (!pre || !post || !conv) {
-    e->sep_far.erase(level);
-    return FC2T2_OK;
-  }
-  const int res = 1 << (level + 1);
-  if (e->rho > 5 || level <= kCoarsest || level >= e->levels || res % 32)
-    return fail(FC2T2_EVALUE, "separable far M2L needs rho <= 5 and a coarse level of >= 32 cells");
-  const int R1 = e->rho + 1;
-  std::vector<double> f(9 * R1 * R1);
-  std::copy(pre, pre + R1 * R1, f.begin());
-  std::copy(post, post + R1 * R1, f.begin() + R1 * R1);
-  std::copy(conv, conv + 7 * R1 * R1, f.begin() + 2 * R1 * R1);
-  e->sep_far[level] = std::move(f);
-  return FC2T2_OK;
-}
-
 int fc2t2_engine_set_sep_fusion(fc2t2_engine* e, int fuse_l2l) {
   if (!e) return fail(FC2T2_EVALUE, "null engine");
   e->sep_fuse_l2l = fuse_l2l != 0;
   return FC2T2_OK;
 }
 
+namespace {
+struct ExpandLayout {
+  size_t coarse_grids = 0, fine_part = 0, coarse_part = 0;
+  size_t total() const { return coarse_grids + fine_part + coarse_part; }
+};
+
+ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
+  ExpandLayout w;
+  const int L = e->levels;
+  for (int l = kCoarsest; l < L; ++l) {
+    w.coarse_grids += 2 * grid_floats(l, channels, e->PP);
+    w.coarse_part = std::max(w.coarse_part,
+                             part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels));
+  }
+  w.fine_part = e->sep ? fc2t2::m2l_sep_workspace_floats(e->rho, L, channels)
+                       : part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
+  return w;
+}
+
+// one level's M2L (tcgen05 or FFMA split-K) into Lg, using scratch `part`,
+// for target cells with x in [x_begin, x_end)
+int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const float* M, float* Lg,
+              int accumulate, float* part, cudaStream_t s, int x_begin = 0, int x_end = -1) {
+  int st;
+  if (use_tc(p, l)) {
+    const fc2t2::TCPlan tp = tc_of(e, p, l);
+    st = cuda_status(fc2t2::tc_prepare(e->rho, channels, tp, M, part, s), "expand split");
+    if (st != FC2T2_OK) return st;
+    return cuda_status(
+        fc2t2::m2l_tc(e->rho, channels, tp, part, Lg, accumulate, s, x_begin, x_end),
+        "expand m2l_tc");
+  }
+  const fc2t2::M2LLaunch ml = launch_of(p, l);
+  return cuda_status(fc2t2::m2l(e->rho, channels, ml, e->d_coef, M, Lg, accumulate, s, part,
+                                fc2t2::m2l_splits(e->rho, channels, ml), x_begin, x_end),
+                     "expand m2l");
+}
+
+// lowest level whose far table does any work (coarser grids are unused)
+int lowest_level(const fc2t2_engine* e) {
+  const int L = e->levels;
+  for (int l = kCoarsest; l <= L; ++l) {
+    const int table = (l == L) ? FC2T2_TABLE_FARNEAR : FC2T2_TABLE_FAR;
+    if (e->plans.at(l).at(table).max_list > 0) return l;
+  }
+  return L;
+}
+
+// the finest x-slab [x0, x1) seen at level l: [x0, x1) >> (L - l), or the
+// whole level when the slab does not map to whole cells there (or to the
+// 4-cell granularity of the tcgen05 kernel / the 2-cell parity stride)
+void level_slab(const fc2t2_engine* e, int l, int x0, int x1, int* b, int* en) {
+  const int L = e->levels, sh = L - l, res = 1 << (l + 1);
+  int lb = x0 >> sh, le = x1 >> sh;
+  bool ok = ((x0 >> sh) << sh) == x0 && ((x1 >> sh) << sh) == x1 && le > lb;
+  if (ok && l > kCoarsest && l < L) {
+    const Plan& p = e->plans.at(l).at(FC2T2_TABLE_FAR);
+    if (use_tc(p, l)) ok = lb % 4 == 0 && le % 4 == 0;
+    else ok = lb % 2 == 0 && le % 2 == 0;
+  }
+  if (!ok) {
+    lb = 0;
+    le = res;
+  }
+  *b = lb;
+  *en = le;
+}
+
+struct Grids {
+  std::vector<float*> M, L;
+  float *fine_part = nullptr, *coarse_part = nullptr;
+};
+
+Grids carve_grids(const fc2t2_engine* e, int channels, const float* d_m, float* d_l, void* d_ws) {
+  const int L = e->levels;
+  const ExpandLayout lay = expand_layout(e, channels);
+  Grids g;
+  g.M.assign(L + 1, nullptr);
+  g.L.assign(L + 1, nullptr);
+  float* w = (float*)d_ws;
+  for (int l = kCoarsest; l < L; ++l) {
+    g.M[l] = w;
+    w += grid_floats(l, channels, e->PP);
+    g.L[l] = w;
+    w += grid_floats(l, channels, e->PP);
+  }
+  g.M[L] = const_cast<float*>(d_m);
+  g.L[L] = d_l;
+  g.fine_part = w;
+  g.coarse_part = w + lay.fine_part;
+  return g;
+}
+
+enum Phase { PH_ALL = 0, PH_UP = 1, PH_DOWN = 2 };
+
+}  // namespace
+
 size_t fc2t2_expand_workspace_size(const fc2t2_engine* e, int channels) {
   if (!e || !e->uploaded || channels < 1) return 0;
   return expand_layout(e, channels).total() * sizeof(float) + 256;
 }
 
-// L_finest = M2L_finest(M_finest) + L2L(L_{finest-1}); the coarse chain
-// (M2M down, then per level L2L + M2L) and the finest M2L are independent, so
-// the finest M2L runs on the engine's side stream (fork/join by events) and
-// the coarse kernels fill the SMs its last wave leaves idle.  The summation
-// order is fixed (M2L written first, L2L accumulated after the join), so
-// results do not depend on the overlap.
-int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
-                 float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream) {
-  return fc2t2_expand_slab(e, channels, d_m_finest, d_l_finest, 0, -1, d_ws, ws_bytes, stream);
-}
-
-// Only the finest-level cells with x in [x_begin, x_end) are guaranteed (the
-// rest of d_l_finest is unspecified): the multi-GPU cascade gives each rank an
-// x-slab of the dominant finest-level M2L and all-gathers the slabs.
-int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_finest,
-                      float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
-                      void* stream) {
+namespace {
+// The cascade (Engine.expand_from_moments, ref expansion.py:268-281) for the
+// finest targets with x in [x0, x1):
+//   UP    M2M chain, each coarse level only on the slab's cells (the caller
+//         all-gathers the coarse M grids afterwards, fc2t2_expand_grid_offset)
+//   DOWN  coarse M2L + L2L on the slab at every level, finest M2L on the slab
+//         (needs the finest M on [x0 - 3, x1 + 3)), final L2L
+//   ALL   full M2M chain, then DOWN (the finest M is complete on entry)
+// L_finest = M2L_finest(M_finest) + L2L(L_{finest-1}).  The coarse chain and
+// the finest M2L are independent, so the finest M2L runs on the engine's side
+// stream (fork/join events) and the coarse kernels fill the SMs its last wave
+// leaves idle.  The summation order is fixed (M2L written first, L2L
+// accumulated after the join), so results do not depend on the overlap.
+int expand_phase(const fc2t2_engine* e, int channels, const float* d_m_finest, float* d_l_finest,
+                 int x0, int x1, void* d_ws, size_t ws_bytes, cudaStream_t s, Phase ph) {
   if (!e || !e->uploaded) return fail(FC2T2_ESTAGE, "engine tables not uploaded");
   if (channels < 1) return fail(FC2T2_EVALUE, "channels must be >= 1");
   const int res_f = 1 << (e->levels + 1);
-  if (x_end < 0) x_end = res_f;
-  if (x_begin < 0 || x_end > res_f || x_begin > x_end || x_begin % 4 || x_end % 4)
+  if (x1 < 0) x1 = res_f;
+  if (x0 < 0 || x1 > res_f || x0 > x1 || x0 % 4 || x1 % 4)
     return fail(FC2T2_EVALUE, "slab bounds must be multiples of 4 inside [0, res]");
   if (ws_bytes < fc2t2_expand_workspace_size(e, channels))
     return fail(FC2T2_EWORKSPACE, "expand workspace too small");
-  cudaStream_t s = (cudaStream_t)stream;
   const int L = e->levels;
-  const ExpandLayout lay = expand_layout(e, channels);
-  std::vector<float*> Mg(L + 1, nullptr), Lg(L + 1, nullptr);
-  float* w = (float*)d_ws;
-  for (int l = kCoarsest; l < L; ++l) {
-    Mg[l] = w;
-    w += grid_floats(l, channels, e->PP);
-    Lg[l] = w;
-    w += grid_floats(l, channels, e->PP);
-  }
-  Mg[L] = const_cast<float*>(d_m_finest);
-  Lg[L] = d_l_finest;
-  float* fine_part = w;
-  float* coarse_part = w + lay.fine_part;
-  // lowest level whose far table does any work (coarser M grids are unused)
-  int lowest = L;
-  for (int l = kCoarsest; l <= L; ++l) {
-    const int table = (l == L) ? FC2T2_TABLE_FARNEAR : FC2T2_TABLE_FAR;
-    if (e->plans.at(l).at(table).max_list > 0) {
-      lowest = l;
-      break;
-    }
-  }
+  Grids G = carve_grids(e, channels, d_m_finest, d_l_finest, d_ws);
+  const int lowest = lowest_level(e);
   const Plan& pL = e->plans.at(L).at(FC2T2_TABLE_FARNEAR);
   const bool fine = pL.max_list > 0, coarse = lowest < L;
+  int st;
+  if (ph == PH_UP) {
+    for (int l = L; l > lowest; --l) {
+      int cb, ce;
+      level_slab(e, l - 1, x0, x1, &cb, &ce);
+      st = cuda_status(fc2t2::m2m(e->rho, l, channels, G.M[l], G.M[l - 1], s, cb, ce),
+                       "expand m2m");
+      if (st != FC2T2_OK) return st;
+    }
+    return FC2T2_OK;
+  }
   // FC2T2_SERIAL_CASCADE=1 keeps everything on the caller's stream (clean
   // per-kernel event timings for profiling)
   static const bool serial = [] {
@@ -916,7 +975,6 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
     return v && v[0] == '1';
   }();
   const bool overlap = fine && coarse && e->side && !serial;
-  int st;
   if (overlap) {
     st = cuda_status(cudaEventRecord(e->fork, s), "expand fork");
     if (st == FC2T2_OK) st = cuda_status(cudaStreamWaitEvent(e->side, e->fork, 0), "expand fork");
@@ -925,20 +983,16 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
   // separable finest M2L with the coarse chain present: its post transform
   // runs after the join with the last L2L fused into it
   const bool sep_fused = fine && e->sep && coarse && e->sep_fuse_l2l;
-  if (fine && e->sep) {
-    st = cuda_status(fc2t2::m2l_sep(e->rho, L, channels, e->sep_pre.data(), e->sep_post.data(),
-                                    e->sep_conv.data(), Mg[L], Lg[L], fine_part, x_begin, x_end,
-                                    overlap ? e->side : s,
-                                    sep_fused ? fc2t2::SEP_FRONT : fc2t2::SEP_ALL),
-                     "expand m2l_sep");
-    if (st != FC2T2_OK) return st;
-    if (overlap) {
-      st = cuda_status(cudaEventRecord(e->join, e->side), "expand join");
-      if (st != FC2T2_OK) return st;
-    }
-  } else if (fine) {
-    st = level_m2l(e, channels, L, pL, Mg[L], Lg[L], 0, fine_part, overlap ? e->side : s,
-                   x_begin, x_end);
+  if (fine) {
+    if (e->sep)
+      st = cuda_status(fc2t2::m2l_sep(e->rho, L, channels, e->sep_pre.data(), e->sep_post.data(),
+                                      e->sep_conv.data(), G.M[L], G.L[L], G.fine_part, x0, x1,
+                                      overlap ? e->side : s,
+                                      sep_fused ? fc2t2::SEP_FRONT : fc2t2::SEP_ALL),
+                       "expand m2l_sep");
+    else
+      st = level_m2l(e, channels, L, pL, G.M[L], G.L[L], 0, G.fine_part, overlap ? e->side : s,
+                     x0, x1);
     if (st != FC2T2_OK) return st;
     if (overlap) {
       st = cuda_status(cudaEventRecord(e->join, e->side), "expand join");
@@ -946,38 +1000,29 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
     }
   }
   if (coarse) {
-    for (int l = L; l > lowest; --l) {
-      st = cuda_status(fc2t2::m2m(e->rho, l, channels, Mg[l], Mg[l - 1], s), "expand m2m");
-      if (st != FC2T2_OK) return st;
-    }
+    if (ph == PH_ALL)
+      for (int l = L; l > lowest; --l) {
+        st = cuda_status(fc2t2::m2m(e->rho, l, channels, G.M[l], G.M[l - 1], s), "expand m2m");
+        if (st != FC2T2_OK) return st;
+      }
     bool have = false;
     for (int l = lowest; l < L; ++l) {
       const Plan& p = e->plans.at(l).at(FC2T2_TABLE_FAR);
-      auto sf = e->sep_far.find(l);
-      if (p.max_list > 0 && sf != e->sep_far.end()) {
-        // separable far table, its post transform with this level's L2L fused
-        const int R1 = e->rho + 1;
-        const double* f = sf->second.data();
-        st = cuda_status(fc2t2::m2l_sep(e->rho, l, channels, f, f + R1 * R1, f + 2 * R1 * R1,
-                                        Mg[l], Lg[l], coarse_part, 0, -1, s, fc2t2::SEP_ALL,
-                                        have ? Lg[l - 1] : nullptr, true),
-                         "expand m2l_sep far");
-        if (st != FC2T2_OK) return st;
-        have = true;
-        continue;
-      }
+      int lb, le;
+      level_slab(e, l, x0, x1, &lb, &le);
       if (have) {
-        st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, Lg[l - 1], Lg[l], 0, s), "expand l2l");
+        st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, G.L[l - 1], G.L[l], 0, s, lb, le),
+                         "expand l2l");
         if (st != FC2T2_OK) return st;
       }
       if (p.max_list > 0) {
-        st = level_m2l(e, channels, l, p, Mg[l], Lg[l], have ? 1 : 0, coarse_part, s);
+        st = level_m2l(e, channels, l, p, G.M[l], G.L[l], have ? 1 : 0, G.coarse_part, s, lb, le);
         if (st != FC2T2_OK) return st;
         have = true;
-      } else if (have == false) {
+      } else if (!have) {
         // nothing at this level yet: the next L2L needs a zero grid
         st = cuda_status(
-            cudaMemsetAsync(Lg[l], 0, grid_floats(l, channels, e->PP) * sizeof(float), s),
+            cudaMemsetAsync(G.L[l], 0, grid_floats(l, channels, e->PP) * sizeof(float), s),
             "expand zero");
         if (st != FC2T2_OK) return st;
         have = true;
@@ -989,20 +1034,74 @@ int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_fine
     }
     if (sep_fused)
       st = cuda_status(fc2t2::m2l_sep(e->rho, L, channels, e->sep_pre.data(), e->sep_post.data(),
-                                      e->sep_conv.data(), Mg[L], Lg[L], fine_part, x_begin, x_end,
-                                      s, fc2t2::SEP_POST, Lg[L - 1]),
+                                      e->sep_conv.data(), G.M[L], G.L[L], G.fine_part, x0, x1, s,
+                                      fc2t2::SEP_POST, G.L[L - 1]),
                        "expand m2l_sep post+l2l");
     else
-      st = cuda_status(fc2t2::l2l(e->rho, L - 1, channels, Lg[L - 1], Lg[L], fine ? 1 : 0, s),
-                       "expand l2l");
+      st = cuda_status(
+          fc2t2::l2l(e->rho, L - 1, channels, G.L[L - 1], G.L[L], fine ? 1 : 0, s, x0, x1),
+          "expand l2l");
     if (st != FC2T2_OK) return st;
   } else if (!fine) {
-    st = cuda_status(
-        cudaMemsetAsync(Lg[L], 0, grid_floats(L, channels, e->PP) * sizeof(float), s),
-        "expand zero");
+    const size_t plane = (size_t)res_f * res_f * channels * e->PP;
+    st = cuda_status(cudaMemsetAsync(G.L[L] + (size_t)x0 * plane, 0,
+                                     (size_t)(x1 - x0) * plane * sizeof(float), s),
+                     "expand zero");
     if (st != FC2T2_OK) return st;
   }
   return FC2T2_OK;
+}
+}  // namespace
+
+int fc2t2_expand(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                 float* d_l_finest, void* d_ws, size_t ws_bytes, void* stream) {
+  return expand_phase(e, channels, d_m_finest, d_l_finest, 0, -1, d_ws, ws_bytes,
+                      (cudaStream_t)stream, PH_ALL);
+}
+
+int fc2t2_expand_slab(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                      float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
+                      void* stream) {
+  return expand_phase(e, channels, d_m_finest, d_l_finest, x_begin, x_end, d_ws, ws_bytes,
+                      (cudaStream_t)stream, PH_ALL);
+}
+
+int fc2t2_expand_up(const fc2t2_engine* e, int channels, const float* d_m_finest, int x_begin,
+                    int x_end, void* d_ws, size_t ws_bytes, void* stream) {
+  return expand_phase(e, channels, d_m_finest, nullptr, x_begin, x_end, d_ws, ws_bytes,
+                      (cudaStream_t)stream, PH_UP);
+}
+
+int fc2t2_expand_down(const fc2t2_engine* e, int channels, const float* d_m_finest,
+                      float* d_l_finest, int x_begin, int x_end, void* d_ws, size_t ws_bytes,
+                      void* stream) {
+  return expand_phase(e, channels, d_m_finest, d_l_finest, x_begin, x_end, d_ws, ws_bytes,
+                      (cudaStream_t)stream, PH_DOWN);
+}
+
+int fc2t2_expand_lowest(const fc2t2_engine* e) {
+  if (!e || !e->uploaded) return -1;
+  return lowest_level(e);
+}
+
+int64_t fc2t2_expand_grid_offset(const fc2t2_engine* e, int channels, int level) {
+  if (!e || !e->uploaded || channels < 1 || level < kCoarsest || level >= e->levels) return -1;
+  size_t off = 0;
+  for (int l = kCoarsest; l < level; ++l) off += 2 * grid_floats(l, channels, e->PP);
+  return (int64_t)(off * sizeof(float));
+}
+
+int fc2t2_expand_slab_split(const fc2t2_engine* e, int x_begin, int x_end) {
+  if (!e || !e->uploaded) return 0;
+  const int L = e->levels, res_f = 1 << (L + 1);
+  if (x_end < 0) x_end = res_f;
+  if (x_begin < 0 || x_end > res_f || x_begin >= x_end || x_begin % 4 || x_end % 4) return 0;
+  for (int l = lowest_level(e); l < L; ++l) {
+    int b, en;
+    level_slab(e, l, x_begin, x_end, &b, &en);
+    if (b == 0 && en == (1 << (l + 1)) && !(x_begin == 0 && x_end == res_f)) return 0;
+  }
+  return 1;
 }
 
 int fc2t2_weighted_grad(const float* d_grad, const float* d_w, int64_t n, int channels,

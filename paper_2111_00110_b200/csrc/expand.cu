@@ -187,11 +187,10 @@ p2m_fixed_kernel(const float* __restrict__ pts, const float* __restrict__ w, int
 template <int RHO>
 __global__ void __launch_bounds__(128)
 m2m_kernel(const float* __restrict__ fine, float* __restrict__ coarse, int C, int cres,
-           float half_fine) {
+           float half_fine, int64_t g0, int64_t g1) {
   constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
   const int fres = 2 * cres;
-  const int64_t n = (int64_t)cres * cres * cres * C;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+  for (int64_t g = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < g1;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cell = g / C;
     const int c = (int)(g - cell * C);
@@ -220,11 +219,10 @@ m2m_kernel(const float* __restrict__ fine, float* __restrict__ coarse, int C, in
 template <int RHO>
 __global__ void __launch_bounds__(128)
 l2l_kernel(const float* __restrict__ coarse, float* __restrict__ fine, int C, int cres,
-           float half_fine, int accumulate) {
+           float half_fine, int accumulate, int64_t g0, int64_t g1) {
   constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
   const int fres = 2 * cres;
-  const int64_t n = (int64_t)fres * fres * fres * C;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
+  for (int64_t g = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < g1;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t cell = g / C;
     const int c = (int)(g - cell * C);
@@ -258,7 +256,7 @@ __global__ void __launch_bounds__(M2L_THREADS, (RHO <= 4 ? 2 : 1))
 m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int res, int stride,
                 int nu, const int4* __restrict__ entries, const int* __restrict__ cls_start,
                 const float* __restrict__ coef, int accumulate, float* __restrict__ part,
-                int64_t part_stride) {
+                int64_t part_stride, int64_t u_begin, int64_t u_end) {
   constexpr int PP = MI<RHO>::PP;
   constexpr int NQ = PP / 4;
   constexpr int ROWS = M2L_THREADS * RPL;
@@ -272,8 +270,8 @@ m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int r
   const int oy = stride == 2 ? (cls >> 1) & 1 : 0;
   const int oz = stride == 2 ? cls & 1 : 0;
   const int tpt = ROWS / C;
-  const int64_t ntgt = (int64_t)nu * nu * nu;
-  const int64_t t0 = (int64_t)blockIdx.x * tpt;
+  const int64_t ntgt = u_end;
+  const int64_t t0 = u_begin + (int64_t)blockIdx.x * tpt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   for (int r = tid; r < ROWS; r += M2L_THREADS) {
@@ -374,8 +372,9 @@ m2l_ffma_kernel(const float* __restrict__ M, float* __restrict__ L, int C, int r
 }
 
 __global__ void m2l_reduce_kernel(float4* __restrict__ L, const float4* __restrict__ part,
-                                  int64_t n4, int64_t stride4, int splits, int accumulate) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+                                  int64_t i0, int64_t n4, int64_t stride4, int splits,
+                                  int accumulate) {
+  for (int64_t i = i0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 s = accumulate ? L[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     for (int z = 0; z < splits; ++z) {
@@ -427,24 +426,31 @@ cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float*
 }
 
 cudaError_t m2m(int rho, int fine_level, int C, const float* fine, float* coarse,
-                cudaStream_t s) {
+                cudaStream_t s, int cx_begin, int cx_end) {
   const int cres = 1 << fine_level;  // res of fine_level - 1
-  const int64_t n = (int64_t)cres * cres * cres * C;
+  if (cx_end < 0) cx_end = cres;
+  const int64_t plane = (int64_t)cres * cres * C;
+  const int64_t g0 = cx_begin * plane, g1 = cx_end * plane;
+  if (g1 <= g0) return cudaSuccess;
   const float half_fine = (float)(0.5 * 2.0 / (double)(2 * cres));
   FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("m2m", s,
-      m2m_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(fine, coarse, C, cres,
-                                                                    half_fine)));
+      m2m_kernel<RHO><<<grid_blocks(g1 - g0, 128, 148 * 64), 128, 0, s>>>(fine, coarse, C, cres,
+                                                                          half_fine, g0, g1)));
   return cudaGetLastError();
 }
 
 cudaError_t l2l(int rho, int coarse_level, int C, const float* coarse, float* fine,
-                int accumulate, cudaStream_t s) {
+                int accumulate, cudaStream_t s, int fx_begin, int fx_end) {
   const int cres = 1 << (coarse_level + 1);
-  const int64_t n = (int64_t)8 * cres * cres * cres * C;
+  const int fres = 2 * cres;
+  if (fx_end < 0) fx_end = fres;
+  const int64_t plane = (int64_t)fres * fres * C;
+  const int64_t g0 = fx_begin * plane, g1 = fx_end * plane;
+  if (g1 <= g0) return cudaSuccess;
   const float half_fine = (float)(0.5 * 2.0 / (double)(2 * cres));
   FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("l2l", s,
-      l2l_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(coarse, fine, C, cres,
-                                                                    half_fine, accumulate)));
+      l2l_kernel<RHO><<<grid_blocks(g1 - g0, 128, 148 * 64), 128, 0, s>>>(
+          coarse, fine, C, cres, half_fine, accumulate, g0, g1)));
   return cudaGetLastError();
 }
 
@@ -471,9 +477,16 @@ int m2l_splits(int rho, int C, const M2LLaunch& plan) {
 }
 
 cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
-                float* L, int accumulate, cudaStream_t s, float* part, int splits) {
+                float* L, int accumulate, cudaStream_t s, float* part, int splits, int x_begin,
+                int x_end) {
   const int res = 1 << (plan.level + 1);
   const int nu = res / plan.stride;
+  if (x_end < 0) x_end = res;
+  // targets with x in [x_begin, x_end): class-lattice x in [x_begin, x_end) / stride
+  if (x_begin % plan.stride || x_end % plan.stride) return cudaErrorInvalidValue;
+  const int64_t u_begin = (int64_t)(x_begin / plan.stride) * nu * nu;
+  const int64_t u_end = (int64_t)(x_end / plan.stride) * nu * nu;
+  if (u_end <= u_begin) return cudaSuccess;
   if (!part) splits = 1;
   const int64_t grid_f = (int64_t)res * res * res * C * pad4(index_count(rho));
   FC2T2_DISPATCH_RHO(rho, {
@@ -481,7 +494,6 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
     constexpr int ROWS = M2L_THREADS * RPL;
     if (C > ROWS) return cudaErrorNotSupported;
     const int tpt = ROWS / C;
-    const int64_t ntgt = (int64_t)nu * nu * nu;
     const size_t smem = m2l_smem<RHO>();
     auto kern = m2l_ffma_kernel<RHO, RPL>;
     static unsigned long long attr = 0;   // devices configured (per instantiation)
@@ -490,17 +502,19 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
                                            (int)smem);
       if (e != cudaSuccess) return e;
     }
-    dim3 grid((unsigned)((ntgt + tpt - 1) / tpt), (unsigned)plan.ncls, (unsigned)splits);
+    dim3 grid((unsigned)((u_end - u_begin + tpt - 1) / tpt), (unsigned)plan.ncls, (unsigned)splits);
     FC2T2_LAUNCH(plan.level_name, s,
                  kern<<<grid, M2L_THREADS, smem, s>>>(M, L, C, res, plan.stride, nu, plan.entries,
                                                       plan.cls_start, coef, accumulate, part,
-                                                      grid_f));
+                                                      grid_f, u_begin, u_end));
   });
   if (splits > 1) {
-    const int64_t n4 = grid_f / 4;
+    // the slab's rows are contiguous: cells x in [x_begin, x_end)
+    const int64_t row4 = (int64_t)res * res * C * pad4(index_count(rho)) / 4;
+    const int64_t i0 = x_begin * row4, i1 = x_end * row4;
     FC2T2_LAUNCH("m2l_reduce", s,
-                 m2l_reduce_kernel<<<grid_blocks(n4, 256, 148 * 16), 256, 0, s>>>(
-                     (float4*)L, (const float4*)part, n4, grid_f / 4, splits, accumulate));
+                 m2l_reduce_kernel<<<grid_blocks(i1 - i0, 256, 148 * 16), 256, 0, s>>>(
+                     (float4*)L, (const float4*)part, i0, i1, grid_f / 4, splits, accumulate));
   }
   return cudaGetLastError();
 }

@@ -27,6 +27,14 @@ size_t scan_ws_words(int64_t n);
 cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* ws,
                            cudaStream_t s);
 
+// p2m_brick.cu -------------------------------------------------------------
+// P2M straight from unsorted points: deterministic stable partition into
+// 8 x 8 x (4|8) cell bricks + one CTA per brick (levels 2..6, C <= 8)
+bool p2m_brick_supported(int level, int C);
+size_t p2m_brick_workspace(int level, int64_t n, int C);
+cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* w, int64_t n,
+                      float* M, int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s);
+
 // expand.cu --------------------------------------------------------------
 // true (FC2T2_P2M_FIXED=1, rho <= 5): P2M sums exactly in fixed point (order
 // free: a cell sort without the per-cell index sort suffices); false
@@ -35,9 +43,12 @@ bool p2m_fixed_point(int rho);
 cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float* w,
                        const int32_t* order, const int32_t* cell_start, float* M,
                        cudaStream_t s);
-cudaError_t m2m(int rho, int fine_level, int C, const float* fine, float* coarse, cudaStream_t s);
+// x ranges (cells of the output level, x_end < 0 = all) restrict the
+// outputs to one x-slab (the multi-GPU cascade)
+cudaError_t m2m(int rho, int fine_level, int C, const float* fine, float* coarse, cudaStream_t s,
+                int cx_begin = 0, int cx_end = -1);
 cudaError_t l2l(int rho, int coarse_level, int C, const float* coarse, float* fine,
-                int accumulate, cudaStream_t s);
+                int accumulate, cudaStream_t s, int fx_begin = 0, int fx_end = -1);
 
 // One M2L launch: every target class (8 parity classes, or 1 for a
 // parity-free stencil) walks its own interaction list.
@@ -53,8 +64,11 @@ struct M2LLaunch {
 // splits > 1 (with a workspace ``part`` of splits * grid floats) splits each
 // class's interaction list across CTAs for small levels; m2l_splits picks it.
 int m2l_splits(int rho, int C, const M2LLaunch& plan);
+// targets restricted to cells with x in [x_begin, x_end) (multiples of the
+// stencil stride; x_end < 0 = all)
 cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const float* M,
-                float* L, int accumulate, cudaStream_t s, float* part = nullptr, int splits = 1);
+                float* L, int accumulate, cudaStream_t s, float* part = nullptr, int splits = 1,
+                int x_begin = 0, int x_end = -1);
 
 // m2l_tc.cu --------------------------------------------------------------
 // tcgen05 M2L for parity levels.  btab is the plan's dense table:

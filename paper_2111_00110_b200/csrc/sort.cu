@@ -67,33 +67,6 @@ __global__ void find_box_kernel(const float* __restrict__ pts, int64_t n, int re
 // Exclusive scan of uint32, three phases (tile scan, scan of tile sums,
 // add-back), recursion on the tile sums.
 
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot,
-                                                         uint32_t& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    warp_tot[lane] = t;  // inclusive warp prefix
-  }
-  __syncthreads();
-  total = warp_tot[(blockDim.x >> 5) - 1];
-  uint32_t before = warp > 0 ? warp_tot[warp - 1] : 0u;
-  __syncthreads();
-  return before + x - v;
-}
-
 __global__ void scan_tiles_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                   int64_t n, uint32_t* __restrict__ tile_sums) {
   __shared__ uint32_t warp_tot[32];

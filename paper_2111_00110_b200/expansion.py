@@ -30,7 +30,7 @@ import torch
 
 from . import _lib, flops
 from .kernel import (COARSEST_LEVEL, KernelModel, M2LTable, fit_m2l_tables,
-                     separable_eligible, separable_factors, separable_far_eligible,
+                     separable_eligible, separable_factors,
                      level_box_width, level_resolution)
 from .multiindex import MultiIndexTable
 
@@ -198,6 +198,7 @@ class DomainFlag:
     def __init__(self):
         self.t = torch.zeros(1, dtype=torch.int32, device=_device())
         self._defer = 0
+        self.reduce_hook = None     # parallel.sharded: max of the flag over the ranks
         self._host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._side = None
         self._mark = None
@@ -241,6 +242,8 @@ class DomainFlag:
             v = int(self._host[0])
         else:
             v = int(self.t.item())
+        if self.reduce_hook is not None:
+            v = self.reduce_hook(v)
         if v & _lib.FLAG_DOMAIN:
             self.t.zero_()      # stream-ordered: after the call's trailing kernels too
             raise DomainError(f"{what} locations must lie strictly inside (-1, 1)^3")
@@ -407,29 +410,6 @@ class _Handle:
             pass
 
 
-class CellSort(tuple):
-    """(order, cell_start) of a stable cell sort (unpacks like a 2-tuple);
-    ``inv`` / ``pts_sorted`` when the sort produced sorted points, and a cache
-    of per-point arrays already permuted into sorted order."""
-
-    def __new__(cls, order, start, inv=None, pts_sorted=None):
-        t = super().__new__(cls, (order, start))
-        t.inv = inv
-        t.pts_sorted = pts_sorted
-        t._perm = {}
-        return t
-
-    def permuted(self, x: torch.Tensor) -> torch.Tensor:
-        """x permuted into sorted order (computed once per tensor object)."""
-        key = id(x)
-        hit = self._perm.get(key)
-        if hit is not None and hit[0] is x:
-            return hit[1]
-        out = Engine.permute_rows(x, self.inv)
-        self._perm[key] = (x, out)
-        return out
-
-
 class Engine:
     """A configured transform (reference expansion.py:154-285)."""
 
@@ -454,6 +434,7 @@ class Engine:
         self._pairs[("near", levels)] = m2l_pairs(self.m2l_tables["near"])
         self._h = None
         self.flag = None
+        self._cascade_hook = None    # parallel.sharded: the multi-GPU cascade
         # finest far + near M2L through the per-axis factors of its tables
         # (kernel.separable_factors, csrc/m2l_sep.cu) when they factor;
         # separable=False or FC2T2_M2L_DENSE=1 keeps the dense tcgen05 path
@@ -463,14 +444,6 @@ class Engine:
             self.m2l_tables, levels, self.rho, lsq, nodes_per_axis)
         self._sep = (separable_factors(kernel, levels, lsq, nodes_per_axis)
                      if self.separable else None)
-        # coarse levels' far tables too: opt-in (FC2T2_SEP_FAR=1) -- measured at
-        # config 2 the 7 passes over the 32^3 level-4 grid (one small wave
-        # each) take longer than the dense tcgen05 launch (1.81 vs 1.72 ms)
-        far_on = bool(separable) and os.environ.get("FC2T2_SEP_FAR", "0") == "1"
-        self._sep_far = {l: separable_factors(kernel, l, lsq, nodes_per_axis)
-                         for l in range(COARSEST_LEVEL + 1, levels)
-                         if far_on and separable_far_eligible(self.m2l_tables, l, levels,
-                                                              self.rho, lsq, nodes_per_axis)}
 
     # the device side is created lazily so the host tables can be built
     # (and pinned by CPU tests) without a GPU
@@ -492,11 +465,6 @@ class Engine:
                 _lib.check(h.lib.fc2t2_engine_set_separable(
                     h.h, f["pre"].ctypes.data, f["post"].ctypes.data, f["conv"].ctypes.data),
                     "engine_set_separable")
-            for lvl, fac in self._sep_far.items():
-                f = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in fac.items()}
-                _lib.check(h.lib.fc2t2_engine_set_separable_far(
-                    h.h, int(lvl), f["pre"].ctypes.data, f["post"].ctypes.data,
-                    f["conv"].ctypes.data), "engine_set_separable_far")
             self._h = h
             self.flag = DomainFlag()
         return self._h.h
@@ -539,16 +507,10 @@ class Engine:
 
     # -- stages -------------------------------------------------------------
 
-    def sort_points(self, pts: torch.Tensor, with_points: bool = False,
-                    stable: bool | None = None, flag: torch.Tensor | None = None) -> "CellSort":
-        """Stable sort by finest cell: (order (n,), cell_start (res^3+1,)); with
-        ``with_points`` also the inverse permutation and the points in sorted
-        order (written by the sort without random reads), which let P2M and the
-        cell-coherent L2P read their inputs coalesced.  Off by default: measured
-        at config 5 (2^27 points) the extra scattered streams (coordinates,
-        inverse, permuted weights) cost more than the random reads they remove
-        (+23 ms vs -13 ms per step); at config 2 the sort grows 0.36 -> 0.95 ms
-        for a 0.14 ms P2M saving."""
+    def sort_points(self, pts: torch.Tensor) -> tuple:
+        """Stable sort by finest cell: (order (n,), cell_start (res^3+1,)) --
+        the np.add.at key order of expansion.py:195 (diagnostics and tests;
+        P2M partitions the points itself, see p2m_device)."""
         n = int(pts.shape[0])
         R = level_resolution(self.levels) ** 3
         ws_bytes = _lib.lib().fc2t2_cell_sort_workspace_size(self.levels, n)
@@ -556,48 +518,23 @@ class Engine:
         order = torch.empty(max(n, 1), dtype=torch.int32, device=pts.device)
         start = torch.empty(R + 1, dtype=torch.int32, device=pts.device)
         _ = self.handle
-        if not with_points or n == 0:
-            # P2M sums exactly in fixed point (rho <= 5): cell binning without the
-            # per-cell index sort gives the same moments; stable=True forces it
-            if stable is None:
-                stable = not bool(_lib.lib().fc2t2_p2m_order_free(self.rho))
-            fn = "fc2t2_cell_sort" if stable else "fc2t2_cell_bin"
-            _lib.call(fn, self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
-                      _ptr(self.flag.t if flag is None else flag), _ptr(ws), int(ws_bytes),
-                      _stream())
-            return CellSort(order, start)
-        inv = torch.empty(n, dtype=torch.int32, device=pts.device)
-        pts_sorted = torch.empty((n, 3), dtype=torch.float32, device=pts.device)
-        _lib.call("fc2t2_cell_sort_ex", self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
-                  _ptr(inv), _ptr(pts_sorted), _ptr(self.flag.t), _ptr(ws), int(ws_bytes),
-                  _stream())
-        return CellSort(order, start, inv, pts_sorted)
+        _lib.call("fc2t2_cell_sort", self.levels, _ptr(pts), n, _ptr(order), _ptr(start),
+                  _ptr(self.flag.t), _ptr(ws), int(ws_bytes), _stream())
+        return order, start
 
-    @staticmethod
-    def permute_rows(x: torch.Tensor, inv: torch.Tensor) -> torch.Tensor:
-        """Rows of x moved to their sorted positions: out[inv[i]] = x[i]."""
-        x = x.contiguous()
-        out = torch.empty_like(x)
-        n = int(x.shape[0])
-        cols = int(x.numel() // max(n, 1))
-        _lib.call("fc2t2_permute_rows", _ptr(x), n, cols, _ptr(inv), _ptr(out), _stream())
-        return out
-
-    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor, sort=None) -> ExpansionGrid:
-        """P2M; ``sort`` = the CellSort of ``pts`` if already computed.  With the
-        sorted points available the weights are permuted once (cached on the
-        sort as ``w_sorted``) and P2M reads both contiguously."""
-        grid = self._empty_grid(self.levels, int(w.shape[1]), "M")
-        sort = sort if sort is not None else self.sort_points(pts)
-        order, start = sort[0], sort[1]
-        if getattr(sort, "pts_sorted", None) is not None:
-            ws_ = sort.permuted(w)
-            _lib.call("fc2t2_p2m", self.handle, int(w.shape[1]), _ptr(sort.pts_sorted),
-                      _ptr(ws_), None, _ptr(start), _ptr(grid.storage), _stream())
-        else:
-            _lib.call("fc2t2_p2m", self.handle, int(w.shape[1]), _ptr(pts), _ptr(w), _ptr(order),
-                      _ptr(start), _ptr(grid.storage), _stream())
-        self.flops.add("p2m", flops.p2m_flops(int(pts.shape[0]), self.rho, self.P))
+    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor) -> ExpansionGrid:
+        """P2M straight from the caller's point order (fc2t2_p2m_points: a
+        deterministic brick partition + per-cell sums in index order); sets
+        the domain flag for points outside (-1, 1)^3."""
+        C = int(w.shape[1])
+        n = int(pts.shape[0])
+        grid = self._empty_grid(self.levels, C, "M")
+        h = self.handle
+        ws_bytes = int(_lib.lib().fc2t2_p2m_points_workspace_size(h, C, n))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=pts.device)
+        _lib.call("fc2t2_p2m_points", h, C, _ptr(pts), _ptr(w), n, _ptr(grid.storage),
+                  _ptr(self.flag.t), _ptr(ws), ws_bytes, _stream())
+        self.flops.add("p2m", flops.p2m_flops(n, self.rho, self.P))
         return grid
 
     def p2m(self, sources: SourceSet) -> ExpansionGrid:
@@ -657,17 +594,60 @@ class Engine:
     def cascade_device(self, m_finest: torch.Tensor, x_range: tuple | None = None) -> torch.Tensor:
         """M2M / M2L / L2L in one C-ABI call; returns the finest L storage.
         ``x_range=(x0, x1)`` (multiples of 4) computes only the finest cells
-        with x in [x0, x1) -- one rank's slab of the sharded cascade; the rest
-        of the returned grid is unspecified."""
+        with x in [x0, x1) -- one rank's slab; the rest of the returned grid
+        is unspecified.  Inside ``parallel.sharded`` the whole-grid cascade of
+        a rank's partial moments goes through the sharded cascade instead
+        (m_finest is then overwritten)."""
         C = int(m_finest.shape[3])
-        out = torch.empty_like(m_finest)
-        ws_bytes = _lib.lib().fc2t2_expand_workspace_size(self.handle, C)
-        ws = torch.empty(int(ws_bytes), dtype=torch.uint8, device=m_finest.device)
-        x0, x1 = (0, -1) if x_range is None else (int(x_range[0]), int(x_range[1]))
-        _lib.call("fc2t2_expand_slab", self.handle, C, _ptr(m_finest), _ptr(out), x0, x1,
-                  _ptr(ws), int(ws_bytes), _stream())
         self.expansion_count += 1
         self._tally_cascade(C)
+        if x_range is None and self._cascade_hook is not None:
+            return self._cascade_hook(m_finest)
+        return self._cascade_raw(m_finest, x_range)
+
+    def _expand_ws(self, C: int, dev) -> torch.Tensor:
+        ws_bytes = int(_lib.lib().fc2t2_expand_workspace_size(self.handle, C))
+        return torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+
+    def _cascade_raw(self, m_finest: torch.Tensor, x_range: tuple | None = None) -> torch.Tensor:
+        C = int(m_finest.shape[3])
+        out = torch.empty_like(m_finest)
+        ws = self._expand_ws(C, m_finest.device)
+        x0, x1 = (0, -1) if x_range is None else (int(x_range[0]), int(x_range[1]))
+        _lib.call("fc2t2_expand_slab", self.handle, C, _ptr(m_finest), _ptr(out), x0, x1,
+                  _ptr(ws), int(ws.numel()), _stream())
+        return out
+
+    # the two-phase slab cascade of the multi-GPU path (parallel.sharded_cascade)
+    def cascade_up(self, m_finest: torch.Tensor, x_range: tuple) -> tuple:
+        """M2M chain on the x-slab (m_finest valid on the slab); returns the
+        state (workspace, channels) whose coarse M grids the caller all-gathers."""
+        C = int(m_finest.shape[3])
+        ws = self._expand_ws(C, m_finest.device)
+        _lib.call("fc2t2_expand_up", self.handle, C, _ptr(m_finest), int(x_range[0]),
+                  int(x_range[1]), _ptr(ws), int(ws.numel()), _stream())
+        return ws, C
+
+    def coarse_views(self, state: tuple) -> list:
+        """[(level, (res, res, res, C, PP) view into the workspace)] of the
+        coarse M grids the slab cascade reads, levels lowest .. levels-1."""
+        ws, C = state
+        lib = _lib.lib()
+        out = []
+        for lvl in range(lib.fc2t2_expand_lowest(self.handle), self.levels):
+            off = int(lib.fc2t2_expand_grid_offset(self.handle, C, lvl))
+            res = level_resolution(lvl)
+            n = res ** 3 * C * self.PP * 4
+            out.append((lvl, ws[off:off + n].view(torch.float32).view(res, res, res, C, self.PP)))
+        return out
+
+    def cascade_down(self, m_finest: torch.Tensor, state: tuple, x_range: tuple) -> torch.Tensor:
+        """Coarse M2L + L2L and the finest M2L on the slab (m_finest valid on
+        the slab plus 3 planes either side); returns the finest L storage."""
+        ws, C = state
+        out = torch.empty_like(m_finest)
+        _lib.call("fc2t2_expand_down", self.handle, C, _ptr(m_finest), _ptr(out), int(x_range[0]),
+                  int(x_range[1]), _ptr(ws), int(ws.numel()), _stream())
         return out
 
     def expand_from_moments(self, m_finest: ExpansionGrid) -> "Accessor":
@@ -677,12 +657,15 @@ class Engine:
         grid = ExpansionGrid(level=self.levels, kind="L", storage=out, rho=self.rho)
         return Accessor(grid, self.table, self.flops)
 
-    def expand_device(self, pts: torch.Tensor, w: torch.Tensor, sort=None) -> "Accessor":
-        """expand() on device tensors without the per-call domain sync."""
-        m = self.p2m_device(pts, w, sort)
-        out = self.cascade_device(m.storage)
+    def accessor_from_moments(self, m_finest: torch.Tensor) -> "Accessor":
+        """Cascade of device moments -> Accessor sharing the engine's flag."""
+        out = self.cascade_device(m_finest)
         grid = ExpansionGrid(level=self.levels, kind="L", storage=out, rho=self.rho)
         return Accessor(grid, self.table, self.flops, flag=self.flag)
+
+    def expand_device(self, pts: torch.Tensor, w: torch.Tensor) -> "Accessor":
+        """expand() on device tensors without the per-call domain sync."""
+        return self.accessor_from_moments(self.p2m_device(pts, w).storage)
 
     def expand(self, sources: SourceSet) -> "Accessor":
         acc = self.expand_device(sources.p, sources.w)

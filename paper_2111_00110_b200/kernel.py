@@ -405,18 +405,3 @@ def separable_eligible(tables: dict, levels: int, rho: int, lsq: bool = True,
                 and np.abs(far.offsets).max() == FAR_REACH)
 
 
-def separable_far_eligible(tables: dict, level: int, levels: int, rho: int, lsq: bool = True,
-                           nodes_per_axis: int = 6) -> bool:
-    """A coarse level's far table (parity stencil minus the hole) runs
-    separably (three disjoint per-axis pieces) when the grid is >= 32 cells
-    wide, the per-axis fit is full rank and the level has work.  Offsets the
-    reference prunes have a peak interaction below PRUNE_TOL
-    (interaction_mask); the separable form includes them, a change below 1e-16
-    of the kernel peak per unit weight."""
-    if not (COARSEST_LEVEL < level < levels) or level_resolution(level) < 32:
-        return False
-    if lsq and rho + 1 > nodes_per_axis:
-        return False
-    far = tables["far"][level]
-    return bool(far.active.any() and not (far.active & far.hole).any()
-                and np.abs(far.offsets).max() == FAR_REACH)

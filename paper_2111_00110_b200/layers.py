@@ -17,8 +17,6 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-import os
-
 import numpy as np
 import torch
 
@@ -50,19 +48,14 @@ class ExplicitResult:
     sources: SourceSet
     engine: Engine
     q_dev: torch.Tensor = None
-    sorts: tuple = None      # ((p order, p cell_start), (q order, q cell_start))
     q_grad: torch.Tensor = None   # (M, C, 3) grad f at q, stored for the backward
-    q_sort_ready: object = None   # event after the aux-stream query sort
 
 
 # q_bar recycling ("expansion recycling"): the forward L2P at q
 # also returns grad f(q) -- the same cell-row gather, 12 B more per point and
 # channel written -- so explicit_jvp forms q_bar = sum_c y_bar_c grad f_c
-# (fc2t2_weighted_grad, bit-identical to the L2P_WGRAD pass it replaces)
-# instead of gathering every query's cell row a second time.
-# FC2T2_NO_RECYCLE=1 restores the second L2P pass.
-RECYCLE_QUERY_GRAD = os.environ.get("FC2T2_NO_RECYCLE", "0") != "1"
-
+# (fc2t2_weighted_grad, bit-identical to an L2P_WGRAD pass) instead of
+# gathering every query's cell row a second time.
 
 def _weighted_grad(grad: torch.Tensor, wts: torch.Tensor, out: torch.Tensor | None = None
                    ) -> torch.Tensor:
@@ -73,126 +66,37 @@ def _weighted_grad(grad: torch.Tensor, wts: torch.Tensor, out: torch.Tensor | No
     return out
 
 
-# Cell-coherent L2P (points evaluated in cell-sorted order so neighbouring
-# threads share rows) for grids larger than this many bytes; 0 = never.  Off
-# by default: with the warp-cooperative row fetch (l2p.cu) natural order is as
-# fast for values and faster for gradients even at config 5's 704 MB grid
-# (B200, 2^27 points: 9.3 / 10.2 ms natural vs 9.0 / 14.3 ms sorted), and it
-# needs no query sort before the forward.  FC2T2_COHERENT_L2P_MB re-enables it.
-COHERENT_L2P_BYTES = int(os.environ.get("FC2T2_COHERENT_L2P_MB", "0")) << 20
-
-
-def _beyond_coherent(nbytes: int) -> bool:
-    return COHERENT_L2P_BYTES > 0 and nbytes > COHERENT_L2P_BYTES
-
-
-def _sorts(res: "ExplicitResult"):
-    """(p sort, q sort) of an explicit result; the query sort is computed on
-    first use unless the forward started it on the engine's aux stream, in
-    which case the current stream joins it here."""
-    p_sort, q_sort = res.sorts
-    if q_sort is None:
-        q_sort = res.engine.sort_points(res.q_dev)
-        res.sorts = (p_sort, q_sort)
-    elif res.q_sort_ready is not None:
-        torch.cuda.current_stream().wait_event(res.q_sort_ready)
-        res.q_sort_ready = None
-    return p_sort, q_sort
-
-
-# The backward's P2M of (q, y_bar) needs the cell sort of q, which depends on
-# q alone: the device forward starts it on the engine's aux stream, where it
-# overlaps the forward cascade and L2P (atomic/scatter-bound sort kernels
-# beside bandwidth/latency-bound cascade kernels), and explicit_jvp joins it.
-# FC2T2_NO_EARLY_QSORT=1 sorts in the backward instead.
-EARLY_QUERY_SORT = os.environ.get("FC2T2_NO_EARLY_QSORT", "0") != "1"
-
-
-def _early_sort(engine: Engine, qd: torch.Tensor, after=None):
-    """(CellSort, ready event) of qd sorted on the engine's aux stream, after
-    the event ``after`` (default: everything enqueued on the current stream)."""
-    cs = torch.cuda.current_stream()
-    aux = engine.aux_stream()
-    if after is not None:
-        aux.wait_event(after)
-    else:
-        aux.wait_stream(cs)
-    # qd is read on aux: keep its block alive until the sort ends even when the
-    # caller drops the result without a backward
-    qd.record_stream(aux)
-    if getattr(engine, "_aux_flag", None) is None:
-        # the aux sort's own domain flag: the forward already checked q on the
-        # compute stream, so this one is never read and can never leak a stale
-        # FLAG_DOMAIN into a later call on the main flag
-        engine._aux_flag = torch.zeros(1, dtype=torch.int32, device=qd.device)
-    with torch.cuda.stream(aux):
-        srt = engine.sort_points(qd, flag=engine._aux_flag)
-        ready = torch.cuda.Event()
-        ready.record(aux)
-    for t in srt:
-        t.record_stream(cs)
-    return srt, ready
-
-
-def _coherent(acc: Accessor, sort):
-    st = acc.grid.storage
-    return sort[0] if _beyond_coherent(st.numel() * st.element_size()) else None
-
-
-def _l2p(acc: Accessor, pts, mode: int, sort=None, wts=None):
-    """L2P at pts.  For grids beyond L2 the points are evaluated in cell order
-    so neighbouring threads share cell rows; with the sort's sorted points the
-    inputs (and weights, permuted once) are read coalesced and only outputs
-    are scattered (FC2T2_L2P_PRESORTED).  Otherwise natural order."""
-    order = _coherent(acc, sort) if sort is not None else None
-    if order is None:
-        return acc.eval_device(pts, mode, wts=wts)
-    if getattr(sort, "pts_sorted", None) is not None:
-        w_s = None if wts is None else sort.permuted(wts)
-        return acc.eval_device(sort.pts_sorted, mode | _lib.L2P_PRESORTED, wts=w_s, order=order)
-    return acc.eval_device(pts, mode, wts=wts, order=order)
+def _expand_checked(engine: Engine, p: torch.Tensor, w: torch.Tensor) -> tuple:
+    """(accessor, mark): P2M of (p, w) -- whose partition pass checks p's
+    domain -- then the flag mark, then the cascade, so raise_if_set(mark)
+    waits only for the checking kernels and the host can enqueue the rest."""
+    m = engine.p2m_device(p, w)
+    checked = engine.flag.mark()
+    return engine.accessor_from_moments(m.storage), checked
 
 
 # Host-tensor callers: the per-point streams (q, y_bar up; values, q_bar down)
 # move in HOST_CHUNKS row chunks so PCIe uploads, downloads (separate streams,
 # both directions at once) and the L2P of finished chunks overlap each other
-# and the expansions.  Cell-coherent L2P (grids beyond L2) needs the whole
-# point set, so it runs unchunked.
+# and the expansions.
 HOST_CHUNKS = 8
 
 
 def _explicit_forward_host(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     qd, chunks = HostIO.h2d(q, 3, chunks=HOST_CHUNKS)
-    p_sort = engine.sort_points(sources.p)
-    acc = engine.expand_device(sources.p, sources.w, p_sort)
+    acc = engine.expand_device(sources.p, sources.w)
     cs = torch.cuda.current_stream()
-    coherent = _beyond_coherent(acc.grid.storage.numel() * 4)
     out = torch.empty((qd.shape[0], acc.channels), dtype=torch.float32, pin_memory=True)
-    q_grad = None
-    sort_ready = None
-    if not coherent:
-        mode = _lib.L2P_VALUE
-        if RECYCLE_QUERY_GRAD:
-            q_grad = torch.empty((qd.shape[0], acc.channels, 3), dtype=torch.float32,
-                                 device=qd.device)
-            mode |= _lib.L2P_GRAD
-        for a, b, ev in chunks:
-            cs.wait_event(ev)
-            if b > a:
-                o = {"grad": q_grad[a:b]} if q_grad is not None else None
-                HostIO.d2h(acc.eval_device(qd[a:b], mode, outs=o)["value"], out[a:b])
-        # sorted by the backward beside the y_bar upload (measured: starting it
-        # here, under the values download, does not shorten the host-tensor
-        # step -- 5.73 vs 5.70 ms -- the PCIe streams bound both halves)
-        q_sort = None
-    else:
-        cs.wait_event(chunks[-1][2])
-        q_sort = engine.sort_points(qd)
-        HostIO.d2h(_l2p(acc, qd, _lib.L2P_VALUE, q_sort)["value"], out)
+    q_grad = torch.empty((qd.shape[0], acc.channels, 3), dtype=torch.float32, device=qd.device)
+    for a, b, ev in chunks:
+        cs.wait_event(ev)
+        if b > a:
+            r = acc.eval_device(qd[a:b], _lib.L2P_VALUE | _lib.L2P_GRAD, outs={"grad": q_grad[a:b]})
+            HostIO.d2h(r["value"], out[a:b])
     HostIO.finish()
     engine.flag.raise_if_set("source/query")
     return ExplicitResult(values=out, accessor=acc, q=q, sources=sources, engine=engine, q_dev=qd,
-                          sorts=(p_sort, q_sort), q_grad=q_grad, q_sort_ready=sort_ready)
+                          q_grad=q_grad)
 
 
 def _recycled_qbar_host(y_bar, res: ExplicitResult):
@@ -224,50 +128,10 @@ def _recycled_qbar_host(y_bar, res: ExplicitResult):
 
 
 def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
-    eng, qd, src, acc = res.engine, res.q_dev, res.sources, res.accessor
-    cs = torch.cuda.current_stream()
-    p_sort, q_sort = res.sorts
-    aux, ready = None, None
-    if res.q_grad is not None:          # stored only outside the cell-coherent mode
-        yb, q_bar = _recycled_qbar_host(y_bar, res)
-        chunks = []
-    else:
-        yb, chunks = HostIO.h2d(y_bar, acc.channels, chunks=HOST_CHUNKS)
-        q_bar = torch.empty((qd.shape[0], 3), dtype=torch.float32, pin_memory=True)
-    if q_sort is None:
-        # the query sort runs beside the per-chunk q_bar work, under the y_bar upload
-        aux = HostIO.aux()
-        aux.wait_stream(cs)
-        with torch.cuda.stream(aux):
-            q_sort = eng.sort_points(qd)
-        for t in (*q_sort, q_sort.inv, q_sort.pts_sorted):
-            if t is not None:
-                t.record_stream(cs)
-        res.sorts = (p_sort, q_sort)
-    elif res.q_sort_ready is not None:
-        ready = res.q_sort_ready
-        res.q_sort_ready = None
-    order = _coherent(acc, q_sort)
-    if order is None:
-        for a, b, ev in chunks:
-            cs.wait_event(ev)
-            if b > a:
-                if res.q_grad is not None:
-                    qb = _weighted_grad(res.q_grad[a:b], yb[a:b])
-                else:
-                    qb = acc.eval_device(qd[a:b], _lib.L2P_WGRAD, wts=yb[a:b])["wgrad"]
-                HostIO.d2h(qb, q_bar[a:b])
-    else:
-        cs.wait_event(chunks[-1][2])
-        if aux is not None:
-            cs.wait_stream(aux)
-        HostIO.d2h(_l2p(acc, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"], q_bar)
-    if aux is not None:
-        cs.wait_stream(aux)
-    elif ready is not None:
-        cs.wait_event(ready)
-    back = eng.expand_device(qd, yb, q_sort)
-    out = _l2p(back, src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, p_sort, wts=src.w)
+    eng, qd, src = res.engine, res.q_dev, res.sources
+    yb, q_bar = _recycled_qbar_host(y_bar, res)
+    back = eng.expand_device(qd, yb)
+    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
     w_bar, p_bar = HostIO.d2h(out["value"]), HostIO.d2h(out["wgrad"])
     HostIO.finish()
     eng.flag.raise_if_set("source/query")
@@ -276,48 +140,26 @@ def _explicit_jvp_host(y_bar, res: ExplicitResult) -> LayerGradients:
 
 def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     _host_domain_check(q, "query")
-    # The cell sorts of the sources and queries are computed once and reused:
-    # p's by P2M now and by the source-side L2P of the backward, q's by the
-    # query L2Ps (cell-coherent order) and by the backward P2M of q.
     if is_host_tensor(q):
         return _explicit_forward_host(engine, sources, q)
     qd = to_device(q, 3, points=True)
-    p_sort = engine.sort_points(sources.p)
-    coherent = _beyond_coherent(engine.finest_grid_bytes(sources.channels))
-    q_sort = engine.sort_points(qd) if coherent else None   # else sorted for the backward
-    ready = None
-    if q_sort is None:
-        # a stand-alone check: the aux-stream query sort also checks q, but
-        # waiting for its end would stall the host for the whole sort when it
-        # outlasts the forward (config 5: +40 ms per step, measured)
-        engine.flag.check_points(qd)
-    checked = engine.flag.mark()
-    if q_sort is None and EARLY_QUERY_SORT:
-        q_sort, ready = _early_sort(engine, qd)
-    acc = engine.expand_device(sources.p, sources.w, p_sort)
-    recycle = RECYCLE_QUERY_GRAD and not coherent
-    r = _l2p(acc, qd, _lib.L2P_VALUE | (_lib.L2P_GRAD if recycle else 0), q_sort)
+    engine.flag.check_points(qd)
+    acc, checked = _expand_checked(engine, sources.p, sources.w)
+    r = acc.eval_device(qd, _lib.L2P_VALUE | _lib.L2P_GRAD)
     engine.flag.raise_if_set("source/query", checked)
     return ExplicitResult(values=like_input(r["value"], q), accessor=acc, q=q, sources=sources,
-                          engine=engine, q_dev=qd, sorts=(p_sort, q_sort),
-                          q_grad=r["grad"] if recycle else None, q_sort_ready=ready)
+                          engine=engine, q_dev=qd, q_grad=r["grad"])
 
 
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     if is_host_tensor(y_bar):
         return _explicit_jvp_host(y_bar, res)
-    eng = res.engine
-    qd = res.q_dev
-    src = res.sources
-    p_sort, q_sort = _sorts(res)
-    checked = eng.flag.mark()           # the sorts re-checked p and q
+    eng, qd, src = res.engine, res.q_dev, res.sources
+    checked = eng.flag.mark()           # p and q were checked by the forward
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    if res.q_grad is not None:
-        q_bar = _weighted_grad(res.q_grad, yb)
-    else:
-        q_bar = _l2p(res.accessor, qd, _lib.L2P_WGRAD, q_sort, wts=yb)["wgrad"]
-    back = eng.expand_device(qd, yb, q_sort)
-    out = _l2p(back, src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, p_sort, wts=src.w)
+    q_bar = _weighted_grad(res.q_grad, yb)
+    back = eng.expand_device(qd, yb)
+    out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
     eng.flag.raise_if_set("source/query", checked)
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),
@@ -396,9 +238,7 @@ def depth_forward(engine: Engine, sources: SourceSet, bundle: RayBundle, bias: f
         raise ValueError("root layers expect a single-channel field")
     if engine.rho > ROOT_MAX_ORDER:
         raise OrderError(f"root layers need rho <= {ROOT_MAX_ORDER}")
-    p_sort = engine.sort_points(sources.p)
-    checked = engine.flag.mark()
-    acc = engine.expand_device(sources.p, sources.w, p_sort)
+    acc, checked = _expand_checked(engine, sources.p, sources.w)
     org, dirs = bundle.dev()
     R = bundle.count
     dev = org.device

@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from .expansion import Engine, SourceSet, _device, _ptr, _stream, to_device
-from .layers import (_l2p, depth_forward, depth_jvp, explicit_forward, explicit_jvp,
+from .layers import (depth_forward, depth_jvp, explicit_forward, explicit_jvp,
                      volumetric_forward, volumetric_jvp)
 
 DOMAIN_MARGIN = 1e-6  # sources are clipped back to (-1+eps, 1-eps)
@@ -215,24 +215,22 @@ def cgls_sdf(engine: Engine, p, q, target, iterations: int) -> dict:
     forward product (expand the sources, evaluate at the samples) and one
     adjoint product (expand the residual at the samples, evaluate at the
     sources).  The CG vectors and scalars are float64 device tensors; the
-    products run through the fp32 engine.  The cell sorts of p and q are made
-    once and reused by every product; nothing is read back until the end.
+    products run through the fp32 engine; nothing is read back until the end.
 
     Returns {"w": (N, 1), "bias": float, "mae": [per iteration], "final_mae"}.
     """
     pd = to_device(p, 3, points=True)
     qd = to_device(q, 3, points=True)
     d = to_device(target).reshape(-1).double()
-    p_sort, q_sort = engine.sort_points(pd), engine.sort_points(qd)
     value = _lib.L2P_VALUE
 
     def a_fwd(w, b):
-        acc = engine.expand_device(pd, w.float().reshape(-1, 1).contiguous(), p_sort)
-        return _l2p(acc, qd, value, q_sort)["value"].reshape(-1).double() + b
+        acc = engine.expand_device(pd, w.float().reshape(-1, 1).contiguous())
+        return acc.eval_device(qd, value)["value"].reshape(-1).double() + b
 
     def a_adj(r):
-        acc = engine.expand_device(qd, r.float().reshape(-1, 1).contiguous(), q_sort)
-        return _l2p(acc, pd, value, p_sort)["value"].reshape(-1).double(), r.sum()
+        acc = engine.expand_device(qd, r.float().reshape(-1, 1).contiguous())
+        return acc.eval_device(pd, value)["value"].reshape(-1).double(), r.sum()
 
     with engine.flag.deferred():
         w = torch.zeros(pd.shape[0], dtype=torch.float64, device=pd.device)

@@ -43,41 +43,47 @@ def test_find_box_bit_exact(cuda, level):
     assert np.array_equal(got.cpu().numpy(), g[f"box_l{level}"])
 
 
-@pytest.mark.parametrize("heavy", [0, 20_000])
-def test_cell_bin_and_order_free_p2m(eng4, heavy):
-    """fc2t2_cell_bin (no per-cell index sort): cells contiguous with the same
-    ranges as the stable sort, each cell's set of points identical; and the
-    fixed-point P2M gives bit-identical moments for the stable order, the
-    binned (arrival) order and a reversed within-cell order; it is exactly
-    homogeneous under power-of-two weight scaling (per-cell scales), even at
-    2^-60 / 2^60."""
-    from paper_2111_00110_b200 import _lib
-    from paper_2111_00110_b200.expansion import CellSort
-    if _lib.lib().fc2t2_p2m_order_free(4) != 1:
-        pytest.skip("fixed-point P2M is opt-in (FC2T2_P2M_FIXED=1)")
-    rng = np.random.default_rng(1)
-    p = rng.uniform(-1, 1, (50_000, 3)).astype(np.float32)
+def _cell_key(p: np.ndarray, level: int) -> np.ndarray:
+    from oracle.fc2t2_oracle import find_box
+    res = 2 ** (level + 1)
+    b = find_box(level, p.astype(np.float64))
+    return (b[:, 0] * res + b[:, 1]) * res + b[:, 2]
+
+
+@pytest.mark.parametrize("level,rho,C,n,heavy", [(4, 4, 1, 50_000, 0), (4, 4, 2, 50_000, 9_000),
+                                                 (5, 4, 1, 200_000, 0), (6, 6, 1, 120_000, 3_000),
+                                                 (3, 4, 3, 7, 0), (5, 4, 1, 0, 0)])
+def test_brick_p2m_is_stable_and_matches_oracle(cuda, level, rho, C, n, heavy):
+    """fc2t2_p2m_points (brick partition + per-brick P2M): equal to the float64
+    oracle (expansion.py:186-198) to float32 rounding; bit-identical to itself
+    run twice (deterministic) and to the same points pre-sorted STABLY by cell
+    (the per-cell summation order is the index order, as np.add.at); heavy
+    cells (> one 2048-record chunk of a brick) and level 6's 512-cell bricks."""
+    from paper_2111_00110_b200 import Engine, KernelModel
+    alpha = {3: 50.0, 4: 200.0, 5: 1000.0, 6: 4000.0}[level]
+    eng = Engine(KernelModel("gaussian", alpha, rho), level, check_admissibility=False)
+    rng = np.random.default_rng(level * 10 + C)
+    p = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
     if heavy:
-        idx = rng.permutation(50_000)
-        p[idx[:heavy]] = p[idx[0]]
-    pt = torch.from_numpy(p).cuda()
-    w = torch.from_numpy(rng.normal(size=(50_000, 2)).astype(np.float32)).cuda()
-    st = eng4.sort_points(pt, stable=True)
-    bn = eng4.sort_points(pt, stable=False)
-    assert torch.equal(st[1], bn[1])
-    so, bo, start = st[0].cpu().numpy(), bn[0].cpu().numpy(), st[1].cpu().numpy()
-    rev = so.copy()
-    for c in np.flatnonzero(np.diff(start) > 1):
-        a, b = start[c], start[c + 1]
-        assert np.array_equal(np.sort(bo[a:b]), so[a:b])
-        rev[a:b] = so[a:b][::-1]
-    m_st = eng4.p2m_device(pt, w, st).storage
-    m_bn = eng4.p2m_device(pt, w, bn).storage
-    m_rv = eng4.p2m_device(pt, w, CellSort(torch.from_numpy(rev).cuda(), st[1])).storage
-    assert torch.equal(m_st, m_bn) and torch.equal(m_st, m_rv)
-    for k in (-60, 60):
-        m_k = eng4.p2m_device(pt, w * 2.0 ** k, bn).storage
-        assert torch.equal(m_k, m_st * 2.0 ** k)
+        idx = rng.permutation(n)
+        p[idx[:heavy]] = (p[idx[0]] * 0.999).astype(np.float32) + \
+            rng.uniform(-1e-4, 1e-4, (heavy, 3)).astype(np.float32)
+    w = rng.normal(size=(n, C)).astype(np.float32)
+    pt, wt = torch.from_numpy(p).cuda(), torch.from_numpy(w).cuda()
+    m1 = eng.p2m_device(pt, wt).storage.clone()
+    m2 = eng.p2m_device(pt, wt).storage
+    assert torch.equal(m1, m2)
+    order = np.argsort(_cell_key(p, level), kind="stable")
+    m3 = eng.p2m_device(torch.from_numpy(p[order]).cuda(), torch.from_numpy(w[order]).cuda()).storage
+    assert torch.equal(m1, m3)
+    ref = Oracle(alpha, rho, level, tables={"far": {}, "near": None}).p2m(p.astype(np.float64),
+                                                                           w.astype(np.float64))
+    got = m1.cpu().numpy().astype(np.float64)[..., :ref.shape[-1]]
+    assert np.all(m1.cpu().numpy()[..., ref.shape[-1]:] == 0)
+    if n:
+        assert rel_l2(got, ref) < 1e-6
+    else:
+        assert np.all(got == 0)
 
 
 @pytest.mark.parametrize("heavy", [0, 5000, 20_000])
@@ -91,22 +97,14 @@ def test_cell_sort_is_stable_counting_sort(eng4, heavy):
         idx = rng.permutation(50_000)
         p[idx[:heavy]] = p[idx[0]]            # a heavy cell, scattered indices
         p[idx[heavy:heavy + 300]] = p[idx[heavy]]
-    srt = eng4.sort_points(torch.from_numpy(p).cuda(), with_points=True)
-    order, start = srt
-    o = order.cpu().numpy()
-    # by-products: inverse permutation and the points in sorted order
-    assert np.array_equal(srt.inv.cpu().numpy()[o], np.arange(o.size))
-    assert np.array_equal(srt.pts_sorted.cpu().numpy(), p[o])
+    order, start = eng4.sort_points(torch.from_numpy(p).cuda())
     from oracle.fc2t2_oracle import find_box
     b = find_box(4, p.astype(np.float64))
     key = (b[:, 0] * 32 + b[:, 1]) * 32 + b[:, 2]
     ref = np.argsort(key, kind="stable")
     assert np.array_equal(order.cpu().numpy(), ref)
-    # the plain sort (no points): segments already in index order skip the network
-    plain, _ = eng4.sort_points(torch.from_numpy(p).cuda(), stable=True)
-    assert np.array_equal(plain.cpu().numpy(), ref)
     pr = p[::-1].copy()        # reversed input: arrival order is mostly descending
-    plain_r, _ = eng4.sort_points(torch.from_numpy(pr).cuda(), stable=True)
+    plain_r, _ = eng4.sort_points(torch.from_numpy(pr).cuda())
     assert np.array_equal(plain_r.cpu().numpy(), np.argsort(key[::-1], kind="stable"))
     counts = np.bincount(key, minlength=32 ** 3)
     assert np.array_equal(start.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
@@ -331,16 +329,13 @@ def test_explicit_torch_io_and_counts(eng4):
     assert rel_l2(_np(g.q_bar), qb) < TOL
 
 
-@pytest.mark.parametrize("coherent", [False, True])
 @pytest.mark.parametrize("m", [5001, 5])
-def test_explicit_host_tensors_match_device(eng4, monkeypatch, coherent, m):
+def test_explicit_host_tensors_match_device(eng4, m):
     """Host (pinned / pageable) torch inputs take the chunked duplex-copy path
     (layers._explicit_*_host); every output must equal the device path bit for
-    bit, for ragged chunk sizes and for the unchunked cell-coherent branch."""
+    bit, for ragged chunk sizes."""
     import paper_2111_00110_b200.layers as layers
     from paper_2111_00110_b200 import SourceSet
-    if coherent:
-        monkeypatch.setattr(layers, "COHERENT_L2P_BYTES", 1)
     rng = np.random.default_rng(7)
     p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32))
     w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32))
@@ -432,31 +427,6 @@ def test_expand_slabs_assemble_full_cascade(cuda, separable):
         assert torch.equal(torch.cat(parts), full)
     with pytest.raises(Exception):
         eng.cascade_device(m, (2, 16))        # not a multiple of 4
-
-
-def test_presorted_l2p_and_p2m_match_natural_order(eng4):
-    """FC2T2_L2P_PRESORTED (inputs permuted into cell order, outputs scattered
-    by order) and P2M on pre-sorted points give bit-identical results to the
-    natural-order paths."""
-    from paper_2111_00110_b200 import _lib
-    from paper_2111_00110_b200.expansion import Accessor
-    gen = torch.Generator(device="cuda").manual_seed(9)
-    p = torch.rand(20_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
-    w = torch.randn(20_000, 2, device="cuda", generator=gen)
-    plain = eng4.p2m_device(p, w, eng4.sort_points(p))
-    srt = eng4.sort_points(p, with_points=True)
-    pre = eng4.p2m_device(p, w, srt)
-    assert torch.equal(plain.storage, pre.storage)
-    from paper_2111_00110_b200.expansion import ExpansionGrid
-    L = ExpansionGrid(plain.level, "L", plain.storage, plain.rho)
-    acc = Accessor(L, eng4.table, eng4.flops, flag=eng4.flag)
-    for mode, keys in ((_lib.L2P_VALUE | _lib.L2P_WGRAD, ("value", "wgrad")),
-                       (_lib.L2P_GRAD, ("grad",))):
-        nat = acc.eval_device(p, mode, wts=w)
-        got = acc.eval_device(srt.pts_sorted, mode | _lib.L2P_PRESORTED, wts=srt.permuted(w),
-                              order=srt[0])
-        for k in keys:
-            assert torch.equal(nat[k], got[k])
 
 
 @pytest.mark.parametrize("rho,level,C,n", [(4, 4, 1, 4133), (4, 3, 3, 70), (6, 5, 1, 3001),
@@ -578,31 +548,21 @@ def test_separable_finest_m2l_matches_dense_and_oracle(cuda, alpha, rho, level, 
         assert rel_l2(a[..., c, :], ref[..., c, :]) < 2e-6
 
 
-@pytest.mark.parametrize("host", [False, True])
-def test_query_gradient_recycling_is_bit_identical(eng4, monkeypatch, host):
+def test_query_gradient_recycling_is_bit_identical(eng4):
     """explicit_forward stores grad f(q) from its VALUE | GRAD L2P and
-    explicit_jvp forms q_bar with fc2t2_weighted_grad: every output equals the
-    second-L2P_WGRAD-pass path bit for bit (device and chunked host paths)."""
-    import paper_2111_00110_b200.layers as layers
-    from paper_2111_00110_b200 import SourceSet
+    explicit_jvp forms q_bar with fc2t2_weighted_grad: equal bit for bit to a
+    second L2P pass with L2P_WGRAD (ref layers.py:183)."""
+    from paper_2111_00110_b200 import SourceSet, _lib
+    from paper_2111_00110_b200 import layers
     rng = np.random.default_rng(12)
-    p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32))
-    w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32))
-    q = torch.from_numpy(rng.uniform(-1, 1, (7001, 3)).astype(np.float32))
-    yb = torch.from_numpy(rng.normal(size=(7001, 2)).astype(np.float32))
-    outs = []
-    for recycle in (True, False):
-        monkeypatch.setattr(layers, "RECYCLE_QUERY_GRAD", recycle)
-        if host:
-            r = layers.explicit_forward(eng4, SourceSet(p.pin_memory(), w.pin_memory()), q.pin_memory())
-            g = layers.explicit_jvp(yb.pin_memory(), r)
-        else:
-            r = layers.explicit_forward(eng4, SourceSet(p.cuda(), w.cuda()), q.cuda())
-            g = layers.explicit_jvp(yb.cuda(), r)
-        assert (r.q_grad is not None) == recycle
-        outs.append((r.values, g.w_bar, g.p_bar, g.q_bar))
-    for a, b in zip(*outs):
-        assert torch.equal(a, b)
+    p = torch.from_numpy(rng.uniform(-1, 1, (3000, 3)).astype(np.float32)).cuda()
+    w = torch.from_numpy(rng.normal(size=(3000, 2)).astype(np.float32)).cuda()
+    q = torch.from_numpy(rng.uniform(-1, 1, (7001, 3)).astype(np.float32)).cuda()
+    yb = torch.from_numpy(rng.normal(size=(7001, 2)).astype(np.float32)).cuda()
+    r = layers.explicit_forward(eng4, SourceSet(p, w), q)
+    g = layers.explicit_jvp(yb, r)
+    second = r.accessor.eval_device(q, _lib.L2P_WGRAD, wts=yb)["wgrad"]
+    assert torch.equal(g.q_bar, second)
 
 
 @pytest.mark.parametrize("C", [1, 3])
@@ -626,65 +586,6 @@ def test_separable_post_with_fused_l2l_is_bit_identical(cuda, C):
     assert torch.equal(out[0][0], out[1][0])
     assert torch.equal(out[0][1], out[1][1])
     assert torch.equal(out[1][1], out[1][0][16:40])
-
-
-def test_separable_far_levels_match_dense(cuda, monkeypatch):
-    """Coarse-level far tables run separably (opt-in FC2T2_SEP_FAR=1; parity
-    box minus the hole as three disjoint per-axis pieces,
-    fc2t2_engine_set_separable_far): the
-    cascade with them equals the one with dense coarse levels to < 1e-6
-    (both with the separable finest level), at levels 5 and 6."""
-    from paper_2111_00110_b200 import Engine, KernelModel
-    for alpha, L in ((1000.0, 5), (1000.0, 6)):
-        k = KernelModel("gaussian", alpha, 4)
-        monkeypatch.setenv("FC2T2_SEP_FAR", "1")
-        far = Engine(k, L, check_admissibility=False)
-        monkeypatch.delenv("FC2T2_SEP_FAR")
-        nofar = Engine(k, L, check_admissibility=False)
-        assert far._sep_far and not nofar._sep_far
-        gen = torch.Generator(device="cuda").manual_seed(L)
-        p = torch.rand(200_000, 3, device="cuda", generator=gen) * 1.999998 - 0.999999
-        w = torch.randn(200_000, 1, device="cuda", generator=gen)
-        m = far.p2m_device(p, w).storage
-        a, b = _np(far.cascade_device(m)), _np(nofar.cascade_device(m))
-        assert rel_l2(a, b) < 1e-6
-
-
-def _run_subprocess(env_extra: dict, code: str) -> str:
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, **env_extra)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
-                       text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
-    return r.stdout
-
-
-def test_opt_in_paths_in_subprocesses(cuda):
-    """The process-wide switches (read once by the library): the order-free
-    fixed-point P2M (FC2T2_P2M_FIXED=1, its own test run with it on) and the
-    cp.async window loader of the separable M2L (FC2T2_SEP_NOTMA=1), whose
-    cascade must equal the TMA loader's bit for bit."""
-    import os
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = _run_subprocess({"FC2T2_P2M_FIXED": "1"},
-                          "import sys, pytest; sys.exit(pytest.main(['-q', '-x', '-p', "
-                          "'no:cacheprovider', '-k', 'cell_bin_and_order_free', "
-                          f"'{root}/tests/test_gpu_expansion.py']))")
-    assert "passed" in out and "skipped" not in out
-    code = ("import torch, hashlib\n"
-            "from paper_2111_00110_b200 import Engine, KernelModel\n"
-            "e = Engine(KernelModel('gaussian', 1000.0, 4), 5, check_admissibility=False)\n"
-            "g = torch.Generator(device='cuda').manual_seed(4)\n"
-            "p = torch.rand(100000, 3, device='cuda', generator=g) * 1.999998 - 0.999999\n"
-            "w = torch.randn(100000, 1, device='cuda', generator=g)\n"
-            "L = e.cascade_device(e.p2m_device(p, w).storage)\n"
-            "print(hashlib.sha1(L.cpu().numpy().tobytes()).hexdigest())\n")
-    a = _run_subprocess({}, code).strip().splitlines()[-1]
-    b = _run_subprocess({"FC2T2_SEP_NOTMA": "1"}, code).strip().splitlines()[-1]
-    assert a == b
 
 
 def test_sharded_layer_single_rank_matches_layers(eng4):

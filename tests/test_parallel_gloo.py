@@ -20,21 +20,60 @@ from paper_2111_00110_b200.parallel import (explicit_forward_sharded, explicit_j
 
 
 class OracleBackend:
+    """The CPU oracle behind the sharding interface.  Everything a rank does
+    not own is poisoned with NaN, so the test proves each phase reads only
+    what the protocol delivered: the slab (M2M chain), the slab plus the
+    3-plane halo (finest M2L), and the all-gathered coarse levels."""
+
     def __init__(self, ora):
         self.o = ora
+        self.levels = ora.levels
         self.slabs = []
 
     def p2m_grid(self, p, w):
         return torch.from_numpy(self.o.p2m(p.numpy(), w.numpy()))
 
-    def cascade_grid(self, m, x_range=None):
+    def slab_split_ok(self, x0, x1):
+        return True
+
+    def cascade(self, m, x_range=None):
         L = torch.from_numpy(self.o.cascade(m.numpy()))
         if x_range is not None:
-            # outside this rank's slab the grid is unspecified: poison it so
-            # the test proves the all-gather assembles only owned slabs
             L[:x_range[0]] = float("nan")
             L[x_range[1]:] = float("nan")
             self.slabs.append(tuple(x_range))
+        return L
+
+    def cascade_up(self, m, x_range):
+        x0, x1 = x_range
+        M = {self.levels: m.clone()}
+        M[self.levels][:x0] = float("nan")
+        M[self.levels][x1:] = float("nan")
+        for lv in range(self.levels, 2, -1):
+            M[lv - 1] = torch.from_numpy(self.o.m2m(M[lv].numpy(), lv))
+        return M
+
+    def coarse_views(self, M):
+        return [(lv, M[lv]) for lv in range(2, self.levels)]
+
+    def cascade_down(self, m, M, x_range):
+        x0, x1 = x_range
+        self.slabs.append(tuple(x_range))
+        mf = m.clone()
+        mf[:max(0, x0 - 3)] = float("nan")
+        mf[x1 + 3:] = float("nan")
+        for lv in range(2, self.levels):
+            assert not torch.isnan(M[lv]).any()       # the coarse all-gathers completed
+        o, t = self.o, self.o.tables
+        L = o.m2l(M[2].numpy(), t["far"][2])
+        for lv in range(3, self.levels):
+            L = o.m2l(M[lv].numpy(), t["far"][lv]) + o.l2l(L, lv - 1)
+        L = o.m2l(mf.numpy(), t["far"][self.levels]) + o.l2l(L, self.levels - 1) + \
+            o.m2l(mf.numpy(), t["near"])
+        L = torch.from_numpy(L)
+        assert not torch.isnan(L[x0:x1]).any()
+        L[:x0] = float("nan")
+        L[x1:] = float("nan")
         return L
 
     def evaluate(self, L, pts, wts, value):
@@ -99,7 +138,8 @@ def test_two_rank_explicit_layer_matches_single_process(tmp_path):
     for got, ref in ((cat("values"), values), (cat("w_bar"), w_bar), (cat("p_bar"), p_bar),
                      (cat("q_bar"), q_bar)):
         assert np.allclose(got, ref, rtol=1e-10, atol=1e-12 * np.abs(ref).max())
-    # each rank computed only its own x-slab of the level-3 (16^3) grid, twice
+    # each rank ran the down phase on its own x-slab of the level-3 (16^3)
+    # grid, once per expansion
     assert [tuple(map(tuple, x["slabs"])) for x in r] == [((0, 8), (0, 8)), ((8, 16), (8, 16))]
 
 
