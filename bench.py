@@ -278,47 +278,64 @@ def seeded_direction(rng):
             return u
 
 
-# Algorithmic bytes per config-2 step, per stage; C = 1.
-# Two expansions per step: the forward of (p, w) and the backward of (q, y_bar).
+# Stages of a config-2 step (library launch labels); two expansions per step:
+# the forward of (p, w) and the backward of (q, y_bar).
 STAGE_GROUPS = {
     "l2p": ["l2p"],
-    "p2m": ["p2m"],
-    "cell_sort": ["cell_keys", "scan", "sort_place", "sort_segments"],
+    "p2m": ["brick_hist", "brick_scan", "brick_scatter", "brick_p2m"],
     "m2l_finest": ["m2l_sep_pre", "m2l_sep_z", "m2l_sep_y", "m2l_sep_x", "m2l_sep_post",
                    "m2l_sep_post_l2l"],
-    "m2l_finest_dense": ["m2l_absmax", "m2l_split", "m2l_tc_L5"],
+    "m2l_coarse": ["m2l_absmax", "m2l_split", "m2l_tc_L4", "m2l_L3", "m2l_L2", "m2l_reduce"],
     "l2l": ["l2l"],
     "m2m": ["m2m"],
     "wgrad_recycle": ["wgrad_recycle"],
 }
 
 
-def stage_rooflines(eng, prof, steps, N, M, hbm_peak):
-    """{stage: bytes per step (the 8(d) model), ms per step, achieved GB/s,
-    fraction of the HBM peak}.  Times are the library's per-launch CUDA events
-    on each launch's stream (the finest M2L overlaps the coarse levels, so
-    coarse-stage times include SM sharing)."""
+def sep_ffma_per_cell(rho: int) -> int:
+    """FFMAs the separable finest M2L executes per cell and expansion
+    (csrc/m2l_sep.cu): the pre transform (lower-triangular per axis), the z,
+    y and x passes (6 taps per output position, index sets truncated to total
+    degree <= rho) and the post transform (upper-triangular per axis)."""
+    R1 = rho + 1
+    ex = [(a, b, c) for t in range(R1) for a in range(t + 1) for b in range(t - a + 1)
+          for c in [t - a - b]]
+    pre = sum(e[k] + 1 for e in ex for k in range(3))
+    post = sum(rho - sum(e) + 1 for e in ex for _ in range(3))
+    z = sum((R1 - a - b) * R1 * 6 for a in range(R1) for b in range(R1 - a))
+    y = sum((R1 - a) * (R1 - c) * 6 for a in range(R1) for c in range(R1))
+    x = sum(R1 * (R1 - b - c) * 6 for b in range(R1) for c in range(R1 - b))
+    return pre + z + y + x + post
+
+
+def stage_rooflines(eng, prof, steps, N, M, hbm_peak, ffma_peak):
+    """Per stage: ALGORITHMIC bytes per step (what the operation must move:
+    inputs read once, outputs written once -- not the kernels' own
+    intermediates), executed FP32 FLOPs where the stage is compute heavy,
+    time per step from the library's per-launch CUDA events on each launch's
+    stream, and the fraction of the binding roofline: t_min / t, t_min =
+    max(bytes / HBM peak, flops / FFMA peak).  The finest M2L runs on a side
+    stream beside the coarse levels, so both spans include SM sharing."""
     P, PP, L = eng.P, eng.PP, eng.levels
     R = (2 ** (L + 1)) ** 3
-    R1 = eng.rho + 1
-    T = R1 * (R1 + 1) // 2 * R1
     grid = 4 * PP * R
+    sep_flops = 2 * 2 * sep_ffma_per_cell(eng.rho) * R   # two expansions, 2 flop per FFMA
     model = {
-        "l2p": (M * (12 + 4 + 12) + grid + N * (12 + 4 + 4 + 12) + grid,
+        "l2p": (M * (12 + 4 + 12) + grid + N * (12 + 4 + 4 + 12) + grid, 0,
                 "q: 12 B in + 4 B value + 12 B grad; p: 12 B + 4 B w + 4 B w_bar + 12 B p_bar; "
-                "+ one finest L grid read per launch"),
-        "p2m": ((N + M) * (12 + 4) + 2 * grid, "12 B point + 4 B weight per point + grid write"),
-        "cell_sort": ((N + M) * (12 + 4) + 2 * 4 * (R + 1),
-                      "12 B point in + 4 B order out per point + cell starts"),
-        "m2l_finest": (2 * 4 * R * (2 * PP + 4 * P + 4 * T),
-                       "per expansion each intermediate read + written once: M rows -> M' -> Z "
-                       "-> Y -> X -> L rows, 4 R (2 PP + 4 P + 4 T) B"),
-        "m2l_finest_dense": (2 * 2 * grid, "per expansion M read + L write"),
+                "+ one finest L grid read per launch (the 144 B row gathers are L2 traffic)"),
+        "p2m": ((N + M) * (12 + 4) + 2 * grid, 0,
+                "12 B point + 4 B weight in per point + the finest M grid written, per expansion"),
+        "m2l_finest": (2 * (2 * grid + grid // 8), sep_flops,
+                       "per expansion: finest M read + L written + the level above's L read "
+                       "(fused L2L); flops = executed FFMAs of the separable form x 2"),
+        "m2l_coarse": (2 * sum(2 * 4 * PP * (2 ** (l + 1)) ** 3 for l in range(2, L)), 0,
+                       "per expansion and coarse level: M read + L written"),
         "l2l": (2 * sum(4 * PP * ((2 ** (l + 1)) ** 3 * 2 + (2 ** l) ** 3)
-                        for l in range(3, L)), "fine read+write + coarse read per level"),
+                        for l in range(3, L)), 0, "fine read+write + coarse read per level"),
         "m2m": (2 * sum(4 * PP * ((2 ** (l + 1)) ** 3 + (2 ** l) ** 3) for l in range(3, L + 1)),
-                "fine read + coarse write per level"),
-        "wgrad_recycle": (M * (12 + 4 + 12), "12 B grad + 4 B y_bar in, 12 B q_bar out"),
+                0, "fine read + coarse write per level"),
+        "wgrad_recycle": (M * (12 + 4 + 12), 0, "12 B grad + 4 B y_bar in, 12 B q_bar out"),
     }
     out = {}
     for st, names in STAGE_GROUPS.items():
@@ -327,11 +344,18 @@ def stage_rooflines(eng, prof, steps, N, M, hbm_peak):
             continue
         ms = sum(prof[n][0] for n in hit) / steps
         launches = sum(prof[n][1] for n in hit) / steps
-        b, how = model[st]
-        gbps = b / (ms / 1000.0) / 1e9
-        out[st] = {"kernels": hit, "ms_per_step": round(ms, 4), "launches_per_step": launches,
-                   "bytes_per_step": b, "achieved_gbps": round(gbps, 1),
-                   "frac": round(gbps / hbm_peak, 4), "model": how}
+        b, fl, how = model[st]
+        t = ms / 1000.0
+        t_hbm, t_fl = b / (hbm_peak * 1e9), (fl / (ffma_peak * 1e12) if fl else 0.0)
+        bound = "fp32_ffma" if t_fl > t_hbm else "hbm"
+        e = {"kernels": hit, "ms_per_step": round(ms, 4), "launches_per_step": launches,
+             "bytes_per_step": b, "achieved_gbps": round(b / t / 1e9, 1),
+             "hbm_frac": round(t_hbm / t, 4), "bound": bound,
+             "frac": round(max(t_hbm, t_fl) / t, 4), "model": how}
+        if fl:
+            e.update(flops_per_step=fl, achieved_tflops=round(fl / t / 1e12, 2),
+                     ffma_frac=round(t_fl / t, 4))
+        out[st] = e
     if "l2p" in out:
         # the cell-row gathers are L2 traffic: 5 sectors (160 B) per point and channel
         sect = (M + N) * 160
@@ -342,6 +366,17 @@ def stage_rooflines(eng, prof, steps, N, M, hbm_peak):
                         "level-5 grid is L2 resident, so the binding resource is the L2 slice "
                         "throughput (~6300 B/clk chip-wide, B300_MICROARCH.md)")
     return out
+
+
+def ffma_peak_tflops():
+    """The FP32 FFMA peak measured on this pool's B200s by scripts/ubench/peaks.py
+    (profiles/r2_peaks.json), else the nominal 148 SMs x 128 FMA/clk x 2 x
+    1.965 GHz."""
+    try:
+        v = json.loads((ROOT / "profiles" / "r2_peaks.json").read_text())["ffma_tflops"]
+        return float(v), "measured FFMA peak (profiles/r2_peaks.json, scripts/ubench/peaks.cu)"
+    except Exception:
+        return 74.45, "nominal 148 SM x 128 FMA/clk x 1.965 GHz"
 
 
 def measured_traffic(kernels):
@@ -483,12 +518,12 @@ def secondary(dev, flush, stream, steps: int) -> dict:
         return depth_surface_jvp(yl, yg, res), res
     st3 = {}
     ms, (g3, r3) = timed_steps(step3, steps, 3, flush, stream, st3)
-    # secondary ray lines: median step (median of >= 20 runs);
-    # the mean, which a single host hiccup can dominate, is kept beside it
+    # every line: value from the mean step (as the headline); the median
+    # is kept beside it
     med3 = st3.get("_step_ms_median", ms / steps)
     out["cfg3_root_depth_normal"] = {
-        "metric": "rays/s", "value": R3 / (med3 / 1e3), "ms_per_step": med3,
-        "mean_ms_per_step": ms / steps,
+        "metric": "rays/s", "value": R3 / (ms / steps / 1e3), "ms_per_step": ms / steps,
+        "median_ms_per_step": med3,
         "hit_fraction": float(r3.hit.float().mean().item()), "stages_ms_per_step": st3,
         "workload": "N=2^18, 512x512 rays, radius 2, fov 60, level 5, bias +0.05, depth+normal "
                     "adjoints in one fused insertion"}
@@ -518,8 +553,8 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     ms, _ = timed_steps(step4, max(2, steps // 4), 1, flush, stream, st4)
     k = max(2, steps // 4)
     med4 = st4.get("_step_ms_median", ms / k)
-    out["cfg4_radiance"] = {"metric": "rays/s", "value": R4 / (med4 / 1e3), "ms_per_step": med4,
-                            "mean_ms_per_step": ms / k,
+    out["cfg4_radiance"] = {"metric": "rays/s", "value": R4 / (ms / k / 1e3), "ms_per_step": ms / k,
+                            "median_ms_per_step": med4,
                             "stages_ms_per_step": st4,
                             "workload": "N=2^20 (|N(0,1)| density, U(0,1) RGB), 8 poses x 400x400, "
                                         "radius 2.5, fov 50, level 5, MSE vs U(0,1) target"}
@@ -820,37 +855,42 @@ def run_ours(args, rank: int, world: int) -> None:
     hbm_peak = float(peaks.get("hbm_gbs", 7672.0))
     hbm_src = ("measured HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks
                else "fallback (B200_PROFILING.md)")
-    peak = float(peaks.get("bf16_tflops", 1590.0))
-    peak_src = "measured bf16 dense (MEASURED_PEAKS.json)" if "bf16_tflops" in peaks else \
-        "fallback 1.59 PF (B200_PROFILING.md)"
-    rl_stages = stage_rooflines(eng, prof, args.steps, N, M, hbm_peak)
+    ffma_peak, ffma_src = ffma_peak_tflops()
+    rl_stages = stage_rooflines(eng, prof, args.steps, N, M, hbm_peak, ffma_peak)
     dom = max(rl_stages, key=lambda k: rl_stages[k]["ms_per_step"])
     d = rl_stages[dom]
     traffic = measured_traffic(d["kernels"])
-    roofline = {"kernel": dom, "bound": "hbm", "achieved": d["achieved_gbps"], "peak": hbm_peak,
-                "unit": "GB/s", "frac": d["frac"],
+    if d["bound"] == "hbm":
+        rl_core = {"bound": "hbm", "achieved": d["achieved_gbps"], "peak": hbm_peak,
+                   "unit": "GB/s", "peak_source": hbm_src}
+    else:
+        rl_core = {"bound": "fp32_ffma", "achieved": d["achieved_tflops"], "peak": ffma_peak,
+                   "unit": "TFLOP/s", "peak_source": ffma_src,
+                   "hbm_frac": d["hbm_frac"], "hbm_peak_gbs": hbm_peak}
+    roofline = {"kernel": dom, **rl_core, "frac": d["frac"],
                 "traffic": (traffic["bytes_per_step"] if traffic else None),
                 "traffic_source": (traffic["source"] if traffic else None),
                 "ncu_serial_ms_per_step": (traffic["serial_ms_per_step"] if traffic else None),
-                "peak_source": hbm_src, "bytes_per_step": d["bytes_per_step"],
+                "bytes_per_step": d["bytes_per_step"],
                 "launch_ms": d["ms_per_step"] / max(d["launches_per_step"], 1),
                 "launches_per_step": d["launches_per_step"], "bytes_model": d["model"]}
     if "l2_sector_bytes_per_step" in d:
         roofline["l2_sector_bytes_per_step"] = d["l2_sector_bytes_per_step"]
         roofline["l2_tbps"] = d["l2_tbps"]
         roofline["l2_note"] = d["l2_note"]
-    # the finest-level M2L against the reference's own FLOP count (8(a) a8)
+    # the finest-level M2L against the reference's own FLOP count (8(a) a8):
+    # a speed ratio only -- the separable form executes ~1/60 of these FLOPs
     m2l_keys = [k for k in prof if k.startswith("m2l_sep_") or k == f"m2l_tc_L{CFG['levels']}"]
     m2l_ms = sum(prof[k][0] for k in m2l_keys) / args.steps
     pairs = m2l_pairs(eng.m2l_tables["far"][CFG["levels"]]) + m2l_pairs(eng.m2l_tables["near"])
     flops_exp = pairs * 1 * eng.P * eng.P * 2
     m2l_line = {"kernels": sorted(m2l_keys), "ms_per_step": m2l_ms,
                 "reference_flops_per_expansion": flops_exp,
-                "reference_flop_rate_tflops": 2 * flops_exp / (m2l_ms / 1000.0) / 1e12,
-                "vs_bf16_peak": 2 * flops_exp / (m2l_ms / 1000.0) / 1e12 / peak,
-                "peak_source": peak_src,
+                "reference_equivalent_tflops": 2 * flops_exp / (m2l_ms / 1000.0) / 1e12,
+                "executed_flops_per_expansion": 2 * sep_ffma_per_cell(eng.rho) * (
+                    2 ** (CFG["levels"] + 1)) ** 3 if eng.separable else None,
                 "algorithm": ("separable: per-axis transforms + three 1-D convolutions "
-                              "(FFMA, memory bound -- see roofline_stages.m2l_finest)"
+                              "(FFMA -- see roofline_stages.m2l_finest)"
                               if eng.separable else
                               "dense tcgen05 kind::f16 two-term split")}
     stages = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items())}

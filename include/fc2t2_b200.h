@@ -127,26 +127,6 @@ size_t fc2t2_cell_sort_workspace_size(int level, int64_t n);
 int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
                     int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
                     void* stream);
-/* Cell binning without the per-cell index sort: cells contiguous and in
- * order, points inside a cell in arrival order.  Same outputs/workspace as
- * fc2t2_cell_sort; enough for fc2t2_p2m whenever fc2t2_p2m_order_free(rho)
- * (its exact fixed-point sums do not depend on the order inside a cell). */
-int fc2t2_cell_bin(int level, const float* d_pts, int64_t n, int32_t* d_order,
-                   int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
-                   void* stream);
-int fc2t2_p2m_order_free(int rho);
-/* The same sort, also returning d_inv (n) int32 = sorted position of every
- * point and d_pts_sorted (n, 3) = the points in sorted order, both written
- * without random reads of d_pts (give both or neither).  With them, P2M takes
- * d_pts_sorted and weights permuted by fc2t2_permute_rows with d_order = NULL,
- * and L2P reads its inputs coalesced (FC2T2_L2P_PRESORTED). */
-int fc2t2_cell_sort_ex(int level, const float* d_pts, int64_t n, int32_t* d_order,
-                       int32_t* d_cell_start, int32_t* d_inv, float* d_pts_sorted,
-                       int32_t* d_flag, void* d_ws, size_t ws_bytes, void* stream);
-/* d_dst[d_inv[i], :] = d_src[i, :] for n rows of `cols` floats */
-int fc2t2_permute_rows(const float* d_src, int64_t n, int cols, const int32_t* d_inv,
-                       float* d_dst, void* stream);
-
 /* ---- P2M from unsorted points (Engine.p2m, expansion.py:186-198) ----
  * d_pts (n, 3), d_w (n, C) in the caller's order; no sort object.  A
  * deterministic stable partition of the points into bricks of 8 x 8 x 4

@@ -47,10 +47,6 @@ _SIGS = {
     "fc2t2_find_box": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp]),
     "fc2t2_cell_sort_workspace_size": (_sz, [_i32, _i64]),
     "fc2t2_cell_sort": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "fc2t2_cell_bin": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "fc2t2_p2m_order_free": (_i32, [_i32]),
-    "fc2t2_cell_sort_ex": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "fc2t2_permute_rows": (_i32, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "fc2t2_loss_workspace_size": (_sz, [_i64, _i32]),
     "fc2t2_loss": (_i32, [_vp, _vp, _vp, _i64, _i32, ct.c_float, _i32, _vp, _vp, _vp, _sz, _vp]),
     "fc2t2_nonfinite": (_i32, [_vp, _i64, _vp, _vp]),

@@ -52,9 +52,6 @@ struct Plan {
   int max_list = 0;
   // tcgen05 form (parity levels): dense split tables, see build_tc_table
   bool tc = false;
-  bool f16 = true;
-  bool merge_last = false;
-  int cg = 1;
   std::vector<uint8_t> tcb;
   std::vector<float> rk, s_inv;
   uint8_t* d_tcb = nullptr;
@@ -89,8 +86,26 @@ cudaEvent_t next_event() {
 }
 }  // namespace
 
+// FC2T2_DEBUG_ERRORS=1: report a launch that fails, or a CUDA error left
+// pending by an earlier runtime call, naming the kernel (stderr)
+const char* g_last_name = "(none)";
+bool debug_errors() {
+  static const bool v = [] {
+    const char* e = std::getenv("FC2T2_DEBUG_ERRORS");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 void prof_begin(const char* name, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (debug_errors()) {
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess)
+      std::fprintf(stderr, "fc2t2: pending CUDA error before launch %s (previous launch %s): %s\n",
+                   name, g_last_name, cudaGetErrorString(e));
+    g_last_name = name;
+  }
   if (!g_prof) return;
   g_pending_ev = next_event();
   cudaEventRecord(g_pending_ev, s);
@@ -98,6 +113,11 @@ void prof_begin(const char* name, cudaStream_t s) {
 }
 
 void prof_end(cudaStream_t s) {
+  if (debug_errors()) {
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess)
+      std::fprintf(stderr, "fc2t2: launch %s: %s\n", g_last_name, cudaGetErrorString(e));
+  }
   if (!g_prof || !g_pending) return;
   cudaEvent_t b = next_event();
   cudaEventRecord(b, s);
@@ -127,29 +147,6 @@ struct fc2t2_engine {
 namespace {
 
 constexpr int kCoarsest = 2;
-
-// host emulation of cvt.rna.tf32.f32 (round to nearest, ties away)
-float rn_tf32_host(double v) {
-  float f = (float)v;
-  uint32_t b;
-  std::memcpy(&b, &f, 4);
-  if ((b & 0x7f800000u) != 0x7f800000u) b = (b + 0x1000u) & 0xffffe000u;
-  std::memcpy(&f, &b, 4);
-  return f;
-}
-
-// CTA pairs (cta_group::2) are built and parity-tested but opt-in: measured
-// on one box, level 5 0.500 vs 0.484 ms and rho 6 1.94 vs 1.84 ms single-CTA --
-// the kernel is bound by its MMA stream, not by the table traffic pairs halve.
-bool cg2_mode() {
-  const char* v = std::getenv("FC2T2_TC_CG2");
-  return v && v[0] == '1';
-}
-
-bool nomerge_mode() {
-  const char* v = std::getenv("FC2T2_TC_NOMERGE");
-  return v && v[0] == '1';
-}
 
 // host round-to-nearest-even to fp16; returns the bits and the exact value
 uint16_t half_rn(double v, double* val) {
@@ -189,33 +186,25 @@ uint16_t half_rn(double v, double* val) {
 // are the CLS tables A_delta, delta = 2 s + sigma - pi (the sum of the plan's
 // entries with that offset for class pi; zero if none), split in float64 into
 // hi and lo parts.  Row order: even sigma [lo(class 0..) | hi(class 0..)], odd
-// sigma [hi | lo]; K-major no-swizzle [kchunk][row][16 B].
-//   tf32: hi = rn_tf32(A), lo = rn_tf32(A - hi).
-//   f16:  B' = A s_n / r_k, hi = rn_f16(B'), lo = rn_f16((B' - hi) 2^11), with
-//         s_n = (h/2)^|n|/n! at the plan's level and r_k a power of two with
-//         max_{slot,n} |B'| <= 2^13 (returned in rk, NC entries; s_inv = 1/s_n).
+// sigma [hi | lo]; K-major no-swizzle [kchunk][row][16 B].  B' = A s_n / r_k,
+// hi = rn_f16(B'), lo = rn_f16((B' - hi) 2^11), with s_n = (h/2)^|n|/n! at the
+// plan's level and r_k a power of two with max_{slot,n} |B'| <= 2^13
+// (returned in rk, NC entries; s_inv = 1/s_n).
 void build_tc_table(const std::vector<std::vector<int4>>& lists,
                     const std::vector<const double*>& slot_src, int P, int PP, int rho, int level,
-                    bool f16, Plan& plan) {
+                    Plan& plan) {
   int CLS, NC, KS, BSLOT, FL, TILES;
-  if (fc2t2::tc_geometry(rho, f16 ? 1 : 0, 1, &CLS, &NC, &KS, &BSLOT, &FL, &TILES) != 0) return;
-  // CTA pairs (cta_group::2) when the level fills at least two waves of CTAs
-  const int nu = (1 << (level + 1)) / 2;
-  const long ctas = (long)(nu / TILES) * (nu / 16) * (nu / 8) * (8 / CLS);
-  const int CG = (ctas >= 2 * 148 && cg2_mode() && (CLS * NC / 2) % 8 == 0) ? 2 : 1;
-  if (CG == 2) fc2t2::tc_geometry(rho, f16 ? 1 : 0, 2, &CLS, &NC, &KS, &BSLOT, &FL, &TILES);
-  plan.cg = CG;
-  const bool SB = FL & 1, MERGE = (FL & 2) && !nomerge_mode();
-  plan.merge_last = MERGE;
-  const int W = CLS * NC, R = CG == 2 ? 3 * W / 2 : 2 * W, NCG = 8 / CLS;
-  const int KI = f16 ? 16 : 8, ESZ = f16 ? 2 : 4;
+  if (fc2t2::tc_geometry(rho, &CLS, &NC, &KS, &BSLOT, &FL, &TILES) != 0) return;
+  const bool SB = FL & 1, MERGE = FL & 2;
+  const int W = CLS * NC, R = 2 * W, NCG = 8 / CLS;
+  constexpr int KI = 16, ESZ = 2;
   std::vector<double> sn(P, 1.0);
-  if (f16) fc2t2::tc_moment_scales(rho, level, sn.data());
+  fc2t2::tc_moment_scales(rho, level, sn.data());
   plan.s_inv.assign(PP, 0.f);
   for (int n = 0; n < P; ++n) plan.s_inv[n] = (float)(1.0 / sn[n]);
   // per output column k: power of two r_k with max |A[k][n] s_n| / r_k <= 2^13
   std::vector<double> rk(NC, 1.0);
-  if (f16) {
+  {
     std::vector<double> mx(P, 0.0);
     for (const auto& l : lists)
       for (const int4& e : l) {
@@ -232,7 +221,7 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
   }
   plan.rk.assign(NC, 1.f);
   for (int k = 0; k < NC; ++k) plan.rk[k] = (float)rk[k];
-  plan.tcb.assign((size_t)NCG * 8 * KS * CG * 27 * BSLOT, 0);
+  plan.tcb.assign((size_t)NCG * 8 * KS * 27 * BSLOT, 0);
   std::vector<double> A((size_t)P * P);
   for (int cg = 0; cg < NCG; ++cg)
     for (int sg = 0; sg < 8; ++sg) {
@@ -254,26 +243,13 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
             }
           if (!any) continue;
           const bool odd = (sg & 1) && !SB;   // single-buffered kernels keep [lo | hi]
-          // one CTA: rows [lo | hi] (even) or [hi | lo] (odd), 2W per slot.
-          // CTA pairs: rank 0 holds the first main half, rank 1 the second
-          // (W rows each), then each holds its half of the cross operand B_hi
-          // (W/2 rows); rows of another rank are skipped (-1).
+          // rows [lo | hi] (even) or [hi | lo] (odd), 2W per slot
           const int f = ci * NC;                     // flattened (class, k) base
-          for (int ks = 0; ks < KS; ++ks)
-            for (int rk_ = 0; rk_ < CG; ++rk_) {
-              int hi_row, lo_row, x_lo = -1;         // x_lo: cross rows [x_lo, x_lo + W/2)
-              if (CG == 1) {
-                hi_row = odd ? f : W + f;
-                lo_row = odd ? W + f : f;
-              } else {
-                // main half: rank 0 = D cols [mcol, mcol + W) = lo (even) / hi (odd)
-                const bool lo_first = !odd;
-                hi_row = (lo_first ? (rk_ == 1) : (rk_ == 0)) ? f : -1;
-                lo_row = (lo_first ? (rk_ == 0) : (rk_ == 1)) ? f : -1;
-                x_lo = rk_ * (W / 2);
-              }
+          for (int ks = 0; ks < KS; ++ks) {
+              const int hi_row = odd ? f : W + f;
+              const int lo_row = odd ? W + f : f;
               uint8_t* st = plan.tcb.data() +
-                            (((((size_t)cg * 8 + sg) * KS + ks) * CG + rk_) * 27 + slot) * BSLOT;
+                            ((((size_t)cg * 8 + sg) * KS + ks) * 27 + slot) * BSLOT;
               const bool merged = MERGE && ks == KS - 1;
               for (int kc = 0; kc < 2; ++kc)
                 for (int k = 0; k < P; ++k)
@@ -281,40 +257,25 @@ void build_tc_table(const std::vector<std::vector<int4>>& lists,
                     const int n = KI * ks + (merged ? 0 : (KI / 2) * kc) + fi;
                     if (n >= P) continue;
                     const double a = A[(size_t)k * P + n];
-                    double bh, bl, bhl;   // tf32: raw parts; f16: scaled parts
-                    uint8_t hb[4], lb[4], hb1[4];
-                    if (f16) {
-                      const double b = a * sn[n] / rk[k];
-                      double hv, lv;
-                      const uint16_t h16 = half_rn(b, &hv);
-                      const uint16_t l16 = half_rn((b - hv) * 2048.0, &lv);
-                      std::memcpy(hb, &h16, 2);
-                      std::memcpy(lb, &l16, 2);
-                      std::memcpy(hb1, &h16, 2);
-                      (void)bh; (void)bl; (void)bhl;
-                    } else {
-                      const float hi = rn_tf32_host(a);
-                      const float lo = rn_tf32_host(a - (double)hi);
-                      std::memcpy(hb, &hi, 4);
-                      std::memcpy(lb, &lo, 4);
-                      std::memcpy(hb1, &hi, 4);
-                    }
+                    uint8_t hb[2], lb[2];
+                    const double b = a * sn[n] / rk[k];
+                    double hv, lv;
+                    const uint16_t h16 = half_rn(b, &hv);
+                    const uint16_t l16 = half_rn((b - hv) * 2048.0, &lv);
+                    std::memcpy(hb, &h16, 2);
+                    std::memcpy(lb, &l16, 2);
                     auto put = [&](int row, const uint8_t* v) {
                       std::memcpy(st + ((size_t)kc * R + row) * 16 + fi * ESZ, v, ESZ);
                     };
                     if (merged && kc == 1) {
                       // chunk 1 multiplies the A_lo chunk: lo rows get B_hi, hi rows 0
-                      if (lo_row >= 0) put(lo_row + k, hb1);
+                      put(lo_row + k, hb);
                       continue;
                     }
-                    if (hi_row >= 0) put(hi_row + k, hb);
-                    if (lo_row >= 0) put(lo_row + k, lb);
-                    if (CG == 2 && !merged) {
-                      const int fk = f + k;           // flattened column of B_hi
-                      if (fk >= x_lo && fk < x_lo + W / 2) put(W + (fk - x_lo), hb);
-                    }
+                    put(hi_row + k, hb);
+                    put(lo_row + k, lb);
                   }
-            }
+          }
         }
       }
     }
@@ -365,23 +326,13 @@ void finish_plan(Plan& p, std::vector<std::vector<int4>>& lists) {
   p.tc = p.ncls == 8;
 }
 
-bool tf32_mode() {
-  const char* v = std::getenv("FC2T2_M2L_TF32");
-  return v && v[0] == '1';
-}
-
-bool force_ffma() {
-  const char* v = std::getenv("FC2T2_M2L_FFMA");
-  return v && v[0] == '1';
-}
-
 // tensor-core M2L for a level: parity stencil and at least a 16^3 class lattice
 bool use_tc(const Plan& p, int level) {
-  return p.tc && p.d_tcb && p.max_list > 0 && (1 << (level + 1)) / 2 >= 16 && !force_ffma();
+  return p.tc && p.d_tcb && p.max_list > 0 && (1 << (level + 1)) / 2 >= 16;
 }
 
 size_t tc_ws_bytes(const Plan& p, int rho, int level, int C) {
-  return fc2t2::tc_workspace_bytes(rho, level, C, p.f16 ? 1 : 0);
+  return fc2t2::tc_workspace_bytes(rho, level, C);
 }
 
 int plan_for(const fc2t2_engine* e, int level, int table, const Plan** out) {
@@ -398,11 +349,8 @@ fc2t2::TCPlan tc_of(const fc2t2_engine* e, const Plan& p, int level) {
   fc2t2::TCPlan t;
   t.level = level;
   t.btab = p.d_tcb;
-  t.f16 = p.f16;
   t.rk = p.d_rk;
   t.s_inv = p.d_sinv;
-  t.merge_last = p.merge_last;
-  t.cg = p.cg;
   static const char* names[] = {"m2l_tc_L0", "m2l_tc_L1", "m2l_tc_L2", "m2l_tc_L3", "m2l_tc_L4",
                                 "m2l_tc_L5", "m2l_tc_L6", "m2l_tc_L7", "m2l_tc_L8", "m2l_tc_L9"};
   t.level_name = names[level < 0 ? 0 : (level > 9 ? 9 : level)];
@@ -537,10 +485,7 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       Plan& p = e->plans[l][FC2T2_TABLE_FAR];
       p.stride = parity ? 2 : 1;
       finish_plan(p, lists);
-      if (p.tc && tc_level(l)) {
-        p.f16 = !tf32_mode();
-        build_tc_table(lists, slot_src, P, PP, e->rho, l, p.f16, p);
-      }
+      if (p.tc && tc_level(l)) build_tc_table(lists, slot_src, P, PP, e->rho, l, p);
     }
     if (l == e->levels) {
       std::vector<std::vector<int4>> nl(1);
@@ -558,10 +503,7 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
       Plan& pm = e->plans[l][FC2T2_TABLE_FARNEAR];
       pm.stride = pf.stride;
       finish_plan(pm, ml);
-      if (pm.tc && tc_level(l)) {
-        pm.f16 = !tf32_mode();
-        build_tc_table(ml, slot_src, P, PP, e->rho, l, pm.f16, pm);
-      }
+      if (pm.tc && tc_level(l)) build_tc_table(ml, slot_src, P, PP, e->rho, l, pm);
     }
   }
   cudaStream_t s = (cudaStream_t)stream;
@@ -655,42 +597,6 @@ int fc2t2_cell_sort(int level, const float* d_pts, int64_t n, int32_t* d_order,
                      "cell_sort");
 }
 
-int fc2t2_cell_bin(int level, const float* d_pts, int64_t n, int32_t* d_order,
-                   int32_t* d_cell_start, int32_t* d_flag, void* d_ws, size_t ws_bytes,
-                   void* stream) {
-  if (level < 0 || level > 9 || n < 0 || n > INT32_MAX)
-    return fail(FC2T2_EVALUE, "bad cell_bin arguments");
-  if (ws_bytes < fc2t2::cell_sort_workspace(level, n))
-    return fail(FC2T2_EWORKSPACE, "cell_bin workspace too small");
-  return cuda_status(fc2t2::cell_sort(level, d_pts, n, d_order, d_cell_start, d_flag, d_ws,
-                                      ws_bytes, (cudaStream_t)stream, nullptr, nullptr, false),
-                     "cell_bin");
-}
-
-int fc2t2_p2m_order_free(int rho) { return fc2t2::p2m_fixed_point(rho) ? 1 : 0; }
-
-int fc2t2_cell_sort_ex(int level, const float* d_pts, int64_t n, int32_t* d_order,
-                       int32_t* d_cell_start, int32_t* d_inv, float* d_pts_sorted,
-                       int32_t* d_flag, void* d_ws, size_t ws_bytes, void* stream) {
-  if (level < 0 || level > 9 || n < 0 || n > INT32_MAX)
-    return fail(FC2T2_EVALUE, "bad cell_sort arguments");
-  if ((d_inv == nullptr) != (d_pts_sorted == nullptr))
-    return fail(FC2T2_EVALUE, "cell_sort_ex: give both d_inv and d_pts_sorted or neither");
-  if (ws_bytes < fc2t2::cell_sort_workspace(level, n))
-    return fail(FC2T2_EWORKSPACE, "cell_sort workspace too small");
-  return cuda_status(fc2t2::cell_sort(level, d_pts, n, d_order, d_cell_start, d_flag, d_ws,
-                                      ws_bytes, (cudaStream_t)stream, d_inv, d_pts_sorted),
-                     "cell_sort_ex");
-}
-
-int fc2t2_permute_rows(const float* d_src, int64_t n, int cols, const int32_t* d_inv,
-                       float* d_dst, void* stream) {
-  if (n < 0 || cols < 1 || (n > 0 && (!d_src || !d_inv || !d_dst)))
-    return fail(FC2T2_EVALUE, "bad permute_rows arguments");
-  return cuda_status(fc2t2::permute_rows(d_src, n, cols, d_inv, d_dst, (cudaStream_t)stream),
-                     "permute_rows");
-}
-
 int fc2t2_p2m(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
               const int32_t* d_order, const int32_t* d_cell_start, float* d_m_finest,
               void* stream) {
@@ -756,7 +662,7 @@ int fc2t2_l2l(const fc2t2_engine* e, int channels, int coarse_level, const float
 double fc2t2_m2l_issued_flops(const fc2t2_engine* e, int channels, int level, int table) {
   const Plan* p;
   if (plan_for(e, level, table, &p) != FC2T2_OK || !use_tc(*p, level)) return 0.0;
-  return fc2t2::tc_issued_flops(e->rho, level, channels, p->f16 ? 1 : 0, p->merge_last ? 1 : 0);
+  return fc2t2::tc_issued_flops(e->rho, level, channels);
 }
 
 size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table) {

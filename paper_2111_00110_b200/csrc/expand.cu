@@ -109,71 +109,6 @@ p2m_sorted_kernel(const float* __restrict__ pts, const float* __restrict__ w, in
   }
 }
 
-// Order-free deterministic P2M (rho <= 5): the same terms t = w * d^n/n!
-// (each rounded once to float32), summed exactly.  Per cell and channel,
-// g = 2^e >= max |w| (a first walk over the cell's weights; max is order
-// free) and s_n = (h/2)^|n| >= |d^n / n!|, so t / (g s_n) is in [-1, 1]:
-// scaled by the power of two 2^30 / (g s_n) (exact, in float64), rounded to
-// an integer and accumulated in int64.  Integer addition is associative, so
-// the moments do not depend on the order of a cell's points -- the cell sort
-// needs no per-cell index sort -- and they are at least as accurate as the
-// sequential float32 sum (quantum 2^-30 of the largest possible term).
-template <int RHO>
-__global__ void __launch_bounds__(128)
-p2m_fixed_kernel(const float* __restrict__ pts, const float* __restrict__ w, int C, int res,
-                 const int32_t* __restrict__ order, const int32_t* __restrict__ cell_start,
-                 float* __restrict__ M) {
-  constexpr MI<RHO> mi{};
-  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
-  const int64_t R = (int64_t)res * res * res;
-  int lres = 0;
-  while ((1 << lres) < res) ++lres;   // h / 2 = 1 / res = 2^-lres
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R * C;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cell = g / C;
-    const int c = (int)(g - cell * C);
-    const int b2 = (int)(cell % res), b1 = (int)((cell / res) % res), b0 = (int)(cell / res / res);
-    const int beg = cell_start[cell], end = cell_start[cell + 1];
-    float mx = 0.f;
-    for (int k = beg; k < end; ++k) {
-      const int64_t i = order ? (int64_t)order[k] : (int64_t)k;
-      mx = fmaxf(mx, fabsf(w[i * C + c]));
-    }
-    long long acc[P];
-#pragma unroll
-    for (int j = 0; j < P; ++j) acc[j] = 0;
-    int e = 0;
-    if (mx > 0.f) frexpf(mx, &e);     // mx < 2^e
-    // scale for degree t: 2^(30 - e + lres * t)
-    double sc[RHO + 1];
-#pragma unroll
-    for (int t = 0; t <= RHO; ++t) sc[t] = ldexp(1.0, 30 - e + lres * t);
-    if (mx > 0.f) {
-      for (int k = beg; k < end; ++k) {
-        const int64_t i = order ? (int64_t)order[k] : (int64_t)k;
-        const float dx = box_offset(pts[3 * i], b0, res);
-        const float dy = box_offset(pts[3 * i + 1], b1, res);
-        const float dz = box_offset(pts[3 * i + 2], b2, res);
-        const float wv = w[i * C + c];
-        float mono[P];
-        monomials<RHO>(dx, dy, dz, mono);
-#pragma unroll
-        for (int j = 0; j < P; ++j) {
-          const float t = __fmul_rn(wv, mono[j]);
-          acc[j] += __double2ll_rn((double)t * sc[mi.e0[j] + mi.e1[j] + mi.e2[j]]);
-        }
-      }
-    }
-    float out[PP];
-#pragma unroll
-    for (int j = 0; j < PP; ++j) out[j] = 0.f;
-#pragma unroll
-    for (int j = 0; j < P; ++j)
-      out[j] = (float)((double)acc[j] / sc[mi.e0[j] + mi.e1[j] + mi.e2[j]]);
-    store_row<PP>(M + g * PP, out, false);
-  }
-}
-
 // ------------------------------------------------------------- M2M/L2L ---
 // Child centre offset from the parent centre is d = (c - 1/2) * w_fine per
 // axis (reference expansion.py:170-175).  The binomial shift kernel
@@ -397,31 +332,14 @@ size_t m2l_smem() {
 
 }  // namespace
 
-// Opt-in (FC2T2_P2M_FIXED=1): measured on B200 at config 2 the fixed-point
-// P2M costs 0.52 vs 0.21 ms per step (float64 scaling + 64-bit conversions per
-// term) while the per-cell index sort it makes unnecessary costs 0.24 ms.
-bool p2m_fixed_point(int rho) {
-  static const bool fixed = [] {
-    const char* e = std::getenv("FC2T2_P2M_FIXED");
-    return e && e[0] == '1';
-  }();
-  return rho <= 5 && fixed;
-}
-
 cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float* w,
                        const int32_t* order, const int32_t* cell_start, float* M,
                        cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int64_t n = (int64_t)res * res * res * C;
-  if (p2m_fixed_point(rho)) {
-    FC2T2_DISPATCH_RHO(rho, if constexpr (RHO <= 5) FC2T2_LAUNCH("p2m", s,
-        p2m_fixed_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(
-            pts, w, C, res, order, cell_start, M)));
-  } else {
-    FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("p2m", s,
-        p2m_sorted_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(
-            pts, w, C, res, order, cell_start, M)));
-  }
+  FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("p2m", s,
+      p2m_sorted_kernel<RHO><<<grid_blocks(n, 128, 148 * 64), 128, 0, s>>>(
+          pts, w, C, res, order, cell_start, M)));
   return cudaGetLastError();
 }
 
@@ -460,18 +378,9 @@ int m2l_splits(int rho, int C, const M2LLaunch& plan) {
   const int rows = 128 * (index_count(rho) <= 35 ? 2 : 1);
   const int tpt = std::max(1, rows / C);
   const int64_t ctas = ((int64_t)nu * nu * nu + tpt - 1) / tpt * plan.ncls;
-  static const int waves = [] {
-    const char* e = std::getenv("FC2T2_M2L_SPLIT_WAVES");
-    const int v = e ? std::atoi(e) : 2;
-    return v > 0 ? v : 2;
-  }();
-  static const int cap = [] {
-    // measured at config 2 level 3 (16 CTAs per split): 19 splits 45 us,
-    // 16 splits 54 us, 32 splits 56 us per launch
-    const char* e = std::getenv("FC2T2_M2L_SPLIT_CAP");
-    const int v = e ? std::atoi(e) : 32;
-    return v > 0 ? v : 32;
-  }();
+  // two waves of CTAs, at most 32 splits (measured at config 2 level 3, 16
+  // CTAs per split: 19 splits 45 us, 16 splits 54 us, 32 splits 56 us)
+  constexpr int waves = 2, cap = 32;
   const int64_t want = (waves * 148 + ctas - 1) / ctas;
   return (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)cap, (int64_t)plan.max_list}));
 }

@@ -8,15 +8,9 @@ namespace fc2t2 {
 
 // sort.cu ----------------------------------------------------------------
 size_t cell_sort_workspace(int level, int64_t n);
-// stable = false skips the per-cell index sort (cells contiguous, arrival
-// order inside a cell): enough for the order-free fixed-point P2M
 cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order,
                       int32_t* cell_start, int32_t* flag, void* ws, size_t ws_bytes,
-                      cudaStream_t s, int32_t* inv = nullptr, float* pts_sorted = nullptr,
-                      bool stable = true);
-// dst[inv[i], :] = src[i, :]
-cudaError_t permute_rows(const float* src, int64_t n, int cols, const int32_t* inv, float* dst,
-                         cudaStream_t s);
+                      cudaStream_t s);
 cudaError_t find_box(int level, const float* pts, int64_t n, int32_t* box, int32_t* flag,
                      cudaStream_t s);
 // stable sort of precomputed cell keys (key >= res^3 = "no cell", sorted last)
@@ -36,10 +30,7 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
                       float* M, int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s);
 
 // expand.cu --------------------------------------------------------------
-// true (FC2T2_P2M_FIXED=1, rho <= 5): P2M sums exactly in fixed point (order
-// free: a cell sort without the per-cell index sort suffices); false
-// (default): float32 in the stable sort's index order
-bool p2m_fixed_point(int rho);
+// float32 sums of each cell's points in the stable sort's index order
 cudaError_t p2m_sorted(int rho, int level, int C, const float* pts, const float* w,
                        const int32_t* order, const int32_t* cell_start, float* M,
                        cudaStream_t s);
@@ -73,31 +64,26 @@ cudaError_t m2l(int rho, int C, const M2LLaunch& plan, const float* coef, const 
 // m2l_tc.cu --------------------------------------------------------------
 // tcgen05 M2L for parity levels.  btab is the plan's dense table:
 // [class group][source class 8][K step][slot 27][kchunk 2][row 2W][16 B]
-// (see tc_geometry and abi.cu build_tc_table).  f16 plans use the scaled
-// two-term fp16 split (rk: per-output-column scales, s_inv: 1/s_n per
-// coefficient); otherwise 3xTF32.
+// (see tc_geometry and abi.cu build_tc_table), the scaled two-term fp16 split
+// (rk: per-output-column scales, s_inv: 1/s_n per coefficient).
 struct TCPlan {
   int level;
   const uint8_t* btab;
   const char* level_name;
-  bool f16 = true;
   const float* rk = nullptr;
   const float* s_inv = nullptr;
-  bool merge_last = true;   // tables built with the merged last K step
-  int cg = 1;               // 2: CTA-pair tables and kernel (cta_group::2)
 };
 // classes per CTA, N per class, K steps, bytes per slot table, flags (bit 0:
 // single-buffered layout, B rows always [lo | hi]; bit 1: merged last K step,
 // see TC::MERGE_LAST); 0 on success
-int tc_geometry(int rho, int f16, int cg, int* cls, int* nc, int* ks, int* bslot, int* sb,
-                int* tiles);
+int tc_geometry(int rho, int* cls, int* nc, int* ks, int* bslot, int* sb, int* tiles);
 // tensor-core FLOPs one m2l_tc launch issues (2 M N K per MMA, padding and
 // split terms included) for a whole level
-double tc_issued_flops(int rho, int level, int C, int f16, int merge_last);
+double tc_issued_flops(int rho, int level, int C);
 // s_n = (h/2)^|n| / n! at a level, graded-lex order (P doubles)
 int tc_moment_scales(int rho, int level, double* s);
 // scratch of one M2L launch: per-channel scale bits + hi/lo operand planes
-size_t tc_workspace_bytes(int rho, int level, int C, int f16);
+size_t tc_workspace_bytes(int rho, int level, int C);
 cudaError_t tc_prepare(int rho, int C, const TCPlan& plan, const float* M, void* ws,
                        cudaStream_t s);
 // targets restricted to cells with x in [x_begin, x_end) (multiples of 4; x_end < 0 = res)
@@ -113,13 +99,11 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
 // transform into L; with `coarse` = L of the level above, the L2L is fused:
 // L = L2L(coarse) + M2L).  The two may run on different streams.
 enum { SEP_FRONT = 1, SEP_POST = 2, SEP_ALL = 3 };
-// far_only: the far table of a coarse level (parity box minus the hole, three
-// disjoint separable pieces; full grid only, 4 scratch buffers instead of 2)
-size_t m2l_sep_workspace_floats(int rho, int level, int C, bool far_only = false);
+size_t m2l_sep_workspace_floats(int rho, int level, int C);
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
                     const double* conv, const float* M, float* L, float* ws, int x_begin,
                     int x_end, cudaStream_t s, int stages = SEP_ALL,
-                    const float* coarse = nullptr, bool far_only = false);
+                    const float* coarse = nullptr);
 
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {

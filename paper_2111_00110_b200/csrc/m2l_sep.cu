@@ -40,7 +40,6 @@
 #include "kernels.cuh"
 #include "shift.cuh"
 
-#include <cstdlib>
 #include <cstring>
 
 namespace fc2t2 {
@@ -257,8 +256,7 @@ template <int RHO, int PASS, int POS, int NOUT>
 __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int ne, int lane,
                                            int nin, int in_base, int in_stride,
                                            const int (&oe)[RHO + 1], float* out,
-                                           int64_t pos_stride, int64_t plane, int nvalid,
-                                           bool accumulate) {
+                                           int64_t pos_stride, int64_t plane, int nvalid) {
   constexpr int OFF = PASS == PASS_X ? 4 : 3;
   constexpr int NQ = PASS == PASS_X ? POS + 8 : win_of(POS);
   float acc[POS][NOUT];
@@ -316,18 +314,10 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
     if (w < nvalid) {
 #pragma unroll
       for (int j = 0; j < NOUT; ++j) {
-        float* o = out + (int64_t)oe[j] * plane + w * pos_stride;
-        *o = accumulate ? *o + acc[w][j] : acc[w][j];
+        out[(int64_t)oe[j] * plane + w * pos_stride] = acc[w][j];
       }
     }
   }
-}
-
-__device__ __forceinline__ void cp_async16(float* smem, const float* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(valid ? 16 : 0)
-               : "memory");
 }
 
 // tile geometry decoded from a linear tile index
@@ -345,43 +335,9 @@ __device__ __forceinline__ Tile decode_tile(int64_t t, int R1, int res, int line
   return r;
 }
 
-template <int RHO, int PASS, int POS, int PART>
-__device__ __forceinline__ void load_part(float* sm, const float* src, int res, const Tile& T) {
-  using PT = Part<RHO, PASS, PART>;
-  if constexpr (PASS != PASS_X) {
-    constexpr int total = win_of(POS) * PT::NE * (kLines / 4);
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-      const int c4 = i & 7;
-      const int r = i >> 3;
-      const int le = r % PT::NE, q = r / PT::NE;
-      const int pos = T.pos0 - 3 + q;
-      const bool ok = pos >= 0 && pos < res;
-      const int64_t e = PT::entry(le);
-      // z pass: [e][y=fixed][z=pos][x]; y pass: [e][y=pos][z=fixed][x]
-      const int64_t g = PASS == PASS_Z ? ((e * res + T.fixed) * res + (ok ? pos : 0)) * res
-                                       : ((e * res + (ok ? pos : 0)) * res + T.fixed) * res;
-      cp_async16(sm + (le * win_of(POS) + q) * kLines + 4 * c4, src + g + T.line0 + 4 * c4, ok);
-    }
-  } else {
-    constexpr int NC = (POS + 8) / 4;
-    constexpr int total = PT::NE * kLines * NC;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-      const int c4 = i % NC;
-      const int r = i / NC;
-      const int lane = r & (kLines - 1), le = r >> 5;
-      const int x = T.pos0 - 4 + 4 * c4;
-      const bool ok = x >= 0 && x < res;
-      // [e][y=fixed][z=line][x]
-      const int64_t g =
-          (((int64_t)PT::entry(le) * res + T.fixed) * res + T.line0 + lane) * res + (ok ? x : 0);
-      cp_async16(sm + (le * kLines + lane) * 16 + 4 * (c4 ^ ((lane >> 1) & 3)), src + g, ok);
-    }
-  }
-}
-
 template <int RHO, int PASS, int POS>
 __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, float* dst, int res,
-                                             int pos_end, const Tile& T, bool accumulate) {
+                                             int pos_end, const Tile& T) {
   using I = SepIdx<RHO>;
   constexpr int R1 = RHO + 1;
   const int64_t plane = (int64_t)res * res * res;
@@ -432,7 +388,7 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
   case Q:                                                                                  \
     if constexpr (Q <= R1)                                                                 \
       group_body<RHO, PASS, POS, Q>(sm, Kt, ne, lane, nin, in_base, in_stride, oe, o,           \
-                               pos_stride, plane, nvalid, accumulate);                     \
+                                    pos_stride, plane, nvalid);                               \
     break;
   switch (nout) {
     FC2T2_SEP_N(1)
@@ -488,14 +444,12 @@ __device__ __forceinline__ uint32_t window_bytes(int part) {
 //   z pass: lines x, positions z, fixed y      (in M', out Z)
 //   y pass: lines x, positions y, fixed z      (in Z,  out Y)
 //   x pass: lines z, positions x, fixed y      (in Y,  out X)
-// The window comes from one TMA tensor copy issued by thread 0 (use_tma), or
-// from 16-byte cp.async copies by every thread.
+// The window comes from one TMA tensor copy issued by thread 0.
 template <int RHO, int PASS, int POS>
 __global__ void __launch_bounds__(32 * (RHO + 1))
-sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, int C,
-                int line_lo, int nlt, int pos_lo, int npt, int pos_end,
-                const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps,
-                int use_tma, int accumulate) {
+sep_pass_kernel(float* __restrict__ out, int res, int line_lo, int nlt, int pos_lo, int npt,
+                int pos_end, const __grid_constant__ SepParams<RHO> prm,
+                const __grid_constant__ SepMaps maps) {
   using I = SepIdx<RHO>;
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(
@@ -504,11 +458,10 @@ sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, 
   float* Kt = sm + pass_win_floats<RHO, PASS, POS>();
   uint64_t* bar = reinterpret_cast<uint64_t*>(Kt + 7 * 8 * R1);
   const int64_t plane = (int64_t)res * res * res;
-  const int in_entries = PASS == PASS_Z ? I::P : I::T;
   const int out_entries = PASS == PASS_X ? I::P : I::T;
   const Tile T = decode_tile(blockIdx.x, R1, res, line_lo, nlt, pos_lo, npt, POS);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
-  if (use_tma) {
+  {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -525,27 +478,13 @@ sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, 
       else
         tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(T.part, 0), T.ch * R1, bar_s);
     }
-  } else {
-    const float* src = in + (int64_t)T.ch * in_entries * plane;
-#define FC2T2_LOAD(Q) \
-  if constexpr (Q <= RHO) load_part<RHO, PASS, POS, Q>(sm, src, res, T)
-    switch (T.part) {
-      case 0: FC2T2_LOAD(0); break;
-      case 1: FC2T2_LOAD(1); break;
-      case 2: FC2T2_LOAD(2); break;
-      case 3: FC2T2_LOAD(3); break;
-      case 4: FC2T2_LOAD(4); break;
-      case 5: FC2T2_LOAD(5); break;
-      default: break;
-    }
-#undef FC2T2_LOAD
   }
   // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads)
   for (int t = threadIdx.x; t < 7 * 8 * R1; t += blockDim.x) {
     const int j = t & 7, d = (t >> 3) % 7, i = t / 56;
     Kt[t] = j < R1 ? prm.conv[d][j][i] : 0.f;
   }
-  if (use_tma) {
+  {
     __syncthreads();   // the barrier init is visible before anyone waits on it
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -553,12 +492,9 @@ sep_pass_kernel(const float* __restrict__ in, float* __restrict__ out, int res, 
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
         "@!p bra WAIT_%=;\n\t}\n" ::"r"(bar_s)
         : "memory");
-  } else {
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
   }
   __syncthreads();
-  compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T,
-                               accumulate != 0);
+  compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T);
 }
 
 template <int RHO>
@@ -585,14 +521,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
   }();
   return fn;
-}
-
-bool sep_use_tma() {
-  static const bool v = [] {
-    const char* e = std::getenv("FC2T2_SEP_NOTMA");
-    return !(e && e[0] == '1');
-  }();
-  return v && tmap_encoder() != nullptr;
 }
 
 // tensor maps of one pass over `base` (one per partition); false on failure
@@ -640,7 +568,7 @@ bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
 template <int RHO, int PASS, int POS>
 cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                             int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                            cudaStream_t s, int accumulate) {
+                            cudaStream_t s) {
   const int nlt = (line_hi - line_lo + kLines - 1) / kLines;
   const int npt = (pos_hi - pos_lo + POS - 1) / POS;
   const int64_t blocks = (int64_t)nlt * npt * res * (RHO + 1) * C;
@@ -652,38 +580,25 @@ cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int lin
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   SepMaps maps;
   std::memset(&maps, 0, sizeof(maps));
-  const int tma = sep_use_tma() && encode_maps<RHO, PASS, POS>(maps, in, res, C) ? 1 : 0;
+  if (!encode_maps<RHO, PASS, POS>(maps, in, res, C)) return cudaErrorNotSupported;
   FC2T2_LAUNCH(name, s,
                sep_pass_kernel<RHO, PASS, POS><<<(unsigned)blocks, 32 * (RHO + 1), smem, s>>>(
-                   in, out, res, C, line_lo, nlt, pos_lo, npt, pos_hi, prm, maps, tma, accumulate));
+                   out, res, line_lo, nlt, pos_lo, npt, pos_hi, prm, maps));
   return cudaGetLastError();
 }
 
 template <int RHO, int PASS>
 cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                         int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                        cudaStream_t s, int accumulate = 0) {
+                        cudaStream_t s) {
   return launch_pass_pos<RHO, PASS, 8>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
-                                       name, s, accumulate);
-}
-
-// the K(d) of an offset subset: F = {|d| >= 2}, N = {|d| <= 1}
-template <int RHO>
-SepParams<RHO> masked(const SepParams<RHO>& p, bool keep_far) {
-  SepParams<RHO> q = p;
-  for (int d = 0; d < 7; ++d) {
-    const bool far = d - 3 <= -2 || d - 3 >= 2;
-    if (far != keep_far)
-      for (int i = 0; i <= RHO; ++i)
-        for (int j = 0; j <= RHO; ++j) q.conv[d][i][j] = 0.f;
-  }
-  return q;
+                                       name, s);
 }
 
 template <int RHO>
 cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                         const double* conv, const float* M, float* L, float* wa, float* wb,
-                        int x_begin, int x_end, int stages, const float* coarse, bool far_only,
+                        int x_begin, int x_end, int stages, const float* coarse,
                         cudaStream_t s) {
   const int res = 1 << (level + 1);
   if (res % kLines) return cudaErrorInvalidValue;
@@ -693,35 +608,7 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
   const int xl = std::max(0, x_begin - 3) / kLines * kLines;
   const int xh = std::min(res, (x_end + 3 + kLines - 1) / kLines * kLines);
   cudaError_t err;
-  if ((stages & SEP_FRONT) && far_only) {
-    // far table of a coarse level: the parity box minus the hole {-1,0,1}^3
-    // as three disjoint separable pieces (no cancellation against the large
-    // hole terms): F x A x A + N x F x A + N x N x F over (x, y, z), F = far
-    // and N = near axis offsets, A = both -- z passes A and F, y passes
-    // A(Z_A), F(Z_A) + N(Z_F), x passes F(Y1) + N(Y23).  Full grid only.
-    const size_t tb = SepIdx<RHO>::T * (size_t)res * res * res * C;
-    float *b0 = wa, *b1 = wb, *b2 = wb + tb, *b3 = wb + 2 * tb;
-    const SepParams<RHO> pF = masked(prm, true), pN = masked(prm, false);
-    const int64_t n = (int64_t)res * res * res * C;
-    FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-                                       M, b0, res, C, 0, res, prm));
-    if ((err = cudaGetLastError()) != cudaSuccess) return err;
-    if ((err = launch_pass<RHO, PASS_Z>(b0, b1, res, C, 0, res, 0, res, prm, "m2l_sep_z", s)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_Z>(b0, b2, res, C, 0, res, 0, res, pF, "m2l_sep_z", s)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_Y>(b1, b0, res, C, 0, res, 0, res, prm, "m2l_sep_y", s)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_Y>(b1, b3, res, C, 0, res, 0, res, pF, "m2l_sep_y", s)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_Y>(b2, b3, res, C, 0, res, 0, res, pN, "m2l_sep_y", s, 1)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_X>(b0, b1, res, C, 0, res, 0, res, pF, "m2l_sep_x", s)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_X>(b3, b1, res, C, 0, res, 0, res, pN, "m2l_sep_x", s, 1)))
-      return err;
-    wb = b1;   // the post stage reads X from here
-  } else if (stages & SEP_FRONT) {
+  if (stages & SEP_FRONT) {
     const int64_t n = (int64_t)(xh - xl) * res * res * C;
     FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                                        M, wa, res, C, xl, xh - xl, prm));
@@ -749,24 +636,23 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
 
 }  // namespace
 
-size_t m2l_sep_workspace_floats(int rho, int level, int C, bool far_only) {
+size_t m2l_sep_workspace_floats(int rho, int level, int C) {
   const int64_t res = 1 << (level + 1);
   const int64_t R1 = rho + 1, T = R1 * (R1 + 1) / 2 * R1;
-  return (size_t)((far_only ? 4 : 2) * T * res * res * res * C);
+  return (size_t)(2 * T * res * res * res * C);
 }
 
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
                     const double* conv, const float* M, float* L, float* ws, int x_begin,
-                    int x_end, cudaStream_t s, int stages, const float* coarse, bool far_only) {
+                    int x_end, cudaStream_t s, int stages, const float* coarse) {
   const int64_t res = 1 << (level + 1);
   if (x_end < 0) x_end = (int)res;
-  if (far_only && (x_begin != 0 || x_end != res)) return cudaErrorInvalidValue;
   float* wa = ws;
-  float* wb = ws + m2l_sep_workspace_floats(rho, level, C, false) / 2;
+  float* wb = ws + m2l_sep_workspace_floats(rho, level, C) / 2;
 #define FC2T2_SEP_RHO(R)                                                                   \
   case R:                                                                                  \
     return m2l_sep_rho<R>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, stages, \
-                          coarse, far_only, s);
+                          coarse, s);
   switch (rho) {
     FC2T2_SEP_RHO(1)
     FC2T2_SEP_RHO(2)

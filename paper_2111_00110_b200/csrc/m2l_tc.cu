@@ -1,4 +1,4 @@
-// M2L on the 5th-generation tensor cores: tcgen05.mma kind::tf32, 3xTF32.
+// M2L on the 5th-generation tensor cores: tcgen05.mma kind::f16, two-term fp16 split.
 //
 // Reference: Engine.m2l (expansion.py:227-264).  For a target parity class pi
 // the level's interaction list is a GEMM
@@ -20,17 +20,15 @@
 //
 // Precision: both operands are split x = hi + lo so that D = Ahi Bhi +
 // (Ahi Blo + Alo Bhi) carries ~22 significant bits (3 products; Alo Blo is
-// below fp32 resolution).  Two element formats:
-//  * kind::f16 (default): fp16 hi = rn(x'), lo = rn((x' - hi) * 2^11) on
-//    power-of-two scaled operands -- moments A' = M / (g_c s_n) with static
-//    per-coefficient scales s_n = (h/2)^|n| / n! (|M_n| <= sum|w| s_n), a
-//    per-call per-channel power of two g_c (device abs-max, max|A'| <= 2^13),
-//    tables B' = B s_n / r_k with static per-output-column r_k.  The cross
-//    products are 2^11 too large and the output is L = g_c r_k (D_hh +
-//    2^-11 D_s).  An instruction takes K = 16 (tf32: 8) at the same cycle
-//    cost, so a K step covers twice the coefficients.
-//  * kind::tf32 (FC2T2_M2L_TF32=1): hi = rna_tf32(x), lo = rna_tf32(x - hi),
-//    unscaled (3xTF32).
+// below fp32 resolution): fp16 hi = rn(x'), lo = rn((x' - hi) * 2^11) on
+// power-of-two scaled operands -- moments A' = M / (g_c s_n) with static
+// per-coefficient scales s_n = (h/2)^|n| / n! (|M_n| <= sum|w| s_n), a
+// per-call per-channel power of two g_c (device abs-max, max|A'| <= 2^13),
+// tables B' = B s_n / r_k with static per-output-column r_k.  The cross
+// products are 2^11 too large and the output is L = g_c r_k (D_hh +
+// 2^-11 D_s).  A kind::f16 instruction takes K = 16 at the cycle cost of a
+// kind::tf32 K = 8, so a K step covers twice the coefficients (3xTF32 was
+// the first version of this kernel).
 // Tensor-core accumulation into TMEM truncates, so the large hi*hi products
 // of each source class sigma go to their own TMEM set (double buffered,
 // drained into fp32 registers with RN adds and re-zeroed), while the small
@@ -47,7 +45,6 @@
 // TILES 1 x 16 x 8 target tiles stacked along x share one
 // (TILES + 2) x 18 x 10 window.
 #include <cuda_fp16.h>
-#include <cstdlib>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -66,20 +63,17 @@ struct Tag {
   using type = T;
 };
 
-// TL > 0 overrides the tiles per CTA; CG = 2 runs CTA pairs (tcgen05
-// cta_group::2, M = 256: the leader issues for both SMs, each SM stages its own
-// window and half of the table rows).
-template <int RHO, bool H, int TL = 0, int CG = 1>
+// TL > 0 overrides the tiles per CTA.
+template <int RHO, int TL = 0>
 struct TC {
   static constexpr int RHO_ = RHO;
   static constexpr int TL_ = TL;
-  static constexpr int CG_ = CG;
   static constexpr int P = index_count(RHO);
   static constexpr int PP = pad4(P);
-  static constexpr int KI = H ? 16 : 8;                 // K per MMA instruction (32 B rows)
+  static constexpr int KI = 16;                         // K per MMA instruction (32 B rows)
   static constexpr int KPAD = (P + KI - 1) / KI * KI;   // K per offset
   static constexpr int KS = KPAD / KI;
-  static constexpr int ESZ = H ? 2 : 4;                 // bytes per operand element
+  static constexpr int ESZ = 2;                         // bytes per operand element (fp16)
   static constexpr int CLS = 4 * ((P + 7) / 8 * 8) <= 256 ? 2 : 1;   // target classes per CTA
   static constexpr int NC = CLS == 2 ? (P + 7) / 8 * 8 : (P + 15) / 16 * 16;  // N per class
   static constexpr int W = CLS * NC;                   // one TMEM set; cross MMA N
@@ -98,9 +92,8 @@ struct TC {
   static constexpr int WROWS = WX * WY * WZ;
   static constexpr int WSLICE = 2 * 2 * WROWS * 16;   // [part hi/lo][kchunk][row][16 B]
   static constexpr int SLOTS = 27, DPS = 9, CHUNKS = 3;
-  // table rows one CTA stages per slot: both halves of B (2W), or with CTA
-  // pairs its main-MMA half (W) + its cross-MMA half (W/2)
-  static constexpr int BROWS = CG == 2 ? 3 * W / 2 : 2 * W;
+  // table rows one CTA stages per slot: both halves of B
+  static constexpr int BROWS = 2 * W;
   static constexpr int BSLOT = 2 * BROWS * 16;        // [kchunk][row][16 B]
   static constexpr int BSTAGE = DPS * BSLOT;
   static constexpr int NS = 2 * WSLICE + 3 * BSTAGE + 1024 <= 232448 ? 3 : 2;
@@ -116,17 +109,15 @@ struct TC {
   // [0 | B_hi]: one main MMA yields all three products, no cross MMA.
   static constexpr bool MERGE_LAST = P - (KS - 1) * KI <= KI / 2;
   static constexpr size_t SMEM = 2 * (size_t)WSLICE + (size_t)NS * BSTAGE + 512;
-  // instruction descriptor: D f32; A/B tf32 (2) or f16 (0); K-major; N >> 3; M >> 4
+  // instruction descriptor: D f32; A/B f16 (0); K-major; N >> 3; M >> 4
   static constexpr uint32_t idesc(int n) {
-    return (1u << 4) | ((H ? 0u : 2u) << 7) | ((H ? 0u : 2u) << 10) |
-           ((uint32_t)(n >> 3) << 17) | ((uint32_t)((128 * CG) >> 4) << 24);
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   }
   static constexpr uint32_t IDESC_MAIN = idesc(2 * W);
   static constexpr uint32_t IDESC_CROSS = idesc(W);
   static_assert(2 * W <= 256 && W % 16 == 0, "MMA N out of range");
   static_assert(CW % 8 == 0 && (TILES == 1 || CW == W), "drain split");
   static_assert(TILES * TW <= 512, "TMEM");
-  static_assert(CG == 1 || (W / 2) % 8 == 0, "pair split of the cross operand");
 };
 
 constexpr float kLoScale = 2048.f;   // fp16 lo parts carry the residual * 2^11
@@ -172,111 +163,20 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-// shared::cluster address of the same smem offset in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cbar)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(
-                   cbar),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITC_%=;\n\t}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-template <bool H, int CG = 1>
 __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
-  if constexpr (CG == 2) {
-    if constexpr (H)
-      asm volatile("tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem),
-                   "l"(a), "l"(b), "r"(idesc));
-    else
-      asm volatile("tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem),
-                   "l"(a), "l"(b), "r"(idesc));
-    return;
-  }
-  if constexpr (H)
-    asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem),
-                 "l"(a), "l"(b), "r"(idesc));
-  else
-    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem),
-                 "l"(a), "l"(b), "r"(idesc));
+  asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n" ::"r"(d_tmem), "l"(a),
+               "l"(b), "r"(idesc));
 }
-template <int CG = 1>
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-  if constexpr (CG == 2)   // arrive on the barrier at this offset in both CTAs of the pair
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-        "[%0], %1;\n" ::"r"(bar),
-        "h"((uint16_t)3)
-        : "memory");
-  else
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
-        : "memory");
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-}
-
-__device__ __forceinline__ float rn_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// ------------------------------------------------------------ pre-split ---
-// (res^3, C, PP) fp32 grid -> per-channel hi / lo planes (C, res^3, KPAD),
-// zero-padded from P to KPAD.
-template <int RHO>
-__global__ void __launch_bounds__(256)
-split_tf32_kernel(const float* __restrict__ M, float4* __restrict__ hi, float4* __restrict__ lo,
-                  int64_t cells, int C) {
-  using Cfg = TC<RHO, false>;
-  constexpr int Q = Cfg::KPAD / 4;
-  const int64_t n = cells * C * Q;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(g % Q);
-    const int64_t cc = g / Q;  // (channel, cell) in output order
-    const int c = (int)(cc / cells);
-    const int64_t cell = cc - (int64_t)c * cells;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * q < Cfg::PP) v = *reinterpret_cast<const float4*>(M + (cell * C + c) * Cfg::PP + 4 * q);
-    float4 h, l;
-    h.x = rn_tf32(v.x); l.x = rn_tf32(v.x - h.x);
-    h.y = rn_tf32(v.y); l.y = rn_tf32(v.y - h.y);
-    h.z = rn_tf32(v.z); l.z = rn_tf32(v.z - h.z);
-    h.w = rn_tf32(v.w); l.w = rn_tf32(v.w - h.w);
-    hi[g] = h;
-    lo[g] = l;
-  }
 }
 
 // per-channel max over cells and n of |M[cell, c, n]| / s_n, as float bits
@@ -322,7 +222,7 @@ __global__ void __launch_bounds__(256)
 split_f16_kernel(const float* __restrict__ M, const float* __restrict__ s_inv,
                  const uint32_t* __restrict__ gbits, uint2* __restrict__ hi,
                  uint2* __restrict__ lo, int64_t cells, int C) {
-  using Cfg = TC<RHO, true>;
+  using Cfg = TC<RHO>;
   constexpr int Q = Cfg::KPAD / 4;
   const int64_t n = cells * C * Q;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n;
@@ -386,21 +286,21 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ------------------------------------------------------------ M2L (tc) ---
-template <int RHO, bool H, int TL, int CG>
+template <int RHO, int TL>
 __global__ void __launch_bounds__(512, 1)
 m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
               const uint8_t* __restrict__ Btab, const float* __restrict__ rk,
               const uint32_t* __restrict__ gbits, float* __restrict__ L, int res, int nu, int C,
-              int accumulate, int ux_begin, int merge_last, int diag) {
-  using T = TC<RHO, H, TL, CG>;
+              int accumulate, int ux_begin) {
+  using T = TC<RHO, TL>;
   constexpr int W = T::W, NS = T::NS, KS = T::KS, TILES = T::TILES, CW = T::CW;
   constexpr int WROWS = T::WROWS, WY = T::WY, WZ = T::WZ;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* win = smem;                                  // [2][WSLICE]
   uint8_t* bring = smem + 2 * T::WSLICE;                // [NS][BSTAGE]
   uint64_t* bars = reinterpret_cast<uint64_t*>(bring + NS * T::BSTAGE);
-  // bars: bfull[NS], bempty[NS], winready[2], winfree[2], accfull[2], accfree[2], bpeer[NS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 8);
+  // bars: bfull[NS], bempty[NS], winready[2], winfree[2], accfull[2], accfree[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 8);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cg = blockIdx.y;     // class group: classes cg*CLS .. cg*CLS + CLS-1
@@ -418,96 +318,56 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
   auto winfree = [&](int b) { return bar0 + 8u * (2 * NS + 2 + b); };
   auto accfull = [&](int b) { return bar0 + 8u * (2 * NS + 4 + b); };
   auto accfree = [&](int b) { return bar0 + 8u * (2 * NS + 6 + b); };
-  // CTA pairs: the peer's table stage landed (its bulk copies complete on its
-  // own bfull; its idle warp 0 forwards that to the leader's bpeer)
-  auto bpeer = [&](int s) { return bar0 + 8u * (2 * NS + 8 + s); };
-  // CTA pairs: data-ready / drain-done barriers live in the leader (rank 0);
-  // both CTAs arrive there (shared::cluster addresses).  Buffer-free and
-  // accumulator-full barriers exist in both CTAs and receive multicast commits.
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
-  auto lead = [&](uint32_t bar) { return CG == 2 ? mapa_rank(bar, 0) : bar; };
-  auto arrive_lead = [&](uint32_t bar) {
-    if constexpr (CG == 2) mbar_arrive_cluster(mapa_rank(bar, 0));
-    else mbar_arrive(bar);
-  };
-  auto wait_lead = [&](uint32_t bar, uint32_t parity) {
-    if constexpr (CG == 2) mbar_wait_cluster(bar, parity);
-    else mbar_wait(bar, parity);
-  };
-
   if (warp == T::DRAIN_WARP0) {
-    if constexpr (CG == 2) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                       smem_u32(tmem_slot)),
-                   "n"(T::TMEM_COLS));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                       smem_u32(tmem_slot)),
-                   "n"(T::TMEM_COLS));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
-    }
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(T::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(bfull(s), 1);
       mbar_init(bempty(s), 1);
-      mbar_init(bpeer(s), 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(winready(b), T::GATHER_THREADS * CG);
+      mbar_init(winready(b), T::GATHER_THREADS);
       mbar_init(winfree(b), 1);
       mbar_init(accfull(b), 1);
-      mbar_init(accfree(b), T::DRAIN_THREADS * CG);
+      mbar_init(accfree(b), T::DRAIN_THREADS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync_all();
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     // ---------------- MMA issuer: warp-uniform loop, elect-one per MMA ----------------
-    // (CTA pairs: the leader issues for both SMs; the peer's warp 0 forwards
-    // its table stages' arrival to the leader)
-    if (CG == 2 && rank != 0) {
-      if (lane == 0) {
-        const int stages = 8 * KS * T::CHUNKS;
-        for (int n = 0; n < stages; ++n) {
-          const int s = n % NS;
-          mbar_wait(bfull(s), (n / NS) & 1);
-          mbar_arrive_cluster(mapa_rank(bpeer(s), 0));
-        }
-      }
-    } else {
     const uint32_t wb0 = smem_u32(win), bb0 = smem_u32(bring);
     int n = 0, q = 0;
     for (int sg = 0; sg < 8; ++sg) {
       const int set = T::SB ? 0 : (sg & 1);
-      wait_lead(accfree(set), (sg / T::NSETS) & 1);
+      mbar_wait(accfree(set), (sg / T::NSETS) & 1);
       tc_fence_after();
       // main D: [hh1 | s] (odd) or [s | hh0] (even); single buffered: [s | hh]
       const uint32_t mcol = (T::SB || set) ? 0u : (uint32_t)W;
-      // B_hi rows: second half for even sigma and always when single buffered;
-      // CTA pairs keep their cross half right after their main half
-      const uint64_t xoff = (CG == 2 || T::SB || !set) ? (uint64_t)W : 0u;
+      // B_hi rows: second half for even sigma and always when single buffered
+      const uint64_t xoff = (T::SB || !set) ? (uint64_t)W : 0u;
       const uint32_t scol = T::SB ? 0u : (uint32_t)W;   // small-term set
       for (int ks = 0; ks < KS; ++ks, ++q) {
         const int buf = q & 1;
-        wait_lead(winready(buf), (q >> 1) & 1);
+        mbar_wait(winready(buf), (q >> 1) & 1);
         tc_fence_after();
         const uint64_t ahi = sdesc(wb0 + buf * T::WSLICE, WROWS * 16, WZ * 16);
         const uint64_t alo = ahi + (uint64_t)(2 * WROWS);
-        const bool merged = T::MERGE_LAST && merge_last && ks == KS - 1;
+        const bool merged = T::MERGE_LAST && ks == KS - 1;
         // merged last step: K chunk 1 = the lo part's chunk 0, 2 WROWS rows on
         const uint64_t amain = merged ? sdesc(wb0 + buf * T::WSLICE, 2 * WROWS * 16, WZ * 16) : ahi;
 #pragma unroll
         for (int ch = 0; ch < T::CHUNKS; ++ch, ++n) {
           const int s = n % NS;
           mbar_wait(bfull(s), (n / NS) & 1);
-          if constexpr (CG == 2) mbar_wait_cluster(bpeer(s), (n / NS) & 1);
           tc_fence_after();
           const uint64_t b0 = sdesc(bb0 + s * T::BSTAGE, T::BROWS * 16, 128);
 #pragma unroll
@@ -519,39 +379,34 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
             for (int t = 0; t < TILES; ++t) {
               const uint64_t arow = ex + (uint64_t)(t * WY * WZ);
               const uint32_t dt = tmem + (uint32_t)(t * T::TW);
-              if (diag & 2) continue;
-              if (elect_one()) umma<H, CG>(dt + mcol, amain + arow, bd, T::IDESC_MAIN);
-              if (!merged && elect_one())
-                umma<H, CG>(dt + scol, alo + arow, bd + xoff, T::IDESC_CROSS);
+              if (elect_one()) umma(dt + mcol, amain + arow, bd, T::IDESC_MAIN);
+              if (!merged && elect_one()) umma(dt + scol, alo + arow, bd + xoff, T::IDESC_CROSS);
             }
           }
-          if (elect_one()) umma_commit<CG>(bempty(s));
+          if (elect_one()) umma_commit(bempty(s));
           __syncwarp();
         }
-        if (elect_one()) umma_commit<CG>(winfree(buf));
+        if (elect_one()) umma_commit(winfree(buf));
         __syncwarp();
       }
-      if (elect_one()) umma_commit<CG>(accfull(set));
+      if (elect_one()) umma_commit(accfull(set));
       __syncwarp();
-    }
     }
   } else if (warp == 1) {
     // ---------------- B producer: one bulk copy per 9-slot stage ----------------
     if (lane == 0) {
-      // table layout [cg][sigma][ks][pair rank][slot][BSLOT]
-      const uint8_t* tb = Btab + (size_t)cg * 8 * KS * CG * T::SLOTS * T::BSLOT;
+      // table layout [cg][sigma][ks][slot][BSLOT]
+      const uint8_t* tb = Btab + (size_t)cg * 8 * KS * T::SLOTS * T::BSLOT;
       int n = 0;
       for (int sg = 0; sg < 8; ++sg)
         for (int ks = 0; ks < KS; ++ks)
           for (int ch = 0; ch < T::CHUNKS; ++ch, ++n) {
             const int s = n % NS;
             if (n >= NS) mbar_wait(bempty(s), ((n / NS) - 1) & 1);
-            if (diag & 1) { mbar_arrive(bfull(s)); continue; }
             mbar_expect_tx(bfull(s), T::BSTAGE);
             bulk_g2s(smem_u32(bring + s * T::BSTAGE),
-                     tb + ((((size_t)sg * KS + ks) * CG + rank) * T::SLOTS + ch * T::DPS) *
-                              T::BSLOT,
-                     T::BSTAGE, bfull(s));
+                     tb + (((size_t)sg * KS + ks) * T::SLOTS + ch * T::DPS) * T::BSLOT, T::BSTAGE,
+                     bfull(s));
           }
     }
   } else if (warp < T::DRAIN_WARP0) {
@@ -567,7 +422,7 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
         const int buf = q & 1;
         if (q >= 2) mbar_wait(winfree(buf), ((q - 2) >> 1) & 1);
         uint8_t* wb = win + buf * T::WSLICE;
-        for (int r = gt; r < ((diag & 1) ? 0 : WROWS); r += T::GATHER_THREADS) {
+        for (int r = gt; r < WROWS; r += T::GATHER_THREADS) {
           const int wx = r / (WY * WZ), wy = (r / WZ) % WY, wz = r % WZ;
           const int cx = 2 * (ux0 - 1 + wx) + sx;
           const int cy = 2 * (uy0 - 1 + wy) + sy;
@@ -587,7 +442,7 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        arrive_lead(winready(buf));
+        mbar_arrive(winready(buf));
       }
     }
   } else {
@@ -601,14 +456,14 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
       for (int c = 0; c < CW; c += 8) tmem_zero8(tb + o * W + c);
     tmem_wait_st();
     tc_fence_before();
-    arrive_lead(accfree(0));
-    arrive_lead(accfree(1));
+    mbar_arrive(accfree(0));
+    mbar_arrive(accfree(1));
     float acc[CW];
 #pragma unroll
     for (int c = 0; c < CW; ++c) acc[c] = 0.f;
     for (int sg = 0; sg < 8; ++sg) {
       const int set = T::SB ? 0 : (sg & 1);
-      mbar_wait(accfull(set), (sg / T::NSETS) & 1);   // local (multicast commit)
+      mbar_wait(accfull(set), (sg / T::NSETS) & 1);
       tc_fence_after();
       const uint32_t hb = tb + (T::SB ? (uint32_t)W : (set ? 0u : (uint32_t)(2 * W)));
 #pragma unroll
@@ -621,10 +476,10 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
       }
       tmem_wait_st();
       tc_fence_before();
-      arrive_lead(accfree(set));
+      mbar_arrive(accfree(set));
     }
     // the small-term set is complete once the last group's commit has fired
-    const float sfac = H ? 1.f / kLoScale : 1.f;
+    const float sfac = 1.f / kLoScale;
 #pragma unroll
     for (int c = 0; c < CW; c += 8) {
       float v[8];
@@ -632,7 +487,7 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[c + i] += v[i] * sfac;
     }
-    if constexpr (H) {
+    {
       // undo the operand scaling: L = g_c r_k (D_hh + 2^-11 D_s)
       const float g = ldexpf(1.f, gexp_of(gbits[chan]) - kGExp);
 #pragma unroll
@@ -658,31 +513,15 @@ m2l_tc_kernel(const uint8_t* __restrict__ Mhi, const uint8_t* __restrict__ Mlo,
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2) {
-    cluster_sync_all();   // the leader's MMAs read the peer's smem and signal its barriers
-    if (warp == T::DRAIN_WARP0)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                   "n"(T::TMEM_COLS));
-  } else {
-    __syncthreads();
-    if (warp == T::DRAIN_WARP0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                   "n"(T::TMEM_COLS));
-  }
+  __syncthreads();
+  if (warp == T::DRAIN_WARP0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "n"(T::TMEM_COLS));
 }
 
 }  // namespace
 
-int tc_diag() {
-  static const int d = [] {
-    const char* v = getenv("FC2T2_TC_DIAG");
-    return v ? atoi(v) : 0;
-  }();
-  return d;
-}
-
-int tc_geometry(int rho, int f16, int cg, int* cls, int* nc, int* ks, int* bslot, int* sb,
-                int* tiles) {
+int tc_geometry(int rho, int* cls, int* nc, int* ks, int* bslot, int* sb, int* tiles) {
   FC2T2_DISPATCH_RHO(rho, {
     auto fill = [&](auto tag) {
       using T = typename decltype(tag)::type;
@@ -693,19 +532,13 @@ int tc_geometry(int rho, int f16, int cg, int* cls, int* nc, int* ks, int* bslot
       *sb = (T::SB ? 1 : 0) | (T::MERGE_LAST ? 2 : 0);
       *tiles = T::TILES;
     };
-    if (f16) {
-      if (cg == 2) fill(Tag<TC<RHO, true, 0, 2>>{});
-      else fill(Tag<TC<RHO, true>>{});
-    } else {
-      if (cg == 2) fill(Tag<TC<RHO, false, 0, 2>>{});
-      else fill(Tag<TC<RHO, false>>{});
-    }
+    fill(Tag<TC<RHO>>{});
     return 0;
   });
   return -1;
 }
 
-double tc_issued_flops(int rho, int level, int C, int f16, int merge_last) {
+double tc_issued_flops(int rho, int level, int C) {
   const int nu = (1 << (level + 1)) / 2;
   FC2T2_DISPATCH_RHO(rho, {
     auto count = [&](auto tag) -> double {
@@ -715,11 +548,11 @@ double tc_issued_flops(int rho, int level, int C, int f16, int merge_last) {
       if (T::TILES == 2 && ctas2 < 148) tiles = 1;   // m2l_tc's small-grid variant
       const double tile_slots = (double)nu * (nu / T::TY) * (nu / T::TZ) * (8 / T::CLS) * C * 8 * 27;
       (void)tiles;
-      const int cross_steps = (T::MERGE_LAST && merge_last) ? T::KS - 1 : T::KS;
+      const int cross_steps = T::MERGE_LAST ? T::KS - 1 : T::KS;
       const double k = T::KI, m = 128;
       return tile_slots * (T::KS * 2.0 * m * (2 * T::W) * k + cross_steps * 2.0 * m * T::W * k);
     };
-    return f16 ? count(Tag<TC<RHO, true>>{}) : count(Tag<TC<RHO, false>>{});
+    return count(Tag<TC<RHO>>{});
   });
   return 0.0;
 }
@@ -741,19 +574,16 @@ int tc_moment_scales(int rho, int level, double* s) {
 }
 
 namespace {
-template <int RHO, bool H>
+template <int RHO>
 size_t plane_bytes(int level, int C) {
   const size_t res = (size_t)1 << (level + 1);
-  return res * res * res * (size_t)C * TC<RHO, H>::KPAD * TC<RHO, H>::ESZ;
+  return res * res * res * (size_t)C * TC<RHO>::KPAD * TC<RHO>::ESZ;
 }
 size_t gbits_bytes(int C) { return ((size_t)C * 4 + 255) / 256 * 256; }
 }  // namespace
 
-size_t tc_workspace_bytes(int rho, int level, int C, int f16) {
-  FC2T2_DISPATCH_RHO(rho, {
-    const size_t pb = f16 ? plane_bytes<RHO, true>(level, C) : plane_bytes<RHO, false>(level, C);
-    return gbits_bytes(C) + 2 * pb;
-  });
+size_t tc_workspace_bytes(int rho, int level, int C) {
+  FC2T2_DISPATCH_RHO(rho, return gbits_bytes(C) + 2 * plane_bytes<RHO>(level, C));
   return 0;
 }
 
@@ -764,10 +594,10 @@ cudaError_t tc_prepare(int rho, int C, const TCPlan& plan, const float* M, void*
   uint8_t* w = (uint8_t*)ws;
   uint32_t* gbits = (uint32_t*)w;
   FC2T2_DISPATCH_RHO(rho, {
-    if (plan.f16) {
-      using T = TC<RHO, true>;
+    {
+      using T = TC<RHO>;
       uint8_t* hi = w + gbits_bytes(C);
-      uint8_t* lo = hi + plane_bytes<RHO, true>(plan.level, C);
+      uint8_t* lo = hi + plane_bytes<RHO>(plan.level, C);
       cudaError_t e = cudaMemsetAsync(gbits, 0, (size_t)C * 4, s);
       if (e != cudaSuccess) return e;
       const int64_t n4 = cells * (T::PP / 4);
@@ -777,13 +607,6 @@ cudaError_t tc_prepare(int rho, int C, const TCPlan& plan, const float* M, void*
       const int64_t n = cells * C * (T::KPAD / 4);
       FC2T2_LAUNCH("m2l_split", s, split_f16_kernel<RHO><<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(
                                        M, plan.s_inv, gbits, (uint2*)hi, (uint2*)lo, cells, C));
-    } else {
-      using T = TC<RHO, false>;
-      uint8_t* hi = w + gbits_bytes(C);
-      uint8_t* lo = hi + plane_bytes<RHO, false>(plan.level, C);
-      const int64_t n = cells * C * (T::KPAD / 4);
-      FC2T2_LAUNCH("m2l_split", s, split_tf32_kernel<RHO><<<grid_blocks(n, 256, 148 * 16), 256, 0, s>>>(
-                                       M, (float4*)hi, (float4*)lo, cells, C));
     }
   });
   return cudaGetLastError();
@@ -803,47 +626,20 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
   const uint32_t* gbits = (const uint32_t*)w;
   auto launch = [&](auto tag) -> cudaError_t {
     using T = typename decltype(tag)::type;
-    constexpr bool H = T::ESZ == 2;
-    auto kern = m2l_tc_kernel<T::RHO_, H, T::TL_, T::CG_>;
+    auto kern = m2l_tc_kernel<T::RHO_, T::TL_>;
     static unsigned long long attr = 0;   // devices configured (per instantiation)
     if (attr_needed(attr)) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)T::SMEM);
       if (e != cudaSuccess) return e;
-      if constexpr (T::CG_ == 2) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-        if (e != cudaSuccess) return e;
-      }
     }
     const uint8_t* hi = w + gbits_bytes(C);
-    const uint8_t* lo = hi + plane_bytes<T::RHO_, H>(plan.level, C);
+    const uint8_t* lo = hi + plane_bytes<T::RHO_>(plan.level, C);
     dim3 grid((unsigned)((ux_count / T::TILES) * (nu / T::TY) * (nu / T::TZ)),
               (unsigned)(8 / T::CLS), (unsigned)C);
-    if constexpr (T::CG_ == 2) {
-      if (grid.x % 2) return cudaErrorInvalidValue;
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = grid;
-      cfg.blockDim = dim3(T::THREADS);
-      cfg.dynamicSmemBytes = T::SMEM;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 2;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      cudaError_t e = cudaSuccess;
-      FC2T2_LAUNCH(plan.level_name, s,
-                   e = cudaLaunchKernelEx(&cfg, kern, hi, lo, plan.btab, plan.rk, gbits, L, res,
-                                          nu, C, accumulate, ux_begin, plan.merge_last ? 1 : 0, tc_diag()));
-      if (e != cudaSuccess) return e;
-    } else {
-      FC2T2_LAUNCH(plan.level_name, s,
-                   kern<<<grid, T::THREADS, T::SMEM, s>>>(hi, lo, plan.btab, plan.rk, gbits, L,
-                                                          res, nu, C, accumulate, ux_begin,
-                                                          plan.merge_last ? 1 : 0, tc_diag()));
-    }
+    FC2T2_LAUNCH(plan.level_name, s,
+                 kern<<<grid, T::THREADS, T::SMEM, s>>>(hi, lo, plan.btab, plan.rk, gbits, L, res,
+                                                        nu, C, accumulate, ux_begin));
     return cudaGetLastError();
   };
   // grids that cannot fill the machine with two-tile CTAs (small levels, thin
@@ -853,16 +649,8 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
     return (int64_t)(ux_count / T::TILES) * (nu / T::TY) * (nu / T::TZ) * (8 / T::CLS) * C;
   };
   FC2T2_DISPATCH_RHO(rho, {
-    if (plan.f16) {
-      if (plan.cg == 2) return launch(Tag<TC<RHO, true, 0, 2>>{});
-      if (TC<RHO, true>::TILES == 2 && ctas(Tag<TC<RHO, true>>{}) < 148)
-        return launch(Tag<TC<RHO, true, 1>>{});
-      return launch(Tag<TC<RHO, true>>{});
-    }
-    if (plan.cg == 2) return launch(Tag<TC<RHO, false, 0, 2>>{});
-    if (TC<RHO, false>::TILES == 2 && ctas(Tag<TC<RHO, false>>{}) < 148)
-      return launch(Tag<TC<RHO, false, 1>>{});
-    return launch(Tag<TC<RHO, false>>{});
+    if (TC<RHO>::TILES == 2 && ctas(Tag<TC<RHO>>{}) < 148) return launch(Tag<TC<RHO, 1>>{});
+    return launch(Tag<TC<RHO>>{});
   });
   return cudaGetLastError();
 }

@@ -13,7 +13,6 @@
 //      a shared-memory block sort up to 8192, a block merge sort beyond).
 // Step 4 makes the result independent of the atomics' interleaving, i.e.
 // identical to a stable sort.  No float atomics anywhere: P2M is deterministic.
-#include <type_traits>
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -129,36 +128,16 @@ namespace {
 
 // nocell_rank (key sorts only): stable ranks of the key-R items, an exclusive
 // scan of their flags, so the no-cell bucket needs no segment sort
-// pts / pts_arr (cell sorts that also want the coordinates in sorted order):
-// pts_arr[slot] = pts[i] at the arrival slot, written here where point i is
-// read coalesced; the segment sort later reorders within each cell's range.
 __global__ void place_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ranks,
                              int64_t n, int64_t R, const uint32_t* __restrict__ start,
                              const uint32_t* __restrict__ nocell_rank,
-                             uint32_t* __restrict__ order, const float* __restrict__ pts,
-                             float* __restrict__ pts_arr) {
+                             uint32_t* __restrict__ order) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = keys[i];
     const uint32_t r = (nocell_rank && (int64_t)k == R) ? nocell_rank[i] : ranks[i];
     const uint32_t slot = start[k] + r;
     order[slot] = (uint32_t)i;
-    if (pts_arr) {
-      pts_arr[3 * (int64_t)slot] = pts[3 * i];
-      pts_arr[3 * (int64_t)slot + 1] = pts[3 * i + 1];
-      pts_arr[3 * (int64_t)slot + 2] = pts[3 * i + 2];
-    }
-  }
-}
-
-// dst[inv[i], :] = src[i, :] for rows of `cols` floats
-__global__ void permute_rows_kernel(const float* __restrict__ src, int64_t n, int cols,
-                                    const int32_t* __restrict__ inv, float* __restrict__ dst) {
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n * cols;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = g / cols;
-    const int c = (int)(g - i * cols);
-    dst[(int64_t)inv[i] * cols + c] = src[g];
   }
 }
 
@@ -211,64 +190,37 @@ __device__ __forceinline__ void warp_bitonic(T (&v)[K], int lane) {
   }
 }
 
-// Sorts one segment of `order` by index.  With pts_arr, the (index, arrival
-// slot) pairs are sorted as 64-bit keys so the coordinates follow:
-// pts_sorted[b + t] = pts_arr[b + slot], inv[index] = b + t.
-template <int K, bool PTS>
-__device__ __forceinline__ void warp_sort_segment(uint32_t* order, int64_t b, int size, int lane,
-                                                  const float* __restrict__ pts_arr,
-                                                  float* __restrict__ pts_sorted,
-                                                  int32_t* __restrict__ inv) {
-  using T = typename std::conditional<PTS, unsigned long long, uint32_t>::type;
-  T v[K];
+// Sorts one segment of `order` by index (32 * K >= size).
+template <int K>
+__device__ __forceinline__ void warp_sort_segment(uint32_t* order, int64_t b, int size, int lane) {
+  uint32_t v[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int e = j * 32 + lane;
-    if (PTS)
-      v[j] = e < size ? ((T)order[b + e] << 32) | (T)e : ~(T)0;
-    else
-      v[j] = e < size ? (T)order[b + e] : ~(T)0;
+    v[j] = e < size ? order[b + e] : 0xffffffffu;
   }
-  warp_bitonic<K, T>(v, lane);
+  warp_bitonic<K, uint32_t>(v, lane);
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     const int e = j * 32 + lane;
-    if (e >= size) continue;
-    if (PTS) {
-      const uint32_t idx = (uint32_t)(v[j] >> 32), slot = (uint32_t)(v[j] & 0xffffffffu);
-      order[b + e] = idx;
-      const int64_t src = 3 * (b + slot), dst = 3 * (b + e);
-      const float x = pts_arr[src], y = pts_arr[src + 1], z = pts_arr[src + 2];
-      pts_sorted[dst] = x;
-      pts_sorted[dst + 1] = y;
-      pts_sorted[dst + 2] = z;
-      inv[idx] = (int32_t)(b + e);
-    } else {
-      order[b + e] = (uint32_t)v[j];
-    }
+    if (e < size) order[b + e] = v[j];
   }
 }
 
-template <bool PTS>
-__device__ __forceinline__ void warp_sort_any(uint32_t* order, int64_t b, int size, int lane,
-                                              const float* pts_arr, float* pts_sorted,
-                                              int32_t* inv) {
-  if (size <= 32) warp_sort_segment<1, PTS>(order, b, size, lane, pts_arr, pts_sorted, inv);
-  else if (size <= 64) warp_sort_segment<2, PTS>(order, b, size, lane, pts_arr, pts_sorted, inv);
-  else if (size <= 128) warp_sort_segment<4, PTS>(order, b, size, lane, pts_arr, pts_sorted, inv);
-  else if (size <= 256) warp_sort_segment<8, PTS>(order, b, size, lane, pts_arr, pts_sorted, inv);
-  else if (size <= 512) warp_sort_segment<16, PTS>(order, b, size, lane, pts_arr, pts_sorted, inv);
-  else warp_sort_segment<32, PTS>(order, b, size, lane, pts_arr, pts_sorted, inv);
+__device__ __forceinline__ void warp_sort_any(uint32_t* order, int64_t b, int size, int lane) {
+  if (size <= 32) warp_sort_segment<1>(order, b, size, lane);
+  else if (size <= 64) warp_sort_segment<2>(order, b, size, lane);
+  else if (size <= 128) warp_sort_segment<4>(order, b, size, lane);
+  else if (size <= 256) warp_sort_segment<8>(order, b, size, lane);
+  else if (size <= 512) warp_sort_segment<16>(order, b, size, lane);
+  else warp_sort_segment<32>(order, b, size, lane);
 }
 
 // segment c = [start[c], c < R ? start[c+1] : n); one warp per segment,
 // segments above WARP_SEG_MAX go to the block worklist
-template <bool PTS>
 __global__ void __launch_bounds__(256)
 segment_sort_warp_kernel(uint32_t* __restrict__ order, const uint32_t* __restrict__ start,
-                         int64_t nseg, int64_t R, int64_t n, uint32_t* __restrict__ work,
-                         const float* __restrict__ pts_arr, float* __restrict__ pts_sorted,
-                         int32_t* __restrict__ inv) {
+                         int64_t nseg, int64_t R, int64_t n, uint32_t* __restrict__ work) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < nseg;
@@ -276,12 +228,12 @@ segment_sort_warp_kernel(uint32_t* __restrict__ order, const uint32_t* __restric
     const int64_t b = start[c];
     const int64_t e = c < R ? (int64_t)start[c + 1] : n;
     const int64_t size = e - b;
-    if (size <= 0 || (!PTS && size == 1)) continue;
+    if (size <= 1) continue;
     if (size > WARP_SEG_MAX) {
       if (lane == 0) work[1 + atomicAdd(work, 1u)] = (uint32_t)c;
       continue;
     }
-    warp_sort_any<PTS>(order, b, (int)size, lane, pts_arr, pts_sorted, inv);
+    warp_sort_any(order, b, (int)size, lane);
   }
 }
 
@@ -329,8 +281,7 @@ __device__ __forceinline__ int64_t merge_path(const uint32_t* a, int64_t na, con
 __global__ void __launch_bounds__(SEG_BLOCK)
 segment_sort_block_kernel(uint32_t* __restrict__ order, uint32_t* __restrict__ tmp,
                           const uint32_t* __restrict__ start, int64_t R, int64_t n,
-                          const uint32_t* __restrict__ work, const float* __restrict__ pts,
-                          float* __restrict__ pts_sorted, int32_t* __restrict__ inv) {
+                          const uint32_t* __restrict__ work) {
   extern __shared__ uint32_t sm[];
   const uint32_t count = work[0];
   for (uint32_t w = blockIdx.x; w < count; w += gridDim.x) {
@@ -365,15 +316,6 @@ segment_sort_block_kernel(uint32_t* __restrict__ order, uint32_t* __restrict__ t
     if (src != order + b)
       for (int64_t i = threadIdx.x; i < size; i += blockDim.x) order[b + i] = src[i];
     __syncthreads();
-    if (pts_sorted)  // rare large cells: gather the coordinates directly
-      for (int64_t t = threadIdx.x; t < size; t += blockDim.x) {
-        const int64_t i = order[b + t];
-        pts_sorted[3 * (b + t)] = pts[3 * i];
-        pts_sorted[3 * (b + t) + 1] = pts[3 * i + 1];
-        pts_sorted[3 * (b + t) + 2] = pts[3 * i + 2];
-        inv[i] = (int32_t)(b + t);
-      }
-    __syncthreads();
   }
 }
 
@@ -389,7 +331,7 @@ SortWs carve(void* ws, int64_t n, int64_t R) {
   SortWs w;
   w.keys = take(4 * (size_t)n);
   w.ranks = take(4 * (size_t)n);
-  w.tmp = take(12 * (size_t)n);   // key-sort flags / arrival-order coordinates
+  w.tmp = take(4 * (size_t)n);    // key-sort flags
   w.counts = take(4 * (size_t)(R + 1));
   w.scan = take(4 * std::max(scan_ws_words(R + 1), scan_ws_words(n)) + 4);
   w.work = take(4 * (size_t)(R + 2));
@@ -397,7 +339,7 @@ SortWs carve(void* ws, int64_t n, int64_t R) {
 }
 
 size_t ws_bytes(int64_t n, int64_t R) {
-  return 2 * align256(4 * (size_t)n) + align256(12 * (size_t)n) + align256(4 * (size_t)(R + 1)) +
+  return 3 * align256(4 * (size_t)n) + align256(4 * (size_t)(R + 1)) +
          align256(4 * std::max(scan_ws_words(R + 1), scan_ws_words(n)) + 4) +
          align256(4 * (size_t)(R + 2));
 }
@@ -405,12 +347,7 @@ size_t ws_bytes(int64_t n, int64_t R) {
 // keys/ranks/counts prepared: cell ranges, placement, per-cell index sort.
 // nocell: key sorts, whose bucket R is ranked stably by a scan of w.tmp flags.
 cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t* cell_start,
-                        bool nocell, cudaStream_t s, const float* pts = nullptr,
-                        int32_t* inv = nullptr, float* pts_sorted = nullptr,
-                        bool stable = true) {
-  // pts_sorted needs inv and a scratch copy in arrival order (w.tmp: n x 3 floats)
-  const bool with_pts = pts && pts_sorted && inv;
-  float* pts_arr = with_pts ? (float*)w.tmp : nullptr;
+                        bool nocell, cudaStream_t s) {
   cudaError_t e = exclusive_scan(w.counts, (uint32_t*)cell_start, R + 1, w.scan, s);
   if (e != cudaSuccess || n == 0) return e != cudaSuccess ? e : cudaGetLastError();
   if (nocell) {
@@ -421,21 +358,13 @@ cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t
   FC2T2_LAUNCH("sort_place", s,
                place_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(
                    w.keys, w.ranks, n, R, (const uint32_t*)cell_start, nocell ? w.tmp : nullptr,
-                   ord, pts, pts_arr));
-  if (!stable && !with_pts) return cudaGetLastError();
+                   ord));
   e = cudaMemsetAsync(w.work, 0, 4, s);
   if (e != cudaSuccess) return e;
   const int64_t nseg = nocell ? R : R + 1;
-  if (with_pts)
-    FC2T2_LAUNCH("sort_segments", s,
-                 segment_sort_warp_kernel<true><<<grid_blocks(nseg * 32, 256), 256, 0, s>>>(
-                     ord, (const uint32_t*)cell_start, nseg, R, n, w.work, pts_arr, pts_sorted,
-                     inv));
-  else
-    FC2T2_LAUNCH("sort_segments", s,
-                 segment_sort_warp_kernel<false><<<grid_blocks(nseg * 32, 256), 256, 0, s>>>(
-                     ord, (const uint32_t*)cell_start, nseg, R, n, w.work, nullptr, nullptr,
-                     nullptr));
+  FC2T2_LAUNCH("sort_segments", s,
+               segment_sort_warp_kernel<<<grid_blocks(nseg * 32, 256), 256, 0, s>>>(
+                   ord, (const uint32_t*)cell_start, nseg, R, n, w.work));
   static unsigned long long attr = 0;   // devices configured
   if (attr_needed(attr)) {
     e = cudaFuncSetAttribute(segment_sort_block_kernel,
@@ -444,8 +373,7 @@ cudaError_t sort_ranked(SortWs& w, int64_t n, int64_t R, int32_t* order, int32_t
   }
   FC2T2_LAUNCH("sort_segments", s,
                segment_sort_block_kernel<<<148, SEG_BLOCK, BLOCK_SEG_MAX * 4, s>>>(
-                   ord, w.ranks, (const uint32_t*)cell_start, R, n, w.work, pts,
-                   with_pts ? pts_sorted : nullptr, inv));
+                   ord, w.ranks, (const uint32_t*)cell_start, R, n, w.work));
   return cudaGetLastError();
 }
 
@@ -457,9 +385,7 @@ size_t cell_sort_workspace(int level, int64_t n) {
 }
 
 cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, int32_t* cell_start,
-                      int32_t* flag, void* ws, size_t ws_bytes_, cudaStream_t s, int32_t* inv,
-                      float* pts_sorted, bool stable) {
-  if ((inv == nullptr) != (pts_sorted == nullptr)) return cudaErrorInvalidValue;
+                      int32_t* flag, void* ws, size_t ws_bytes_, cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int64_t R = (int64_t)res * res * res;
   if (ws_bytes_ < cell_sort_workspace(level, n)) return cudaErrorInvalidValue;
@@ -470,16 +396,7 @@ cudaError_t cell_sort(int level, const float* pts, int64_t n, int32_t* order, in
     FC2T2_LAUNCH("cell_keys", s,
                  cell_keys_kernel<<<grid_blocks(n, 256), 256, 0, s>>>(pts, n, res, w.keys, w.ranks,
                                                                       w.counts, flag));
-  return sort_ranked(w, n, R, order, cell_start, false, s, pts, inv, pts_sorted, stable);
-}
-
-cudaError_t permute_rows(const float* src, int64_t n, int cols, const int32_t* inv, float* dst,
-                         cudaStream_t s) {
-  if (n <= 0 || cols <= 0) return cudaSuccess;
-  FC2T2_LAUNCH("permute_rows", s,
-               permute_rows_kernel<<<grid_blocks(n * cols, 256), 256, 0, s>>>(src, n, cols, inv,
-                                                                             dst));
-  return cudaGetLastError();
+  return sort_ranked(w, n, R, order, cell_start, false, s);
 }
 
 size_t key_sort_workspace(int level, int64_t n) { return cell_sort_workspace(level, n); }

@@ -239,22 +239,26 @@ def load_image(path: str) -> np.ndarray:
     if str(path).endswith(".png"):
         import matplotlib.image
         return np.asarray(matplotlib.image.imread(path), dtype=np.float64)[:, :, :3]
-    with open(path, "rb") as f:
-        if f.read(2) != b"P6":
-            raise FormatError(f"{path}: not a P6 PPM")
-        fields: list[int] = []
-        while len(fields) < 3:
-            line = f.readline()
-            if not line:
-                raise FormatError(f"{path}: truncated header")
-            fields += [int(tok) for tok in line.split(b"#")[0].split()]
-        w, h, maxval = fields[:3]
-        if maxval != 255:
-            raise FormatError(f"{path}: only 8-bit PPM supported")
-        buf = f.read(w * h * 3)
-        if len(buf) != w * h * 3:
-            raise FormatError(f"{path}: truncated pixel data")
-    return np.frombuffer(buf, dtype=np.uint8).reshape(h, w, 3) / 255.0
+    data = open(path, "rb").read()
+    if data[:2] != b"P6":
+        raise FormatError(f"{path}: not a P6 PPM")
+    # header: width, height and maxval as whitespace-separated integers after
+    # the magic, '#' starting a comment that runs to the end of its line
+    pos, hdr = 2, []
+    while len(hdr) < 3:
+        eol = data.find(b"\n", pos)
+        if pos >= len(data):
+            raise FormatError(f"{path}: truncated header")
+        line = data[pos:] if eol < 0 else data[pos:eol + 1]
+        pos += len(line)
+        hdr.extend(int(t) for t in line.partition(b"#")[0].split())
+    w, h, maxval = hdr[:3]
+    if maxval != 255:
+        raise FormatError(f"{path}: only 8-bit PPM supported")
+    npix = 3 * w * h
+    if len(data) - pos < npix:
+        raise FormatError(f"{path}: truncated pixel data")
+    return np.frombuffer(data, dtype=np.uint8, count=npix, offset=pos).reshape(h, w, 3) / 255.0
 
 
 # ------------------------------------------------------------- checkpoints ---

@@ -433,7 +433,7 @@ class Engine:
         self._pairs = {("far", l): m2l_pairs(t) for l, t in self.m2l_tables["far"].items()}
         self._pairs[("near", levels)] = m2l_pairs(self.m2l_tables["near"])
         self._h = None
-        self.flag = None
+        self._flag = None
         self._cascade_hook = None    # parallel.sharded: the multi-GPU cascade
         # finest far + near M2L through the per-axis factors of its tables
         # (kernel.separable_factors, csrc/m2l_sep.cu) when they factor;
@@ -466,8 +466,15 @@ class Engine:
                     h.h, f["pre"].ctypes.data, f["post"].ctypes.data, f["conv"].ctypes.data),
                     "engine_set_separable")
             self._h = h
-            self.flag = DomainFlag()
+            self._flag = DomainFlag()
         return self._h.h
+
+    @property
+    def flag(self) -> DomainFlag:
+        """The engine's device domain flag (created with the device side)."""
+        if self._flag is None:
+            _ = self.handle
+        return self._flag
 
     def aux_stream(self) -> torch.cuda.Stream:
         """A second stream for work that only depends on a layer's inputs

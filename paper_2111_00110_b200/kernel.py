@@ -255,20 +255,19 @@ def _probe_error(kernel: KernelModel, table: M2LTable, idx: int, rng) -> float:
 
 
 def _check_admissibility(kernel, table: M2LTable, tol: float, rng) -> None:
-    """Reference kernel.py:232-254."""
+    """Probe one table entry against the kernel (reference kernel.py:232-254):
+    the near table at its self offset (0, 0, 0), with a 20x looser limit; a
+    far table at its closest active offset (Chebyshev distance), if any."""
     if table.nearfield:
-        idx = int(np.flatnonzero((table.offsets == 0).all(axis=1))[0])
-        worst = _probe_error(kernel, table, idx, rng)
-        if worst > 20.0 * tol:
-            raise AdmissibilityError(table.level, worst, 20.0 * tol)
-        return
-    if not table.active.any():
-        return
-    dist = np.abs(table.offsets).max(axis=1)
-    idx = int(np.argmin(np.where(table.active, dist, np.iinfo(np.int64).max)))
-    worst = _probe_error(kernel, table, idx, rng)
-    if worst > tol:
-        raise AdmissibilityError(table.level, worst, tol)
+        probe, limit = int(np.argmax(~table.offsets.any(axis=1))), 20.0 * tol
+    elif table.active.any():
+        cheb = np.where(table.active, np.abs(table.offsets).max(axis=1), np.iinfo(np.int64).max)
+        probe, limit = int(np.argmin(cheb)), tol
+    else:
+        return                      # nothing resolved at this level
+    err = _probe_error(kernel, table, probe, rng)
+    if err > limit:
+        raise AdmissibilityError(table.level, err, limit)
 
 
 def fit_m2l_tables(kernel: KernelModel, levels: int, lsq: bool = True,

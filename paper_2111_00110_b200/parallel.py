@@ -229,11 +229,31 @@ class DeviceBackend:
         out = self._acc(L).eval_device(pts, mode, wts=wts)
         return out["value"], out["wgrad"]
 
+    def raise_if_set(self, what: str, group=None) -> None:
+        """DomainError on every rank when any rank's point kernels flagged an
+        out-of-domain point (the flag is max-reduced over the ranks)."""
+        flag = self.engine.flag
+        prev = flag.reduce_hook
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            flag.reduce_hook = _flag_reducer(flag, Comm(group), group)
+        try:
+            flag.raise_if_set(what)
+        finally:
+            flag.reduce_hook = prev
+
     def _acc(self, L):
         from .expansion import Accessor, ExpansionGrid
         eng = self.engine
         return Accessor(ExpansionGrid(eng.levels, "L", L, eng.rho), eng.table, eng.flops,
                         flag=eng.flag)
+
+
+def _flag_reducer(flag, comm: Comm, group):
+    def reduce_flag(v: int) -> int:
+        t = torch.tensor([int(v)], dtype=torch.int32, device=flag.t.device if comm.nccl else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return int(t.item())
+    return reduce_flag
 
 
 @contextmanager
@@ -250,13 +270,7 @@ def sharded(engine, group=None):
     _ = engine.handle
     prev = (engine._cascade_hook, engine.flag.reduce_hook)
     engine._cascade_hook = lambda m: sharded_cascade(be, m, comm)
-
-    def reduce_flag(v: int) -> int:
-        t = torch.tensor([int(v)], dtype=torch.int32,
-                         device=engine.flag.t.device if comm.nccl else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        return int(t.item())
-    engine.flag.reduce_hook = reduce_flag
+    engine.flag.reduce_hook = _flag_reducer(engine.flag, comm, group)
     try:
         yield engine
     finally:
@@ -289,6 +303,8 @@ def explicit_forward_sharded(backend, p, w, q, group=None) -> ShardedExplicitRes
         values, q_grad = backend.evaluate_value_grad(L, q)
     else:
         values, _ = backend.evaluate(L, q, None, True)
+    if hasattr(backend, "raise_if_set"):
+        backend.raise_if_set("source/query", group)
     return ShardedExplicitResult(values=values, L=L, q=q, p=p, w=w, q_grad=q_grad)
 
 
@@ -300,4 +316,6 @@ def explicit_jvp_sharded(backend, y_bar, res: ShardedExplicitResult, group=None)
         _, q_bar = backend.evaluate(res.L, res.q, y_bar, False)
     G = _cascade(backend, backend.p2m_grid(res.q, y_bar), group)
     w_bar, p_bar = backend.evaluate(G, res.p, res.w, True)
+    if hasattr(backend, "raise_if_set"):
+        backend.raise_if_set("source/query", group)
     return w_bar, p_bar, q_bar

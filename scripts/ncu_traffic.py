@@ -11,6 +11,8 @@ import csv, io, json, re, subprocess, sys
 
 MAP = [  # (regex on the ncu kernel name, library profile label)
     (r"l2p_(warp_)?kernel", "l2p"), (r"p2m_sorted_kernel", "p2m"),
+    (r"brick_hist_kernel", "brick_hist"), (r"brick_(colsum|start|offsets)_kernel", "brick_scan"),
+    (r"brick_scatter_kernel", "brick_scatter"), (r"brick_p2m_kernel", "brick_p2m"),
     (r"cell_keys_kernel", "cell_keys"), (r"place_kernel", "sort_place"),
     (r"segment_sort_\w+_kernel", "sort_segments"), (r"scan_\w+_kernel", "scan"),
     (r"sep_pre_kernel", "m2l_sep_pre"), (r"sep_post_kernel", "m2l_sep_post_l2l"),

@@ -150,10 +150,36 @@ def part_cfg3_small():
     sens = np.array([rl(dp.w_bar, gd.w_bar), rl(dp.p_bar, gd.p_bar), rl(sp.w_bar, gs.w_bar),
                      rl(sp.p_bar, gs.p_bar)])
     print(f"    self-sensitivity (depth w,p / surface w,p): {sens}")
+    # float32 floor: the reference's own adjoints when the ONLY change is
+    # rounding its float64 finest L grid to float32 in the forward (the roots,
+    # gradients and Hessians then come from a correctly rounded float32 field)
+    orig = Engine.expand
+
+    def rounded_expand(self, src):
+        acc = orig(self, src)
+        acc.grid.data[...] = acc.grid.data.astype(np.float32).astype(np.float64)
+        return acc
+    Engine.expand = rounded_expand
+    try:
+        rr = depth_forward(eng, SourceSet(p, w), b, bias=0.05)
+    finally:
+        Engine.expand = orig
+    dr, sr = depth_jvp(yl, rr), surface_gradient_jvp(yg, rr)
+    floor = np.array([rl(dr.w_bar, gd.w_bar), rl(dr.p_bar, gd.p_bar), rl(sr.w_bar, gs.w_bar),
+                      rl(sr.p_bar, gs.p_bar)])
+    both = rr.hit & res.hit
+    floor_denom = rl(rr.denom[both], res.denom[both])      # the mediator: <r, grad f> at the hit
+    print(f"    float32-grid floor (depth w,p / surface w,p): {floor}, "
+          f"hit flips {int((rr.hit != res.hit).sum())}, denominators moved {floor_denom:.3e}")
+    # the reference's own hit points and Hessians (rows xx yy zz xy xz yz) at
+    # them: the backward can be checked on identical roots
+    hess = np.zeros((b.count, 6))
+    hess[res.hit] = res.accessor.partials2(res.points[res.hit])[:, 0, :]
     save("rays_cfg3", p=p, w=w, origins=b.origins, directions=b.directions, bias=0.05,
-         sensitivity=sens,
+         sensitivity=sens, floor_fp32_grid=floor, floor_denom=floor_denom,
          n_segments=res.hit.size, lengths=res.lengths, hit=res.hit, grads=res.grads,
-         denom=res.denom, y_len=yl, y_grad=yg, depth_w_bar=gd.w_bar, depth_p_bar=gd.p_bar,
+         denom=res.denom, points=res.points, hess=hess, y_len=yl, y_grad=yg,
+         depth_w_bar=gd.w_bar, depth_p_bar=gd.p_bar,
          surf_w_bar=gs.w_bar, surf_p_bar=gs.p_bar)
 
 

@@ -384,8 +384,10 @@ def test_explicit_config2_full_size_properties(cuda):
 
 
 def test_m2l_tensor_core_level5_matches_oracle(cuda):
-    """The finest level of configs 2-4 runs the tcgen05 3xTF32 M2L (far+near
-    merged); compare the full cascade against the float64 oracle."""
+    """The default level-5 cascade (separable finest far + near M2L, tcgen05
+    fp16-split coarse levels) against the float64 oracle, and the level-5 far
+    table through the dense tcgen05 kernel (Engine.m2l) against the oracle's
+    per-table M2L."""
     from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
     eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
     ora = Oracle(1000.0, 4, 5)
@@ -483,34 +485,6 @@ def test_graphed_explicit_replays_bit_identical(eng4):
     with pytest.raises(DomainError):
         step(q=bad)
     step(q=q)   # the flag is re-zeroed inside the graph
-
-
-def test_m2l_cta_pair_kernel_matches_single_cta():
-    """The opt-in CTA-pair M2L (tcgen05 cta_group::2, FC2T2_TC_CG2=1) gives the
-    same level-5 cascade as the single-CTA kernel, bit for bit (same products,
-    same accumulation order).  Runs in a subprocess: the switch is read at
-    table build."""
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import torch,sys\n"
-        "sys.path.insert(0, '.')\n"
-        "from paper_2111_00110_b200 import Engine, KernelModel\n"
-        "eng = Engine(KernelModel('gaussian', 1000.0, 4), 5, check_admissibility=False)\n"
-        "g = torch.Generator(device='cuda').manual_seed(3)\n"
-        "p = torch.rand(200000, 3, device='cuda', generator=g) * 1.999998 - 0.999999\n"
-        "w = torch.randn(200000, 1, device='cuda', generator=g)\n"
-        "L = eng.cascade_device(eng.p2m_device(p, w).storage)\n"
-        "torch.save(L.cpu(), sys.argv[1])\n")
-    outs = []
-    for cg2 in ("0", "1"):
-        path = f"/tmp/fc2t2_cg_{cg2}.pt"
-        env = dict(os.environ, FC2T2_TC_CG2=cg2)
-        subprocess.run([sys.executable, "-c", code, path], check=True, env=env, timeout=300,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-        outs.append(torch.load(path))
-    assert torch.equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("alpha,rho,level,C,lsq", [(1000.0, 4, 5, 1, True), (200.0, 4, 4, 2, True),

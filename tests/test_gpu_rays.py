@@ -113,32 +113,90 @@ def test_depth_invariants(small, eng3):
     assert np.max(np.abs(f)) < 1e-5
 
 
+def _backward_on_reference_roots(res, g, keep, y_len, y_grad):
+    """Our device backward (payload + insertion + expansion + source adjoints)
+    run on the REFERENCE's roots: its hit points, gradients, denominators and
+    Hessians from the golden file, for the rays in ``keep``."""
+    import dataclasses
+
+    import torch
+    from paper_2111_00110_b200.layers import _root_jvp
+    dev = res.dev["hit"].device
+    hit = torch.from_numpy((g["hit"] & keep).astype(np.uint8)).to(dev)
+    pts = np.where(g["hit"][:, None], g["points"], 0.0)
+    d = {"hit": hit, "points": torch.from_numpy(pts).to(dev),
+         "grads": torch.from_numpy(np.nan_to_num(g["grads"]).astype(np.float32)).to(dev),
+         "hess": torch.from_numpy(g["hess"].astype(np.float32)).to(dev),
+         "denom": torch.from_numpy(np.nan_to_num(g["denom"]).astype(np.float32)).to(dev)}
+    return _root_jvp(dataclasses.replace(res, dev=d), y_len, y_grad)
+
+
+def test_config3_backward_on_reference_roots(cuda):
+    """The root-layer backward alone, at config-3 geometry, on the reference's
+    own roots: every float32 step after the root walk (IFT weights, dipole
+    payloads, insertion, expansion, source adjoints) to 1e-5."""
+    from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
+    from paper_2111_00110_b200.layers import depth_forward
+    g = golden("rays_cfg3")
+    eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
+    res = depth_forward(eng, SourceSet(g["p"], g["w"]), _bundle(g), bias=float(g["bias"]))
+    allr = np.ones(g["hit"].size, bool)
+    gd = _backward_on_reference_roots(res, g, allr, g["y_len"], None)
+    gs = _backward_on_reference_roots(res, g, allr, None, g["y_grad"])
+    errs = [rel_l2(gd.w_bar, g["depth_w_bar"]), rel_l2(gd.p_bar, g["depth_p_bar"]),
+            rel_l2(gs.w_bar, g["surf_w_bar"]), rel_l2(gs.p_bar, g["surf_p_bar"])]
+    print("backward on reference roots (depth w,p / surface w,p):", errs)
+    assert max(errs) < TOL, errs
+
+
 def test_config3_small_matches_reference(cuda):
-    """Config-3 geometry at level 5 (reduced N and camera; golden from the reference)."""
+    """Config-3 geometry at level 5 (reduced N and camera; golden from the reference).
+
+    Forward: hit mask (flips counted, <= 0.2 %), lengths and gradients < 1e-5.
+    Adjoints, always compared: tangents of rays whose hit status differs are
+    zeroed on our side, and their reference contribution is removed from the
+    golden by linearity (our backward on the reference's roots for those rays,
+    pinned to 1e-5 by test_config3_backward_on_reference_roots).
+
+    Tolerance: the root-layer adjoints are ill-conditioned in the IFT
+    denominators <r, grad f> at the hits.  The reference's OWN adjoints move by
+    ``floor_fp32_grid`` (1.6-1.9e-5, > 1e-5) when the only change is rounding
+    its float64 L grid to float32, which moves its denominators by
+    ``floor_denom``; so no float32 field can reach 1e-5.  Our field is a
+    float32 cascade (denominators off by e_den), and the adjoint error must be
+    what that conditioning predicts: <= 3 x floor x e_den / floor_denom."""
     from paper_2111_00110_b200 import Engine, KernelModel, SourceSet
     from paper_2111_00110_b200.layers import depth_forward, depth_jvp, surface_gradient_jvp
     g = golden("rays_cfg3")
     eng = Engine(KernelModel("gaussian", 1000.0, 4), 5, check_admissibility=False)
     res = depth_forward(eng, SourceSet(g["p"], g["w"]), _bundle(g), bias=float(g["bias"]))
-    mism = int((res.hit != g["hit"]).sum())
+    flip = res.hit != g["hit"]
+    mism = int(flip.sum())
+    print(f"config 3: {mism} hit flips of {flip.size} rays")
     assert mism <= max(2, int(0.002 * g["hit"].size)), mism
     both = res.hit & g["hit"]
     assert rel_l2(res.lengths[both], g["lengths"][both]) < TOL
     assert rel_l2(res.grads[both], g["grads"][both]) < TOL
-    if mism == 0:
-        # The root-layer adjoints are ill-conditioned: the IFT weights
-        # -y/<r, grad f> are large and of both signs and w_bar sums them with
-        # cancellation.  The reference itself moves by `sensitivity` (~2.3e-5)
-        # when the weights are perturbed by 2^-24 relative (stored in the
-        # golden file).  Tolerance: 25x that floor -- our float32 field carries
-        # ~1e-6 relative error, ~16x a 2^-24 perturbation.
-        sens = g["sensitivity"]
-        gd = depth_jvp(g["y_len"], res)
-        assert rel_l2(gd.w_bar, g["depth_w_bar"]) < 25 * sens[0]
-        assert rel_l2(gd.p_bar, g["depth_p_bar"]) < 25 * sens[1]
-        gs = surface_gradient_jvp(g["y_grad"], res)
-        assert rel_l2(gs.w_bar, g["surf_w_bar"]) < 25 * sens[2]
-        assert rel_l2(gs.p_bar, g["surf_p_bar"]) < 25 * sens[3]
+    e_den = rel_l2(res.denom[both], g["denom"][both])
+    yl = np.where(flip, 0.0, g["y_len"])
+    yg = np.where(flip[:, None], 0.0, g["y_grad"])
+    ref = {k: g[k].copy() for k in ("depth_w_bar", "depth_p_bar", "surf_w_bar", "surf_p_bar")}
+    if mism:
+        fd = _backward_on_reference_roots(res, g, flip, g["y_len"], None)
+        fs = _backward_on_reference_roots(res, g, flip, None, g["y_grad"])
+        ref["depth_w_bar"] -= fd.w_bar
+        ref["depth_p_bar"] -= fd.p_bar
+        ref["surf_w_bar"] -= fs.w_bar
+        ref["surf_p_bar"] -= fs.p_bar
+    gd = depth_jvp(yl, res)
+    gs = surface_gradient_jvp(yg, res)
+    errs = np.array([rel_l2(gd.w_bar, ref["depth_w_bar"]), rel_l2(gd.p_bar, ref["depth_p_bar"]),
+                     rel_l2(gs.w_bar, ref["surf_w_bar"]), rel_l2(gs.p_bar, ref["surf_p_bar"])])
+    bound = 3.0 * g["floor_fp32_grid"] * e_den / float(g["floor_denom"])
+    print(f"config-3 adjoints (depth w,p / surface w,p) {errs}; denominators off by {e_den:.2e} "
+          f"(reference float32-grid floor: {g['floor_fp32_grid']} at {float(g['floor_denom']):.2e}); "
+          f"bound {bound}")
+    assert np.all(errs <= bound), (errs, bound)
 
 
 def test_line_integral_matches_reference(small, eng3):
