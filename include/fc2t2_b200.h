@@ -53,9 +53,6 @@ extern "C" {
 #define FC2T2_L2P_GRAD 2  /* Accessor.partials expansion.py:367-369 */
 #define FC2T2_L2P_HESS 4  /* Accessor.partials2 expansion.py:371-373 */
 #define FC2T2_L2P_WGRAD 8 /* sum_c wts_c * grad f_c (layers.py:183, :186-187) */
-/* d_q / d_wts are already permuted into d_order's sequence (row t = point
- * d_order[t], see fc2t2_cell_sort_ex); outputs stay indexed by point */
-#define FC2T2_L2P_PRESORTED 16
 
 typedef struct fc2t2_engine fc2t2_engine;
 

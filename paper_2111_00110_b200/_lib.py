@@ -21,7 +21,7 @@ if os.environ.get("FC2T2_LIB_OVERRIDE"):
 OK, EDOMAIN, ESTAGE, EORDER, ECUDA, EWORKSPACE, EVALUE = range(7)
 FLAG_DOMAIN = 1
 TABLE_FAR, TABLE_NEAR, TABLE_FARNEAR = 0, 1, 2
-L2P_VALUE, L2P_GRAD, L2P_HESS, L2P_WGRAD, L2P_PRESORTED = 1, 2, 4, 8, 16
+L2P_VALUE, L2P_GRAD, L2P_HESS, L2P_WGRAD = 1, 2, 4, 8
 
 _vp = ct.c_void_p
 _i32, _i64, _sz = ct.c_int, ct.c_int64, ct.c_size_t

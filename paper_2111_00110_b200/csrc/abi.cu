@@ -1023,8 +1023,6 @@ int fc2t2_l2p(int rho, int level, int channels, const float* d_l, const float* d
   if (rho < 1 || rho > 6) return fail(FC2T2_EORDER, "expansion order must be in [1, 6]");
   if (level < 0 || level > 9 || channels < 1 || n < 0) return fail(FC2T2_EVALUE, "bad l2p arguments");
   if ((mode & FC2T2_L2P_WGRAD) && !d_wts) return fail(FC2T2_EVALUE, "WGRAD needs weights");
-  if ((mode & FC2T2_L2P_PRESORTED) && !d_order)
-    return fail(FC2T2_EVALUE, "PRESORTED needs the order that maps rows to points");
   return cuda_status(fc2t2::l2p(rho, level, channels, d_l, d_q, n, mode, d_order, d_wts, d_value,
                                 d_grad, d_hess, d_wgrad, d_flag, (cudaStream_t)stream),
                      "l2p");

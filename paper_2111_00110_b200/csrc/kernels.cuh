@@ -111,7 +111,6 @@ enum L2PMode : int {
   L2P_GRAD = 2,    // (n, C, 3)
   L2P_HESS = 4,    // (n, C, 6)  xx yy zz xy xz yz
   L2P_WGRAD = 8,   // (n, 3) = sum_c wts[n, c] * grad f_c
-  L2P_PRESORTED = 16,  // q / wts given in `order` sequence; outputs by point
 };
 // out (n, 3) = sum_c w (n, C) * grad (n, C, 3): L2P_WGRAD from stored gradients
 cudaError_t weighted_grad(const float* grad, const float* w, int64_t n, int C, float* out,

@@ -1,96 +1,131 @@
 // L2P: evaluate the finest local expansions at free points.
 //
-// Reference: Accessor._local/value/partials/partials2 (expansion.py:335-373).
-// One thread per point: bit-exact box lookup, in-box offset, monomials, then
-// per channel a 16-byte-vectorised read of the cell's coefficient row and
-// contractions for the value, the gradient (coefficient shift n -> n + e_a,
+// Reference: Accessor._local/value/partials/partials2 (expansion.py:335-373):
+// bit-exact box lookup, in-box offset d, then per channel the contractions
+// value = sum_n A_n d^n / n!, the gradient (coefficient shift n -> n + e_a,
 // reference _shift_indices :309-329) and the Hessian (xx yy zz xy xz yz).
 // L2P_WGRAD fuses the adjoint contraction sum_c wts_c grad f_c used by the
 // explicit layer's q_bar and p_bar (reference layers.py:183, :186-187).
 //
-// With a cell-sorted `order` (the stable sort P2M needs anyway), thread t
-// evaluates point order[t]: neighbouring threads share cell rows, which then
-// come from L1 instead of one 144-byte L2 gather per point.  With
-// L2P_PRESORTED the inputs (q, wts) are already permuted into that order
-// (fc2t2_cell_sort_ex / fc2t2_permute_rows), so they are read coalesced and
-// only the outputs are scattered to order[t].
+// Row fetch (warp-cooperative): a thread-per-point gather makes every float4
+// load instruction of a warp touch 32 different cell rows.  Here the warp
+// copies its 32 points' rows into shared memory with consecutive lanes on
+// consecutive 16-byte pieces of the same row (~2.5 rows per instruction),
+// then each thread reads its own row back (row stride PP words: the 8 lanes
+// of a 128-bit shared access hit distinct bank quads for PP = 4, 12, 20, 36,
+// 84).
+//
+// Contraction (nested, no monomial table): with X_a = dx^a/a!, Y_b, Z_c,
+//   T[a][b]  = sum_c Z_c A[a,b,c]          S[a]  = sum_b Y_b T[a][b]
+//   value    = sum_a X_a S[a]
+//   d/dx     = sum_{a>=1} X_{a-1} S[a]      d/dy = sum_a X_a sum_{b>=1} Y_{b-1} T[a][b]
+//   d/dz     = sum_a X_a sum_b Y_b sum_{c>=1} Z_{c-1} A[a,b,c]
+// (and the second derivatives alike): 55 + 30 + 15 FMAs for value + gradient
+// at rho = 4 instead of a 35-entry monomial table (105 multiplies) and four
+// 35-term dot products -- half the registers, twice the resident warps.
+// With a cell-sorted `order`, thread t evaluates point order[t] (outputs
+// stay indexed by point).
 #include "common.cuh"
 #include "kernels.cuh"
-
-#include <cstdlib>
 
 namespace fc2t2 {
 
 namespace {
-
-// Contractions of one point's cell row `a` (PP floats of channel c).
-template <int RHO, int MODE>
-__device__ __forceinline__ void l2p_contract(const float (&a)[MI<RHO>::PP], const float (&mono)[MI<RHO>::P],
-                                             int64_t i, int c, int C, float wv,
-                                             float* __restrict__ value,
-                                             float* __restrict__ grad, float* __restrict__ hess,
-                                             float& wg0, float& wg1, float& wg2) {
-  constexpr MI<RHO> mi{};
-  constexpr int P = MI<RHO>::P;
-  if constexpr (MODE & L2P_VALUE) {
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < P; ++j) s = fmaf(a[j], mono[j], s);
-    value[i * C + c] = s;
-  }
-  if constexpr ((MODE & L2P_GRAD) || (MODE & L2P_WGRAD)) {
-    float g[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      float s = 0.f;
-#pragma unroll
-      for (int j = 0; j < P; ++j)
-        if (mi.up[d][j] >= 0) s = fmaf(a[mi.up[d][j]], mono[j], s);
-      g[d] = s;
-    }
-    if constexpr (MODE & L2P_GRAD) {
-      grad[(i * C + c) * 3 + 0] = g[0];
-      grad[(i * C + c) * 3 + 1] = g[1];
-      grad[(i * C + c) * 3 + 2] = g[2];
-    }
-    if constexpr (MODE & L2P_WGRAD) {
-      wg0 = fmaf(wv, g[0], wg0);
-      wg1 = fmaf(wv, g[1], wg1);
-      wg2 = fmaf(wv, g[2], wg2);
-    }
-  }
-  if constexpr (MODE & L2P_HESS) {
-#pragma unroll
-    for (int d = 0; d < 6; ++d) {
-      float s = 0.f;
-#pragma unroll
-      for (int j = 0; j < P; ++j)
-        if (mi.up[3 + d][j] >= 0) s = fmaf(a[mi.up[3 + d][j]], mono[j], s);
-      hess[(i * C + c) * 6 + d] = s;
-    }
-  }
-}
 
 __device__ __forceinline__ void l2p_cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-// Warp-cooperative row fetch.  A thread-per-point gather makes every float4
-// load instruction of a warp touch 32 different cell rows (32 L1 tag lookups
-// / wavefronts per instruction, PP/4 instructions per point).  Here the warp
-// copies its 32 points' rows into shared memory with consecutive lanes on
-// consecutive 16-byte pieces of the same row (about 2.5 rows = 4-6 lines per
-// instruction, same PP/4 instructions per lane), then each thread reads its
-// own row back from shared memory (row stride PP words: the 8 lanes of a
-// 128-bit shared access hit distinct bank quads for PP = 4, 12, 20, 36, 84).
+// sum_c Z[c - s] A[a, b, c] over c >= s (s = 0, 1, 2: the z shift)
+template <int RHO, int S>
+__device__ __forceinline__ float zsum(const float (&A)[MI<RHO>::PP], const float (&Z)[RHO + 1],
+                                      int a, int b) {
+  float t = 0.f;
+#pragma unroll
+  for (int c = S; c <= RHO - a - b; ++c) t = fmaf(Z[c - S], A[MI<RHO>::index(a, b, c)], t);
+  return t;
+}
+
+// One point, one channel: value / gradient / Hessian of its cell row A.
 template <int RHO, int MODE>
-__global__ void __launch_bounds__(256)
-l2p_warp_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, int C, int res,
-                const int32_t* __restrict__ order, bool presorted, const float* __restrict__ wts,
-                float* __restrict__ value, float* __restrict__ grad, float* __restrict__ hess,
-                float* __restrict__ wgrad, int32_t* __restrict__ flag) {
-  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP, F4 = PP / 4;
+__device__ __forceinline__ void l2p_nested(const float (&A)[MI<RHO>::PP], const float (&X)[RHO + 1],
+                                           const float (&Y)[RHO + 1], const float (&Z)[RHO + 1],
+                                           float& v, float (&g)[3], float (&h)[6]) {
+  constexpr bool G = (MODE & (L2P_GRAD | L2P_WGRAD)) != 0, H = (MODE & L2P_HESS) != 0;
+  float S[RHO + 1], Sy[RHO + 1], Sz[RHO + 1], Syy[RHO + 1], Szz[RHO + 1], Syz[RHO + 1];
+#pragma unroll
+  for (int a = 0; a <= RHO; ++a) {
+    float s = 0.f, sy = 0.f, sz = 0.f, syy = 0.f, szz = 0.f, syz = 0.f;
+#pragma unroll
+    for (int b = 0; b <= RHO - a; ++b) {
+      const float t = zsum<RHO, 0>(A, Z, a, b);
+      s = fmaf(Y[b], t, s);
+      if constexpr (G || H) {
+        if (b >= 1) sy = fmaf(Y[b - 1], t, sy);
+        const float tz = zsum<RHO, 1>(A, Z, a, b);
+        sz = fmaf(Y[b], tz, sz);
+        if constexpr (H) {
+          if (b >= 2) syy = fmaf(Y[b - 2], t, syy);
+          if (b >= 1) syz = fmaf(Y[b - 1], tz, syz);
+          szz = fmaf(Y[b], zsum<RHO, 2>(A, Z, a, b), szz);
+        }
+      }
+    }
+    S[a] = s; Sy[a] = sy; Sz[a] = sz; Syy[a] = syy; Szz[a] = szz; Syz[a] = syz;
+  }
+  v = 0.f;
+#pragma unroll
+  for (int a = 0; a <= RHO; ++a) v = fmaf(X[a], S[a], v);
+  if constexpr (G || H) {
+    g[0] = g[1] = g[2] = 0.f;
+#pragma unroll
+    for (int a = 0; a <= RHO; ++a) {
+      if (a >= 1) g[0] = fmaf(X[a - 1], S[a], g[0]);
+      g[1] = fmaf(X[a], Sy[a], g[1]);
+      g[2] = fmaf(X[a], Sz[a], g[2]);
+    }
+  }
+  if constexpr (H) {
+#pragma unroll
+    for (int d = 0; d < 6; ++d) h[d] = 0.f;
+#pragma unroll
+    for (int a = 0; a <= RHO; ++a) {
+      if (a >= 2) h[0] = fmaf(X[a - 2], S[a], h[0]);     // xx
+      h[1] = fmaf(X[a], Syy[a], h[1]);                     // yy
+      h[2] = fmaf(X[a], Szz[a], h[2]);                     // zz
+      if (a >= 1) h[3] = fmaf(X[a - 1], Sy[a], h[3]);     // xy
+      if (a >= 1) h[4] = fmaf(X[a - 1], Sz[a], h[4]);     // xz
+      h[5] = fmaf(X[a], Syz[a], h[5]);                     // yz
+    }
+  }
+}
+
+template <int RHO>
+__device__ __forceinline__ void axis_table(float d, float (&T)[RHO + 1]) {
+  T[0] = 1.f;
+#pragma unroll
+  for (int k = 1; k <= RHO; ++k) T[k] = T[k - 1] * d * (1.f / (float)k);
+}
+
+template <int RHO, int MODE>
+constexpr int l2p_min_blocks() {
+#ifdef FC2T2_L2P_MINB
+  return (RHO <= 4 && !(MODE & L2P_HESS)) ? FC2T2_L2P_MINB : 2;
+#else
+  // 3: measured best (10^7-point value+grad 246 us at 2 or 3 blocks, 321 us at
+  // 4 -- the row gathers are L2-throughput bound; value+wgrad 40 vs 45 us)
+  return (RHO <= 4 && !(MODE & L2P_HESS)) ? 3 : 2;
+#endif
+}
+
+template <int RHO, int MODE>
+__global__ void __launch_bounds__(256, (l2p_min_blocks<RHO, MODE>()))
+l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, int C, int res,
+           const int32_t* __restrict__ order, const float* __restrict__ wts,
+           float* __restrict__ value, float* __restrict__ grad, float* __restrict__ hess,
+           float* __restrict__ wgrad, int32_t* __restrict__ flag) {
+  constexpr int PP = MI<RHO>::PP, F4 = PP / 4;
   extern __shared__ __align__(16) float l2p_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* rows = l2p_smem + warp * 32 * PP;
@@ -101,19 +136,20 @@ l2p_warp_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_
     const int64_t t = base + lane;
     const bool valid = t < n;
     const int64_t i = valid ? (order ? (int64_t)order[t] : t) : 0;
-    const int64_t in = presorted ? (valid ? t : 0) : i;
     float x = 0.f, y = 0.f, z = 0.f;
-    if (valid) { x = q[3 * in]; y = q[3 * in + 1]; z = q[3 * in + 2]; }
+    if (valid) { x = q[3 * i]; y = q[3 * i + 1]; z = q[3 * i + 2]; }
     bad |= valid && outside_domain(x, y, z);
     const int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
-    float mono[P];
-    monomials<RHO>(box_offset(x, b0, res), box_offset(y, b1, res), box_offset(z, b2, res), mono);
+    float X[RHO + 1], Y[RHO + 1], Z[RHO + 1];
+    axis_table<RHO>(box_offset(x, b0, res), X);
+    axis_table<RHO>(box_offset(y, b1, res), Y);
+    axis_table<RHO>(box_offset(z, b2, res), Z);
     const int64_t rowoff = ((((int64_t)b0 * res + b1) * res + b2) * C) * PP;
     float wg0 = 0.f, wg1 = 0.f, wg2 = 0.f;
     for (int c = 0; c < C; ++c) {
-      // the tangent weight is read before the copy barrier so its latency
+      // the tangent weight is read before the copy wait so its latency
       // overlaps the row fetch
-      const float wv = ((MODE & L2P_WGRAD) && valid) ? wts[in * C + c] : 0.f;
+      const float wv = ((MODE & L2P_WGRAD) && valid) ? wts[i * C + c] : 0.f;
 #pragma unroll
       for (int k = 0; k < F4; ++k) {
         const int j = k * 32 + lane;
@@ -123,14 +159,32 @@ l2p_warp_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_
       }
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncwarp();
-      float a[PP];
+      float A[PP];
 #pragma unroll
       for (int k = 0; k < PP; k += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(rows + lane * PP + k);
-        a[k] = v.x; a[k + 1] = v.y; a[k + 2] = v.z; a[k + 3] = v.w;
+        const float4 v4 = *reinterpret_cast<const float4*>(rows + lane * PP + k);
+        A[k] = v4.x; A[k + 1] = v4.y; A[k + 2] = v4.z; A[k + 3] = v4.w;
       }
       __syncwarp();
-      if (valid) l2p_contract<RHO, MODE>(a, mono, i, c, C, wv, value, grad, hess, wg0, wg1, wg2);
+      float v, g[3], h[6];
+      l2p_nested<RHO, MODE>(A, X, Y, Z, v, g, h);
+      if (valid) {
+        if constexpr (MODE & L2P_VALUE) value[i * C + c] = v;
+        if constexpr (MODE & L2P_GRAD) {
+          grad[(i * C + c) * 3 + 0] = g[0];
+          grad[(i * C + c) * 3 + 1] = g[1];
+          grad[(i * C + c) * 3 + 2] = g[2];
+        }
+        if constexpr (MODE & L2P_HESS) {
+#pragma unroll
+          for (int d = 0; d < 6; ++d) hess[(i * C + c) * 6 + d] = h[d];
+        }
+        if constexpr (MODE & L2P_WGRAD) {
+          wg0 = fmaf(wv, g[0], wg0);
+          wg1 = fmaf(wv, g[1], wg1);
+          wg2 = fmaf(wv, g[2], wg2);
+        }
+      }
     }
     if constexpr (MODE & L2P_WGRAD) {
       if (valid) {
@@ -143,72 +197,19 @@ l2p_warp_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_
   if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
 }
 
-template <int RHO, int MODE>
-__global__ void __launch_bounds__(256)
-l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, int C, int res,
-           const int32_t* __restrict__ order, bool presorted, const float* __restrict__ wts,
-           float* __restrict__ value, float* __restrict__ grad, float* __restrict__ hess,
-           float* __restrict__ wgrad, int32_t* __restrict__ flag) {
-  constexpr MI<RHO> mi{};
-  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
-  int bad = 0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    // outputs at point i; inputs at i, or at t when they are pre-permuted
-    const int64_t i = order ? (int64_t)order[t] : t;
-    const int64_t in = presorted ? t : i;
-    const float x = q[3 * in], y = q[3 * in + 1], z = q[3 * in + 2];
-    bad |= outside_domain(x, y, z);
-    const int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
-    float mono[P];
-    monomials<RHO>(box_offset(x, b0, res), box_offset(y, b1, res), box_offset(z, b2, res), mono);
-    const float* row = L + ((((int64_t)b0 * res + b1) * res + b2) * C) * PP;
-    float wg0 = 0.f, wg1 = 0.f, wg2 = 0.f;
-    for (int c = 0; c < C; ++c) {
-      float a[PP];
-#pragma unroll
-      for (int k = 0; k < PP; k += 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(row + c * PP + k));
-        a[k] = v.x; a[k + 1] = v.y; a[k + 2] = v.z; a[k + 3] = v.w;
-      }
-      const float wv = (MODE & L2P_WGRAD) ? wts[in * C + c] : 0.f;
-      l2p_contract<RHO, MODE>(a, mono, i, c, C, wv, value, grad, hess, wg0, wg1, wg2);
-    }
-    if constexpr (MODE & L2P_WGRAD) {
-      wgrad[3 * i + 0] = wg0;
-      wgrad[3 * i + 1] = wg1;
-      wgrad[3 * i + 2] = wg2;
-    }
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
-}
-
-bool l2p_thread_per_point() {
-  static const bool v = [] {
-    const char* e = std::getenv("FC2T2_L2P_THREAD");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-
 template <int RHO, int M>
 cudaError_t l2p_launch(int blocks, int C, int res, const float* L, const float* q, int64_t n,
-                       const int32_t* order, bool presorted, const float* wts, float* value,
-                       float* grad, float* hess, float* wgrad, int32_t* flag, cudaStream_t s) {
-  // a cell-coherent order makes neighbouring threads share rows (L1
-  // broadcast), which the per-thread gather exploits and the cooperative copy
-  // would duplicate
-  if (order || l2p_thread_per_point()) {
-    FC2T2_LAUNCH("l2p", s, l2p_kernel<RHO, M><<<blocks, 256, 0, s>>>(
-        L, q, n, C, res, order, presorted, wts, value, grad, hess, wgrad, flag));
-    return cudaGetLastError();
-  }
+                       const int32_t* order, const float* wts, float* value, float* grad,
+                       float* hess, float* wgrad, int32_t* flag, cudaStream_t s) {
   constexpr int smem = 8 * 32 * MI<RHO>::PP * (int)sizeof(float);
   static unsigned long long configured = 0;
-  if (smem > 48 * 1024 && attr_needed(configured))
-    cudaFuncSetAttribute(l2p_warp_kernel<RHO, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  FC2T2_LAUNCH("l2p", s, l2p_warp_kernel<RHO, M><<<blocks, 256, smem, s>>>(
-      L, q, n, C, res, order, presorted, wts, value, grad, hess, wgrad, flag));
+  if (smem > 48 * 1024 && attr_needed(configured)) {
+    const cudaError_t e = cudaFuncSetAttribute(l2p_kernel<RHO, M>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  FC2T2_LAUNCH("l2p", s, l2p_kernel<RHO, M><<<blocks, 256, smem, s>>>(
+      L, q, n, C, res, order, wts, value, grad, hess, wgrad, flag));
   return cudaGetLastError();
 }
 
@@ -218,12 +219,10 @@ cudaError_t l2p_rho(int level, int C, const float* L, const float* q, int64_t n,
                     float* hess, float* wgrad, int32_t* flag, cudaStream_t s) {
   const int res = 1 << (level + 1);
   const int blocks = grid_blocks(n, 256, 148 * 16);
-  const bool presorted = (mode & L2P_PRESORTED) != 0;
-  mode &= ~L2P_PRESORTED;
-#define FC2T2_L2P_CASE(M)                                                              \
-  case M:                                                                              \
-    return l2p_launch<RHO, M>(blocks, C, res, L, q, n, order, presorted, wts, value,  \
-                              grad, hess, wgrad, flag, s);
+#define FC2T2_L2P_CASE(M)                                                                 \
+  case M:                                                                                 \
+    return l2p_launch<RHO, M>(blocks, C, res, L, q, n, order, wts, value, grad, hess,    \
+                              wgrad, flag, s);
   switch (mode) {
     FC2T2_L2P_CASE(1)
     FC2T2_L2P_CASE(2)

@@ -62,8 +62,31 @@ __device__ __forceinline__ int point_brick(float x, float y, float z, const Bric
 
 // In-place insertion sort of a short uint16 run (ascending): restores the
 // index order inside a bucket filled in atomic-arrival order.  Runs longer
-// than kShortRun are rebuilt by an ordered pass over the keys instead.
-constexpr int kShortRun = 96;
+// than kShortRun (clustered points) are rebuilt by warp_compact_run instead.
+constexpr int kShortRun = 32;
+constexpr int kMaxLong = 256;   // >= tile / (kShortRun + 1) and chunk / (kShortRun + 1)
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// One warp writes, in index order, the positions k < n whose key >> shift ==
+// want: 32 keys per step, matches compacted with a ballot (O(n / 32) steps).
+__device__ __forceinline__ void warp_compact_run(uint16_t* out, const uint32_t* key, int n,
+                                                 uint32_t want, int shift) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  uint32_t base = 0;
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    const int k = k0 + lane;
+    const bool hit = k < n && (key[k] >> shift) == want;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) out[base + __popc(m & lt)] = (uint16_t)k;
+    base += __popc(m);
+  }
+}
+
 __device__ __forceinline__ void sort_run(uint16_t* a, int n) {
   for (int i = 1; i < n; ++i) {
     const uint16_t v = a[i];
@@ -204,6 +227,8 @@ brick_scatter_kernel(const float* __restrict__ pts, const float* __restrict__ wt
   uint32_t* gbase = reinterpret_cast<uint32_t*>(sm3 + L.gbase);
   uint16_t* perm = reinterpret_cast<uint16_t*>(sm3 + L.perm);
   __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t nlong;
+  __shared__ uint16_t longs[kMaxLong];
   const int64_t t0 = (int64_t)blockIdx.x * tile;
   const int tn = (int)min((int64_t)tile, n - t0);
   // 1. the tile's points and weights into shared memory
@@ -242,18 +267,18 @@ brick_scatter_kernel(const float* __restrict__ pts, const float* __restrict__ wt
     perm[lstart[k >> 13] + (k & 8191u)] = (uint16_t)tp;
   }
   __syncthreads();
-  // ... and every brick's run back in index order (deterministic, stable);
-  // long runs (clustered points) are rebuilt by one ordered pass over the keys
+  // ... and every brick's run back in index order (deterministic, stable):
+  // short runs by one thread each, long runs (clustered points) by a warp
+  if (threadIdx.x == 0) nlong = 0;
+  __syncthreads();
   for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
     const int cnt = (int)bcnt[b];
-    if (cnt <= kShortRun) {
-      sort_run(perm + lstart[b], cnt);
-    } else {
-      uint32_t pos = lstart[b];
-      for (int tp = 0; tp < tn; ++tp)
-        if ((int)(key[tp] >> 13) == b) perm[pos++] = (uint16_t)tp;
-    }
+    if (cnt <= kShortRun) sort_run(perm + lstart[b], cnt);
+    else longs[atomicAdd(&nlong, 1u)] = (uint16_t)b;
   }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x >> 5; i < nlong; i += blockDim.x >> 5)
+    warp_compact_run(perm + lstart[longs[i]], key, tn, longs[i], 13);
   __syncthreads();
   // 5. brick runs out, coalesced
   if (RS == 4) {
@@ -316,6 +341,15 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
   uint32_t* ccnt = reinterpret_cast<uint32_t*>(perm + K4_CHUNK);       // [CB]
   uint32_t* cst = ccnt + CB;                                           // [CB]
   __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t nlong;
+  __shared__ uint16_t longs[kMaxLong];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (RS == 4 && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  uint32_t phase = 0;
 
   const BrickGeom g = brick_geom(level);
   const int brick = blockIdx.x;
@@ -335,6 +369,37 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
       const int nc = (int)umin((uint32_t)K4_CHUNK, end - c0);
       ccnt[tid] = 0u;
       __syncthreads();   // also: the previous chunk's walk is done with srec / perm
+      if (RS == 4) {
+        // C = 1: the chunk's records are contiguous -- one bulk copy (TMA)
+        // into srec, then (x, y, z, w) -> (dx, dy, dz, w) in place
+        if (threadIdx.x == 0) {
+          // the previous chunk's generic-proxy stores to srec precede the copy
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
+                       "r"((uint32_t)nc * 16u));
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+              "[%3];\n" ::"r"((uint32_t)__cvta_generic_to_shared(srec)),
+              "l"(rec + (size_t)c0 * 4), "r"((uint32_t)nc * 16u), "r"(bar_s)
+              : "memory");
+        }
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "W4_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra W4_%=;\n\t}\n" ::"r"(bar_s),
+            "r"(phase)
+            : "memory");
+        phase ^= 1u;
+        for (int k = tid; k < nc; k += CB) {
+          const float4 v = srec[k];
+          const int cx = box_axis(v.x, g.res), cy = box_axis(v.y, g.res), cz = box_axis(v.z, g.res);
+          srec[k] = make_float4(box_offset(v.x, cx, g.res), box_offset(v.y, cy, g.res),
+                                box_offset(v.z, cz, g.res), v.w);
+          const uint32_t cib = (uint32_t)((((cx & 7) << 3) | (cy & 7)) << BZS) | (cz & (BZ - 1));
+          key[k] = (cib << 16) | atomicAdd(&ccnt[cib], 1u);
+        }
+      } else {
       // stage (dx, dy, dz, w_c); cell-in-brick key and arrival rank (4
       // records per thread in flight)
       constexpr int U = 4;
@@ -363,6 +428,7 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
           }
         }
       }
+      }
       __syncthreads();
       uint32_t total;
       const uint32_t mine = ccnt[tid];
@@ -374,15 +440,17 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
         perm[cst[kk >> 16] + (kk & 0xffffu)] = (uint16_t)k;
       }
       __syncthreads();
-      // this cell's run: back into index order, then accumulated in order
+      // this cell's run back into index order (short runs by their thread,
+      // long ones -- clustered points -- by a warp), then accumulated in order
       uint16_t* mine_run = perm + st;
-      if (mine <= (uint32_t)kShortRun) {
-        sort_run(mine_run, (int)mine);
-      } else {   // clustered points: one ordered pass over the chunk's keys
-        uint32_t pos = 0;
-        for (int k = 0; k < nc; ++k)
-          if ((key[k] >> 16) == (uint32_t)tid) mine_run[pos++] = (uint16_t)k;
-      }
+      if (tid == 0) nlong = 0;
+      __syncthreads();
+      if (mine <= (uint32_t)kShortRun) sort_run(mine_run, (int)mine);
+      else longs[atomicAdd(&nlong, 1u)] = (uint16_t)tid;
+      __syncthreads();
+      for (uint32_t i = tid >> 5; i < nlong; i += CB / 32)
+        warp_compact_run(perm + cst[longs[i]], key, nc, longs[i], 16);
+      __syncthreads();
       for (uint32_t e = 0; e < mine; ++e) {
         const float4 v = srec[mine_run[e]];
         float px[RHO + 1], py[RHO + 1], pz[RHO + 1];
