@@ -138,6 +138,10 @@ struct fc2t2_engine {
   // M2M chain and the coarse levels run on the caller's stream
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  // coarse levels: every level's M2L on its own stream (cs[l & 1]) as soon as
+  // its M grid exists (ev_m[l]); the L2L chain waits for each (ev_c[l])
+  cudaStream_t cs[2] = {nullptr, nullptr};
+  cudaEvent_t ev_m[10] = {}, ev_c[10] = {};
   // separable finest M2L (m2l_sep.cu): per-axis factors, [out][in] float64
   bool sep = false;
   bool sep_fuse_l2l = true;  // fc2t2_engine_set_sep_fusion
@@ -440,6 +444,12 @@ void fc2t2_engine_destroy(fc2t2_engine* e) {
   if (e->side) cudaStreamDestroy(e->side);
   if (e->fork) cudaEventDestroy(e->fork);
   if (e->join) cudaEventDestroy(e->join);
+  for (cudaStream_t c : e->cs)
+    if (c) cudaStreamDestroy(c);
+  for (int l = 0; l < 10; ++l) {
+    if (e->ev_m[l]) cudaEventDestroy(e->ev_m[l]);
+    if (e->ev_c[l]) cudaEventDestroy(e->ev_c[l]);
+  }
   for (auto& lv : e->plans)
     for (auto& t : lv.second) {
       cudaFree(t.second.d_entries);
@@ -549,6 +559,12 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
   err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking);
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming);
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming);
+  for (int k = 0; k < 2 && err == cudaSuccess; ++k)
+    err = cudaStreamCreateWithFlags(&e->cs[k], cudaStreamNonBlocking);
+  for (int l = 0; l < 10 && err == cudaSuccess; ++l) {
+    err = cudaEventCreateWithFlags(&e->ev_m[l], cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->ev_c[l], cudaEventDisableTiming);
+  }
   if (err != cudaSuccess) return cuda_status(err, "engine_upload streams");
   e->uploaded = true;
   return FC2T2_OK;
@@ -736,6 +752,7 @@ int fc2t2_engine_set_sep_fusion(fc2t2_engine* e, int fuse_l2l) {
 namespace {
 struct ExpandLayout {
   size_t coarse_grids = 0, fine_part = 0, coarse_part = 0;
+  size_t part_off[10] = {};   // per coarse level: its M2L scratch (levels run concurrently)
   size_t total() const { return coarse_grids + fine_part + coarse_part; }
 };
 
@@ -744,8 +761,8 @@ ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
   const int L = e->levels;
   for (int l = kCoarsest; l < L; ++l) {
     w.coarse_grids += 2 * grid_floats(l, channels, e->PP);
-    w.coarse_part = std::max(w.coarse_part,
-                             part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels));
+    w.part_off[l] = w.coarse_part;
+    w.coarse_part += (part_floats(e, e->plans.at(l).at(FC2T2_TABLE_FAR), l, channels) + 63) / 64 * 64;
   }
   w.fine_part = e->sep ? fc2t2::m2l_sep_workspace_floats(e->rho, L, channels)
                        : part_floats(e, e->plans.at(L).at(FC2T2_TABLE_FARNEAR), L, channels);
@@ -802,8 +819,8 @@ void level_slab(const fc2t2_engine* e, int l, int x0, int x1, int* b, int* en) {
 }
 
 struct Grids {
-  std::vector<float*> M, L;
-  float *fine_part = nullptr, *coarse_part = nullptr;
+  std::vector<float*> M, L, part;
+  float* fine_part = nullptr;
 };
 
 Grids carve_grids(const fc2t2_engine* e, int channels, const float* d_m, float* d_l, void* d_ws) {
@@ -822,7 +839,8 @@ Grids carve_grids(const fc2t2_engine* e, int channels, const float* d_m, float* 
   g.M[L] = const_cast<float*>(d_m);
   g.L[L] = d_l;
   g.fine_part = w;
-  g.coarse_part = w + lay.fine_part;
+  g.part.assign(L + 1, nullptr);
+  for (int l = kCoarsest; l < L; ++l) g.part[l] = w + lay.fine_part + lay.part_off[l];
   return g;
 }
 
@@ -906,33 +924,49 @@ int expand_phase(const fc2t2_engine* e, int channels, const float* d_m_finest, f
     }
   }
   if (coarse) {
-    if (ph == PH_ALL)
+    // M grids of the coarse levels: the M2M chain here (ev_m[l] marks M_l),
+    // or given on entry (PH_DOWN: all-gathered by the caller)
+    if (ph == PH_ALL) {
       for (int l = L; l > lowest; --l) {
         st = cuda_status(fc2t2::m2m(e->rho, l, channels, G.M[l], G.M[l - 1], s), "expand m2m");
+        if (st == FC2T2_OK) st = cuda_status(cudaEventRecord(e->ev_m[l - 1], s), "expand ev_m");
         if (st != FC2T2_OK) return st;
       }
-    bool have = false;
+    } else {
+      st = cuda_status(cudaEventRecord(e->ev_m[lowest], s), "expand ev_m");
+      if (st != FC2T2_OK) return st;
+    }
+    // every coarse level's M2L, L_l = M2L_l(M_l), concurrently on its own
+    // stream (each with its own scratch); levels without interactions start
+    // from zero
     for (int l = lowest; l < L; ++l) {
       const Plan& p = e->plans.at(l).at(FC2T2_TABLE_FAR);
       int lb, le;
       level_slab(e, l, x0, x1, &lb, &le);
-      if (have) {
-        st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, G.L[l - 1], G.L[l], 0, s, lb, le),
+      cudaStream_t cl = serial ? s : e->cs[l & 1];
+      const int ml = ph == PH_ALL ? l : lowest;
+      st = cuda_status(cudaStreamWaitEvent(cl, e->ev_m[ml], 0), "expand wait M");
+      if (st != FC2T2_OK) return st;
+      if (p.max_list > 0)
+        st = level_m2l(e, channels, l, p, G.M[l], G.L[l], 0, G.part[l], cl, lb, le);
+      else
+        st = cuda_status(cudaMemsetAsync(G.L[l], 0, grid_floats(l, channels, e->PP) * sizeof(float),
+                                         cl),
+                         "expand zero");
+      if (st == FC2T2_OK) st = cuda_status(cudaEventRecord(e->ev_c[l], cl), "expand ev_c");
+      if (st != FC2T2_OK) return st;
+    }
+    // the L2L chain: L_l += L2L(L_{l-1}), coarsest first (fixed order)
+    st = cuda_status(cudaStreamWaitEvent(s, e->ev_c[lowest], 0), "expand wait M2L");
+    if (st != FC2T2_OK) return st;
+    for (int l = lowest + 1; l < L; ++l) {
+      int lb, le;
+      level_slab(e, l, x0, x1, &lb, &le);
+      st = cuda_status(cudaStreamWaitEvent(s, e->ev_c[l], 0), "expand wait M2L");
+      if (st == FC2T2_OK)
+        st = cuda_status(fc2t2::l2l(e->rho, l - 1, channels, G.L[l - 1], G.L[l], 1, s, lb, le),
                          "expand l2l");
-        if (st != FC2T2_OK) return st;
-      }
-      if (p.max_list > 0) {
-        st = level_m2l(e, channels, l, p, G.M[l], G.L[l], have ? 1 : 0, G.coarse_part, s, lb, le);
-        if (st != FC2T2_OK) return st;
-        have = true;
-      } else if (!have) {
-        // nothing at this level yet: the next L2L needs a zero grid
-        st = cuda_status(
-            cudaMemsetAsync(G.L[l], 0, grid_floats(l, channels, e->PP) * sizeof(float), s),
-            "expand zero");
-        if (st != FC2T2_OK) return st;
-        have = true;
-      }
+      if (st != FC2T2_OK) return st;
     }
     if (overlap) {
       st = cuda_status(cudaStreamWaitEvent(s, e->join, 0), "expand join");

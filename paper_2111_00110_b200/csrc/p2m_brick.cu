@@ -307,6 +307,136 @@ brick_scatter_kernel(const float* __restrict__ pts, const float* __restrict__ wt
   }
 }
 
+// K3r (levels <= 5, <= 1024 bricks): the same tile partition with
+// deterministic ranks and no fix-up sort.  Warp w of the 512-thread CTA (two
+// per SM, so one CTA's loads overlap the other's ranking) owns
+// tile points [128 w, 128 w + 128) and ranks them 32 at a time against the
+// warp's own 16-bit brick counters: a lane alone on its brick in the group
+// (counter read before and after the group's atomicAdds differ by one) takes
+// the old count; lanes sharing a brick (~40 % of the groups at 1024 bricks)
+// add their lane-order rank among those peers (__match_any_sync over the
+// clashing lanes only) -- deterministic whatever order the atomics ran in.  Then slot = tile start of the
+// brick + the counts of the brick in earlier warps + rank.
+constexpr int K3R_PER_WARP = 128;
+constexpr int K3R_THREADS = 512;                              // 2 CTAs per SM
+constexpr int K3R_TILE = K3R_PER_WARP * (K3R_THREADS / 32);  // 2048
+
+struct K3RSmem {
+  size_t pts, wts, key, wc, lstart, gbase, perm, total;
+};
+__host__ __device__ inline K3RSmem k3r_smem(int C, int nb) {
+  K3RSmem m;
+  size_t o = 0;
+  auto take = [&](size_t b) { const size_t r = o; o += (b + 15) & ~(size_t)15; return r; };
+  m.pts = take((size_t)K3R_TILE * 12);
+  m.wts = take((size_t)K3R_TILE * C * 4);
+  m.key = take((size_t)K3R_TILE * 4);
+  m.wc = take((size_t)(K3R_THREADS / 32) * nb * 2);    // packed 16-bit counters
+  m.lstart = take((size_t)nb * 4);
+  m.gbase = take((size_t)nb * 4);
+  m.perm = take((size_t)K3R_TILE * 2);
+  m.total = o;
+  return m;
+}
+
+__global__ void __launch_bounds__(K3R_THREADS)
+brick_scatter_rank_kernel(const float* __restrict__ pts, const float* __restrict__ wts, int C,
+                          int RS, int64_t n, int level, const uint32_t* __restrict__ cpre,
+                          const uint32_t* __restrict__ bstart, float* __restrict__ rec) {
+  extern __shared__ __align__(16) unsigned char sm3[];
+  constexpr int NW = K3R_THREADS / 32;
+  const BrickGeom g = brick_geom(level);
+  const K3RSmem L = k3r_smem(C, g.nb);
+  float* sp = reinterpret_cast<float*>(sm3 + L.pts);
+  float* sw = reinterpret_cast<float*>(sm3 + L.wts);
+  uint32_t* key = reinterpret_cast<uint32_t*>(sm3 + L.key);
+  uint32_t* wcw = reinterpret_cast<uint32_t*>(sm3 + L.wc);          // [NW][nb / 2] words
+  uint16_t* wc = reinterpret_cast<uint16_t*>(sm3 + L.wc);           // [NW][nb]
+  uint32_t* lstart = reinterpret_cast<uint32_t*>(sm3 + L.lstart);
+  uint32_t* gbase = reinterpret_cast<uint32_t*>(sm3 + L.gbase);
+  uint16_t* perm = reinterpret_cast<uint16_t*>(sm3 + L.perm);
+  __shared__ uint32_t warp_tot[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * K3R_TILE;
+  const int tn = (int)min((int64_t)K3R_TILE, n - t0);
+  stage_floats(sp, pts + 3 * t0, 3 * tn);
+  stage_floats(sw, wts + (int64_t)C * t0, C * tn);
+  const int nbw = (g.nb + 1) >> 1;   // counter words per warp
+  for (int i = threadIdx.x; i < NW * nbw; i += blockDim.x) wcw[i] = 0u;
+  for (int b = threadIdx.x; b < g.nb; b += blockDim.x)
+    gbase[b] = bstart[b] + cpre[(size_t)blockIdx.x * g.nb + b];
+  __syncthreads();
+  // 1. ranks within the warp's points, in index order
+  const unsigned lt = lanemask_lt();
+  uint32_t* myw = wcw + (size_t)w * nbw;
+  for (int grp = 0; grp < K3R_PER_WARP; grp += 32) {
+    const int tp = w * K3R_PER_WARP + grp + lane;
+    const bool ok = tp < tn;
+    const int b = ok ? point_brick(sp[3 * tp], sp[3 * tp + 1], sp[3 * tp + 2], g) : 0;
+    const uint32_t sh = (uint32_t)(b & 1) << 4;
+    const uint32_t pre = (myw[b >> 1] >> sh) & 0xffffu;   // only this warp writes its row
+    __syncwarp();
+    if (ok) atomicAdd(myw + (b >> 1), 1u << sh);
+    __syncwarp();
+    // more than one lane on this brick: rank the group in lane order
+    const bool clash = ok && ((myw[b >> 1] >> sh) & 0xffffu) != pre + 1;
+    const unsigned cm = __ballot_sync(0xffffffffu, clash);
+    uint32_t r = pre;
+    if (clash) r += (uint32_t)__popc(__match_any_sync(cm, b) & lt);
+    if (ok) key[tp] = ((uint32_t)b << 13) | r;
+    __syncwarp();
+  }
+  __syncthreads();
+  // 2. per brick: exclusive prefix over the warps (in place), tile starts
+  constexpr int BPT = 1024 / K3R_THREADS;   // bricks per thread (nb <= 1024)
+  uint32_t cnt[BPT], mine = 0;
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    const int b = threadIdx.x * BPT + k;
+    cnt[k] = 0;
+    if (b < g.nb) {
+      for (int q = 0; q < NW; ++q) {
+        const uint32_t v = wc[(size_t)q * (2 * nbw) + b];
+        wc[(size_t)q * (2 * nbw) + b] = (uint16_t)cnt[k];
+        cnt[k] += v;
+      }
+    }
+    mine += cnt[k];
+  }
+  uint32_t total;
+  uint32_t st = block_exclusive_scan(mine, warp_tot, total);
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    const int b = threadIdx.x * BPT + k;
+    if (b < g.nb) lstart[b] = st;
+    st += cnt[k];
+  }
+  __syncthreads();
+  // 3. sorted position of every point of the tile
+  for (int tp = threadIdx.x; tp < tn; tp += blockDim.x) {
+    const uint32_t k = key[tp];
+    const int bb = (int)(k >> 13);
+    perm[lstart[bb] + wc[(size_t)(tp / K3R_PER_WARP) * (2 * nbw) + bb] + (k & 8191u)] =
+        (uint16_t)tp;
+  }
+  __syncthreads();
+  // 4. brick runs out, coalesced
+  const int r4 = RS / 4;
+  for (int e = threadIdx.x; e < tn * r4; e += blockDim.x) {
+    const int s = r4 == 1 ? e : e / r4, f = e - s * r4;
+    const int tp = perm[s];
+    const int bb = (int)(key[tp] >> 13);
+    const size_t gs = (size_t)gbase[bb] + (s - lstart[bb]);
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = 4 * f + j;
+      v[j] = c < 3 ? sp[3 * tp + c] : (c < 3 + C ? sw[C * tp + c - 3] : 0.f);
+    }
+    reinterpret_cast<float4*>(rec)[gs * r4 + f] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 // ------------------------------------------------------------------- K4 ---
 // One CTA (CB threads) per brick; thread = cell of the brick, one channel at
 // a time.  The brick's records stream through shared memory in chunks of
@@ -493,8 +623,14 @@ int rec_floats(int C) { return 4 * ((3 + C + 3) / 4); }
 
 // points per K1/K3 tile: ~8 per brick (short runs for the in-order fix-up),
 // between 256 and 6144, and at most 96 KB of raw points + weights in smem
+bool rank_scatter(int level, int C) {
+  const BrickGeom g = brick_geom(level);
+  return g.nb <= 1024 && k3r_smem(C, g.nb).total <= 100 * 1024 && g.nb >= 64;
+}
+
 int brick_tile(int level, int C) {
   const BrickGeom g = brick_geom(level);
+  if (rank_scatter(level, C)) return K3R_TILE;
   const int cap = std::min(6144, 98304 / ((3 + C) * 4) / K13_THREADS * K13_THREADS);
   const int want = (8 * g.nb + K13_THREADS - 1) / K13_THREADS * K13_THREADS;
   return std::max(K13_THREADS, std::min(cap, want));
@@ -560,11 +696,15 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
   const int64_t nt = brick_tiles(n, level, C);
   if (nt > INT32_MAX / 2) return cudaErrorInvalidValue;
   const int RS = rec_floats(C);
-  const size_t sm3 = k3_smem(tile, C, g.nb).total;
+  const bool rk = rank_scatter(level, C);
+  const size_t sm3 = rk ? k3r_smem(C, g.nb).total : k3_smem(tile, C, g.nb).total;
   static unsigned long long attr = 0;
   if (attr_needed(attr)) {
     cudaError_t e = cudaFuncSetAttribute(brick_scatter_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(brick_scatter_rank_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
   }
   if (sm3 > 200 * 1024) return cudaErrorInvalidValue;
@@ -574,7 +714,11 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
   FC2T2_LAUNCH("brick_scan", s,
                brick_colscan_kernel<<<(g.nb + 7) / 8, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.tot));
   FC2T2_LAUNCH("brick_scan", s, brick_start_kernel<<<1, 1024, 0, s>>>(b.tot, g.nb, b.bstart));
-  if (n > 0)
+  if (n > 0 && rk)
+    FC2T2_LAUNCH("brick_scatter", s,
+                 brick_scatter_rank_kernel<<<(unsigned)nt, K3R_THREADS, sm3, s>>>(
+                     pts, w, C, RS, n, level, b.cnt, b.bstart, b.rec));
+  else if (n > 0)
     FC2T2_LAUNCH("brick_scatter", s,
                  brick_scatter_kernel<<<(unsigned)nt, K3_THREADS, sm3, s>>>(
                      pts, w, C, RS, n, level, tile, b.cnt, b.bstart, b.rec));
