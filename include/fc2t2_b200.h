@@ -281,11 +281,21 @@ int fc2t2_vol_forward_ex(int rho, int level, int colors, const float* d_l, const
 int fc2t2_vol_totals(int rho, int level, int colors, const float* d_l, const double* d_org,
                      const double* d_dir, int64_t R, const double* d_efit, uint32_t* d_n_alive,
                      double* d_totals, double* d_depth_final, void* stream);
+/* Backward pass B (volumetric_jvp, layers.py:483-544): per alive segment its
+ * cell key and a segment record of fc2t2_vol_record_floats(colors) floats
+ * (d_payload (A, rec)): line base + direction and the (1 + colors) x 5 power
+ * moments of the node-weighted adjoint densities.  fc2t2_vol_insert expands
+ * the records of every cell, in the stable key order of fc2t2_key_sort, and
+ * sums them into the moment grid (res^3, 1 + colors, PP) -- the
+ * _insert_moments of layers.py:144-153 without payload rows in memory. */
 int fc2t2_vol_payload(int rho, int level, int colors, const float* d_l, const double* d_org,
                       const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
                       const float* d_ybar, const uint32_t* d_alive_offsets,
                       const double* d_totals, const double* d_depth_final, const double* d_gl_x,
                       const double* d_gl_w, uint32_t* d_keys, float* d_payload, void* stream);
+int fc2t2_vol_record_floats(int colors);
+int fc2t2_vol_insert(int rho, int level, int colors, const float* d_rec, const int32_t* d_order,
+                     const int32_t* d_cell_start, float* d_m, void* stream);
 
 /* ---- training glue: trainer.py (reference trainer.py:70-152) ----
  * Losses (loss_and_tangent, trainer.py:70-105): diff = pred + bias - target

@@ -89,6 +89,8 @@ _SIGS = {
     "fc2t2_key_sort_workspace_size": (_sz, [_i32, _i64]),
     "fc2t2_key_sort": (_i32, [_i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
     "fc2t2_insert": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "fc2t2_vol_record_floats": (_i32, [_i32]),
+    "fc2t2_vol_insert": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "fc2t2_vol_gauss_nodes": (_i32, [_i32]),
     "fc2t2_vol_forward": (_i32, [_i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
                                  _vp, _vp]),

@@ -115,6 +115,17 @@ int fc2t2_insert(int rho, int level, int channels, const float* d_payload, const
 
 int fc2t2_vol_gauss_nodes(int rho) { return fc2t2::vol_gauss_nodes(rho); }
 
+int fc2t2_vol_record_floats(int colors) { return fc2t2::vol_record_floats(colors); }
+
+int fc2t2_vol_insert(int rho, int level, int colors, const float* d_rec, const int32_t* d_order,
+                     const int32_t* d_cell_start, float* d_m, void* stream) {
+  if (rho != 4) return rfail(FC2T2_EORDER, "the radiance layer is built for rho = 4");
+  if (colors < 1 || colors > 4) return rfail(FC2T2_EVALUE, "1..4 colour channels supported");
+  return rstatus(fc2t2::vol_insert(rho, level, colors, d_rec, d_order, d_cell_start, d_m,
+                                   (cudaStream_t)stream),
+                 "vol_insert");
+}
+
 int fc2t2_vol_forward(int rho, int level, int colors, const float* d_l, const double* d_org,
                       const double* d_dir, int64_t R, const double* d_efit, const double* d_bg,
                       float* d_rgb, double* d_depth_final, const uint32_t* d_seg_offsets,

@@ -156,6 +156,11 @@ cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double
 cudaError_t vol_totals(int rho, int level, int CC, const float* L, const double* org,
                        const double* dir, int64_t R, const double* efit, uint32_t* n_alive,
                        double* totals, double* depth_final, cudaStream_t s);
+// segment records (vol_record_floats(CC) floats each) expanded and summed per
+// cell in the key sort's order into M (res^3, 1 + CC, PP)
+int vol_record_floats(int CC);
+cudaError_t vol_insert(int rho, int level, int CC, const float* rec, const int32_t* order,
+                       const int32_t* cell_start, float* M, cudaStream_t s);
 cudaError_t vol_payload(int rho, int level, int CC, const float* L, const double* org,
                         const double* dir, int64_t R, const double* efit, const double* bg,
                         const float* ybar, const uint32_t* alive_offsets, const double* totals,

@@ -230,16 +230,13 @@ vol_totals_kernel(const float* __restrict__ L, int res, const double* __restrict
 // x dir: pay[ch][n] = sum_g wn[ch][g] mono_n(p(x_g)).  Each monomial is a
 // polynomial in x, mono_n(p(x)) = inv_fact[n] prod_a (base_a + x dir_a)^{n_a}
 // = sum_i c_{n,i} x^i (|n| <= RHO), so pay[ch][n] = sum_i c_{n,i} mu[ch][i] with
-// the power moments mu[ch][i] = sum_g wn[ch][g] x_g^i: ~1.5k instead of ~3.6k
-// FMAs per segment at rho 4 (same absolute rounding scale).  Rows go to
-// dst[ch * PP .. ] as float4.
+// the power moments mu[ch][i] = sum_g wn[ch][g] x_g^i.  A segment is therefore
+// fully described by the record {base, dir, mu} (VOL_REC floats): the
+// backward's walker writes records (not NCH x PP payload rows), and the
+// per-cell insertion expands them while it sums (vol_insert_kernel).
 template <int RHO, int NCH, int GNODES>
-__device__ __forceinline__ void segment_moments(const float base[3], const float dirf[3],
-                                                const float (&xs)[GNODES], const float* wn,
-                                                float* __restrict__ dst) {
-  constexpr MI<RHO> mi{};
-  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
-  float mu[NCH][RHO + 1];
+__device__ __forceinline__ void segment_power_moments(const float (&xs)[GNODES], const float* wn,
+                                                      float (&mu)[NCH][RHO + 1]) {
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
@@ -258,6 +255,16 @@ __device__ __forceinline__ void segment_moments(const float base[3], const float
       for (int ch = 0; ch < NCH; ++ch) w[ch] *= x;
     }
   }
+}
+
+// acc[ch][n - N0] += pay[ch][n] for n in [N0, N1) and every channel: the
+// segment's rows restricted to one slice of the coefficient index
+template <int RHO, int NCH, int N0, int N1>
+__device__ __forceinline__ void add_segment_rows(const float base[3], const float dirf[3],
+                                                 const float (&mu)[NCH][RHO + 1],
+                                                 float (&acc)[NCH][N1 - N0]) {
+  constexpr MI<RHO> mi{};
+  constexpr int P = MI<RHO>::P;
   // per-axis binomial polynomials Q[a][k][i] = coefficient of x^i in (b + x d)^k
   float Q[3][RHO + 1][RHO + 1];
 #pragma unroll
@@ -270,43 +277,36 @@ __device__ __forceinline__ void segment_moments(const float base[3], const float
         Q[a][k][i] = (i < k ? Q[a][k - 1][i] * base[a] : 0.f) +
                      (i > 0 ? Q[a][k - 1][i - 1] * dirf[a] : 0.f);
   }
-  float out[NCH][4];
 #pragma unroll
-  for (int n = 0; n < PP; ++n) {
-    if (n < P) {
-      const int n0 = mi.e0[n], n1 = mi.e1[n], n2 = mi.e2[n];
-      float c01[RHO + 1], c[RHO + 1];
+  for (int n = N0; n < N1 && n < P; ++n) {
+    const int n0 = mi.e0[n], n1 = mi.e1[n], n2 = mi.e2[n];
+    float c01[RHO + 1], c[RHO + 1];
 #pragma unroll
-      for (int i = 0; i <= RHO; ++i) c01[i] = c[i] = 0.f;
+    for (int i = 0; i <= RHO; ++i) c01[i] = c[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i <= RHO; ++i)
+#pragma unroll
+      for (int j = 0; j <= RHO; ++j)
+        if (i <= n0 && j <= n1) c01[i + j] = fmaf(Q[0][n0][i], Q[1][n1][j], c01[i + j]);
+#pragma unroll
+    for (int i = 0; i <= RHO; ++i)
+#pragma unroll
+      for (int j = 0; j <= RHO; ++j)
+        if (i <= n0 + n1 && j <= n2 && i + j <= RHO) c[i + j] = fmaf(c01[i], Q[2][n2][j], c[i + j]);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+      float v = 0.f;
 #pragma unroll
       for (int i = 0; i <= RHO; ++i)
-#pragma unroll
-        for (int j = 0; j <= RHO; ++j)
-          if (i <= n0 && j <= n1) c01[i + j] = fmaf(Q[0][n0][i], Q[1][n1][j], c01[i + j]);
-#pragma unroll
-      for (int i = 0; i <= RHO; ++i)
-#pragma unroll
-        for (int j = 0; j <= RHO; ++j)
-          if (i <= n0 + n1 && j <= n2 && i + j <= RHO) c[i + j] = fmaf(c01[i], Q[2][n2][j], c[i + j]);
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) {
-        float v = 0.f;
-#pragma unroll
-        for (int i = 0; i <= RHO; ++i)
-          if (i <= n0 + n1 + n2) v = fmaf(c[i], mu[ch][i], v);
-        out[ch][n & 3] = v * mi.inv_fact[n];
-      }
-    } else {
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch) out[ch][n & 3] = 0.f;
-    }
-    if ((n & 3) == 3) {
-#pragma unroll
-      for (int ch = 0; ch < NCH; ++ch)
-        *reinterpret_cast<float4*>(dst + ch * PP + (n - 3)) =
-            make_float4(out[ch][0], out[ch][1], out[ch][2], out[ch][3]);
+        if (i <= n0 + n1 + n2) v = fmaf(c[i], mu[ch][i], v);
+      acc[ch][n - N0] = __fadd_rn(acc[ch][n - N0], __fmul_rn(v, mi.inv_fact[n]));
     }
   }
+}
+
+// record floats: base 3 + dir 3 + NCH x (RHO + 1) power moments, 16-byte rows
+__host__ __device__ constexpr int vol_rec_floats(int rho, int nch) {
+  return (6 + nch * (rho + 1) + 3) / 4 * 4;
 }
 
 constexpr int VOL_THREADS = 128;
@@ -428,12 +428,65 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
         float xs[GN];
 #pragma unroll
         for (int g = 0; g < GN; ++g) xs[g] = (float)(half * (GL_X[g] + 1.0));
-        segment_moments<RHO, NCH, GN>(base, dirf, xs, wn, payload + item * NCH * PP);
+        float mu[NCH][RHO + 1];
+        segment_power_moments<RHO, NCH, GN>(xs, wn, mu);
+        constexpr int RV = vol_rec_floats(RHO, NCH);
+        float rv[RV];
+        rv[0] = base[0]; rv[1] = base[1]; rv[2] = base[2];
+        rv[3] = dirf[0]; rv[4] = dirf[1]; rv[5] = dirf[2];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+          for (int i = 0; i <= RHO; ++i) rv[6 + ch * (RHO + 1) + i] = mu[ch][i];
+#pragma unroll
+        for (int k = 6 + NCH * (RHO + 1); k < RV; ++k) rv[k] = 0.f;
+        float4* dst = reinterpret_cast<float4*>(payload + item * RV);
+#pragma unroll
+        for (int k = 0; k < RV / 4; ++k)
+          dst[k] = make_float4(rv[4 * k], rv[4 * k + 1], rv[4 * k + 2], rv[4 * k + 3]);
         ++item;
       }
       depth += send;
       return true;
     });
+  }
+}
+
+// Per (cell, channel), in the key sort's order: the segment records of the
+// cell expanded to payload rows and summed (the same float32 row values the
+// row-materialising version wrote and summed, without the NCH x PP rows in HBM)
+// Per (cell, channel), in the key sort's order: the cell's segment records
+// expanded to payload rows and summed -- the same float32 row values the
+// row-materialising version wrote and summed, without the NCH x PP rows in
+// HBM.  (Measured alternatives: three threads per cell splitting the
+// coefficient index, 3.6 ms vs 2.4 ms at config 4 -- 168 registers.)
+template <int RHO, int NCH>
+__global__ void __launch_bounds__(128)
+vol_insert_kernel(const float* __restrict__ rec, int64_t R3, const int32_t* __restrict__ order,
+                  const int32_t* __restrict__ cell_start, float* __restrict__ M) {
+  constexpr int PP = MI<RHO>::PP, RV = vol_rec_floats(RHO, NCH);
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < R3 * NCH;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = g / NCH;
+    const int ch = (int)(g - cell * NCH);
+    const int beg = cell_start[cell], end = cell_start[cell + 1];
+    float acc[1][PP];
+#pragma unroll
+    for (int j = 0; j < PP; ++j) acc[0][j] = 0.f;
+    for (int k = beg; k < end; ++k) {
+      const float* r = rec + (int64_t)order[k] * RV;
+      const float4 a = __ldg(reinterpret_cast<const float4*>(r));
+      const float2 b = __ldg(reinterpret_cast<const float2*>(r + 4));
+      const float base[3] = {a.x, a.y, a.z}, dirf[3] = {a.w, b.x, b.y};
+      float mu[1][RHO + 1];
+#pragma unroll
+      for (int i = 0; i <= RHO; ++i) mu[0][i] = __ldg(r + 6 + ch * (RHO + 1) + i);
+      add_segment_rows<RHO, 1, 0, PP>(base, dirf, mu, acc);
+    }
+#pragma unroll
+    for (int j = 0; j < PP; j += 4)
+      *reinterpret_cast<float4*>(M + g * PP + j) =
+          make_float4(acc[0][j], acc[0][j + 1], acc[0][j + 2], acc[0][j + 3]);
   }
 }
 
@@ -449,6 +502,19 @@ vol_payload_kernel(const float* __restrict__ L, int res, const double* __restric
 }  // namespace
 
 int vol_gauss_nodes(int rho) { return GN; }
+
+int vol_record_floats(int CC) { return vol_rec_floats(4, 1 + CC); }
+
+cudaError_t vol_insert(int rho, int level, int CC, const float* rec, const int32_t* order,
+                       const int32_t* cell_start, float* M, cudaStream_t s) {
+  if (rho != 4) return cudaErrorNotSupported;
+  constexpr int RHO = 4;
+  const int64_t res = (int64_t)1 << (level + 1), R3 = res * res * res;
+  FC2T2_VOL_DISPATCH(CC, FC2T2_LAUNCH("insert", s,
+      vol_insert_kernel<RHO, 1 + CC><<<grid_blocks(R3 * (1 + CC), 128, 148 * 64), 128, 0, s>>>(
+          rec, R3, order, cell_start, M)));
+  return cudaGetLastError();
+}
 
 cudaError_t vol_forward(int rho, int level, int CC, const float* L, const double* org,
                         const double* dir, int64_t R, const double* efit, const double* bg,

@@ -169,10 +169,12 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
 # ---------------------------------------------------------------- insertion ---
 
 def insert_and_expand(engine: Engine, keys: torch.Tensor, payload: torch.Tensor,
-                      channels: int) -> Accessor:
+                      channels: int, records: int | None = None) -> Accessor:
     """_insert_moments (reference layers.py:144-153): stable sort of the item
     cell keys, per-cell sums of the payload rows in sorted order (no atomics,
-    deterministic), then one cascade -- the one extra expansion of a JVP."""
+    deterministic), then one cascade -- the one extra expansion of a JVP.
+    With ``records`` (= colours) the items are radiance segment records,
+    expanded to rows inside the per-cell sum (fc2t2_vol_insert)."""
     n = int(keys.shape[0])
     lv = engine.levels
     R3 = level_resolution(lv) ** 3
@@ -184,8 +186,12 @@ def insert_and_expand(engine: Engine, keys: torch.Tensor, payload: torch.Tensor,
     _lib.call("fc2t2_key_sort", lv, _ptr(keys), n, _ptr(order), _ptr(start), _ptr(ws), ws_b,
               _stream())
     m = engine._empty_grid(lv, channels, "M")
-    _lib.call("fc2t2_insert", engine.rho, lv, channels, _ptr(payload), _ptr(order), _ptr(start),
-              _ptr(m.storage), _stream())
+    if records is not None:   # segment records expanded while summing (radiance layer)
+        _lib.call("fc2t2_vol_insert", engine.rho, lv, records, _ptr(payload), _ptr(order),
+                  _ptr(start), _ptr(m.storage), _stream())
+    else:
+        _lib.call("fc2t2_insert", engine.rho, lv, channels, _ptr(payload), _ptr(order),
+                  _ptr(start), _ptr(m.storage), _stream())
     out = engine.cascade_device(m.storage)
     grid = ExpansionGrid(level=lv, kind="L", storage=out, rho=engine.rho)
     return Accessor(grid, engine.table, engine.flops, flag=engine.flag)
@@ -568,11 +574,12 @@ def volumetric_jvp(y_bar, res: RenderResult) -> LayerGradients:
     G = int(_lib.lib().fc2t2_vol_gauss_nodes(eng.rho))
     gx, gw = _gauss_dev(G, dev)
     keys = torch.empty(max(A, 1), dtype=torch.int32, device=dev)
-    payload = torch.empty((max(A, 1), 1 + C, eng.PP), dtype=torch.float32, device=dev)
+    rec = torch.empty((max(A, 1), int(_lib.lib().fc2t2_vol_record_floats(C))),
+                      dtype=torch.float32, device=dev)
     _lib.call("fc2t2_vol_payload", eng.rho, eng.levels, C, _ptr(st), _ptr(org), _ptr(dirs), R,
               _ptr(efit), _ptr(bg), _ptr(yb), _ptr(offs), _ptr(totals), _ptr(dfin), _ptr(gx),
-              _ptr(gw), _ptr(keys), _ptr(payload), _stream())
-    back = insert_and_expand(eng, keys[:A], payload[:A], 1 + C)
+              _ptr(gw), _ptr(keys), _ptr(rec), _stream())
+    back = insert_and_expand(eng, keys[:A], rec[:A], 1 + C, records=C)
     src = res.dev["src"]
     val, p_bar = _source_adjoints(back, src)
     w_bar = val.clone()
