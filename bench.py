@@ -8,24 +8,30 @@ Gaussian alpha = 1000 (reference default kernel, DEFAULT_ALPHA[5]).
 
   value  (N+M) / device time of explicit_forward + explicit_jvp, inputs resident
          in HBM, CUDA events per step on the launching stream, L2 flushed
-         between steps (outside the events).
+         between steps (outside the events); the mean step.
   e2e    the same metric through the public API with pinned HOST torch tensors:
          H2D of p, w, q, y_bar and D2H of values, w_bar, p_bar, q_bar inside
          the timed region.
-  roofline  the dominant kernel (finest-level M2L) timed live by the library's
-         event profiler during the timed steps; algorithmic FLOPs per launch =
-         the reference's count (expansion.py:262) for far+near at level 5.
+  roofline_stages  per stage: algorithmic bytes (inputs once, outputs once)
+         and, for the separable M2L, executed FFMA flops; time from the
+         library's per-launch CUDA events; frac = max(bytes / HBM peak,
+         flops / FFMA peak) / time (peaks measured: MEASURED_PEAKS.json,
+         profiles/r2_peaks.json).
+  roofline  the stage with the largest serialised time in the committed ncu
+         capture (profiles/traffic.json), with its measured DRAM traffic.
   cpu_baseline / --impl reference  the oracle port (float64 NumPy restatement
-         of the reference, all host threads for BLAS) on a bounded sample.
+         of the reference, speed-faithful, all host threads for BLAS) on a
+         1/32 slice of the step.
 
-Multi-GPU (torchrun): weak scaling -- every rank owns a per-GPU shard of
-config-2 size of one global problem; the finest moment grids are summed with
-one NCCL all-reduce per expansion (paper_2111_00110_b200/parallel.py); timing
-is the max over ranks of the device time.
+Multi-GPU (torchrun) and --config 5: BASELINE config 5 as strong scaling --
+the global N = 2^24, M = 2^27, rho = 6, level 6 problem split over the ranks;
+every expansion runs the sharded cascade (parallel.py: reduce-scatter into
+x-slabs, 3-plane halos, slab cascade at every level, all-gathers); timing is
+the max over ranks of the device time.
 
-Secondary lines (rank 0, single GPU): configs 1, 3 and 4 (explicit 2D-lifted,
-root-implicit depth+normal, radiance) are measured in the same run and
-reported under "secondary" with their own metrics (points/s, rays/s).
+Secondary lines (rank 0, single GPU): configs 1, 3, 4 and one-GPU config 5
+(explicit 2D-lifted, root-implicit depth+normal, radiance, rho 6) with their
+own metrics (points/s, rays/s), and the fitting loops (training lines).
 """
 
 from __future__ import annotations
@@ -282,6 +288,7 @@ def seeded_direction(rng):
 # the forward of (p, w) and the backward of (q, y_bar).
 STAGE_GROUPS = {
     "l2p": ["l2p"],
+    "domain_check": ["domain_check"],
     "p2m": ["brick_hist", "brick_scan", "brick_scatter", "brick_p2m"],
     "m2l_finest": ["m2l_sep_pre", "m2l_sep_z", "m2l_sep_y", "m2l_sep_x", "m2l_sep_post",
                    "m2l_sep_post_l2l"],
@@ -336,6 +343,7 @@ def stage_rooflines(eng, prof, steps, N, M, hbm_peak, ffma_peak):
         "m2m": (2 * sum(4 * PP * ((2 ** (l + 1)) ** 3 + (2 ** l) ** 3) for l in range(3, L + 1)),
                 0, "fine read + coarse write per level"),
         "wgrad_recycle": (M * (12 + 4 + 12), 0, "12 B grad + 4 B y_bar in, 12 B q_bar out"),
+        "domain_check": (M * 12, 0, "12 B per query read"),
     }
     out = {}
     for st, names in STAGE_GROUPS.items():
@@ -857,7 +865,14 @@ def run_ours(args, rank: int, world: int) -> None:
                else "fallback (B200_PROFILING.md)")
     ffma_peak, ffma_src = ffma_peak_tflops()
     rl_stages = stage_rooflines(eng, prof, args.steps, N, M, hbm_peak, ffma_peak)
-    dom = max(rl_stages, key=lambda k: rl_stages[k]["ms_per_step"])
+    # dominant stage: the largest SERIALISED time (the committed ncu launch
+    # capture, profiles/traffic.json) -- live event spans of the concurrent
+    # cascade streams include waiting for SMs; live time when no capture
+    for st, e in rl_stages.items():
+        tr = measured_traffic(e["kernels"])
+        e["ncu_serial_ms_per_step"] = tr["serial_ms_per_step"] if tr else None
+    ser = {k: e["ncu_serial_ms_per_step"] for k, e in rl_stages.items() if e["ncu_serial_ms_per_step"]}
+    dom = max(ser, key=ser.get) if ser else max(rl_stages, key=lambda k: rl_stages[k]["ms_per_step"])
     d = rl_stages[dom]
     traffic = measured_traffic(d["kernels"])
     if d["bound"] == "hbm":

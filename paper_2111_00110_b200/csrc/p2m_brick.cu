@@ -7,9 +7,10 @@
 //   K1 brick_hist     CTA tiles of TILE consecutive points (6144 up to level
 //                     5); per tile a shared-memory histogram over bricks ->
 //                     cnt[tile][brick]
-//   S  brick_scan     per brick, the exclusive prefix of cnt over the tiles (a
-//                     warp per brick); brick_start = exclusive scan of the
-//                     brick totals (one CTA)
+//   S  brick_scan     per brick, the exclusive prefix of cnt over the tiles
+//                     (blocks of 32 bricks x 128 tiles read row-wise: segment
+//                     sums, their scan, the in-segment fill); brick_start =
+//                     exclusive scan of the brick totals (one CTA)
 //   K3 brick_scatter  a CTA copies its tile's points and weights into shared
 //                     memory (16-byte loads), finds every point's brick and an
 //                     arrival rank (smem atomics), counting-sorts the tile by
@@ -124,36 +125,75 @@ brick_hist_kernel(const float* __restrict__ pts, int64_t n, int level, int tile,
 }
 
 // ------------------------------------------------------------------- S ---
-// cnt[c][b] <- exclusive prefix over CTAs c; tot[b] = the column total.  One
-// warp per brick, 32 CTAs per step.
+// cnt[t][b] <- exclusive prefix over tiles t; tot[b] = the column total.
+// Blocks of 32 bricks x SEG_T tiles, read row-wise (128-byte coalesced rows):
+//   S1 brick_segsum   per block and brick the segment sum -> part[seg][b]
+//   S2 brick_segscan  per brick the exclusive scan of part over segments, tot
+//   S3 brick_segfill  per block: warps' sums, their prefix, then each warp
+//                     rewrites its SEG_T / 8 tiles with the running prefix
+constexpr int SEG_T = 128;   // tiles per segment (8 warps x 16)
+
 __global__ void __launch_bounds__(256)
-brick_colscan_kernel(uint32_t* __restrict__ cnt, int ncta, int nb, uint32_t* __restrict__ tot) {
+brick_segsum_kernel(const uint32_t* __restrict__ cnt, int nt, int nb, uint32_t* __restrict__ part) {
+  __shared__ uint32_t ws[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + lane, seg = blockIdx.y;
+  const int t0 = seg * SEG_T + w * (SEG_T / 8), t1 = min(nt, t0 + SEG_T / 8);
+  uint32_t s = 0;
+  if (b < nb)
+#pragma unroll 8
+    for (int t = t0; t < t1; ++t) s += cnt[(size_t)t * nb + b];
+  ws[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && b < nb) {
+    uint32_t tot = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += ws[q][lane];
+    part[(size_t)seg * nb + b] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+brick_segscan_kernel(uint32_t* __restrict__ part, int nseg, int nb, uint32_t* __restrict__ tot) {
   const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // a warp per brick
   if (b >= nb) return;
-  constexpr int V = 8;   // loads in flight per lane
   uint32_t carry = 0;
-  for (int c0 = 0; c0 < ncta; c0 += 32 * V) {
-    uint32_t v[V];
+  for (int g0 = 0; g0 < nseg; g0 += 32) {
+    const int g = g0 + lane;
+    const uint32_t v = g < nseg ? part[(size_t)g * nb + b] : 0u;
+    uint32_t x = v;
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const int c = c0 + k * 32 + lane;
-      v[k] = c < ncta ? cnt[(size_t)c * nb + b] : 0u;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-      const int c = c0 + k * 32 + lane;
-      uint32_t x = v[k];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (c < ncta) cnt[(size_t)c * nb + b] = carry + x - v[k];
-      carry += __shfl_sync(0xffffffffu, x, 31);
-    }
+    if (g < nseg) part[(size_t)g * nb + b] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
   if (lane == 0) tot[b] = carry;
+}
+
+__global__ void __launch_bounds__(256)
+brick_segfill_kernel(uint32_t* __restrict__ cnt, int nt, int nb, const uint32_t* __restrict__ part) {
+  __shared__ uint32_t ws[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + lane, seg = blockIdx.y;
+  const int t0 = seg * SEG_T + w * (SEG_T / 8), t1 = min(nt, t0 + SEG_T / 8);
+  uint32_t s = 0;
+  if (b < nb)
+#pragma unroll 8
+    for (int t = t0; t < t1; ++t) s += cnt[(size_t)t * nb + b];
+  ws[w][lane] = s;
+  __syncthreads();
+  if (b >= nb) return;
+  uint32_t run = part[(size_t)seg * nb + b];
+  for (int q = 0; q < w; ++q) run += ws[q][lane];
+  for (int t = t0; t < t1; ++t) {
+    const uint32_t v = cnt[(size_t)t * nb + b];
+    cnt[(size_t)t * nb + b] = run;
+    run += v;
+  }
 }
 
 // one CTA: brick_start = exclusive scan of the brick totals (nb + 1 entries)
@@ -613,7 +653,7 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
 }
 
 struct BrickWs {
-  uint32_t *cnt, *tot, *bstart;
+  uint32_t *cnt, *part, *tot, *bstart;
   float* rec;
 };
 
@@ -648,6 +688,7 @@ BrickWs brick_carve(void* ws, int level, int64_t n, int C) {
   auto take = [&](size_t bytes) { char* q = p; p += al256(bytes); return (void*)q; };
   BrickWs w;
   w.cnt = (uint32_t*)take((size_t)nt * g.nb * 4);
+  w.part = (uint32_t*)take((size_t)((nt + SEG_T - 1) / SEG_T) * g.nb * 4);
   w.tot = (uint32_t*)take((size_t)g.nb * 4);
   w.bstart = (uint32_t*)take((size_t)(g.nb + 1) * 4);
   w.rec = (float*)take((size_t)std::max<int64_t>(n, 1) * rec_floats(C) * 4);
@@ -681,7 +722,8 @@ bool p2m_brick_supported(int level, int C) {
 size_t p2m_brick_workspace(int level, int64_t n, int C) {
   const BrickGeom g = brick_geom(level);
   const int64_t nt = brick_tiles(n, level, C);
-  return al256((size_t)nt * g.nb * 4) + al256((size_t)g.nb * 4) + al256((size_t)(g.nb + 1) * 4) +
+  return al256((size_t)nt * g.nb * 4) + al256((size_t)((nt + SEG_T - 1) / SEG_T) * g.nb * 4) +
+         al256((size_t)g.nb * 4) + al256((size_t)(g.nb + 1) * 4) +
          al256((size_t)std::max<int64_t>(n, 1) * rec_floats(C) * 4);
 }
 
@@ -711,8 +753,14 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
   FC2T2_LAUNCH("brick_hist", s,
                brick_hist_kernel<<<(unsigned)nt, K13_THREADS, g.nb * 4, s>>>(pts, n, level, tile,
                                                                             b.cnt, flag));
+  const int nseg = (int)((nt + SEG_T - 1) / SEG_T);
+  const dim3 sgrid((unsigned)((g.nb + 31) / 32), (unsigned)nseg);
   FC2T2_LAUNCH("brick_scan", s,
-               brick_colscan_kernel<<<(g.nb + 7) / 8, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.tot));
+               brick_segsum_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part));
+  FC2T2_LAUNCH("brick_scan", s,
+               brick_segscan_kernel<<<(g.nb + 7) / 8, 256, 0, s>>>(b.part, nseg, g.nb, b.tot));
+  FC2T2_LAUNCH("brick_scan", s,
+               brick_segfill_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part));
   FC2T2_LAUNCH("brick_scan", s, brick_start_kernel<<<1, 1024, 0, s>>>(b.tot, g.nb, b.bstart));
   if (n > 0 && rk)
     FC2T2_LAUNCH("brick_scatter", s,

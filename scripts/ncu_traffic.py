@@ -10,15 +10,15 @@ with a cold cache, so these are upper bounds for the L2-resident stages)."""
 import csv, io, json, re, subprocess, sys
 
 MAP = [  # (regex on the ncu kernel name, library profile label)
-    (r"l2p_(warp_)?kernel", "l2p"), (r"p2m_sorted_kernel", "p2m"),
-    (r"brick_hist_kernel", "brick_hist"), (r"brick_(colsum|start|offsets)_kernel", "brick_scan"),
-    (r"brick_scatter_kernel", "brick_scatter"), (r"brick_p2m_kernel", "brick_p2m"),
+    (r"l2p_(warp_)?kernel", "l2p"), (r"vol_insert_kernel", "insert"), (r"insert_(sorted|heavy)_kernel", "insert"), (r"p2m_sorted_kernel", "p2m"),
+    (r"brick_hist_kernel", "brick_hist"), (r"brick_(colscan|segsum|segscan|segfill|start)_kernel", "brick_scan"),
+    (r"brick_scatter(_rank)?_kernel", "brick_scatter"), (r"brick_p2m_kernel", "brick_p2m"),
     (r"cell_keys_kernel", "cell_keys"), (r"place_kernel", "sort_place"),
     (r"segment_sort_\w+_kernel", "sort_segments"), (r"scan_\w+_kernel", "scan"),
     (r"sep_pre_kernel", "m2l_sep_pre"), (r"sep_post_kernel", "m2l_sep_post_l2l"),
     (r"sep_pass_kernel<\d+, 0", "m2l_sep_z"), (r"sep_pass_kernel<\d+, 1", "m2l_sep_y"),
-    (r"sep_pass_kernel<\d+, 2", "m2l_sep_x"), (r"m2l_tc_kernel", "m2l_tc"),
-    (r"m2l_ffma_kernel", "m2l_ffma"), (r"m2l_reduce_kernel", "m2l_reduce"),
+    (r"sep_pass_kernel<\d+, 2", "m2l_sep_x"), (r"m2l_tc_kernel", "m2l_tc_L4"),
+    (r"m2l_ffma_kernel", "m2l_L3"), (r"m2l_reduce_kernel", "m2l_reduce"),
     (r"absmax_kernel", "m2l_absmax"), (r"split_\w+_kernel", "m2l_split"),
     (r"l2l_kernel", "l2l"), (r"m2m_kernel", "m2m"), (r"weighted_grad_kernel", "wgrad_recycle"),
     (r"domain_check_kernel", "domain_check"),
