@@ -113,6 +113,7 @@ struct SepParams {
   float pre[RHO + 1][RHO + 1];
   float post[RHO + 1][RHO + 1];
   float conv[7][RHO + 1][RHO + 1];  // K(d) for d = -3..3, [out][in]
+  float kt[RHO + 1][7][8];          // the passes' shared-memory layout: kt[i][d][j] = conv[d][j][i]
 };
 
 namespace {
@@ -283,55 +284,68 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
 #pragma unroll
       for (int q = 0; q < NQ; ++q) v[q] = sm[(le * NQ + q) * kLines + lane];
     }
-    float k[7][NOUT];
+    // K(d) columns one d at a time (NOUT live coefficient registers); per
+    // accumulator the FMAs still run over d ascending (unchanged sums)
     const float4* kc = reinterpret_cast<const float4*>(Kt + i * 56);
 #pragma unroll
-    for (int d = 0; d < 7; ++d) {
-      const float4 lo = kc[2 * d];
+    for (int d = -3; d <= 3; ++d) {
+      float k[NOUT];
+      const float4 lo = kc[2 * (d + 3)];
       const float lo_[4] = {lo.x, lo.y, lo.z, lo.w};
 #pragma unroll
-      for (int j = 0; j < NOUT && j < 4; ++j) k[d][j] = lo_[j];
+      for (int j = 0; j < NOUT && j < 4; ++j) k[j] = lo_[j];
       if constexpr (NOUT > 4) {
-        const float4 hi = kc[2 * d + 1];
+        const float4 hi = kc[2 * (d + 3) + 1];
         const float hi_[4] = {hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-        for (int j = 4; j < NOUT; ++j) k[d][j] = hi_[j - 4];
+        for (int j = 4; j < NOUT; ++j) k[j] = hi_[j - 4];
       }
-    }
 #pragma unroll
-    for (int w = 0; w < POS; ++w) {
-#pragma unroll
-      for (int kk = 0; kk < 6; ++kk) {
-        const int d = kk - 2 - (w & 1);
+      for (int w = 0; w < POS; ++w) {
+        // even positions take d in -2..3, odd ones -3..2
+        if (d < -2 - (w & 1) || d > 3 - (w & 1)) continue;
         const float x = v[w + OFF + d];
 #pragma unroll
-        for (int j = 0; j < NOUT; ++j) acc[w][j] = fmaf(k[d + 3][j], x, acc[w][j]);
+        for (int j = 0; j < NOUT; ++j) acc[w][j] = fmaf(k[j], x, acc[w][j]);
       }
     }
   }
+  // 32-bit offsets from `out` (a channel block holds < 2^31 floats); the
+  // positions are pos_stride apart
+  int ob[NOUT];
 #pragma unroll
-  for (int w = 0; w < POS; ++w) {
-    if (w < nvalid) {
+  for (int j = 0; j < NOUT; ++j) ob[j] = oe[j] * (int)plane;
+  const int ps = (int)pos_stride;
+  if (nvalid == POS) {
 #pragma unroll
-      for (int j = 0; j < NOUT; ++j) {
-        out[(int64_t)oe[j] * plane + w * pos_stride] = acc[w][j];
+    for (int w = 0; w < POS; ++w)
+#pragma unroll
+      for (int j = 0; j < NOUT; ++j) out[ob[j] + w * ps] = acc[w][j];
+  } else {
+#pragma unroll
+    for (int w = 0; w < POS; ++w)
+      if (w < nvalid) {
+#pragma unroll
+        for (int j = 0; j < NOUT; ++j) out[ob[j] + w * ps] = acc[w][j];
       }
-    }
   }
 }
 
-// tile geometry decoded from a linear tile index
+// tile geometry from the 3-D grid: x = line tile, y = position tile,
+// z = (channel * R1 + partition) * res + fixed plane (res = 2^lres)
 struct Tile {
   int ch, part, fixed, line0, pos0;
 };
-__device__ __forceinline__ Tile decode_tile(int64_t t, int R1, int res, int line_lo, int nlt,
-                                            int pos_lo, int npt, int POS) {
+template <int R1>
+__device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, int POS) {
   Tile r;
-  r.line0 = line_lo + (int)(t % nlt) * kLines; t /= nlt;
-  r.pos0 = pos_lo + (int)(t % npt) * POS; t /= npt;
-  r.fixed = (int)(t % res); t /= res;
-  r.part = (int)(t % R1);
-  r.ch = (int)(t / R1);
+  r.line0 = line_lo + (int)blockIdx.x * kLines;
+  r.pos0 = pos_lo + (int)blockIdx.y * POS;
+  const int z = (int)blockIdx.z;
+  r.fixed = z & ((1 << lres) - 1);
+  const int cp = z >> lres;
+  r.part = cp % R1;
+  r.ch = cp / R1;
   return r;
 }
 
@@ -447,9 +461,8 @@ __device__ __forceinline__ uint32_t window_bytes(int part) {
 // The window comes from one TMA tensor copy issued by thread 0.
 template <int RHO, int PASS, int POS>
 __global__ void __launch_bounds__(32 * (RHO + 1))
-sep_pass_kernel(float* __restrict__ out, int res, int line_lo, int nlt, int pos_lo, int npt,
-                int pos_end, const __grid_constant__ SepParams<RHO> prm,
-                const __grid_constant__ SepMaps maps) {
+sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos_lo, int pos_end,
+                const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps) {
   using I = SepIdx<RHO>;
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(
@@ -459,7 +472,7 @@ sep_pass_kernel(float* __restrict__ out, int res, int line_lo, int nlt, int pos_
   uint64_t* bar = reinterpret_cast<uint64_t*>(Kt + 7 * 8 * R1);
   const int64_t plane = (int64_t)res * res * res;
   const int out_entries = PASS == PASS_X ? I::P : I::T;
-  const Tile T = decode_tile(blockIdx.x, R1, res, line_lo, nlt, pos_lo, npt, POS);
+  const Tile T = decode_tile<R1>(lres, line_lo, pos_lo, POS);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
   {
     if (threadIdx.x == 0) {
@@ -479,11 +492,9 @@ sep_pass_kernel(float* __restrict__ out, int res, int line_lo, int nlt, int pos_
         tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(T.part, 0), T.ch * R1, bar_s);
     }
   }
-  // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads)
-  for (int t = threadIdx.x; t < 7 * 8 * R1; t += blockDim.x) {
-    const int j = t & 7, d = (t >> 3) % 7, i = t / 56;
-    Kt[t] = j < R1 ? prm.conv[d][j][i] : 0.f;
-  }
+  // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads),
+  // laid out on the host
+  for (int t = threadIdx.x; t < 7 * 8 * R1; t += blockDim.x) Kt[t] = (&prm.kt[0][0][0])[t];
   {
     __syncthreads();   // the barrier init is visible before anyone waits on it
     asm volatile(
@@ -507,6 +518,9 @@ SepParams<RHO> to_params(const double* pre, const double* post, const double* co
       p.post[i][j] = (float)post[i * R1 + j];
       for (int d = 0; d < 7; ++d) p.conv[d][i][j] = (float)conv[(d * R1 + i) * R1 + j];
     }
+  for (int i = 0; i < R1; ++i)
+    for (int d = 0; d < 7; ++d)
+      for (int j = 0; j < 8; ++j) p.kt[i][d][j] = j < R1 ? p.conv[d][j][i] : 0.f;
   return p;
 }
 
@@ -571,8 +585,10 @@ cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int lin
                             cudaStream_t s) {
   const int nlt = (line_hi - line_lo + kLines - 1) / kLines;
   const int npt = (pos_hi - pos_lo + POS - 1) / POS;
-  const int64_t blocks = (int64_t)nlt * npt * res * (RHO + 1) * C;
-  if (blocks <= 0) return cudaSuccess;
+  if ((int64_t)nlt * npt * res * (RHO + 1) * C <= 0) return cudaSuccess;
+  int lres = 0;
+  while ((1 << lres) < res) ++lres;
+  const dim3 grid((unsigned)nlt, (unsigned)npt, (unsigned)(res * (RHO + 1) * C));
   constexpr int smem = pass_smem_floats<RHO, PASS, POS>() * (int)sizeof(float);
   static unsigned long long configured = 0;
   if (smem > 48 * 1024 && attr_needed(configured))
@@ -582,8 +598,8 @@ cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int lin
   std::memset(&maps, 0, sizeof(maps));
   if (!encode_maps<RHO, PASS, POS>(maps, in, res, C)) return cudaErrorNotSupported;
   FC2T2_LAUNCH(name, s,
-               sep_pass_kernel<RHO, PASS, POS><<<(unsigned)blocks, 32 * (RHO + 1), smem, s>>>(
-                   out, res, line_lo, nlt, pos_lo, npt, pos_hi, prm, maps));
+               sep_pass_kernel<RHO, PASS, POS><<<grid, 32 * (RHO + 1), smem, s>>>(
+                   out, res, lres, line_lo, pos_lo, pos_hi, prm, maps));
   return cudaGetLastError();
 }
 
