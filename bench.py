@@ -721,7 +721,7 @@ def run_ours(args, rank: int, world: int) -> None:
     from paper_2111_00110_b200.parallel import (DeviceBackend, explicit_forward_sharded,
                                                 explicit_jvp_sharded)
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     N, M = (CFG["N"], CFG["M"]) if not args.small else (1 << 16, 1 << 20)
@@ -951,7 +951,7 @@ def run_scaling(args, rank: int, world: int) -> None:
     from paper_2111_00110_b200.layers import explicit_forward, explicit_jvp
     from paper_2111_00110_b200.parallel import DeviceBackend, shard_range, sharded, slab_range
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     C5 = dict(CFG5)
@@ -1053,7 +1053,7 @@ def run_scaling(args, rank: int, world: int) -> None:
                    "l2": "inputs 2.4 GB > 126 MB L2, and a 256 MB L2 flush between steps",
                    "parallelism": (f"dp{world}: reduce-scatter + 3-plane halo + slab cascade "
                                    f"at every level + all-gathers "
-                                   f"({'NCCL' if world > 1 else 'single GPU'})"),
+                                   f"({dist.get_backend().upper() if world > 1 else 'single GPU'})"),
                    "slab_cascade_no_replication": bool(split)},
         "e2e": {"value": (N + M) / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
@@ -1064,6 +1064,15 @@ def run_scaling(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
+def _local_device() -> int:
+    """This rank's GPU: LOCAL_RANK, or LOCAL_RANK modulo the visible GPUs when
+    more ranks than GPUs run (functional check of the sharded path only)."""
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    n = torch.cuda.device_count()
+    return local % n if n else local
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -1072,8 +1081,10 @@ def main():
         import torch.distributed as dist
         if args.impl == "ours":
             import torch
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-            dist.init_process_group("nccl")
+            torch.cuda.set_device(_local_device())
+            # one process per GPU over NCCL (NVLink); with fewer GPUs than ranks
+            # (a functional check on one GPU) gloo stages through the host
+            dist.init_process_group("nccl" if torch.cuda.device_count() >= world else "gloo")
         else:
             dist.init_process_group("gloo")
     try:
