@@ -477,8 +477,10 @@ class Engine:
         return self._flag
 
     def aux_stream(self) -> torch.cuda.Stream:
-        """A second stream for work that only depends on a layer's inputs
-        (the query sort the backward needs, started by the forward)."""
+        """A second stream for short kernels that only depend on a layer's
+        inputs (the forward's query domain check, the backward's recycled
+        q_bar): they overlap the P2M on the caller's stream, which joins the
+        aux stream before anything reads their results."""
         if getattr(self, "_aux", None) is None:
             self._aux = torch.cuda.Stream(device=_device())
         return self._aux

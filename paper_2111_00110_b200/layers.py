@@ -143,8 +143,17 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     if is_host_tensor(q):
         return _explicit_forward_host(engine, sources, q)
     qd = to_device(q, 3, points=True)
-    engine.flag.check_points(qd)
-    acc, checked = _expand_checked(engine, sources.p, sources.w)
+    # the query domain check overlaps the source P2M (aux stream); the
+    # caller's stream joins it before the flag mark
+    cs = torch.cuda.current_stream()
+    aux = engine.aux_stream()
+    aux.wait_stream(cs)
+    with torch.cuda.stream(aux):
+        engine.flag.check_points(qd)
+    m = engine.p2m_device(sources.p, sources.w)
+    cs.wait_stream(aux)
+    checked = engine.flag.mark()
+    acc = engine.accessor_from_moments(m.storage)
     r = acc.eval_device(qd, _lib.L2P_VALUE | _lib.L2P_GRAD)
     engine.flag.raise_if_set("source/query", checked)
     return ExplicitResult(values=like_input(r["value"], q), accessor=acc, q=q, sources=sources,
@@ -157,9 +166,17 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     eng, qd, src = res.engine, res.q_dev, res.sources
     checked = eng.flag.mark()           # p and q were checked by the forward
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    q_bar = _weighted_grad(res.q_grad, yb)
+    # q_bar from the stored gradient on the aux stream, beside the query P2M;
+    # the caller's stream joins it before returning
+    cs = torch.cuda.current_stream()
+    aux = eng.aux_stream()
+    aux.wait_stream(cs)
+    with torch.cuda.stream(aux):
+        q_bar = _weighted_grad(res.q_grad, yb)
+    q_bar.record_stream(cs)             # the caller uses it on its stream
     back = eng.expand_device(qd, yb)
     out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
+    cs.wait_stream(aux)
     eng.flag.raise_if_set("source/query", checked)
     ref = y_bar
     return LayerGradients(w_bar=like_input(out["value"], ref), p_bar=like_input(out["wgrad"], ref),
