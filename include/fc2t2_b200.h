@@ -135,6 +135,14 @@ size_t fc2t2_p2m_points_workspace_size(const fc2t2_engine* e, int channels, int6
 int fc2t2_p2m_points(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
                      int64_t n, float* d_m_finest, int32_t* d_flag, void* d_ws, size_t ws_bytes,
                      void* stream);
+/* The same in two phases on one workspace: phase 1 = the partition of the
+ * points (counts and brick starts; reads only d_pts, sets FLAG_DOMAIN),
+ * phase 2 = records + per-brick sums (needs d_w and a workspace prepared by
+ * phase 1 for the same points); 3 = both.  Lets a caller partition points
+ * early (the explicit backward's queries, beside the forward's tail). */
+int fc2t2_p2m_points_phase(const fc2t2_engine* e, int channels, const float* d_pts,
+                           const float* d_w, int64_t n, float* d_m_finest, int32_t* d_flag,
+                           void* d_ws, size_t ws_bytes, int phase, void* stream);
 
 /* ---- stages (expansion.py:186-264) ---- */
 /* d_order NULL: d_pts / d_w are already in cell-sorted order */

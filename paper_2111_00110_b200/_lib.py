@@ -55,6 +55,7 @@ _SIGS = {
     "fc2t2_p2m": (_i32, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fc2t2_p2m_points_workspace_size": (_sz, [_vp, _i32, _i64]),
     "fc2t2_p2m_points": (_i32, [_vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "fc2t2_p2m_points_phase": (_i32, [_vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _sz, _i32, _vp]),
     "fc2t2_m2m": (_i32, [_vp, _i32, _i32, _vp, _vp, _vp]),
     "fc2t2_l2l": (_i32, [_vp, _i32, _i32, _vp, _vp, _i32, _vp]),
     "fc2t2_m2l_issued_flops": (ct.c_double, [_vp, _i32, _i32, _i32]),

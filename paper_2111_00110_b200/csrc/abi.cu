@@ -633,27 +633,39 @@ size_t fc2t2_p2m_points_workspace_size(const fc2t2_engine* e, int channels, int6
          256 + 4 * (size_t)(R + 1) + 256;
 }
 
-int fc2t2_p2m_points(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
-                     int64_t n, float* d_m_finest, int32_t* d_flag, void* d_ws, size_t ws_bytes,
-                     void* stream) {
+int fc2t2_p2m_points_phase(const fc2t2_engine* e, int channels, const float* d_pts,
+                           const float* d_w, int64_t n, float* d_m_finest, int32_t* d_flag,
+                           void* d_ws, size_t ws_bytes, int phase, void* stream) {
   if (!e || channels < 1 || n < 0 || n > INT32_MAX) return fail(FC2T2_EVALUE, "bad p2m arguments");
+  if (phase < 1 || phase > 3) return fail(FC2T2_EVALUE, "p2m phase must be 1, 2 or 3");
   if (ws_bytes < fc2t2_p2m_points_workspace_size(e, channels, n))
     return fail(FC2T2_EWORKSPACE, "p2m workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
   if (fc2t2::p2m_brick_supported(e->levels, channels))
     return cuda_status(fc2t2::p2m_brick(e->rho, e->levels, channels, d_pts, d_w, n, d_m_finest,
-                                        d_flag, d_ws, ws_bytes, s),
+                                        d_flag, d_ws, ws_bytes, s, phase),
                        "p2m_points");
+  // level >= 7: the stable cell sort (points only) then the gather P2M
   const size_t sw = fc2t2::cell_sort_workspace(e->levels, n);
   char* p = (char*)d_ws + ((sw + 255) & ~(size_t)255);
   int32_t* order = (int32_t*)p;
   int32_t* start = (int32_t*)(p + ((4 * (size_t)std::max<int64_t>(n, 1) + 255) & ~(size_t)255));
-  int st = cuda_status(fc2t2::cell_sort(e->levels, d_pts, n, order, start, d_flag, d_ws, sw, s),
-                       "p2m_points sort");
-  if (st != FC2T2_OK) return st;
+  if (phase & 1) {
+    int st = cuda_status(fc2t2::cell_sort(e->levels, d_pts, n, order, start, d_flag, d_ws, sw, s),
+                         "p2m_points sort");
+    if (st != FC2T2_OK) return st;
+  }
+  if (!(phase & 2)) return FC2T2_OK;
   return cuda_status(fc2t2::p2m_sorted(e->rho, e->levels, channels, d_pts, d_w, order, start,
                                        d_m_finest, s),
                      "p2m_points");
+}
+
+int fc2t2_p2m_points(const fc2t2_engine* e, int channels, const float* d_pts, const float* d_w,
+                     int64_t n, float* d_m_finest, int32_t* d_flag, void* d_ws, size_t ws_bytes,
+                     void* stream) {
+  return fc2t2_p2m_points_phase(e, channels, d_pts, d_w, n, d_m_finest, d_flag, d_ws, ws_bytes, 3,
+                                stream);
 }
 
 int fc2t2_m2m(const fc2t2_engine* e, int channels, int fine_level, const float* d_fine,

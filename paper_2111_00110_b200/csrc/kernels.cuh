@@ -26,8 +26,12 @@ cudaError_t exclusive_scan(const uint32_t* in, uint32_t* out, int64_t n, uint32_
 // 8 x 8 x (4|8) cell bricks + one CTA per brick (levels 2..6, C <= 8)
 bool p2m_brick_supported(int level, int C);
 size_t p2m_brick_workspace(int level, int64_t n, int C);
+// phases: P2M_PREPARE (partition counts, points only) and P2M_FINISH (records,
+// per-brick sums; needs the weights and the prepared workspace)
+enum { P2M_PREPARE = 1, P2M_FINISH = 2, P2M_ALL = 3 };
 cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* w, int64_t n,
-                      float* M, int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s);
+                      float* M, int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s,
+                      int phase = P2M_ALL);
 
 // expand.cu --------------------------------------------------------------
 // float32 sums of each cell's points in the stable sort's index order

@@ -728,7 +728,8 @@ size_t p2m_brick_workspace(int level, int64_t n, int C) {
 }
 
 cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* w, int64_t n,
-                      float* M, int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s) {
+                      float* M, int32_t* flag, void* ws, size_t ws_bytes, cudaStream_t s,
+                      int phase) {
   if (!p2m_brick_supported(level, C) || n < 0 || n > (int64_t)UINT32_MAX - 1)
     return cudaErrorNotSupported;
   if (ws_bytes < p2m_brick_workspace(level, n, C)) return cudaErrorInvalidValue;
@@ -750,6 +751,7 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
     if (e != cudaSuccess) return e;
   }
   if (sm3 > 200 * 1024) return cudaErrorInvalidValue;
+  if (phase & P2M_PREPARE) {
   FC2T2_LAUNCH("brick_hist", s,
                brick_hist_kernel<<<(unsigned)nt, K13_THREADS, g.nb * 4, s>>>(pts, n, level, tile,
                                                                             b.cnt, flag));
@@ -762,6 +764,8 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
   FC2T2_LAUNCH("brick_scan", s,
                brick_segfill_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part));
   FC2T2_LAUNCH("brick_scan", s, brick_start_kernel<<<1, 1024, 0, s>>>(b.tot, g.nb, b.bstart));
+  }
+  if (!(phase & P2M_FINISH)) return cudaGetLastError();
   if (n > 0 && rk)
     FC2T2_LAUNCH("brick_scatter", s,
                  brick_scatter_rank_kernel<<<(unsigned)nt, K3R_THREADS, sm3, s>>>(

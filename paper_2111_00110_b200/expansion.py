@@ -531,18 +531,37 @@ class Engine:
                   _ptr(self.flag.t), _ptr(ws), int(ws_bytes), _stream())
         return order, start
 
-    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor) -> ExpansionGrid:
+    def p2m_prepare(self, pts: torch.Tensor, channels: int) -> dict:
+        """Phase 1 of P2M on the current stream: the brick partition of the
+        points (reads only pts; sets the domain flag).  The returned handle
+        goes to ``p2m_device(pts, w, prepared=...)`` for the same points."""
+        n = int(pts.shape[0])
+        h = self.handle
+        ws_bytes = int(_lib.lib().fc2t2_p2m_points_workspace_size(h, channels, n))
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=pts.device)
+        _lib.call("fc2t2_p2m_points_phase", h, channels, _ptr(pts), _ptr(None), n, _ptr(None),
+                  _ptr(self.flag.t), _ptr(ws), ws_bytes, 1, _stream())
+        return {"ws": ws, "n": n, "C": int(channels)}
+
+    def p2m_device(self, pts: torch.Tensor, w: torch.Tensor, prepared: dict | None = None
+                   ) -> ExpansionGrid:
         """P2M straight from the caller's point order (fc2t2_p2m_points: a
         deterministic brick partition + per-cell sums in index order); sets
-        the domain flag for points outside (-1, 1)^3."""
+        the domain flag for points outside (-1, 1)^3.  With ``prepared``
+        (p2m_prepare of the same points) only phase 2 runs."""
         C = int(w.shape[1])
         n = int(pts.shape[0])
         grid = self._empty_grid(self.levels, C, "M")
         h = self.handle
-        ws_bytes = int(_lib.lib().fc2t2_p2m_points_workspace_size(h, C, n))
-        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=pts.device)
-        _lib.call("fc2t2_p2m_points", h, C, _ptr(pts), _ptr(w), n, _ptr(grid.storage),
-                  _ptr(self.flag.t), _ptr(ws), ws_bytes, _stream())
+        if prepared is not None and prepared["n"] == n and prepared["C"] == C:
+            ws = prepared["ws"]
+            _lib.call("fc2t2_p2m_points_phase", h, C, _ptr(pts), _ptr(w), n, _ptr(grid.storage),
+                      _ptr(self.flag.t), _ptr(ws), int(ws.numel()), 2, _stream())
+        else:
+            ws_bytes = int(_lib.lib().fc2t2_p2m_points_workspace_size(h, C, n))
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=pts.device)
+            _lib.call("fc2t2_p2m_points", h, C, _ptr(pts), _ptr(w), n, _ptr(grid.storage),
+                      _ptr(self.flag.t), _ptr(ws), ws_bytes, _stream())
         self.flops.add("p2m", flops.p2m_flops(n, self.rho, self.P))
         return grid
 

@@ -49,6 +49,7 @@ class ExplicitResult:
     engine: Engine
     q_dev: torch.Tensor = None
     q_grad: torch.Tensor = None   # (M, C, 3) grad f at q, stored for the backward
+    q_ready: object = None        # event: q_dev valid (the backward partitions q early)
 
 
 # q_bar recycling ("expansion recycling"): the forward L2P at q
@@ -148,6 +149,7 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     cs = torch.cuda.current_stream()
     aux = engine.aux_stream()
     aux.wait_stream(cs)
+    q_ready = cs.record_event()
     with torch.cuda.stream(aux):
         engine.flag.check_points(qd)
     m = engine.p2m_device(sources.p, sources.w)
@@ -157,7 +159,7 @@ def explicit_forward(engine: Engine, sources: SourceSet, q) -> ExplicitResult:
     r = acc.eval_device(qd, _lib.L2P_VALUE | _lib.L2P_GRAD)
     engine.flag.raise_if_set("source/query", checked)
     return ExplicitResult(values=like_input(r["value"], q), accessor=acc, q=q, sources=sources,
-                          engine=engine, q_dev=qd, q_grad=r["grad"])
+                          engine=engine, q_dev=qd, q_grad=r["grad"], q_ready=q_ready)
 
 
 def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
@@ -166,15 +168,27 @@ def explicit_jvp(y_bar, res: ExplicitResult) -> LayerGradients:
     eng, qd, src = res.engine, res.q_dev, res.sources
     checked = eng.flag.mark()           # p and q were checked by the forward
     yb = to_device(y_bar).reshape(qd.shape[0], -1).contiguous()
-    # q_bar from the stored gradient on the aux stream, beside the query P2M;
-    # the caller's stream joins it before returning
+    # On the aux stream, beside the tail of the forward still running on the
+    # caller's stream: the brick partition of q (it needs only q, valid since
+    # the forward's start), then q_bar from the stored gradient; the caller's
+    # stream waits for the partition before the query P2M's second phase and
+    # joins the aux stream before returning
     cs = torch.cuda.current_stream()
     aux = eng.aux_stream()
-    aux.wait_stream(cs)
+    y_ready = cs.record_event()
+    prep = None
     with torch.cuda.stream(aux):
+        if res.q_ready is not None:
+            aux.wait_event(res.q_ready)
+            prep = eng.p2m_prepare(qd, int(yb.shape[1]))
+            prep_done = aux.record_event()
+        aux.wait_event(y_ready)
         q_bar = _weighted_grad(res.q_grad, yb)
     q_bar.record_stream(cs)             # the caller uses it on its stream
-    back = eng.expand_device(qd, yb)
+    if prep is not None:
+        prep["ws"].record_stream(cs)
+        cs.wait_event(prep_done)
+    back = eng.accessor_from_moments(eng.p2m_device(qd, yb, prepared=prep).storage)
     out = back.eval_device(src.p, _lib.L2P_VALUE | _lib.L2P_WGRAD, wts=src.w)
     cs.wait_stream(aux)
     eng.flag.raise_if_set("source/query", checked)
