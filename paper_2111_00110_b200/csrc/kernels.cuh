@@ -109,6 +109,9 @@ cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* 
                     int x_end, cudaStream_t s, int stages = SEP_ALL,
                     const float* coarse = nullptr);
 
+// cuTensorMapEncodeTiled from the driver (nullptr when unavailable)
+void* tensor_map_encoder();
+
 // l2p.cu -----------------------------------------------------------------
 enum L2PMode : int {
   L2P_VALUE = 1,   // (n, C)

@@ -25,8 +25,13 @@
 // 35-term dot products -- half the registers, twice the resident warps.
 // With a cell-sorted `order`, thread t evaluates point order[t] (outputs
 // stay indexed by point).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+#include <cstring>
 
 namespace fc2t2 {
 
@@ -113,9 +118,9 @@ constexpr int l2p_min_blocks() {
 #ifdef FC2T2_L2P_MINB
   return (RHO <= 4 && !(MODE & L2P_HESS)) ? FC2T2_L2P_MINB : 2;
 #else
-  // 3: measured best (10^7-point value+grad 246 us at 2 or 3 blocks, 321 us at
-  // 4 -- the row gathers are L2-throughput bound; value+wgrad 40 vs 45 us)
-  return (RHO <= 4 && !(MODE & L2P_HESS)) ? 3 : 2;
+  // 4 with the TMA row fetch (10^7-point value + grad: 190 us at 4 blocks,
+  // 212 at 3, 256 at 2; the cp.async fetch was L1/TEX bound and slower at 4)
+  return (RHO <= 4 && !(MODE & L2P_HESS)) ? 4 : 2;
 #endif
 }
 
@@ -197,6 +202,142 @@ l2p_kernel(const float* __restrict__ L, const float* __restrict__ q, int64_t n, 
   if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
 }
 
+// Row fetch by TMA gather4 (FC2T2_L2P_TMA): lanes 0..7 of a warp each load
+// four of its 32 points' rows (a 2-D tensor map over the grid as
+// [cells * C, PP] floats) straight into shared memory -- the L1/TEX pipe
+// then only serves the read-back.
+struct L2PMap {
+  CUtensorMap m;
+};
+
+template <int RHO, int MODE>
+__global__ void __launch_bounds__(256, (l2p_min_blocks<RHO, MODE>()))
+l2p_tma_kernel(const __grid_constant__ L2PMap map, const float* __restrict__ q, int64_t n, int C,
+               int res, const int32_t* __restrict__ order, const float* __restrict__ wts,
+               float* __restrict__ value, float* __restrict__ grad, float* __restrict__ hess,
+               float* __restrict__ wgrad, int32_t* __restrict__ flag) {
+  constexpr int PP = MI<RHO>::PP;
+  constexpr int GS = (4 * PP * 4 + 127) / 128 * 32;   // floats per 128-byte aligned group of 4 rows
+  extern __shared__ __align__(128) float l2p_smem[];
+  __shared__ __align__(8) uint64_t bars[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float* sm0 = reinterpret_cast<float*>(
+      reinterpret_cast<unsigned char*>(l2p_smem) +
+      ((128 - ((unsigned)__cvta_generic_to_shared(l2p_smem) & 127)) & 127));
+  float* rows = sm0 + warp * 8 * GS;   // group k = points 4k..4k+3 at k * GS
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[warp]);
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rows);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int bad = 0;
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 32; base < n;
+       base += warps_total * 32) {
+    const int64_t t = base + lane;
+    const bool valid = t < n;
+    const int64_t i = valid ? (order ? (int64_t)order[t] : t) : 0;
+    float x = 0.f, y = 0.f, z = 0.f;
+    if (valid) { x = q[3 * i]; y = q[3 * i + 1]; z = q[3 * i + 2]; }
+    bad |= valid && outside_domain(x, y, z);
+    const int b0 = box_axis(x, res), b1 = box_axis(y, res), b2 = box_axis(z, res);
+    float X[RHO + 1], Y[RHO + 1], Z[RHO + 1];
+    axis_table<RHO>(box_offset(x, b0, res), X);
+    axis_table<RHO>(box_offset(y, b1, res), Y);
+    axis_table<RHO>(box_offset(z, b2, res), Z);
+    const int cellrow = ((b0 * res + b1) * res + b2) * C;
+    float wg0 = 0.f, wg1 = 0.f, wg2 = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float wv = ((MODE & L2P_WGRAD) && valid) ? wts[i * C + c] : 0.f;
+      const int r = cellrow + c;
+      const int r0 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4);
+      const int r1 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 1);
+      const int r2 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 2);
+      const int r3 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 3);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                     "r"(32 * PP * 4));
+      __syncwarp();
+      if (lane < 8) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst + lane * GS * 4),
+            "l"(reinterpret_cast<uint64_t>(&map.m)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+            "r"(bar)
+            : "memory");
+      }
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "L2PW_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra L2PW_%=;\n\t}\n" ::"r"(bar),
+          "r"(phase)
+          : "memory");
+      phase ^= 1u;
+      float A[PP];
+#pragma unroll
+      for (int k = 0; k < PP; k += 4) {
+        const float4 v4 =
+            *reinterpret_cast<const float4*>(rows + (lane >> 2) * GS + (lane & 3) * PP + k);
+        A[k] = v4.x; A[k + 1] = v4.y; A[k + 2] = v4.z; A[k + 3] = v4.w;
+      }
+      __syncwarp();
+      float v, g[3], h[6];
+      l2p_nested<RHO, MODE>(A, X, Y, Z, v, g, h);
+      if (valid) {
+        if constexpr (MODE & L2P_VALUE) value[i * C + c] = v;
+        if constexpr (MODE & L2P_GRAD) {
+          grad[(i * C + c) * 3 + 0] = g[0];
+          grad[(i * C + c) * 3 + 1] = g[1];
+          grad[(i * C + c) * 3 + 2] = g[2];
+        }
+        if constexpr (MODE & L2P_HESS) {
+#pragma unroll
+          for (int d = 0; d < 6; ++d) hess[(i * C + c) * 6 + d] = h[d];
+        }
+        if constexpr (MODE & L2P_WGRAD) {
+          wg0 = fmaf(wv, g[0], wg0);
+          wg1 = fmaf(wv, g[1], wg1);
+          wg2 = fmaf(wv, g[2], wg2);
+        }
+      }
+    }
+    if constexpr (MODE & L2P_WGRAD) {
+      if (valid) {
+        wgrad[3 * i + 0] = wg0;
+        wgrad[3 * i + 1] = wg1;
+        wgrad[3 * i + 2] = wg2;
+      }
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, FLAG_DOMAIN);
+}
+
+template <int RHO>
+constexpr int l2p_tma_smem() {
+  return 8 * 8 * ((4 * MI<RHO>::PP * 4 + 127) / 128 * 128) + 128;
+}
+
+// 2-D tensor map [rows = cells * C, PP floats] over the grid; false on failure
+template <int RHO>
+bool l2p_map(L2PMap& out, const float* L, int res, int C) {
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+  if (!enc) return false;
+  constexpr int PP = MI<RHO>::PP;
+  const cuuint64_t rows = (cuuint64_t)res * res * res * C;
+  cuuint64_t dims[2] = {(cuuint64_t)PP, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)PP * 4};
+  cuuint32_t box[2] = {(cuuint32_t)PP, 1}, es[2] = {1, 1};
+  std::memset(&out, 0, sizeof(out));
+  return enc(&out.m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(L), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int RHO, int M>
 cudaError_t l2p_launch(int blocks, int C, int res, const float* L, const float* q, int64_t n,
                        const int32_t* order, const float* wts, float* value, float* grad,
@@ -208,6 +349,23 @@ cudaError_t l2p_launch(int blocks, int C, int res, const float* L, const float* 
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }
+#ifndef FC2T2_L2P_NO_TMA
+  {
+    L2PMap map;
+    if ((int64_t)res * res * res * C < (int64_t)INT32_MAX && l2p_map<RHO>(map, L, res, C)) {
+      constexpr int tsm = l2p_tma_smem<RHO>();
+      static unsigned long long cfg2 = 0;
+      if (tsm > 48 * 1024 && attr_needed(cfg2)) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            l2p_tma_kernel<RHO, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+        if (e != cudaSuccess) return e;
+      }
+      FC2T2_LAUNCH("l2p", s, l2p_tma_kernel<RHO, M><<<blocks, 256, tsm, s>>>(
+          map, q, n, C, res, order, wts, value, grad, hess, wgrad, flag));
+      return cudaGetLastError();
+    }
+  }
+#endif
   FC2T2_LAUNCH("l2p", s, l2p_kernel<RHO, M><<<blocks, 256, smem, s>>>(
       L, q, n, C, res, order, wts, value, grad, hess, wgrad, flag));
   return cudaGetLastError();

@@ -652,6 +652,8 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
 
 }  // namespace
 
+void* tensor_map_encoder() { return reinterpret_cast<void*>(tmap_encoder()); }
+
 size_t m2l_sep_workspace_floats(int rho, int level, int C) {
   const int64_t res = 1 << (level + 1);
   const int64_t R1 = rho + 1, T = R1 * (R1 + 1) / 2 * R1;
