@@ -882,7 +882,10 @@ def run_ours(args, rank: int, world: int) -> None:
         rl_core = {"bound": "fp32_ffma", "achieved": d["achieved_tflops"], "peak": ffma_peak,
                    "unit": "TFLOP/s", "peak_source": ffma_src,
                    "hbm_frac": d["hbm_frac"], "hbm_peak_gbs": hbm_peak}
+    ser_ms = d.get("ncu_serial_ms_per_step")
     roofline = {"kernel": dom, **rl_core, "frac": d["frac"],
+                "frac_at_ncu_serial_time": (round(d["frac"] * d["ms_per_step"] / ser_ms, 4)
+                                            if ser_ms else None),
                 "traffic": (traffic["bytes_per_step"] if traffic else None),
                 "traffic_source": (traffic["source"] if traffic else None),
                 "ncu_serial_ms_per_step": (traffic["serial_ms_per_step"] if traffic else None),

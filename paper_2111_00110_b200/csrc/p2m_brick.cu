@@ -485,11 +485,17 @@ brick_scatter_rank_kernel(const float* __restrict__ pts, const float* __restrict
 // thread accumulates its cell's run in order.  Coefficient tables per axis
 // carry the factorials (and the weight): px[k] = w dx^k / k!, so
 // w d^n / n! = px[a] py[b] pz[c] (expansion.py:96-113).
-constexpr int K4_CHUNK = 4096;
+#ifndef FC2T2_K4_CHUNK
+#define FC2T2_K4_CHUNK 2048
+#endif
+#ifndef FC2T2_K4_MINB
+#define FC2T2_K4_MINB 3
+#endif
+constexpr int K4_CHUNK = FC2T2_K4_CHUNK;
 
 template <int RHO, int CB>
 constexpr int k4_min_blocks() {
-  return CB >= 512 ? 1 : 2;
+  return CB >= 512 ? 1 : FC2T2_K4_MINB;
 }
 
 template <int CB>

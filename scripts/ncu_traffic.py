@@ -10,7 +10,7 @@ with a cold cache, so these are upper bounds for the L2-resident stages)."""
 import csv, io, json, re, subprocess, sys
 
 MAP = [  # (regex on the ncu kernel name, library profile label)
-    (r"l2p_(warp_)?kernel", "l2p"), (r"vol_insert_kernel", "insert"), (r"insert_(sorted|heavy)_kernel", "insert"), (r"p2m_sorted_kernel", "p2m"),
+    (r"l2p(_tma|_warp)?_kernel", "l2p"), (r"vol_insert_kernel", "insert"), (r"insert_(sorted|heavy)_kernel", "insert"), (r"p2m_sorted_kernel", "p2m"),
     (r"brick_hist_kernel", "brick_hist"), (r"brick_(colscan|segsum|segscan|segfill|start)_kernel", "brick_scan"),
     (r"brick_scatter(_rank)?_kernel", "brick_scatter"), (r"brick_p2m_kernel", "brick_p2m"),
     (r"cell_keys_kernel", "cell_keys"), (r"place_kernel", "sort_place"),
