@@ -76,6 +76,30 @@ __device__ __forceinline__ float box_offset(double x, int b, int res) {
   return (float)(x - c);
 }
 
+// The same two functions for float32 x in float32 arithmetic only (no
+// float64 conversions on the hot kernels), bit-identical to the float64
+// forms above for every float32 input, NaN and +-inf included
+// (scripts/box_axis_check.py sweeps this on the CPU):
+//  * (x + 1) * h, h = res / 2, has floor(x * h) + h as its exact floor; x * h
+//    is exact (h a power of two).  The float64 sum x + 1 rounds to 1 only
+//    for x in [-2^-54, 0), which the select maps to 0.  Clamping to
+//    [-h, h - 1] before the floor is the clip (NaN -> -h -> box 0, as the
+//    float64 cast gives 0); floor is a round-down add of 1.5 * 2^23.
+//  * the centre (2b + 1 - res) / res is exact in float32 and x - c is rounded
+//    once, which the float64 difference also is: it is exact in float64
+//    unless |x| < 2^-37, where both round to -c.
+__device__ __forceinline__ int box_axis(float x, int res) {
+  const float h = (float)(res >> 1);
+  const float xs = x >= -0x1p-54f ? fmaxf(x, 0.f) : x;
+  const float y = fminf(fmaxf(xs * h, -h), h - 1.f);
+  return __float_as_int(__fadd_rd(y, 12582912.f)) - 0x4B400000 + (res >> 1);
+}
+
+__device__ __forceinline__ float box_offset(float x, int b, int res) {
+  const float c = (float)(2 * b + 1 - res) * (1.f / (float)res);
+  return __fsub_rn(x, c);
+}
+
 // Per-axis power tables x^0..x^RHO.
 template <int RHO, typename T>
 __device__ __forceinline__ void powers(T x, T (&p)[RHO + 1]) {

@@ -218,12 +218,12 @@ l2p_tma_kernel(const __grid_constant__ L2PMap map, const float* __restrict__ q, 
                float* __restrict__ wgrad, int32_t* __restrict__ flag) {
   constexpr int PP = MI<RHO>::PP;
   constexpr int GS = (4 * PP * 4 + 127) / 128 * 32;   // floats per 128-byte aligned group of 4 rows
-  extern __shared__ __align__(128) float l2p_smem[];
+  extern __shared__ __align__(128) float l2p_tma_smem_raw[];
   __shared__ __align__(8) uint64_t bars[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float* sm0 = reinterpret_cast<float*>(
-      reinterpret_cast<unsigned char*>(l2p_smem) +
-      ((128 - ((unsigned)__cvta_generic_to_shared(l2p_smem) & 127)) & 127));
+      reinterpret_cast<unsigned char*>(l2p_tma_smem_raw) +
+      ((128 - ((unsigned)__cvta_generic_to_shared(l2p_tma_smem_raw) & 127)) & 127));
   float* rows = sm0 + warp * 8 * GS;   // group k = points 4k..4k+3 at k * GS
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[warp]);
   const uint32_t dst = (uint32_t)__cvta_generic_to_shared(rows);

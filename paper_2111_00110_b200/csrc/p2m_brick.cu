@@ -4,26 +4,29 @@
 // over the cell key of :195 -- the per-cell summation order is the point
 // order).
 //
-//   K1 brick_hist     CTA tiles of TILE consecutive points (6144 up to level
+//   K1 brick_hist     CTA tiles of TILE consecutive points (2048 up to level
 //                     5); per tile a shared-memory histogram over bricks ->
 //                     cnt[tile][brick]
 //   S  brick_scan     per brick, the exclusive prefix of cnt over the tiles
 //                     (blocks of 32 bricks x 128 tiles read row-wise: segment
 //                     sums, their scan, the in-segment fill); brick_start =
-//                     exclusive scan of the brick totals (one CTA)
-//   K3 brick_scatter  a CTA copies its tile's points and weights into shared
-//                     memory (16-byte loads), finds every point's brick and an
-//                     arrival rank (smem atomics), counting-sorts the tile by
-//                     brick, sorts every brick's short run back into index
-//                     order, and writes the runs contiguously at brick_start +
-//                     the tile prefix as records {x, y, z, w..}: a STABLE
-//                     partition, coalesced stores
+//                     exclusive scan of the brick totals (one CTA), folded
+//                     into cnt by the fill: cnt[tile][brick] = the first
+//                     record of the tile's run of the brick
+//   K3 brick_scatter  a CTA bulk-copies its tile's points and weights into
+//                     shared memory, finds every point's brick and a
+//                     deterministic rank (per-warp counters, lane-order ranks
+//                     among lanes sharing a brick), counting-sorts the tile
+//                     by brick and writes the runs contiguously as records
+//                     {x, y, z, w..}: a STABLE partition, coalesced stores
+//                     (level 6, 4096 bricks: smem atomics + a fix-up sort of
+//                     the short runs)
 //   K4 brick_p2m      one CTA per brick, one thread per cell.  The brick's
-//                     records stream through shared memory in chunks of 4096:
-//                     cell keys and arrival ranks (smem atomics), a counting
-//                     sort, every cell's run sorted back into record (= index)
-//                     order, and each thread accumulates its cell's moment row
-//                     in registers.
+//                     records stream through shared memory in chunks of 2048
+//                     (one bulk copy each): cell keys and deterministic ranks
+//                     as in K3, a counting sort (every cell's run is in record
+//                     = index order), and each thread accumulates its cell's
+//                     moment row in registers.
 //
 // No float atomics, and every summation order is the point order: moments are
 // bit-reproducible run to run (the atomics only count).  Bytes per point: 12 (K1) + 12 + 4C (K3 in) +
@@ -48,9 +51,9 @@ __host__ __device__ inline BrickGeom brick_geom(int level) {
   g.res = 1 << (level + 1);
   g.bz = level >= 6 ? 8 : 4;
   g.bzs = level >= 6 ? 3 : 2;   // log2(bz)
-  g.nbx = g.res / 8 > 0 ? g.res / 8 : 1;
+  g.nbx = g.res >= 8 ? g.res >> 3 : 1;
   g.nby = g.nbx;
-  g.nbz = g.res / g.bz > 0 ? g.res / g.bz : 1;
+  g.nbz = g.res >= g.bz ? g.res >> g.bzs : 1;
   g.nb = g.nbx * g.nby * g.nbz;
   g.cb = 64 * g.bz;
   return g;
@@ -175,7 +178,8 @@ brick_segscan_kernel(uint32_t* __restrict__ part, int nseg, int nb, uint32_t* __
 }
 
 __global__ void __launch_bounds__(256)
-brick_segfill_kernel(uint32_t* __restrict__ cnt, int nt, int nb, const uint32_t* __restrict__ part) {
+brick_segfill_kernel(uint32_t* __restrict__ cnt, int nt, int nb, const uint32_t* __restrict__ part,
+                     const uint32_t* __restrict__ bstart) {
   __shared__ uint32_t ws[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int b = blockIdx.x * 32 + lane, seg = blockIdx.y;
@@ -187,7 +191,7 @@ brick_segfill_kernel(uint32_t* __restrict__ cnt, int nt, int nb, const uint32_t*
   ws[w][lane] = s;
   __syncthreads();
   if (b >= nb) return;
-  uint32_t run = part[(size_t)seg * nb + b];
+  uint32_t run = part[(size_t)seg * nb + b] + bstart[b];
   for (int q = 0; q < w; ++q) run += ws[q][lane];
   for (int t = t0; t < t1; ++t) {
     const uint32_t v = cnt[(size_t)t * nb + b];
@@ -255,7 +259,7 @@ __device__ __forceinline__ void stage_floats(float* dst, const float* __restrict
 __global__ void __launch_bounds__(K3_THREADS)
 brick_scatter_kernel(const float* __restrict__ pts, const float* __restrict__ wts, int C, int RS,
                      int64_t n, int level, int tile, const uint32_t* __restrict__ cpre,
-                     const uint32_t* __restrict__ bstart, float* __restrict__ rec) {
+                     float* __restrict__ rec) {
   extern __shared__ __align__(16) unsigned char sm3[];
   const BrickGeom g = brick_geom(level);
   const K3Smem L = k3_smem(tile, C, g.nb);
@@ -276,7 +280,7 @@ brick_scatter_kernel(const float* __restrict__ pts, const float* __restrict__ wt
   stage_floats(sw, wts + (int64_t)C * t0, C * tn);
   for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
     bcnt[b] = 0u;
-    gbase[b] = bstart[b] + cpre[(size_t)blockIdx.x * g.nb + b];
+    gbase[b] = cpre[(size_t)blockIdx.x * g.nb + b];
   }
   __syncthreads();
   // 2. brick and arrival rank of every point
@@ -355,14 +359,18 @@ brick_scatter_kernel(const float* __restrict__ pts, const float* __restrict__ wt
 // (counter read before and after the group's atomicAdds differ by one) takes
 // the old count; lanes sharing a brick (~40 % of the groups at 1024 bricks)
 // add their lane-order rank among those peers (__match_any_sync over the
-// clashing lanes only) -- deterministic whatever order the atomics ran in.  Then slot = tile start of the
-// brick + the counts of the brick in earlier warps + rank.
+// clashing lanes only) -- deterministic whatever order the atomics ran in.
+// Then slot = tile start of the brick + the counts of the brick in earlier
+// warps + rank; the tile's points arrive by one bulk copy (TMA) while the
+// counters are cleared, and cpre already holds every brick's global start
+// for this tile (brick_segfill folds brick_start in).
 constexpr int K3R_PER_WARP = 128;
 constexpr int K3R_THREADS = 512;                              // 2 CTAs per SM
-constexpr int K3R_TILE = K3R_PER_WARP * (K3R_THREADS / 32);  // 2048
+constexpr int K3R_NW = K3R_THREADS / 32;
+constexpr int K3R_TILE = K3R_PER_WARP * K3R_NW;               // 2048
 
 struct K3RSmem {
-  size_t pts, wts, key, wc, lstart, gbase, perm, total;
+  size_t pts, wts, key, wc, delta, perm, total;
 };
 __host__ __device__ inline K3RSmem k3r_smem(int C, int nb) {
   K3RSmem m;
@@ -371,20 +379,41 @@ __host__ __device__ inline K3RSmem k3r_smem(int C, int nb) {
   m.pts = take((size_t)K3R_TILE * 12);
   m.wts = take((size_t)K3R_TILE * C * 4);
   m.key = take((size_t)K3R_TILE * 4);
-  m.wc = take((size_t)(K3R_THREADS / 32) * nb * 2);    // packed 16-bit counters
-  m.lstart = take((size_t)nb * 4);
-  m.gbase = take((size_t)nb * 4);
+  m.wc = take((size_t)K3R_NW * nb * 2);    // packed 16-bit counters [NW][nb]
+  m.delta = take((size_t)nb * 4);
   m.perm = take((size_t)K3R_TILE * 2);
   m.total = o;
   return m;
 }
 
+// bulk (TMA) copy of nbytes global -> shared on barrier bar when both ends
+// are 16-byte aligned (the sub-16-byte tail by plain loads); false: caller
+// stages with ordinary loads.  Issued by thread 0; the tail by threads 1..3.
+__device__ __forceinline__ bool bulk_stage(void* dst, const void* src, uint32_t nbytes,
+                                           uint32_t bar, uint32_t& expect) {
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) != 0)
+    return false;
+  const uint32_t body = nbytes & ~15u;
+  if (threadIdx.x == 0 && body)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(src), "r"(body), "r"(bar)
+        : "memory");
+  const uint32_t tail = (nbytes - body) >> 2;
+  if (threadIdx.x >= 1 && threadIdx.x <= tail)
+    reinterpret_cast<float*>(dst)[(body >> 2) + threadIdx.x - 1] =
+        __ldg(reinterpret_cast<const float*>(src) + (body >> 2) + threadIdx.x - 1);
+  expect += body;
+  return true;
+}
+
 __global__ void __launch_bounds__(K3R_THREADS)
 brick_scatter_rank_kernel(const float* __restrict__ pts, const float* __restrict__ wts, int C,
-                          int RS, int64_t n, int level, const uint32_t* __restrict__ cpre,
-                          const uint32_t* __restrict__ bstart, float* __restrict__ rec) {
+                          int RS, int64_t n, int level, const uint32_t* __restrict__ gstart,
+                          float* __restrict__ rec) {
   extern __shared__ __align__(16) unsigned char sm3[];
-  constexpr int NW = K3R_THREADS / 32;
+  constexpr int NW = K3R_NW;
   const BrickGeom g = brick_geom(level);
   const K3RSmem L = k3r_smem(C, g.nb);
   float* sp = reinterpret_cast<float*>(sm3 + L.pts);
@@ -392,23 +421,43 @@ brick_scatter_rank_kernel(const float* __restrict__ pts, const float* __restrict
   uint32_t* key = reinterpret_cast<uint32_t*>(sm3 + L.key);
   uint32_t* wcw = reinterpret_cast<uint32_t*>(sm3 + L.wc);          // [NW][nb / 2] words
   uint16_t* wc = reinterpret_cast<uint16_t*>(sm3 + L.wc);           // [NW][nb]
-  uint32_t* lstart = reinterpret_cast<uint32_t*>(sm3 + L.lstart);
-  uint32_t* gbase = reinterpret_cast<uint32_t*>(sm3 + L.gbase);
+  uint32_t* delta = reinterpret_cast<uint32_t*>(sm3 + L.delta);     // global - tile slot
   uint16_t* perm = reinterpret_cast<uint16_t*>(sm3 + L.perm);
   __shared__ uint32_t warp_tot[32];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * K3R_TILE;
   const int tn = (int)min((int64_t)K3R_TILE, n - t0);
-  stage_floats(sp, pts + 3 * t0, 3 * tn);
-  stage_floats(sw, wts + (int64_t)C * t0, C * tn);
-  const int nbw = (g.nb + 1) >> 1;   // counter words per warp
-  for (int i = threadIdx.x; i < NW * nbw; i += blockDim.x) wcw[i] = 0u;
-  for (int b = threadIdx.x; b < g.nb; b += blockDim.x)
-    gbase[b] = bstart[b] + cpre[(size_t)blockIdx.x * g.nb + b];
+  const int nbw = g.nb >> 1;   // counter words per warp (nb even, <= 1024)
+  // 0. the tile's points and weights: one bulk copy each (TMA)
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
+  uint32_t expect = 0;
+  if (!bulk_stage(sp, pts + 3 * t0, (uint32_t)(12 * tn), bar_s, expect))
+    stage_floats(sp, pts + 3 * t0, 3 * tn);
+  if (!bulk_stage(sw, wts + (int64_t)C * t0, (uint32_t)(4 * C * tn), bar_s, expect))
+    stage_floats(sw, wts + (int64_t)C * t0, C * tn);
+  if (threadIdx.x == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
+                 "r"(expect));
+  // ... meanwhile: clear the counters
+  for (int i = threadIdx.x; i < NW * nbw / 4; i += blockDim.x)
+    reinterpret_cast<uint4*>(wcw)[i] = make_uint4(0u, 0u, 0u, 0u);
+  __syncthreads();
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "K3W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra K3W_%=;\n\t}\n" ::"r"(bar_s)
+      : "memory");
   // 1. ranks within the warp's points, in index order
   const unsigned lt = lanemask_lt();
   uint32_t* myw = wcw + (size_t)w * nbw;
+#pragma unroll
   for (int grp = 0; grp < K3R_PER_WARP; grp += 32) {
     const int tp = w * K3R_PER_WARP + grp + lane;
     const bool ok = tp < tn;
@@ -427,64 +476,73 @@ brick_scatter_rank_kernel(const float* __restrict__ pts, const float* __restrict
     __syncwarp();
   }
   __syncthreads();
-  // 2. per brick: exclusive prefix over the warps (in place), tile starts
-  constexpr int BPT = 1024 / K3R_THREADS;   // bricks per thread (nb <= 1024)
-  uint32_t cnt[BPT], mine = 0;
+  // 2. thread t owns counter word t (bricks 2t, 2t + 1): the exclusive
+  //    prefix over the warps (packed: both halves stay < 2^11), the tile
+  //    starts, then every warp's counter := tile slot of its first point
+  uint32_t pre[NW], run = 0;
+  const int t = threadIdx.x;
+  if (t < nbw) {
 #pragma unroll
-  for (int k = 0; k < BPT; ++k) {
-    const int b = threadIdx.x * BPT + k;
-    cnt[k] = 0;
-    if (b < g.nb) {
-      for (int q = 0; q < NW; ++q) {
-        const uint32_t v = wc[(size_t)q * (2 * nbw) + b];
-        wc[(size_t)q * (2 * nbw) + b] = (uint16_t)cnt[k];
-        cnt[k] += v;
-      }
+    for (int q = 0; q < NW; ++q) {
+      pre[q] = run;
+      run += wcw[q * nbw + t];
     }
-    mine += cnt[k];
   }
+  const uint32_t c0 = run & 0xffffu, c1 = run >> 16;
   uint32_t total;
-  uint32_t st = block_exclusive_scan(mine, warp_tot, total);
+  const uint32_t st = block_exclusive_scan(c0 + c1, warp_tot, total);
+  if (t < nbw) {
+    const uint32_t base = st | ((st + c0) << 16);
 #pragma unroll
-  for (int k = 0; k < BPT; ++k) {
-    const int b = threadIdx.x * BPT + k;
-    if (b < g.nb) lstart[b] = st;
-    st += cnt[k];
+    for (int q = 0; q < NW; ++q) wcw[q * nbw + t] = pre[q] + base;
+    const uint32_t* gs = gstart + (size_t)blockIdx.x * g.nb + 2 * t;
+    delta[2 * t] = __ldg(gs) - st;
+    delta[2 * t + 1] = __ldg(gs + 1) - (st + c0);
   }
   __syncthreads();
-  // 3. sorted position of every point of the tile
+  // 3. tile slot of every point
   for (int tp = threadIdx.x; tp < tn; tp += blockDim.x) {
     const uint32_t k = key[tp];
-    const int bb = (int)(k >> 13);
-    perm[lstart[bb] + wc[(size_t)(tp / K3R_PER_WARP) * (2 * nbw) + bb] + (k & 8191u)] =
-        (uint16_t)tp;
+    perm[wc[(tp / K3R_PER_WARP) * g.nb + (k >> 13)] + (k & 8191u)] = (uint16_t)tp;
   }
   __syncthreads();
-  // 4. brick runs out, coalesced
-  const int r4 = RS / 4;
-  for (int e = threadIdx.x; e < tn * r4; e += blockDim.x) {
-    const int s = r4 == 1 ? e : e / r4, f = e - s * r4;
-    const int tp = perm[s];
-    const int bb = (int)(key[tp] >> 13);
-    const size_t gs = (size_t)gbase[bb] + (s - lstart[bb]);
-    float v[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = 4 * f + j;
-      v[j] = c < 3 ? sp[3 * tp + c] : (c < 3 + C ? sw[C * tp + c - 3] : 0.f);
+  // 4. brick runs out, coalesced: slot s -> record delta[brick] + s
+  if (RS == 4) {
+    for (int s = threadIdx.x; s < tn; s += blockDim.x) {
+      const int tp = perm[s];
+      const uint32_t gsl = delta[key[tp] >> 13] + (uint32_t)s;
+      reinterpret_cast<float4*>(rec)[gsl] =
+          make_float4(sp[3 * tp], sp[3 * tp + 1], sp[3 * tp + 2], sw[tp]);
     }
-    reinterpret_cast<float4*>(rec)[gs * r4 + f] = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    const int r4 = RS / 4;
+    for (int e = threadIdx.x; e < tn * r4; e += blockDim.x) {
+      const int s = e / r4, f = e - s * r4;
+      const int tp = perm[s];
+      const size_t gsl = delta[key[tp] >> 13] + (uint32_t)s;
+      float v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = 4 * f + j;
+        v[j] = c < 3 ? sp[3 * tp + c] : (c < 3 + C ? sw[C * tp + c - 3] : 0.f);
+      }
+      reinterpret_cast<float4*>(rec)[gsl * r4 + f] = make_float4(v[0], v[1], v[2], v[3]);
+    }
   }
 }
 
 // ------------------------------------------------------------------- K4 ---
 // One CTA (CB threads) per brick; thread = cell of the brick, one channel at
 // a time.  The brick's records stream through shared memory in chunks of
-// K4_CHUNK: cell-in-brick keys and arrival ranks by smem atomics, a counting
-// sort, every cell's run sorted back into record (= index) order, then each
-// thread accumulates its cell's run in order.  Coefficient tables per axis
-// carry the factorials (and the weight): px[k] = w dx^k / k!, so
-// w d^n / n! = px[a] py[b] pz[c] (expansion.py:96-113).
+// K4_CHUNK.  Warp w ranks records [w K4_CHUNK / NW, ...) of the chunk, 32 at
+// a time, against its own 16-bit cell counters (the K3r scheme: an atomicAdd
+// per lane, lanes that share a cell in the group ranked in lane order by
+// __match_any_sync) -- so every cell's run comes out in record (= index)
+// order with no fix-up sort.  Per cell the exclusive prefix over the warps
+// and the chunk's counting-sort starts, then each thread accumulates its
+// cell's run in order.  Coefficient tables per axis carry the factorials
+// (and the weight): px[k] = w dx^k / k!, so w d^n / n! = px[a] py[b] pz[c]
+// (expansion.py:96-113).
 #ifndef FC2T2_K4_CHUNK
 #define FC2T2_K4_CHUNK 2048
 #endif
@@ -495,13 +553,23 @@ constexpr int K4_CHUNK = FC2T2_K4_CHUNK;
 
 template <int RHO, int CB>
 constexpr int k4_min_blocks() {
-  return CB >= 512 ? 1 : FC2T2_K4_MINB;
+  return CB >= 512 ? 1 : (RHO >= 5 ? 2 : FC2T2_K4_MINB);   // rho >= 5: 56+ accumulators
 }
+
+// records per warp and the key layout: cell-in-brick << RB | rank in warp
+template <int CB>
+struct K4Keys {
+  static constexpr int NW = CB / 32, PER_WARP = K4_CHUNK / NW;
+  static constexpr int RB = CB >= 512 ? 7 : 8;
+  static_assert(PER_WARP <= (1 << RB) && (CB - 1) < (1 << (16 - RB)), "16-bit keys");
+  static_assert(PER_WARP % 32 == 0, "whole groups");
+};
 
 template <int CB>
 constexpr size_t k4_smem() {
-  // srec float4 + key uint32 + perm uint16 per record, count + start per cell
-  return (size_t)K4_CHUNK * (16 + 4 + 2) + (size_t)CB * 8;
+  // srec float4 + key uint16 + perm uint16 per record; per-warp packed 16-bit
+  // cell counters; per cell its chunk start and count
+  return (size_t)K4_CHUNK * (16 + 2 + 2) + (size_t)(CB / 32) * CB * 2 + (size_t)CB * 8;
 }
 
 template <int RHO, int CB>
@@ -510,15 +578,17 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
                  const uint32_t* __restrict__ brick_start, float* __restrict__ M) {
   constexpr int PP = MI<RHO>::PP;
   constexpr int BZ = CB / 64, BZS = BZ == 8 ? 3 : 2;
+  using KK = K4Keys<CB>;
+  constexpr int NW = KK::NW, PW = KK::PER_WARP, RB = KK::RB, CW = CB / 2;
   extern __shared__ __align__(16) unsigned char smem[];
   float4* srec = reinterpret_cast<float4*>(smem);                      // [K4_CHUNK]
-  uint32_t* key = reinterpret_cast<uint32_t*>(srec + K4_CHUNK);        // [K4_CHUNK]
-  uint16_t* perm = reinterpret_cast<uint16_t*>(key + K4_CHUNK);        // [K4_CHUNK]
-  uint32_t* ccnt = reinterpret_cast<uint32_t*>(perm + K4_CHUNK);       // [CB]
-  uint32_t* cst = ccnt + CB;                                           // [CB]
+  uint16_t* key = reinterpret_cast<uint16_t*>(srec + K4_CHUNK);        // [K4_CHUNK]
+  uint16_t* perm = key + K4_CHUNK;                                     // [K4_CHUNK]
+  uint32_t* wcw = reinterpret_cast<uint32_t*>(perm + K4_CHUNK);        // [NW][CB / 2]
+  uint16_t* wc = reinterpret_cast<uint16_t*>(wcw);                     // [NW][CB]
+  uint32_t* cst = wcw + NW * CW;                                       // [CB]
+  uint32_t* ccnt = cst + CB;                                           // [CB]
   __shared__ uint32_t warp_tot[32];
-  __shared__ uint32_t nlong;
-  __shared__ uint16_t longs[kMaxLong];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
   if (RS == 4 && threadIdx.x == 0) {
@@ -529,13 +599,15 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
 
   const BrickGeom g = brick_geom(level);
   const int brick = blockIdx.x;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt();
   const int bz = brick % g.nbz, by = (brick / g.nbz) % g.nby, bx = brick / (g.nbz * g.nby);
   // this thread's cell
   const int ccx = bx * 8 + (tid >> (3 + BZS)), ccy = by * 8 + ((tid >> BZS) & 7),
             ccz = bz * BZ + (tid & (BZ - 1));
   const int64_t cell = ((int64_t)ccx * g.res + ccy) * g.res + ccz;
   const uint32_t beg = brick_start[brick], end = brick_start[brick + 1];
+  uint32_t* myw = wcw + warp * CW;
 
   for (int c = 0; c < C; ++c) {
     float acc[PP];
@@ -543,11 +615,10 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
     for (int j = 0; j < PP; ++j) acc[j] = 0.f;
     for (uint32_t c0 = beg; c0 < end; c0 += K4_CHUNK) {
       const int nc = (int)umin((uint32_t)K4_CHUNK, end - c0);
-      ccnt[tid] = 0u;
+      for (int i = tid; i < NW * CW; i += CB) wcw[i] = 0u;
       __syncthreads();   // also: the previous chunk's walk is done with srec / perm
       if (RS == 4) {
         // C = 1: the chunk's records are contiguous -- one bulk copy (TMA)
-        // into srec, then (x, y, z, w) -> (dx, dy, dz, w) in place
         if (threadIdx.x == 0) {
           // the previous chunk's generic-proxy stores to srec precede the copy
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -567,66 +638,72 @@ brick_p2m_kernel(const float* __restrict__ rec, int C, int RS, int level,
             "r"(phase)
             : "memory");
         phase ^= 1u;
+      } else {
         for (int k = tid; k < nc; k += CB) {
+          const float* r = rec + (size_t)(c0 + k) * RS;
+          srec[k] = make_float4(__ldg(r), __ldg(r + 1), __ldg(r + 2), __ldg(r + 3 + c));
+        }
+        __syncthreads();
+      }
+      // (x, y, z, w) -> (dx, dy, dz, w) in place; cell-in-brick key and the
+      // deterministic rank within the warp's records
+#pragma unroll 2
+      for (int k0 = warp * PW; k0 < warp * PW + PW; k0 += 32) {
+        const int k = k0 + lane;
+        const bool ok = k < nc;
+        uint32_t cib = 0;
+        if (ok) {
           const float4 v = srec[k];
           const int cx = box_axis(v.x, g.res), cy = box_axis(v.y, g.res), cz = box_axis(v.z, g.res);
           srec[k] = make_float4(box_offset(v.x, cx, g.res), box_offset(v.y, cy, g.res),
                                 box_offset(v.z, cz, g.res), v.w);
-          const uint32_t cib = (uint32_t)((((cx & 7) << 3) | (cy & 7)) << BZS) | (cz & (BZ - 1));
-          key[k] = (cib << 16) | atomicAdd(&ccnt[cib], 1u);
+          cib = (uint32_t)((((cx & 7) << 3) | (cy & 7)) << BZS) | (cz & (BZ - 1));
         }
-      } else {
-      // stage (dx, dy, dz, w_c); cell-in-brick key and arrival rank (4
-      // records per thread in flight)
-      constexpr int U = 4;
-      for (int k0 = 0; k0 < nc; k0 += U * CB) {
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int k = k0 + u * CB + tid;
-          if (k < nc) {
-            const float* r = rec + (size_t)(c0 + k) * RS;
-            v[u] = RS == 4 ? __ldg(reinterpret_cast<const float4*>(r))
-                           : make_float4(__ldg(r), __ldg(r + 1), __ldg(r + 2), __ldg(r + 3 + c));
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int k = k0 + u * CB + tid;
-          if (k < nc) {
-            const int cx = box_axis(v[u].x, g.res), cy = box_axis(v[u].y, g.res),
-                      cz = box_axis(v[u].z, g.res);
-            srec[k] = make_float4(box_offset(v[u].x, cx, g.res), box_offset(v[u].y, cy, g.res),
-                                  box_offset(v[u].z, cz, g.res), v[u].w);
-            const uint32_t cib =
-                (uint32_t)((((cx & 7) << 3) | (cy & 7)) << BZS) | (cz & (BZ - 1));
-            key[k] = (cib << 16) | atomicAdd(&ccnt[cib], 1u);
-          }
-        }
-      }
+        const uint32_t sh = (cib & 1u) << 4;
+        const uint32_t pre = (myw[cib >> 1] >> sh) & 0xffffu;
+        __syncwarp();
+        if (ok) atomicAdd(myw + (cib >> 1), 1u << sh);
+        __syncwarp();
+        const bool clash = ok && ((myw[cib >> 1] >> sh) & 0xffffu) != pre + 1;
+        const unsigned cm = __ballot_sync(0xffffffffu, clash);
+        uint32_t r = pre;
+        if (clash) r += (uint32_t)__popc(__match_any_sync(cm, cib) & lt);
+        if (ok) key[k] = (uint16_t)((cib << RB) | r);
+        __syncwarp();
       }
       __syncthreads();
+      // per cell: prefix over the warps (thread t < CB / 2 owns cells 2t,
+      // 2t + 1; packed halves stay < 2^12), chunk starts, then every warp's
+      // counter := chunk slot of its first record of the cell
+      uint32_t pre[NW], run = 0;
+      if (tid < CW) {
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+          pre[q] = run;
+          run += wcw[q * CW + tid];
+        }
+      }
+      const uint32_t n0 = run & 0xffffu, n1 = run >> 16;
       uint32_t total;
-      const uint32_t mine = ccnt[tid];
-      const uint32_t st = block_exclusive_scan(mine, warp_tot, total);
-      cst[tid] = st;
+      const uint32_t st = block_exclusive_scan(n0 + n1, warp_tot, total);
+      if (tid < CW) {
+        const uint32_t base = st | ((st + n0) << 16);
+#pragma unroll
+        for (int q = 0; q < NW; ++q) wcw[q * CW + tid] = pre[q] + base;
+        cst[2 * tid] = st;
+        cst[2 * tid + 1] = st + n0;
+        ccnt[2 * tid] = n0;
+        ccnt[2 * tid + 1] = n1;
+      }
       __syncthreads();
       for (int k = tid; k < nc; k += CB) {
         const uint32_t kk = key[k];
-        perm[cst[kk >> 16] + (kk & 0xffffu)] = (uint16_t)k;
+        perm[wc[(k / PW) * CB + (kk >> RB)] + (kk & ((1u << RB) - 1u))] = (uint16_t)k;
       }
       __syncthreads();
-      // this cell's run back into index order (short runs by their thread,
-      // long ones -- clustered points -- by a warp), then accumulated in order
-      uint16_t* mine_run = perm + st;
-      if (tid == 0) nlong = 0;
-      __syncthreads();
-      if (mine <= (uint32_t)kShortRun) sort_run(mine_run, (int)mine);
-      else longs[atomicAdd(&nlong, 1u)] = (uint16_t)tid;
-      __syncthreads();
-      for (uint32_t i = tid >> 5; i < nlong; i += CB / 32)
-        warp_compact_run(perm + cst[longs[i]], key, nc, longs[i], 16);
-      __syncthreads();
+      // this cell's run, in index order
+      const uint32_t mine = ccnt[tid];
+      const uint16_t* mine_run = perm + cst[tid];
       for (uint32_t e = 0; e < mine; ++e) {
         const float4 v = srec[mine_run[e]];
         float px[RHO + 1], py[RHO + 1], pz[RHO + 1];
@@ -708,7 +785,9 @@ cudaError_t launch_k4(const BrickWs& b, int C, int RS, int level, int nb, float*
                       cudaStream_t s) {
   constexpr size_t sm = k4_smem<CB>();
   static unsigned long long configured = 0;
-  if (sm > 48 * 1024 && attr_needed(configured)) {
+  // static + dynamic shared memory above 48 KB needs the opt-in (the
+  // kernel's static part is ~0.6 KB, so set it from 32 KB of dynamic)
+  if (sm > 32 * 1024 && attr_needed(configured)) {
     cudaError_t e = cudaFuncSetAttribute(brick_p2m_kernel<RHO, CB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -767,19 +846,19 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
                brick_segsum_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part));
   FC2T2_LAUNCH("brick_scan", s,
                brick_segscan_kernel<<<(g.nb + 7) / 8, 256, 0, s>>>(b.part, nseg, g.nb, b.tot));
-  FC2T2_LAUNCH("brick_scan", s,
-               brick_segfill_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part));
   FC2T2_LAUNCH("brick_scan", s, brick_start_kernel<<<1, 1024, 0, s>>>(b.tot, g.nb, b.bstart));
+  FC2T2_LAUNCH("brick_scan", s,
+               brick_segfill_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part, b.bstart));
   }
   if (!(phase & P2M_FINISH)) return cudaGetLastError();
   if (n > 0 && rk)
     FC2T2_LAUNCH("brick_scatter", s,
                  brick_scatter_rank_kernel<<<(unsigned)nt, K3R_THREADS, sm3, s>>>(
-                     pts, w, C, RS, n, level, b.cnt, b.bstart, b.rec));
+                     pts, w, C, RS, n, level, b.cnt, b.rec));
   else if (n > 0)
     FC2T2_LAUNCH("brick_scatter", s,
                  brick_scatter_kernel<<<(unsigned)nt, K3_THREADS, sm3, s>>>(
-                     pts, w, C, RS, n, level, tile, b.cnt, b.bstart, b.rec));
+                     pts, w, C, RS, n, level, tile, b.cnt, b.rec));
   cudaError_t e = cudaSuccess;
   FC2T2_DISPATCH_RHO(rho, {
     if (g.cb == 512) e = launch_k4<RHO, 512>(b, C, RS, level, g.nb, M, s);

@@ -43,6 +43,26 @@ def test_find_box_bit_exact(cuda, level):
     assert np.array_equal(got.cpu().numpy(), g[f"box_l{level}"])
 
 
+@pytest.mark.parametrize("level", [2, 5, 6, 7])
+def test_find_box_float32_edges(cuda, level):
+    """The float32-only box_axis (csrc/common.cuh) at the inputs where it could
+    part from the float64 floor((x + 1) res / 2) of expansion.py:85-93: x in
+    [-2^-54, 0) (where float64 x + 1 rounds to 1), denormals, +-0, every
+    plane and one float32 ulp either side, -1 and the largest x < 1."""
+    from oracle.fc2t2_oracle import find_box as oracle_box
+    from paper_2111_00110_b200.expansion import find_box
+    res = 2 ** (level + 1)
+    planes = (np.arange(res + 1) / (res / 2) - 1).astype(np.float32)
+    v = np.concatenate([
+        np.array([0.0, -0.0, -2.0**-54, -2.0**-55, -2.0**-53, -2.0**-52, 2.0**-54, -1e-45, 1e-45,
+                  -1e-38, -1e-30, -1e-20, -1e-17, -1e-16, -1.0, np.nextafter(1.0, 0.0)], np.float32),
+        planes, np.nextafter(planes, np.float32(2)), np.nextafter(planes, np.float32(-2))])
+    v = v[np.abs(v) < 1]
+    p = np.stack([v, v[::-1], np.roll(v, 7)], 1).astype(np.float32)
+    got = find_box(level, torch.from_numpy(p).cuda()).cpu().numpy()
+    assert np.array_equal(got, oracle_box(level, p.astype(np.float64)))
+
+
 def _cell_key(p: np.ndarray, level: int) -> np.ndarray:
     from oracle.fc2t2_oracle import find_box
     res = 2 ** (level + 1)
