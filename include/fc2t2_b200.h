@@ -177,6 +177,17 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
 int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double* post,
                                const double* conv);
 int fc2t2_engine_separable(const fc2t2_engine* e);
+/* The far table of a coarse level (kCoarsest < level < levels, >= 16 cells per
+ * axis) through that level's per-axis factors: the parity stencil minus the
+ * hole {-1,0,1}^3 (ref expansion.py:246-249, kernel.py:257-300) as three
+ * disjoint separable pieces, F x A x A + N x F x A + N x N x F with the axis tap
+ * sets A = parity box, F = {|d| >= 2}, N = {|d| <= 1} -- seven 1-D passes
+ * instead of 189 dense tables per target.  Offsets the reference prunes (peak
+ * interaction below 1e-16, kernel.py:275) are included; the caller checks
+ * eligibility (kernel.py separable_far_eligible).  Same argument layout as
+ * fc2t2_engine_set_separable; NULL pointers restore the dense path. */
+int fc2t2_engine_set_separable_far(fc2t2_engine* e, int level, const double* pre,
+                                   const double* post, const double* conv);
 /* 1 (default): the separable M2L's post transform runs after the coarse chain
  * with the finest L2L fused into it (one pass over the finest L grid fewer);
  * 0: separate accumulate-L2L launch.  Results are bit-identical. */

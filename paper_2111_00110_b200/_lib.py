@@ -63,6 +63,7 @@ _SIGS = {
     "fc2t2_m2l": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, _i32, _vp, _sz, _vp]),
     "fc2t2_engine_set_separable": (_i32, [_vp, _vp, _vp, _vp]),
     "fc2t2_engine_separable": (_i32, [_vp]),
+    "fc2t2_engine_set_separable_far": (_i32, [_vp, _i32, _vp, _vp, _vp]),
     "fc2t2_engine_set_sep_fusion": (_i32, [_vp, _i32]),
     "fc2t2_expand_workspace_size": (_sz, [_vp, _i32]),
     "fc2t2_weighted_grad": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp]),

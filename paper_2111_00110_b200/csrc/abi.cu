@@ -141,11 +141,17 @@ struct fc2t2_engine {
   // coarse levels: every level's M2L on its own stream (cs[l & 1]) as soon as
   // its M grid exists (ev_m[l]); the L2L chain waits for each (ev_c[l])
   cudaStream_t cs[2] = {nullptr, nullptr};
+  // the M2M chain of an overlapped cascade: high priority like cs[], so the
+  // coarse chain's few CTAs are placed ahead of the finest level's many
+  cudaStream_t up = nullptr;
   cudaEvent_t ev_m[10] = {}, ev_c[10] = {};
   // separable finest M2L (m2l_sep.cu): per-axis factors, [out][in] float64
   bool sep = false;
   bool sep_fuse_l2l = true;  // fc2t2_engine_set_sep_fusion
   std::vector<double> sep_pre, sep_post, sep_conv;
+  // separable far tables of coarse levels: level -> {pre, post, conv}
+  // (fc2t2_engine_set_separable_far)
+  std::map<int, std::vector<double>> sep_far;
 };
 
 namespace {
@@ -442,6 +448,7 @@ void fc2t2_engine_destroy(fc2t2_engine* e) {
   if (!e) return;
   cudaFree(e->d_coef);
   if (e->side) cudaStreamDestroy(e->side);
+  if (e->up) cudaStreamDestroy(e->up);
   if (e->fork) cudaEventDestroy(e->fork);
   if (e->join) cudaEventDestroy(e->join);
   for (cudaStream_t c : e->cs)
@@ -559,8 +566,11 @@ int fc2t2_engine_upload(fc2t2_engine* e, void* stream) {
   err = cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking);
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming);
   if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming);
+  int prio_lo = 0, prio_hi = 0;
+  if (err == cudaSuccess) err = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int k = 0; k < 2 && err == cudaSuccess; ++k)
-    err = cudaStreamCreateWithFlags(&e->cs[k], cudaStreamNonBlocking);
+    err = cudaStreamCreateWithPriority(&e->cs[k], cudaStreamNonBlocking, prio_hi);
+  if (err == cudaSuccess) err = cudaStreamCreateWithPriority(&e->up, cudaStreamNonBlocking, prio_hi);
   for (int l = 0; l < 10 && err == cudaSuccess; ++l) {
     err = cudaEventCreateWithFlags(&e->ev_m[l], cudaEventDisableTiming);
     if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e->ev_c[l], cudaEventDisableTiming);
@@ -696,6 +706,8 @@ double fc2t2_m2l_issued_flops(const fc2t2_engine* e, int channels, int level, in
 size_t fc2t2_m2l_workspace_size(const fc2t2_engine* e, int channels, int level, int table) {
   const Plan* p;
   if (plan_for(e, level, table, &p) != FC2T2_OK) return 0;
+  if (table == FC2T2_TABLE_FAR && level < e->levels && e->sep_far.count(level))
+    return fc2t2::m2l_sep_workspace_floats(e->rho, level, channels, true) * sizeof(float);
   return use_tc(*p, level) ? tc_ws_bytes(*p, e->rho, level, channels) : 0;
 }
 
@@ -710,6 +722,19 @@ int fc2t2_m2l(const fc2t2_engine* e, int channels, int level, int table, const f
     if (accumulate) return FC2T2_OK;
     return cuda_status(
         cudaMemsetAsync(d_l, 0, grid_floats(level, channels, e->PP) * sizeof(float), s), "m2l");
+  }
+  if (table == FC2T2_TABLE_FAR && level < e->levels && !accumulate && d_ws) {
+    // a coarse level's far table through its separable factors
+    auto sf = e->sep_far.find(level);
+    if (sf != e->sep_far.end() &&
+        ws_bytes >= fc2t2::m2l_sep_workspace_floats(e->rho, level, channels, true) * sizeof(float)) {
+      const int R1 = e->rho + 1;
+      const double* f = sf->second.data();
+      return cuda_status(
+          fc2t2::m2l_sep(e->rho, level, channels, f, f + R1 * R1, f + 2 * R1 * R1, d_m, d_l,
+                         (float*)d_ws, 0, -1, s, fc2t2::SEP_ALL, nullptr, true),
+          "m2l_sep far");
+    }
   }
   const size_t need = use_tc(*p, level) ? tc_ws_bytes(*p, e->rho, level, channels) : 0;
   if (need && d_ws && ws_bytes >= need) {
@@ -728,6 +753,8 @@ namespace {
 // split-K partial grids
 size_t part_floats(const fc2t2_engine* e, const Plan& p, int level, int channels) {
   if (p.max_list == 0) return 0;
+  if (level < e->levels && e->sep_far.count(level))
+    return fc2t2::m2l_sep_workspace_floats(e->rho, level, channels, true);
   if (use_tc(p, level)) return (tc_ws_bytes(p, e->rho, level, channels) + 3) / 4;
   const int sp = fc2t2::m2l_splits(e->rho, channels, launch_of(p, level));
   return sp > 1 ? (size_t)sp * grid_floats(level, channels, e->PP) : 0;
@@ -754,6 +781,26 @@ int fc2t2_engine_set_separable(fc2t2_engine* e, const double* pre, const double*
 }
 
 int fc2t2_engine_separable(const fc2t2_engine* e) { return e && e->sep ? 1 : 0; }
+
+int fc2t2_engine_set_separable_far(fc2t2_engine* e, int level, const double* pre,
+                                   const double* post, const double* conv) {
+  if (!e) return fail(FC2T2_EVALUE, "null engine");
+  if (!pre || !post || !conv) {
+    e->sep_far.erase(level);
+    return FC2T2_OK;
+  }
+  const int res = 1 << (level + 1);
+  if (e->rho > 5 || level <= kCoarsest || level >= e->levels || res < 16)
+    return fail(FC2T2_EVALUE,
+                "separable far M2L needs rho <= 5 and a coarse level of >= 16 cells per axis");
+  const int R1 = e->rho + 1;
+  std::vector<double> f(9 * R1 * R1);
+  std::copy(pre, pre + R1 * R1, f.begin());
+  std::copy(post, post + R1 * R1, f.begin() + R1 * R1);
+  std::copy(conv, conv + 7 * R1 * R1, f.begin() + 2 * R1 * R1);
+  e->sep_far[level] = std::move(f);
+  return FC2T2_OK;
+}
 
 int fc2t2_engine_set_sep_fusion(fc2t2_engine* e, int fuse_l2l) {
   if (!e) return fail(FC2T2_EVALUE, "null engine");
@@ -786,6 +833,16 @@ ExpandLayout expand_layout(const fc2t2_engine* e, int channels) {
 int level_m2l(const fc2t2_engine* e, int channels, int l, const Plan& p, const float* M, float* Lg,
               int accumulate, float* part, cudaStream_t s, int x_begin = 0, int x_end = -1) {
   int st;
+  if (l < e->levels) {
+    auto sf = e->sep_far.find(l);
+    if (sf != e->sep_far.end() && !accumulate) {
+      const int R1 = e->rho + 1;
+      const double* f = sf->second.data();
+      return cuda_status(fc2t2::m2l_sep(e->rho, l, channels, f, f + R1 * R1, f + 2 * R1 * R1, M, Lg,
+                                        part, x_begin, x_end, s, fc2t2::SEP_ALL, nullptr, true),
+                         "expand m2l_sep far");
+    }
+  }
   if (use_tc(p, l)) {
     const fc2t2::TCPlan tp = tc_of(e, p, l);
     st = cuda_status(fc2t2::tc_prepare(e->rho, channels, tp, M, part, s), "expand split");
@@ -812,14 +869,16 @@ int lowest_level(const fc2t2_engine* e) {
 
 // the finest x-slab [x0, x1) seen at level l: [x0, x1) >> (L - l), or the
 // whole level when the slab does not map to whole cells there (or to the
-// 4-cell granularity of the tcgen05 kernel / the 2-cell parity stride)
+// 4-cell granularity of the tcgen05 and separable kernels / the 2-cell parity
+// stride)
 void level_slab(const fc2t2_engine* e, int l, int x0, int x1, int* b, int* en) {
   const int L = e->levels, sh = L - l, res = 1 << (l + 1);
   int lb = x0 >> sh, le = x1 >> sh;
   bool ok = ((x0 >> sh) << sh) == x0 && ((x1 >> sh) << sh) == x1 && le > lb;
   if (ok && l > kCoarsest && l < L) {
     const Plan& p = e->plans.at(l).at(FC2T2_TABLE_FAR);
-    if (use_tc(p, l)) ok = lb % 4 == 0 && le % 4 == 0;
+    // (the separable passes' TMA windows start 16-byte aligned: x % 4 == 0)
+    if (use_tc(p, l) || e->sep_far.count(l)) ok = lb % 4 == 0 && le % 4 == 0;
     else ok = lb % 2 == 0 && le % 2 == 0;
   }
   if (!ok) {
@@ -939,9 +998,16 @@ int expand_phase(const fc2t2_engine* e, int channels, const float* d_m_finest, f
     // M grids of the coarse levels: the M2M chain here (ev_m[l] marks M_l),
     // or given on entry (PH_DOWN: all-gathered by the caller)
     if (ph == PH_ALL) {
+      // overlapped: on the high-priority `up` stream behind the fork (every
+      // ev_c[l] the caller's stream waits for below is downstream of it)
+      cudaStream_t su = overlap && e->up ? e->up : s;
+      if (su != s) {
+        st = cuda_status(cudaStreamWaitEvent(su, e->fork, 0), "expand fork up");
+        if (st != FC2T2_OK) return st;
+      }
       for (int l = L; l > lowest; --l) {
-        st = cuda_status(fc2t2::m2m(e->rho, l, channels, G.M[l], G.M[l - 1], s), "expand m2m");
-        if (st == FC2T2_OK) st = cuda_status(cudaEventRecord(e->ev_m[l - 1], s), "expand ev_m");
+        st = cuda_status(fc2t2::m2m(e->rho, l, channels, G.M[l], G.M[l - 1], su), "expand m2m");
+        if (st == FC2T2_OK) st = cuda_status(cudaEventRecord(e->ev_m[l - 1], su), "expand ev_m");
         if (st != FC2T2_OK) return st;
       }
     } else {

@@ -41,6 +41,7 @@
 #include "shift.cuh"
 
 #include <cstring>
+#include <mutex>
 
 namespace fc2t2 {
 
@@ -226,6 +227,7 @@ sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int
 // Every contraction is sum_{d, i} K(d)[j][i] in_i(pos + d).
 
 enum { PASS_Z = 0, PASS_Y = 1, PASS_X = 2 };
+enum { TAPS_ALL = 0, TAPS_FAR = 1, TAPS_NEAR = 2 };
 
 template <int RHO, int PASS, int PART>
 struct Part {
@@ -253,11 +255,12 @@ struct Part {
 // pass's window layout) is compile-time, so the whole pass is a handful of
 // small code paths (instruction-cache resident); the K(d)[.][i] column of an
 // input comes from shared memory (Kt[i][d][j], warp-uniform broadcast).
-template <int RHO, int PASS, int POS, int NOUT>
+template <int RHO, int PASS, int POS, int NL, int TAPS, int NOUT>
 __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int ne, int lane,
                                            int nin, int in_base, int in_stride,
                                            const int (&oe)[RHO + 1], float* out,
-                                           int64_t pos_stride, int64_t plane, int nvalid) {
+                                           int64_t pos_stride, int64_t plane, int nvalid,
+                                           bool accumulate) {
   constexpr int OFF = PASS == PASS_X ? 4 : 3;
   constexpr int NQ = PASS == PASS_X ? POS + 8 : win_of(POS);
   float acc[POS][NOUT];
@@ -272,7 +275,7 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
     if constexpr (PASS == PASS_X) {
       // [le][lane][16], 16-byte chunk c of lane l in slot c ^ ((l >> 1) & 3)
       // (the TMA 64-byte swizzle): conflict-free 128-bit reads
-      const float4* r4 = reinterpret_cast<const float4*>(sm + (le * kLines + lane) * 16);
+      const float4* r4 = reinterpret_cast<const float4*>(sm + (le * NL + lane) * 16);
       const int sw = (lane >> 1) & 3;
 #pragma unroll
       for (int q = 0; q < NQ / 4; ++q) {
@@ -282,13 +285,16 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
     } else {
       // [le][q][lane]
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) v[q] = sm[(le * NQ + q) * kLines + lane];
+      for (int q = 0; q < NQ; ++q) v[q] = sm[(le * NQ + q) * NL + lane];
     }
     // K(d) columns one d at a time (NOUT live coefficient registers); per
     // accumulator the FMAs still run over d ascending (unchanged sums)
     const float4* kc = reinterpret_cast<const float4*>(Kt + i * 56);
 #pragma unroll
     for (int d = -3; d <= 3; ++d) {
+      // the tap subset of a far-table piece: F = {|d| >= 2}, N = {|d| <= 1}
+      if ((TAPS == TAPS_FAR && d >= -1 && d <= 1) || (TAPS == TAPS_NEAR && (d < -1 || d > 1)))
+        continue;
       float k[NOUT];
       const float4 lo = kc[2 * (d + 3)];
       const float lo_[4] = {lo.x, lo.y, lo.z, lo.w};
@@ -316,7 +322,20 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
 #pragma unroll
   for (int j = 0; j < NOUT; ++j) ob[j] = oe[j] * (int)plane;
   const int ps = (int)pos_stride;
-  if (nvalid == POS) {
+  if (accumulate) {
+    // all the loads first (one round trip), then the sums and stores
+#pragma unroll
+    for (int w = 0; w < POS; ++w)
+#pragma unroll
+      for (int j = 0; j < NOUT; ++j)
+        acc[w][j] = (w < nvalid ? __ldcg(out + ob[j] + w * ps) : 0.f) + acc[w][j];
+#pragma unroll
+    for (int w = 0; w < POS; ++w)
+      if (w < nvalid) {
+#pragma unroll
+        for (int j = 0; j < NOUT; ++j) out[ob[j] + w * ps] = acc[w][j];
+      }
+  } else if (nvalid == POS) {
 #pragma unroll
     for (int w = 0; w < POS; ++w)
 #pragma unroll
@@ -337,9 +356,9 @@ struct Tile {
   int ch, part, fixed, line0, pos0;
 };
 template <int R1>
-__device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, int POS) {
+__device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, int POS, int NL) {
   Tile r;
-  r.line0 = line_lo + (int)blockIdx.x * kLines;
+  r.line0 = line_lo + (int)blockIdx.x * NL;
   r.pos0 = pos_lo + (int)blockIdx.y * POS;
   const int z = (int)blockIdx.z;
   r.fixed = z & ((1 << lres) - 1);
@@ -349,9 +368,9 @@ __device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, i
   return r;
 }
 
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL, int TAPS>
 __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, float* dst, int res,
-                                             int pos_end, const Tile& T) {
+                                             int pos_end, const Tile& T, bool accumulate) {
   using I = SepIdx<RHO>;
   constexpr int R1 = RHO + 1;
   const int64_t plane = (int64_t)res * res * res;
@@ -387,7 +406,7 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
 #pragma unroll
     for (int j = 0; j < R1; ++j) oe[j] = MI<RHO>::index(j, P_, g) < 0 ? 0 : MI<RHO>::index(j, P_, g);
   }
-  if (g >= ng) return;
+  if (g >= ng || lane >= NL) return;
   float* o;
   int64_t pos_stride;
   if (PASS == PASS_Z) {
@@ -401,8 +420,8 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
 #define FC2T2_SEP_N(Q)                                                                     \
   case Q:                                                                                  \
     if constexpr (Q <= R1)                                                                 \
-      group_body<RHO, PASS, POS, Q>(sm, Kt, ne, lane, nin, in_base, in_stride, oe, o,           \
-                                    pos_stride, plane, nvalid);                               \
+      group_body<RHO, PASS, POS, NL, TAPS, Q>(sm, Kt, ne, lane, nin, in_base, in_stride, oe, o, \
+                                              pos_stride, plane, nvalid, accumulate);       \
     break;
   switch (nout) {
     FC2T2_SEP_N(1)
@@ -417,15 +436,15 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
 #undef FC2T2_SEP_N
 }
 
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL>
 constexpr int pass_win_floats() {
   constexpr int R1 = RHO + 1;
-  return PASS == PASS_X ? R1 * R1 * kLines * 16
-                        : win_of(POS) * (PASS == PASS_Z ? R1 * (R1 + 1) / 2 : R1 * R1) * kLines;
+  return PASS == PASS_X ? R1 * R1 * NL * 16
+                        : win_of(POS) * (PASS == PASS_Z ? R1 * (R1 + 1) / 2 : R1 * R1) * NL;
 }
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL>
 constexpr int pass_smem_floats() {  // window + Kt[i][d][8] + mbarrier + 1 KB alignment slack
-  return pass_win_floats<RHO, PASS, POS>() + 7 * 8 * (RHO + 1) + 2 + 256;
+  return pass_win_floats<RHO, PASS, POS, NL>() + 7 * 8 * (RHO + 1) + 2 + 256;
 }
 
 // TMA: one tensor map per partition (box = the partition's window); the
@@ -446,12 +465,12 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL>
 __device__ __forceinline__ uint32_t window_bytes(int part) {
   constexpr int R1 = RHO + 1;
   const int ne = PASS == PASS_Z ? (R1 - part) * (R1 - part + 1) / 2
                                 : (PASS == PASS_Y ? (R1 - part) * R1 : R1 * (R1 - part));
-  return (uint32_t)(PASS == PASS_X ? 16 * kLines * ne * 4 : win_of(POS) * kLines * ne * 4);
+  return (uint32_t)(PASS == PASS_X ? 16 * NL * ne * 4 : win_of(POS) * NL * ne * 4);
 }
 
 // One pass.  Tile = 32 lines x 8 output positions of one partition/channel:
@@ -459,27 +478,28 @@ __device__ __forceinline__ uint32_t window_bytes(int part) {
 //   y pass: lines x, positions y, fixed z      (in Z,  out Y)
 //   x pass: lines z, positions x, fixed y      (in Y,  out X)
 // The window comes from one TMA tensor copy issued by thread 0.
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL, int TAPS>
 __global__ void __launch_bounds__(32 * (RHO + 1))
 sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos_lo, int pos_end,
-                const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps) {
+                const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps,
+                int accumulate) {
   using I = SepIdx<RHO>;
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(
       smraw + ((1024 - ((unsigned)__cvta_generic_to_shared(smraw) & 1023)) & 1023));
   constexpr int R1 = RHO + 1;
-  float* Kt = sm + pass_win_floats<RHO, PASS, POS>();
+  float* Kt = sm + pass_win_floats<RHO, PASS, POS, NL>();
   uint64_t* bar = reinterpret_cast<uint64_t*>(Kt + 7 * 8 * R1);
   const int64_t plane = (int64_t)res * res * res;
   const int out_entries = PASS == PASS_X ? I::P : I::T;
-  const Tile T = decode_tile<R1>(lres, line_lo, pos_lo, POS);
+  const Tile T = decode_tile<R1>(lres, line_lo, pos_lo, POS, NL);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
   {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
-                   "r"(window_bytes<RHO, PASS, POS>(T.part)));
+                   "r"(window_bytes<RHO, PASS, POS, NL>(T.part)));
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm);
       const CUtensorMap* mp = &maps.m[T.part];
       if (PASS == PASS_Z)
@@ -505,7 +525,8 @@ sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos
         : "memory");
   }
   __syncthreads();
-  compute_tile<RHO, PASS, POS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res, pos_end, T);
+  compute_tile<RHO, PASS, POS, NL, TAPS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res,
+                                         pos_end, T, accumulate != 0);
 }
 
 template <int RHO>
@@ -538,7 +559,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 // tensor maps of one pass over `base` (one per partition); false on failure
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL>
 bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
   using I = SepIdx<RHO>;
   constexpr int R1 = RHO + 1;
@@ -557,7 +578,7 @@ bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
       dims[3] = I::NAB;
       dims[4] = (cuuint64_t)C * R1;
       strides[3] = (cuuint64_t)I::NAB * r * r * r * f;
-      box[0] = 16; box[1] = kLines; box[2] = 1; box[3] = R1 - part; box[4] = R1;
+      box[0] = 16; box[1] = NL; box[2] = 1; box[3] = R1 - part; box[4] = R1;
       sw = CU_TENSOR_MAP_SWIZZLE_64B;
     } else {
       const int ent = PASS == PASS_Z ? I::P : I::T;
@@ -565,7 +586,7 @@ bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
       dims[3] = (cuuint64_t)C * ent;
       dims[4] = 1;
       strides[3] = dims[3] * r * r * r * f;
-      box[0] = kLines;
+      box[0] = NL;
       box[1] = PASS == PASS_Z ? win_of(POS) : 1;
       box[2] = PASS == PASS_Z ? 1 : win_of(POS);
       box[3] = ne;
@@ -579,52 +600,118 @@ bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
   return true;
 }
 
-template <int RHO, int PASS, int POS>
+template <int RHO, int PASS, int POS, int NL, int TAPS>
 cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                             int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                            cudaStream_t s) {
-  const int nlt = (line_hi - line_lo + kLines - 1) / kLines;
+                            cudaStream_t s, int accumulate) {
+  const int nlt = (line_hi - line_lo + NL - 1) / NL;
   const int npt = (pos_hi - pos_lo + POS - 1) / POS;
   if ((int64_t)nlt * npt * res * (RHO + 1) * C <= 0) return cudaSuccess;
   int lres = 0;
   while ((1 << lres) < res) ++lres;
   const dim3 grid((unsigned)nlt, (unsigned)npt, (unsigned)(res * (RHO + 1) * C));
-  constexpr int smem = pass_smem_floats<RHO, PASS, POS>() * (int)sizeof(float);
+  constexpr int smem = pass_smem_floats<RHO, PASS, POS, NL>() * (int)sizeof(float);
   static unsigned long long configured = 0;
   if (smem > 48 * 1024 && attr_needed(configured))
-    cudaFuncSetAttribute(sep_pass_kernel<RHO, PASS, POS>,
+    cudaFuncSetAttribute(sep_pass_kernel<RHO, PASS, POS, NL, TAPS>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // the maps depend on (base, res, C) only; workspaces come back at the same
+  // address call after call, so keep the last few encodings
+  struct Cached {
+    const float* base = nullptr;
+    int res = 0, C = 0;
+    SepMaps maps;
+  };
+  static std::mutex mu;
+  static Cached cache[8];
+  static unsigned next = 0;
   SepMaps maps;
-  std::memset(&maps, 0, sizeof(maps));
-  if (!encode_maps<RHO, PASS, POS>(maps, in, res, C)) return cudaErrorNotSupported;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    const Cached* hit = nullptr;
+    for (const Cached& c : cache)
+      if (c.base == in && c.res == res && c.C == C) hit = &c;
+    if (!hit) {
+      Cached& c = cache[next++ % 8];
+      c.base = nullptr;
+      std::memset(&c.maps, 0, sizeof(c.maps));
+      if (!encode_maps<RHO, PASS, POS, NL>(c.maps, in, res, C)) return cudaErrorNotSupported;
+      c.base = in;
+      c.res = res;
+      c.C = C;
+      hit = &c;
+    }
+    maps = hit->maps;
+  }
   FC2T2_LAUNCH(name, s,
-               sep_pass_kernel<RHO, PASS, POS><<<grid, 32 * (RHO + 1), smem, s>>>(
-                   out, res, lres, line_lo, pos_lo, pos_hi, prm, maps));
+               (sep_pass_kernel<RHO, PASS, POS, NL, TAPS><<<grid, 32 * (RHO + 1), smem, s>>>(
+                   out, res, lres, line_lo, pos_lo, pos_hi, prm, maps, accumulate)));
   return cudaGetLastError();
 }
 
-template <int RHO, int PASS>
+// 32 lines per tile, or 16 on a 16-cell grid (the far table of a coarse level)
+template <int RHO, int PASS, int TAPS = TAPS_ALL>
 cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                         int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                        cudaStream_t s) {
-  return launch_pass_pos<RHO, PASS, 8>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi, prm,
-                                       name, s);
+                        cudaStream_t s, int accumulate = 0) {
+  if (res >= kLines)
+    return launch_pass_pos<RHO, PASS, 8, kLines, TAPS>(in, out, res, C, line_lo, line_hi, pos_lo,
+                                                       pos_hi, prm, name, s, accumulate);
+  return launch_pass_pos<RHO, PASS, 8, 16, TAPS>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi,
+                                                 prm, name, s, accumulate);
 }
 
 template <int RHO>
 cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                         const double* conv, const float* M, float* L, float* wa, float* wb,
-                        int x_begin, int x_end, int stages, const float* coarse,
+                        int x_begin, int x_end, int stages, const float* coarse, bool far_only,
                         cudaStream_t s) {
   const int res = 1 << (level + 1);
-  if (res % kLines) return cudaErrorInvalidValue;
+  const int nl = std::min(res, kLines);
+  if (res % nl || res < 16) return cudaErrorInvalidValue;
   const SepParams<RHO> prm = to_params<RHO>(pre, post, conv);
   // x range the z/y passes must cover: the slab plus the x pass's halo,
-  // widened to whole 32-line tiles
-  const int xl = std::max(0, x_begin - 3) / kLines * kLines;
-  const int xh = std::min(res, (x_end + 3 + kLines - 1) / kLines * kLines);
+  // widened to whole line tiles
+  const int xl = std::max(0, x_begin - 3) / nl * nl;
+  const int xh = std::min(res, (x_end + 3 + nl - 1) / nl * nl);
   cudaError_t err;
-  if (stages & SEP_FRONT) {
+  if ((stages & SEP_FRONT) && far_only) {
+    // The far table of a coarse level: the parity box minus the hole
+    // {-1,0,1}^3 as three disjoint separable pieces (no cancellation against
+    // the large hole terms).  With the per-axis tap sets A = parity box,
+    // F = {|d| >= 2}, N = {|d| <= 1} over (x, y, z):
+    //   F x A x A  +  N x F x A  +  N x N x F
+    // z passes A and F of M'; y passes A(Z_A), F(Z_A) + N(Z_F); x passes
+    // F(Y_AA) + N(Y_FA+NF).
+    const size_t tb = (size_t)SepIdx<RHO>::T * res * res * res * C;
+    float *b0 = wa, *b1 = wb, *b2 = wb + tb, *b3 = wb + 2 * tb;
+    const int64_t n = (int64_t)(xh - xl) * res * res * C;
+    FC2T2_LAUNCH("m2l_sepfar_pre", s,
+                 sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+                     M, b0, res, C, xl, xh - xl, prm));
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+    if ((err = launch_pass<RHO, PASS_Z, TAPS_ALL>(b0, b1, res, C, xl, xh, 0, res, prm,
+                                                  "m2l_sepfar_z", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Z, TAPS_FAR>(b0, b2, res, C, xl, xh, 0, res, prm,
+                                                  "m2l_sepfar_z", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y, TAPS_ALL>(b1, b0, res, C, xl, xh, 0, res, prm,
+                                                  "m2l_sepfar_y", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y, TAPS_FAR>(b1, b3, res, C, xl, xh, 0, res, prm,
+                                                  "m2l_sepfar_y", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_Y, TAPS_NEAR>(b2, b3, res, C, xl, xh, 0, res, prm,
+                                                   "m2l_sepfar_y", s, 1)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_X, TAPS_FAR>(b0, b1, res, C, 0, res, x_begin, x_end, prm,
+                                                  "m2l_sepfar_x", s)))
+      return err;
+    if ((err = launch_pass<RHO, PASS_X, TAPS_NEAR>(b3, b1, res, C, 0, res, x_begin, x_end, prm,
+                                                   "m2l_sepfar_x", s, 1)))
+      return err;
+  } else if (stages & SEP_FRONT) {
     const int64_t n = (int64_t)(xh - xl) * res * res * C;
     FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                                        M, wa, res, C, xl, xh - xl, prm));
@@ -654,23 +741,23 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
 
 void* tensor_map_encoder() { return reinterpret_cast<void*>(tmap_encoder()); }
 
-size_t m2l_sep_workspace_floats(int rho, int level, int C) {
+size_t m2l_sep_workspace_floats(int rho, int level, int C, bool far_only) {
   const int64_t res = 1 << (level + 1);
   const int64_t R1 = rho + 1, T = R1 * (R1 + 1) / 2 * R1;
-  return (size_t)(2 * T * res * res * res * C);
+  return (size_t)((far_only ? 4 : 2) * T * res * res * res * C);
 }
 
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,
                     const double* conv, const float* M, float* L, float* ws, int x_begin,
-                    int x_end, cudaStream_t s, int stages, const float* coarse) {
+                    int x_end, cudaStream_t s, int stages, const float* coarse, bool far_only) {
   const int64_t res = 1 << (level + 1);
   if (x_end < 0) x_end = (int)res;
   float* wa = ws;
-  float* wb = ws + m2l_sep_workspace_floats(rho, level, C) / 2;
+  float* wb = ws + m2l_sep_workspace_floats(rho, level, C, false) / 2;
 #define FC2T2_SEP_RHO(R)                                                                   \
   case R:                                                                                  \
     return m2l_sep_rho<R>(level, C, pre, post, conv, M, L, wa, wb, x_begin, x_end, stages, \
-                          coarse, s);
+                          coarse, far_only, s);
   switch (rho) {
     FC2T2_SEP_RHO(1)
     FC2T2_SEP_RHO(2)

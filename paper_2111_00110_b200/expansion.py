@@ -30,7 +30,7 @@ import torch
 
 from . import _lib, flops
 from .kernel import (COARSEST_LEVEL, KernelModel, M2LTable, fit_m2l_tables,
-                     separable_eligible, separable_factors,
+                     separable_eligible, separable_factors, separable_far_eligible,
                      level_box_width, level_resolution)
 from .multiindex import MultiIndexTable
 
@@ -444,6 +444,12 @@ class Engine:
             self.m2l_tables, levels, self.rho, lsq, nodes_per_axis)
         self._sep = (separable_factors(kernel, levels, lsq, nodes_per_axis)
                      if self.separable else None)
+        # coarse levels' far tables through their own per-axis factors (the
+        # parity box minus the hole as three disjoint separable pieces)
+        self._sep_far = {l: separable_factors(kernel, l, lsq, nodes_per_axis)
+                         for l in range(COARSEST_LEVEL + 1, levels)
+                         if separable and separable_far_eligible(
+                             self.m2l_tables, l, levels, self.rho, lsq, nodes_per_axis)}
 
     # the device side is created lazily so the host tables can be built
     # (and pinned by CPU tests) without a GPU
@@ -465,6 +471,11 @@ class Engine:
                 _lib.check(h.lib.fc2t2_engine_set_separable(
                     h.h, f["pre"].ctypes.data, f["post"].ctypes.data, f["conv"].ctypes.data),
                     "engine_set_separable")
+            for lvl, fac in self._sep_far.items():
+                f = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in fac.items()}
+                _lib.check(h.lib.fc2t2_engine_set_separable_far(
+                    h.h, int(lvl), f["pre"].ctypes.data, f["post"].ctypes.data,
+                    f["conv"].ctypes.data), "engine_set_separable_far")
             self._h = h
             self._flag = DomainFlag()
         return self._h.h

@@ -337,6 +337,27 @@ def fit_m2l_tables(kernel: KernelModel, levels: int, lsq: bool = True,
 # (measured 1.3e-7 rel-L2 per coefficient vs the float64 tables; the
 # monomial-basis form inv(H) (x) K (x) inv(H) loses 2e-3).
 
+def separable_far_eligible(tables: dict, level: int, levels: int, rho: int, lsq: bool = True,
+                           nodes_per_axis: int = 6) -> bool:
+    """A coarse level's far table (parity stencil minus the hole, reference
+    expansion.py:246-249) runs separably (three disjoint per-axis pieces,
+    csrc/m2l_sep.cu) when the grid is at least 16 cells wide, the per-axis fit
+    is full rank and the level has work.  Offsets the reference prunes have a
+    peak interaction below PRUNE_TOL (interaction_mask); the separable form
+    includes them, a change below 1e-16 of the kernel peak per unit weight."""
+    if not (COARSEST_LEVEL < level < levels) or level_resolution(level) < 16:
+        return False
+    if lsq and rho + 1 > nodes_per_axis:
+        return False
+    if rho > 5:
+        return False
+    far = tables["far"][level]
+    hole = np.abs(far.offsets).max(axis=1) <= 1
+    return bool(far.active.any() and np.array_equal(far.hole, hole)
+                and not (far.active & far.hole).any()
+                and np.abs(far.offsets).max() == FAR_REACH)
+
+
 def separable_factors(kernel: KernelModel, level: int, lsq: bool = True,
                       nodes_per_axis: int = 6) -> dict:
     """Per-axis factors of the finest-level tables: ``pre`` (R^{-T}, lower

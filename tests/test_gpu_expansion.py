@@ -603,3 +603,43 @@ def test_sharded_layer_single_rank_matches_layers(eng4):
     assert rs.q_grad is not None
     assert torch.equal(rs.values, rl.values)
     assert torch.equal(qb, g.q_bar) and torch.equal(wb, g.w_bar) and torch.equal(pb, g.p_bar)
+
+
+# ------------------------------------------- separable far tables (coarse) ---
+
+@pytest.mark.parametrize("alpha,levels,rho,level,C", [
+    (1000.0, 5, 4, 4, 1),     # config 2: level 4 (32^3), 308 of 316 offsets active
+    (1000.0, 5, 4, 3, 2),     # config 2: level 3 (16^3, 16-line tiles), 90 active
+    (200.0, 4, 4, 3, 1),      # config 1: level 3, 308 active
+    (60.0, 5, 3, 4, 1),       # wide kernel: every offset active
+])
+def test_separable_far_matches_dense_and_oracle(cuda, alpha, levels, rho, level, C):
+    """A coarse level's far table through its per-axis factors (three disjoint
+    separable pieces, csrc/m2l_sep.cu) against the dense tables of the same
+    engine configuration and the float64 oracle (ref expansion.py:227-264)."""
+    from paper_2111_00110_b200 import Engine, KernelModel
+    k = KernelModel("gaussian", alpha, rho)
+    eng = Engine(k, levels, check_admissibility=False)
+    dense = Engine(k, levels, check_admissibility=False, separable=False)
+    assert level in eng._sep_far and not dense._sep_far
+    ora = Oracle(alpha, rho, levels)
+    rng = np.random.default_rng(77 + level)
+    m = eng.zero_grid(level, C, "M")
+    # moment-like magnitudes: degree-n entries scale like (h/2)^n
+    h = 2.0 / (1 << (level + 1))
+    deg = eng.table.entries.sum(axis=1)
+    mdata = (rng.normal(size=tuple(m.data.shape)) * (h / 2) ** deg).astype(np.float32)
+    m.data[:] = torch.from_numpy(mdata).cuda()
+    md = dense.zero_grid(level, C, "M")
+    md.data[:] = m.data
+    sep = _np(eng.m2l(m, eng.m2l_tables["far"][level]).data)
+    den = _np(dense.m2l(md, dense.m2l_tables["far"][level]).data)
+    ref = ora.m2l(mdata.astype(np.float64), ora.tables["far"][level])
+    assert rel_l2(den, ref) < 1e-5
+    assert rel_l2(sep, ref) < 2e-6
+    # coefficient by coefficient (the degrees differ by orders of magnitude)
+    for j in range(sep.shape[-1]):
+        assert rel_l2(sep[..., j], ref[..., j]) < 1e-5, j
+    # deterministic
+    again = _np(eng.m2l(m, eng.m2l_tables["far"][level]).data)
+    assert np.array_equal(sep, again)
