@@ -67,6 +67,10 @@ const char* fc2t2_last_error(void);
 int64_t fc2t2_launch_count(void);
 int fc2t2_profile_enable(int on);
 int fc2t2_profile_read(int max_entries, char* names, double* ms, int64_t* counts);
+/* The recorded launches one by one, in issue order: names (32 bytes each) and
+ * the begin / end event times in ms relative to the first launch's begin
+ * event (a device timeline across the library's streams).  Returns the count. */
+int fc2t2_profile_timeline(int max_entries, char* names, double* begin_ms, double* end_ms);
 
 /* ---- engine: replaces Engine.__init__ table state (expansion.py:157-177) ---- */
 int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out);

@@ -33,6 +33,7 @@ _SIGS = {
     "fc2t2_launch_count": (_i64, []),
     "fc2t2_profile_enable": (_i32, [_i32]),
     "fc2t2_profile_read": (_i32, [_i32, _vp, _vp, _vp]),
+    "fc2t2_profile_timeline": (_i32, [_i32, _vp, _vp, _vp]),
     "fc2t2_engine_create": (_i32, [_i32, _i32, ct.POINTER(_vp)]),
     "fc2t2_engine_destroy": (None, [_vp]),
     "fc2t2_engine_set_table": (_i32, [_vp, _i32, _i32, _i64, _vp, _vp, _vp]),
@@ -144,6 +145,21 @@ def check(code: int, what: str = "") -> None:
         rmsg = lib().fc2t2_ray_last_error().decode(errors="replace")
         msg = rmsg if rmsg and not msg else (msg + ("; " + rmsg if rmsg else ""))
         raise _exc_for(code)(f"{what}: {msg}" if what else msg)
+
+
+def profile_timeline(max_entries: int = 512) -> list:
+    """[(kernel name, begin ms, end ms)] of the launches recorded since
+    profile_enable(True), in issue order, relative to the first one."""
+    import numpy as np
+    names = ct.create_string_buffer(32 * max_entries)
+    t0 = np.zeros(max_entries, dtype=np.float64)
+    t1 = np.zeros(max_entries, dtype=np.float64)
+    n = lib().fc2t2_profile_timeline(max_entries, names, t0.ctypes.data, t1.ctypes.data)
+    if n < 0:
+        check(ECUDA, "profile_timeline")
+    raw = names.raw
+    return [(raw[32 * k:32 * (k + 1)].split(b"\0", 1)[0].decode(), float(t0[k]), float(t1[k]))
+            for k in range(n)]
 
 
 def launch_count() -> int:

@@ -429,6 +429,23 @@ int fc2t2_profile_read(int max_entries, char* names, double* ms, int64_t* counts
   return n;
 }
 
+int fc2t2_profile_timeline(int max_entries, char* names, double* begin_ms, double* end_ms) {
+  const int n = (int)std::min<size_t>(fc2t2::g_recs.size(), (size_t)max_entries);
+  if (n == 0) return 0;
+  const cudaEvent_t t0 = fc2t2::g_recs[0].a;
+  for (int k = 0; k < n; ++k) {
+    const auto& r = fc2t2::g_recs[k];
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return fail(FC2T2_ECUDA, "profile sync");
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, t0, r.a);
+    cudaEventElapsedTime(&b, t0, r.b);
+    std::snprintf(names + 32 * k, 32, "%s", r.name);
+    begin_ms[k] = a;
+    end_ms[k] = b;
+  }
+  return n;
+}
+
 const char* fc2t2_last_error(void) { return g_last_error.c_str(); }
 
 int fc2t2_engine_create(int rho, int levels, fc2t2_engine** out) {

@@ -33,6 +33,8 @@
 // 2 x 4 RS (K3 out, K4 in), RS = record floats; plus the grid write.  No
 // random gathers (the round-1 cell sort + gather P2M read every point through
 // an index).
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -215,6 +217,86 @@ brick_start_kernel(const uint32_t* __restrict__ tot, int nb, uint32_t* __restric
     run += tot[b0 + k];
   }
   if (threadIdx.x == blockDim.x - 1) brick_start[nb] = total;
+}
+
+// Small inputs (nt <= kSmallScanTiles): S1-S3 and the brick starts in one
+// launch -- a CTA per 32 bricks scans all their tiles (32 warps x nt / 32 tiles),
+// the brick totals meet at a grid barrier (at most 128 CTAs, all resident;
+// the counters reset themselves; one slot per launch in flight), and every
+// CTA derives its bricks' starts from the totals before it.  Same cnt / tot /
+// brick_start contents as the four-kernel path.
+constexpr int kSmallScanTiles = 2048;
+constexpr int kScanSlots = 32;
+__device__ unsigned int g_scan_sync[kScanSlots][2];
+
+__global__ void __launch_bounds__(1024)
+brick_scan_small_kernel(uint32_t* __restrict__ cnt, int nt, int nb, uint32_t* __restrict__ tot,
+                        uint32_t* __restrict__ brick_start, int slot) {
+  __shared__ uint32_t ws[32][32];
+  __shared__ uint32_t red[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + lane;
+  const int per = (nt + 31) / 32;
+  const int t0 = w * per, t1 = min(nt, t0 + per);
+  uint32_t s = 0;
+  if (b < nb)
+#pragma unroll 16
+    for (int t = t0; t < t1; ++t) s += cnt[(size_t)t * nb + b];
+  ws[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && b < nb) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) t += ws[q][lane];
+    tot[b] = t;
+  }
+  // grid barrier: every CTA's totals are visible past it
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&g_scan_sync[slot][0], 1u);
+    while (*reinterpret_cast<volatile unsigned int*>(&g_scan_sync[slot][0]) < gridDim.x) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  // the totals of the bricks before this CTA's
+  uint32_t part = 0;
+  for (int i = threadIdx.x; i < (int)blockIdx.x * 32; i += blockDim.x) part += __ldcg(tot + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[w] = part;
+  __syncthreads();
+  uint32_t base = 0;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) base += red[q];
+  const uint32_t mine = b < nb ? __ldcg(tot + b) : 0u;
+  uint32_t x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  const uint32_t start = base + x - mine;
+  if (w == 0 && b < nb) {
+    brick_start[b] = start;
+    if (b == nb - 1) brick_start[nb] = start + mine;
+  }
+  if (b < nb) {
+    uint32_t run = start;
+    for (int q = 0; q < w; ++q) run += ws[q][lane];
+    for (int t = t0; t < t1; ++t) {
+      const uint32_t v = cnt[(size_t)t * nb + b];
+      cnt[(size_t)t * nb + b] = run;
+      run += v;
+    }
+  }
+  // the last CTA out resets the slot
+  if (threadIdx.x == 0 && atomicAdd(&g_scan_sync[slot][1], 1u) == gridDim.x - 1) {
+    g_scan_sync[slot][0] = 0u;
+    g_scan_sync[slot][1] = 0u;
+    __threadfence();
+  }
 }
 
 // ------------------------------------------------------------------- K3 ---
@@ -842,6 +924,13 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
                                                                             b.cnt, flag));
   const int nseg = (int)((nt + SEG_T - 1) / SEG_T);
   const dim3 sgrid((unsigned)((g.nb + 31) / 32), (unsigned)nseg);
+  if (nt <= kSmallScanTiles && (g.nb + 31) / 32 <= 128) {
+    static std::atomic<unsigned> next_slot{0};
+    const int slot = (int)(next_slot.fetch_add(1, std::memory_order_relaxed) % kScanSlots);
+    FC2T2_LAUNCH("brick_scan", s,
+                 brick_scan_small_kernel<<<(unsigned)((g.nb + 31) / 32), 1024, 0, s>>>(
+                     b.cnt, (int)nt, g.nb, b.tot, b.bstart, slot));
+  } else {
   FC2T2_LAUNCH("brick_scan", s,
                brick_segsum_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part));
   FC2T2_LAUNCH("brick_scan", s,
@@ -849,6 +938,7 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
   FC2T2_LAUNCH("brick_scan", s, brick_start_kernel<<<1, 1024, 0, s>>>(b.tot, g.nb, b.bstart));
   FC2T2_LAUNCH("brick_scan", s,
                brick_segfill_kernel<<<sgrid, 256, 0, s>>>(b.cnt, (int)nt, g.nb, b.part, b.bstart));
+  }
   }
   if (!(phase & P2M_FINISH)) return cudaGetLastError();
   if (n > 0 && rk)
