@@ -151,6 +151,46 @@ m2m_kernel(const float* __restrict__ fine, float* __restrict__ coarse, int C, in
   }
 }
 
+// M2M with a thread per child: the 8 children of a parent sit in 8 adjacent
+// lanes (child = lane & 7, x slowest), each shifts its own row, and an xor
+// butterfly over the 8 lanes forms the parent's sum -- (c0+c1)+(c2+c3) +
+// (c4+c5)+(c6+c7), the same tree in every lane -- 8x the threads of the
+// per-parent loop on these small grids.
+template <int RHO>
+__global__ void __launch_bounds__(256)
+m2m_child_kernel(const float* __restrict__ fine, float* __restrict__ coarse, int C, int cres,
+                 float half_fine, int64_t g0, int64_t g1) {
+  constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
+  const int fres = 2 * cres;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int ch = (int)(t & 7);
+  const int64_t gq = g0 + (t >> 3);
+  const bool valid = gq < g1;
+  const int64_t g = valid ? gq : g1 - 1;
+  const int64_t cell = g / C;
+  const int c = (int)(g - cell * C);
+  const int Z = (int)(cell % cres), Y = (int)((cell / cres) % cres), X = (int)(cell / cres / cres);
+  const int cx = ch >> 2, cy = (ch >> 1) & 1, cz = ch & 1;
+  const int64_t fc = (((int64_t)(2 * X + cx) * fres + (2 * Y + cy)) * fres + (2 * Z + cz));
+  float f[PP];
+  load_row<PP>(fine + (fc * C + c) * PP, f);
+  float v[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] = f[j];
+  shift3<RHO, true>(v, cx ? half_fine : -half_fine, cy ? half_fine : -half_fine,
+                    cz ? half_fine : -half_fine);
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1)
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+  if (valid && ch == 0) {
+    float out[PP];
+#pragma unroll
+    for (int j = 0; j < PP; ++j) out[j] = j < P ? v[j] : 0.f;
+    store_row<PP>(coarse + g * PP, out, false);
+  }
+}
+
 template <int RHO>
 __global__ void __launch_bounds__(128)
 l2l_kernel(const float* __restrict__ coarse, float* __restrict__ fine, int C, int cres,
@@ -351,6 +391,14 @@ cudaError_t m2m(int rho, int fine_level, int C, const float* fine, float* coarse
   const int64_t g0 = cx_begin * plane, g1 = cx_end * plane;
   if (g1 <= g0) return cudaSuccess;
   const float half_fine = (float)(0.5 * 2.0 / (double)(2 * cres));
+  // grids of up to 64^3 parents: a thread per child (latency bound otherwise)
+  if (cres <= 64) {
+    const int64_t threads = (g1 - g0) * 8;
+    FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("m2m", s,
+        m2m_child_kernel<RHO><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+            fine, coarse, C, cres, half_fine, g0, g1)));
+    return cudaGetLastError();
+  }
   FC2T2_DISPATCH_RHO(rho, FC2T2_LAUNCH("m2m", s,
       m2m_kernel<RHO><<<grid_blocks(g1 - g0, 128, 148 * 64), 128, 0, s>>>(fine, coarse, C, cres,
                                                                           half_fine, g0, g1)));
