@@ -104,7 +104,7 @@ cudaError_t m2l_tc(int rho, int C, const TCPlan& plan, const void* ws, float* L,
 // L = L2L(coarse) + M2L).  The two may run on different streams.
 enum { SEP_FRONT = 1, SEP_POST = 2, SEP_ALL = 3 };
 // far_only: the far table of a coarse level (grids of >= 16 cells): the parity
-// box minus the hole as three disjoint separable pieces (7 passes, 4 scratch
+// box minus the hole as three disjoint separable pieces (5 passes, 4 scratch
 // buffers instead of 2); pre/post/conv are that level's factors.
 size_t m2l_sep_workspace_floats(int rho, int level, int C, bool far_only = false);
 cudaError_t m2l_sep(int rho, int level, int C, const double* pre, const double* post,

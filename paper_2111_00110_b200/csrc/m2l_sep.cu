@@ -227,7 +227,7 @@ sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int
 // Every contraction is sum_{d, i} K(d)[j][i] in_i(pos + d).
 
 enum { PASS_Z = 0, PASS_Y = 1, PASS_X = 2 };
-enum { TAPS_ALL = 0, TAPS_FAR = 1, TAPS_NEAR = 2 };
+enum { TAPS_ALL = 0, TAPS_FAR = 1, TAPS_NEAR = 2, TAPS_NONE = 3 };
 
 template <int RHO, int PASS, int PART>
 struct Part {
@@ -256,18 +256,11 @@ struct Part {
 // small code paths (instruction-cache resident); the K(d)[.][i] column of an
 // input comes from shared memory (Kt[i][d][j], warp-uniform broadcast).
 template <int RHO, int PASS, int POS, int NL, int TAPS, int NOUT>
-__device__ __forceinline__ void group_body(const float* sm, const float* Kt, int ne, int lane,
-                                           int nin, int in_base, int in_stride,
-                                           const int (&oe)[RHO + 1], float* out,
-                                           int64_t pos_stride, int64_t plane, int nvalid,
-                                           bool accumulate) {
+__device__ __forceinline__ void accum_input(float (&acc)[POS][NOUT], const float* sm,
+                                            const float* Kt, int lane, int nin, int in_base,
+                                            int in_stride) {
   constexpr int OFF = PASS == PASS_X ? 4 : 3;
   constexpr int NQ = PASS == PASS_X ? POS + 8 : win_of(POS);
-  float acc[POS][NOUT];
-#pragma unroll
-  for (int w = 0; w < POS; ++w)
-#pragma unroll
-    for (int j = 0; j < NOUT; ++j) acc[w][j] = 0.f;
 #pragma unroll 1
   for (int i = 0; i < nin; ++i) {
     const int le = in_base + i * in_stride;
@@ -316,26 +309,30 @@ __device__ __forceinline__ void group_body(const float* sm, const float* Kt, int
       }
     }
   }
+}
+
+// TAPS1 != TAPS_NONE: a second window (sm1, same layout) contributes with its
+// own tap subset to the same outputs -- the two-term pieces of a far table.
+template <int RHO, int PASS, int POS, int NL, int TAPS0, int TAPS1, int NOUT>
+__device__ __forceinline__ void group_body(const float* sm0, const float* sm1, const float* Kt,
+                                           int lane, int nin, int in_base, int in_stride,
+                                           const int (&oe)[RHO + 1], float* out,
+                                           int64_t pos_stride, int64_t plane, int nvalid) {
+  float acc[POS][NOUT];
+#pragma unroll
+  for (int w = 0; w < POS; ++w)
+#pragma unroll
+    for (int j = 0; j < NOUT; ++j) acc[w][j] = 0.f;
+  accum_input<RHO, PASS, POS, NL, TAPS0, NOUT>(acc, sm0, Kt, lane, nin, in_base, in_stride);
+  if constexpr (TAPS1 != TAPS_NONE)
+    accum_input<RHO, PASS, POS, NL, TAPS1, NOUT>(acc, sm1, Kt, lane, nin, in_base, in_stride);
   // 32-bit offsets from `out` (a channel block holds < 2^31 floats); the
   // positions are pos_stride apart
   int ob[NOUT];
 #pragma unroll
   for (int j = 0; j < NOUT; ++j) ob[j] = oe[j] * (int)plane;
   const int ps = (int)pos_stride;
-  if (accumulate) {
-    // all the loads first (one round trip), then the sums and stores
-#pragma unroll
-    for (int w = 0; w < POS; ++w)
-#pragma unroll
-      for (int j = 0; j < NOUT; ++j)
-        acc[w][j] = (w < nvalid ? __ldcg(out + ob[j] + w * ps) : 0.f) + acc[w][j];
-#pragma unroll
-    for (int w = 0; w < POS; ++w)
-      if (w < nvalid) {
-#pragma unroll
-        for (int j = 0; j < NOUT; ++j) out[ob[j] + w * ps] = acc[w][j];
-      }
-  } else if (nvalid == POS) {
+  if (nvalid == POS) {
 #pragma unroll
     for (int w = 0; w < POS; ++w)
 #pragma unroll
@@ -368,9 +365,9 @@ __device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, i
   return r;
 }
 
-template <int RHO, int PASS, int POS, int NL, int TAPS>
-__device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, float* dst, int res,
-                                             int pos_end, const Tile& T, bool accumulate) {
+template <int RHO, int PASS, int POS, int NL, int TAPS, int TAPS1>
+__device__ __forceinline__ void compute_tile(const float* sm, const float* sm1, const float* Kt,
+                                             float* dst, int res, int pos_end, const Tile& T) {
   using I = SepIdx<RHO>;
   constexpr int R1 = RHO + 1;
   const int64_t plane = (int64_t)res * res * res;
@@ -420,8 +417,9 @@ __device__ __forceinline__ void compute_tile(const float* sm, const float* Kt, f
 #define FC2T2_SEP_N(Q)                                                                     \
   case Q:                                                                                  \
     if constexpr (Q <= R1)                                                                 \
-      group_body<RHO, PASS, POS, NL, TAPS, Q>(sm, Kt, ne, lane, nin, in_base, in_stride, oe, o, \
-                                              pos_stride, plane, nvalid, accumulate);       \
+      group_body<RHO, PASS, POS, NL, TAPS, TAPS1, Q>(sm, sm1, Kt, lane, nin, in_base,          \
+                                                     in_stride, oe, o, pos_stride, plane,     \
+                                                     nvalid);                                 \
     break;
   switch (nout) {
     FC2T2_SEP_N(1)
@@ -442,9 +440,9 @@ constexpr int pass_win_floats() {
   return PASS == PASS_X ? R1 * R1 * NL * 16
                         : win_of(POS) * (PASS == PASS_Z ? R1 * (R1 + 1) / 2 : R1 * R1) * NL;
 }
-template <int RHO, int PASS, int POS, int NL>
-constexpr int pass_smem_floats() {  // window + Kt[i][d][8] + mbarrier + 1 KB alignment slack
-  return pass_win_floats<RHO, PASS, POS, NL>() + 7 * 8 * (RHO + 1) + 2 + 256;
+template <int RHO, int PASS, int POS, int NL, int NWIN = 1>
+constexpr int pass_smem_floats() {  // window(s) + Kt[i][d][8] + mbarrier + 1 KB alignment slack
+  return NWIN * pass_win_floats<RHO, PASS, POS, NL>() + 7 * 8 * (RHO + 1) + 2 + 256;
 }
 
 // TMA: one tensor map per partition (box = the partition's window); the
@@ -478,17 +476,19 @@ __device__ __forceinline__ uint32_t window_bytes(int part) {
 //   y pass: lines x, positions y, fixed z      (in Z,  out Y)
 //   x pass: lines z, positions x, fixed y      (in Y,  out X)
 // The window comes from one TMA tensor copy issued by thread 0.
-template <int RHO, int PASS, int POS, int NL, int TAPS>
+template <int RHO, int PASS, int POS, int NL, int TAPS, int TAPS1>
 __global__ void __launch_bounds__(32 * (RHO + 1))
 sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos_lo, int pos_end,
                 const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps,
-                int accumulate) {
+                const __grid_constant__ SepMaps maps1) {
   using I = SepIdx<RHO>;
   extern __shared__ __align__(16) unsigned char smraw[];
   float* sm = reinterpret_cast<float*>(
       smraw + ((1024 - ((unsigned)__cvta_generic_to_shared(smraw) & 1023)) & 1023));
   constexpr int R1 = RHO + 1;
-  float* Kt = sm + pass_win_floats<RHO, PASS, POS, NL>();
+  constexpr int NWIN = TAPS1 == TAPS_NONE ? 1 : 2;
+  float* sm1 = sm + pass_win_floats<RHO, PASS, POS, NL>();
+  float* Kt = sm + NWIN * pass_win_floats<RHO, PASS, POS, NL>();
   uint64_t* bar = reinterpret_cast<uint64_t*>(Kt + 7 * 8 * R1);
   const int64_t plane = (int64_t)res * res * res;
   const int out_entries = PASS == PASS_X ? I::P : I::T;
@@ -499,17 +499,21 @@ sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
-                   "r"(window_bytes<RHO, PASS, POS, NL>(T.part)));
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm);
-      const CUtensorMap* mp = &maps.m[T.part];
-      if (PASS == PASS_Z)
-        tma_load_5d(dst, mp, T.line0, T.pos0 - 3, T.fixed, T.ch * I::P + I::ab(T.part, 0), 0,
-                    bar_s);
-      else if (PASS == PASS_Y)
-        tma_load_5d(dst, mp, T.line0, T.fixed, T.pos0 - 3, T.ch * I::T + I::pair(T.part, 0) * R1,
-                    0, bar_s);
-      else
-        tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(T.part, 0), T.ch * R1, bar_s);
+                   "r"(NWIN * window_bytes<RHO, PASS, POS, NL>(T.part)));
+#pragma unroll
+      for (int wi = 0; wi < NWIN; ++wi) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(wi ? sm1 : sm);
+        const CUtensorMap* mp = wi ? &maps1.m[T.part] : &maps.m[T.part];
+        if (PASS == PASS_Z)
+          tma_load_5d(dst, mp, T.line0, T.pos0 - 3, T.fixed, T.ch * I::P + I::ab(T.part, 0), 0,
+                      bar_s);
+        else if (PASS == PASS_Y)
+          tma_load_5d(dst, mp, T.line0, T.fixed, T.pos0 - 3,
+                      T.ch * I::T + I::pair(T.part, 0) * R1, 0, bar_s);
+        else
+          tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(T.part, 0), T.ch * R1,
+                      bar_s);
+      }
     }
   }
   // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads),
@@ -525,8 +529,9 @@ sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos
         : "memory");
   }
   __syncthreads();
-  compute_tile<RHO, PASS, POS, NL, TAPS>(sm, Kt, out + (int64_t)T.ch * out_entries * plane, res,
-                                         pos_end, T, accumulate != 0);
+  compute_tile<RHO, PASS, POS, NL, TAPS, TAPS1>(sm, sm1, Kt,
+                                                out + (int64_t)T.ch * out_entries * plane, res,
+                                                pos_end, T);
 }
 
 template <int RHO>
@@ -600,23 +605,10 @@ bool encode_maps(SepMaps& maps, const float* base, int res, int C) {
   return true;
 }
 
-template <int RHO, int PASS, int POS, int NL, int TAPS>
-cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int line_lo, int line_hi,
-                            int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                            cudaStream_t s, int accumulate) {
-  const int nlt = (line_hi - line_lo + NL - 1) / NL;
-  const int npt = (pos_hi - pos_lo + POS - 1) / POS;
-  if ((int64_t)nlt * npt * res * (RHO + 1) * C <= 0) return cudaSuccess;
-  int lres = 0;
-  while ((1 << lres) < res) ++lres;
-  const dim3 grid((unsigned)nlt, (unsigned)npt, (unsigned)(res * (RHO + 1) * C));
-  constexpr int smem = pass_smem_floats<RHO, PASS, POS, NL>() * (int)sizeof(float);
-  static unsigned long long configured = 0;
-  if (smem > 48 * 1024 && attr_needed(configured))
-    cudaFuncSetAttribute(sep_pass_kernel<RHO, PASS, POS, NL, TAPS>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  // the maps depend on (base, res, C) only; workspaces come back at the same
-  // address call after call, so keep the last few encodings
+// tensor maps of (base, res, C): workspaces come back at the same address
+// call after call, so keep the last few encodings per instantiation
+template <int RHO, int PASS, int POS, int NL>
+bool cached_maps(SepMaps& maps, const float* in, int res, int C) {
   struct Cached {
     const float* base = nullptr;
     int res = 0, C = 0;
@@ -625,40 +617,66 @@ cudaError_t launch_pass_pos(const float* in, float* out, int res, int C, int lin
   static std::mutex mu;
   static Cached cache[8];
   static unsigned next = 0;
-  SepMaps maps;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    const Cached* hit = nullptr;
-    for (const Cached& c : cache)
-      if (c.base == in && c.res == res && c.C == C) hit = &c;
-    if (!hit) {
-      Cached& c = cache[next++ % 8];
-      c.base = nullptr;
-      std::memset(&c.maps, 0, sizeof(c.maps));
-      if (!encode_maps<RHO, PASS, POS, NL>(c.maps, in, res, C)) return cudaErrorNotSupported;
-      c.base = in;
-      c.res = res;
-      c.C = C;
-      hit = &c;
-    }
-    maps = hit->maps;
+  std::lock_guard<std::mutex> lock(mu);
+  const Cached* hit = nullptr;
+  for (const Cached& c : cache)
+    if (c.base == in && c.res == res && c.C == C) hit = &c;
+  if (!hit) {
+    Cached& c = cache[next++ % 8];
+    c.base = nullptr;
+    std::memset(&c.maps, 0, sizeof(c.maps));
+    if (!encode_maps<RHO, PASS, POS, NL>(c.maps, in, res, C)) return false;
+    c.base = in;
+    c.res = res;
+    c.C = C;
+    hit = &c;
+  }
+  maps = hit->maps;
+  return true;
+}
+
+// one pass over `in` with tap subset TAPS; with TAPS1 != TAPS_NONE a second
+// input `in1` (same layout) adds its TAPS1 taps to the same outputs
+template <int RHO, int PASS, int POS, int NL, int TAPS, int TAPS1>
+cudaError_t launch_pass_pos(const float* in, const float* in1, float* out, int res, int C,
+                            int line_lo, int line_hi, int pos_lo, int pos_hi,
+                            const SepParams<RHO>& prm, const char* name, cudaStream_t s) {
+  const int nlt = (line_hi - line_lo + NL - 1) / NL;
+  const int npt = (pos_hi - pos_lo + POS - 1) / POS;
+  if ((int64_t)nlt * npt * res * (RHO + 1) * C <= 0) return cudaSuccess;
+  int lres = 0;
+  while ((1 << lres) < res) ++lres;
+  const dim3 grid((unsigned)nlt, (unsigned)npt, (unsigned)(res * (RHO + 1) * C));
+  constexpr int NWIN = TAPS1 == TAPS_NONE ? 1 : 2;
+  constexpr int smem = pass_smem_floats<RHO, PASS, POS, NL, NWIN>() * (int)sizeof(float);
+  static unsigned long long configured = 0;
+  if (smem > 48 * 1024 && attr_needed(configured))
+    cudaFuncSetAttribute(sep_pass_kernel<RHO, PASS, POS, NL, TAPS, TAPS1>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  SepMaps maps, maps1;
+  if (!cached_maps<RHO, PASS, POS, NL>(maps, in, res, C)) return cudaErrorNotSupported;
+  if (NWIN == 2) {
+    if (!cached_maps<RHO, PASS, POS, NL>(maps1, in1, res, C)) return cudaErrorNotSupported;
+  } else {
+    maps1 = maps;
   }
   FC2T2_LAUNCH(name, s,
-               (sep_pass_kernel<RHO, PASS, POS, NL, TAPS><<<grid, 32 * (RHO + 1), smem, s>>>(
-                   out, res, lres, line_lo, pos_lo, pos_hi, prm, maps, accumulate)));
+               (sep_pass_kernel<RHO, PASS, POS, NL, TAPS, TAPS1>
+                <<<grid, 32 * (RHO + 1), smem, s>>>(out, res, lres, line_lo, pos_lo, pos_hi, prm,
+                                                    maps, maps1)));
   return cudaGetLastError();
 }
 
 // 32 lines per tile, or 16 on a 16-cell grid (the far table of a coarse level)
-template <int RHO, int PASS, int TAPS = TAPS_ALL>
+template <int RHO, int PASS, int TAPS = TAPS_ALL, int TAPS1 = TAPS_NONE>
 cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo, int line_hi,
                         int pos_lo, int pos_hi, const SepParams<RHO>& prm, const char* name,
-                        cudaStream_t s, int accumulate = 0) {
+                        cudaStream_t s, const float* in1 = nullptr) {
   if (res >= kLines)
-    return launch_pass_pos<RHO, PASS, 8, kLines, TAPS>(in, out, res, C, line_lo, line_hi, pos_lo,
-                                                       pos_hi, prm, name, s, accumulate);
-  return launch_pass_pos<RHO, PASS, 8, 16, TAPS>(in, out, res, C, line_lo, line_hi, pos_lo, pos_hi,
-                                                 prm, name, s, accumulate);
+    return launch_pass_pos<RHO, PASS, 8, kLines, TAPS, TAPS1>(in, in1, out, res, C, line_lo,
+                                                              line_hi, pos_lo, pos_hi, prm, name, s);
+  return launch_pass_pos<RHO, PASS, 8, 16, TAPS, TAPS1>(in, in1, out, res, C, line_lo, line_hi,
+                                                        pos_lo, pos_hi, prm, name, s);
 }
 
 template <int RHO>
@@ -681,8 +699,8 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
     // the large hole terms).  With the per-axis tap sets A = parity box,
     // F = {|d| >= 2}, N = {|d| <= 1} over (x, y, z):
     //   F x A x A  +  N x F x A  +  N x N x F
-    // z passes A and F of M'; y passes A(Z_A), F(Z_A) + N(Z_F); x passes
-    // F(Y_AA) + N(Y_FA+NF).
+    // z passes A and F of M'; y passes A(Z_A) and [F(Z_A) + N(Z_F)] (one
+    // kernel over two windows); x pass [F(Y_AA) + N(Y_FA+NF)] likewise.
     const size_t tb = (size_t)SepIdx<RHO>::T * res * res * res * C;
     float *b0 = wa, *b1 = wb, *b2 = wb + tb, *b3 = wb + 2 * tb;
     const int64_t n = (int64_t)(xh - xl) * res * res * C;
@@ -699,17 +717,11 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
     if ((err = launch_pass<RHO, PASS_Y, TAPS_ALL>(b1, b0, res, C, xl, xh, 0, res, prm,
                                                   "m2l_sepfar_y", s)))
       return err;
-    if ((err = launch_pass<RHO, PASS_Y, TAPS_FAR>(b1, b3, res, C, xl, xh, 0, res, prm,
-                                                  "m2l_sepfar_y", s)))
+    if ((err = launch_pass<RHO, PASS_Y, TAPS_FAR, TAPS_NEAR>(b1, b3, res, C, xl, xh, 0, res, prm,
+                                                             "m2l_sepfar_y", s, b2)))
       return err;
-    if ((err = launch_pass<RHO, PASS_Y, TAPS_NEAR>(b2, b3, res, C, xl, xh, 0, res, prm,
-                                                   "m2l_sepfar_y", s, 1)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_X, TAPS_FAR>(b0, b1, res, C, 0, res, x_begin, x_end, prm,
-                                                  "m2l_sepfar_x", s)))
-      return err;
-    if ((err = launch_pass<RHO, PASS_X, TAPS_NEAR>(b3, b1, res, C, 0, res, x_begin, x_end, prm,
-                                                   "m2l_sepfar_x", s, 1)))
+    if ((err = launch_pass<RHO, PASS_X, TAPS_FAR, TAPS_NEAR>(b0, b1, res, C, 0, res, x_begin,
+                                                             x_end, prm, "m2l_sepfar_x", s, b3)))
       return err;
   } else if (stages & SEP_FRONT) {
     const int64_t n = (int64_t)(xh - xl) * res * res * C;
@@ -728,7 +740,7 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
     const int64_t n = (int64_t)(x_end - x_begin) * res * res * C;
     const float half_fine = (float)(1.0 / (double)res);
     if (n > 0) {
-      FC2T2_LAUNCH(coarse ? "m2l_sep_post_l2l" : "m2l_sep_post", s,
+      FC2T2_LAUNCH(far_only ? "m2l_sepfar_post" : (coarse ? "m2l_sep_post_l2l" : "m2l_sep_post"), s,
                    sep_post_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
                        wb, L, res, C, x_begin, x_end - x_begin, coarse, half_fine, prm));
       if ((err = cudaGetLastError()) != cudaSuccess) return err;
