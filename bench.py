@@ -432,6 +432,15 @@ def kernel_rooflines(eng, prof, steps, N, M, hbm_peak, ffma_peak):
     return out
 
 
+def _peaks():
+    """(HBM GB/s, FP32 FFMA TFLOP/s): the measured peaks, else the fallbacks."""
+    try:
+        hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs", 7672.0))
+    except Exception:
+        hbm = 7672.0
+    return hbm, ffma_peak_tflops()[0]
+
+
 def ffma_peak_tflops():
     """The FP32 FFMA peak measured on this pool's B200s by scripts/ubench/peaks.py
     (profiles/r2_peaks.json), else the nominal 148 SMs x 128 FMA/clk x 2 x
@@ -510,8 +519,21 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     from paper_2111_00110_b200.layers import (depth_forward, depth_surface_jvp,
                                               explicit_forward, explicit_jvp,
                                               volumetric_forward, volumetric_jvp)
-    from paper_2111_00110_b200.ray import Camera, RayBundle, generate_rays
+    from paper_2111_00110_b200.ray import Camera, RayBundle, generate_rays, traverse
     out = {}
+    hbm_peak, ffma_peak = _peaks()
+
+    def ray_roofline(ms, nbytes, flops, how):
+        """SURVEY 8(d), ray kernels: both bounds -- per-ray I/O plus the
+        per-box coefficient gather (an HBM upper bound: the grid is mostly L2
+        resident) and the paper's per-box FLOP counts against the measured
+        FP32 FFMA peak; the higher fraction binds."""
+        t = ms / 1e3
+        fh, ff = nbytes / (hbm_peak * 1e9) / t, flops / (ffma_peak * 1e12) / t
+        return {"ms_per_step": round(ms, 4), "bytes_per_step": int(nbytes),
+                "flops_per_step": int(flops), "hbm_frac": round(fh, 4), "fp32_frac": round(ff, 4),
+                "bound": "hbm" if fh >= ff else "fp32", "frac": round(max(fh, ff), 4),
+                "model": how}
     # config 1: 2D explicit layer lifted to z = 0.03125, level 4
     rng = np.random.default_rng(11)
     n = 4096
@@ -585,7 +607,30 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     # every line: value from the mean step (as the headline); the median
     # is kept beside it
     med3 = st3.get("_step_ms_median", ms / steps)
+    # boxes the walker visits: every box entered before the first root (all of
+    # a missing ray's), from the traversal and the hit lengths
+    tr3 = traverse(b3, 5)
+    len3 = torch.as_tensor(r3.lengths, device=dev).double()
+    hit3 = torch.as_tensor(r3.hit, device=dev).bool()
+    rid3 = tr3.ray_id.long()
+    vis3 = int(((tr3.t0 < len3[rid3]) | ~hit3[rid3]).sum().item())
+    nh3 = int(hit3.sum().item())
+    P4, PP4, cells5 = 35, 36, 64 ** 3
+    rl3 = {"visited_boxes": vis3, "total_boxes": int(tr3.t0.shape[0]), "hits": nh3}
+    if "depth_walk" in st3:
+        rl3["depth_walk"] = ray_roofline(
+            st3["depth_walk"], R3 * (48 + 4 + 12 + 12 + 4) + vis3 * 4 * P4, vis3 * (668 + 136),
+            "48 B ray in, length + point + gradient + denominator out, 140 B cell row per "
+            "visited box; line2poly 668 + Ferrari 136 FLOP per visited box (PAPER.md:609, :624); "
+            "the root finder itself runs in float64")
+    if "insert" in st3:
+        rl3["insert"] = ray_roofline(
+            st3["insert"], 4 * nh3 * (4 + 4 * PP4) + 4 * PP4 * cells5, 4 * nh3 * P4,
+            "depth + 3 normal-adjoint items per hit: 4 B key + one 144 B payload row each, and "
+            "the finest M grid written; one add per coefficient")
+    del tr3
     out["cfg3_root_depth_normal"] = {
+        "roofline_kernels": rl3,
         "metric": "rays/s", "value": R3 / (ms / steps / 1e3), "ms_per_step": ms / steps,
         "median_ms_per_step": med3,
         "hit_fraction": float(r3.hit.float().mean().item()), "stages_ms_per_step": st3,
@@ -617,7 +662,28 @@ def secondary(dev, flush, stream, steps: int) -> dict:
     ms, _ = timed_steps(step4, max(2, steps // 4), 1, flush, stream, st4)
     k = max(2, steps // 4)
     med4 = st4.get("_step_ms_median", ms / k)
+    res4 = volumetric_forward(e5, p, ws, wc, b4, bg)
+    alive4 = int(torch.as_tensor(res4.alive).sum().item())
+    del res4
+    C4 = 4
+    rl4 = {"alive_segments": alive4}
+    if "vol_forward" in st4:
+        rl4["vol_forward"] = ray_roofline(
+            st4["vol_forward"], R4 * (48 + 12) + alive4 * 4 * C4 * P4, alive4 * 1563,
+            "48 B ray in, 12 B rgb out, 560 B of cell rows (sigma + 3 colours) per alive box; "
+            "1563 FLOP per box (PAPER.md:1118)")
+    if "vol_payload" in st4:
+        rl4["vol_payload"] = ray_roofline(
+            st4["vol_payload"], R4 * (48 + 12) + alive4 * (4 * C4 * P4 + 112 + 4), alive4 * 2452,
+            "ray + rgb tangent in, 560 B of cell rows per alive box, one 112 B segment record "
+            "+ 4 B key out; 2452 FLOP per box (PAPER.md:1119)")
+    if "insert" in st4:
+        rl4["insert"] = ray_roofline(
+            st4["insert"], alive4 * (112 + 4 + 4) + 4 * C4 * PP4 * cells5, alive4 * 1489,
+            "112 B record + key + order per alive box, the 4-channel finest M grid written; "
+            "1489 FLOP per box (PAPER.md:1120)")
     out["cfg4_radiance"] = {"metric": "rays/s", "value": R4 / (ms / k / 1e3), "ms_per_step": ms / k,
+                            "roofline_kernels": rl4,
                             "median_ms_per_step": med4,
                             "stages_ms_per_step": st4,
                             "workload": "N=2^20 (|N(0,1)| density, U(0,1) RGB), 8 poses x 400x400, "

@@ -167,3 +167,43 @@ def test_separable_eligibility():
     pruned = fit_m2l_tables(KernelModel("gaussian", 12000.0, 2), 4, check=False, device=False)
     assert not pruned["far"][4].active[~pruned["far"][4].hole].all()
     assert not separable_eligible(pruned, 4, 2)
+
+
+@pytest.mark.parametrize("alpha,rho,levels,level", [(1000.0, 4, 5, 4), (1000.0, 4, 5, 3),
+                                                    (200.0, 4, 4, 3), (60.0, 3, 5, 4)])
+def test_separable_far_pieces_reproduce_coarse_tables(alpha, rho, levels, level):
+    """Coarse-level far tables through their own per-axis factors: every
+    active table equals its factored form (float64), the offsets the reference
+    prunes (peak interaction < 1e-16, kernel.py:275) have negligible factored
+    tables, and the three disjoint pieces F x A x A + N x F x A + N x N x F of
+    csrc/m2l_sep.cu cover each parity stencil minus the hole exactly once."""
+    from paper_2111_00110_b200.kernel import (separable_dense, separable_factors,
+                                              separable_far_eligible)
+    k = KernelModel("gaussian", alpha, rho)
+    tabs = fit_m2l_tables(k, levels, check=False, device=False)
+    assert separable_far_eligible(tabs, level, levels, rho)
+    assert not separable_far_eligible(tabs, levels, levels, rho)      # the finest level
+    assert not separable_far_eligible(tabs, 2, levels, rho)           # the coarsest stencil
+    t = tabs["far"][level]
+    f = separable_factors(k, level)
+    peak = max(np.abs(t.coeffs[i]).max() for i in np.flatnonzero(t.active))
+    for i in range(t.offsets.shape[0]):
+        if t.hole[i]:
+            continue
+        d = separable_dense(f, k.table, t.offsets[i])
+        if t.active[i]:
+            assert np.abs(d - t.coeffs[i]).max() <= 2e-7 * np.abs(t.coeffs[i]).max()
+        else:
+            assert np.abs(d).max() <= 1e-12 * peak
+    # the pieces: per parity, count how often each offset of the box is applied
+    far_taps, near_taps = {-3, -2, 2, 3}, {-1, 0, 1}
+    for par in range(2):
+        box = set(range(-2 - par, 4 - par))
+        F, N, A = box & far_taps, box & near_taps, box
+        cover = {}
+        for xs, ys, zs in ((F, A, A), (N, F, A), (N, N, F)):
+            for o in ((x, y, z) for x in xs for y in ys for z in zs):
+                cover[o] = cover.get(o, 0) + 1
+        want = {(x, y, z) for x in box for y in box for z in box
+                if max(abs(x), abs(y), abs(z)) > 1}
+        assert set(cover) == want and set(cover.values()) == {1}
