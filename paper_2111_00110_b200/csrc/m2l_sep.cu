@@ -123,19 +123,19 @@ namespace {
 // lanes along x.
 template <int RHO>
 __global__ void __launch_bounds__(256)
-sep_pre_kernel(const float* __restrict__ M, float* __restrict__ Mp, int res, int C, int x_lo,
-               int nx, const __grid_constant__ SepParams<RHO> prm) {
+sep_pre_kernel(const float* __restrict__ M, float* __restrict__ Mp, int res, int lres, int C,
+               int x_lo, int nx, const __grid_constant__ SepParams<RHO> prm) {
   using I = SepIdx<RHO>;
   constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
   constexpr MI<RHO> mi{};
-  const int64_t cells = (int64_t)nx * res * res;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= cells * C) return;
-  const int ch = (int)(t / cells);
-  const int64_t r = t - (int64_t)ch * cells;
-  const int x = x_lo + (int)(r % nx);
-  const int64_t yz = r / nx;
-  const int z = (int)(yz % res), y = (int)(yz / res);
+  // grid (cells / 256, C); 32-bit index arithmetic (cells <= 2^24), res = 2^lres
+  const unsigned cells = (unsigned)nx << (2 * lres);
+  const unsigned r = blockIdx.x * 256u + threadIdx.x;
+  if (r >= cells) return;
+  const int ch = (int)blockIdx.y;
+  const unsigned yz = r / (unsigned)nx;
+  const int x = x_lo + (int)(r - yz * (unsigned)nx);
+  const int z = (int)(yz & (unsigned)(res - 1)), y = (int)(yz >> lres);
   const float* row = M + ((((int64_t)x * res + y) * res + z) * C + ch) * PP;
   float v[P];
 #pragma unroll
@@ -161,18 +161,18 @@ sep_pre_kernel(const float* __restrict__ M, float* __restrict__ Mp, int res, int
 // same float32 sum the separate accumulate-L2L launch forms.
 template <int RHO>
 __global__ void __launch_bounds__(256)
-sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int C, int x_lo,
-                int nx, const float* __restrict__ coarse, float half_fine,
+sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int lres, int C,
+                int x_lo, int nx, const float* __restrict__ coarse, float half_fine,
                 const __grid_constant__ SepParams<RHO> prm) {
   constexpr int P = MI<RHO>::P, PP = MI<RHO>::PP;
-  const int64_t cells = (int64_t)nx * res * res;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= cells * C) return;
-  const int ch = (int)(t / cells);
-  const int64_t r = t - (int64_t)ch * cells;
-  const int z = (int)(r % res);
-  const int64_t xy = r / res;
-  const int y = (int)(xy % res), x = x_lo + (int)(xy / res);
+  // grid (cells / 256, C); shifts and masks only (res = 2^lres)
+  const unsigned cells = (unsigned)nx << (2 * lres);
+  const unsigned r = blockIdx.x * 256u + threadIdx.x;
+  if (r >= cells) return;
+  const int ch = (int)blockIdx.y;
+  const int z = (int)(r & (unsigned)(res - 1));
+  const unsigned xy = r >> lres;
+  const int y = (int)(xy & (unsigned)(res - 1)), x = x_lo + (int)(xy >> lres);
   const int64_t plane = (int64_t)res * res * res;
   const float* in = X + (int64_t)ch * P * plane + ((int64_t)x * res + y) * res + z;
   float v[P];
@@ -326,24 +326,20 @@ __device__ __forceinline__ void group_body(const float* sm0, const float* sm1, c
   accum_input<RHO, PASS, POS, NL, TAPS0, NOUT>(acc, sm0, Kt, lane, nin, in_base, in_stride);
   if constexpr (TAPS1 != TAPS_NONE)
     accum_input<RHO, PASS, POS, NL, TAPS1, NOUT>(acc, sm1, Kt, lane, nin, in_base, in_stride);
-  // 32-bit offsets from `out` (a channel block holds < 2^31 floats); the
-  // positions are pos_stride apart
-  int ob[NOUT];
+  // one 64-bit pointer per output entry, advanced by the (uniform) position
+  // stride: two integer adds + STG per store
+  char* pb[NOUT];
 #pragma unroll
-  for (int j = 0; j < NOUT; ++j) ob[j] = oe[j] * (int)plane;
-  const int ps = (int)pos_stride;
-  if (nvalid == POS) {
+  for (int j = 0; j < NOUT; ++j) pb[j] = reinterpret_cast<char*>(out + (int64_t)oe[j] * plane);
+  const int64_t psb = pos_stride * (int64_t)sizeof(float);
 #pragma unroll
-    for (int w = 0; w < POS; ++w)
+  for (int w = 0; w < POS; ++w) {
+    if (w < nvalid) {
 #pragma unroll
-      for (int j = 0; j < NOUT; ++j) out[ob[j] + w * ps] = acc[w][j];
-  } else {
+      for (int j = 0; j < NOUT; ++j) *reinterpret_cast<float*>(pb[j]) = acc[w][j];
+    }
 #pragma unroll
-    for (int w = 0; w < POS; ++w)
-      if (w < nvalid) {
-#pragma unroll
-        for (int j = 0; j < NOUT; ++j) out[ob[j] + w * ps] = acc[w][j];
-      }
+    for (int j = 0; j < NOUT; ++j) pb[j] += psb;
   }
 }
 
@@ -518,7 +514,7 @@ sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos
   }
   // Kt[i][d][j] = K(d - 3)[j][i], rows padded to 8 (two 128-bit loads),
   // laid out on the host
-  for (int t = threadIdx.x; t < 7 * 8 * R1; t += blockDim.x) Kt[t] = (&prm.kt[0][0][0])[t];
+  for (int t = threadIdx.x; t < 7 * 8 * R1; t += 32 * R1) Kt[t] = (&prm.kt[0][0][0])[t];
   {
     __syncthreads();   // the barrier init is visible before anyone waits on it
     asm volatile(
@@ -687,6 +683,7 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
   const int res = 1 << (level + 1);
   const int nl = std::min(res, kLines);
   if (res % nl || res < 16) return cudaErrorInvalidValue;
+  const int lres = level + 1;
   const SepParams<RHO> prm = to_params<RHO>(pre, post, conv);
   // x range the z/y passes must cover: the slab plus the x pass's halo,
   // widened to whole line tiles
@@ -703,10 +700,10 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
     // kernel over two windows); x pass [F(Y_AA) + N(Y_FA+NF)] likewise.
     const size_t tb = (size_t)SepIdx<RHO>::T * res * res * res * C;
     float *b0 = wa, *b1 = wb, *b2 = wb + tb, *b3 = wb + 2 * tb;
-    const int64_t n = (int64_t)(xh - xl) * res * res * C;
+    const int64_t n = (int64_t)(xh - xl) * res * res;
     FC2T2_LAUNCH("m2l_sepfar_pre", s,
-                 sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-                     M, b0, res, C, xl, xh - xl, prm));
+                 sep_pre_kernel<RHO><<<dim3((unsigned)((n + 255) / 256), (unsigned)C), 256, 0, s>>>(
+                     M, b0, res, lres, C, xl, xh - xl, prm));
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if ((err = launch_pass<RHO, PASS_Z, TAPS_ALL>(b0, b1, res, C, xl, xh, 0, res, prm,
                                                   "m2l_sepfar_z", s)))
@@ -724,9 +721,10 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                                                              x_end, prm, "m2l_sepfar_x", s, b3)))
       return err;
   } else if (stages & SEP_FRONT) {
-    const int64_t n = (int64_t)(xh - xl) * res * res * C;
-    FC2T2_LAUNCH("m2l_sep_pre", s, sep_pre_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-                                       M, wa, res, C, xl, xh - xl, prm));
+    const int64_t n = (int64_t)(xh - xl) * res * res;
+    FC2T2_LAUNCH("m2l_sep_pre", s,
+                 sep_pre_kernel<RHO><<<dim3((unsigned)((n + 255) / 256), (unsigned)C), 256, 0, s>>>(
+                     M, wa, res, lres, C, xl, xh - xl, prm));
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if ((err = launch_pass<RHO, PASS_Z>(wa, wb, res, C, xl, xh, 0, res, prm, "m2l_sep_z", s)))
       return err;
@@ -737,12 +735,13 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
       return err;
   }
   if (stages & SEP_POST) {
-    const int64_t n = (int64_t)(x_end - x_begin) * res * res * C;
+    const int64_t n = (int64_t)(x_end - x_begin) * res * res;
     const float half_fine = (float)(1.0 / (double)res);
     if (n > 0) {
       FC2T2_LAUNCH(far_only ? "m2l_sepfar_post" : (coarse ? "m2l_sep_post_l2l" : "m2l_sep_post"), s,
-                   sep_post_kernel<RHO><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
-                       wb, L, res, C, x_begin, x_end - x_begin, coarse, half_fine, prm));
+                   sep_post_kernel<RHO><<<dim3((unsigned)((n + 255) / 256), (unsigned)C), 256, 0,
+                                          s>>>(wb, L, res, lres, C, x_begin, x_end - x_begin, coarse,
+                                               half_fine, prm));
       if ((err = cudaGetLastError()) != cudaSuccess) return err;
     }
   }
