@@ -1,11 +1,9 @@
-# A/B of an env switch on one box: GPU tests, diag, headline bench with/without
-# usage: bash scripts/gpu_ab.sh VAR
-VAR=${1:-FC2T2_L2P_THREAD}
-timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-for v in 0 1; do
-  echo "== $VAR=$v"
-  env $VAR=$v LEVEL=5 RHO=4 M=10000000 timeout 300 python scripts/diag_l2p.py 2>&1 | tail -2
-  env $VAR=$v LEVEL=6 RHO=6 timeout 300 python scripts/diag_l2p.py 2>&1 | tail -2
-  env $VAR=$v timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-secondary > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
-  python -c "import json;d=json.load(open('gpurun_out/ab_$v.json'));print('value',d['value'],'ms',d['ms_per_step'],'e2e_ms',d['e2e']['ms_per_step'],'l2p',d['stages_ms_per_step']['l2p'])"
+# same-box A/B of the step: default library vs $ALT (FC2T2_LIB_OVERRIDE), interleaved
+ALT=${ALT:?path of the alternative libfc2t2 build}
+mkdir -p gpurun_out
+for r in 1 2 3; do
+for v in def alt; do
+  if [ $v = alt ]; then export FC2T2_LIB_OVERRIDE=$PWD/$ALT; else unset FC2T2_LIB_OVERRIDE; fi
+  timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-secondary > gpurun_out/ab_$v.json 2>/dev/null; python -c "import json;d=json.loads(open('gpurun_out/ab_$v.json').read().strip().splitlines()[-1]);s=d['stages_ms_per_step'];print('$v', round(d['ms_per_step'],4), round(d['graphed']['ms_per_step'],4), {k:s[k] for k in s if 'pre' in k or 'post' in k})"
+done
 done
