@@ -221,11 +221,12 @@ brick_start_kernel(const uint32_t* __restrict__ tot, int nb, uint32_t* __restric
 
 // Small inputs (nt <= kSmallScanTiles): S1-S3 and the brick starts in one
 // launch -- a CTA per 32 bricks scans all their tiles (32 warps x nt / 32 tiles),
-// the brick totals meet at a grid barrier (at most 128 CTAs, all resident;
+// the brick totals meet at a grid barrier (at most 64 CTAs, all resident;
 // the counters reset themselves; one slot per launch in flight), and every
 // CTA derives its bricks' starts from the totals before it.  Same cnt / tot /
 // brick_start contents as the four-kernel path.
 constexpr int kSmallScanTiles = 2048;
+constexpr int kSmallScanCtas = 64;   // two such launches in flight still leave SMs free
 constexpr int kScanSlots = 32;
 __device__ unsigned int g_scan_sync[kScanSlots][2];
 
@@ -924,7 +925,7 @@ cudaError_t p2m_brick(int rho, int level, int C, const float* pts, const float* 
                                                                             b.cnt, flag));
   const int nseg = (int)((nt + SEG_T - 1) / SEG_T);
   const dim3 sgrid((unsigned)((g.nb + 31) / 32), (unsigned)nseg);
-  if (nt <= kSmallScanTiles && (g.nb + 31) / 32 <= 128) {
+  if (nt <= kSmallScanTiles && (g.nb + 31) / 32 <= kSmallScanCtas) {
     static std::atomic<unsigned> next_slot{0};
     const int slot = (int)(next_slot.fetch_add(1, std::memory_order_relaxed) % kScanSlots);
     FC2T2_LAUNCH("brick_scan", s,
