@@ -343,12 +343,44 @@ __device__ __forceinline__ void group_body(const float* sm0, const float* sm1, c
   }
 }
 
+// Partitions are very unequal (z pass at rho = 4: 15, 10, 6, 3, 1 inputs), and
+// every CTA pays the same fixed cost (window copy, barrier, index set-up), so
+// the light tail shares one CTA: slot s < TAIL is partition s, slot TAIL is
+// partitions TAIL .. RHO one after the other, their windows back to back in
+// the shared memory sized for partition 0.  TAIL = the first partition from
+// which the rest together has no more work and no more window entries than
+// partition 0.
+template <int RHO, int PASS>
+struct Slots {
+  static constexpr int R1 = RHO + 1;
+  static constexpr int ne(int p) {
+    return PASS == PASS_Z ? (R1 - p) * (R1 - p + 1) / 2
+                          : (PASS == PASS_Y ? (R1 - p) * R1 : R1 * (R1 - p));
+  }
+  static constexpr int work(int p) {
+    return PASS == PASS_Y ? (R1 - p) : (R1 - p) * (R1 - p + 1) / 2;
+  }
+  static constexpr int tail() {
+    for (int t = 1; t < R1; ++t) {
+      int w = 0, e = 0;
+      for (int p = t; p < R1; ++p) {
+        w += work(p);
+        e += ne(p);
+      }
+      if (w <= work(0) && e <= ne(0)) return t;
+    }
+    return R1 - 1;
+  }
+  static constexpr int TAIL = tail();
+  static constexpr int NSLOT = TAIL + 1;
+};
+
 // tile geometry from the 3-D grid: x = line tile, y = position tile,
-// z = (channel * R1 + partition) * res + fixed plane (res = 2^lres)
+// z = (channel * NSLOT + slot) * res + fixed plane (res = 2^lres)
 struct Tile {
   int ch, part, fixed, line0, pos0;
 };
-template <int R1>
+template <int NSLOT>
 __device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, int POS, int NL) {
   Tile r;
   r.line0 = line_lo + (int)blockIdx.x * NL;
@@ -356,8 +388,8 @@ __device__ __forceinline__ Tile decode_tile(int lres, int line_lo, int pos_lo, i
   const int z = (int)blockIdx.z;
   r.fixed = z & ((1 << lres) - 1);
   const int cp = z >> lres;
-  r.part = cp % R1;
-  r.ch = cp / R1;
+  r.part = cp % NSLOT;   // the slot; the kernel walks its partitions
+  r.ch = cp / NSLOT;
   return r;
 }
 
@@ -488,27 +520,36 @@ sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos
   uint64_t* bar = reinterpret_cast<uint64_t*>(Kt + 7 * 8 * R1);
   const int64_t plane = (int64_t)res * res * res;
   const int out_entries = PASS == PASS_X ? I::P : I::T;
-  const Tile T = decode_tile<R1>(lres, line_lo, pos_lo, POS, NL);
+  using SL = Slots<RHO, PASS>;
+  Tile T = decode_tile<SL::NSLOT>(lres, line_lo, pos_lo, POS, NL);
+  const int p_first = T.part, p_last = T.part < SL::TAIL ? T.part : R1 - 1;
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bar);
   {
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s));
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      uint32_t bytes = 0;
+      for (int part = p_first; part <= p_last; ++part)
+        bytes += window_bytes<RHO, PASS, POS, NL>(part);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s),
-                   "r"(NWIN * window_bytes<RHO, PASS, POS, NL>(T.part)));
+                   "r"(NWIN * bytes));
+      uint32_t off = 0;   // bytes into the window area
+      for (int part = p_first; part <= p_last; ++part) {
 #pragma unroll
-      for (int wi = 0; wi < NWIN; ++wi) {
-        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(wi ? sm1 : sm);
-        const CUtensorMap* mp = wi ? &maps1.m[T.part] : &maps.m[T.part];
-        if (PASS == PASS_Z)
-          tma_load_5d(dst, mp, T.line0, T.pos0 - 3, T.fixed, T.ch * I::P + I::ab(T.part, 0), 0,
-                      bar_s);
-        else if (PASS == PASS_Y)
-          tma_load_5d(dst, mp, T.line0, T.fixed, T.pos0 - 3,
-                      T.ch * I::T + I::pair(T.part, 0) * R1, 0, bar_s);
-        else
-          tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(T.part, 0), T.ch * R1,
-                      bar_s);
+        for (int wi = 0; wi < NWIN; ++wi) {
+          const uint32_t dst = (uint32_t)__cvta_generic_to_shared(wi ? sm1 : sm) + off;
+          const CUtensorMap* mp = wi ? &maps1.m[part] : &maps.m[part];
+          if (PASS == PASS_Z)
+            tma_load_5d(dst, mp, T.line0, T.pos0 - 3, T.fixed, T.ch * I::P + I::ab(part, 0), 0,
+                        bar_s);
+          else if (PASS == PASS_Y)
+            tma_load_5d(dst, mp, T.line0, T.fixed, T.pos0 - 3,
+                        T.ch * I::T + I::pair(part, 0) * R1, 0, bar_s);
+          else
+            tma_load_5d(dst, mp, T.pos0 - 4, T.line0, T.fixed, I::pair(part, 0), T.ch * R1,
+                        bar_s);
+        }
+        off += window_bytes<RHO, PASS, POS, NL>(part);
       }
     }
   }
@@ -525,9 +566,15 @@ sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos
         : "memory");
   }
   __syncthreads();
-  compute_tile<RHO, PASS, POS, NL, TAPS, TAPS1>(sm, sm1, Kt,
-                                                out + (int64_t)T.ch * out_entries * plane, res,
-                                                pos_end, T);
+  uint32_t off = 0;   // floats into the window area
+#pragma unroll 1
+  for (int part = p_first; part <= p_last; ++part) {
+    T.part = part;
+    compute_tile<RHO, PASS, POS, NL, TAPS, TAPS1>(sm + off, sm1 + off, Kt,
+                                                  out + (int64_t)T.ch * out_entries * plane, res,
+                                                  pos_end, T);
+    off += window_bytes<RHO, PASS, POS, NL>(part) / 4;
+  }
 }
 
 template <int RHO>
@@ -642,7 +689,8 @@ cudaError_t launch_pass_pos(const float* in, const float* in1, float* out, int r
   if ((int64_t)nlt * npt * res * (RHO + 1) * C <= 0) return cudaSuccess;
   int lres = 0;
   while ((1 << lres) < res) ++lres;
-  const dim3 grid((unsigned)nlt, (unsigned)npt, (unsigned)(res * (RHO + 1) * C));
+  const dim3 grid((unsigned)nlt, (unsigned)npt,
+                  (unsigned)(res * Slots<RHO, PASS>::NSLOT * C));
   constexpr int NWIN = TAPS1 == TAPS_NONE ? 1 : 2;
   constexpr int smem = pass_smem_floats<RHO, PASS, POS, NL, NWIN>() * (int)sizeof(float);
   static unsigned long long configured = 0;
