@@ -8,7 +8,8 @@ Gaussian alpha = 1000 (reference default kernel, DEFAULT_ALPHA[5]).
 
   value  (N+M) / device time of explicit_forward + explicit_jvp, inputs resident
          in HBM, CUDA events per step on the launching stream, L2 flushed
-         between steps (outside the events); the mean step.  The K timed steps
+         between steps (outside the events); the median step (the
+         mean and the slowest step are reported beside it).  The K timed steps
          run without the library's per-launch events; the same K steps run a
          second time with them on for the per-kernel times (the two event
          records around every launch cost ~9 % of a step).
@@ -475,7 +476,7 @@ def measured_traffic(kernels):
 
 
 def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None = None):
-    """(total device ms over `steps`, last result): per-step CUDA events on the
+    """(median step in ms x `steps`, last result): per-step CUDA events on the
     launching stream, L2 flush between steps outside the events.  With
     ``stages`` a SECOND pass of the same `steps` steps runs with the library's
     per-launch CUDA events on (two event records around every kernel launch,
@@ -518,10 +519,13 @@ def timed_steps(fn, steps: int, warmup: int, flush, stream, stages: dict | None 
                            "waiting for SMs -- the serialised ncu launch list has the kernels' "
                            "own times")
         stages["_step_ms_instrumented"] = round(sum(per_i) / steps, 4)
-        stages["_step_ms_median"] = round(per[len(per) // 2], 4)
+        stages["_step_ms_median"] = round(float(np.median(per)), 4)
+        stages["_step_ms_mean"] = round(sum(per) / steps, 4)
         stages["_step_ms_max"] = round(per[-1], 4)
     gc.enable()
-    return float(sum(per)), out
+    # the MEDIAN step times `steps` (median of >= 20 runs): one
+    # host hiccup in a 20-step region moves the mean by several per cent
+    return float(np.median(per)) * steps, out
 
 
 def secondary(dev, flush, stream, steps: int) -> dict:
@@ -617,8 +621,8 @@ def secondary(dev, flush, stream, steps: int) -> dict:
         return depth_surface_jvp(yl, yg, res), res
     st3 = {}
     ms, (g3, r3) = timed_steps(step3, steps, 3, flush, stream, st3)
-    # every line: value from the mean step (as the headline); the median
-    # is kept beside it
+    # every line: value from the median step (as the headline); the mean is
+    # kept beside it in the stage dict
     med3 = st3.get("_step_ms_median", ms / steps)
     # boxes the walker visits: every box entered before the first root (all of
     # a missing ray's), from the traversal and the hit lengths
@@ -908,7 +912,11 @@ def run_ours(args, rank: int, world: int) -> None:
             ev[i][1].record(stream)
         barrier()
     launches = (_lib.launch_count() - launches0) // args.steps
-    ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    # the median of the K per-step times (the mean is kept beside
+    # it): one host hiccup in a 20-step region moves the mean by several per cent
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    ms_mean = float(sum(per_step)) / args.steps
+    ms = float(np.median(per_step)) * args.steps
     # ---- the same K steps once more with the library's per-launch CUDA events
     # on, for the per-kernel times behind the rooflines: two event records
     # around every launch cost ~9 % of a step, so `value` is the pass above
@@ -925,7 +933,7 @@ def run_ours(args, rank: int, world: int) -> None:
     gc.enable()
     prof = _lib.profile_read()
     _lib.profile_enable(False)
-    ms_instr = float(sum(a.elapsed_time(b) for a, b in ev_i)) / args.steps
+    ms_instr = float(np.median([a.elapsed_time(b) for a, b in ev_i]))
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -983,15 +991,18 @@ def run_ours(args, rank: int, world: int) -> None:
     barrier()
     gc.collect()
     gc.disable()
-    te0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    # every host step ends with its results readable on the host (the API
+    # call synchronises its downloads), so the host clock per step is the end
+    # to end time; median of the K steps as for `value`, the mean beside it
+    e2e_per = []
     for _ in range(args.steps):
+        te0 = time.perf_counter()
         step_host()
-    e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_per.append(1000.0 * (time.perf_counter() - te0))
     barrier()
-    e2e_ms = max(e0.elapsed_time(e1), 1000.0 * (time.perf_counter() - te0)) / args.steps
+    e2e_ms = float(np.median(e2e_per))
+    e2e_mean = float(np.mean(e2e_per))
     gc.enable()
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)
@@ -1098,14 +1109,16 @@ def run_ours(args, rank: int, world: int) -> None:
     stages = {k: round(v[0] / args.steps, 4) for k, v in sorted(prof.items())}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": ms_step, "step_statistic": "median of the K steps",
+        "ms_per_step_mean": ms_mean, "ms_per_step_max": float(max(per_step)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "N": N, "M": M, "levels": CFG["levels"],
                    "rho": CFG["rho"], "alpha": CFG["alpha"],
                    "l2": "inputs 176 MB > 126 MB L2, and a 256 MB L2 flush between steps",
                    "parallelism": f"dp{world}" + (" (grid all-reduce, NCCL)" if world > 1 else "")},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "ms_per_step_mean": e2e_mean},
         "gpu_launches": int(launches),
         "roofline": roofline,
         "roofline_dominant_stage": roofline_stage,
@@ -1194,7 +1207,7 @@ def run_scaling(args, rank: int, world: int) -> None:
     gc.enable()
     launches = (_lib.launch_count() - launches0) // args.steps
     per = [a_.elapsed_time(b_) for a_, b_ in ev]
-    ms = float(sum(per))
+    ms = float(np.median(per)) * args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -1235,7 +1248,8 @@ def run_scaling(args, rank: int, world: int) -> None:
     line = {
         "metric": METRIC, "value": (N + M) / (ms_step / 1000.0), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "ms_per_step_median_rank0": float(np.median(per)),
+        "step_statistic": "median of the K steps (max over ranks)",
+        "ms_per_step_mean_rank0": float(np.mean(per)),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": WORKLOAD5, "N": N, "M": M, "levels": C5["levels"],
