@@ -505,7 +505,7 @@ __device__ __forceinline__ uint32_t window_bytes(int part) {
 //   x pass: lines z, positions x, fixed y      (in Y,  out X)
 // The window comes from one TMA tensor copy issued by thread 0.
 template <int RHO, int PASS, int POS, int NL, int TAPS, int TAPS1>
-__global__ void __launch_bounds__(32 * (RHO + 1))
+__global__ void __launch_bounds__(32 * (RHO + 1), (PASS == PASS_Z && TAPS1 == TAPS_NONE ? 5 : 1))
 sep_pass_kernel(float* __restrict__ out, int res, int lres, int line_lo, int pos_lo, int pos_end,
                 const __grid_constant__ SepParams<RHO> prm, const __grid_constant__ SepMaps maps,
                 const __grid_constant__ SepMaps maps1) {
