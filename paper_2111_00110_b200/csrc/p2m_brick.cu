@@ -630,7 +630,7 @@ brick_scatter_rank_kernel(const float* __restrict__ pts, const float* __restrict
 #define FC2T2_K4_CHUNK 2048
 #endif
 #ifndef FC2T2_K4_MINB
-#define FC2T2_K4_MINB 3
+#define FC2T2_K4_MINB 4
 #endif
 constexpr int K4_CHUNK = FC2T2_K4_CHUNK;
 
