@@ -199,6 +199,25 @@ sep_post_kernel(const float* __restrict__ X, float* __restrict__ L, int res, int
 #pragma unroll
     for (int j = 0; j < P; ++j) v[j] = pv[j] + v[j];
   }
+  if constexpr (8 * 32 * (PP + 1) * 4 <= 48 * 1024) if (C == 1) {
+    // one channel: the warp's 32 rows (consecutive cells) are one contiguous
+    // 32 * PP float block -- transpose through shared memory and write it with
+    // fully coalesced stores instead of 16-byte pieces 144 bytes apart
+    __shared__ float tile[8][32 * (PP + 1)];
+    float* t = tile[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < PP; ++j) t[lane * (PP + 1) + j] = j < P ? v[j] : 0.f;
+    __syncwarp();
+    // (cells is a multiple of 256, so warps are whole)
+    float* blk = L + ((int64_t)x_lo * res * res + (int64_t)(r - lane)) * PP;
+#pragma unroll
+    for (int i = 0; i < PP; ++i) {
+      const int idx = i * 32 + lane, rr = idx / PP;
+      blk[idx] = t[idx + rr];   // rr * (PP + 1) + (idx - rr * PP)
+    }
+    return;
+  }
   float* row = L + ((((int64_t)x * res + y) * res + z) * C + ch) * PP;
 #pragma unroll
   for (int k = 0; k < PP; k += 4) {
@@ -723,6 +742,17 @@ cudaError_t launch_pass(const float* in, float* out, int res, int C, int line_lo
                                                         pos_lo, pos_hi, prm, name, s);
 }
 
+// the pre transform over cells with x in [xl, xh)
+template <int RHO>
+void launch_pre(const char* name, const float* M, float* Mp, int res, int lres, int C, int xl,
+                int xh, const SepParams<RHO>& prm, cudaStream_t s) {
+  const int64_t n = (int64_t)(xh - xl) * res * res;
+  if (n <= 0) return;
+  FC2T2_LAUNCH(name, s,
+               sep_pre_kernel<RHO><<<dim3((unsigned)((n + 255) / 256), (unsigned)C), 256, 0, s>>>(
+                   M, Mp, res, lres, C, xl, xh - xl, prm));
+}
+
 template <int RHO>
 cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                         const double* conv, const float* M, float* L, float* wa, float* wb,
@@ -748,10 +778,7 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
     // kernel over two windows); x pass [F(Y_AA) + N(Y_FA+NF)] likewise.
     const size_t tb = (size_t)SepIdx<RHO>::T * res * res * res * C;
     float *b0 = wa, *b1 = wb, *b2 = wb + tb, *b3 = wb + 2 * tb;
-    const int64_t n = (int64_t)(xh - xl) * res * res;
-    FC2T2_LAUNCH("m2l_sepfar_pre", s,
-                 sep_pre_kernel<RHO><<<dim3((unsigned)((n + 255) / 256), (unsigned)C), 256, 0, s>>>(
-                     M, b0, res, lres, C, xl, xh - xl, prm));
+    launch_pre<RHO>("m2l_sepfar_pre", M, b0, res, lres, C, xl, xh, prm, s);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if ((err = launch_pass<RHO, PASS_Z, TAPS_ALL>(b0, b1, res, C, xl, xh, 0, res, prm,
                                                   "m2l_sepfar_z", s)))
@@ -769,10 +796,7 @@ cudaError_t m2l_sep_rho(int level, int C, const double* pre, const double* post,
                                                              x_end, prm, "m2l_sepfar_x", s, b3)))
       return err;
   } else if (stages & SEP_FRONT) {
-    const int64_t n = (int64_t)(xh - xl) * res * res;
-    FC2T2_LAUNCH("m2l_sep_pre", s,
-                 sep_pre_kernel<RHO><<<dim3((unsigned)((n + 255) / 256), (unsigned)C), 256, 0, s>>>(
-                     M, wa, res, lres, C, xl, xh - xl, prm));
+    launch_pre<RHO>("m2l_sep_pre", M, wa, res, lres, C, xl, xh, prm, s);
     if ((err = cudaGetLastError()) != cudaSuccess) return err;
     if ((err = launch_pass<RHO, PASS_Z>(wa, wb, res, C, xl, xh, 0, res, prm, "m2l_sep_z", s)))
       return err;
