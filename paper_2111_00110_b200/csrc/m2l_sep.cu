@@ -1,5 +1,6 @@
-// Finest-level M2L (far + near) as three 1-D convolutions between two
-// per-axis triangular transforms.
+// M2L through the per-axis factors of the reference's tables: the finest
+// level (far + near) as three 1-D convolutions between two per-axis
+// triangular transforms, coarse levels' far tables as three such pieces.
 //
 // Reference: Engine.m2l (expansion.py:227-264) over the finest far table
 // (parity stencil, :246-249) plus the near table, with the tables of
@@ -33,6 +34,14 @@
 // lines of the entries one partition needs (lanes along the contiguous
 // axis); warp g computes one output group for all 8 positions of its lane's
 // line with the accumulators in registers (see "passes" below).
+//
+// Coarse levels (expansion.py:272-275) apply the parity stencil minus the
+// 3 x 3 x 3 hole.  Their tables factor the same way with the level's own
+// K(d), and box^3 - hole is the disjoint union of three products of per-axis
+// tap sets (A = the parity box, F = {|d| >= 2}, N = {|d| <= 1}):
+//   F x A x A  +  N x F x A  +  N x N x F              (x, y, z)
+// so a far table is the same passes with tap subsets (TAPS), the two-term
+// pieces as one pass over two staged windows (TAPS1): m2l_sep(far_only).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
